@@ -1,0 +1,46 @@
+# B200-native build (sm_100a). `make` builds the product library and the
+# test-only oracle; `make ref` additionally compiles the unmodified reference
+# into oracle/_ref (needs /root/reference, i.e. this container only).
+NVCC     ?= /usr/local/cuda/bin/nvcc
+PKG      := paper_2505_02977_b200
+LIBDIR   := $(PKG)/lib
+LIB      := $(LIBDIR)/libparac_gpu.so
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+# -ffp-contract=off on the host side: input generators of the form a + b*U
+# must not contract. Device factor code uses explicit
+# __dadd_rn/__dmul_rn/__ddiv_rn; never --use_fast_math.
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr \
+            -Xcompiler -fPIC,-ffp-contract=off,-O3 -Xptxas -warn-spills
+CU_SRCS  := $(wildcard $(PKG)/csrc/cuda/*.cu)
+CPP_SRCS := $(wildcard $(PKG)/csrc/host/*.cpp)
+HDRS     := $(wildcard $(PKG)/csrc/cuda/*.cuh) $(wildcard $(PKG)/csrc/host/*.hpp) include/parac_gpu.h
+OBJDIR   := $(PKG)/build
+CU_OBJS  := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
+CPP_OBJS := $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(CPP_SRCS))
+
+.PHONY: all lib oracle ref clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(PKG)/csrc/cuda/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJDIR)/host_%.o: $(PKG)/csrc/host/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(CU_OBJS) $(CPP_OBJS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf $(OBJDIR) $(LIBDIR)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,225 @@
+/*
+ * parac_gpu.h — C ABI of the B200-native (sm_100a) randomized approximate
+ * Cholesky (rchol / ParAC, arXiv 2505.02977) factorization of graph
+ * Laplacians and the PCG solve that consumes it.
+ *
+ * This is the drop-in boundary for the reference library `parac`
+ * (/root/reference/proj). Each entry point names the reference interface it
+ * replaces (file:line, paths relative to proj/). Conventions:
+ *   - plain pointers and sizes only, no C++ or torch types;
+ *   - every fallible call returns an int status: 0 = ok, otherwise the
+ *     reference's `parac::Errc` value (include/parac/error.hpp:9-27), so a C++
+ *     shim can rethrow `parac::Error(Errc(code), parac_gpu_last_error())`;
+ *   - inputs are never owned; outputs go to caller buffers (or are freed by
+ *     the matching *_free call);
+ *   - there is NO CPU fallback: without a CUDA device every device entry point
+ *     fails with PARAC_INTERNAL_ERROR and a message saying so.
+ * See INTEGRATION.md for the C++ shim (parac::factor_gpu / pcg_solve_gpu).
+ */
+#ifndef PARAC_GPU_H
+#define PARAC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: identical numbering to parac::Errc (error.hpp:9-27) ---- */
+enum {
+  PARAC_OK = 0,
+  PARAC_ASYMMETRIC_INPUT = 1,
+  PARAC_POSITIVE_OFF_DIAGONAL = 2,
+  PARAC_ROW_SUM_VIOLATION = 3,
+  PARAC_TOO_LARGE_FOR_DENSE = 4,
+  PARAC_PARSE_ERROR = 5,
+  PARAC_UNSUPPORTED_FIELD = 6,
+  PARAC_BUDGET_EXCEEDED = 7,
+  PARAC_NOT_A_PERMUTATION = 8,
+  PARAC_DENSE_BLOWUP = 9,
+  PARAC_ARENA_EXHAUSTED = 10,
+  PARAC_QUEUE_STALL = 11,
+  PARAC_WORKSPACE_FULL = 12,
+  PARAC_DIMENSION_MISMATCH = 13,
+  PARAC_NOT_CONNECTED = 14,
+  PARAC_TOO_MANY_NEIGHBORS = 15,
+  PARAC_IO_ERROR = 16,
+  PARAC_INTERNAL_ERROR = 17
+};
+
+/* errc_name (src/error.cpp:5-27): "ArenaExhausted", ... */
+const char* parac_errc_name(int code);
+/* Message of the last failing call on this host thread. */
+const char* parac_gpu_last_error(void);
+
+/* ---- graphs: LaplacianGraph (include/parac/graph.hpp:25-60) as CSR ---------
+ * Label space, neighbours ascending within a row, weights > 0, both halves
+ * stored (nnz = ptr[n] = 2E). wdeg (the derived diagonal) is optional on
+ * input; the library recomputes it in the reference's order when needed. */
+typedef struct {
+  int32_t n;
+  const int64_t* ptr; /* n+1 */
+  const int32_t* adj; /* ptr[n] */
+  const double* w;    /* ptr[n] */
+} parac_csr;
+
+/* Library-owned CSR produced by the host builders below. */
+typedef struct {
+  int32_t n;
+  int64_t nnz; /* = ptr[n] */
+  int64_t* ptr;
+  int32_t* adj;
+  double* w;
+  double* wdeg;
+} parac_graph;
+void parac_graph_free(parac_graph* g);
+
+/* LaplacianGraph::from_edges (graph.hpp:33, src/graph.cpp:21-83): unique
+ * undirected edges (a_i != b_i), w_i > 0; rejects self-loops, non-positive
+ * weights, out-of-range endpoints and duplicates with PARAC_INTERNAL_ERROR. */
+int parac_graph_from_edges(int32_t n, int64_t m, const int32_t* a, const int32_t* b,
+                           const double* w, parac_graph* out);
+
+/* gen_poisson3d (generators.hpp:26, src/generators.cpp:14-65).
+ * variant: 0 uniform, 1 anisotropic (z-edges epsilon), 2 contrast. */
+int parac_gen_poisson3d(int32_t n, int variant, double epsilon, double contrast_ratio,
+                        uint64_t seed, parac_graph* out);
+/* 2D 5-point n x n grid, unit weights, id = x + n*y (BASELINE config 1). */
+int parac_gen_poisson2d(int32_t n, parac_graph* out);
+/* 3D 27-point (Chebyshev distance 1) n^3 grid, w(a,b) = 0.5 + 1.5 *
+ * unit_uniform(derive_seed(seed, kSaltCells), a, b) for a < b (config 3). */
+int parac_gen_poisson27(int32_t n, uint64_t seed, parac_graph* out);
+/* R-MAT (Graph500 a,b,c = .57,.19,.19), 2^scale vertices, edge_factor *
+ * 2^scale samples, self-loops dropped, deduplicated, w in U[0.5,2) keyed by
+ * (u,v) (config 4). */
+int parac_gen_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, parac_graph* out);
+/* gen_random_connected / gen_random_components (src/generators.cpp:110-175),
+ * same SplitMix64 streams, so the graphs equal the reference's. */
+int parac_gen_random_connected(int32_t n, int64_t extra_edges, uint64_t seed,
+                               int unit_weights, parac_graph* out);
+int parac_gen_random_components(int32_t n, int32_t components, int64_t extra_edges,
+                                uint64_t seed, parac_graph* out);
+
+/* ---- orderings: Ordering::perm (include/parac/ordering.hpp:13-24) ---------
+ * perm[label] = elimination position. */
+/* ordering_random (ordering.hpp:28, src/ordering.cpp:38-47) */
+int parac_ordering_random(int32_t n, uint64_t seed, int32_t* perm);
+/* ordering_nnz_sort (ordering.hpp:32, src/ordering.cpp:49-70) */
+int parac_ordering_nnz_sort(const parac_csr* g, uint64_t seed, int32_t* perm);
+/* Ordering::from_positions validation (src/ordering.cpp:22-36):
+ * PARAC_NOT_A_PERMUTATION unless perm is a bijection on [0,n). */
+int parac_ordering_check(int32_t n, const int32_t* perm);
+
+/* ---- device context --------------------------------------------------------
+ * Owns the device buffers (reused across calls, grown on demand) and a CUDA
+ * stream. Re-entrant per context; use one context per concurrent problem
+ * (e.g. one per GPU / per stream for the batch configuration). */
+typedef struct parac_gpu_ctx parac_gpu_ctx;
+int parac_gpu_create(int32_t device, parac_gpu_ctx** out);
+void parac_gpu_destroy(parac_gpu_ctx* ctx);
+/* Number of visible CUDA devices (0 on a CPU-only host). */
+int parac_gpu_device_count(void);
+
+/* Mirrors ParOptions (include/parac/factor_par.hpp:31-45). */
+typedef struct {
+  int64_t fill_pool_entries;     /* overflow fill pool (16 B entries); <0: default */
+  int64_t column_arena_entries;  /* G column arena; <0: default */
+  int32_t first_chunk;           /* preallocated fill slots per vertex; <=0: default */
+  double watchdog_seconds;       /* <=0: 60 s (ParOptions::watchdog_seconds) */
+  int32_t record_stats;          /* keep merged_degree/samples/fills per position */
+  int32_t verify;                /* device-side TestHooks::verify analogue */
+  int32_t grid_ctas;             /* persistent-kernel CTAs; <=0: occupancy-sized */
+  int32_t delay_ns;              /* >0: random __nanosleep injection (TestHooks::delay) */
+} parac_gpu_options;
+void parac_gpu_default_options(parac_gpu_options* opt);
+
+/* FactorStats (include/parac/factor_seq.hpp:22-30) scalars + timings. */
+typedef struct {
+  int32_t n;
+  int64_t num_edges;        /* E = nnz_lower */
+  int64_t nnz_off_diagonal; /* Z; LdlFactor::nnz() = Z + n */
+  int64_t total_fills;      /* F */
+  int64_t fill_pool_used;   /* overflow pool entries used */
+  int64_t arena_used;       /* column arena entries used (= Z) */
+  int32_t max_raw;          /* largest gathered column (edges + fills) */
+  int32_t large_columns;    /* columns that took the large-column path */
+  double setup_ms;          /* device: forward-CSR build + dependency init */
+  double eliminate_ms;      /* device: persistent elimination kernel */
+  double assemble_ms;       /* device: CSC assembly */
+  double device_ms;         /* device total (events around all factor kernels) */
+  double upload_ms;         /* host->device copy (0 for resident inputs) */
+  double wall_ms;           /* host wall clock of the call */
+} parac_gpu_factor_info;
+
+/* Stage graph + ordering on the device of ctx (host->device copy). */
+int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm);
+
+/* Factor the staged input; the factor stays resident in ctx.
+ * Replaces factor_parallel_left/right (include/parac/factor_par.hpp:53-62)
+ * and factor_randomized (factor_seq.hpp:34-36): byte-identical LdlFactor
+ * (LdlFactor::same_values, src/factor.cpp:10-13) for the same graph,
+ * ordering and seed. Errors: PARAC_ARENA_EXHAUSTED (pool/arena budget),
+ * PARAC_QUEUE_STALL (device watchdog), PARAC_DIMENSION_MISMATCH. */
+int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt,
+                              parac_gpu_factor_info* info);
+
+/* One call: upload + factor (the drop-in for factor_parallel_left). */
+int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
+                     const parac_gpu_options* opt, parac_gpu_factor_info* info);
+
+/* Copy the resident factor to caller buffers (LdlFactor fields,
+ * include/parac/factor.hpp:18-25): col_ptr[n+1], rows[Z], values[Z],
+ * diag[n]; stats arrays [n] may be NULL (need record_stats). */
+int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, double* values,
+                       double* diag, int32_t* merged_degree, int32_t* samples_emitted,
+                       int32_t* fills_received);
+
+/* Stage an existing factor (e.g. one computed by the reference) on the
+ * device for the solve entry points. */
+int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_ptr,
+                            const int32_t* rows, const double* values, const double* diag,
+                            const int32_t* perm);
+
+/* schedule_levels (include/parac/factor_par.hpp:66, src/factor_par.cpp:659-684)
+ * of the resident factor; returns the depth in *depth. levels may be NULL. */
+int parac_gpu_schedule_levels(parac_gpu_ctx* ctx, int32_t* levels, int32_t* depth);
+
+/* ---- solve ------------------------------------------------------------------
+ * SolveConfig / SolveReport (include/parac/solver.hpp:13-25). */
+typedef struct {
+  int32_t iterations;
+  double relative_residual;   /* recomputed ||b - Lx|| / ||b|| */
+  double recurrence_residual;
+  int32_t converged;
+  double solve_ms;            /* device time of the solve */
+  double wall_ms;
+} parac_gpu_solve_report;
+
+/* pcg_solve (include/parac/solver.hpp:39-42, src/solver.cpp:95-175) on the
+ * resident graph + factor. b, x are host arrays of length n (label space).
+ * PARAC_NOT_CONNECTED for a disconnected graph, as the reference. */
+int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_iters, double* x,
+                  parac_gpu_solve_report* report);
+/* apply_preconditioner (solver.hpp:30, src/solver.cpp:32-74) */
+int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* z);
+/* laplacian_apply (solver.hpp:33, src/solver.cpp:76-93) */
+int parac_gpu_laplacian_apply(parac_gpu_ctx* ctx, const double* x, double* y);
+/* make_rhs (solver.hpp:47, src/solver.cpp:177-193); host computation (libm),
+ * mode 1 = random_projected, 2 = from_random_x. */
+int parac_make_rhs(const parac_csr* g, int mode, uint64_t seed, double* out);
+
+/* ---- misc ---------------------------------------------------------------- */
+/* LdlFactor::checksum (src/factor.cpp:17-36), host. */
+uint64_t parac_factor_checksum(int32_t n, const int64_t* col_ptr, const int32_t* rows,
+                               const double* values, const double* diag);
+/* Pinned host memory for fast H2D/D2H (cudaMallocHost). */
+void* parac_host_alloc(size_t bytes);
+void parac_host_free(void* p);
+/* Count of this library's kernel launches since process start. */
+int64_t parac_gpu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARAC_GPU_H */

@@ -1,0 +1,498 @@
+// C ABI of the device path (include/parac_gpu.h): context, buffers, factor
+// driver, downloads. Host orchestration only; all arithmetic is in the
+// kernels. There is no CPU fallback: every entry point fails loudly when no
+// CUDA device is usable.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../../include/parac_gpu.h"
+#include "../host/errors.hpp"
+#include "../host/host_rng.hpp"
+#include "factor_kernels.cuh"
+#include "solve_kernels.cuh"
+
+namespace parac_gpu {
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void note_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Failure{internal_error, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t cap = 0;
+  void ensure(std::size_t count) {
+    if (count <= cap && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const std::size_t c = std::max<std::size_t>(count, 1);
+    check(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
+    cap = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+}  // namespace
+}  // namespace parac_gpu
+
+using namespace parac_gpu;
+
+struct parac_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  // staged input (label space)
+  int n = -1;
+  long long nnz = 0;
+  DevBuf<long long> ptr;
+  DevBuf<int> adj;
+  DevBuf<double> w;
+  DevBuf<int> perm;
+  // factor working state
+  DevBuf<int> inv, fdeg, dp, queue, fill_cnt, samples, col_len, arena_rows;
+  DevBuf<long long> fwd_ptr, col_start, tiles;
+  DevBuf<int> fwd_to;
+  DevBuf<double> fwd_w, diag, arena_vals;
+  DevBuf<int4> pool0, ovf;
+  DevBuf<unsigned> dir;
+  DevBuf<char> large_pool;
+  DevBuf<Ctrl> ctrl;
+  // resident factor (CSC, position space)
+  DevBuf<long long> col_ptr;
+  DevBuf<int> rows;
+  DevBuf<double> vals;
+  int f_n = -1;
+  long long f_nnz = 0;
+  bool f_has_stats = false;
+  bool f_external = false;  // uploaded via parac_gpu_upload_factor
+  DevBuf<double> f_diag_ext;
+  DevBuf<int> f_perm_ext;
+  // solve state
+  SolveState solve;
+};
+
+namespace {
+
+void activate(parac_gpu_ctx* ctx) { check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
+
+void require_ctx(parac_gpu_ctx* ctx) {
+  if (!ctx) throw Failure{internal_error, "null context"};
+  activate(ctx);
+}
+
+struct Budgets {
+  long long ovf, arena, large;
+  int c0;
+};
+
+Budgets default_budgets(int n, long long E, const parac_gpu_options& o) {
+  Budgets b;
+  const long long base = E + n;
+  b.c0 = o.first_chunk > 0 ? o.first_chunk : 16;
+  b.ovf = o.fill_pool_entries >= 0 ? o.fill_pool_entries : 4 * base + 4096;
+  b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : 4 * base + 4096;
+  b.large = base + 65536;
+  return b;
+}
+
+// One attempt of the factorization with the given budgets. Returns status.
+int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& o,
+               const Budgets& b, parac_gpu_factor_info* info) {
+  const int n = ctx->n;
+  const long long E = ctx->nnz / 2;
+  cudaStream_t s = ctx->stream;
+  const std::size_t nn = static_cast<std::size_t>(std::max(n, 1));
+  ctx->inv.ensure(nn);
+  ctx->fdeg.ensure(nn);
+  ctx->dp.ensure(nn);
+  ctx->queue.ensure(nn);
+  ctx->fill_cnt.ensure(nn);
+  ctx->samples.ensure(nn);
+  ctx->col_len.ensure(nn);
+  ctx->col_start.ensure(nn);
+  ctx->diag.ensure(nn);
+  ctx->fwd_ptr.ensure(nn + 1);
+  ctx->fwd_to.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
+  ctx->fwd_w.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
+  ctx->pool0.ensure(nn * static_cast<std::size_t>(b.c0));
+  ctx->dir.ensure(nn * kDirChunks);
+  ctx->ovf.ensure(static_cast<std::size_t>(std::max<long long>(b.ovf, 1)));
+  ctx->arena_rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
+  ctx->arena_vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
+  ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * 48);
+  ctx->ctrl.ensure(1);
+  ctx->tiles.ensure(static_cast<std::size_t>(scan_tiles(n) + 1));
+  ctx->col_ptr.ensure(nn + 1);
+
+  FactorDev d{};
+  d.n = n;
+  d.ptr = ctx->ptr.p;
+  d.adj = ctx->adj.p;
+  d.w = ctx->w.p;
+  d.perm = ctx->perm.p;
+  d.inv = ctx->inv.p;
+  d.fwd_ptr = ctx->fwd_ptr.p;
+  d.fwd_to = ctx->fwd_to.p;
+  d.fwd_w = ctx->fwd_w.p;
+  d.fdeg = ctx->fdeg.p;
+  d.dp = ctx->dp.p;
+  d.queue = ctx->queue.p;
+  d.fill_cnt = ctx->fill_cnt.p;
+  d.pool0 = ctx->pool0.p;
+  d.dir = ctx->dir.p;
+  d.ovf = ctx->ovf.p;
+  d.ovf_cap = b.ovf;
+  d.c0 = b.c0;
+  d.col_start = ctx->col_start.p;
+  d.col_len = ctx->col_len.p;
+  d.diag = ctx->diag.p;
+  d.arena_rows = ctx->arena_rows.p;
+  d.arena_vals = ctx->arena_vals.p;
+  d.arena_cap = b.arena;
+  d.samples = ctx->samples.p;
+  d.large_pool = ctx->large_pool.p;
+  d.large_cap = b.large;
+  d.ctrl = ctx->ctrl.p;
+  d.sample_seed = derive_seed(seed, kSaltSampling);
+  const double wd = o.watchdog_seconds > 0 ? o.watchdog_seconds : 60.0;
+  d.watchdog_ns = static_cast<unsigned long long>(wd * 1e9);
+  d.verify = o.verify;
+  d.delay_ns = o.delay_ns;
+
+  check(cudaEventRecord(ctx->ev[0], s), "event");
+  check(cudaMemsetAsync(ctx->inv.p, 0xff, nn * sizeof(int), s), "memset");
+  check(cudaMemsetAsync(ctx->dir.p, 0, nn * kDirChunks * sizeof(unsigned), s), "memset");
+  check(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s), "memset");
+  check(launch_pos_graph(d, ctx->tiles.p, s), "pos_graph launch");
+  check(launch_initial_ready(d, s), "initial_ready launch");
+  check(cudaEventRecord(ctx->ev[1], s), "event");
+  int grid = 0;
+  check(launch_eliminate(d, o.grid_ctas, s, &grid), "eliminate launch");
+  check(cudaEventRecord(ctx->ev[2], s), "event");
+  Ctrl c{};
+  check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl copy");
+  check(cudaStreamSynchronize(s), "eliminate");
+  if (c.status != 0) {
+    ctx->f_n = -1;
+    std::string msg;
+    if (c.status == arena_exhausted)
+      msg = "pool budget exhausted at position " + std::to_string(c.err_info) +
+            " (overflow used " + std::to_string(c.ovf_bump) + "/" + std::to_string(b.ovf) +
+            ", arena " + std::to_string(c.arena_bump) + "/" + std::to_string(b.arena) +
+            ", large " + std::to_string(c.large_bump) + "/" + std::to_string(b.large) + ")";
+    else if (c.status == queue_stall)
+      msg = "no elimination for " + std::to_string(wd) + "s while waiting on queue slot " +
+            std::to_string(c.err_info) + " (" + std::to_string(c.q_tail) + "/" +
+            std::to_string(n) + " published)";
+    else if (c.status == not_a_permutation)
+      msg = "ordering is not a permutation (vertex " + std::to_string(c.err_info) + ")";
+    else
+      msg = "device verify failure at position " + std::to_string(c.err_info);
+    set_last_error(std::string(errc_name(c.status)) + ": " + msg);
+    return c.status;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int parac_gpu_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int64_t parac_gpu_launch_count(void) { return g_launches.load(); }
+
+void parac_gpu_default_options(parac_gpu_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->fill_pool_entries = -1;
+  o->column_arena_entries = -1;
+  o->first_chunk = 0;
+  o->watchdog_seconds = 60.0;
+  o->record_stats = 1;
+  o->verify = 0;
+  o->grid_ctas = 0;
+  o->delay_ns = 0;
+}
+
+int parac_gpu_create(int32_t device, parac_gpu_ctx** out) {
+  return guarded([&] {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      throw Failure{internal_error, std::string("no CUDA device available (") +
+                                        cudaGetErrorString(e) +
+                                        "); this library has no CPU fallback"};
+    if (device < 0 || device >= count) throw Failure{internal_error, "device ordinal out of range"};
+    auto* ctx = new parac_gpu_ctx;
+    ctx->device = device;
+    try {
+      activate(ctx);
+      check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+      for (auto& ev : ctx->ev) check(cudaEventCreate(&ev), "event");
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+void parac_gpu_destroy(parac_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
+  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->queue.release();
+  ctx->fill_cnt.release(); ctx->samples.release(); ctx->col_len.release();
+  ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
+  ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
+  ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
+  ctx->large_pool.release(); ctx->ctrl.release(); ctx->col_ptr.release(); ctx->rows.release();
+  ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
+  solve_release(ctx->solve);
+  for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!g || g->n < 0) throw Failure{dimension_mismatch, "bad graph"};
+    const int n = g->n;
+    const long long nnz = g->ptr[n];
+    ctx->ptr.ensure(static_cast<std::size_t>(n) + 1);
+    ctx->adj.ensure(static_cast<std::size_t>(std::max<long long>(nnz, 1)));
+    ctx->w.ensure(static_cast<std::size_t>(std::max<long long>(nnz, 1)));
+    ctx->perm.ensure(static_cast<std::size_t>(std::max(n, 1)));
+    cudaStream_t s = ctx->stream;
+    check(cudaMemcpyAsync(ctx->ptr.p, g->ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s), "h2d");
+    if (nnz > 0) {
+      check(cudaMemcpyAsync(ctx->adj.p, g->adj, sizeof(int) * nnz, cudaMemcpyHostToDevice, s), "h2d");
+      check(cudaMemcpyAsync(ctx->w.p, g->w, sizeof(double) * nnz, cudaMemcpyHostToDevice, s), "h2d");
+    }
+    if (n > 0)
+      check(cudaMemcpyAsync(ctx->perm.p, perm, sizeof(int) * n, cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaStreamSynchronize(s), "h2d sync");
+    ctx->n = n;
+    ctx->nnz = nnz;
+    ctx->f_n = -1;
+    solve_invalidate(ctx->solve);
+  });
+}
+
+int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt,
+                              parac_gpu_factor_info* info) {
+  Timer wall;
+  parac_gpu_options o;
+  if (opt) o = *opt; else parac_gpu_default_options(&o);
+  int rc = guarded([&] {
+    require_ctx(ctx);
+    if (ctx->n < 0) throw Failure{dimension_mismatch, "no graph staged (call parac_gpu_upload)"};
+  });
+  if (rc) return rc;
+  const int n = ctx->n;
+  const long long E = ctx->nnz / 2;
+  Budgets b = default_budgets(n, E, o);
+  for (int attempt = 0;; ++attempt) {
+    rc = 0;
+    int st = 0;
+    rc = guarded([&] { st = run_factor(ctx, seed, o, b, info); });
+    if (rc) return rc;
+    if (st == 0) break;
+    // Budget exhaustion with library-chosen budgets: grow and retry (the
+    // caller's explicit budgets fail cleanly, like ParOptions::arena_budget).
+    const bool defaults = o.fill_pool_entries < 0 && o.column_arena_entries < 0;
+    if (st == arena_exhausted && defaults && attempt < 4) {
+      b.ovf *= 2;
+      b.arena *= 2;
+      b.large *= 4;
+      continue;
+    }
+    return st;
+  }
+  rc = guarded([&] {
+    cudaStream_t s = ctx->stream;
+    Ctrl c{};
+    check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
+    check(cudaStreamSynchronize(s), "sync");
+    const long long Z = static_cast<long long>(c.arena_bump);
+    ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
+    ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
+    FactorDev d{};
+    d.n = n;
+    d.col_len = ctx->col_len.p;
+    d.col_start = ctx->col_start.p;
+    d.arena_rows = ctx->arena_rows.p;
+    d.arena_vals = ctx->arena_vals.p;
+    d.samples = ctx->samples.p;
+    d.ctrl = ctx->ctrl.p;
+    check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, s), "assemble");
+    check(cudaEventRecord(ctx->ev[3], s), "event");
+    check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
+    check(cudaStreamSynchronize(s), "assemble sync");
+    ctx->f_n = n;
+    ctx->f_nnz = Z;
+    ctx->f_has_stats = true;
+    ctx->f_external = false;
+    solve_invalidate_factor(ctx->solve);
+    if (info) {
+      std::memset(info, 0, sizeof(*info));
+      info->n = n;
+      info->num_edges = E;
+      info->nnz_off_diagonal = Z;
+      info->total_fills = c.total_fills;
+      info->fill_pool_used = static_cast<long long>(c.ovf_bump);
+      info->arena_used = Z;
+      info->max_raw = c.max_raw;
+      info->large_columns = c.large_cols;
+      float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
+      cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&t12, ctx->ev[1], ctx->ev[2]);
+      cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+      cudaEventElapsedTime(&t03, ctx->ev[0], ctx->ev[3]);
+      info->setup_ms = t01;
+      info->eliminate_ms = t12;
+      info->assemble_ms = t23;
+      info->device_ms = t03;
+      info->wall_ms = wall.ms();
+    }
+  });
+  return rc;
+}
+
+int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
+                     const parac_gpu_options* opt, parac_gpu_factor_info* info) {
+  Timer wall;
+  int rc = parac_gpu_upload(ctx, g, perm);
+  if (rc) return rc;
+  const double up = wall.ms();
+  rc = parac_gpu_factor_resident(ctx, seed, opt, info);
+  if (rc == 0 && info) {
+    info->upload_ms = up;
+    info->wall_ms = wall.ms();
+  }
+  return rc;
+}
+
+int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, double* values,
+                       double* diag, int32_t* merged_degree, int32_t* samples_emitted,
+                       int32_t* fills_received) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ctx->f_n < 0) throw Failure{dimension_mismatch, "no resident factor"};
+    const int n = ctx->f_n;
+    const long long Z = ctx->f_nnz;
+    cudaStream_t s = ctx->stream;
+    if (col_ptr)
+      check(cudaMemcpyAsync(col_ptr, ctx->col_ptr.p, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost, s), "d2h");
+    if (rows && Z)
+      check(cudaMemcpyAsync(rows, ctx->rows.p, sizeof(int) * Z, cudaMemcpyDeviceToHost, s), "d2h");
+    if (values && Z)
+      check(cudaMemcpyAsync(values, ctx->vals.p, sizeof(double) * Z, cudaMemcpyDeviceToHost, s), "d2h");
+    const double* dsrc = ctx->f_external ? ctx->f_diag_ext.p : ctx->diag.p;
+    if (diag && n)
+      check(cudaMemcpyAsync(diag, dsrc, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    if ((merged_degree || samples_emitted || fills_received) && !ctx->f_has_stats)
+      throw Failure{internal_error, "factor has no device stats (uploaded externally)"};
+    if (merged_degree && n)
+      check(cudaMemcpyAsync(merged_degree, ctx->col_len.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    if (samples_emitted && n)
+      check(cudaMemcpyAsync(samples_emitted, ctx->samples.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    if (fills_received && n)
+      check(cudaMemcpyAsync(fills_received, ctx->fill_cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    check(cudaStreamSynchronize(s), "d2h sync");
+  });
+}
+
+int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_ptr,
+                            const int32_t* rows, const double* values, const double* diag,
+                            const int32_t* perm) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const long long Z = col_ptr[n];
+    cudaStream_t s = ctx->stream;
+    ctx->col_ptr.ensure(static_cast<std::size_t>(n) + 1);
+    ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
+    ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
+    ctx->f_diag_ext.ensure(static_cast<std::size_t>(std::max(n, 1)));
+    ctx->f_perm_ext.ensure(static_cast<std::size_t>(std::max(n, 1)));
+    check(cudaMemcpyAsync(ctx->col_ptr.p, col_ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s), "h2d");
+    if (Z) {
+      check(cudaMemcpyAsync(ctx->rows.p, rows, sizeof(int) * Z, cudaMemcpyHostToDevice, s), "h2d");
+      check(cudaMemcpyAsync(ctx->vals.p, values, sizeof(double) * Z, cudaMemcpyHostToDevice, s), "h2d");
+    }
+    if (n) {
+      check(cudaMemcpyAsync(ctx->f_diag_ext.p, diag, sizeof(double) * n, cudaMemcpyHostToDevice, s), "h2d");
+      check(cudaMemcpyAsync(ctx->f_perm_ext.p, perm, sizeof(int) * n, cudaMemcpyHostToDevice, s), "h2d");
+    }
+    check(cudaStreamSynchronize(s), "h2d sync");
+    ctx->f_n = n;
+    ctx->f_nnz = Z;
+    ctx->f_has_stats = false;
+    ctx->f_external = true;
+    solve_invalidate_factor(ctx->solve);
+  });
+}
+
+void* parac_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, std::max<size_t>(bytes, 1)) != cudaSuccess) return nullptr;
+  return p;
+}
+void parac_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"
+
+// Accessors used by the solve translation unit.
+namespace parac_gpu {
+SolveInputs solve_inputs(parac_gpu_ctx* ctx) {
+  SolveInputs in{};
+  in.n = ctx->n;
+  in.ptr = ctx->ptr.p;
+  in.adj = ctx->adj.p;
+  in.w = ctx->w.p;
+  in.f_n = ctx->f_n;
+  in.f_nnz = ctx->f_nnz;
+  in.col_ptr = ctx->col_ptr.p;
+  in.rows = ctx->rows.p;
+  in.vals = ctx->vals.p;
+  in.diag = ctx->f_external ? ctx->f_diag_ext.p : ctx->diag.p;
+  in.perm = ctx->f_external ? ctx->f_perm_ext.p : ctx->perm.p;
+  in.stream = ctx->stream;
+  in.device = ctx->device;
+  in.state = &ctx->solve;
+  return in;
+}
+void ctx_activate(parac_gpu_ctx* ctx) { require_ctx(ctx); }
+}  // namespace parac_gpu

@@ -1,0 +1,83 @@
+// Device state and launch interface of the factorization path.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace parac_gpu {
+
+// Fill entries are 16 B {row, source, weight}: one v4 store / load.
+// Fill storage per vertex (position) lo:
+//   slots [0, C0)                     -> pool0[lo*C0 + s]      (preallocated)
+//   chunk c>=1: slots [C0(2^c-1), C0(2^(c+1)-1)) -> ovf[dir[lo][c-1]-1 ...]
+//   chunks are bump-allocated on first touch by the writer of their first slot.
+constexpr int kDirChunks = 16;
+
+struct Ctrl {
+  int status;            // 0 or Errc
+  int q_head;            // next queue slot to claim
+  int q_tail;            // next queue slot to publish
+  int eliminated;        // progress counter (watchdog)
+  int max_raw;           // largest gathered column
+  int large_cols;        // columns that used the global-scratch path
+  int pad0, pad1;
+  unsigned long long ovf_bump;    // fill overflow pool (entries)
+  unsigned long long arena_bump;  // G column arena (entries)
+  unsigned long long large_bump;  // large-column scratch pool (entries)
+  long long total_fills;
+  long long err_info;
+};
+
+struct FactorDev {
+  int n;
+  // label-space input (LaplacianGraph CSR) + ordering
+  const long long* ptr;
+  const int* adj;
+  const double* w;
+  const int* perm;
+  // position-space forward graph (PosGraph, factor_common.hpp:23-29)
+  int* inv;
+  long long* fwd_ptr;
+  int* fwd_to;
+  double* fwd_w;
+  int* fdeg;
+  // dependency counters + ready queue
+  int* dp;
+  int* queue;
+  // fills
+  int* fill_cnt;
+  int4* pool0;
+  unsigned* dir;
+  int4* ovf;
+  long long ovf_cap;
+  int c0;
+  // G columns (arena, then assembled into CSC)
+  long long* col_start;
+  int* col_len;
+  double* diag;
+  int* arena_rows;
+  double* arena_vals;
+  long long arena_cap;
+  int* samples;
+  // large-column scratch pool: 48 B per entry
+  char* large_pool;
+  long long large_cap;
+  // control
+  Ctrl* ctrl;
+  unsigned long long sample_seed;
+  unsigned long long watchdog_ns;
+  int verify;
+  int delay_ns;
+};
+
+// Launchers (stream-ordered). All return cudaError_t of the launch.
+cudaError_t launch_pos_graph(const FactorDev& d, long long* tile_scratch, cudaStream_t s);
+cudaError_t launch_initial_ready(const FactorDev& d, cudaStream_t s);
+cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used);
+cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, double* vals,
+                            long long* tile_scratch, cudaStream_t s);
+cudaError_t launch_scan(const int* in, long long n, long long* out, long long* tile_scratch,
+                        cudaStream_t s);
+long long scan_tiles(long long n);
+int eliminate_occupancy_grid(int device);
+
+}  // namespace parac_gpu

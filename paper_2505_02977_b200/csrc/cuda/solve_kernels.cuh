@@ -1,0 +1,62 @@
+// Device PCG state (solve path): SpMV, level-ordered sync-free triangular
+// sweeps, fused vector ops. See solve_kernels.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+struct parac_gpu_ctx;
+
+namespace parac_gpu {
+
+struct SolveState {
+  bool graph_ready = false;   // wdeg computed for the staged graph
+  bool factor_ready = false;  // G^T (CSR), inverse perm, level order built
+  int n = 0;
+  double* wdeg = nullptr;
+  int* inv = nullptr;
+  // G in row form (CSR over positions): entries (k, G(r,k)), k ascending
+  long long* gt_ptr = nullptr;
+  int* gt_col = nullptr;
+  double* gt_val = nullptr;
+  int* level = nullptr;       // forward ASAP level per position
+  int* order = nullptr;       // positions sorted by level
+  long long* lvl_off = nullptr;  // level offsets into order
+  int* flags = nullptr;       // sweep completion stamps per position
+  int depth = 0;
+  int epoch = 0;
+  // vectors
+  double *x = nullptr, *r = nullptr, *p = nullptr, *lp = nullptr, *z = nullptr, *best = nullptr;
+  double *yf = nullptr, *yd = nullptr, *zb = nullptr, *rhs = nullptr;
+  double* partials = nullptr;  // per-block partial sums
+  double* scalars = nullptr;   // device scalars
+  int* counters = nullptr;     // claim counters
+  long long* tiles = nullptr;
+  int* tmp_int = nullptr;
+  std::size_t cap_n = 0, cap_z = 0;
+  int blocks = 0;
+};
+
+struct SolveInputs {
+  int n;
+  const long long* ptr;
+  const int* adj;
+  const double* w;
+  int f_n;
+  long long f_nnz;
+  const long long* col_ptr;
+  const int* rows;
+  const double* vals;
+  const double* diag;
+  const int* perm;
+  cudaStream_t stream;
+  int device;
+  SolveState* state;
+};
+
+void solve_release(SolveState& s);
+void solve_invalidate(SolveState& s);
+void solve_invalidate_factor(SolveState& s);
+SolveInputs solve_inputs(parac_gpu_ctx* ctx);
+void ctx_activate(parac_gpu_ctx* ctx);
+
+}  // namespace parac_gpu

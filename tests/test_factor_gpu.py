@@ -1,0 +1,115 @@
+"""GPU: the sm_100a factorization is byte-identical (LdlFactor::same_values,
+proj/src/factor.cpp:10-13) to the oracle on the reference's test corpus, and
+its FactorStats agree (proj/tests/test_factor_par.cpp:172-190)."""
+import numpy as np
+import pytest
+
+import paper_2505_02977_b200 as P
+from corpus import case, digest, factor_from_port
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_factor(ctx, g, perm, seed, **opts):
+    stats = P.FactorStats()
+    f = P.factor_gpu(g, P.Ordering(perm), seed, P.GpuOptions(**opts), stats, ctx=ctx)
+    return f, stats
+
+
+def assert_same(f, ref_f, name=""):
+    assert f.same_values(ref_f), name
+
+
+def test_golden_corpus_byte_identical(gpu_ctx, port, gold):
+    for e in gold["factors"]:
+        g, perm, seed = case(e["name"])
+        f, st = gpu_factor(gpu_ctx, g, perm, seed, verify=True)
+        assert f"{f.checksum():016x}" == e["checksum"], e["name"]
+        want = port.factor(g, perm, seed)
+        assert_same(f, factor_from_port(want), e["name"])
+        assert np.array_equal(st.merged_degree, want["merged_degree"]), e["name"]
+        assert np.array_equal(st.samples_emitted, want["samples_emitted"]), e["name"]
+        assert np.array_equal(st.fills_received, want["fills_received"]), e["name"]
+        assert st.total_fills == e["total_fills"]
+
+
+@pytest.mark.parametrize("opts", [dict(grid_ctas=1), dict(first_chunk=1), dict(first_chunk=2, grid_ctas=3),
+                                  dict(delay_ns=2000, verify=True)])
+def test_schedule_and_pool_shape_do_not_change_bits(gpu_ctx, port, opts):
+    # the claim order, CTA count and fill-chunk layout must never move a bit
+    for name in ("poisson16_random0", "rc200_s1_nnz", "components3000_s0"):
+        g, perm, seed = case(name)
+        f, _ = gpu_factor(gpu_ctx, g, perm, seed, **opts)
+        assert_same(f, factor_from_port(port.factor(g, perm, seed)), name)
+
+
+def test_repeat_stress(gpu_ctx, port):
+    # proj/tests/test_factor_par.cpp:146-170 (delay injection, 25 runs)
+    g = P.gen_random_connected(200, 360, 17)
+    perm = P.ordering_random(200, 3).perm
+    want = factor_from_port(port.factor(g, perm, 5))
+    for run in range(25):
+        f, _ = gpu_factor(gpu_ctx, g, perm, 5, verify=True, delay_ns=500 * (run % 5))
+        assert_same(f, want)
+
+
+@pytest.mark.parametrize("builder,seed", [
+    (lambda: P.gen_poisson2d(64), 0),
+    (lambda: P.gen_poisson27(12, 1), 0),
+    (lambda: P.gen_poisson3d(24, "contrast", contrast_ratio=1e6, seed=1), 3),
+    (lambda: P.gen_rmat(12, 16, 0), 0),
+    (lambda: P.gen_random_components(5000, 7, 20000, 2), 4),
+])
+def test_paper_shapes_byte_identical(gpu_ctx, port, builder, seed):
+    g = builder()
+    for perm in (P.ordering_random(g.n, seed).perm, P.ordering_nnz_sort(g, seed).perm):
+        f, st = gpu_factor(gpu_ctx, g, perm, seed)
+        want = port.factor(g, perm, seed)
+        assert_same(f, factor_from_port(want))
+        assert np.array_equal(st.fills_received, want["fills_received"])
+
+
+def test_poisson64_matches_reference_checksum(gpu_ctx, gold):
+    e = next(x for x in gold["factors"] if x["name"] == "poisson64_random0")
+    g, perm, seed = case(e["name"])
+    f, _ = gpu_factor(gpu_ctx, g, perm, seed)
+    assert f"{f.checksum():016x}" == e["checksum"] == "3bbec4ec5f0cad7b"
+
+
+def test_edge_cases(gpu_ctx, port):
+    # empty graph, isolated vertices, single vertex, two vertices
+    for n, edges in ((1, []), (6, []), (2, [(0, 1, 2.5)]), (5, [(1, 3, 1.0)])):
+        g = P.LaplacianGraph.from_edges(n, edges)
+        for s in range(3):
+            perm = P.ordering_random(n, s).perm
+            f, _ = gpu_factor(gpu_ctx, g, perm, s)
+            assert_same(f, factor_from_port(port.factor(g, perm, s)))
+
+
+def test_arena_exhaustion_is_clean(gpu_ctx):
+    # proj/tests/test_factor_par.cpp:105-118: explicit tiny budgets fail cleanly
+    g = P.gen_random_connected(100, 300, 3)
+    perm = P.ordering_random(100, 1).perm
+    with pytest.raises(P.Error) as ei:
+        gpu_factor(gpu_ctx, g, perm, 0, column_arena_entries=64)
+    assert ei.value.code == P.Errc.arena_exhausted
+    with pytest.raises(P.Error) as ei:
+        gpu_factor(gpu_ctx, g, perm, 0, fill_pool_entries=4, first_chunk=1)
+    assert ei.value.code == P.Errc.arena_exhausted
+    # the context stays usable afterwards
+    f, _ = gpu_factor(gpu_ctx, g, perm, 0)
+    assert f.nnz_off_diagonal() > 0
+
+
+def test_dimension_mismatch(gpu_ctx):
+    g = P.gen_poisson3d(4)
+    with pytest.raises(P.Error) as ei:
+        P.factor_gpu(g, P.Ordering.identity(10), 0, ctx=gpu_ctx)
+    assert ei.value.code == P.Errc.dimension_mismatch
+
+
+def test_native_library_is_what_ran(gpu_ctx):
+    before = P.rchol.lib.parac_gpu_launch_count()
+    g, perm, seed = case("poisson16_random0")
+    gpu_factor(gpu_ctx, g, perm, seed)
+    assert P.rchol.lib.parac_gpu_launch_count() > before

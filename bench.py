@@ -1,0 +1,447 @@
+#!/usr/bin/env python3
+"""Benchmark of the rchol hot path (BASELINE.json metric): randomized approximate
+Cholesky factorization of the 3D 7-point Poisson Laplacian 128^3 (config[1]) on
+B200, reported as factor nnz/s (LdlFactor::nnz() / factor seconds), with the PCG
+solve to 1e-8 that consumes the factor measured in the same run.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload poisson3d_128|poisson2d_256|poisson27_96|rmat_22|batch_64x64]
+
+One process per GPU (torchrun for N>1). A single factorization does not shard
+(SURVEY §8(e)): every rank factors its own independent Laplacian (seed = rank),
+so per-GPU work is fixed and scaling is "weak"; there is no data-path collective.
+
+Step = one factorization of the workload with its inputs resident in HBM
+(`value`, device time from CUDA events on the library's stream, L2 flushed
+between steps). `e2e` = the same factorization through the C ABI
+(parac_gpu_factor + parac_gpu_download) from pinned host buffers, host<->device
+copies inside the timed region. `--impl reference` times the reference's own
+multithreaded CPU path (oracle/_ref: factor_parallel_left/right, unmodified
+sources) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factorization time & factor nnz/s; PCG iters+solve time, 3D Poisson 128³"
+FALLBACK_HBM = 6650.0
+
+WORKLOADS = {
+    # name: (builder, description)
+    "poisson3d_128": ("gen_poisson3d", 128, "3D 7-point Poisson 128^3 (config[1])"),
+    "poisson2d_256": ("gen_poisson2d", 256, "2D 5-point Poisson 256^2 (config[0])"),
+    "poisson27_96": ("gen_poisson27", 96, "3D 27-point 96^3, w=0.5+1.5U (config[2])"),
+    "rmat_22": ("gen_rmat", 22, "R-MAT scale 22, ef 16 (config[3])"),
+    "batch_64x64": ("gen_poisson3d", 64, "batch of 64 x 3D Poisson 64^3 (config[4])"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def build_graph(P, workload: str, seed: int):
+    kind, size, _ = WORKLOADS[workload]
+    if kind == "gen_poisson3d":
+        return P.gen_poisson3d(size)
+    if kind == "gen_poisson2d":
+        return P.gen_poisson2d(size)
+    if kind == "gen_poisson27":
+        return P.gen_poisson27(size, 1)
+    if kind == "gen_rmat":
+        return P.gen_rmat(size, 16, seed)
+    raise KeyError(workload)
+
+
+def algorithmic_bytes(n: int, E: int, Z: int, F: int) -> dict:
+    """B_fact = 16(n+1) + 8n + 12E + 40F + 20Z. The dominant kernel
+    (K3, eliminate) accounts for all of it except the 8(n+1) col_ptr written by K4."""
+    b_fact = 16 * (n + 1) + 8 * n + 12 * E + 40 * F + 20 * Z
+    return {"fact": b_fact, "k3": b_fact - 8 * (n + 1)}
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return rank, world, local, pg
+
+
+def barrier(pg, device):
+    import torch
+    torch.cuda.synchronize(device)
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize(device)
+
+
+def allreduce(pg, device, value: float, op: str) -> float:
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=getattr(pg.ReduceOp, op))
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- reference CPU
+def cpu_reference_factor(graph, perm, seed, workers_list, repeats=1):
+    """Wall clock around the reference API call (host graph in, LdlFactor out),
+    BASELINE.md §2: min over {par-left, par-right} x workers."""
+    import oracle
+    R = oracle.Reference()
+    h = R.graph_from_csr(graph)
+    best = None
+    rows = []
+    for backend, bname in ((R.LEFT, "par-left"), (R.RIGHT, "par-right")):
+        for w in workers_list:
+            for _ in range(repeats):
+                f, wall = R.factor(h, perm, seed, backend=backend, workers=w)
+                nnz = R.L.pref_factor_nnz_off(f) + graph.n
+                R.free_factor(f)
+                rows.append((wall, bname, w))
+                if best is None or wall < best[0]:
+                    best = (wall, bname, w, nnz)
+    R.free_graph(h)
+    return best, rows
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # other ranks exit without work (the CPU path does not shard)
+    import oracle
+    import paper_2505_02977_b200 as P
+    workload = args.workload
+    cores = os.cpu_count() or 1
+    if not oracle.Reference.available():
+        kind = "port"
+    else:
+        kind = "reference"
+    g = build_graph(P, workload, 0)
+    perm = P.ordering_random(g.n, 0).perm
+    cands = sorted({w for w in (cores, max(1, cores // 2), min(cores, 32), min(cores, 16), 8) if w <= cores})
+    if kind == "port":
+        port = oracle.Port()
+        run_one = lambda: port.factor(g, perm, 0)  # noqa: E731
+        t = time.perf_counter(); f = run_one(); wall = time.perf_counter() - t
+        nnz = len(f["rows"]) + g.n
+        best_cfg = ("oracle port (factor_randomized restatement)", 1)
+        cores_used = 1
+        times = []
+        for _ in range(args.steps):
+            t = time.perf_counter(); run_one(); times.append(time.perf_counter() - t)
+    else:
+        # warm-up: pick the best backend x workers (BASELINE.md §2 T_cpu rule)
+        (w0, bname, wk, nnz), rows = cpu_reference_factor(g, perm, 0, cands)
+        log("reference sweep:", [(round(a, 3), b, c) for a, b, c in rows])
+        best_cfg = (bname, wk)
+        cores_used = wk
+        import oracle as O
+        R = O.Reference()
+        h = R.graph_from_csr(g)
+        backend = R.LEFT if bname == "par-left" else R.RIGHT
+        for _ in range(max(0, args.warmup - 1)):
+            f, _ = R.factor(h, perm, 0, backend=backend, workers=wk)
+            R.free_factor(f)
+        times = []
+        for _ in range(args.steps):
+            f, wall = R.factor(h, perm, 0, backend=backend, workers=wk)
+            R.free_factor(f)
+            times.append(wall)
+        R.free_graph(h)
+    sec = sum(times) / len(times)
+    value = nnz / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "desc": WORKLOADS[workload][2], "n": g.n,
+                   "edges": g.num_edges(), "ordering": "ordering_random(n, 0)", "seed": 0,
+                   "backend": best_cfg[0], "workers": best_cfg[1]},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": cores_used, "kind": kind,
+                         "sample": f"{args.steps} full factorizations of {workload}, wall clock "
+                                   f"around the API call (host graph in, LdlFactor out)"},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours (GPU)
+def pinned_copy(P, arr: np.ndarray):
+    nbytes = arr.nbytes
+    ptr = P.rchol.lib.parac_host_alloc(max(nbytes, 1))
+    if not ptr:
+        raise MemoryError("parac_host_alloc failed")
+    buf = (C.c_char * max(nbytes, 1)).from_address(ptr)
+    out = np.frombuffer(buf, dtype=arr.dtype, count=arr.size)
+    out[:] = arr
+    return ptr, out
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2505_02977_b200 as P
+    from paper_2505_02977_b200 import _lib as L
+
+    rank, world, local, pg = dist_setup(args.gpus)
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    seed = rank
+    workload = args.workload
+    lib = P.rchol.lib
+
+    g = build_graph(P, workload, seed)
+    order = P.ordering_random(g.n, seed)
+    n, E = g.n, g.num_edges()
+    ctx = P.GpuContext(local)
+    opts = P.GpuOptions().native()
+    info = L.parac_gpu_factor_info()
+
+    # pinned host inputs/outputs for the end-to-end leg
+    hp = [pinned_copy(P, a) for a in (g.ptr, g.adj, g.w, order.perm)]
+    csr = L.parac_csr(n, hp[0][0], hp[1][0], hp[2][0])
+    perm_ptr = hp[3][0]
+
+    def check(rc):
+        if rc != 0:
+            raise P.Error(rc, lib.parac_gpu_last_error().decode())
+
+    # resident input for the device-time leg
+    check(lib.parac_gpu_upload(ctx.handle, C.byref(csr), perm_ptr))
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    def device_step():
+        check(lib.parac_gpu_factor_resident(ctx.handle, seed, C.byref(opts), C.byref(info)))
+        return info.device_ms, info.eliminate_ms
+
+    for _ in range(args.warmup):
+        device_step()
+    Z = info.nnz_off_diagonal
+    F = info.total_fills
+    nnz = Z + n
+    out_bufs = [pinned_copy(P, np.zeros(k, dt)) for k, dt in
+                ((n + 1, np.int64), (max(Z, 1), np.int32), (max(Z, 1), np.float64), (max(n, 1), np.float64))]
+
+    # ---- timed: resident inputs, device time (CUDA events on the library stream)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    l0 = lib.parac_gpu_launch_count()
+    barrier(pg, device)
+    dev_ms, k3_ms = [], []
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (256 MiB > 126 MB L2) between steps, outside the events
+        torch.cuda.synchronize(device)
+        a, b = device_step()
+        dev_ms.append(a)
+        k3_ms.append(b)
+    barrier(pg, device)
+    wall_resident = time.perf_counter() - t_wall
+    launches = lib.parac_gpu_launch_count() - l0
+    clk = clocks.stop() if clocks else None
+    total_dev_s = sum(dev_ms) / 1e3
+    max_dev_s = allreduce(pg, device, total_dev_s, "MAX")
+    total_nnz = allreduce(pg, device, float(nnz * args.steps), "SUM")
+    value = total_nnz / max_dev_s
+
+    # ---- timed: end to end through the C ABI from pinned host memory
+    barrier(pg, device)
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        check(lib.parac_gpu_factor(ctx.handle, C.byref(csr), perm_ptr, seed, C.byref(opts), C.byref(info)))
+        check(lib.parac_gpu_download(ctx.handle, out_bufs[0][0], out_bufs[1][0], out_bufs[2][0],
+                                     out_bufs[3][0], None, None, None))
+        e2e_s.append(time.perf_counter() - t0)
+    barrier(pg, device)
+    e2e_total = allreduce(pg, device, sum(e2e_s), "MAX")
+    e2e_value = total_nnz / e2e_total
+    h2d = 8 * (n + 1) + 12 * 2 * E + 4 * n
+    d2h = 8 * (n + 1) + 12 * Z + 8 * n
+    # parity of the e2e output against the resident run (same bits every call)
+    f_e2e = P.LdlFactor(n, out_bufs[0][1], out_bufs[1][1][:Z], out_bufs[2][1][:Z], out_bufs[3][1][:n], order.perm)
+    checksum = f_e2e.checksum()
+
+    # ---- PCG to 1e-8 on the resident factor (BASELINE metric, second half)
+    pcg = None
+    if not args.no_pcg and workload != "rmat_22":
+        check(lib.parac_gpu_factor_resident(ctx.handle, seed, C.byref(opts), C.byref(info)))
+        b = P.make_rhs(g, "random_projected", 0)
+        P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))  # warm (builds G rows + levels)
+        x, rep = P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))
+        pcg = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
+               "converged": rep.converged, "solve_ms": rep.device_ms, "wall_ms": rep.solve_seconds * 1e3,
+               "tol": 1e-8}
+
+    peak, peak_src = read_peaks()
+    by = algorithmic_bytes(n, E, Z, F)
+    k3_avg_s = sum(k3_ms) / len(k3_ms) / 1e3
+    achieved = by["k3"] / k3_avg_s / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                traffic = json.load(fh).get(workload, {}).get("eliminate_kernel_dram_bytes")
+        except Exception:
+            traffic = None
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = os.cpu_count() or 1
+            (wall, bname, wk, cnnz), _ = cpu_reference_factor(g, order.perm, seed, [cores])
+            cpu_base = {"value": cnnz / wall, "unit": "nnz/s", "cores": wk, "kind": "reference",
+                        "sample": f"1 full {workload} factorization, {bname} x {wk} threads "
+                                  f"(best of par-left/par-right), wall clock around the API call",
+                        "seconds": wall}
+        except Exception as exc:  # oracle/_ref missing -> port timing would be 1-core
+            cpu_base = {"value": None, "unit": "nnz/s", "cores": 0, "kind": "reference",
+                        "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": max_dev_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (host generators = reference gen_poisson3d etc.; ordering_random(n, rank), seed = rank)",
+            "config": {"workload": workload, "desc": WORKLOADS[workload][2], "n": n, "edges": E,
+                       "nnz_G": nnz, "fills": F, "factor_checksum": f"{checksum:016x}",
+                       "per_gpu": "one independent factorization per rank",
+                       "l2": "flushed between steps (256 MiB memset); working set > L2 anyway",
+                       "parallelism": f"replicas x{world}"},
+            "factor_ms": {"device": max_dev_s / args.steps * 1e3,
+                          "eliminate_k3": sum(k3_ms) / len(k3_ms), "wall_resident_loop_s": wall_resident},
+            "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},
+            "pcg": pcg,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "eliminate_kernel (K3)", "algorithmic_bytes": by["k3"],
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu_base,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="poisson3d_128")
+    ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

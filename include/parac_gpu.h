@@ -131,6 +131,7 @@ typedef struct {
   int32_t verify;                /* device-side TestHooks::verify analogue */
   int32_t grid_ctas;             /* persistent-kernel CTAs; <=0: occupancy-sized */
   int32_t delay_ns;              /* >0: random __nanosleep injection (TestHooks::delay) */
+  int32_t record_times;          /* ParOptions::record_vertex_times: start/end per position */
 } parac_gpu_options;
 void parac_gpu_default_options(parac_gpu_options* opt);
 
@@ -174,6 +175,12 @@ int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
 int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, double* values,
                        double* diag, int32_t* merged_degree, int32_t* samples_emitted,
                        int32_t* fills_received);
+
+/* Per-position elimination phase timestamps (%globaltimer ns) of the last
+ * factor run with record_times set: start_end[8*k + i], i = 0 start, 1 gathered
+ * and sorted, 2 merged, 3 column written, 4 weight-sorted + suffix, 5 fills
+ * emitted, 6 decremented, 7 end (after publishing). Zero = phase skipped. */
+int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end);
 
 /* Stage an existing factor (e.g. one computed by the reference) on the
  * device for the solve entry points. */

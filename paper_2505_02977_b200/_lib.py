@@ -37,7 +37,8 @@ class parac_graph(C.Structure):
 class parac_gpu_options(C.Structure):
     _fields_ = [("fill_pool_entries", i64), ("column_arena_entries", i64),
                 ("first_chunk", i32), ("watchdog_seconds", f64), ("record_stats", i32),
-                ("verify", i32), ("grid_ctas", i32), ("delay_ns", i32)]
+                ("verify", i32), ("grid_ctas", i32), ("delay_ns", i32),
+                ("record_times", i32)]
 
 
 class parac_gpu_factor_info(C.Structure):
@@ -76,6 +77,7 @@ SIGNATURES = {
     "parac_gpu_factor": (C.c_int, [vp, P(parac_csr), vp, u64, P(parac_gpu_options),
                                    P(parac_gpu_factor_info)]),
     "parac_gpu_download": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "parac_gpu_download_times": (C.c_int, [vp, vp]),
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "parac_gpu_schedule_levels": (C.c_int, [vp, vp, P(i32)]),
     "parac_gpu_pcg": (C.c_int, [vp, vp, f64, i32, vp, P(parac_gpu_solve_report)]),

@@ -73,7 +73,7 @@ struct parac_gpu_ctx {
   DevBuf<double> w;
   DevBuf<int> perm;
   // factor working state
-  DevBuf<int> inv, fdeg, dp, queue, fill_cnt, samples, col_len, arena_rows;
+  DevBuf<int> inv, fdeg, dp, queue, bqueue, fill_cnt, samples, col_len, arena_rows;
   DevBuf<long long> fwd_ptr, col_start, tiles;
   DevBuf<int> fwd_to;
   DevBuf<double> fwd_w, diag, arena_vals;
@@ -81,6 +81,10 @@ struct parac_gpu_ctx {
   DevBuf<unsigned> dir;
   DevBuf<char> large_pool;
   DevBuf<Ctrl> ctrl;
+  DevBuf<unsigned long long> vtimes;
+  bool has_times = false;
+  Ctrl last_ctrl{};
+  long long last_z = 0;
   // resident factor (CSC, position space)
   DevBuf<long long> col_ptr;
   DevBuf<int> rows;
@@ -112,9 +116,11 @@ struct Budgets {
 Budgets default_budgets(int n, long long E, const parac_gpu_options& o) {
   Budgets b;
   const long long base = E + n;
-  b.c0 = o.first_chunk > 0 ? o.first_chunk : 16;
+  // 64 preallocated slots per position cover the fill count of ~99.5% of
+  // 128^3 positions (p99 66), so the directory lookup is rare.
+  b.c0 = o.first_chunk > 0 ? o.first_chunk : 64;
   b.ovf = o.fill_pool_entries >= 0 ? o.fill_pool_entries : 4 * base + 4096;
-  b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : 4 * base + 4096;
+  b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : 6 * base + 4096;
   b.large = base + 65536;
   return b;
 }
@@ -130,6 +136,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->fdeg.ensure(nn);
   ctx->dp.ensure(nn);
   ctx->queue.ensure(nn);
+  ctx->bqueue.ensure(nn);
   ctx->fill_cnt.ensure(nn);
   ctx->samples.ensure(nn);
   ctx->col_len.ensure(nn);
@@ -143,7 +150,9 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->ovf.ensure(static_cast<std::size_t>(std::max<long long>(b.ovf, 1)));
   ctx->arena_rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->arena_vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
-  ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * 48);
+  ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * 24);
+  ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
+  ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->ctrl.ensure(1);
   ctx->tiles.ensure(static_cast<std::size_t>(scan_tiles(n) + 1));
   ctx->col_ptr.ensure(nn + 1);
@@ -161,6 +170,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.fdeg = ctx->fdeg.p;
   d.dp = ctx->dp.p;
   d.queue = ctx->queue.p;
+  d.bqueue = ctx->bqueue.p;
   d.fill_cnt = ctx->fill_cnt.p;
   d.pool0 = ctx->pool0.p;
   d.dir = ctx->dir.p;
@@ -182,6 +192,13 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.watchdog_ns = static_cast<unsigned long long>(wd * 1e9);
   d.verify = o.verify;
   d.delay_ns = o.delay_ns;
+  d.vtimes = nullptr;
+  ctx->has_times = o.record_times != 0;
+  if (o.record_times) {
+    ctx->vtimes.ensure(8 * nn);
+    check(cudaMemsetAsync(ctx->vtimes.p, 0, 8 * nn * sizeof(unsigned long long), s), "memset");
+    d.vtimes = ctx->vtimes.p;
+  }
 
   check(cudaEventRecord(ctx->ev[0], s), "event");
   check(cudaMemsetAsync(ctx->inv.p, 0xff, nn * sizeof(int), s), "memset");
@@ -193,9 +210,15 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   int grid = 0;
   check(launch_eliminate(d, o.grid_ctas, s, &grid), "eliminate launch");
   check(cudaEventRecord(ctx->ev[2], s), "event");
+  check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, s), "assemble");
+  check(cudaEventRecord(ctx->ev[3], s), "event");
   Ctrl c{};
+  long long z = 0;
   check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl copy");
-  check(cudaStreamSynchronize(s), "eliminate");
+  check(cudaMemcpyAsync(&z, ctx->col_ptr.p + n, sizeof(long long), cudaMemcpyDeviceToHost, s), "z copy");
+  check(cudaStreamSynchronize(s), "factor sync");
+  ctx->last_ctrl = c;
+  ctx->last_z = z;
   if (c.status != 0) {
     ctx->f_n = -1;
     std::string msg;
@@ -270,12 +293,12 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
-  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->queue.release();
+  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->queue.release(); ctx->bqueue.release();
   ctx->fill_cnt.release(); ctx->samples.release(); ctx->col_len.release();
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
   ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
-  ctx->large_pool.release(); ctx->ctrl.release(); ctx->col_ptr.release(); ctx->rows.release();
+  ctx->large_pool.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->col_ptr.release(); ctx->rows.release();
   ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
   solve_release(ctx->solve);
   for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -340,25 +363,8 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
     return st;
   }
   rc = guarded([&] {
-    cudaStream_t s = ctx->stream;
-    Ctrl c{};
-    check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
-    check(cudaStreamSynchronize(s), "sync");
-    const long long Z = static_cast<long long>(c.arena_bump);
-    ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
-    ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));
-    FactorDev d{};
-    d.n = n;
-    d.col_len = ctx->col_len.p;
-    d.col_start = ctx->col_start.p;
-    d.arena_rows = ctx->arena_rows.p;
-    d.arena_vals = ctx->arena_vals.p;
-    d.samples = ctx->samples.p;
-    d.ctrl = ctx->ctrl.p;
-    check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, s), "assemble");
-    check(cudaEventRecord(ctx->ev[3], s), "event");
-    check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
-    check(cudaStreamSynchronize(s), "assemble sync");
+    const Ctrl c = ctx->last_ctrl;
+    const long long Z = ctx->last_z;
     ctx->f_n = n;
     ctx->f_nnz = Z;
     ctx->f_has_stats = true;
@@ -460,6 +466,15 @@ int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_pt
     ctx->f_has_stats = false;
     ctx->f_external = true;
     solve_invalidate_factor(ctx->solve);
+  });
+}
+
+int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
+    check(cudaMemcpy(start_end, ctx->vtimes.p, sizeof(unsigned long long) * 8 * ctx->f_n,
+                     cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

@@ -42,6 +42,13 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Acquire fence: orders this thread's earlier relaxed reads (the observed
+// flag / queue slot) before its later loads ("ld.relaxed; fence.acquire"
+// acquire pattern). Used once per hand-off instead of polling with ld.acquire,
+// which would invalidate the SM's L1 (CCTL.IVALL) on every poll.
+__device__ __forceinline__ void fence_acq_rel() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

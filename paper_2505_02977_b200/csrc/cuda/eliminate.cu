@@ -1,0 +1,980 @@
+// K3: the persistent elimination kernel (sm_100a).
+//
+// One elimination = factor_sequential's loop body (proj/src/factor_seq.cpp:70-138)
+// with the par-backends' dependency hand-off (proj/src/factor_par.cpp:282-293,
+// 424-477); SURVEY Appendix A steps 1-9:
+//   gather (forward edges ++ fills) -> sort by (row, source) -> merge runs
+//   (serial sums) -> lkk (serial) -> column -> sort by (weight, row) -> suffix
+//   (serial, right to left) -> sample + emit fills (dp[hi]++) -> fence ->
+//   decrement dp[row] by multiplicity -> rows reaching zero are ready.
+//
+// Work split. Persistent CTAs of 8 warps, two roles:
+//   * small CTAs: every warp eliminates its own vertex, raw size R <= kSmallCap,
+//     sorted entirely in registers (bitonic network over 32*ITEMS elements);
+//   * big CTAs (every 4th): the whole CTA eliminates one vertex with
+//     R <= kBigCap in shared memory (256-thread bitonic networks); wider
+//     columns use a global slab.
+// A vertex that becomes ready is routed by its final R to the main or the big
+// ready queue. The warp/CTA that makes vertices ready keeps the widest one it
+// can hold and eliminates it next without a queue round trip (keep-one): the
+// critical path runs through exactly these hand-offs.
+//
+// Bit-exactness: the serial sums use __dadd_rn in the reference's order, the
+// products/divisions __dmul_rn/__ddiv_rn; sort keys are unique, so any sorting
+// network reproduces the reference's order.
+#include "factor_device.cuh"
+#include "factor_kernels.cuh"
+
+namespace parac_gpu {
+
+void note_launches(long long k);
+
+using namespace dev;
+using namespace fdev;
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kEntryBytes = 24;  // A (u64), B (f64), C (f64) per column entry
+constexpr int kSmallBytes = kSmallCap * kEntryBytes;
+// big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
+constexpr int kBigBytes = kBigCap * 8 * 5;
+constexpr int kCtaSmem = kWarps * kSmallBytes > kBigBytes ? kWarps * kSmallBytes : kBigBytes;
+constexpr int kBatch = 4;  // samples / decrements per lane in flight (small path)
+
+// Role of this CTA. On a full grid the role follows the SM (every 4th SM runs
+// only big CTAs) so each SM executes a single code path and its instruction
+// cache holds one path's working set; tiny grids (tests) fall back to CTA ids.
+__device__ __forceinline__ bool is_big_cta() {
+  if (gridDim.x < 148) return (blockIdx.x & 3) == 3 || blockIdx.x == gridDim.x - 1;
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  return (smid & 3) == 3;
+}
+
+#define PHASE(i) \
+  do { if (d.vtimes && lead) d.vtimes[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
+
+// Column scratch views. A: raw key (row << 32 | source+1), then merged
+// (row << 32 | multiplicity); B: weights; C: suffix sums, then the ready list.
+struct Scratch {
+  unsigned long long* A;
+  double* B;
+  double* C;
+};
+__device__ __forceinline__ Scratch carve(char* base, int cap) {
+  return {reinterpret_cast<unsigned long long*>(base),
+          reinterpret_cast<double*>(base + 8 * static_cast<long long>(cap)),
+          reinterpret_cast<double*>(base + 16 * static_cast<long long>(cap))};
+}
+
+// What the keeper already knows about the vertex it keeps.
+struct Next {
+  int k;        // vertex, -1 none
+  int fdeg;     // forward degree (-1: unknown)
+  int fc;       // fills received
+  long long fb; // forward-CSR offset
+};
+
+// ------------------------------------------------------------ claiming
+// Claim the next slot of a ready queue and spin on it (relaxed polls, backoff
+// by distance to the tail). Returns the vertex, -1 when every vertex is
+// eliminated, -2 on abort. The caller issues the acquire fence.
+__device__ int claim(const FactorDev& d, bool big) {
+  int* queue = big ? d.bqueue : d.queue;
+  int* head = big ? &d.ctrl->b_head : &d.ctrl->q_head;
+  int* tail_p = big ? &d.ctrl->b_tail : &d.ctrl->q_tail;
+  const int idx = atomicAdd(head, 1);
+  if (idx >= d.n) return -1;
+  int v = ld_relaxed(&queue[idx]);
+  if (v >= 0) return v;
+  unsigned long long t0 = globaltimer_ns();
+  int last = ld_relaxed(&d.ctrl->eliminated);
+  int iter = 0;
+  while (true) {
+    const int dist = idx - ld_relaxed(tail_p);
+    const unsigned ns = dist <= 0 ? 32u : (dist < 16 ? 128u * dist : 2048u);
+    __nanosleep(ns);
+    v = ld_relaxed(&queue[idx]);
+    if (v >= 0) return v;
+    if (ld_relaxed(&d.ctrl->status) != 0) return -2;
+    if ((++iter & 7) == 0) {
+      const int done = ld_relaxed(&d.ctrl->eliminated);
+      if (done >= d.n) return -1;
+      const unsigned long long now = globaltimer_ns();
+      if (done != last) {
+        last = done;
+        t0 = now;
+      } else if (now - t0 > d.watchdog_ns) {
+        fail(d, kErrStall, idx);
+        return -2;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ sorting
+// (weight bits, A) strictly-less: fill_sorted_view order (factor_common.hpp:140-144);
+// A = row << 32 | mult and rows are unique, so the multiplicity never decides.
+__device__ __forceinline__ bool wless(unsigned long long wa, unsigned long long aa,
+                                      unsigned long long wb, unsigned long long ab) {
+  return wa < wb || (wa == wb && aa < ab);
+}
+
+// ------------------------------------------------------------ sorting networks
+// All networks sort (key, val) u64 pairs ascending under Less (keys are unique
+// under Less). Stage loops are runtime loops on purpose: fully unrolled
+// networks made K3 ~0.5 MB of SASS and the critical path instruction-fetch
+// bound (measured).
+
+struct RawLess {  // unique raw keys; the payload (weight bits) never decides
+  __device__ __forceinline__ bool operator()(unsigned long long a, unsigned long long,
+                                             unsigned long long b, unsigned long long) const {
+    return a < b;
+  }
+};
+struct WeightLess {  // key = weight bits, val = row << 32 | mult
+  __device__ __forceinline__ bool operator()(unsigned long long wa, unsigned long long aa,
+                                             unsigned long long wb, unsigned long long ab) const {
+    return wless(wa, aa, wb, ab);
+  }
+};
+
+// Compare-exchange of items i < p held by one thread (ascending if up).
+template <typename Less>
+__device__ __forceinline__ void cx(unsigned long long& ki, unsigned long long& vi,
+                                   unsigned long long& kp, unsigned long long& vp, bool up, Less less) {
+  const bool sw = less(kp, vp, ki, vi) == up;
+  const unsigned long long k0 = sw ? kp : ki, k1 = sw ? ki : kp;
+  const unsigned long long v0 = sw ? vp : vi, v1 = sw ? vi : vp;
+  ki = k0;
+  kp = k1;
+  vi = v0;
+  vp = v1;
+}
+
+// Intra-thread stage (distance j < ITEMS <= 4), element g = base + i.
+template <int ITEMS, typename Less>
+__device__ __forceinline__ void intra_stage(unsigned long long (&key)[ITEMS],
+                                            unsigned long long (&val)[ITEMS], int base, int k, int j,
+                                            Less less) {
+  if constexpr (ITEMS >= 2) {
+    if (j == 1) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; i += 2) cx(key[i], val[i], key[i + 1], val[i + 1], ((base + i) & k) == 0, less);
+    }
+  }
+  if constexpr (ITEMS >= 4) {
+    if (j == 2) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if ((i & 2) == 0) cx(key[i], val[i], key[i + 2], val[i + 2], ((base + i) & k) == 0, less);
+    }
+  }
+}
+
+// Cross-lane stage through shuffles: partner lane = lane ^ lm.
+template <int ITEMS, typename Less>
+__device__ __forceinline__ void shfl_stage(unsigned long long (&key)[ITEMS],
+                                           unsigned long long (&val)[ITEMS], int base, int k, int lm,
+                                           bool lower, Less less) {
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const unsigned long long pk = __shfl_xor_sync(kFull, key[i], lm);
+    const unsigned long long pv = __shfl_xor_sync(kFull, val[i], lm);
+    const bool up = ((base + i) & k) == 0;
+    const bool take = (lower == up) ? less(pk, pv, key[i], val[i]) : less(key[i], val[i], pk, pv);
+    key[i] = take ? pk : key[i];
+    val[i] = take ? pv : val[i];
+  }
+}
+
+// Warp register bitonic sort of 32*ITEMS elements, blocked layout
+// (element g = lane*ITEMS + i).
+template <int ITEMS, typename Less>
+__device__ __forceinline__ void warp_reg_sort(unsigned long long (&key)[ITEMS],
+                                           unsigned long long (&val)[ITEMS], int lane, Less less) {
+  constexpr int P = 32 * ITEMS;
+  const int base = lane * ITEMS;
+#pragma unroll 1
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < ITEMS) intra_stage<ITEMS>(key, val, base, k, j, less);
+      else shfl_stage<ITEMS>(key, val, base, k, j / ITEMS, (lane & (j / ITEMS)) == 0, less);
+    }
+  }
+}
+
+// Hybrid CTA bitonic network over P = 256*ITEMS elements in registers
+// (element g = tid*ITEMS + i): intra-thread, then shuffles, and stages wider
+// than a warp exchange through shared memory, double-buffered (striped layout
+// i*256 + tid, conflict-free), one barrier per such stage.
+struct XBuf {
+  unsigned long long* k0;
+  unsigned long long* v0;
+  unsigned long long* k1;
+  unsigned long long* v1;
+};
+
+template <int ITEMS, typename Less>
+__device__ __forceinline__ void cta_reg_sort(unsigned long long (&key)[ITEMS],
+                                          unsigned long long (&val)[ITEMS], XBuf xb, Less less) {
+  constexpr int P = kThreads * ITEMS;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int base = tid * ITEMS;
+  int buf = 0;
+#pragma unroll 1
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < ITEMS) {
+        intra_stage<ITEMS>(key, val, base, k, j, less);
+      } else if (j < 32 * ITEMS) {
+        shfl_stage<ITEMS>(key, val, base, k, j / ITEMS, (lane & (j / ITEMS)) == 0, less);
+      } else {
+        const int tm = j / ITEMS;
+        unsigned long long* KB = buf ? xb.k1 : xb.k0;
+        unsigned long long* VB = buf ? xb.v1 : xb.v0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          KB[i * kThreads + tid] = key[i];
+          VB[i * kThreads + tid] = val[i];
+        }
+        __syncthreads();
+        const int pt = tid ^ tm;
+        const bool lower = (tid & tm) == 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const unsigned long long pk = KB[i * kThreads + pt];
+          const unsigned long long pv = VB[i * kThreads + pt];
+          const bool up = ((base + i) & k) == 0;
+          const bool take = (lower == up) ? less(pk, pv, key[i], val[i]) : less(key[i], val[i], pk, pv);
+          key[i] = take ? pk : key[i];
+          val[i] = take ? pv : val[i];
+        }
+        buf ^= 1;
+      }
+    }
+  }
+}
+
+// Shared/global-memory bitonic networks for the whole CTA (slab path, P > kBigCap).
+__device__ __noinline__ void cta_sort_key(unsigned long long* A, double* B, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += kThreads) {
+        const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int b = a + j;
+        const unsigned long long ka = A[a], kb = A[b];
+        if ((ka > kb) == ((a & k) == 0)) {
+          A[a] = kb;
+          A[b] = ka;
+          const double t = B[a];
+          B[a] = B[b];
+          B[b] = t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __noinline__ void cta_sort_weight(unsigned long long* A, double* B, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += kThreads) {
+        const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int b = a + j;
+        const unsigned long long aa = A[a], ab = A[b];
+        const unsigned long long wa = dbits(B[a]), wb = dbits(B[b]);
+        if (wless(wb, ab, wa, aa) == ((a & k) == 0)) {
+          A[a] = ab;
+          A[b] = aa;
+          B[a] = bitsd(wb);
+          B[b] = bitsd(wa);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- warp path: gather + raw sort, weight sort (results in A/B, natural order)
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_raw(const FactorDev& d, int k, long long fb, int fdeg,
+                                              int R, Scratch S, int lane) {
+  unsigned long long key[ITEMS], val[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = lane * ITEMS + i;
+    key[i] = ~0ull;
+    val[i] = 0;
+    if (g < R) {
+      double w;
+      load_raw(d, k, fb, fdeg, g, key[i], w);
+      val[i] = dbits(w);
+    }
+  }
+  warp_reg_sort<ITEMS>(key, val, lane, RawLess{});
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    S.A[lane * ITEMS + i] = key[i];
+    S.B[lane * ITEMS + i] = bitsd(val[i]);
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_weight(int m, Scratch S, int lane) {
+  unsigned long long wk[ITEMS], ak[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = lane * ITEMS + i;
+    wk[i] = g < m ? dbits(S.B[g]) : kInfBits;
+    ak[i] = g < m ? S.A[g] : ~0ull;
+  }
+  __syncwarp();
+  warp_reg_sort<ITEMS>(wk, ak, lane, WeightLess{});
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    S.A[lane * ITEMS + i] = ak[i];
+    S.B[lane * ITEMS + i] = bitsd(wk[i]);
+  }
+}
+
+// ---- CTA path
+template <int ITEMS>
+__device__ __forceinline__ void cta_gather_sort_raw(const FactorDev& d, int k, long long fb, int fdeg,
+                                                    int R, const unsigned* dirrow,
+                                                    unsigned long long* A, double* B, XBuf xb) {
+  unsigned long long key[ITEMS], val[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = threadIdx.x * ITEMS + i;
+    key[i] = ~0ull;
+    val[i] = 0;
+    if (g < R) {
+      double w;
+      load_raw_dir(d, k, fb, fdeg, g, dirrow, key[i], w);
+      val[i] = dbits(w);
+    }
+  }
+  cta_reg_sort<ITEMS>(key, val, xb, RawLess{});
+  __syncthreads();  // exchange buffers alias A/B
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    A[threadIdx.x * ITEMS + i] = key[i];
+    B[threadIdx.x * ITEMS + i] = bitsd(val[i]);
+  }
+  __syncthreads();
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void cta_sort_weight_reg(int m, unsigned long long* A, double* B, XBuf xb) {
+  unsigned long long wk[ITEMS], ak[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = threadIdx.x * ITEMS + i;
+    wk[i] = g < m ? dbits(B[g]) : kInfBits;
+    ak[i] = g < m ? A[g] : ~0ull;
+  }
+  __syncthreads();  // exchange buffers alias A/B
+  cta_reg_sort<ITEMS>(wk, ak, xb, WeightLess{});
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    A[threadIdx.x * ITEMS + i] = ak[i];
+    B[threadIdx.x * ITEMS + i] = bitsd(wk[i]);
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ serial chains
+// lkk = ((0 + w0) + w1) + ... in row order (factor_common.hpp:117-121)
+__device__ __forceinline__ double serial_total(const double* B, int m) {
+  double s = 0.0;
+  int i = 0;
+  for (; i + 4 <= m; i += 4) {
+    const double x0 = B[i], x1 = B[i + 1], x2 = B[i + 2], x3 = B[i + 3];
+    s = __dadd_rn(s, x0);
+    s = __dadd_rn(s, x1);
+    s = __dadd_rn(s, x2);
+    s = __dadd_rn(s, x3);
+  }
+  for (; i < m; ++i) s = __dadd_rn(s, B[i]);
+  return s;
+}
+
+// suffix[g] = w[g] + suffix[g+1], strictly right to left (sampling.hpp:72-76)
+__device__ __forceinline__ void serial_suffix(const double* B, double* C, int m) {
+  double s = B[m - 1];
+  C[m - 1] = s;
+  int g = m - 2;
+  for (; g >= 3; g -= 4) {
+    const double x0 = B[g], x1 = B[g - 1], x2 = B[g - 2], x3 = B[g - 3];
+    s = __dadd_rn(x0, s);
+    C[g] = s;
+    s = __dadd_rn(x1, s);
+    C[g - 1] = s;
+    s = __dadd_rn(x2, s);
+    C[g - 2] = s;
+    s = __dadd_rn(x3, s);
+    C[g - 3] = s;
+  }
+  for (; g >= 0; --g) {
+    s = __dadd_rn(B[g], s);
+    C[g] = s;
+  }
+}
+
+// Final raw size of a vertex that just became ready (all its fills landed):
+// (R << 32 | row). The forward offset/degree and fill count are also what a
+// keeper needs to skip its first gather round trip.
+__device__ __forceinline__ unsigned long long ready_info(const FactorDev& d, int r) {
+  const long long rdeg = d.fwd_ptr[r + 1] - d.fwd_ptr[r];
+  return (static_cast<unsigned long long>(rdeg + ld_relaxed(&d.fill_cnt[r])) << 32) |
+         static_cast<unsigned>(r);
+}
+
+// ============================================================ small path
+// One warp eliminates k (R <= kSmallCap). Returns the kept vertex, -1, or -2.
+__device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane) {
+  const int k = nx.k;
+  const bool lead = lane == 0;
+  Ctrl* ctrl = d.ctrl;
+  if (d.verify && lead && ld_relaxed(&d.dp[k]) != 0) fail(d, kErrInternal, k);
+  maybe_delay(d, k, 0);
+
+  // ---- 1. gather
+  long long fb = nx.fb;
+  int fdeg = nx.fdeg, fc = nx.fc;
+  if (fdeg < 0) {
+    fb = d.fwd_ptr[k];
+    fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
+    fc = ld_relaxed(&d.fill_cnt[k]);
+  }
+  const int R = fdeg + fc;
+  if (R > kSmallCap) {  // mis-routed (cannot happen with exact routing): hand to a big CTA
+    publish(d, lead, true, k, lane);
+    return {-3, -1, 0, 0};
+  }
+  long long start = 0;
+  if (lead && R > 0)
+    start = static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R)));
+
+  // ---- 2. sort raw by (row, source)  (factor_common.hpp:100-104), in registers
+  if (R <= 32) warp_sort_raw<1>(d, k, fb, fdeg, R, S, lane);
+  else if (R <= 64) warp_sort_raw<2>(d, k, fb, fdeg, R, S, lane);
+  else warp_sort_raw<4>(d, k, fb, fdeg, R, S, lane);
+  __syncwarp();
+  PHASE(1);
+
+  // ---- 3. merge runs in place: left-to-right sums, multiplicity = run length
+  //      (factor_common.hpp:105-113). Chunk c writes only below 32(c+1).
+  int m = 0;
+  int carry_row = -1;
+  for (int base = 0; base < R; base += 32) {
+    const int t = base + lane;
+    const int row = t < R ? static_cast<int>(S.A[t] >> 32) : -2;
+    int prev = __shfl_up_sync(kFull, row, 1);
+    if (lane == 0) prev = carry_row;
+    const bool head = t < R && row != prev;
+    double acc = 0.0;
+    int c = 0;
+    if (head) {
+      acc = S.B[t];
+      c = 1;
+      while (t + c < R && static_cast<int>(S.A[t + c] >> 32) == row) {
+        acc = __dadd_rn(acc, S.B[t + c]);
+        ++c;
+      }
+    }
+    carry_row = __shfl_sync(kFull, row, 31);
+    const unsigned b = __ballot_sync(kFull, head);
+    __syncwarp();
+    if (head) {
+      const int idx = m + __popc(b & lanemask_lt());
+      S.A[idx] = (static_cast<unsigned long long>(static_cast<unsigned>(row)) << 32) |
+                 static_cast<unsigned>(c);
+      S.B[idx] = acc;
+    }
+    m += __popc(b);
+    __syncwarp();
+  }
+  PHASE(2);
+  if (m == 0) {  // factor_seq.cpp:92-95 (col_len/col_start already 0 from K1)
+    if (lead) d.diag[k] = 0.0;
+    return {-1, -1, 0, 0};
+  }
+
+  // ---- 5. lkk + column k: rows ascending, values (-w)/lkk (factor_seq.cpp:97-102)
+  double lkk = lead ? serial_total(S.B, m) : 0.0;
+  lkk = __shfl_sync(kFull, lkk, 0);
+  start = __shfl_sync(kFull, start, 0);
+  if (start + m > d.arena_cap) {
+    if (lead) fail(d, kErrArena, k);
+    return {-2, -1, 0, 0};
+  }
+  for (int t = lane; t < m; t += 32) {
+    d.arena_rows[start + t] = static_cast<int>(S.A[t] >> 32);
+    d.arena_vals[start + t] = __ddiv_rn(-S.B[t], lkk);
+  }
+  if (lead) {
+    d.diag[k] = lkk;
+    d.col_start[k] = start;
+    d.col_len[k] = m;
+  }
+  PHASE(3);
+
+  // ---- 6-7. weight sort (registers) + suffix
+  if (m >= 2) {
+    if (m <= 32) warp_sort_weight<1>(m, S, lane);
+    else if (m <= 64) warp_sort_weight<2>(m, S, lane);
+    else warp_sort_weight<4>(m, S, lane);
+    __syncwarp();
+    if (lead) serial_suffix(S.B, S.C, m);
+    __syncwarp();
+  }
+  PHASE(4);
+
+  // ---- 8. sampling + fill emission (m - 1 <= 127 samples: one batch)
+  int emitted = 0;
+  bool bad = false;
+  {
+    bool em[kBatch];
+    int lo[kBatch], hi[kBatch], slot[kBatch];
+    double wv[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int i = b * 32 + lane;
+      em[b] = i < m - 1 && draw_sample(d, k, i, m, S.A, S.B, S.C, lkk, lo[b], hi[b], wv[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      if (em[b]) {
+        slot[b] = reserve_fill_slot(d, lo[b]);
+        red_add_relaxed(&d.dp[hi[b]], 1);
+        bad = bad || slot[b] < 0;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      if (em[b] && !bad) bad = !write_fill(d, lo[b], slot[b], hi[b], k, wv[b]);
+      emitted += __popc(__ballot_sync(kFull, em[b]));
+    }
+  }
+  if (__any_sync(kFull, bad)) return {-2, -1, 0, 0};
+  if (lead) d.samples[k] = emitted;
+  PHASE(5);
+  maybe_delay(d, k, 1);
+
+  // ---- 9. release every emission, then decrement (factor_par.cpp:282-293)
+  fence_acq_rel();
+  __syncwarp();
+  unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
+  int nready = 0;
+  {
+    int row[kBatch], old[kBatch], mult[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int t = b * 32 + lane;
+      row[b] = -1;
+      old[b] = mult[b] = 0;
+      if (t < m) {
+        const unsigned long long a = S.A[t];
+        row[b] = static_cast<int>(a >> 32);
+        mult[b] = static_cast<int>(a & 0xffffffffu);
+        old[b] = atom_add_relaxed(&d.dp[row[b]], -mult[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      if (d.verify && row[b] >= 0 && old[b] < mult[b]) fail(d, kErrInternal, row[b]);
+      const bool now_ready = row[b] >= 0 && old[b] == mult[b];
+      const unsigned bm = __ballot_sync(kFull, now_ready);
+      if (bm) {
+        fence_acq_rel();  // acquire: the other decrementers' emissions are visible
+        if (now_ready) ready[nready + __popc(bm & lanemask_lt())] = ready_info(d, row[b]);
+      }
+      nready += __popc(bm);
+    }
+  }
+  __syncwarp();
+  PHASE(6);
+  maybe_delay(d, k, 2);
+  if (nready == 0) return {-1, -1, 0, 0};
+
+  // keep-one: the widest ready column this warp can hold; publish the rest
+  unsigned long long best = 0;
+  for (int t = lane; t < nready; t += 32) {
+    const unsigned long long rr = ready[t];
+    if (static_cast<int>(rr >> 32) <= kSmallCap && (rr | (1ull << 63)) > best) best = rr | (1ull << 63);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(kFull, best, o);
+    best = other > best ? other : best;
+  }
+  const int keep = best ? static_cast<int>(best & 0xffffffffu) : -1;
+  for (int base = 0; base < nready; base += 32) {
+    const int t = base + lane;
+    bool pub = false, big = false;
+    int r = 0;
+    if (t < nready) {
+      const unsigned long long rr = ready[t];
+      r = static_cast<int>(rr & 0xffffffffu);
+      big = static_cast<int>(rr >> 32) > kSmallCap;
+      pub = r != keep;
+    }
+    publish(d, pub, big, r, lane);
+  }
+  if (keep < 0) return {-1, -1, 0, 0};
+  return {keep, -1, 0, 0};
+}
+
+// ============================================================ big path
+struct CtaShared {
+  int k;
+  int m;
+  int nready;
+  int emitted;
+  int carry_row;
+  int bad;
+  double lkk;
+  long long start;
+  long long slab;
+  unsigned dirrow[kDirChunks];
+  int wcount[kWarps];
+  unsigned long long best[kWarps];
+};
+
+// The whole CTA eliminates k. Returns the kept vertex (any width), -1, or -2.
+__device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool lead = tid == 0;
+  Ctrl* ctrl = d.ctrl;
+  if (d.verify && lead && ld_relaxed(&d.dp[k]) != 0) fail(d, kErrInternal, k);
+  maybe_delay(d, k, 0);
+
+  // ---- 1. gather (the directory row is fetched in the same round trip)
+  if (tid < kDirChunks)
+    sh.dirrow[tid] = static_cast<unsigned>(
+        ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
+  const long long fb = d.fwd_ptr[k];
+  const int fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
+  const int fc = ld_relaxed(&d.fill_cnt[k]);
+  const int R = fdeg + fc;
+  const int P = next_pow2(R);
+  if (lead) {
+    sh.start = R > 0 ? static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R))) : 0;
+    sh.bad = 0;
+    if (P > kBigCap) {
+      const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(P)));
+      if (base + P > d.large_cap) {
+        fail(d, kErrArena, k);
+        sh.bad = 1;
+      }
+      atomicAdd(&ctrl->large_cols, 1);
+      sh.slab = base;
+    }
+    if (R > 64) atomicMax(&ctrl->max_raw, R);
+  }
+  __syncthreads();
+  if (sh.bad) return -2;
+  const bool wide = P > kBigCap;
+  Scratch S = wide ? carve(d.large_pool + sh.slab * kEntryBytes, P) : carve(smem, kBigCap);
+  const XBuf xb{S.A, reinterpret_cast<unsigned long long*>(S.B),
+                reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
+                reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
+  if (wide) {  // global slab, shared-memory-free network
+    for (int t = tid; t < P; t += kThreads) {
+      unsigned long long key = ~0ull;
+      double w = 0.0;
+      if (t < R) load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key, w);
+      S.A[t] = key;
+      S.B[t] = w;
+    }
+    __syncthreads();
+    cta_sort_key(S.A, S.B, P);
+  } else if (P <= kThreads) {
+    cta_gather_sort_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+  } else if (P <= 2 * kThreads) {
+    cta_gather_sort_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+  } else {
+    cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+  }
+  PHASE(1);
+
+  // ---- 3. merge runs in place, chunks of 256 (writes stay below the chunk end)
+  int m = 0;
+  if (lead) sh.carry_row = -1;
+  __syncthreads();
+  for (int base = 0; base < R; base += kThreads) {
+    const int t = base + tid;
+    const int row = t < R ? static_cast<int>(S.A[t] >> 32) : -2;
+    const int prev = tid == 0 ? sh.carry_row : (t - 1 < R ? static_cast<int>(S.A[t - 1] >> 32) : -2);
+    const bool head = t < R && row != prev;
+    double acc = 0.0;
+    int c = 0;
+    if (head) {
+      acc = S.B[t];
+      c = 1;
+      while (t + c < R && static_cast<int>(S.A[t + c] >> 32) == row) {
+        acc = __dadd_rn(acc, S.B[t + c]);
+        ++c;
+      }
+    }
+    const unsigned b = __ballot_sync(kFull, head);
+    if (lane == 0) sh.wcount[warp] = __popc(b);
+    __syncthreads();  // all reads of this chunk done; counts visible
+    int before = m;
+    int total = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      before += w2 < warp ? sh.wcount[w2] : 0;
+      total += sh.wcount[w2];
+    }
+    if (tid == kThreads - 1) sh.carry_row = row;
+    if (head) {
+      const int idx = before + __popc(b & lanemask_lt());
+      S.A[idx] = (static_cast<unsigned long long>(static_cast<unsigned>(row)) << 32) |
+                 static_cast<unsigned>(c);
+      S.B[idx] = acc;
+    }
+    m += total;
+    __syncthreads();
+  }
+  PHASE(2);
+  if (m == 0) {
+    if (lead) d.diag[k] = 0.0;
+    return -1;
+  }
+
+  // ---- 5. lkk + column
+  if (lead) sh.lkk = serial_total(S.B, m);
+  __syncthreads();
+  const double lkk = sh.lkk;
+  const long long start = sh.start;
+  if (start + m > d.arena_cap) {
+    if (lead) fail(d, kErrArena, k);
+    return -2;
+  }
+  for (int t = tid; t < m; t += kThreads) {
+    d.arena_rows[start + t] = static_cast<int>(S.A[t] >> 32);
+    d.arena_vals[start + t] = __ddiv_rn(-S.B[t], lkk);
+  }
+  if (lead) {
+    d.diag[k] = lkk;
+    d.col_start[k] = start;
+    d.col_len[k] = m;
+  }
+  PHASE(3);
+
+  // ---- 6-7. weight sort + suffix
+  if (m >= 2) {
+    const int Pm = next_pow2(m);
+    if (Pm > kBigCap) {
+      for (int t = m + tid; t < Pm; t += kThreads) {
+        S.A[t] = ~0ull;
+        S.B[t] = bitsd(kInfBits);
+      }
+      __syncthreads();
+      cta_sort_weight(S.A, S.B, Pm);
+    } else if (Pm <= kThreads) {
+      cta_sort_weight_reg<1>(m, S.A, S.B, xb);
+    } else if (Pm <= 2 * kThreads) {
+      cta_sort_weight_reg<2>(m, S.A, S.B, xb);
+    } else {
+      cta_sort_weight_reg<4>(m, S.A, S.B, xb);
+    }
+    if (lead) serial_suffix(S.B, S.C, m);
+    __syncthreads();
+  }
+  PHASE(4);
+
+  // ---- 8. sampling + emission, one sample per thread per round
+  int emitted = 0;
+  bool bad = false;
+  for (int base = 0; base < m - 1; base += kThreads) {
+    const int i = base + tid;
+    int lo = 0, hi = 0, slot = 0;
+    double wv = 0.0;
+    const bool em = i < m - 1 && draw_sample(d, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv);
+    if (em) {
+      slot = reserve_fill_slot(d, lo);
+      red_add_relaxed(&d.dp[hi], 1);
+      bad = bad || slot < 0;
+    }
+    __syncwarp();
+    if (em && !bad) bad = !write_fill(d, lo, slot, hi, k, wv);
+    emitted += __popc(__ballot_sync(kFull, em));
+  }
+  if (lane == 0) sh.wcount[warp] = emitted;
+  if (bad) sh.bad = 1;
+  __syncthreads();
+  if (sh.bad) return -2;
+  if (lead) {
+    int e = 0;
+    for (int w2 = 0; w2 < kWarps; ++w2) e += sh.wcount[w2];
+    d.samples[k] = e;
+    sh.nready = 0;
+  }
+  PHASE(5);
+  maybe_delay(d, k, 1);
+
+  // ---- 9. release, decrement, collect ready rows into C
+  fence_acq_rel();
+  __syncthreads();
+  unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
+  for (int t = tid; t < m; t += kThreads) {
+    const unsigned long long a = S.A[t];
+    const int row = static_cast<int>(a >> 32);
+    const int mult = static_cast<int>(a & 0xffffffffu);
+    const int old = atom_add_relaxed(&d.dp[row], -mult);
+    if (d.verify && old < mult) fail(d, kErrInternal, row);
+    if (old == mult) {
+      fence_acq_rel();
+      ready[atomicAdd(&sh.nready, 1)] = ready_info(d, row);
+    }
+  }
+  __syncthreads();
+  const int nready = sh.nready;
+  PHASE(6);
+  maybe_delay(d, k, 2);
+  if (nready == 0) return -1;
+
+  // keep-one (any width) + publish the rest
+  unsigned long long best = 0;
+  for (int t = tid; t < nready; t += kThreads) {
+    const unsigned long long rr = ready[t] | (1ull << 63);
+    best = rr > best ? rr : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(kFull, best, o);
+    best = other > best ? other : best;
+  }
+  if (lane == 0) sh.best[warp] = best;
+  __syncthreads();
+  best = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < kWarps; ++w2) best = sh.best[w2] > best ? sh.best[w2] : best;
+  const int keep = static_cast<int>(best & 0xffffffffu);
+  for (int base = 0; base < nready; base += kThreads) {
+    const int t = base + tid;
+    bool pub = false, big = false;
+    int r = 0;
+    if (t < nready) {
+      const unsigned long long rr = ready[t];
+      r = static_cast<int>(rr & 0xffffffffu);
+      big = static_cast<int>(rr >> 32) > kSmallCap;
+      pub = r != keep;
+    }
+    publish(d, pub, big, r, lane);
+  }
+  __syncthreads();  // ready list (C) is reused by the next elimination
+  return keep;
+}
+
+// ============================================================ kernel
+__global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ CtaShared sh;
+  char* smem = reinterpret_cast<char*>(smem_raw);
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  if (ld_relaxed(&d.ctrl->status) != 0) return;
+
+  if (!is_big_cta()) {
+    Scratch S = carve(smem + warp * kSmallBytes, kSmallCap);
+    int done_local = 0;
+    Next nx{-1, -1, 0, 0};
+    while (true) {
+      if (nx.k < 0) {
+        int k = -1;
+        if (lane == 0) {
+          if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
+          k = claim(d, false);
+        }
+        done_local = 0;
+        k = __shfl_sync(kFull, k, 0);
+        if (k < 0) break;
+        nx = {k, -1, 0, 0};
+      }
+      __syncwarp();
+      fence_acq_rel();  // acquire: everything published before k became ready is visible
+      const int k = nx.k;
+      const bool lead = lane == 0;
+      PHASE(0);
+      Next nn = warp_eliminate(d, nx, S, lane);
+      if (nn.k == -2) break;
+      if (nn.k != -3) {
+        PHASE(7);
+        ++done_local;
+      }
+      nx = nn.k >= 0 ? nn : Next{-1, -1, 0, 0};
+    }
+    if (lane == 0 && done_local) atomicAdd(&d.ctrl->eliminated, done_local);
+    return;
+  }
+
+  // big CTA: the whole CTA eliminates one vertex at a time
+  int done_local = 0;
+  int k = -1;
+  while (true) {
+    if (k < 0) {
+      if (threadIdx.x == 0) {
+        if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
+        sh.k = claim(d, true);
+      }
+      done_local = 0;
+      __syncthreads();
+      k = sh.k;
+      __syncthreads();
+      if (k < 0) break;
+    }
+    fence_acq_rel();
+    const bool lead = threadIdx.x == 0;
+    PHASE(0);
+    const int next = cta_eliminate(d, k, smem, sh);
+    if (next == -2) break;
+    PHASE(7);
+    ++done_local;
+    k = next;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && done_local) atomicAdd(&d.ctrl->eliminated, done_local);
+}
+
+int num_sms(int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms > 0 ? sms : 148;
+}
+
+}  // namespace
+
+int eliminate_occupancy_grid(int device) {
+  cudaFuncSetAttribute(eliminate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eliminate_kernel, kThreads, kCtaSmem);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * num_sms(device);
+}
+
+cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used) {
+  if (d.n == 0) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int occ = eliminate_occupancy_grid(dev);
+  int grid = grid_ctas > 0 ? grid_ctas : occ;
+  if (grid > occ) grid = occ;  // persistent: every CTA must be co-resident
+  if (grid < 2) grid = 2;      // at least one small and one big CTA
+  if (grid_used) *grid_used = grid;
+  eliminate_kernel<<<grid, kThreads, kCtaSmem, s>>>(d);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace parac_gpu

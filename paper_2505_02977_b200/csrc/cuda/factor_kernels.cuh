@@ -8,23 +8,33 @@ namespace parac_gpu {
 // Fill entries are 16 B {row, source, weight}: one v4 store / load.
 // Fill storage per vertex (position) lo:
 //   slots [0, C0)                     -> pool0[lo*C0 + s]      (preallocated)
-//   chunk c>=1: slots [C0(2^c-1), C0(2^(c+1)-1)) -> ovf[dir[lo][c-1]-1 ...]
+//   chunk c>=1: slots [C0(2^c-1), C0(2^(c+1)-1)) -> ovf[(dir[lo][c-1]-1)*C0 ...]
 //   chunks are bump-allocated on first touch by the writer of their first slot.
 constexpr int kDirChunks = 16;
 
+// Two warp tiers in the persistent elimination kernel: "small" warps hold
+// columns of up to kSmallCap raw entries in shared memory, one "big" warp per
+// CTA holds up to kBigCap (wider columns use a global-memory slab). A vertex is
+// routed to the matching ready queue when it becomes ready.
+constexpr int kSmallCap = 128;
+constexpr int kBigCap = 1024;
+
 struct Ctrl {
   int status;            // 0 or Errc
-  int q_head;            // next queue slot to claim
-  int q_tail;            // next queue slot to publish
-  int eliminated;        // progress counter (watchdog)
+  int q_head;            // main (small-column) queue: next slot to claim
+  int q_tail;            //                            next slot to publish
+  int b_head;            // big-column queue
+  int b_tail;
+  int eliminated;        // vertices done (flushed per warp before it waits)
   int max_raw;           // largest gathered column
-  int large_cols;        // columns that used the global-scratch path
-  int pad0, pad1;
+  int large_cols;        // columns that used the global-memory slab
   unsigned long long ovf_bump;    // fill overflow pool (entries)
   unsigned long long arena_bump;  // G column arena (entries)
-  unsigned long long large_bump;  // large-column scratch pool (entries)
+  unsigned long long large_bump;  // large-column slab pool (entries)
   long long total_fills;
   long long err_info;
+  int kept;              // hand-offs that skipped the queue (keep-one)
+  int pad;
 };
 
 struct FactorDev {
@@ -40,9 +50,10 @@ struct FactorDev {
   int* fwd_to;
   double* fwd_w;
   int* fdeg;
-  // dependency counters + ready queue
+  // dependency counters + ready queues
   int* dp;
-  int* queue;
+  int* queue;   // main queue [n]
+  int* bqueue;  // big-column queue [n]
   // fills
   int* fill_cnt;
   int4* pool0;
@@ -58,7 +69,7 @@ struct FactorDev {
   double* arena_vals;
   long long arena_cap;
   int* samples;
-  // large-column scratch pool: 48 B per entry
+  // large-column slab pool: 24 B per entry
   char* large_pool;
   long long large_cap;
   // control
@@ -67,6 +78,7 @@ struct FactorDev {
   unsigned long long watchdog_ns;
   int verify;
   int delay_ns;
+  unsigned long long* vtimes;  // optional [2n] start/end globaltimer per position
 };
 
 // Launchers (stream-ordered). All return cudaError_t of the launch.

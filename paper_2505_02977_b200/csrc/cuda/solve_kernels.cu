@@ -208,6 +208,17 @@ __global__ void gt_sort_kernel(int n, const long long* gt_ptr, int* gt_col, doub
   }
 }
 
+// Relaxed polling with exponential backoff (no L1 invalidation per poll); the
+// caller follows with fence_acq_rel() before reading the producer's data.
+__device__ __forceinline__ void wait_stamp(const int* flag, int stamp) {
+  if (ld_relaxed(flag) >= stamp) return;
+  unsigned ns = 32;
+  do {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  } while (ld_relaxed(flag) < stamp);
+}
+
 // ASAP levels of the factor DAG (schedule_levels, src/factor_par.cpp:659-684):
 // level[r] = 1 + max level over G's row r. Sync-free, positions claimed in
 // ascending order (all dependencies are earlier positions => deadlock-free).
@@ -222,7 +233,8 @@ __global__ void level_kernel(int n, const long long* gt_ptr, const int* gt_col, 
     int lv = 0;
     for (long long t = gt_ptr[r] + lane; t < gt_ptr[r + 1]; t += 32) {
       const int k = gt_col[t];
-      while (ld_acquire(&flags[k]) < stamp) __nanosleep(20);
+      wait_stamp(&flags[k], stamp);
+      fence_acq_rel();
       lv = max(lv, ld_relaxed(&level[k]));
     }
     lv = warp_max(lv) + 1;
@@ -376,9 +388,13 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
       const long long t = base + lane;
       double prod = 0.0;
       bool use = false;
+      int k = 0;
       if (t < e) {
-        const int k = gt_col[t];
-        while (ld_acquire(&flags[k]) < stamp) __nanosleep(16);
+        k = gt_col[t];
+        wait_stamp(&flags[k], stamp);
+      }
+      fence_acq_rel();
+      if (t < e) {
         const double yk = __ldcg(yf + k);
         use = yk != 0.0;
         prod = __dmul_rn(gt_val[t], yk);
@@ -415,11 +431,13 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
     for (long long base = b; base < e; base += 32) {
       const long long t = base + lane;
       double prod = 0.0;
+      int r = 0;
       if (t < e) {
-        const int r = rows[t];
-        while (ld_acquire(&flags[r]) < stamp) __nanosleep(16);
-        prod = __dmul_rn(vals[t], __ldcg(zb + r));
+        r = rows[t];
+        wait_stamp(&flags[r], stamp);
       }
+      fence_acq_rel();
+      if (t < e) prod = __dmul_rn(vals[t], __ldcg(zb + r));
       const int cnt = static_cast<int>(min(32ll, e - base));
       for (int j = 0; j < cnt; ++j) acc = __dsub_rn(acc, __shfl_sync(kFull, prod, j));
     }

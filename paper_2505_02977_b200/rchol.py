@@ -233,6 +233,7 @@ class GpuOptions:
     verify: bool = False             # TestHooks::verify analogue (device assertions)
     grid_ctas: int = 0
     delay_ns: int = 0                # TestHooks::delay analogue (random __nanosleep)
+    record_times: bool = False       # ParOptions::record_vertex_times analogue
 
     def native(self) -> "L.parac_gpu_options":
         o = L.parac_gpu_options()
@@ -245,6 +246,7 @@ class GpuOptions:
         o.verify = int(self.verify)
         o.grid_ctas = self.grid_ctas
         o.delay_ns = self.delay_ns
+        o.record_times = int(self.record_times)
         return o
 
 
@@ -335,6 +337,14 @@ class GpuContext:
                                       _ptr(diag), *[(_ptr(a) if a is not None else None) for a in st]))
         f = LdlFactor(n, col_ptr, rows[:z], vals[:z], diag[:n], ordering.perm)
         return f, [a[:n] if a is not None else None for a in st]
+
+    def vertex_times(self) -> np.ndarray:
+        """[n, 8] phase timestamps (globaltimer ns) per position (record_times runs);
+        column 0 = start, 7 = end; see parac_gpu_download_times."""
+        n = self._factor_n
+        out = np.empty(8 * max(n, 1), np.uint64)
+        _check(lib.parac_gpu_download_times(self.handle, _ptr(out)))
+        return out[:8 * n].reshape(n, 8)
 
     def upload_factor(self, f: LdlFactor) -> None:
         _check(lib.parac_gpu_upload_factor(self.handle, f.n, _ptr(f.col_ptr), _ptr(f.rows),

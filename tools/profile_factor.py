@@ -1,0 +1,122 @@
+#!/usr/bin/env python3
+"""Timeline analysis of one factorization (record_times): where does the
+eliminate kernel's time go? Prints the elimination-rate profile, per-vertex
+service time vs column size, and the realised critical path split into
+service time (inside eliminate_vertex) and hand-off latency (ready -> claimed).
+
+  python tools/profile_factor.py [--n 128] [--workload poisson3d] [--json out.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2505_02977_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--workload", default="poisson3d")
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--grid", type=int, default=0)
+    args = ap.parse_args()
+    if args.workload == "poisson3d":
+        g = P.gen_poisson3d(args.n)
+    elif args.workload == "poisson27":
+        g = P.gen_poisson27(args.n, 1)
+    elif args.workload == "poisson2d":
+        g = P.gen_poisson2d(args.n)
+    else:
+        g = P.gen_rmat(args.n, 16, 0)
+    o = P.ordering_random(g.n, 0)
+    ctx = P.GpuContext(0)
+    opts = P.GpuOptions(record_times=True, grid_ctas=args.grid)
+    st = P.FactorStats()
+    for _ in range(2):
+        f = P.factor_gpu(g, o, 0, opts, st, ctx=ctx)
+    tt = ctx.vertex_times().astype(np.int64)
+    n = g.n
+    t0 = tt[:, 0].min()
+    start = (tt[:, 0] - t0) / 1e3  # us
+    end = (tt[:, 7] - t0) / 1e3
+    dur = end - start
+    # per-phase durations (a skipped phase inherits the previous timestamp)
+    ph = tt.copy()
+    for i in range(1, 8):
+        ph[:, i] = np.where(ph[:, i] == 0, ph[:, i - 1], ph[:, i])
+    pdur = np.diff(ph, axis=1) / 1e3
+    names = ["gather+sort", "merge", "lkk+column", "wsort+suffix", "sample+emit", "fence+decrement",
+             "ready+publish"]
+    raw = g_fdeg = None
+    m = st.merged_degree
+    fills = st.fills_received
+    # forward degree per position
+    pos = o.perm
+    src = np.repeat(np.arange(n), np.diff(g.ptr))
+    fwd = np.zeros(n, np.int64)
+    np.add.at(fwd, pos[src][pos[g.adj] > pos[src]], 1)
+    raw = fwd + fills
+    # ready time: last decrement = end of the latest column containing k
+    ready = np.full(n, -1.0)
+    cols = np.repeat(np.arange(n), np.diff(f.col_ptr))
+    np.maximum.at(ready, f.rows, end[cols])
+    hop = np.where(ready >= 0, start - np.maximum(ready, 0), start)
+    total = end.max()
+    out = {"n": n, "eliminate_ms": st.eliminate_ms, "span_us": float(total),
+           "service_us_mean": float(dur.mean()), "hop_us_median": float(np.median(hop[ready >= 0]))}
+    # rate profile
+    edges = np.linspace(0, total, 21)
+    hist, _ = np.histogram(end, bins=edges)
+    out["completions_per_5pct"] = hist.tolist()
+    # service time by raw size
+    bins = [0, 8, 16, 32, 64, 128, 256, 1024, 1 << 30]
+    by = []
+    for lo, hi in zip(bins[:-1], bins[1:]):
+        sel = (raw >= lo) & (raw < hi)
+        if sel.any():
+            by.append({"raw": f"[{lo},{hi})", "count": int(sel.sum()),
+                       "service_us_mean": float(dur[sel].mean()),
+                       "service_us_p99": float(np.percentile(dur[sel], 99)),
+                       "phases_us": {nm: round(float(pdur[sel, i].mean()), 2)
+                                     for i, nm in enumerate(names)}})
+    out["service_by_raw"] = by
+    # realised critical path: walk back from the last finisher via its latest dep
+    parent_of = np.full(n, -1, np.int64)
+    best = np.full(n, -1.0)
+    order = np.argsort(cols, kind="stable")
+    # latest-finishing dependency per row
+    for_rows = f.rows
+    e_cols = end[cols]
+    idx = np.lexsort((e_cols, for_rows))
+    last = np.ones(len(idx), bool)
+    last[:-1] = for_rows[idx][1:] != for_rows[idx][:-1]
+    sel = idx[last]
+    parent_of[for_rows[sel]] = cols[sel]
+    k = int(np.argmax(end))
+    chain = []
+    while k >= 0:
+        chain.append(k)
+        k = int(parent_of[k])
+    chain = chain[::-1]
+    ch = np.array(chain)
+    out["critical_path"] = {
+        "length": len(chain), "service_us": float(dur[ch].sum()), "hop_us": float(hop[ch].sum()),
+        "initial_wait_us": float(start[ch[0]]), "raw_mean": float(raw[ch].mean()),
+        "m_mean": float(m[ch].mean()), "service_us_per_vertex": float(dur[ch].mean()),
+        "hop_us_per_vertex": float(hop[ch[1:]].mean()) if len(ch) > 1 else 0.0,
+        "phases_us_per_vertex": {nm: round(float(pdur[ch, i].mean()), 2) for i, nm in enumerate(names)},
+    }
+    print(json.dumps(out, indent=1))
+    if args.json:
+        with open(args.json, "w") as fh:
+            json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

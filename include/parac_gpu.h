@@ -208,6 +208,14 @@ typedef struct {
  * PARAC_NOT_CONNECTED for a disconnected graph, as the reference. */
 int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_iters, double* x,
                   parac_gpu_solve_report* report);
+/* Triangular-sweep mode of the preconditioner on ctx:
+ *   0 default: parac_gpu_apply_preconditioner bit-identical to the reference
+ *     (solver.cpp:32-74 summation order), parac_gpu_pcg in fast mode;
+ *   1 exact for both; 2 fast for both. Fast mode sums each row with a
+ *   deterministic (run-to-run identical) tree over entries ordered by
+ *   dependency level: same operator, different rounding, far shorter
+ *   critical path. */
+int parac_gpu_set_preconditioner_mode(parac_gpu_ctx* ctx, int32_t mode);
 /* apply_preconditioner (solver.hpp:30, src/solver.cpp:32-74) */
 int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* z);
 /* laplacian_apply (solver.hpp:33, src/solver.cpp:76-93) */

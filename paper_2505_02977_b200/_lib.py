@@ -81,6 +81,7 @@ SIGNATURES = {
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "parac_gpu_schedule_levels": (C.c_int, [vp, vp, P(i32)]),
     "parac_gpu_pcg": (C.c_int, [vp, vp, f64, i32, vp, P(parac_gpu_solve_report)]),
+    "parac_gpu_set_preconditioner_mode": (C.c_int, [vp, i32]),
     "parac_gpu_apply_preconditioner": (C.c_int, [vp, vp, vp]),
     "parac_gpu_laplacian_apply": (C.c_int, [vp, vp, vp]),
     "parac_make_rhs": (C.c_int, [P(parac_csr), C.c_int, u64, vp]),

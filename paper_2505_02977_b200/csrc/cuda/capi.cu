@@ -73,7 +73,7 @@ struct parac_gpu_ctx {
   DevBuf<double> w;
   DevBuf<int> perm;
   // factor working state
-  DevBuf<int> inv, fdeg, dp, queue, bqueue, fill_cnt, samples, col_len, arena_rows;
+  DevBuf<int> inv, fdeg, dp, queue, bqueue, fill_cnt, samples, col_len, arena_rows, level;
   DevBuf<long long> fwd_ptr, col_start, tiles;
   DevBuf<int> fwd_to;
   DevBuf<double> fwd_w, diag, arena_vals;
@@ -139,6 +139,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->bqueue.ensure(nn);
   ctx->fill_cnt.ensure(nn);
   ctx->samples.ensure(nn);
+  ctx->level.ensure(nn);
   ctx->col_len.ensure(nn);
   ctx->col_start.ensure(nn);
   ctx->diag.ensure(nn);
@@ -184,6 +185,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.arena_vals = ctx->arena_vals.p;
   d.arena_cap = b.arena;
   d.samples = ctx->samples.p;
+  d.level = ctx->level.p;
   d.large_pool = ctx->large_pool.p;
   d.large_cap = b.large;
   d.ctrl = ctx->ctrl.p;
@@ -293,7 +295,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
-  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->queue.release(); ctx->bqueue.release();
+  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->level.release(); ctx->queue.release(); ctx->bqueue.release();
   ctx->fill_cnt.release(); ctx->samples.release(); ctx->col_len.release();
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
@@ -504,6 +506,7 @@ SolveInputs solve_inputs(parac_gpu_ctx* ctx) {
   in.vals = ctx->vals.p;
   in.diag = ctx->f_external ? ctx->f_diag_ext.p : ctx->diag.p;
   in.perm = ctx->f_external ? ctx->f_perm_ext.p : ctx->perm.p;
+  in.level = ctx->f_external ? nullptr : ctx->level.p;
   in.stream = ctx->stream;
   in.device = ctx->device;
   in.state = &ctx->solve;

@@ -92,14 +92,20 @@ __device__ int claim(const FactorDev& d, bool big) {
   unsigned long long t0 = globaltimer_ns();
   int last = ld_relaxed(&d.ctrl->eliminated);
   int iter = 0;
+  (void)tail_p;
   while (true) {
-    const int dist = idx - ld_relaxed(tail_p);
-    const unsigned ns = dist <= 0 ? 32u : (dist < 16 ? 128u * dist : 2048u);
+    // Distance probe on a slot-specific address (no shared word polled by
+    // every waiter): if the slot 16 places earlier is still empty, we are far
+    // from the publishing front and sleep long.
+    unsigned ns;
+    if (idx < 16 || ld_relaxed(&queue[idx - 16]) >= 0) ns = 32;
+    else if (idx < 256 || ld_relaxed(&queue[idx - 256]) >= 0) ns = 512;
+    else ns = 4096;
     __nanosleep(ns);
     v = ld_relaxed(&queue[idx]);
     if (v >= 0) return v;
-    if (ld_relaxed(&d.ctrl->status) != 0) return -2;
-    if ((++iter & 7) == 0) {
+    if ((++iter & 15) == 0) {
+      if (ld_relaxed(&d.ctrl->status) != 0) return -2;
       const int done = ld_relaxed(&d.ctrl->eliminated);
       if (done >= d.n) return -1;
       const unsigned long long now = globaltimer_ns();
@@ -566,6 +572,12 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
   }
   if (__any_sync(kFull, bad)) return {-2, -1, 0, 0};
   if (lead) d.samples[k] = emitted;
+  // ASAP level of the factor DAG (schedule_levels, factor_par.cpp:659-684):
+  // level[row] >= level[k] + 1, published before the decrements release row.
+  if (d.level) {
+    const int lk = ld_relaxed(&d.level[k]) + 1;
+    for (int t = lane; t < m; t += 32) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
+  }
   PHASE(5);
   maybe_delay(d, k, 1);
 
@@ -819,6 +831,10 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     for (int w2 = 0; w2 < kWarps; ++w2) e += sh.wcount[w2];
     d.samples[k] = e;
     sh.nready = 0;
+  }
+  if (d.level) {  // ASAP levels, as in the warp path
+    const int lk = ld_relaxed(&d.level[k]) + 1;
+    for (int t = tid; t < m; t += kThreads) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
   }
   PHASE(5);
   maybe_delay(d, k, 1);

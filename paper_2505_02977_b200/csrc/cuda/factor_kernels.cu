@@ -42,6 +42,7 @@ __global__ void pos_count_kernel(FactorDev d) {
   d.samples[p] = 0;
   d.col_len[p] = 0;  // K4 stays in bounds even when an aborted run skipped p
   d.col_start[p] = 0;
+  if (d.level) d.level[p] = 1;
 }
 
 // Warp per position: forward neighbours (q > p) in ascending position order.

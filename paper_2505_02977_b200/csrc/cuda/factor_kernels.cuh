@@ -69,6 +69,7 @@ struct FactorDev {
   double* arena_vals;
   long long arena_cap;
   int* samples;
+  int* level;  // optional: ASAP level per position (schedule_levels), 1-based
   // large-column slab pool: 24 B per entry
   char* large_pool;
   long long large_cap;

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,6 +38,7 @@ namespace {
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed => deterministic reductions
 constexpr int kRedThreads = 256;
 constexpr int kSweepThreads = 256;
+constexpr int kRowBlock = 256;  // row entries staged per warp before the serial chain
 
 enum Slot { kSlotA = 0, kSlotB = 1, kSlotC = 2, kSlots = 3 };
 enum Scalar { kRz0 = 0, kRz1 = 1, kPlpOk = 2, kScalars = 8 };
@@ -368,13 +371,216 @@ __global__ void diff_norm_kernel(int n, const double* a, const double* b, double
 }
 
 // ------------------------------------------------------------------- K6
-// Forward: y[r] = rhs[r] - sum_{k<r} G(r,k) y[k], k ascending, skipping y[k]==0
-// exactly like the column scatter (solver.cpp:45-52); then the D^+ step
-// (:54-58) writes yd[r]. rhs[r] = rvec[inv[r]] (permutation in, :40-43).
+// Level-pipelined triangular sweeps. Rows are claimed in ASAP-level order
+// (forward: ascending, backward: descending). A row of level L starts once
+// every row of level L-1 (forward) / L+1 (backward) has finished: by
+// induction all its dependencies are then complete, so only one counter is
+// polled per row (lane 0, backoff by distance to the highest finished level)
+// instead of one flag per dependency -- per-dependency polling by ~9.5k warps
+// saturated L2 with requests. done[L] counts finished rows of level L; the
+// finishing row's increment follows a release fence, the waiter's relaxed
+// read is followed by an acquire fence.
+__device__ __forceinline__ int level_size(const long long* lvl_off, int L) {
+  return static_cast<int>(lvl_off[L + 1] - lvl_off[L]);
+}
+
+// Wait until level L is complete. The sleep follows the distance to the
+// finishing front, probed on level-specific counters 1, 3 and 15 levels back
+// in sweep order (step = -1 forward, +1 backward): no word is polled by every
+// waiter, and the thousands of waiters far from the front poll rarely, which
+// keeps L2 latency low for the rows on the critical path.
+__device__ __forceinline__ bool level_done(const int* done, const long long* lvl_off, int L, int lo,
+                                           int hi) {
+  return L < lo || L > hi || ld_relaxed(&done[L]) >= level_size(lvl_off, L);
+}
+
+__device__ __forceinline__ void wait_level(const int* done, const long long* lvl_off, int L, int step,
+                                           int depth) {
+  if (level_done(done, lvl_off, L, 1, depth)) return;
+  while (true) {
+    unsigned ns;
+    if (level_done(done, lvl_off, L + step, 1, depth)) ns = 32;
+    else if (level_done(done, lvl_off, L + 3 * step, 1, depth)) ns = 256;
+    else if (level_done(done, lvl_off, L + 15 * step, 1, depth)) ns = 1024;
+    else ns = 4096;
+    __nanosleep(ns);
+    if (level_done(done, lvl_off, L, 1, depth)) return;
+  }
+}
+
+__device__ __forceinline__ void finish_row(int* done, int L) {
+  fence_acq_rel();  // release: this row's value before the count
+  atomicAdd(&done[L], 1);
+}
+
+// acc -= prod[0] - ... - prod[cnt-1], strictly in order, by lane 0 from the
+// warp's shared slots (loads hoisted 4 at a time; ~one DSUB latency per term).
+__device__ __forceinline__ double serial_sub(double acc, const double* buf, int cnt) {
+  int j = 0;
+  for (; j + 8 <= cnt; j += 8) {
+    double p[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) p[q] = buf[j + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = __dsub_rn(acc, p[q]);
+  }
+  for (; j < cnt; ++j) acc = __dsub_rn(acc, buf[j]);
+  return acc;
+}
+
+// Products G(.,.) * x[idx] of one block of a row into the warp's shared slots.
+// All index loads, then all value loads, then the stores: explicit register
+// staging, because global loads through generic pointers are otherwise not
+// hoisted above the shared-memory stores (measured 50 -> ~12 cycles/entry).
+// skip_zero replaces terms with x == 0 by +0.0 (see the forward sweep).
+__device__ __forceinline__ void stage_products(const int* idx, const double* g, const double* x, int cnt,
+                                               int lane, bool skip_zero, double* wbuf) {
+  constexpr int Q = kRowBlock / 32;
+  int ci[Q];
+  double xv[Q], gv[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) ci[q] = q * 32 + lane < cnt ? idx[q * 32 + lane] : 0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    xv[q] = q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+    gv[q] = q * 32 + lane < cnt ? g[q * 32 + lane] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (q * 32 + lane < cnt) wbuf[q * 32 + lane] = (skip_zero && xv[q] == 0.0) ? 0.0 : __dmul_rn(gv[q], xv[q]);
+}
+
+// Forward: y[r] = rhs[r] - sum_{k<r} G(r,k) y[k], k ascending, skipping
+// y[k] == 0 exactly like the column scatter (solver.cpp:45-52; a skipped term
+// is replaced by +0.0, which leaves acc bit-identical); then D^+ (:54-58) into
+// yd. rhs[r] = rvec[inv[r]] (permutation in, :40-43).
 __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
-    int n, const int* order, const long long* gt_ptr, const int* gt_col, const double* gt_val,
-    const double* diag, const int* inv, const double* rvec, double* yf, double* yd, int* flags,
-    int stamp, int* counter) {
+    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
+    const int* gt_col, const double* gt_val, const double* diag, const int* inv,
+    const double* rvec, double* yf, double* yd, int* done, int* frontier, int* counter,
+    unsigned long long* trace) {
+  __shared__ double buf[kSweepThreads / 32][kRowBlock];
+  const int lane = lane_id();
+  double* wbuf = buf[threadIdx.x >> 5];
+  while (true) {
+    int i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= n) return;
+    const int r = order[i];
+    const int L = level[r];
+    if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
+    if (L > 1 && lane == 0) wait_level(done, lvl_off, L - 1, -1, depth);
+    __syncwarp();
+    fence_acq_rel();
+    if (trace && lane == 0) trace[3 * r] = globaltimer_ns();
+    double acc = rvec[inv[r]];
+    const long long b = gt_ptr[r], e = gt_ptr[r + 1];
+    for (long long base = b; base < e; base += kRowBlock) {
+      const int cnt = static_cast<int>(min(static_cast<long long>(kRowBlock), e - base));
+      stage_products(gt_col + base, gt_val + base, yf, cnt, lane, true, wbuf);
+      __syncwarp();
+      if (lane == 0) acc = serial_sub(acc, wbuf, cnt);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      yf[r] = acc;
+      const double d = diag[r];
+      yd[r] = d > 0.0 ? __ddiv_rn(acc, d) : 0.0;
+      if (trace) trace[3 * r + 1] = globaltimer_ns();
+      finish_row(done, L);
+    }
+  }
+}
+
+// Backward: z[k] = yd[k] - sum_{r in col k, ascending} G(r,k) z[r] (solver.cpp:60-66).
+__global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
+    int n, int depth, const int* order, const int* level, const long long* lvl_off,
+    const long long* col_ptr, const int* rows, const double* vals, const double* yd, double* zb,
+    int* done, int* frontier, int* counter, unsigned long long* trace) {
+  __shared__ double buf[kSweepThreads / 32][kRowBlock];
+  const int lane = lane_id();
+  double* wbuf = buf[threadIdx.x >> 5];
+  while (true) {
+    int i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= n) return;
+    const int k = order[n - 1 - i];
+    const int L = level[k];
+    if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
+    if (L < depth && lane == 0) wait_level(done, lvl_off, L + 1, +1, depth);
+    __syncwarp();
+    fence_acq_rel();
+    if (trace && lane == 0) trace[3 * k] = globaltimer_ns();
+    double acc = yd[k];
+    const long long b = col_ptr[k], e = col_ptr[k + 1];
+    for (long long base = b; base < e; base += kRowBlock) {
+      const int cnt = static_cast<int>(min(static_cast<long long>(kRowBlock), e - base));
+      stage_products(rows + base, vals + base, zb, cnt, lane, false, wbuf);
+      __syncwarp();
+      if (lane == 0) acc = serial_sub(acc, wbuf, cnt);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      zb[k] = acc;
+      if (trace) trace[3 * k + 1] = globaltimer_ns();
+      finish_row(done, L);
+    }
+  }
+}
+
+// ------------------------------------------------------------ K6 (fast mode)
+// PCG does not need the reference's summation order (only its iteration count
+// and residual, BASELINE north_star), so the default preconditioner for the
+// solve sums each row with a fixed per-lane split + warp tree (deterministic,
+// run-to-run identical) and -- the point -- consumes a row's entries sorted by
+// the level of the value they read: every block of 32 waits only for its own
+// latest dependency level, so all but the last block of a row are summed while
+// earlier levels are still finishing. After the last dependency lands, a row
+// costs one load round trip plus a 5-step tree.
+//
+// Invariant (both directions): done[X] == size(X) implies every level before X
+// in sweep order is complete -- each row of level X reads a value of the
+// previous level (ASAP levels), so it cannot finish before that level did.
+
+// Segmented sort of (idx, val) within each segment by key = level-derived u64.
+// Warp per segment; <= 32 in registers, longer segments by ranking in place
+// through a scratch copy (rare: long rows of the last few hundred levels).
+__global__ void level_sort_kernel(int nseg, const long long* seg, const int* idx_in, const double* val_in,
+                                  const int* level, int desc, int maxlevel, int* idx_out, double* val_out,
+                                  int* lvl_out) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int sgi = gw; sgi < nseg; sgi += nw) {
+    const long long b = seg[sgi];
+    const int len = static_cast<int>(seg[sgi + 1] - b);
+    auto key_of = [&](int j) -> unsigned long long {
+      const int id = idx_in[b + j];
+      const int lv = level[id];
+      const unsigned hi = desc ? static_cast<unsigned>(maxlevel - lv) : static_cast<unsigned>(lv);
+      return (static_cast<unsigned long long>(hi) << 32) | static_cast<unsigned>(id);
+    };
+    for (int base = 0; base < len; base += 32) {
+      const int t = base + lane;
+      const unsigned long long mk = t < len ? key_of(t) : ~0ull;
+      int rank = 0;
+      for (int j = 0; j < len; ++j) rank += key_of(j) < mk;
+      if (t < len) {
+        idx_out[b + rank] = idx_in[b + t];
+        val_out[b + rank] = val_in[b + t];
+        lvl_out[b + rank] = level[idx_in[b + t]];
+      }
+    }
+  }
+}
+
+// Forward, fast: y[r] = rhs[r] - sum G(r,k) y[k]; entries sorted by level[k] ascending.
+__global__ void __launch_bounds__(kSweepThreads) sweep_forward_fast_kernel(
+    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
+    const int* fcol, const double* fval, const int* flvl, const double* diag, const int* inv,
+    const double* rvec, double* yf, double* yd, int* done, int* counter) {
   const int lane = lane_id();
   while (true) {
     int i = 0;
@@ -382,43 +588,38 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
     i = __shfl_sync(kFull, i, 0);
     if (i >= n) return;
     const int r = order[i];
-    double acc = rvec[inv[r]];
+    const int L = level[r];
     const long long b = gt_ptr[r], e = gt_ptr[r + 1];
+    double part = 0.0;
+    int waited = 0;  // highest level known complete
     for (long long base = b; base < e; base += 32) {
       const long long t = base + lane;
-      double prod = 0.0;
-      bool use = false;
-      int k = 0;
-      if (t < e) {
-        k = gt_col[t];
-        wait_stamp(&flags[k], stamp);
+      const long long last = min(base + 31, e - 1);
+      const int need = flvl[last];  // the block's latest dependency level
+      if (need > waited) {
+        if (lane == 0) wait_level(done, lvl_off, need, -1, depth);
+        __syncwarp();
+        fence_acq_rel();
+        waited = need;
       }
-      fence_acq_rel();
-      if (t < e) {
-        const double yk = __ldcg(yf + k);
-        use = yk != 0.0;
-        prod = __dmul_rn(gt_val[t], yk);
-      }
-      const int cnt = static_cast<int>(min(32ll, e - base));
-      for (int j = 0; j < cnt; ++j) {
-        const double pj = __shfl_sync(kFull, prod, j);
-        const bool uj = __shfl_sync(kFull, use, j);
-        if (uj) acc = __dsub_rn(acc, pj);
-      }
+      if (t < e) part += fval[t] * __ldcg(yf + fcol[t]);
     }
+    const double sum = warp_sum(part);
     if (lane == 0) {
+      const double acc = rvec[inv[r]] - sum;
       yf[r] = acc;
       const double d = diag[r];
-      yd[r] = d > 0.0 ? __ddiv_rn(acc, d) : 0.0;
-      st_release(&flags[r], stamp);
+      yd[r] = d > 0.0 ? acc / d : 0.0;
+      finish_row(done, L);
     }
   }
 }
 
-// Backward: z[k] = yd[k] - sum_{r in col k, ascending} G(r,k) z[r] (solver.cpp:60-66).
-__global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
-    int n, const int* order, const long long* col_ptr, const int* rows, const double* vals,
-    const double* yd, double* zb, int* flags, int stamp, int* counter) {
+// Backward, fast: z[k] = yd[k] - sum G(r,k) z[r]; entries sorted by level[r] descending.
+__global__ void __launch_bounds__(kSweepThreads) sweep_backward_fast_kernel(
+    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* col_ptr,
+    const int* brow, const double* bval, const int* blvl, const double* yd, double* zb, int* done,
+    int* counter) {
   const int lane = lane_id();
   while (true) {
     int i = 0;
@@ -426,24 +627,26 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
     i = __shfl_sync(kFull, i, 0);
     if (i >= n) return;
     const int k = order[n - 1 - i];
-    double acc = yd[k];
+    const int L = level[k];
     const long long b = col_ptr[k], e = col_ptr[k + 1];
+    double part = 0.0;
+    int waited = depth + 1;  // lowest level known complete
     for (long long base = b; base < e; base += 32) {
       const long long t = base + lane;
-      double prod = 0.0;
-      int r = 0;
-      if (t < e) {
-        r = rows[t];
-        wait_stamp(&flags[r], stamp);
+      const long long last = min(base + 31, e - 1);
+      const int need = blvl[last];
+      if (need < waited) {
+        if (lane == 0) wait_level(done, lvl_off, need, +1, depth);
+        __syncwarp();
+        fence_acq_rel();
+        waited = need;
       }
-      fence_acq_rel();
-      if (t < e) prod = __dmul_rn(vals[t], __ldcg(zb + r));
-      const int cnt = static_cast<int>(min(32ll, e - base));
-      for (int j = 0; j < cnt; ++j) acc = __dsub_rn(acc, __shfl_sync(kFull, prod, j));
+      if (t < e) part += bval[t] * __ldcg(zb + brow[t]);
     }
+    const double sum = warp_sum(part);
     if (lane == 0) {
-      zb[k] = acc;
-      st_release(&flags[k], stamp);
+      zb[k] = yd[k] - sum;
+      finish_row(done, L);
     }
   }
 }
@@ -468,7 +671,8 @@ void ensure_vectors(SolveState& s, int n) {
   dalloc(s.x, c); dalloc(s.r, c); dalloc(s.p, c); dalloc(s.lp, c); dalloc(s.z, c);
   dalloc(s.best, c); dalloc(s.yf, c); dalloc(s.yd, c); dalloc(s.zb, c); dalloc(s.rhs, c);
   dalloc(s.wdeg, c); dalloc(s.inv, c); dalloc(s.level, c); dalloc(s.order, c);
-  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2);
+  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2); dalloc(s.done, 2 * c + 8);
+  if (std::getenv("PARAC_SWEEP_TRACE")) dalloc(s.trace, 6 * c);  // diagnostics only
   dalloc(s.partials, static_cast<std::size_t>(kRedBlocks) * kSlots);
   dalloc(s.scalars, kScalars);
   dalloc(s.counters, 16);
@@ -524,8 +728,15 @@ void prepare_factor(const SolveInputs& in) {
   const int blocks = (n + 255) / 256;
   const int sms = sm_count(in.device);
   if (s.cap_z < static_cast<std::size_t>(std::max<long long>(Z, 1))) {
-    dalloc(s.gt_col, static_cast<std::size_t>(std::max<long long>(Z, 1)));
-    dalloc(s.gt_val, static_cast<std::size_t>(std::max<long long>(Z, 1)));
+    const std::size_t cz = static_cast<std::size_t>(std::max<long long>(Z, 1));
+    dalloc(s.gt_col, cz);
+    dalloc(s.gt_val, cz);
+    dalloc(s.ff_col, cz);
+    dalloc(s.ff_val, cz);
+    dalloc(s.ff_lvl, cz);
+    dalloc(s.fb_row, cz);
+    dalloc(s.fb_val, cz);
+    dalloc(s.fb_lvl, cz);
     s.cap_z = static_cast<std::size_t>(std::max<long long>(Z, 1));
   }
   inverse_perm_kernel<<<blocks, 256, 0, st>>>(n, in.perm, s.inv);
@@ -538,11 +749,17 @@ void prepare_factor(const SolveInputs& in) {
   gt_fill_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.gt_ptr, cnt, s.gt_col, s.gt_val);
   gt_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val);
   note_launches(2);
-  // levels
-  const int stamp = ++s.epoch;
+  // levels: recorded by the elimination kernel for factors computed here,
+  // recomputed (sync-free pass over G's rows) for uploaded ones
   check(cudaMemsetAsync(s.counters, 0, sizeof(int) * 4, st), "memset");
-  level_kernel<<<sweep_grid(in.device), kSweepThreads, 0, st>>>(n, s.gt_ptr, s.gt_col, s.level,
-                                                                s.flags, stamp, s.counters);
+  if (in.level) {
+    check(cudaMemcpyAsync(s.level, in.level, sizeof(int) * n, cudaMemcpyDeviceToDevice, st), "d2d");
+  } else {
+    const int stamp = ++s.epoch;
+    level_kernel<<<sweep_grid(in.device), kSweepThreads, 0, st>>>(n, s.gt_ptr, s.gt_col, s.level,
+                                                                  s.flags, stamp, s.counters);
+    note_launches(1);
+  }
   // counting sort of positions by level
   int* hist = s.tmp_int;  // levels are 1..n
   check(cudaMemsetAsync(hist, 0, sizeof(int) * (n + 2), st), "memset");
@@ -556,6 +773,13 @@ void prepare_factor(const SolveInputs& in) {
   check(cudaMemcpyAsync(&depth, s.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "prepare_factor");
   s.depth = depth;
+  // fast-mode copies: G rows sorted by level[k] ascending, G columns by level[r] descending
+  level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val, s.level, 0, depth + 1,
+                                             s.ff_col, s.ff_val, s.ff_lvl);
+  level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.level, 1, depth + 1,
+                                             s.fb_row, s.fb_val, s.fb_lvl);
+  note_launches(2);
+  check(cudaGetLastError(), "level sort");
   s.factor_ready = true;
 }
 
@@ -586,16 +810,29 @@ struct Solver {
   }
 
   // z (label space) = M^-1 r (label space); partial r.z into slot.
-  void precond(const double* r, double* z, int slot) {
-    const int f_stamp = ++s.epoch;
-    const int b_stamp = ++s.epoch;
-    check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 2, st), "memset");
+  void precond(const double* r, double* z, int slot, bool exact = true) {
+    const int D = s.depth;
+    int* done_f = s.done;
+    int* done_b = s.done + (D + 2);
+    check(cudaMemsetAsync(s.done, 0, sizeof(int) * 2 * (D + 2), st), "memset");
+    check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
+    if (!exact) {
+      sweep_forward_fast_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+          in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, in.diag,
+          s.inv, r, s.yf, s.yd, done_f, s.counters + 2);
+      sweep_backward_fast_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+          in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, s.yd, s.zb,
+          done_b, s.counters + 3);
+      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
+      note_launches(3);
+      return;
+    }
     sweep_forward_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
-        in.f_n, s.order, s.gt_ptr, s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, s.flags,
-        f_stamp, s.counters + 2);
+        in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.gt_col, s.gt_val, in.diag, s.inv, r,
+        s.yf, s.yd, done_f, s.counters + 4, s.counters + 2, s.trace);
     sweep_backward_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
-        in.f_n, s.order, in.col_ptr, in.rows, in.vals, s.yd, s.zb, s.flags, b_stamp,
-        s.counters + 3);
+        in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, in.rows, in.vals, s.yd, s.zb, done_b,
+        s.counters + 5, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
     gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
     note_launches(3);
   }
@@ -621,6 +858,22 @@ void download(double* dst, const double* src, int n, cudaStream_t st) {
   check(cudaStreamSynchronize(st), "d2h sync");
 }
 
+// Diagnostics (PARAC_SWEEP_TRACE=<file>): per-position start/end of the last
+// forward and backward sweeps, levels and level order, as raw little-endian arrays.
+void dump_sweep_trace(const SolveInputs& in, const char* path) {
+  const int n = in.f_n;
+  std::vector<unsigned long long> tr(6 * static_cast<std::size_t>(n));
+  std::vector<int> lv(n);
+  check(cudaMemcpy(tr.data(), in.state->trace, tr.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+  check(cudaMemcpy(lv.data(), in.state->level, lv.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return;
+  std::fwrite(&n, 4, 1, f);
+  std::fwrite(tr.data(), 8, tr.size(), f);
+  std::fwrite(lv.data(), 4, lv.size(), f);
+  std::fclose(f);
+}
+
 void need_graph(const SolveInputs& in) {
   if (in.n < 0) throw Failure{dimension_mismatch, "no graph staged (call parac_gpu_upload)"};
 }
@@ -632,7 +885,8 @@ void need_factor(const SolveInputs& in) {
 
 void solve_release(SolveState& s) {
   dfree(s.wdeg); dfree(s.inv); dfree(s.gt_ptr); dfree(s.gt_col); dfree(s.gt_val);
-  dfree(s.level); dfree(s.order); dfree(s.lvl_off); dfree(s.flags); dfree(s.x); dfree(s.r); dfree(s.p);
+  dfree(s.level); dfree(s.order); dfree(s.done); dfree(s.trace);
+  dfree(s.ff_col); dfree(s.ff_val); dfree(s.ff_lvl); dfree(s.fb_row); dfree(s.fb_val); dfree(s.fb_lvl); dfree(s.lvl_off); dfree(s.flags); dfree(s.x); dfree(s.r); dfree(s.p);
   dfree(s.lp); dfree(s.z); dfree(s.best); dfree(s.yf); dfree(s.yd); dfree(s.zb); dfree(s.rhs);
   dfree(s.partials); dfree(s.scalars); dfree(s.counters); dfree(s.tiles); dfree(s.tmp_int);
   s = SolveState{};
@@ -690,9 +944,18 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     prepare_factor(in);
     Solver sv(in);
     upload(in.state->r, r, in.f_n, in.stream);
-    sv.precond(in.state->r, in.state->z, kSlotC);
+    sv.precond(in.state->r, in.state->z, kSlotC, in.state->mode != kModeFast);
     check(cudaGetLastError(), "precond");
     download(z, in.state->z, in.f_n, in.stream);
+    if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
+  });
+}
+
+int parac_gpu_set_preconditioner_mode(parac_gpu_ctx* ctx, int32_t mode) {
+  return guarded([&] {
+    ctx_activate(ctx);
+    if (mode < 0 || mode > 2) throw Failure{internal_error, "mode must be 0 (default), 1 (exact) or 2 (fast)"};
+    solve_inputs(ctx).state->mode = mode;
   });
 }
 
@@ -742,7 +1005,7 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     if (b_norm == 0.0) {
       rep.converged = 1;
     } else {
-      sv.precond(s.r, s.z, kSlotC);
+      sv.precond(s.r, s.z, kSlotC, s.mode == kModeExact);
       update_p_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotC), s.scalars, kRz0, kRz0, 1, s.z, s.p);
       copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.x, s.best);
       note_launches(2);
@@ -766,7 +1029,7 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
           copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.x, s.best);
           note_launches(1);
         }
-        sv.precond(s.r, s.z, kSlotC);
+        sv.precond(s.r, s.z, kSlotC, s.mode == kModeExact);
         const int next = slot == kRz0 ? kRz1 : kRz0;
         update_p_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotC), s.scalars, slot, next, 0, s.z, s.p);
         note_launches(1);

@@ -21,7 +21,13 @@ struct SolveState {
   int* level = nullptr;       // forward ASAP level per position
   int* order = nullptr;       // positions sorted by level
   long long* lvl_off = nullptr;  // level offsets into order
-  int* flags = nullptr;       // sweep completion stamps per position
+  int* flags = nullptr;       // completion stamps per position (level pass)
+  int* done = nullptr;
+  // fast-mode sweep copies (entries sorted by dependency level) + level of each entry
+  int *ff_col = nullptr, *ff_lvl = nullptr, *fb_row = nullptr, *fb_lvl = nullptr;
+  double *ff_val = nullptr, *fb_val = nullptr;
+  int mode = 0;  // 0 default (pcg fast, apply exact), 1 exact, 2 fast
+  unsigned long long* trace = nullptr;  // PARAC_SWEEP_TRACE diagnostics        // per-level finished-row counters, forward + backward
   int depth = 0;
   int epoch = 0;
   // vectors
@@ -36,6 +42,8 @@ struct SolveState {
   int blocks = 0;
 };
 
+enum : int { kModeDefault = 0, kModeExact = 1, kModeFast = 2 };
+
 struct SolveInputs {
   int n;
   const long long* ptr;
@@ -48,6 +56,7 @@ struct SolveInputs {
   const double* vals;
   const double* diag;
   const int* perm;
+  const int* level;  // ASAP levels from K3 (nullptr: compute them)
   cudaStream_t stream;
   int device;
   SolveState* state;

@@ -346,6 +346,12 @@ class GpuContext:
         _check(lib.parac_gpu_download_times(self.handle, _ptr(out)))
         return out[:8 * n].reshape(n, 8)
 
+    PRECOND_MODES = {"default": 0, "exact": 1, "fast": 2}
+
+    def set_preconditioner_mode(self, mode: str) -> None:
+        """'default' (apply exact, pcg fast), 'exact' or 'fast'; see parac_gpu.h."""
+        _check(lib.parac_gpu_set_preconditioner_mode(self.handle, self.PRECOND_MODES[mode]))
+
     def upload_factor(self, f: LdlFactor) -> None:
         _check(lib.parac_gpu_upload_factor(self.handle, f.n, _ptr(f.col_ptr), _ptr(f.rows),
                                            _ptr(f.values), _ptr(f.diag), _ptr(f.perm)))

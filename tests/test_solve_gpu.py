@@ -98,3 +98,34 @@ def test_pcg_errors_and_limits(gpu_ctx):
     assert rep.iterations == 3 and not rep.converged
     x, rep = P.pcg_solve_gpu(g, f, np.zeros(512), ctx=gpu_ctx)
     assert rep.converged and rep.iterations == 0 and not x.any()
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_pcg_modes_iterations(gpu_ctx, gold, mode):
+    # both sweep modes: same operator M^-1; iterations within 10% of the reference
+    e = next(x for x in gold["pcg"] if x["name"] == "poisson32_random_1e-8")
+    g = P.gen_poisson3d(32)
+    f = P.factor_gpu(g, P.ordering_random(32 ** 3, 0), e["seed"], ctx=gpu_ctx)
+    b = P.make_rhs(g, "random_projected", e["rhs_seed"])
+    gpu_ctx.set_preconditioner_mode(mode)
+    try:
+        x, rep = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+        x2, rep2 = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+    finally:
+        gpu_ctx.set_preconditioner_mode("default")
+    assert rep.converged and rep.relative_residual <= 1e-8
+    assert abs(rep.iterations - e["iterations"]) <= max(1, 0.1 * e["iterations"])
+    assert x.tobytes() == x2.tobytes()  # deterministic run to run
+
+
+def test_fast_preconditioner_close_to_exact(gpu_ctx, port):
+    g, perm, seed = case("poisson16_random0")
+    f = port.factor(g, perm, seed)
+    r = P.make_rhs(g, "random_projected", 3)
+    want = port.apply_preconditioner(f, r)
+    gpu_ctx.set_preconditioner_mode("fast")
+    try:
+        z = P.apply_preconditioner_gpu(factor_from_port(f), r, ctx=gpu_ctx)
+    finally:
+        gpu_ctx.set_preconditioner_mode("default")
+    assert np.allclose(z, want, rtol=1e-10, atol=1e-12 * np.abs(want).max())

@@ -93,14 +93,17 @@ __device__ int claim(const FactorDev& d, bool big) {
   int last = ld_relaxed(&d.ctrl->eliminated);
   int iter = 0;
   (void)tail_p;
+  unsigned ns = 32;
   while (true) {
     // Distance probe on a slot-specific address (no shared word polled by
     // every waiter): if the slot 16 places earlier is still empty, we are far
-    // from the publishing front and sleep long.
-    unsigned ns;
-    if (idx < 16 || ld_relaxed(&queue[idx - 16]) >= 0) ns = 32;
-    else if (idx < 256 || ld_relaxed(&queue[idx - 256]) >= 0) ns = 512;
-    else ns = 4096;
+    // from the publishing front and sleep long. Probes are dependent round
+    // trips, so they run on every 8th poll only.
+    if ((iter & 7) == 0 || ns >= 512) {  // long sleepers re-probe every time
+      if (idx < 16 || ld_relaxed(&queue[idx - 16]) >= 0) ns = 32;
+      else if (idx < 256 || ld_relaxed(&queue[idx - 256]) >= 0) ns = 512;
+      else ns = 4096;
+    }
     __nanosleep(ns);
     v = ld_relaxed(&queue[idx]);
     if (v >= 0) return v;

@@ -39,6 +39,7 @@ constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed => deterministic reductio
 constexpr int kRedThreads = 256;
 constexpr int kSweepThreads = 256;
 constexpr int kRowBlock = 256;  // row entries staged per warp before the serial chain
+constexpr int kFastBlock = 128;  // fast-mode batch (4 entries per lane in flight)
 
 enum Slot { kSlotA = 0, kSlotB = 1, kSlotC = 2, kSlots = 3 };
 enum Scalar { kRz0 = 0, kRz1 = 1, kPlpOk = 2, kScalars = 8 };
@@ -396,15 +397,33 @@ __device__ __forceinline__ bool level_done(const int* done, const long long* lvl
 
 __device__ __forceinline__ void wait_level(const int* done, const long long* lvl_off, int L, int step,
                                            int depth) {
-  if (level_done(done, lvl_off, L, 1, depth)) return;
-  while (true) {
-    unsigned ns;
-    if (level_done(done, lvl_off, L + step, 1, depth)) ns = 32;
-    else if (level_done(done, lvl_off, L + 3 * step, 1, depth)) ns = 256;
-    else if (level_done(done, lvl_off, L + 15 * step, 1, depth)) ns = 1024;
-    else ns = 4096;
+  const int target = level_size(lvl_off, L);
+  if (ld_relaxed(&done[L]) >= target) return;
+  // Near the front every waiter of the next level polls done[L]; a wide next
+  // level means many pollers of one word, so the near interval grows with it.
+  const int nxt = L - step;
+  const int pollers = (nxt >= 1 && nxt <= depth) ? level_size(lvl_off, nxt) : 1;
+  const unsigned near_ns = 32u + static_cast<unsigned>(min(pollers, 4096)) / 4u;
+  // The distance probes cost dependent round trips: re-classify only every 8th
+  // poll, so a waiter near the front re-checks done[L] every ~near_ns + 1 RT.
+  unsigned ns = near_ns;
+  const unsigned long long t0 = globaltimer_ns();
+  for (int it = 0;; ++it) {
+    if ((it & 7) == 0 || ns >= 1024) {  // long sleepers re-probe every time
+      // done[0] (level 0 does not exist) is the sweep's abort word: a wait
+      // that exceeds 20 s raises it, and every waiter then bails out.
+      if (ld_relaxed(&done[0]) != 0) return;
+      if (globaltimer_ns() - t0 > 20000000000ull) {
+        atomicExch(const_cast<int*>(&done[0]), 1);
+        return;
+      }
+      if (level_done(done, lvl_off, L + step, 1, depth)) ns = near_ns;
+      else if (level_done(done, lvl_off, L + 3 * step, 1, depth)) ns = 256 + near_ns;
+      else if (level_done(done, lvl_off, L + 15 * step, 1, depth)) ns = 1024;
+      else ns = 4096;
+    }
     __nanosleep(ns);
-    if (level_done(done, lvl_off, L, 1, depth)) return;
+    if (ld_relaxed(&done[L]) >= target) return;
   }
 }
 
@@ -426,6 +445,13 @@ __device__ __forceinline__ double serial_sub(double acc, const double* buf, int 
   }
   for (; j < cnt; ++j) acc = __dsub_rn(acc, buf[j]);
   return acc;
+}
+
+// Row j of the level order belongs to warp j mod W: a level's rows are spread
+// round-robin and consecutive narrow levels land on consecutive warps, so the
+// warp owning a tail row arrives there early and stages it while waiting.
+__device__ __forceinline__ long long first_row(long long lb, int w, int W) {
+  return lb + ((w - lb % W) % W + W) % W;
 }
 
 // Products G(.,.) * x[idx] of one block of a row into the warp's shared slots.
@@ -462,13 +488,16 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
   __shared__ double buf[kSweepThreads / 32][kRowBlock];
   const int lane = lane_id();
   double* wbuf = buf[threadIdx.x >> 5];
-  while (true) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= n) return;
-    const int r = order[i];
-    const int L = level[r];
+  // Static round-robin of each level's rows over the persistent warps, levels
+  // in sweep order: no claim atomics (a single claim counter capped the wide
+  // early levels at the L2 same-address atomic rate).
+  const int W = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  (void)counter;
+  (void)level;
+  for (int L = 1; L <= depth; ++L) {
+   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
+    const int r = order[j];
     if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
     if (L > 1 && lane == 0) wait_level(done, lvl_off, L - 1, -1, depth);
     __syncwarp();
@@ -491,6 +520,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
       finish_row(done, L);
     }
   }
+  }
 }
 
 // Backward: z[k] = yd[k] - sum_{r in col k, ascending} G(r,k) z[r] (solver.cpp:60-66).
@@ -501,13 +531,13 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
   __shared__ double buf[kSweepThreads / 32][kRowBlock];
   const int lane = lane_id();
   double* wbuf = buf[threadIdx.x >> 5];
-  while (true) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= n) return;
-    const int k = order[n - 1 - i];
-    const int L = level[k];
+  const int W = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  (void)counter;
+  (void)level;
+  for (int L = depth; L >= 1; --L) {
+   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
+    const int k = order[j];
     if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
     if (L < depth && lane == 0) wait_level(done, lvl_off, L + 1, +1, depth);
     __syncwarp();
@@ -527,6 +557,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
       if (trace) trace[3 * k + 1] = globaltimer_ns();
       finish_row(done, L);
     }
+  }
   }
 }
 
@@ -576,36 +607,59 @@ __global__ void level_sort_kernel(int nseg, const long long* seg, const int* idx
   }
 }
 
+// One batch of up to 32*Q entries of a fast-mode row: index/coefficient loads
+// first (independent of the wait), then -- once the batch's latest dependency
+// level is complete -- all value loads in flight together, then the lane's
+// partial sum in fixed order (deterministic).
+template <int Q>
+__device__ __forceinline__ double fast_batch(const int* idx, const double* g, const double* x, int cnt,
+                                             int lane, double part) {
+  int ci[Q];
+  double gv[Q], xv[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const bool ok = q * 32 + lane < cnt;
+    ci[q] = ok ? idx[q * 32 + lane] : 0;
+    gv[q] = ok ? g[q * 32 + lane] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) xv[q] = q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) part += gv[q] * xv[q];
+  return part;
+}
+
 // Forward, fast: y[r] = rhs[r] - sum G(r,k) y[k]; entries sorted by level[k] ascending.
-__global__ void __launch_bounds__(kSweepThreads) sweep_forward_fast_kernel(
+__global__ void __launch_bounds__(kSweepThreads, 6) sweep_forward_fast_kernel(
     int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
     const int* fcol, const double* fval, const int* flvl, const double* diag, const int* inv,
-    const double* rvec, double* yf, double* yd, int* done, int* counter) {
+    const double* rvec, double* yf, double* yd, int* done, int* counter, unsigned long long* trace) {
   const int lane = lane_id();
-  while (true) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= n) return;
-    const int r = order[i];
-    const int L = level[r];
+  // Static round-robin of each level's rows over the persistent warps, levels
+  // in sweep order: no claim atomics (a single claim counter capped the wide
+  // early levels at the L2 same-address atomic rate).
+  const int W = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  (void)counter;
+  (void)level;
+  for (int L = 1; L <= depth; ++L) {
+   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
+    const int r = order[j];
+    if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
     const long long b = gt_ptr[r], e = gt_ptr[r + 1];
     double part = 0.0;
-    int waited = 0;  // highest level known complete
-    for (long long base = b; base < e; base += 32) {
-      const long long t = base + lane;
-      const long long last = min(base + 31, e - 1);
-      const int need = flvl[last];  // the block's latest dependency level
-      if (need > waited) {
-        if (lane == 0) wait_level(done, lvl_off, need, -1, depth);
-        __syncwarp();
-        fence_acq_rel();
-        waited = need;
-      }
-      if (t < e) part += fval[t] * __ldcg(yf + fcol[t]);
+    for (long long base = b; base < e; base += kFastBlock) {
+      const int cnt = static_cast<int>(min(static_cast<long long>(kFastBlock), e - base));
+      const int need = flvl[base + cnt - 1];  // latest dependency level in the batch
+      if (lane == 0) wait_level(done, lvl_off, need, -1, depth);
+      __syncwarp();
+      fence_acq_rel();
+      part = fast_batch<kFastBlock / 32>(fcol + base, fval + base, yf, cnt, lane, part);
     }
+    if (trace && lane == 0) trace[3 * r] = globaltimer_ns();
     const double sum = warp_sum(part);
     if (lane == 0) {
+      if (trace) trace[3 * r + 1] = globaltimer_ns();
       const double acc = rvec[inv[r]] - sum;
       yf[r] = acc;
       const double d = diag[r];
@@ -613,56 +667,70 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_fast_kernel(
       finish_row(done, L);
     }
   }
+  }
 }
 
 // Backward, fast: z[k] = yd[k] - sum G(r,k) z[r]; entries sorted by level[r] descending.
-__global__ void __launch_bounds__(kSweepThreads) sweep_backward_fast_kernel(
+__global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
     int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* col_ptr,
     const int* brow, const double* bval, const int* blvl, const double* yd, double* zb, int* done,
-    int* counter) {
+    int* counter, unsigned long long* trace) {
   const int lane = lane_id();
-  while (true) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= n) return;
-    const int k = order[n - 1 - i];
-    const int L = level[k];
+  const int W = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  (void)counter;
+  (void)level;
+  for (int L = depth; L >= 1; --L) {
+   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
+    const int k = order[j];
+    if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
     const long long b = col_ptr[k], e = col_ptr[k + 1];
     double part = 0.0;
-    int waited = depth + 1;  // lowest level known complete
-    for (long long base = b; base < e; base += 32) {
-      const long long t = base + lane;
-      const long long last = min(base + 31, e - 1);
-      const int need = blvl[last];
-      if (need < waited) {
-        if (lane == 0) wait_level(done, lvl_off, need, +1, depth);
-        __syncwarp();
-        fence_acq_rel();
-        waited = need;
-      }
-      if (t < e) part += bval[t] * __ldcg(zb + brow[t]);
+    for (long long base = b; base < e; base += kFastBlock) {
+      const int cnt = static_cast<int>(min(static_cast<long long>(kFastBlock), e - base));
+      const int need = blvl[base + cnt - 1];
+      if (lane == 0) wait_level(done, lvl_off, need, +1, depth);
+      __syncwarp();
+      fence_acq_rel();
+      part = fast_batch<kFastBlock / 32>(brow + base, bval + base, zb, cnt, lane, part);
     }
+    if (trace && lane == 0) trace[3 * k] = globaltimer_ns();
     const double sum = warp_sum(part);
     if (lane == 0) {
+      if (trace) trace[3 * k + 1] = globaltimer_ns();
       zb[k] = yd[k] - sum;
       finish_row(done, L);
     }
   }
+  }
 }
 
-int sweep_grid(int device) {
-  static int cached[64] = {0};
-  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+// Persistent sweep grids: exactly the co-resident capacity of each kernel.
+// The static row assignment needs every CTA resident (a non-resident CTA's
+// rows would never run while resident ones wait on their level), so each
+// kernel is sized from its own occupancy (register/smem use differ).
+template <typename K>
+int occupancy_grid(K kernel, int device) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_forward_kernel, kSweepThreads, 0);
-  int per_sm_b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, sweep_backward_kernel, kSweepThreads, 0);
-  per_sm = std::max(1, std::min(per_sm, per_sm_b));
-  const int g = per_sm * sm_count(device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSweepThreads, 0);
+  return std::max(1, per_sm) * sm_count(device);
+}
+
+struct SweepGrids {
+  int fwd, bwd, fwd_fast, bwd_fast, level;
+};
+
+SweepGrids sweep_grids(int device) {
+  static SweepGrids cached[64] = {};
+  if (device >= 0 && device < 64 && cached[device].fwd) return cached[device];
+  SweepGrids g{occupancy_grid(sweep_forward_kernel, device), occupancy_grid(sweep_backward_kernel, device),
+               occupancy_grid(sweep_forward_fast_kernel, device),
+               occupancy_grid(sweep_backward_fast_kernel, device), occupancy_grid(level_kernel, device)};
   if (device >= 0 && device < 64) cached[device] = g;
   return g;
 }
+
+int sweep_grid(int device) { return sweep_grids(device).level; }
 
 // ---------------------------------------------------------------- host side
 void ensure_vectors(SolveState& s, int n) {
@@ -794,11 +862,11 @@ struct Solver {
   SolveState& s;
   cudaStream_t st;
   int n;
-  int sweep_blocks;
+  SweepGrids grids;
   std::vector<double> hp = std::vector<double>(kRedBlocks);
 
   explicit Solver(const SolveInputs& i)
-      : in(i), s(*i.state), st(i.stream), n(i.n), sweep_blocks(sweep_grid(i.device)) {}
+      : in(i), s(*i.state), st(i.stream), n(i.n), grids(sweep_grids(i.device)) {}
 
   double* part(int slot) const { return s.partials + slot * kRedBlocks; }
 
@@ -817,24 +885,34 @@ struct Solver {
     check(cudaMemsetAsync(s.done, 0, sizeof(int) * 2 * (D + 2), st), "memset");
     check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
     if (!exact) {
-      sweep_forward_fast_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+      sweep_forward_fast_kernel<<<grids.fwd_fast, kSweepThreads, 0, st>>>(
           in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, in.diag,
-          s.inv, r, s.yf, s.yd, done_f, s.counters + 2);
-      sweep_backward_fast_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+          s.inv, r, s.yf, s.yd, done_f, s.counters + 2, s.trace);
+      sweep_backward_fast_kernel<<<grids.bwd_fast, kSweepThreads, 0, st>>>(
           in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, s.yd, s.zb,
-          done_b, s.counters + 3);
+          done_b, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
       gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
       note_launches(3);
       return;
     }
-    sweep_forward_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+    sweep_forward_kernel<<<grids.fwd, kSweepThreads, 0, st>>>(
         in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.gt_col, s.gt_val, in.diag, s.inv, r,
         s.yf, s.yd, done_f, s.counters + 4, s.counters + 2, s.trace);
-    sweep_backward_kernel<<<sweep_blocks, kSweepThreads, 0, st>>>(
+    sweep_backward_kernel<<<grids.bwd, kSweepThreads, 0, st>>>(
         in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, in.rows, in.vals, s.yd, s.zb, done_b,
         s.counters + 5, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
     gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
     note_launches(3);
+  }
+
+  // The sweeps' abort words (done[0] of each direction, see wait_level).
+  void check_abort() {
+    int flags[2] = {0, 0};
+    check(cudaMemcpyAsync(&flags[0], s.done, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaMemcpyAsync(&flags[1], s.done + (s.depth + 2), sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "sync");
+    if (flags[0] || flags[1])
+      throw Failure{queue_stall, "triangular sweep made no progress for 20 s (watchdog)"};
   }
 
   void spmv(const double* x, double* y, int slot) {
@@ -947,6 +1025,7 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     sv.precond(in.state->r, in.state->z, kSlotC, in.state->mode != kModeFast);
     check(cudaGetLastError(), "precond");
     download(z, in.state->z, in.f_n, in.stream);
+    sv.check_abort();
     if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
   });
 }
@@ -1052,6 +1131,7 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     }
     check(cudaEventRecord(e1, st), "event");
     check(cudaGetLastError(), "pcg");
+    if (b_norm != 0.0) sv.check_abort();
     download(x, s.x, n, st);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);

@@ -13,6 +13,7 @@ def run(path, n3):
     g = P.gen_poisson3d(n3)
     o = P.ordering_random(g.n, 0)
     ctx = P.GpuContext(0)
+    ctx.set_preconditioner_mode(os.environ.get("SWEEP_MODE", "default"))
     f = P.factor_gpu(g, o, 0, ctx=ctx)
     r = P.make_rhs(g, "random_projected", 0)
     for _ in range(3):
@@ -68,3 +69,33 @@ if __name__ == "__main__":
     if len(sys.argv) <= 2:
         run(path, 128)
     analyse(path)
+
+
+def bands(path):
+    """Per level band: level duration, and per-row (ready-notice) = start - finish(prev level)."""
+    raw = open(path, "rb").read()
+    n = int(np.frombuffer(raw[:4], np.int32)[0])
+    tr = np.frombuffer(raw[4:4 + 48 * n], np.uint64).astype(np.int64).reshape(2, n, 3)
+    lv = np.frombuffer(raw[4 + 48 * n:], np.int32)[:n]
+    depth = lv.max()
+    t = tr[0]
+    t0 = t[:, 2].min()
+    start, end, claim = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
+    fin = np.zeros(depth + 2)
+    np.maximum.at(fin, lv, end)
+    for lo, hi in ((2, 6), (6, 20), (20, 50), (50, 100), (100, 200), (200, 500), (500, 1000), (1000, depth + 1)):
+        sel = (lv >= lo) & (lv < hi)
+        notice = start[sel] - fin[lv[sel] - 1]
+        durl = np.diff(fin[lo - 1:hi])
+        # rows finishing last in their level: how late did they start?
+        lastrow = np.zeros(depth + 2, np.int64)
+        order = np.lexsort((end, lv))
+        lastrow[lv[order]] = order
+        lr = lastrow[lo:hi]
+        print(f"levels [{lo},{hi}): rows {sel.sum():7d} level dur median {np.median(durl):7.2f} us | "
+              f"notice median {np.median(notice):7.2f} p90 {np.percentile(notice, 90):7.2f} | "
+              f"last row: notice {np.median(start[lr] - fin[lv[lr] - 1]):6.2f} claim-after-prev {np.median(claim[lr] - fin[lv[lr] - 1]):7.2f}")
+
+
+if __name__ == "__main__" and os.environ.get("BANDS"):
+    bands(sys.argv[1] if len(sys.argv) > 1 else "/tmp/sweep.bin")

@@ -417,10 +417,15 @@ __device__ __forceinline__ void wait_level(const int* done, const long long* lvl
         atomicExch(const_cast<int*>(&done[0]), 1);
         return;
       }
+      // sleep ~ distance to the front (levels take ~3-30 us each): a waiter
+      // far ahead must not poll -- thousands of early waiters polling slowed
+      // the L2 for the rows on the critical path by 2-3x (measured).
       if (level_done(done, lvl_off, L + step, 1, depth)) ns = near_ns;
-      else if (level_done(done, lvl_off, L + 3 * step, 1, depth)) ns = 256 + near_ns;
-      else if (level_done(done, lvl_off, L + 15 * step, 1, depth)) ns = 1024;
-      else ns = 4096;
+      else if (level_done(done, lvl_off, L + 2 * step, 1, depth)) ns = 1024;
+      else if (level_done(done, lvl_off, L + 4 * step, 1, depth)) ns = 3072;
+      else if (level_done(done, lvl_off, L + 8 * step, 1, depth)) ns = 8192;
+      else if (level_done(done, lvl_off, L + 16 * step, 1, depth)) ns = 16384;
+      else ns = 32768;
     }
     __nanosleep(ns);
     if (ld_relaxed(&done[L]) >= target) return;
@@ -476,6 +481,84 @@ __device__ __forceinline__ void stage_products(const int* idx, const double* g, 
     if (q * 32 + lane < cnt) wbuf[q * 32 + lane] = (skip_zero && xv[q] == 0.0) ? 0.0 : __dmul_rn(gv[q], xv[q]);
 }
 
+// Wide levels (>= kLaneRowsPerWarp rows per warp): one row per LANE, summed
+// sequentially in the reference's order (so these rows are bit-exact in both
+// modes) -- 32 independent rows per warp instead of one keeps the first,
+// widest levels (10^5 rows each at 128^3) from being latency-bound per row.
+constexpr int kLaneRowsPerWarp = 2;
+
+__device__ __forceinline__ bool lane_mode(const long long* lvl_off, int L, int W) {
+  return level_size(lvl_off, L) >= kLaneRowsPerWarp * W;
+}
+
+// Forward rows of level L, one per lane (gather form, k ascending, zero skip).
+__device__ __forceinline__ void lane_level_forward(int L, int depth, int w, int W, int lane,
+                                                   const int* order, const long long* lvl_off,
+                                                   const long long* gt_ptr, const int* gt_col,
+                                                   const double* gt_val, const double* diag,
+                                                   const int* inv, const double* rvec, double* yf,
+                                                   double* yd, int* done) {
+  const long long lb = lvl_off[L], le = lvl_off[L + 1];
+  const long long ntask = (le - lb + 31) / 32;
+  bool waited = L == 1;
+  for (long long t = w; t < ntask; t += W) {
+    if (!waited) {
+      if (lane == 0) wait_level(done, lvl_off, L - 1, -1, depth);
+      __syncwarp();
+      fence_acq_rel();
+      waited = true;
+    }
+    const long long j = lb + t * 32 + lane;
+    if (j < le) {
+      const int r = order[j];
+      double acc = rvec[inv[r]];
+      const long long b = gt_ptr[r], e = gt_ptr[r + 1];
+      for (long long q = b; q < e; ++q) {
+        const double yk = __ldcg(yf + gt_col[q]);
+        if (yk != 0.0) acc = __dsub_rn(acc, __dmul_rn(gt_val[q], yk));
+      }
+      yf[r] = acc;
+      const double dd = diag[r];
+      yd[r] = dd > 0.0 ? __ddiv_rn(acc, dd) : 0.0;
+    }
+    const unsigned ok = __ballot_sync(kFull, j < le);
+    fence_acq_rel();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&done[L], __popc(ok));
+  }
+}
+
+// Backward rows (columns of G) of level L, one per lane, rows ascending.
+__device__ __forceinline__ void lane_level_backward(int L, int depth, int w, int W, int lane,
+                                                    const int* order, const long long* lvl_off,
+                                                    const long long* col_ptr, const int* rows,
+                                                    const double* vals, const double* yd, double* zb,
+                                                    int* done) {
+  const long long lb = lvl_off[L], le = lvl_off[L + 1];
+  const long long ntask = (le - lb + 31) / 32;
+  bool waited = L == depth;
+  for (long long t = w; t < ntask; t += W) {
+    if (!waited) {
+      if (lane == 0) wait_level(done, lvl_off, L + 1, +1, depth);
+      __syncwarp();
+      fence_acq_rel();
+      waited = true;
+    }
+    const long long j = lb + t * 32 + lane;
+    if (j < le) {
+      const int k = order[j];
+      double acc = yd[k];
+      const long long b = col_ptr[k], e = col_ptr[k + 1];
+      for (long long q = b; q < e; ++q) acc = __dsub_rn(acc, __dmul_rn(vals[q], __ldcg(zb + rows[q])));
+      zb[k] = acc;
+    }
+    const unsigned ok = __ballot_sync(kFull, j < le);
+    fence_acq_rel();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&done[L], __popc(ok));
+  }
+}
+
 // Forward: y[r] = rhs[r] - sum_{k<r} G(r,k) y[k], k ascending, skipping
 // y[k] == 0 exactly like the column scatter (solver.cpp:45-52; a skipped term
 // is replaced by +0.0, which leaves acc bit-identical); then D^+ (:54-58) into
@@ -496,6 +579,11 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
   (void)counter;
   (void)level;
   for (int L = 1; L <= depth; ++L) {
+   if (lane_mode(lvl_off, L, W)) {
+     lane_level_forward(L, depth, w, W, lane, order, lvl_off, gt_ptr, gt_col, gt_val, diag, inv, rvec,
+                        yf, yd, done);
+     continue;
+   }
    for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
     const int r = order[j];
     if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
@@ -536,6 +624,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
   (void)counter;
   (void)level;
   for (int L = depth; L >= 1; --L) {
+   if (lane_mode(lvl_off, L, W)) {
+     lane_level_backward(L, depth, w, W, lane, order, lvl_off, col_ptr, rows, vals, yd, zb, done);
+     continue;
+   }
    for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
     const int k = order[j];
     if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
@@ -632,8 +724,9 @@ __device__ __forceinline__ double fast_batch(const int* idx, const double* g, co
 // Forward, fast: y[r] = rhs[r] - sum G(r,k) y[k]; entries sorted by level[k] ascending.
 __global__ void __launch_bounds__(kSweepThreads, 6) sweep_forward_fast_kernel(
     int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
-    const int* fcol, const double* fval, const int* flvl, const double* diag, const int* inv,
-    const double* rvec, double* yf, double* yd, int* done, int* counter, unsigned long long* trace) {
+    const int* fcol, const double* fval, const int* flvl, const int* gt_col, const double* gt_val,
+    const double* diag, const int* inv, const double* rvec, double* yf, double* yd, int* done, int* counter,
+    unsigned long long* trace) {
   const int lane = lane_id();
   // Static round-robin of each level's rows over the persistent warps, levels
   // in sweep order: no claim atomics (a single claim counter capped the wide
@@ -643,6 +736,11 @@ __global__ void __launch_bounds__(kSweepThreads, 6) sweep_forward_fast_kernel(
   (void)counter;
   (void)level;
   for (int L = 1; L <= depth; ++L) {
+   if (lane_mode(lvl_off, L, W)) {
+     lane_level_forward(L, depth, w, W, lane, order, lvl_off, gt_ptr, gt_col, gt_val, diag, inv, rvec,
+                        yf, yd, done);
+     continue;
+   }
    for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
     const int r = order[j];
     if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
@@ -673,14 +771,18 @@ __global__ void __launch_bounds__(kSweepThreads, 6) sweep_forward_fast_kernel(
 // Backward, fast: z[k] = yd[k] - sum G(r,k) z[r]; entries sorted by level[r] descending.
 __global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
     int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* col_ptr,
-    const int* brow, const double* bval, const int* blvl, const double* yd, double* zb, int* done,
-    int* counter, unsigned long long* trace) {
+    const int* brow, const double* bval, const int* blvl, const int* rows, const double* vals,
+    const double* yd, double* zb, int* done, int* counter, unsigned long long* trace) {
   const int lane = lane_id();
   const int W = (gridDim.x * blockDim.x) >> 5;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   (void)counter;
   (void)level;
   for (int L = depth; L >= 1; --L) {
+   if (lane_mode(lvl_off, L, W)) {
+     lane_level_backward(L, depth, w, W, lane, order, lvl_off, col_ptr, rows, vals, yd, zb, done);
+     continue;
+   }
    for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
     const int k = order[j];
     if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
@@ -886,11 +988,11 @@ struct Solver {
     check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
     if (!exact) {
       sweep_forward_fast_kernel<<<grids.fwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, in.diag,
-          s.inv, r, s.yf, s.yd, done_f, s.counters + 2, s.trace);
+          in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, s.gt_col,
+          s.gt_val, in.diag, s.inv, r, s.yf, s.yd, done_f, s.counters + 2, s.trace);
       sweep_backward_fast_kernel<<<grids.bwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, s.yd, s.zb,
-          done_b, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
+          in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, in.rows,
+          in.vals, s.yd, s.zb, done_b, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
       gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
       note_launches(3);
       return;

@@ -1,0 +1,210 @@
+// parac_gpu_shim.hpp -- the C++ face of the B200 backend, in the reference's
+// own namespace and types (/root/reference/proj/include/parac/*.hpp), so a
+// maintainer adds `--backend gpu` to run_factor (proj/tools/parac_cli.cpp:106-128)
+// with one include and one call. Header-only; it needs the reference headers
+// on the include path and links against libparac_gpu.so (C ABI, parac_gpu.h).
+//
+//   LdlFactor parac::factor_gpu(graph, ordering, seed, GpuOptions, FactorStats*)
+//       same shape as factor_parallel_left (include/parac/factor_par.hpp:53-62);
+//       result is LdlFactor::same_values-identical to factor_randomized.
+//   std::pair<std::vector<double>, SolveReport>
+//   parac::pcg_solve_gpu(graph, factor, b, SolveConfig)
+//       same shape as pcg_solve (include/parac/solver.hpp:39-42).
+//   parac::apply_preconditioner_gpu / laplacian_apply_gpu   (solver.hpp:30,33)
+//
+// Errors: the C ABI returns parac::Errc values; they are rethrown here as
+// parac::Error(code, detail) exactly like the CPU backends throw
+// (ArenaExhausted, QueueStall, NotConnected, DimensionMismatch, ...).
+// No exception crosses the C boundary; no CPU fallback exists behind it.
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "parac/error.hpp"
+#include "parac/factor.hpp"
+#include "parac/factor_seq.hpp"
+#include "parac/graph.hpp"
+#include "parac/ordering.hpp"
+#include "parac/solver.hpp"
+#include "parac_gpu.h"
+
+namespace parac {
+
+// ParOptions analogue (include/parac/factor_par.hpp:31-45). workers has no
+// meaning on the device; arena_budget maps to the column arena, the fill
+// pool budget is separate (fills live in their own 16-byte slot pool).
+struct GpuOptions {
+  int device = 0;
+  Index arena_budget = -1;       // column arena entries; <0: default (grown on demand)
+  Index fill_pool_budget = -1;   // overflow fill entries; <0: default (grown on demand)
+  double watchdog_seconds = 60.0;
+  bool record_vertex_times = false;
+  bool verify = false;           // TestHooks::verify analogue (device-side checks)
+  int delay_ns = 0;              // TestHooks::delay analogue (random __nanosleep)
+};
+
+namespace gpu_detail {
+
+[[noreturn]] inline void rethrow(int code) {
+  std::string msg = parac_gpu_last_error();
+  // the C ABI message is "<ErrcName>: detail"; Error prepends the name itself
+  const std::string name = parac_errc_name(code);
+  if (msg.rfind(name + ": ", 0) == 0) msg = msg.substr(name.size() + 2);
+  throw Error(static_cast<Errc>(code), msg);
+}
+inline void check(int rc) {
+  if (rc != 0) rethrow(rc);
+}
+
+struct CtxDeleter {
+  void operator()(parac_gpu_ctx* c) const { parac_gpu_destroy(c); }
+};
+using Ctx = std::unique_ptr<parac_gpu_ctx, CtxDeleter>;
+
+inline Ctx make_ctx(int device) {
+  parac_gpu_ctx* c = nullptr;
+  check(parac_gpu_create(device, &c));
+  return Ctx(c);
+}
+
+// LaplacianGraph keeps ptr_ private; its public spans are views into the
+// contiguous adjacency arrays (graph.hpp:36-44), so the row pointer is rebuilt
+// from degree() and the arrays are passed without copying.
+struct CsrView {
+  std::vector<std::int64_t> ptr;
+  parac_csr csr{};
+  explicit CsrView(const LaplacianGraph& g) {
+    const VertexId n = g.num_vertices();
+    ptr.resize(static_cast<std::size_t>(n) + 1, 0);
+    for (VertexId v = 0; v < n; ++v) ptr[v + 1] = ptr[v] + g.degree(v);
+    csr.n = n;
+    csr.ptr = ptr.data();
+    csr.adj = n > 0 ? g.neighbors(0).data() : nullptr;
+    csr.w = n > 0 ? g.weights(0).data() : nullptr;
+  }
+};
+
+inline void stage_factor(parac_gpu_ctx* ctx, const LdlFactor& f) {
+  check(parac_gpu_upload_factor(ctx, f.n, f.col_ptr.data(), f.rows.data(), f.values.data(),
+                                f.diag.data(), f.perm.data()));
+}
+
+}  // namespace gpu_detail
+
+inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& ordering,
+                            std::uint64_t seed, const GpuOptions& options = {},
+                            FactorStats* stats = nullptr) {
+  using namespace gpu_detail;
+  const VertexId n = graph.num_vertices();
+  if (ordering.size() != n)
+    throw Error(Errc::dimension_mismatch, "ordering size does not match the graph");
+  auto ctx = make_ctx(options.device);
+  CsrView v(graph);
+  parac_gpu_options o;
+  parac_gpu_default_options(&o);
+  o.column_arena_entries = options.arena_budget;
+  o.fill_pool_entries = options.fill_pool_budget;
+  o.watchdog_seconds = options.watchdog_seconds;
+  o.record_stats = 1;
+  o.verify = options.verify ? 1 : 0;
+  o.delay_ns = options.delay_ns;
+  o.record_times = options.record_vertex_times ? 1 : 0;
+  parac_gpu_factor_info info{};
+  check(parac_gpu_factor(ctx.get(), &v.csr, ordering.perm.data(), seed, &o, &info));
+  LdlFactor f;
+  f.n = n;
+  f.col_ptr.resize(static_cast<std::size_t>(n) + 1);
+  f.rows.resize(static_cast<std::size_t>(info.nnz_off_diagonal));
+  f.values.resize(static_cast<std::size_t>(info.nnz_off_diagonal));
+  f.diag.resize(static_cast<std::size_t>(n));
+  f.perm = ordering.perm;
+  std::vector<std::int32_t> md, se, fr;
+  if (stats) {
+    md.resize(n);
+    se.resize(n);
+    fr.resize(n);
+  }
+  check(parac_gpu_download(ctx.get(), f.col_ptr.data(), f.rows.data(), f.values.data(),
+                           f.diag.data(), stats ? md.data() : nullptr,
+                           stats ? se.data() : nullptr, stats ? fr.data() : nullptr));
+  if (stats) {
+    stats->merged_degree = std::move(md);
+    stats->samples_emitted = std::move(se);
+    stats->fills_received = std::move(fr);
+    stats->total_fills = info.total_fills;
+    stats->arena_used = info.arena_used;
+    stats->seconds = info.device_ms * 1e-3;
+    if (options.record_vertex_times) {
+      std::vector<std::uint64_t> t(8 * static_cast<std::size_t>(n));
+      check(parac_gpu_download_times(ctx.get(), t.data()));
+      std::uint64_t t0 = ~0ull;
+      for (VertexId k = 0; k < n; ++k)
+        if (t[8 * k] && t[8 * k] < t0) t0 = t[8 * k];
+      stats->vertex_seconds.assign(n, 0.0);
+      for (VertexId k = 0; k < n; ++k)
+        if (t[8 * k + 7]) stats->vertex_seconds[k] = static_cast<double>(t[8 * k + 7] - t0) * 1e-9;
+    }
+  }
+  return f;
+}
+
+inline std::pair<std::vector<double>, SolveReport> pcg_solve_gpu(const LaplacianGraph& graph,
+                                                                 const LdlFactor& factor,
+                                                                 std::span<const double> b,
+                                                                 const SolveConfig& config = {},
+                                                                 int device = 0) {
+  using namespace gpu_detail;
+  const VertexId n = graph.num_vertices();
+  if (factor.n != n || static_cast<VertexId>(b.size()) != n)
+    throw Error(Errc::dimension_mismatch, "graph, factor and rhs sizes differ");
+  auto ctx = make_ctx(device);
+  CsrView v(graph);
+  check(parac_gpu_upload(ctx.get(), &v.csr, factor.perm.data()));
+  stage_factor(ctx.get(), factor);
+  std::vector<double> x(static_cast<std::size_t>(n));
+  parac_gpu_solve_report r{};
+  check(parac_gpu_pcg(ctx.get(), b.data(), config.tol, config.max_iters, x.data(), &r));
+  SolveReport rep;
+  rep.iterations = r.iterations;
+  rep.relative_residual = r.relative_residual;
+  rep.recurrence_residual = r.recurrence_residual;
+  rep.converged = r.converged != 0;
+  rep.solve_seconds = r.wall_ms * 1e-3;
+  return {std::move(x), rep};
+}
+
+inline std::vector<double> apply_preconditioner_gpu(const LdlFactor& factor,
+                                                    std::span<const double> r, int device = 0) {
+  using namespace gpu_detail;
+  if (static_cast<VertexId>(r.size()) != factor.n)
+    throw Error(Errc::dimension_mismatch, "rhs size differs from the factor");
+  auto ctx = make_ctx(device);
+  stage_factor(ctx.get(), factor);
+  std::vector<double> z(r.size());
+  check(parac_gpu_apply_preconditioner(ctx.get(), r.data(), z.data()));
+  return z;
+}
+
+inline std::vector<double> laplacian_apply_gpu(const LaplacianGraph& graph,
+                                               std::span<const double> x, int device = 0) {
+  using namespace gpu_detail;
+  if (static_cast<VertexId>(x.size()) != graph.num_vertices())
+    throw Error(Errc::dimension_mismatch, "vector size differs from the graph");
+  auto ctx = make_ctx(device);
+  CsrView v(graph);
+  std::vector<std::int32_t> ident(static_cast<std::size_t>(graph.num_vertices()));
+  for (VertexId i = 0; i < graph.num_vertices(); ++i) ident[i] = i;
+  check(parac_gpu_upload(ctx.get(), &v.csr, ident.data()));
+  std::vector<double> y(x.size());
+  check(parac_gpu_laplacian_apply(ctx.get(), x.data(), y.data()));
+  return y;
+}
+
+}  // namespace parac

@@ -37,7 +37,8 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kEntryBytes = 24;  // A (u64), B (f64), C (f64) per column entry
-constexpr int kSmallBytes = kSmallCap * kEntryBytes;
+// small warps: A, B, C + two rank-sort segment buffers (X1, X2)
+constexpr int kSmallBytes = kSmallCap * 8 * 5;
 // big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
 constexpr int kBigBytes = kBigCap * 8 * 5;
 constexpr int kCtaSmem = kWarps * kSmallBytes > kBigBytes ? kWarps * kSmallBytes : kBigBytes;
@@ -62,11 +63,15 @@ struct Scratch {
   unsigned long long* A;
   double* B;
   double* C;
+  unsigned long long* X1;  // rank-sort sorted-segment buffers (shared-memory scratch only)
+  unsigned long long* X2;
 };
 __device__ __forceinline__ Scratch carve(char* base, int cap) {
   return {reinterpret_cast<unsigned long long*>(base),
           reinterpret_cast<double*>(base + 8 * static_cast<long long>(cap)),
-          reinterpret_cast<double*>(base + 16 * static_cast<long long>(cap))};
+          reinterpret_cast<double*>(base + 16 * static_cast<long long>(cap)),
+          reinterpret_cast<unsigned long long*>(base + 24 * static_cast<long long>(cap)),
+          reinterpret_cast<unsigned long long*>(base + 32 * static_cast<long long>(cap))};
 }
 
 // What the keeper already knows about the vertex it keeps.
@@ -311,6 +316,173 @@ __device__ __noinline__ void cta_sort_weight(unsigned long long* A, double* B, i
   }
 }
 
+// ------------------------------------------------------------ rank sort
+// Sort of R <= T*ITEMS unique keys held in registers (element g = i*T + tid),
+// T = 32 (one warp) or kThreads (the CTA). Keys are (k1) or (k1, k2)
+// lexicographic. Two phases, no data-dependent control flow:
+//   1. rank inside the element's 32-element warp segment, by 32 shuffles;
+//      write the segment in sorted order to X1/X2;
+//   2. add, for every other segment, the count of its keys below the
+//      element's (5-step binary search of the sorted segment).
+// O(R (32 + 5 R/32)) compare steps instead of a log^2 network: at R ~ 100-300
+// it is 3-5x faster than the bitonic network and far smaller code.
+template <bool TWO>
+__device__ __forceinline__ bool key_less(unsigned long long a1, unsigned long long a2, unsigned long long b1,
+                                         unsigned long long b2) {
+  return TWO ? (a1 < b1 || (a1 == b1 && a2 < b2)) : a1 < b1;
+}
+
+template <int T, int ITEMS, bool TWO>
+__device__ __forceinline__ void rank_sort(const unsigned long long (&k1)[ITEMS], const unsigned long long (&k2)[ITEMS],
+                                          int R, unsigned long long* X1, unsigned long long* X2,
+                                          int (&rank)[ITEMS]) {
+  const int tid = T == 32 ? lane_id() : static_cast<int>(threadIdx.x);
+  const int lane = tid & 31;
+  const int wid = tid >> 5;
+  int lr[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int seg = i * (T / 32) + wid;
+    const int len = min(32, R - seg * 32);  // may be <= 0 (segment fully padding)
+    int c = 0;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      const unsigned long long o1 = __shfl_sync(kFull, k1[i], t);
+      const unsigned long long o2 = TWO ? __shfl_sync(kFull, k2[i], t) : 0ull;
+      c += (t < len && key_less<TWO>(o1, o2, k1[i], k2[i])) ? 1 : 0;
+    }
+    lr[i] = c;
+    if (lane < len) {
+      X1[seg * 32 + c] = k1[i];
+      if (TWO) X2[seg * 32 + c] = k2[i];
+    }
+  }
+  if (T == 32) __syncwarp(); else __syncthreads();
+  const int nseg = (R + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int seg = i * (T / 32) + wid;
+    int r = lr[i];
+    if (seg * 32 + lane < R) {
+      for (int s2 = 0; s2 < nseg; ++s2) {
+        if (s2 == seg) continue;
+        const int base = s2 * 32;
+        int lo = 0, hi = min(32, R - base);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const unsigned long long m1 = X1[base + mid];
+          const unsigned long long m2 = TWO ? X2[base + mid] : 0ull;
+          if (key_less<TWO>(m1, m2, k1[i], k2[i])) lo = mid + 1; else hi = mid;
+        }
+        r += lo;
+      }
+    }
+    rank[i] = r;
+  }
+}
+
+// ---- warp path (rank sort): gather + raw sort, weight sort (results in A/B)
+template <int ITEMS>
+__device__ __forceinline__ void warp_rank_raw(const FactorDev& d, int k, long long fb, int fdeg, int R,
+                                              Scratch S, int lane) {
+  unsigned long long key[ITEMS], val[ITEMS], none[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * 32 + lane;
+    key[i] = ~0ull;
+    val[i] = 0;
+    none[i] = 0;
+    if (g < R) {
+      double w;
+      load_raw(d, k, fb, fdeg, g, key[i], w);
+      val[i] = dbits(w);
+    }
+  }
+  int rank[ITEMS];
+  rank_sort<32, ITEMS, false>(key, none, R, S.X1, S.X2, rank);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (i * 32 + lane < R) {
+      S.A[rank[i]] = key[i];
+      S.B[rank[i]] = bitsd(val[i]);
+    }
+  }
+  __syncwarp();
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_rank_weight(int m, Scratch S, int lane) {
+  unsigned long long wk[ITEMS], ak[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * 32 + lane;
+    wk[i] = g < m ? dbits(S.B[g]) : kInfBits;
+    ak[i] = g < m ? S.A[g] : ~0ull;
+  }
+  int rank[ITEMS];
+  rank_sort<32, ITEMS, true>(wk, ak, m, S.X1, S.X2, rank);
+  __syncwarp();  // every lane has read A/B
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (i * 32 + lane < m) {
+      S.A[rank[i]] = ak[i];
+      S.B[rank[i]] = bitsd(wk[i]);
+    }
+  }
+  __syncwarp();
+}
+
+// ---- CTA path (rank sort), R <= kThreads * ITEMS
+template <int ITEMS>
+__device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long long fb, int fdeg, int R,
+                                             const unsigned* dirrow, Scratch S) {
+  unsigned long long key[ITEMS], val[ITEMS], none[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * kThreads + threadIdx.x;
+    key[i] = ~0ull;
+    val[i] = 0;
+    none[i] = 0;
+    if (g < R) {
+      double w;
+      load_raw_dir(d, k, fb, fdeg, g, dirrow, key[i], w);
+      val[i] = dbits(w);
+    }
+  }
+  int rank[ITEMS];
+  rank_sort<kThreads, ITEMS, false>(key, none, R, S.X1, S.X2, rank);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (i * kThreads + static_cast<int>(threadIdx.x) < R) {
+      S.A[rank[i]] = key[i];
+      S.B[rank[i]] = bitsd(val[i]);
+    }
+  }
+  __syncthreads();
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
+  unsigned long long wk[ITEMS], ak[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * kThreads + threadIdx.x;
+    wk[i] = g < m ? dbits(S.B[g]) : kInfBits;
+    ak[i] = g < m ? S.A[g] : ~0ull;
+  }
+  int rank[ITEMS];
+  rank_sort<kThreads, ITEMS, true>(wk, ak, m, S.X1, S.X2, rank);
+  __syncthreads();  // every thread has read A/B
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (i * kThreads + static_cast<int>(threadIdx.x) < m) {
+      S.A[rank[i]] = ak[i];
+      S.B[rank[i]] = bitsd(wk[i]);
+    }
+  }
+  __syncthreads();
+}
+
 // ---- warp path: gather + raw sort, weight sort (results in A/B, natural order)
 template <int ITEMS>
 __device__ __forceinline__ void warp_sort_raw(const FactorDev& d, int k, long long fb, int fdeg,
@@ -474,9 +646,9 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
     start = static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R)));
 
   // ---- 2. sort raw by (row, source)  (factor_common.hpp:100-104), in registers
-  if (R <= 32) warp_sort_raw<1>(d, k, fb, fdeg, R, S, lane);
-  else if (R <= 64) warp_sort_raw<2>(d, k, fb, fdeg, R, S, lane);
-  else warp_sort_raw<4>(d, k, fb, fdeg, R, S, lane);
+  if (R <= 32) warp_rank_raw<1>(d, k, fb, fdeg, R, S, lane);
+  else if (R <= 64) warp_rank_raw<2>(d, k, fb, fdeg, R, S, lane);
+  else warp_rank_raw<4>(d, k, fb, fdeg, R, S, lane);
   __syncwarp();
   PHASE(1);
 
@@ -539,9 +711,9 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
 
   // ---- 6-7. weight sort (registers) + suffix
   if (m >= 2) {
-    if (m <= 32) warp_sort_weight<1>(m, S, lane);
-    else if (m <= 64) warp_sort_weight<2>(m, S, lane);
-    else warp_sort_weight<4>(m, S, lane);
+    if (m <= 32) warp_rank_weight<1>(m, S, lane);
+    else if (m <= 64) warp_rank_weight<2>(m, S, lane);
+    else warp_rank_weight<4>(m, S, lane);
     __syncwarp();
     if (lead) serial_suffix(S.B, S.C, m);
     __syncwarp();
@@ -714,9 +886,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     __syncthreads();
     cta_sort_key(S.A, S.B, P);
   } else if (P <= kThreads) {
-    cta_gather_sort_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+    cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S);
   } else if (P <= 2 * kThreads) {
-    cta_gather_sort_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+    cta_rank_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S);
   } else {
     cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
   }
@@ -798,9 +970,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       __syncthreads();
       cta_sort_weight(S.A, S.B, Pm);
     } else if (Pm <= kThreads) {
-      cta_sort_weight_reg<1>(m, S.A, S.B, xb);
+      cta_rank_weight<1>(m, S);
     } else if (Pm <= 2 * kThreads) {
-      cta_sort_weight_reg<2>(m, S.A, S.B, xb);
+      cta_rank_weight<2>(m, S);
     } else {
       cta_sort_weight_reg<4>(m, S.A, S.B, xb);
     }

@@ -791,7 +791,8 @@ __global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
     for (long long base = b; base < e; base += kFastBlock) {
       const int cnt = static_cast<int>(min(static_cast<long long>(kFastBlock), e - base));
       const int need = blvl[base + cnt - 1];
-      if (lane == 0) wait_level(done, lvl_off, need, +1, depth);
+      // levels above depth belong to the tail (already swept before this kernel)
+      if (lane == 0 && need <= depth) wait_level(done, lvl_off, need, +1, depth);
       __syncwarp();
       fence_acq_rel();
       part = fast_batch<kFastBlock / 32>(brow + base, bval + base, zb, cnt, lane, part);
@@ -805,6 +806,588 @@ __global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
     }
   }
   }
+}
+
+// ------------------------------------------------------------ K6 (fast mode): narrow tail
+// The last levels of the factor DAG are narrow and long: at 128^3 the last 774
+// of 1,206 levels hold 4,644 rows. Run grid-wide, each costs a global
+// completion hand-off (several us). The tail T is instead swept by ONE CTA with
+// its solution vector in shared memory and one __syncthreads per level:
+//   forward:  y_T = G_TT^-1 (rhs_T - G_TH y_H)   (prologue: the G_TH part, grid-wide)
+//   backward: z_T = G_TT^-T yd_T                  (self-contained; runs first)
+// T is level-sorted, so tail index i = order position - tail_base and the rows
+// of one level are a contiguous index range.
+// Asynchronous L2 prefetch of [p, p + bytes) (16-byte aligned superset), in
+// 64 KB bulk requests: the sweeps know every future level's G entries, so
+// they pull them from HBM into L2 a few levels ahead of use.
+__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
+  if (bytes <= 0) return;
+  unsigned long long a = reinterpret_cast<unsigned long long>(p) & ~15ull;
+  const unsigned long long e = (reinterpret_cast<unsigned long long>(p) + bytes + 15) & ~15ull;
+  while (a < e) {
+    const unsigned sz = static_cast<unsigned>(min(e - a, 65536ull));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+    a += sz;
+  }
+}
+constexpr int kPrefetchLevels = 3;
+constexpr int kTailThreads = 1024;
+constexpr int kTailWarps = kTailThreads / 32;
+constexpr int kTailMaxRows = 24 * 1024;  // 192 KB of shared fp64
+
+// tpos[order[tail_base + i]] = i; count T-part entries of forward row i and
+// the H/T split of its level-sorted entries.
+__global__ void tail_index_kernel(int nt, int tail_base, const int* order, int* tpos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nt) tpos[order[tail_base + i]] = i;
+}
+
+__global__ void tail_count_kernel(int nt, int tail_base, int L0, const int* order, const long long* gt_ptr,
+                                  const int* ff_lvl, const long long* col_ptr, long long* hsplit,
+                                  int* fcnt, int* bcnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int r = order[tail_base + i];
+  long long lo = gt_ptr[r], hi = gt_ptr[r + 1];
+  const long long e = hi;
+  while (lo < hi) {  // first entry with level > L0 (entries sorted by level ascending)
+    const long long mid = (lo + hi) >> 1;
+    if (ff_lvl[mid] > L0) hi = mid; else lo = mid + 1;
+  }
+  hsplit[i] = lo;
+  fcnt[i] = static_cast<int>(e - lo);
+  bcnt[i] = static_cast<int>(col_ptr[r + 1] - col_ptr[r]);
+}
+
+__global__ void tail_fill_kernel(int nt, int tail_base, const int* order, const int* tpos,
+                                 const long long* gt_ptr, const long long* hsplit, const int* ff_col,
+                                 const double* ff_val, const long long* tf_ptr, int* tf_col, double* tf_val,
+                                 const long long* col_ptr, const int* fb_row, const double* fb_val,
+                                 const long long* tb_ptr, int* tb_row, double* tb_val) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < nt; i += nw) {
+    const int r = order[tail_base + i];
+    const long long s = hsplit[i], e = gt_ptr[r + 1], o = tf_ptr[i];
+    for (long long q = s + lane; q < e; q += 32) {
+      tf_col[o + (q - s)] = tpos[ff_col[q]];
+      tf_val[o + (q - s)] = ff_val[q];
+    }
+    const long long cb = col_ptr[r], ce = col_ptr[r + 1], ob = tb_ptr[i];
+    for (long long q = cb + lane; q < ce; q += 32) {
+      tb_row[ob + (q - cb)] = tpos[fb_row[q]];
+      tb_val[ob + (q - cb)] = fb_val[q];
+    }
+  }
+}
+
+// Forward prologue (grid-wide, after the head sweep): s_i = rhs - G_TH y_H.
+__global__ void tail_fwd_prologue_kernel(int nt, int tail_base, const int* order, const long long* gt_ptr,
+                                         const long long* hsplit, const int* ff_col, const double* ff_val,
+                                         const int* inv, const double* rvec, const double* yf, double* ts) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < nt; i += nw) {
+    const int r = order[tail_base + i];
+    const long long b = gt_ptr[r], e = hsplit[i];
+    double part = 0.0;
+    for (long long q = b + lane; q < e; q += 32) part += ff_val[q] * __ldcg(yf + ff_col[q]);
+    part = warp_sum(part);
+    if (lane == 0) ts[i] = rvec[inv[r]] - part;
+  }
+}
+
+// One tail row against the shared solution vector: sum of val * xs[idx] over
+// [b, e), lane-strided with 4 loads in flight, fixed-order warp tree.
+__device__ __forceinline__ double tail_row_sum(const int* idx, const double* val, long long b, long long e,
+                                               const double* xs, int lane) {
+  double part = 0.0;
+  long long q = b + lane;
+  for (; q + 96 < e; q += 128) {
+    const int c0 = idx[q], c1 = idx[q + 32], c2 = idx[q + 64], c3 = idx[q + 96];
+    const double v0 = val[q], v1 = val[q + 32], v2 = val[q + 64], v3 = val[q + 96];
+    part += v0 * xs[c0];
+    part += v1 * xs[c1];
+    part += v2 * xs[c2];
+    part += v3 * xs[c3];
+  }
+  for (; q < e; q += 32) part += val[q] * xs[idx[q]];
+  return warp_sum(part);
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) tail_forward_kernel(
+    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const double* ts,
+    const long long* tf_ptr, const int* tf_col, const double* tf_val, const double* diag, double* yf,
+    double* yd, unsigned long long* ltime) {
+  extern __shared__ double ys[];
+  const int nt = static_cast<int>(lvl_off[depth + 1] - tail_base);
+  auto prefetch_level = [&](int Lp) {
+    if (Lp > depth) return;
+    const long long lb = lvl_off[Lp] - tail_base, le = lvl_off[Lp + 1] - tail_base;
+    const long long ea = tf_ptr[lb], ez = tf_ptr[le];
+    prefetch_l2(tf_col + ea, (ez - ea) * 4);
+    prefetch_l2(tf_val + ea, (ez - ea) * 8);
+  };
+  if (threadIdx.x == kTailThreads - 32)
+    for (int Lp = L0 + 1; Lp <= L0 + 2 * kPrefetchLevels; ++Lp) prefetch_level(Lp);
+  for (int i = threadIdx.x; i < nt; i += kTailThreads) ys[i] = ts[i];
+  __syncthreads();
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int L = L0 + 1; L <= depth; ++L) {
+    if (threadIdx.x == kTailThreads - 32) prefetch_level(L + 2 * kPrefetchLevels);
+    const int lb = static_cast<int>(lvl_off[L] - tail_base), le = static_cast<int>(lvl_off[L + 1] - tail_base);
+    for (int i = lb + warp; i < le; i += kTailWarps) {
+      const double sum = tail_row_sum(tf_col, tf_val, tf_ptr[i], tf_ptr[i + 1], ys, lane);
+      if (lane == 0) {
+        const double acc = ys[i] - sum;
+        ys[i] = acc;
+        const int r = order[tail_base + i];
+        yf[r] = acc;
+        const double d = diag[r];
+        yd[r] = d > 0.0 ? acc / d : 0.0;
+      }
+    }
+    __syncthreads();
+    if (ltime && threadIdx.x == 0) ltime[L - L0 - 1] = globaltimer_ns();
+  }
+}
+
+// Backward tail: z_k = yd_k - sum_{r in col k} G(r,k) z_r, levels descending.
+__global__ void __launch_bounds__(kTailThreads, 1) tail_backward_kernel(
+    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const long long* tb_ptr,
+    const int* tb_row, const double* tb_val, const double* yd, double* zb, unsigned long long* ltime) {
+  extern __shared__ double zs[];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  auto prefetch_level = [&](int Lp) {
+    if (Lp <= L0) return;
+    const long long lb = lvl_off[Lp] - tail_base, le = lvl_off[Lp + 1] - tail_base;
+    const long long ea = tb_ptr[lb], ez = tb_ptr[le];
+    prefetch_l2(tb_row + ea, (ez - ea) * 4);
+    prefetch_l2(tb_val + ea, (ez - ea) * 8);
+  };
+  if (threadIdx.x == kTailThreads - 32)
+    for (int Lp = depth; Lp > depth - 2 * kPrefetchLevels; --Lp) prefetch_level(Lp);
+  for (int L = depth; L > L0; --L) {
+    if (threadIdx.x == kTailThreads - 32) prefetch_level(L - 2 * kPrefetchLevels);
+    const int lb = static_cast<int>(lvl_off[L] - tail_base), le = static_cast<int>(lvl_off[L + 1] - tail_base);
+    for (int i = lb + warp; i < le; i += kTailWarps) {
+      const double sum = tail_row_sum(tb_row, tb_val, tb_ptr[i], tb_ptr[i + 1], zs, lane);
+      if (lane == 0) {
+        const int k = order[tail_base + i];
+        const double acc = yd[k] - sum;
+        zs[i] = acc;
+        zb[k] = acc;
+      }
+    }
+    __syncthreads();
+    if (ltime && threadIdx.x == 0) ltime[depth - L] = globaltimer_ns();
+  }
+}
+
+// ------------------------------------------------------------ K6: cluster sweeps
+// One thread-block cluster (16 CTAs x 1024 threads = 512 warps, one CTA per SM)
+// sweeps the head levels level-synchronously: every row of level L is computed,
+// then ONE hardware cluster barrier (barrier.cluster arrive.release /
+// wait.acquire, measured 235 ns on B200 vs ~1.2 us for a grid-wide sync and
+// 0.5-1 us per global flag hand-off) publishes the level. At the barrier all of
+// a row's dependencies are complete, so rows read plain CSR data -- no
+// per-level counters, no polling, no level-sorted copies. Solution values are
+// written with plain stores and read with ld.global.cg (L2), so no stale L1
+// line can be observed after the acquire.
+//   EXACT: per-row sums in the reference's order (solver.cpp:44-66), lane 0
+//          serial over register-staged products -> bit-identical to
+//          apply_preconditioner; FAST: per-lane strided partials + fixed warp
+//          tree (deterministic). Wide levels run one row per lane, serial, in
+//          the reference's order in both modes.
+constexpr int kCThreads = 1024;
+constexpr int kCWarps = kCThreads / 32;
+constexpr int kCStage = 128;  // exact mode: products staged per warp before the serial chain
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctas() {
+  unsigned r;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+
+
+// Sum of g[q] * x[idx[q]] over [b, e) by one warp.
+//   EXACT: acc - p_b - p_{b+1} - ... strictly in order (lane 0), optional
+//          zero skip (forward column-scatter semantics: a term with x == 0 is
+//          never subtracted, solver.cpp:47-51).
+//   FAST:  acc - (fixed-order tree of lane partials).
+template <bool EXACT>
+__device__ __forceinline__ double warp_row(double acc, const int* idx, const double* g, const double* x,
+                                           long long b, long long e, int lane, bool skip_zero,
+                                           double* wbuf) {
+  if constexpr (!EXACT) {
+    double part = 0.0;
+    long long q = b + lane;
+    for (; q + 96 < e; q += 128) {
+      const int c0 = idx[q], c1 = idx[q + 32], c2 = idx[q + 64], c3 = idx[q + 96];
+      const double g0 = g[q], g1 = g[q + 32], g2 = g[q + 64], g3 = g[q + 96];
+      const double x0 = __ldcg(x + c0), x1 = __ldcg(x + c1), x2 = __ldcg(x + c2), x3 = __ldcg(x + c3);
+      part += g0 * x0;
+      part += g1 * x1;
+      part += g2 * x2;
+      part += g3 * x3;
+    }
+    for (; q < e; q += 32) part += g[q] * __ldcg(x + idx[q]);
+    return acc - warp_sum(part);
+  } else {
+  for (long long base = b; base < e; base += kCStage) {
+    const int cnt = static_cast<int>(min(static_cast<long long>(kCStage), e - base));
+    constexpr int Q = kCStage / 32;
+    int ci[Q];
+    double gv[Q], xv[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const bool ok = q * 32 + lane < cnt;
+      ci[q] = ok ? idx[base + q * 32 + lane] : 0;
+      gv[q] = ok ? g[base + q * 32 + lane] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) xv[q] = q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (q * 32 + lane < cnt) wbuf[q * 32 + lane] = (skip_zero && xv[q] == 0.0) ? 0.0 : __dmul_rn(gv[q], xv[q]);
+    __syncwarp();
+    if (lane == 0) acc = serial_sub(acc, wbuf, cnt);
+    __syncwarp();
+  }
+  return __shfl_sync(kFull, acc, 0);
+  }
+}
+
+// One row per lane, serial in the reference's order (exact in both modes).
+__device__ __forceinline__ double lane_row(double acc, const int* idx, const double* g, const double* x,
+                                           long long b, long long e, bool skip_zero) {
+  for (long long q = b; q < e; ++q) {
+    const double xv = __ldcg(x + idx[q]);
+    if (!(skip_zero && xv == 0.0)) acc = __dsub_rn(acc, __dmul_rn(g[q], xv));
+  }
+  return acc;
+}
+
+// Forward G y = P r over levels 1..H (gather form over G's rows, k ascending),
+// then D^+ into yd; afterwards (fast mode with a tail) the G_TH part of every
+// tail row: ts_i = rhs_i - sum_{k in H} G(r,k) y_k.
+template <bool EXACT>
+__global__ void __launch_bounds__(kCThreads, 1) cluster_forward_kernel(
+    int H, const long long* lvl_off, const int* order, const long long* gt_ptr, const int* gt_col,
+    const double* gt_val, const double* diag, const int* inv, const double* rvec, double* yf, double* yd,
+    int nt, int tail_base, const long long* hsplit, const int* ff_col, const double* ff_val, double* ts) {
+  __shared__ double stage[EXACT ? kCWarps * kCStage : 1];
+  const int lane = lane_id(), wl = threadIdx.x >> 5;
+  const int W = static_cast<int>(cluster_nctas()) * kCWarps;
+  const int w = static_cast<int>(cluster_rank()) * kCWarps + wl;
+  double* wbuf = stage + (EXACT ? wl * kCStage : 0);
+  for (int L = 1; L <= H; ++L) {
+    const long long lb = lvl_off[L], le = lvl_off[L + 1];
+    if (le - lb >= 2LL * W) {
+      for (long long j = lb + static_cast<long long>(w) * 32 + lane; j < le; j += 32LL * W) {
+        const int r = order[j];
+        const double acc = lane_row(rvec[inv[r]], gt_col, gt_val, yf, gt_ptr[r], gt_ptr[r + 1], true);
+        yf[r] = acc;
+        const double d = diag[r];
+        yd[r] = d > 0.0 ? __ddiv_rn(acc, d) : 0.0;
+      }
+    } else {
+      for (long long j = lb + w; j < le; j += W) {
+        const int r = order[j];
+        const double acc =
+            warp_row<EXACT>(rvec[inv[r]], gt_col, gt_val, yf, gt_ptr[r], gt_ptr[r + 1], lane, true, wbuf);
+        if (lane == 0) {
+          yf[r] = acc;
+          const double d = diag[r];
+          yd[r] = d > 0.0 ? __ddiv_rn(acc, d) : 0.0;
+        }
+      }
+    }
+    cluster_barrier();
+  }
+  if (!EXACT) {
+    for (int i = w; i < nt; i += W) {
+      const int r = order[tail_base + i];
+      const double acc = warp_row<false>(rvec[inv[r]], ff_col, ff_val, yf, gt_ptr[r], hsplit[i], lane, false, wbuf);
+      if (lane == 0) ts[i] = acc;
+    }
+  }
+}
+
+// Backward G^T z = yd over levels H..1 (columns of G, rows ascending); rows of
+// higher levels (the tail) are final before launch.
+template <bool EXACT>
+__global__ void __launch_bounds__(kCThreads, 1) cluster_backward_kernel(
+    int H, const long long* lvl_off, const int* order, const long long* col_ptr, const int* rows,
+    const double* vals, const double* yd, double* zb) {
+  __shared__ double stage[EXACT ? kCWarps * kCStage : 1];
+  const int lane = lane_id(), wl = threadIdx.x >> 5;
+  const int W = static_cast<int>(cluster_nctas()) * kCWarps;
+  const int w = static_cast<int>(cluster_rank()) * kCWarps + wl;
+  double* wbuf = stage + (EXACT ? wl * kCStage : 0);
+  for (int L = H; L >= 1; --L) {
+    const long long lb = lvl_off[L], le = lvl_off[L + 1];
+    if (le - lb >= 2LL * W) {
+      for (long long j = lb + static_cast<long long>(w) * 32 + lane; j < le; j += 32LL * W) {
+        const int k = order[j];
+        zb[k] = lane_row(yd[k], rows, vals, zb, col_ptr[k], col_ptr[k + 1], false);
+      }
+    } else {
+      for (long long j = lb + w; j < le; j += W) {
+        const int k = order[j];
+        const double acc = warp_row<EXACT>(yd[k], rows, vals, zb, col_ptr[k], col_ptr[k + 1], lane, false, wbuf);
+        if (lane == 0) zb[k] = acc;
+      }
+    }
+    cluster_barrier();
+  }
+}
+
+// ---- fast mode, entry-parallel: rows of each level stored contiguously in
+// level order (lptr/lidx/lval), each level cut into chunks of whole rows of
+// ~equal (entries + rows). A warp takes a chunk, issues ALL of its products'
+// loads at once (8 per lane in flight) into a shared-memory product buffer,
+// then sums rows from it: lane per row for short rows, warp tree for long
+// ones (fixed orders -> run-to-run deterministic). Per level this costs about
+// two L2 round trips plus the cluster barrier, instead of (rows per warp) x
+// (two dependent round trips).
+constexpr int kChunkCap = 768;  // product buffer entries per warp (6 KB; 192 KB per CTA)
+constexpr int kShortRow = 16;   // rows up to this length are summed by one lane
+
+template <bool FWD>
+__device__ __forceinline__ void finish_row(int j, double s, const int* order, const double* rhs_pos,
+                                           const int* inv, const double* rvec, const double* diag, double* x,
+                                           double* yd) {
+  if constexpr (FWD) {
+    const int r = order[j];
+    const double acc = rvec[inv[r]] - s;
+    x[r] = acc;
+    const double d = diag[r];
+    yd[r] = d > 0.0 ? acc / d : 0.0;
+  } else {
+    const int k = order[j];
+    x[k] = rhs_pos[k] - s;
+  }
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(kCThreads, 1) cluster_sweep_fast_kernel(
+    int Lfirst, int nlev, const int* chunk, const int* chunk_base, const long long* lptr, const int* lidx,
+    const double* lval, const int* order, const double* rhs_pos, const int* inv, const double* rvec,
+    const double* diag, double* x, double* yd, int nt, int tail_base, const long long* gt_ptr,
+    const long long* hsplit, const int* ff_col, const double* ff_val, double* ts, unsigned long long* ltime) {
+  extern __shared__ double pbuf_all[];
+  const int lane = lane_id(), wl = threadIdx.x >> 5;
+  const int W = static_cast<int>(cluster_nctas()) * kCWarps;
+  const int w = static_cast<int>(cluster_rank()) * kCWarps + wl;
+  double* pbuf = pbuf_all + wl * kChunkCap;
+  const bool pf_thread = threadIdx.x == kCThreads - 32;  // lane 0 of the last warp
+  const int nc = static_cast<int>(cluster_nctas()), cr = static_cast<int>(cluster_rank());
+  auto prefetch_level = [&](int tt) {
+    if (tt >= nlev) return;
+    const int Lp = FWD ? Lfirst + tt : Lfirst - tt;
+    const long long ja = chunk[chunk_base[Lp]], jz = chunk[chunk_base[Lp + 1] - 1];
+    const long long ea = lptr[ja], ez = lptr[jz];
+    const long long s0 = ea + (ez - ea) * cr / nc, s1 = ea + (ez - ea) * (cr + 1) / nc;
+    prefetch_l2(lidx + s0, (s1 - s0) * 4);
+    prefetch_l2(lval + s0, (s1 - s0) * 8);
+    const long long r0 = ja + (jz - ja) * cr / nc, r1 = ja + (jz - ja) * (cr + 1) / nc;
+    prefetch_l2(lptr + r0, (r1 - r0 + 1) * 8);
+    prefetch_l2(order + r0, (r1 - r0) * 4);
+  };
+  if (pf_thread)
+    for (int tt = 0; tt < kPrefetchLevels; ++tt) prefetch_level(tt);
+  for (int t = 0; t < nlev; ++t) {
+    const int L = FWD ? Lfirst + t : Lfirst - t;
+    if (pf_thread) prefetch_level(t + kPrefetchLevels);
+    const int cb = chunk_base[L], ce = chunk_base[L + 1] - 1;  // chunks [cb, ce), starts chunk[cb..ce]
+    for (int c = cb + w; c < ce; c += W) {
+      const int jb = chunk[c], je = chunk[c + 1];
+      if (jb >= je) continue;
+      const long long eb = lptr[jb], ee = lptr[je];
+      if (ee - eb <= kChunkCap) {
+        const int cnt = static_cast<int>(ee - eb);
+        for (int base = 0; base < cnt; base += 256) {
+          int ci[8];
+          double gv[8], xv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int e = base + q * 32 + lane;
+            ci[q] = e < cnt ? lidx[eb + e] : 0;
+            gv[q] = e < cnt ? lval[eb + e] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xv[q] = base + q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (base + q * 32 + lane < cnt) pbuf[base + q * 32 + lane] = gv[q] * xv[q];
+        }
+        __syncwarp();
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          int b = 0, e = 0;
+          if (j < je) {
+            b = static_cast<int>(lptr[j] - eb);
+            e = static_cast<int>(lptr[j + 1] - eb);
+            if (e - b <= kShortRow) {
+              double s = 0.0;
+              for (int q = b; q < e; ++q) s += pbuf[q];
+              finish_row<FWD>(j, s, order, rhs_pos, inv, rvec, diag, x, yd);
+            }
+          }
+          unsigned longs = __ballot_sync(kFull, j < je && e - b > kShortRow);
+          while (longs) {
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int lb2 = __shfl_sync(kFull, b, src), le2 = __shfl_sync(kFull, e, src);
+            double part = 0.0;
+            for (int q = lb2 + lane; q < le2; q += 32) part += pbuf[q];
+            part = warp_sum(part);
+            if (lane == 0) finish_row<FWD>(j0 + src, part, order, rhs_pos, inv, rvec, diag, x, yd);
+          }
+        }
+        __syncwarp();
+      } else {
+        for (int j = jb; j < je; ++j) {
+          double part = 0.0;
+          const long long b = lptr[j], e = lptr[j + 1];
+          for (long long q = b + lane; q < e; q += 32) part += lval[q] * __ldcg(x + lidx[q]);
+          part = warp_sum(part);
+          if (lane == 0) finish_row<FWD>(j, part, order, rhs_pos, inv, rvec, diag, x, yd);
+        }
+      }
+    }
+    cluster_barrier();
+    if (ltime && w == 0 && lane == 0) ltime[t] = globaltimer_ns();
+  }
+  if constexpr (FWD) {  // G_TH part of the tail rows (fast mode with a tail)
+    for (int i = w; i < nt; i += W) {
+      const int r = order[tail_base + i];
+      const long long b = gt_ptr[r], e = hsplit[i];
+      double part = 0.0;
+      for (long long q = b + lane; q < e; q += 32) part += ff_val[q] * __ldcg(x + ff_col[q]);
+      part = warp_sum(part);
+      if (lane == 0) ts[i] = rvec[inv[r]] - part;
+    }
+  }
+}
+
+// Level-ordered row copies: lens, then entries (warp per row).
+__global__ void lvl_len_kernel(int n, const int* order, const long long* aptr, const long long* bptr,
+                               int* alen, int* blen) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int r = order[j];
+  alen[j] = static_cast<int>(aptr[r + 1] - aptr[r]);
+  blen[j] = static_cast<int>(bptr[r + 1] - bptr[r]);
+}
+
+__global__ void lvl_copy_kernel(int n, const int* order, const long long* src_ptr, const int* src_idx,
+                                const double* src_val, const long long* dst_ptr, int* dst_idx, double* dst_val) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int j = gw; j < n; j += nw) {
+    const int r = order[j];
+    const long long sb = src_ptr[r], se = src_ptr[r + 1], db = dst_ptr[j];
+    for (long long q = sb + lane; q < se; q += 32) {
+      dst_idx[db + (q - sb)] = src_idx[q];
+      dst_val[db + (q - sb)] = src_val[q];
+    }
+  }
+}
+
+// chunk[chunk_base[L] + c] = first row j of level L whose weighted prefix
+// (entries + rows from the level start) reaches c * target[L].
+__global__ void chunk_fill_kernel(int depth, const long long* lvl_off, const long long* lptr,
+                                  const int* chunk_base, const long long* target, int* chunk) {
+  const int L = blockIdx.x + 1;
+  if (L > depth) return;
+  const long long lb = lvl_off[L], le = lvl_off[L + 1];
+  const int nch = chunk_base[L + 1] - chunk_base[L] - 1;
+  const long long t = target[L];
+  for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
+    long long j;
+    if (c == nch) {
+      j = le;
+    } else {
+      const long long goal = static_cast<long long>(c) * t;
+      long long lo = lb, hi = le;
+      while (lo < hi) {  // first j with (lptr[j] - lptr[lb]) + (j - lb) >= goal
+        const long long mid = (lo + hi) >> 1;
+        if ((lptr[mid] - lptr[lb]) + (mid - lb) >= goal) hi = mid; else lo = mid + 1;
+      }
+      j = lo;
+    }
+    chunk[chunk_base[L] + c] = static_cast<int>(j);
+  }
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize, 1, 1);
+  cfg.blockDim = dim3(kCThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Largest launchable cluster (16 non-portable, else 8) of 1024-thread CTAs.
+template <typename... KArgs>
+int pick_cluster(void (*kernel)(KArgs...), std::size_t smem = 0) {
+  if (smem) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  for (int c : {16, 8, 4}) {
+    if (c > 8) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c, 1, 1);
+    cfg.blockDim = dim3(kCThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kernel, &cfg) == cudaSuccess && nclusters > 0) return c;
+    cudaGetLastError();
+  }
+  return 1;
+}
+
+struct ClusterSizes {
+  int fwd_fast, fwd_exact, bwd_fast, bwd_exact, sweep_f, sweep_b;
+};
+constexpr std::size_t kChunkSmem = static_cast<std::size_t>(kCWarps) * kChunkCap * sizeof(double);
+ClusterSizes cluster_sizes(int device) {
+  static ClusterSizes cached[64] = {};
+  if (device >= 0 && device < 64 && cached[device].fwd_fast) return cached[device];
+  ClusterSizes c{pick_cluster(cluster_forward_kernel<false>), pick_cluster(cluster_forward_kernel<true>),
+                 pick_cluster(cluster_backward_kernel<false>), pick_cluster(cluster_backward_kernel<true>),
+                 pick_cluster(cluster_sweep_fast_kernel<true>, kChunkSmem),
+                 pick_cluster(cluster_sweep_fast_kernel<false>, kChunkSmem)};
+  if (device >= 0 && device < 64) cached[device] = c;
+  return c;
 }
 
 // Persistent sweep grids: exactly the co-resident capacity of each kernel.
@@ -841,7 +1424,7 @@ void ensure_vectors(SolveState& s, int n) {
   dalloc(s.x, c); dalloc(s.r, c); dalloc(s.p, c); dalloc(s.lp, c); dalloc(s.z, c);
   dalloc(s.best, c); dalloc(s.yf, c); dalloc(s.yd, c); dalloc(s.zb, c); dalloc(s.rhs, c);
   dalloc(s.wdeg, c); dalloc(s.inv, c); dalloc(s.level, c); dalloc(s.order, c);
-  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2); dalloc(s.done, 2 * c + 8);
+  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2); dalloc(s.tpos, c); dalloc(s.done, 2 * c + 8);
   if (std::getenv("PARAC_SWEEP_TRACE")) dalloc(s.trace, 6 * c);  // diagnostics only
   dalloc(s.partials, static_cast<std::size_t>(kRedBlocks) * kSlots);
   dalloc(s.scalars, kScalars);
@@ -887,6 +1470,153 @@ int component_count(const SolveInputs& in) {
   check(cudaMemcpyAsync(&h, count, sizeof(int), cudaMemcpyDeviceToHost, st), "cc");
   check(cudaStreamSynchronize(st), "cc sync");
   return h;
+}
+
+// Choose the narrow tail (levels > L0 with width <= PARAC_TAIL_WIDTH, default
+// 64, at most kTailMaxRows rows) and build its index-remapped entry lists.
+void build_tail(const SolveInputs& in, SolveState& s, int sms) {
+  const int n = in.f_n, depth = s.depth;
+  cudaStream_t st = in.stream;
+  s.tail_L0 = depth;
+  s.tail_n = 0;
+  s.tail_base = n;
+  const char* env = std::getenv("PARAC_TAIL_WIDTH");
+  const int wt = env ? std::atoi(env) : 64;
+  if (n == 0 || depth < 2 || wt <= 0) return;
+  std::vector<long long> off(static_cast<std::size_t>(depth) + 2);
+  check(cudaMemcpyAsync(off.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "tail sync");
+  int L0 = depth;
+  while (L0 >= 1 && off[L0 + 1] - off[L0] <= wt) --L0;
+  while (L0 < depth && off[depth + 1] - off[L0 + 1] > kTailMaxRows) ++L0;
+  if (L0 >= depth) return;
+  const int base = static_cast<int>(off[L0 + 1]);
+  const int nt = static_cast<int>(off[depth + 1]) - base;
+  if (s.cap_tail < static_cast<std::size_t>(nt) + 1) {
+    dalloc(s.tf_ptr, static_cast<std::size_t>(nt) + 1);
+    dalloc(s.tb_ptr, static_cast<std::size_t>(nt) + 1);
+    dalloc(s.hsplit, static_cast<std::size_t>(nt));
+    dalloc(s.tail_s, static_cast<std::size_t>(nt));
+    dalloc(s.tail_cnt, 2 * (static_cast<std::size_t>(nt) + 1));
+    s.cap_tail = static_cast<std::size_t>(nt) + 1;
+  }
+  int* fcnt = s.tail_cnt;
+  int* bcnt = s.tail_cnt + (nt + 1);
+  const int tb = (nt + 255) / 256;
+  tail_index_kernel<<<tb, 256, 0, st>>>(nt, base, s.order, s.tpos);
+  tail_count_kernel<<<tb, 256, 0, st>>>(nt, base, L0, s.order, s.gt_ptr, s.ff_lvl, in.col_ptr, s.hsplit,
+                                        fcnt, bcnt);
+  note_launches(2);
+  check(launch_scan(fcnt, nt, s.tf_ptr, s.tiles, st), "scan");
+  check(launch_scan(bcnt, nt, s.tb_ptr, s.tiles, st), "scan");
+  long long tot[2] = {0, 0};
+  check(cudaMemcpyAsync(&tot[0], s.tf_ptr + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaMemcpyAsync(&tot[1], s.tb_ptr + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "tail sync");
+  const std::size_t need = static_cast<std::size_t>(std::max<long long>(std::max(tot[0], tot[1]), 1));
+  if (s.cap_tail_nnz < need) {
+    dalloc(s.tf_col, need);
+    dalloc(s.tf_val, need);
+    dalloc(s.tb_row, need);
+    dalloc(s.tb_val, need);
+    s.cap_tail_nnz = need;
+  }
+  tail_fill_kernel<<<sms * 8, 256, 0, st>>>(nt, base, s.order, s.tpos, s.gt_ptr, s.hsplit, s.ff_col, s.ff_val,
+                                            s.tf_ptr, s.tf_col, s.tf_val, in.col_ptr, s.fb_row, s.fb_val,
+                                            s.tb_ptr, s.tb_row, s.tb_val);
+  note_launches(1);
+  check(cudaGetLastError(), "tail build");
+  static bool attr = false;
+  if (!attr) {
+    check(cudaFuncSetAttribute(tail_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kTailMaxRows * 8), "attr");
+    check(cudaFuncSetAttribute(tail_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kTailMaxRows * 8), "attr");
+    attr = true;
+  }
+  s.tail_L0 = L0;
+  s.tail_n = nt;
+  s.tail_base = base;
+}
+
+__global__ void gather_ll_kernel(int cnt, const long long* idx, const long long* src, long long* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) dst[i] = src[idx[i]];
+}
+
+// Chunk table of one direction for a cluster of W warps (see cluster_sweep_fast_kernel).
+void build_chunks(const SolveInputs& in, SolveState& s, const long long* lptr, int W, int*& chunk,
+                  int*& cbase, std::size_t& cap_chunk) {
+  const int depth = s.depth;
+  cudaStream_t st = in.stream;
+  // entry offsets at the level boundaries
+  long long* bnd = s.lvl_target;  // scratch (depth + 2)
+  gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, lptr, bnd);
+  note_launches(1);
+  std::vector<long long> eoff(depth + 2), roff(depth + 2);
+  check(cudaMemcpyAsync(eoff.data(), bnd, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaMemcpyAsync(roff.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "chunk sync");
+  std::vector<int> base(depth + 2, 0);
+  std::vector<long long> target(depth + 2, 1);
+  long long total = 0;
+  for (int L = 1; L <= depth; ++L) {
+    const long long tot = (eoff[L + 1] - eoff[L]) + (roff[L + 1] - roff[L]);
+    long long t = std::max<long long>(1, (tot + W - 1) / W);
+    t = std::min<long long>(t, kChunkCap / 2);
+    const long long nch = std::max<long long>(1, (tot + t - 1) / t);
+    target[L] = t;
+    base[L] = static_cast<int>(total);
+    total += nch + 1;
+  }
+  base[depth + 1] = static_cast<int>(total);
+  if (cap_chunk < static_cast<std::size_t>(total)) {
+    dalloc(chunk, static_cast<std::size_t>(total));
+    cap_chunk = static_cast<std::size_t>(total);
+  }
+  if (!cbase) dalloc(cbase, s.cap_levels);  // cap_levels = n + 2 >= depth + 2
+  check(cudaMemcpyAsync(cbase, base.data(), sizeof(int) * (depth + 2), cudaMemcpyHostToDevice, st), "h2d");
+  check(cudaMemcpyAsync(s.lvl_target, target.data(), sizeof(long long) * (depth + 2), cudaMemcpyHostToDevice, st), "h2d");
+  chunk_fill_kernel<<<depth, 256, 0, st>>>(depth, s.lvl_off, lptr, cbase, s.lvl_target, chunk);
+  note_launches(1);
+  check(cudaStreamSynchronize(st), "chunk sync");  // host vectors go out of scope
+}
+
+// Level-ordered copies of G's rows and columns + chunk tables (fast mode).
+void build_level_layout(const SolveInputs& in, SolveState& s, int sms) {
+  const int n = in.f_n, depth = s.depth;
+  const long long Z = in.f_nnz;
+  cudaStream_t st = in.stream;
+  if (n == 0 || depth == 0) return;
+  const std::size_t cz = static_cast<std::size_t>(std::max<long long>(Z, 1));
+  if (s.cap_lz < cz) {
+    dalloc(s.lf_idx, cz); dalloc(s.lf_val, cz); dalloc(s.lb_idx, cz); dalloc(s.lb_val, cz);
+    s.cap_lz = cz;
+  }
+  if (s.cap_levels < static_cast<std::size_t>(n) + 2) {
+    dalloc(s.lf_ptr, static_cast<std::size_t>(n) + 1);
+    dalloc(s.lb_ptr, static_cast<std::size_t>(n) + 1);
+    dalloc(s.lvl_target, static_cast<std::size_t>(n) + 2);
+    dfree(s.f_cbase);
+    dfree(s.b_cbase);
+    s.cap_levels = static_cast<std::size_t>(n) + 2;
+  }
+  int* alen = s.tmp_int;
+  int* blen = nullptr;
+  dalloc(blen, static_cast<std::size_t>(n) + 1);
+  const int blocks = (n + 255) / 256;
+  lvl_len_kernel<<<blocks, 256, 0, st>>>(n, s.order, s.gt_ptr, in.col_ptr, alen, blen);
+  note_launches(1);
+  check(launch_scan(alen, n, s.lf_ptr, s.tiles, st), "scan");
+  check(launch_scan(blen, n, s.lb_ptr, s.tiles, st), "scan");
+  lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, s.gt_ptr, s.gt_col, s.gt_val, s.lf_ptr, s.lf_idx, s.lf_val);
+  lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, in.col_ptr, in.rows, in.vals, s.lb_ptr, s.lb_idx, s.lb_val);
+  note_launches(2);
+  const ClusterSizes cs = cluster_sizes(in.device);
+  build_chunks(in, s, s.lf_ptr, cs.sweep_f * kCWarps, s.f_chunk, s.f_cbase, s.cap_fchunk);
+  build_chunks(in, s, s.lb_ptr, cs.sweep_b * kCWarps, s.b_chunk, s.b_cbase, s.cap_bchunk);
+  dfree(blen);
+  check(cudaGetLastError(), "level layout");
 }
 
 void prepare_factor(const SolveInputs& in) {
@@ -950,6 +1680,16 @@ void prepare_factor(const SolveInputs& in) {
                                              s.fb_row, s.fb_val, s.fb_lvl);
   note_launches(2);
   check(cudaGetLastError(), "level sort");
+  build_tail(in, s, sms);
+  build_level_layout(in, s, sms);
+  if (std::getenv("PARAC_SWEEP_PROFILE")) {
+    const std::size_t need = 4 * (static_cast<std::size_t>(s.depth) + 2);
+    if (s.cap_ltime < need) {
+      dalloc(s.ltime, need);
+      s.cap_ltime = need;
+    }
+    check(cudaMemsetAsync(s.ltime, 0, need * 8, st), "memset");
+  }
   s.factor_ready = true;
 }
 
@@ -986,15 +1726,94 @@ struct Solver {
     int* done_b = s.done + (D + 2);
     check(cudaMemsetAsync(s.done, 0, sizeof(int) * 2 * (D + 2), st), "memset");
     check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
+    static const std::string sweep = std::getenv("PARAC_SWEEP") ? std::getenv("PARAC_SWEEP") : "chunk";
+    const bool legacy = sweep == "legacy";
+    if (!exact && sweep == "chunk") {
+      const ClusterSizes cs = cluster_sizes(in.device);
+      const int H = s.tail_L0;
+      const int nt = s.tail_n;
+      check(launch_cluster(cluster_sweep_fast_kernel<true>, cs.sweep_f, kChunkSmem, st, 1, H, s.f_chunk,
+                           s.f_cbase, s.lf_ptr, s.lf_idx, s.lf_val, s.order, nullptr, s.inv, r, in.diag, s.yf,
+                           s.yd, nt, s.tail_base, s.gt_ptr, s.hsplit, s.ff_col, s.ff_val, s.tail_s,
+                           s.ltime ? s.ltime : nullptr),
+            "chunk forward");
+      note_launches(1);
+      if (nt > 0) {
+        const std::size_t smem = static_cast<std::size_t>(nt) * 8;
+        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
+                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
+                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
+        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
+                                                            s.tb_row, s.tb_val, s.yd, s.zb,
+                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
+        note_launches(2);
+      }
+      check(launch_cluster(cluster_sweep_fast_kernel<false>, cs.sweep_b, kChunkSmem, st, H, H, s.b_chunk,
+                           s.b_cbase, s.lb_ptr, s.lb_idx, s.lb_val, s.order, s.yd, nullptr, nullptr, nullptr,
+                           s.zb, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           s.ltime ? s.ltime + 3 * (D + 2) : nullptr),
+            "chunk backward");
+      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
+      note_launches(2);
+      return;
+    }
+    if (!legacy) {
+      const ClusterSizes cs = cluster_sizes(in.device);
+      const int H = exact ? D : s.tail_L0;  // head depth (== D without a tail)
+      const int nt = exact ? 0 : s.tail_n;
+      if (exact)
+        check(launch_cluster(cluster_forward_kernel<true>, cs.fwd_exact, 0, st, H, s.lvl_off, s.order, s.gt_ptr,
+                             s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, 0, 0, s.hsplit, s.ff_col,
+                             s.ff_val, s.tail_s), "cluster forward");
+      else
+        check(launch_cluster(cluster_forward_kernel<false>, cs.fwd_fast, 0, st, H, s.lvl_off, s.order, s.gt_ptr,
+                             s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, nt, s.tail_base, s.hsplit,
+                             s.ff_col, s.ff_val, s.tail_s), "cluster forward");
+      note_launches(1);
+      if (nt > 0) {
+        const std::size_t smem = static_cast<std::size_t>(nt) * 8;
+        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
+                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
+                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
+        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
+                                                            s.tb_row, s.tb_val, s.yd, s.zb,
+                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
+        note_launches(2);
+      }
+      if (exact)
+        check(launch_cluster(cluster_backward_kernel<true>, cs.bwd_exact, 0, st, H, s.lvl_off, s.order, in.col_ptr,
+                             in.rows, in.vals, s.yd, s.zb), "cluster backward");
+      else
+        check(launch_cluster(cluster_backward_kernel<false>, cs.bwd_fast, 0, st, H, s.lvl_off, s.order, in.col_ptr,
+                             in.rows, in.vals, s.yd, s.zb), "cluster backward");
+      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
+      note_launches(2);
+      return;
+    }
     if (!exact) {
+      const int H = s.tail_L0;  // head depth (== D without a tail)
       sweep_forward_fast_kernel<<<grids.fwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, s.gt_col,
+          in.f_n, H, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, s.gt_col,
           s.gt_val, in.diag, s.inv, r, s.yf, s.yd, done_f, s.counters + 2, s.trace);
+      note_launches(1);
+      if (s.tail_n > 0) {
+        const int sms = sm_count(in.device);
+        const std::size_t smem = static_cast<std::size_t>(s.tail_n) * 8;
+        tail_fwd_prologue_kernel<<<sms * 4, 256, 0, st>>>(s.tail_n, s.tail_base, s.order, s.gt_ptr, s.hsplit,
+                                                         s.ff_col, s.ff_val, s.inv, r, s.yf, s.tail_s);
+        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
+                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
+                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
+        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
+                                                            s.tb_row, s.tb_val, s.yd, s.zb,
+                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
+        note_launches(3);
+      }
       sweep_backward_fast_kernel<<<grids.bwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, in.rows,
+          in.f_n, H, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, in.rows,
           in.vals, s.yd, s.zb, done_b, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
       gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
-      note_launches(3);
+      note_launches(2);
       return;
     }
     sweep_forward_kernel<<<grids.fwd, kSweepThreads, 0, st>>>(
@@ -1069,6 +1888,10 @@ void solve_release(SolveState& s) {
   dfree(s.ff_col); dfree(s.ff_val); dfree(s.ff_lvl); dfree(s.fb_row); dfree(s.fb_val); dfree(s.fb_lvl); dfree(s.lvl_off); dfree(s.flags); dfree(s.x); dfree(s.r); dfree(s.p);
   dfree(s.lp); dfree(s.z); dfree(s.best); dfree(s.yf); dfree(s.yd); dfree(s.zb); dfree(s.rhs);
   dfree(s.partials); dfree(s.scalars); dfree(s.counters); dfree(s.tiles); dfree(s.tmp_int);
+  dfree(s.tpos); dfree(s.tf_ptr); dfree(s.tb_ptr); dfree(s.hsplit); dfree(s.tf_col); dfree(s.tb_row);
+  dfree(s.tf_val); dfree(s.tb_val); dfree(s.tail_s); dfree(s.tail_cnt);
+  dfree(s.lf_ptr); dfree(s.lb_ptr); dfree(s.lf_idx); dfree(s.lb_idx); dfree(s.lf_val); dfree(s.lb_val);
+  dfree(s.f_chunk); dfree(s.f_cbase); dfree(s.b_chunk); dfree(s.b_cbase); dfree(s.lvl_target); dfree(s.ltime);
   s = SolveState{};
 }
 void solve_invalidate(SolveState& s) {
@@ -1129,6 +1952,17 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     download(z, in.state->z, in.f_n, in.stream);
     sv.check_abort();
     if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
+    if (in.state->ltime) {  // diagnostics: [H, depth, L0] then 4 x (depth+2) timestamps
+      const SolveState& ss = *in.state;
+      std::vector<unsigned long long> t(4 * (static_cast<std::size_t>(ss.depth) + 2));
+      check(cudaMemcpy(t.data(), ss.ltime, t.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+      if (FILE* f = std::fopen(std::getenv("PARAC_SWEEP_PROFILE"), "wb")) {
+        const int hdr[3] = {ss.tail_L0, ss.depth, ss.tail_n};
+        std::fwrite(hdr, 4, 3, f);
+        std::fwrite(t.data(), 8, t.size(), f);
+        std::fclose(f);
+      }
+    }
   });
 }
 

@@ -26,6 +26,25 @@ struct SolveState {
   // fast-mode sweep copies (entries sorted by dependency level) + level of each entry
   int *ff_col = nullptr, *ff_lvl = nullptr, *fb_row = nullptr, *fb_lvl = nullptr;
   double *ff_val = nullptr, *fb_val = nullptr;
+  // fast-mode narrow tail (levels > tail_L0), swept by one CTA (see solve_kernels.cu)
+  int tail_L0 = 0;            // head depth; == depth when there is no tail
+  int tail_n = 0, tail_base = 0;
+  int* tpos = nullptr;
+  long long *tf_ptr = nullptr, *tb_ptr = nullptr, *hsplit = nullptr;
+  int *tf_col = nullptr, *tb_row = nullptr;
+  double *tf_val = nullptr, *tb_val = nullptr, *tail_s = nullptr;
+  int* tail_cnt = nullptr;
+  // fast-mode chunked cluster sweeps: rows (forward) / columns (backward) of G
+  // copied in level order, and per-level chunk tables for the cluster's warps
+  long long *lf_ptr = nullptr, *lb_ptr = nullptr;
+  int *lf_idx = nullptr, *lb_idx = nullptr;
+  double *lf_val = nullptr, *lb_val = nullptr;
+  int *f_chunk = nullptr, *f_cbase = nullptr, *b_chunk = nullptr, *b_cbase = nullptr;
+  long long* lvl_target = nullptr;
+  unsigned long long* ltime = nullptr;  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
+  std::size_t cap_ltime = 0;
+  std::size_t cap_lz = 0, cap_fchunk = 0, cap_bchunk = 0, cap_levels = 0;
+  std::size_t cap_tail = 0, cap_tail_nnz = 0;
   int mode = 0;  // 0 default (pcg fast, apply exact), 1 exact, 2 fast
   unsigned long long* trace = nullptr;  // PARAC_SWEEP_TRACE diagnostics        // per-level finished-row counters, forward + backward
   int depth = 0;

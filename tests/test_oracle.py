@@ -154,3 +154,20 @@ def test_port_pcg_rejects_disconnected(port):
     b = np.zeros(20)
     b[0], b[1] = 1.0, -1.0
     assert port.pcg(g, f, b)[0] == 14  # Errc::not_connected
+
+
+def test_fullsize_fixture_pins_survey_values():
+    # tests/golden/fullsize.json (made from oracle/_ref at the BASELINE sizes)
+    # agrees with the survey's independent probe.
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fullsize.json")) as fh:
+        full = {c["name"]: c for c in json.load(fh)["configs"]}
+    assert full["poisson3d_128"]["checksum"] == "13308715cf34482c"
+    assert full["poisson3d_128"]["nnz_off"] == 22048797
+    assert full["poisson3d_128"]["total_fills"] == 19951646
+    assert full["poisson3d_128"]["depth"] == 1206
+    assert full["poisson3d_128"]["pcg"]["iterations"] == 34
+    assert full["poisson2d_256"]["nnz_off"] == 330229 and full["poisson2d_256"]["depth"] == 139
+    assert full["poisson2d_256"]["pcg"]["iterations"] == 50
+    assert full["rmat_22"]["n"] == 4194304

@@ -169,6 +169,25 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
 int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
                      const parac_gpu_options* opt, parac_gpu_factor_info* info);
 
+/* ---- batch (BASELINE config[4]: many independent Laplacians per GPU) ------
+ * Stage `count` problems (graph i, ordering perms[i], seed seeds[i]) as one
+ * disjoint-union problem so a single persistent elimination factors all of
+ * them concurrently; every problem's factor is byte-identical to its
+ * stand-alone parac_gpu_factor (same graph, ordering and seed). There is no
+ * reference entry point for a batch: the reference loops over
+ * factor_randomized / factor_parallel_left, one problem at a time. */
+int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                           const int32_t* const* perms, const uint64_t* seeds);
+/* upload_batch + factor_resident. */
+int parac_gpu_factor_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                           const int32_t* const* perms, const uint64_t* seeds, const parac_gpu_options* opt,
+                           parac_gpu_factor_info* info);
+/* Off-diagonal count of problem i's factor (size its rows/values buffers). */
+int parac_gpu_batch_nnz(parac_gpu_ctx* ctx, int32_t i, int64_t* nnz_off);
+/* Problem i's LdlFactor arrays, in its own position space. */
+int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, int32_t* rows,
+                             double* values, double* diag);
+
 /* Copy the resident factor to caller buffers (LdlFactor fields,
  * include/parac/factor.hpp:18-25): col_ptr[n+1], rows[Z], values[Z],
  * diag[n]; stats arrays [n] may be NULL (need record_stats). */
@@ -181,6 +200,10 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
  * and sorted, 2 merged, 3 column written, 4 weight-sorted + suffix, 5 fills
  * emitted, 6 decremented, 7 end (after publishing). Zero = phase skipped. */
 int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end);
+/* Diagnostics: sub-phase timestamps sub[8*k + i] of the same run (i = 0 setup
+ * loads done, 1 gather landed, 2 weight sort done, 3 samples drawn, 4 fills
+ * written, 5 release fence done; zero = not recorded on that path). */
+int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub);
 
 /* Stage an existing factor (e.g. one computed by the reference) on the
  * device for the solve entry points. */

@@ -78,6 +78,12 @@ SIGNATURES = {
                                    P(parac_gpu_factor_info)]),
     "parac_gpu_download": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "parac_gpu_download_times": (C.c_int, [vp, vp]),
+    "parac_gpu_download_subtimes": (C.c_int, [vp, vp]),
+    "parac_gpu_upload_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp]),
+    "parac_gpu_factor_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp, P(parac_gpu_options),
+                                         P(parac_gpu_factor_info)]),
+    "parac_gpu_batch_nnz": (C.c_int, [vp, i32, P(i64)]),
+    "parac_gpu_download_batch": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "parac_gpu_schedule_levels": (C.c_int, [vp, vp, P(i32)]),
     "parac_gpu_pcg": (C.c_int, [vp, vp, f64, i32, vp, P(parac_gpu_solve_report)]),

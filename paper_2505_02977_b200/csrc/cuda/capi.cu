@@ -81,7 +81,7 @@ struct parac_gpu_ctx {
   DevBuf<unsigned> dir;
   DevBuf<char> large_pool;
   DevBuf<Ctrl> ctrl;
-  DevBuf<unsigned long long> vtimes;
+  DevBuf<unsigned long long> vtimes, vsub;
   bool has_times = false;
   Ctrl last_ctrl{};
   long long last_z = 0;
@@ -95,6 +95,13 @@ struct parac_gpu_ctx {
   bool f_external = false;  // uploaded via parac_gpu_upload_factor
   DevBuf<double> f_diag_ext;
   DevBuf<int> f_perm_ext;
+  // batch staging (parac_gpu_upload_batch): problem of each position, first
+  // position per problem (count+1), derived sample seed per problem
+  int batch_count = 0;
+  std::vector<long long> batch_base_h;
+  DevBuf<int> pos_pid;
+  DevBuf<long long> pid_base;
+  DevBuf<unsigned long long> pid_seed;
   // solve state
   SolveState solve;
 };
@@ -190,16 +197,23 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.large_cap = b.large;
   d.ctrl = ctx->ctrl.p;
   d.sample_seed = derive_seed(seed, kSaltSampling);
+  d.pos_pid = ctx->batch_count > 0 ? ctx->pos_pid.p : nullptr;
+  d.pid_base = ctx->batch_count > 0 ? ctx->pid_base.p : nullptr;
+  d.pid_seed = ctx->batch_count > 0 ? ctx->pid_seed.p : nullptr;
   const double wd = o.watchdog_seconds > 0 ? o.watchdog_seconds : 60.0;
   d.watchdog_ns = static_cast<unsigned long long>(wd * 1e9);
   d.verify = o.verify;
   d.delay_ns = o.delay_ns;
   d.vtimes = nullptr;
+  d.vsub = nullptr;
   ctx->has_times = o.record_times != 0;
   if (o.record_times) {
     ctx->vtimes.ensure(8 * nn);
     check(cudaMemsetAsync(ctx->vtimes.p, 0, 8 * nn * sizeof(unsigned long long), s), "memset");
     d.vtimes = ctx->vtimes.p;
+    ctx->vsub.ensure(8 * nn);
+    check(cudaMemsetAsync(ctx->vsub.p, 0, 8 * nn * sizeof(unsigned long long), s), "memset");
+    d.vsub = ctx->vsub.p;
   }
 
   check(cudaEventRecord(ctx->ev[0], s), "event");
@@ -300,7 +314,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
   ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
-  ctx->large_pool.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->col_ptr.release(); ctx->rows.release();
+  ctx->large_pool.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->vsub.release(); ctx->col_ptr.release(); ctx->rows.release();
   ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
   solve_release(ctx->solve);
   for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -330,7 +344,120 @@ int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
     ctx->n = n;
     ctx->nnz = nnz;
     ctx->f_n = -1;
+    ctx->batch_count = 0;
     solve_invalidate(ctx->solve);
+  });
+}
+
+// Batch (BASELINE config[4]): stage `count` independent problems as ONE
+// disjoint-union graph -- labels and positions of problem i are offset by the
+// sizes of problems 0..i-1 -- so one persistent elimination kernel factors
+// them all at once. Each position keeps its own problem's sample seed and
+// local position as the RNG key, and fills never cross components, so every
+// problem's factor is byte-identical to its stand-alone factorization.
+int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                           const int32_t* const* perms, const uint64_t* seeds) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (count <= 0 || !graphs || !perms || !seeds) throw Failure{dimension_mismatch, "empty batch"};
+    long long N = 0, NNZ = 0;
+    std::vector<long long> base(static_cast<std::size_t>(count) + 1, 0);
+    for (int i = 0; i < count; ++i) {
+      if (graphs[i].n < 0) throw Failure{dimension_mismatch, "bad graph in batch"};
+      base[i] = N;
+      N += graphs[i].n;
+      NNZ += graphs[i].ptr[graphs[i].n];
+    }
+    base[count] = N;
+    if (N > 2147483647LL) throw Failure{dimension_mismatch, "batch exceeds 2^31 vertices"};
+    std::vector<int64_t> ptr(static_cast<std::size_t>(N) + 1);
+    std::vector<int32_t> adj(static_cast<std::size_t>(std::max<long long>(NNZ, 1)));
+    std::vector<double> w(static_cast<std::size_t>(std::max<long long>(NNZ, 1)));
+    std::vector<int32_t> perm(static_cast<std::size_t>(std::max<long long>(N, 1)));
+    std::vector<int> pid(static_cast<std::size_t>(std::max<long long>(N, 1)));
+    std::vector<unsigned long long> ps(static_cast<std::size_t>(count));
+    long long e0 = 0;
+    for (int i = 0; i < count; ++i) {
+      const parac_csr& g = graphs[i];
+      const int b = static_cast<int>(base[i]);
+      for (int v = 0; v < g.n; ++v) {
+        ptr[b + v] = e0 + g.ptr[v];
+        perm[b + v] = perms[i][v] + b;
+        pid[b + v] = i;
+      }
+      const long long m = g.ptr[g.n];
+      for (long long e = 0; e < m; ++e) {
+        adj[e0 + e] = g.adj[e] + b;
+        w[e0 + e] = g.w[e];
+      }
+      e0 += m;
+      ps[i] = derive_seed(seeds[i], kSaltSampling);
+    }
+    ptr[N] = e0;
+    parac_csr u{static_cast<int32_t>(N), ptr.data(), adj.data(), w.data()};
+    const int rc = parac_gpu_upload(ctx, &u, perm.data());
+    if (rc) throw Failure{rc, parac_gpu_last_error()};
+    cudaStream_t s = ctx->stream;
+    ctx->pos_pid.ensure(static_cast<std::size_t>(std::max<long long>(N, 1)));
+    ctx->pid_base.ensure(static_cast<std::size_t>(count) + 1);
+    ctx->pid_seed.ensure(static_cast<std::size_t>(count));
+    // positions: problem i owns positions [base_i, base_{i+1})
+    check(cudaMemcpyAsync(ctx->pos_pid.p, pid.data(), sizeof(int) * N, cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaMemcpyAsync(ctx->pid_base.p, base.data(), sizeof(long long) * (count + 1), cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaMemcpyAsync(ctx->pid_seed.p, ps.data(), sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaStreamSynchronize(s), "h2d sync");
+    ctx->batch_count = count;
+    ctx->batch_base_h = base;
+  });
+}
+
+int parac_gpu_factor_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                           const int32_t* const* perms, const uint64_t* seeds, const parac_gpu_options* opt,
+                           parac_gpu_factor_info* info) {
+  Timer wall;
+  int rc = parac_gpu_upload_batch(ctx, count, graphs, perms, seeds);
+  if (rc) return rc;
+  const double up = wall.ms();
+  rc = parac_gpu_factor_resident(ctx, 0, opt, info);
+  if (rc == 0 && info) {
+    info->upload_ms = up;
+    info->wall_ms = wall.ms();
+  }
+  return rc;
+}
+
+int parac_gpu_batch_nnz(parac_gpu_ctx* ctx, int32_t i, int64_t* nnz_off) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ctx->f_n < 0 || ctx->batch_count <= 0 || i < 0 || i >= ctx->batch_count)
+      throw Failure{dimension_mismatch, "no resident batch factor / index out of range"};
+    long long c[2];
+    const long long b = ctx->batch_base_h[i], e = ctx->batch_base_h[i + 1];
+    check(cudaMemcpy(&c[0], ctx->col_ptr.p + b, sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+    check(cudaMemcpy(&c[1], ctx->col_ptr.p + e, sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+    *nnz_off = c[1] - c[0];
+  });
+}
+
+int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, int32_t* rows, double* values,
+                             double* diag) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ctx->f_n < 0 || ctx->batch_count <= 0 || i < 0 || i >= ctx->batch_count)
+      throw Failure{dimension_mismatch, "no resident batch factor / index out of range"};
+    const long long b = ctx->batch_base_h[i], e = ctx->batch_base_h[i + 1];
+    const long long n = e - b;
+    cudaStream_t s = ctx->stream;
+    check(cudaMemcpyAsync(col_ptr, ctx->col_ptr.p + b, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost, s), "d2h");
+    check(cudaStreamSynchronize(s), "d2h sync");
+    const long long z0 = col_ptr[0], z = col_ptr[n] - z0;
+    if (rows && z) check(cudaMemcpyAsync(rows, ctx->rows.p + z0, sizeof(int) * z, cudaMemcpyDeviceToHost, s), "d2h");
+    if (values && z) check(cudaMemcpyAsync(values, ctx->vals.p + z0, sizeof(double) * z, cudaMemcpyDeviceToHost, s), "d2h");
+    if (diag && n) check(cudaMemcpyAsync(diag, ctx->diag.p + b, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    check(cudaStreamSynchronize(s), "d2h sync");
+    for (long long k = 0; k <= n; ++k) col_ptr[k] -= z0;
+    if (rows)
+      for (long long t = 0; t < z; ++t) rows[t] -= static_cast<int>(b);
   });
 }
 
@@ -477,6 +604,14 @@ int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end) {
     if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
     check(cudaMemcpy(start_end, ctx->vtimes.p, sizeof(unsigned long long) * 8 * ctx->f_n,
                      cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
+    check(cudaMemcpy(sub, ctx->vsub.p, sizeof(unsigned long long) * 8 * ctx->f_n, cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

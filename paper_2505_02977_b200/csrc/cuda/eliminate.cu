@@ -56,6 +56,10 @@ __device__ __forceinline__ bool is_big_cta() {
 
 #define PHASE(i) \
   do { if (d.vtimes && lead) d.vtimes[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
+// sub-phase stamps (record_times diagnostics): 0 setup done, 1 gather landed,
+// 2 weight sort done, 3 samples drawn, 4 fills written, 5 fence done
+#define SUB(i) \
+  do { if (d.vsub && lead) d.vsub[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
 
 // Column scratch views. A: raw key (row << 32 | source+1), then merged
 // (row << 32 | multiplicity); B: weights; C: suffix sums, then the ready list.
@@ -317,45 +321,46 @@ __device__ __noinline__ void cta_sort_weight(unsigned long long* A, double* B, i
 }
 
 // ------------------------------------------------------------ rank sort
-// Sort of R <= T*ITEMS unique keys held in registers (element g = i*T + tid),
-// T = 32 (one warp) or kThreads (the CTA). Keys are (k1) or (k1, k2)
-// lexicographic. Two phases, no data-dependent control flow:
-//   1. rank inside the element's 32-element warp segment, by 32 shuffles;
-//      write the segment in sorted order to X1/X2;
-//   2. add, for every other segment, the count of its keys below the
-//      element's (5-step binary search of the sorted segment).
-// O(R (32 + 5 R/32)) compare steps instead of a log^2 network: at R ~ 100-300
-// it is 3-5x faster than the bitonic network and far smaller code.
-template <bool TWO>
-__device__ __forceinline__ bool key_less(unsigned long long a1, unsigned long long a2, unsigned long long b1,
-                                         unsigned long long b2) {
-  return TWO ? (a1 < b1 || (a1 == b1 && a2 < b2)) : a1 < b1;
-}
-
-template <int T, int ITEMS, bool TWO>
-__device__ __forceinline__ void rank_sort(const unsigned long long (&k1)[ITEMS], const unsigned long long (&k2)[ITEMS],
-                                          int R, unsigned long long* X1, unsigned long long* X2,
-                                          int (&rank)[ITEMS]) {
+// Stable sort of R <= T*ITEMS u64 keys held in registers (element g = i*T +
+// tid; ties keep g order), T = 32 (one warp) or kThreads (the CTA). Two
+// phases, branch-free compares, broadcast shared-memory reads:
+//   1. rank inside the element's 32-element segment (32 broadcast loads of
+//      the unsorted keys, staged in X2); the segment is written sorted to X1;
+//   2. add, for every other segment, how many of its keys precede the
+//      element (5-step binary search of the sorted segment: keys <= k for
+//      earlier segments, < k for later ones -- that is the stable tie rule).
+// Raw keys (row << 32 | source+1) are unique. The weight sort needs (weight,
+// row) order; its input is already row-ascending, so a STABLE sort on the
+// weight bits alone gives exactly fill_sorted_view's order
+// (factor_common.hpp:133-145).
+template <int T, int ITEMS>
+__device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], int R, unsigned long long* X1,
+                                          unsigned long long* X2, int (&rank)[ITEMS]) {
   const int tid = T == 32 ? lane_id() : static_cast<int>(threadIdx.x);
   const int lane = tid & 31;
   const int wid = tid >> 5;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * T + tid;
+    if (g < R) X2[g] = k[i];
+  }
+  if (T == 32) __syncwarp(); else __syncthreads();
   int lr[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int seg = i * (T / 32) + wid;
-    const int len = min(32, R - seg * 32);  // may be <= 0 (segment fully padding)
+    const int len = min(32, R - seg * 32);  // <= 0: segment fully padding
+    const unsigned long long* K = X2 + seg * 32;
     int c = 0;
+    if (len > 0) {
 #pragma unroll 8
-    for (int t = 0; t < 32; ++t) {
-      const unsigned long long o1 = __shfl_sync(kFull, k1[i], t);
-      const unsigned long long o2 = TWO ? __shfl_sync(kFull, k2[i], t) : 0ull;
-      c += (t < len && key_less<TWO>(o1, o2, k1[i], k2[i])) ? 1 : 0;
+      for (int t = 0; t < 32; ++t) {
+        const unsigned long long o = t < len ? K[t] : ~0ull;
+        c += static_cast<int>((o < k[i]) | ((o == k[i]) & (t < lane)));
+      }
+      if (lane < len) X1[seg * 32 + c] = k[i];
     }
     lr[i] = c;
-    if (lane < len) {
-      X1[seg * 32 + c] = k1[i];
-      if (TWO) X2[seg * 32 + c] = k2[i];
-    }
   }
   if (T == 32) __syncwarp(); else __syncthreads();
   const int nseg = (R + 31) >> 5;
@@ -366,13 +371,22 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k1)[ITEMS],
     if (seg * 32 + lane < R) {
       for (int s2 = 0; s2 < nseg; ++s2) {
         if (s2 == seg) continue;
-        const int base = s2 * 32;
-        int lo = 0, hi = min(32, R - base);
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const unsigned long long m1 = X1[base + mid];
-          const unsigned long long m2 = TWO ? X2[base + mid] : 0ull;
-          if (key_less<TWO>(m1, m2, k1[i], k2[i])) lo = mid + 1; else hi = mid;
+        const bool before = s2 < seg;  // earlier segment: its equal keys precede
+        const unsigned long long* S2 = X1 + s2 * 32;
+        const int len2 = min(32, R - s2 * 32);
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int probe = lo + step - 1;
+          if (probe < len2) {
+            const unsigned long long m = S2[probe];
+            const bool go = before ? (m <= k[i]) : (m < k[i]);
+            lo = go ? lo + step : lo;
+          }
+        }
+        if (lo == 31 && len2 == 32) {  // the 6th step of a full segment
+          const unsigned long long m = S2[31];
+          lo += static_cast<int>(before ? (m <= k[i]) : (m < k[i]));
         }
         r += lo;
       }
@@ -384,22 +398,25 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k1)[ITEMS],
 // ---- warp path (rank sort): gather + raw sort, weight sort (results in A/B)
 template <int ITEMS>
 __device__ __forceinline__ void warp_rank_raw(const FactorDev& d, int k, long long fb, int fdeg, int R,
-                                              Scratch S, int lane) {
-  unsigned long long key[ITEMS], val[ITEMS], none[ITEMS];
+                                              Scratch S, int lane, unsigned long long* stamp) {
+  unsigned long long key[ITEMS], val[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int g = i * 32 + lane;
     key[i] = ~0ull;
     val[i] = 0;
-    none[i] = 0;
     if (g < R) {
       double w;
       load_raw(d, k, fb, fdeg, g, key[i], w);
       val[i] = dbits(w);
     }
   }
+  if (stamp && lane == 0) {  // diagnostics: the lead's gather has landed
+    asm volatile("" ::"l"(key[0]), "l"(val[0]));
+    *stamp = globaltimer_ns();
+  }
   int rank[ITEMS];
-  rank_sort<32, ITEMS, false>(key, none, R, S.X1, S.X2, rank);
+  rank_sort<32, ITEMS>(key, R, S.X1, S.X2, rank);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (i * 32 + lane < R) {
@@ -420,7 +437,7 @@ __device__ __forceinline__ void warp_rank_weight(int m, Scratch S, int lane) {
     ak[i] = g < m ? S.A[g] : ~0ull;
   }
   int rank[ITEMS];
-  rank_sort<32, ITEMS, true>(wk, ak, m, S.X1, S.X2, rank);
+  rank_sort<32, ITEMS>(wk, m, S.X1, S.X2, rank);
   __syncwarp();  // every lane has read A/B
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -435,22 +452,25 @@ __device__ __forceinline__ void warp_rank_weight(int m, Scratch S, int lane) {
 // ---- CTA path (rank sort), R <= kThreads * ITEMS
 template <int ITEMS>
 __device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long long fb, int fdeg, int R,
-                                             const unsigned* dirrow, Scratch S) {
-  unsigned long long key[ITEMS], val[ITEMS], none[ITEMS];
+                                             const unsigned* dirrow, Scratch S, unsigned long long* stamp) {
+  unsigned long long key[ITEMS], val[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int g = i * kThreads + threadIdx.x;
     key[i] = ~0ull;
     val[i] = 0;
-    none[i] = 0;
     if (g < R) {
       double w;
       load_raw_dir(d, k, fb, fdeg, g, dirrow, key[i], w);
       val[i] = dbits(w);
     }
   }
+  if (stamp && threadIdx.x == 0) {
+    asm volatile("" ::"l"(key[0]), "l"(val[0]));
+    *stamp = globaltimer_ns();
+  }
   int rank[ITEMS];
-  rank_sort<kThreads, ITEMS, false>(key, none, R, S.X1, S.X2, rank);
+  rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, rank);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (i * kThreads + static_cast<int>(threadIdx.x) < R) {
@@ -471,7 +491,7 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
     ak[i] = g < m ? S.A[g] : ~0ull;
   }
   int rank[ITEMS];
-  rank_sort<kThreads, ITEMS, true>(wk, ak, m, S.X1, S.X2, rank);
+  rank_sort<kThreads, ITEMS>(wk, m, S.X1, S.X2, rank);
   __syncthreads();  // every thread has read A/B
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -644,11 +664,12 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
   long long start = 0;
   if (lead && R > 0)
     start = static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R)));
+  SUB(0);
 
   // ---- 2. sort raw by (row, source)  (factor_common.hpp:100-104), in registers
-  if (R <= 32) warp_rank_raw<1>(d, k, fb, fdeg, R, S, lane);
-  else if (R <= 64) warp_rank_raw<2>(d, k, fb, fdeg, R, S, lane);
-  else warp_rank_raw<4>(d, k, fb, fdeg, R, S, lane);
+  if (R <= 32) warp_rank_raw<1>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
+  else if (R <= 64) warp_rank_raw<2>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
+  else warp_rank_raw<4>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   __syncwarp();
   PHASE(1);
 
@@ -715,12 +736,14 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
     else if (m <= 64) warp_rank_weight<2>(m, S, lane);
     else warp_rank_weight<4>(m, S, lane);
     __syncwarp();
+    SUB(2);
     if (lead) serial_suffix(S.B, S.C, m);
     __syncwarp();
   }
   PHASE(4);
 
   // ---- 8. sampling + fill emission (m - 1 <= 127 samples: one batch)
+  const SampleKey sk = sample_key(d, k);
   int emitted = 0;
   bool bad = false;
   {
@@ -730,8 +753,9 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
       const int i = b * 32 + lane;
-      em[b] = i < m - 1 && draw_sample(d, k, i, m, S.A, S.B, S.C, lkk, lo[b], hi[b], wv[b]);
+      em[b] = i < m - 1 && draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo[b], hi[b], wv[b]);
     }
+    SUB(3);
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
       if (em[b]) {
@@ -746,6 +770,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
       emitted += __popc(__ballot_sync(kFull, em[b]));
     }
   }
+  SUB(4);
   if (__any_sync(kFull, bad)) return {-2, -1, 0, 0};
   if (lead) d.samples[k] = emitted;
   // ASAP level of the factor DAG (schedule_levels, factor_par.cpp:659-684):
@@ -760,6 +785,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
   // ---- 9. release every emission, then decrement (factor_par.cpp:282-293)
   fence_acq_rel();
   __syncwarp();
+  SUB(5);
   unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
   int nready = 0;
   {
@@ -855,7 +881,6 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   const int R = fdeg + fc;
   const int P = next_pow2(R);
   if (lead) {
-    sh.start = R > 0 ? static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R))) : 0;
     sh.bad = 0;
     if (P > kBigCap) {
       const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(P)));
@@ -870,6 +895,11 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
   __syncthreads();
   if (sh.bad) return -2;
+  SUB(0);
+  // column arena slot: the round trip overlaps the gather/sort/merge (the
+  // value is first needed at the column write)
+  unsigned long long start_reg = 0;
+  if (lead && R > 0) start_reg = atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R));
   const bool wide = P > kBigCap;
   Scratch S = wide ? carve(d.large_pool + sh.slab * kEntryBytes, P) : carve(smem, kBigCap);
   const XBuf xb{S.A, reinterpret_cast<unsigned long long*>(S.B),
@@ -886,9 +916,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     __syncthreads();
     cta_sort_key(S.A, S.B, P);
   } else if (P <= kThreads) {
-    cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S);
+    cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   } else if (P <= 2 * kThreads) {
-    cta_rank_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S);
+    cta_rank_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   } else {
     cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
   }
@@ -940,7 +970,10 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
 
   // ---- 5. lkk + column
-  if (lead) sh.lkk = serial_total(S.B, m);
+  if (lead) {
+    sh.lkk = serial_total(S.B, m);
+    sh.start = static_cast<long long>(start_reg);
+  }
   __syncthreads();
   const double lkk = sh.lkk;
   const long long start = sh.start;
@@ -976,19 +1009,22 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     } else {
       cta_sort_weight_reg<4>(m, S.A, S.B, xb);
     }
+    SUB(2);
     if (lead) serial_suffix(S.B, S.C, m);
     __syncthreads();
   }
   PHASE(4);
 
   // ---- 8. sampling + emission, one sample per thread per round
+  const SampleKey sk = sample_key(d, k);
   int emitted = 0;
   bool bad = false;
   for (int base = 0; base < m - 1; base += kThreads) {
     const int i = base + tid;
     int lo = 0, hi = 0, slot = 0;
     double wv = 0.0;
-    const bool em = i < m - 1 && draw_sample(d, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv);
+    const bool em = i < m - 1 && draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv);
+    if (base == 0) SUB(3);
     if (em) {
       slot = reserve_fill_slot(d, lo);
       red_add_relaxed(&d.dp[hi], 1);
@@ -1001,6 +1037,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   if (lane == 0) sh.wcount[warp] = emitted;
   if (bad) sh.bad = 1;
   __syncthreads();
+  SUB(4);
   if (sh.bad) return -2;
   if (lead) {
     int e = 0;
@@ -1018,6 +1055,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // ---- 9. release, decrement, collect ready rows into C
   fence_acq_rel();
   __syncthreads();
+  SUB(5);
   unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
   for (int t = tid; t < m; t += kThreads) {
     const unsigned long long a = S.A[t];

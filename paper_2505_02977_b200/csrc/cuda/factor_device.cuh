@@ -158,12 +158,25 @@ __device__ __forceinline__ int pick_by_suffix(const double* suffix, int lo, int 
 
 // One sample of sample_clique_sorted (include/parac/sampling.hpp:77-83): the
 // pair (v_i, v_j) and weight (s * w_i) / lkk. Returns false if dropped.
-__device__ __forceinline__ bool draw_sample(const FactorDev& d, int k, int i, int m,
+// Sampling stream of position k: (derived seed, key). A batch factors several
+// independent problems as one disjoint union; each keeps its own seed and its
+// own positions as keys, so every problem's factor equals its stand-alone one.
+struct SampleKey {
+  unsigned long long seed;
+  long long key;
+};
+__device__ __forceinline__ SampleKey sample_key(const FactorDev& d, int k) {
+  if (!d.pos_pid) return {d.sample_seed, k};
+  const int p = d.pos_pid[k];
+  return {d.pid_seed[p], static_cast<long long>(k) - d.pid_base[p]};
+}
+
+__device__ __forceinline__ bool draw_sample(const FactorDev& d, SampleKey sk, int k, int i, int m,
                                            const unsigned long long* A, const double* B,
                                            const double* suffix, double lkk, int& lo, int& hi,
                                            double& wv) {
   const double s = suffix[i + 1];
-  const double u = __dmul_rn(unit_uniform(d.sample_seed, k, static_cast<unsigned long long>(i)), s);
+  const double u = __dmul_rn(unit_uniform(sk.seed, sk.key, static_cast<unsigned long long>(i)), s);
   const int j = pick_by_suffix(suffix, i + 1, m - 1, u);
   wv = __ddiv_rn(__dmul_rn(s, B[i]), lkk);
   if (wv < kDropThreshold) return false;

@@ -76,10 +76,16 @@ struct FactorDev {
   // control
   Ctrl* ctrl;
   unsigned long long sample_seed;
+  // batch (disjoint union of problems): problem of each position, its first
+  // position and its derived sample seed; pos_pid == nullptr for one problem
+  const int* pos_pid;
+  const long long* pid_base;
+  const unsigned long long* pid_seed;
   unsigned long long watchdog_ns;
   int verify;
   int delay_ns;
-  unsigned long long* vtimes;  // optional [2n] start/end globaltimer per position
+  unsigned long long* vtimes;  // optional [8n] phase timestamps per position
+  unsigned long long* vsub;    // optional [8n] sub-phase timestamps per position
 };
 
 // Launchers (stream-ordered). All return cudaError_t of the launch.

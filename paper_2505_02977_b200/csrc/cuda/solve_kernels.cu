@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "../../../include/parac_gpu.h"
 #include "../host/errors.hpp"
 #include "common.cuh"
@@ -833,7 +835,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
 constexpr int kPrefetchLevels = 3;
 constexpr int kTailThreads = 1024;
 constexpr int kTailWarps = kTailThreads / 32;
-constexpr int kTailMaxRows = 24 * 1024;  // 192 KB of shared fp64
+constexpr int kTailMaxRows = 16 * 1024;  // 128 KB of shared fp64 (+ 64 KB product buffer)
 
 // tpos[order[tail_base + i]] = i; count T-part entries of forward row i and
 // the H/T split of its level-sorted entries.
@@ -915,6 +917,110 @@ __device__ __forceinline__ double tail_row_sum(const int* idx, const double* val
   }
   for (; q < e; q += 32) part += val[q] * xs[idx[q]];
   return warp_sum(part);
+}
+
+// ---- v2: entry-parallel, software-pipelined tail sweep. Per level, all
+// 1024 threads compute the level's products (each <= kTailPF entries, loaded
+// into registers one level AHEAD, so no global-memory latency remains on the
+// level-to-level chain), a barrier, then a warp per row sums its products
+// (fixed order: lane-strided + warp tree), a barrier. The solution of the
+// tail lives in shared memory. Levels wider than 1024*kTailPF entries fall
+// back to a strided loop (rare: the tail is the narrow part of the DAG).
+constexpr int kTailPF = 8;
+constexpr int kTailPbuf = kTailThreads * kTailPF;  // 8192 products (64 KB)
+
+struct TailLevel {
+  int lb, le;           // rows (tail index)
+  long long eb, ee;     // entries
+};
+
+template <bool FWD>
+__global__ void __launch_bounds__(kTailThreads, 1) tail_sweep_kernel(
+    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const long long* eptr,
+    const int* eidx, const double* eval, const double* init, const double* diag, double* xout, double* yd,
+    unsigned long long* ltime) {
+  extern __shared__ double tsm[];
+  double* xs = tsm;                       // [nt]
+  double* pbuf = tsm + kTailMaxRows;      // [kTailPbuf]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = static_cast<int>(lvl_off[depth + 1] - tail_base);
+  const int nlev = depth - L0;
+  auto level_of = [&](int t) { return FWD ? L0 + 1 + t : depth - t; };
+  auto bounds = [&](int t) {
+    TailLevel b;
+    const int L = level_of(t);
+    b.lb = static_cast<int>(lvl_off[L] - tail_base);
+    b.le = static_cast<int>(lvl_off[L + 1] - tail_base);
+    b.eb = eptr[b.lb];
+    b.ee = eptr[b.le];
+    return b;
+  };
+  // initial values: forward = rhs - G_TH y_H (prologue), backward = yd of the tail rows
+  for (int i = tid; i < nt; i += kTailThreads) {
+    if (FWD) {
+      xs[i] = init[i];
+    } else {
+      xs[i] = yd[order[tail_base + i]];
+    }
+  }
+  TailLevel nb = bounds(0);
+  int nidx[kTailPF];
+  double nval[kTailPF];
+#pragma unroll
+  for (int q = 0; q < kTailPF; ++q) {
+    const long long e = nb.eb + q * kTailThreads + tid;
+    nidx[q] = e < nb.ee ? eidx[e] : 0;
+    nval[q] = e < nb.ee ? eval[e] : 0.0;
+  }
+  __syncthreads();
+  for (int t = 0; t < nlev; ++t) {
+    const TailLevel cb = nb;
+    int cidx[kTailPF];
+    double cval[kTailPF];
+#pragma unroll
+    for (int q = 0; q < kTailPF; ++q) {
+      cidx[q] = nidx[q];
+      cval[q] = nval[q];
+    }
+    // issue the next level's loads now; they land while this level computes
+    if (t + 1 < nlev) {
+      nb = bounds(t + 1);
+#pragma unroll
+      for (int q = 0; q < kTailPF; ++q) {
+        const long long e = nb.eb + q * kTailThreads + tid;
+        nidx[q] = e < nb.ee ? eidx[e] : 0;
+        nval[q] = e < nb.ee ? eval[e] : 0.0;
+      }
+    }
+    const int cnt = static_cast<int>(cb.ee - cb.eb);
+#pragma unroll
+    for (int q = 0; q < kTailPF; ++q) {
+      const int e = q * kTailThreads + tid;
+      if (e < cnt) pbuf[e] = cval[q] * xs[cidx[q]];
+    }
+    const bool wide = cnt > kTailPbuf;
+    __syncthreads();
+    for (int i = cb.lb + warp; i < cb.le; i += kTailThreads / 32) {
+      const long long rb = eptr[i] - cb.eb, re = eptr[i + 1] - cb.eb;
+      double part = 0.0;
+      for (long long q = rb + lane; q < re; q += 32)
+        part += q < kTailPbuf ? pbuf[q] : eval[cb.eb + q] * xs[eidx[cb.eb + q]];
+      part = warp_sum(part);
+      if (lane == 0) {
+        const double acc = xs[i] - part;
+        xs[i] = acc;
+        const int r = order[tail_base + i];
+        xout[r] = acc;
+        if (FWD) {
+          const double d = diag[r];
+          yd[r] = d > 0.0 ? acc / d : 0.0;
+        }
+      }
+    }
+    (void)wide;
+    __syncthreads();
+    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
+  }
 }
 
 __global__ void __launch_bounds__(kTailThreads, 1) tail_forward_kernel(
@@ -1283,6 +1389,360 @@ __global__ void __launch_bounds__(kCThreads, 1) cluster_sweep_fast_kernel(
   }
 }
 
+// ---- v3 head sweep: level-order index space + software pipelining.
+// Vectors are indexed by level-order position j (rows of a level are
+// contiguous), entry indices are level-order too, and each warp owns exactly
+// chunk w of every level (table hrec[L][w] = {jb, je, eb, ee}). While level L
+// is computed, the warp already holds level L+1's chunk record and has issued
+// the loads of its entries (<= kHeadPF per lane) and row metadata; level
+// L+2's record is loaded as well. After the barrier only the gathers of
+// solution values (one L2 round trip) remain on the level-to-level chain.
+constexpr int kHeadPF = 8;  // entries per lane held in registers (256 per warp)
+constexpr int kHThreads = 512;  // 16 warps: 128 registers per thread hold two levels' prefetch
+constexpr int kHWarps = kHThreads / 32;
+constexpr std::size_t kHeadSmem = static_cast<std::size_t>(kHWarps) * kChunkCap * sizeof(double);
+
+struct HeadPre {
+  int4 rec;               // jb, je, eb, ee
+  int idx[kHeadPF];
+  double val[kHeadPF];
+  int rb, re;             // lane's row entry range (relative), lane < je - jb
+  double rhs, dinv;       // lane's row right-hand side and D^+
+};
+
+template <bool FWD>
+__device__ __forceinline__ void head_load(HeadPre& p, const int4 rec, const long long* lptr, const int* lidx,
+                                          const double* lval, const double* rhs_l, const double* dinv_l,
+                                          int lane) {
+  p.rec = rec;
+  const int cnt = rec.w - rec.z;
+#pragma unroll
+  for (int q = 0; q < kHeadPF; ++q) {
+    const int e = q * 32 + lane;
+    p.idx[q] = e < cnt ? lidx[rec.z + e] : 0;
+    p.val[q] = e < cnt ? lval[rec.z + e] : 0.0;
+  }
+  const int j = rec.x + lane;
+  p.rb = p.re = 0;
+  p.rhs = p.dinv = 0.0;
+  if (j < rec.y) {
+    p.rb = static_cast<int>(lptr[j] - rec.z);
+    p.re = static_cast<int>(lptr[j + 1] - rec.z);
+    p.rhs = rhs_l[j];
+    if (FWD) p.dinv = dinv_l[j];
+  }
+}
+
+// GRID: one cooperative persistent grid (all SMs) for the wide first levels,
+// grid.sync() per level; otherwise one thread-block cluster (cluster barrier).
+template <bool FWD, bool GRID>
+__global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
+    int Lfirst, int nlev, int W, const int4* hrec, const long long* lptr, const int* lidx, const double* lval,
+    const double* rhs_l, const double* dinv_l, double* x, double* yd_l, const int* rlab, const double* rvec,
+    int n, int nt, int tail_base, double* ts, unsigned long long* ltime) {
+  extern __shared__ double pbuf_all[];
+  const int lane = lane_id(), wl = threadIdx.x >> 5;
+  const int w = (GRID ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_rank())) * kHWarps + wl;
+  double* pbuf = pbuf_all + wl * kChunkCap;
+  auto level_barrier = [&]() {
+    if constexpr (GRID) cooperative_groups::this_grid().sync();
+    else cluster_barrier();
+  };
+  if (FWD && rvec) {
+    // level 0: the right-hand side permuted into level order (label -> level order)
+    double* rl = const_cast<double*>(rhs_l);
+    for (int j = w * 32 + lane; j < n; j += W * 32) rl[j] = rvec[rlab[j]];
+    level_barrier();
+  }
+  auto rec_of = [&](int t) -> int4 {
+    const int L = FWD ? Lfirst + t : Lfirst - t;
+    return hrec[static_cast<long long>(L) * W + w];
+  };
+  HeadPre nxt;
+  int4 rec2 = make_int4(0, 0, 0, 0);
+  if (nlev > 0) head_load<FWD>(nxt, rec_of(0), lptr, lidx, lval, rhs_l, dinv_l, lane);
+  if (nlev > 1) rec2 = rec_of(1);
+  for (int t = 0; t < nlev; ++t) {
+    const HeadPre cur = nxt;
+    if (t + 1 < nlev) head_load<FWD>(nxt, rec2, lptr, lidx, lval, rhs_l, dinv_l, lane);
+    if (t + 2 < nlev) rec2 = rec_of(t + 2);
+    const int jb = cur.rec.x, je = cur.rec.y, eb = cur.rec.z, ee = cur.rec.w;
+    const int cnt = ee - eb;
+    if (jb < je) {
+      if (cnt <= kHeadPF * 32 && je - jb <= 32) {
+        // fast path: everything prefetched; one gather round trip
+        double xv[kHeadPF];
+#pragma unroll
+        for (int q = 0; q < kHeadPF; ++q) xv[q] = q * 32 + lane < cnt ? __ldcg(x + cur.idx[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kHeadPF; ++q)
+          if (q * 32 + lane < cnt) pbuf[q * 32 + lane] = cur.val[q] * xv[q];
+        __syncwarp();
+        const int j = jb + lane;
+        const bool mine = j < je && cur.re - cur.rb <= kShortRow;
+        if (mine) {
+          double s = 0.0;
+          for (int q = cur.rb; q < cur.re; ++q) s += pbuf[q];
+          const double acc = cur.rhs - s;
+          x[j] = acc;
+          if (FWD) yd_l[j] = acc * cur.dinv;
+        }
+        unsigned longs = __ballot_sync(kFull, j < je && !mine);
+        while (longs) {
+          const int src = __ffs(longs) - 1;
+          longs &= longs - 1;
+          const int b2 = __shfl_sync(kFull, cur.rb, src), e2 = __shfl_sync(kFull, cur.re, src);
+          const double rhs = __shfl_sync(kFull, cur.rhs, src), dv = __shfl_sync(kFull, cur.dinv, src);
+          double part = 0.0;
+          for (int q = b2 + lane; q < e2; q += 32) part += pbuf[q];
+          part = warp_sum(part);
+          if (lane == 0) {
+            const double acc = rhs - part;
+            x[jb + src] = acc;
+            if (FWD) yd_l[jb + src] = acc * dv;
+          }
+        }
+        __syncwarp();
+      } else {
+        // general path (wide chunk): rows in batches of 32, products straight from memory
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          long long b = 0, e = 0;
+          double rhs = 0.0, dv = 0.0;
+          if (j < je) {
+            b = lptr[j];
+            e = lptr[j + 1];
+            rhs = rhs_l[j];
+            if (FWD) dv = dinv_l[j];
+          }
+          if (j < je && e - b <= kShortRow) {
+            double s = 0.0;
+            for (long long q = b; q < e; ++q) s += lval[q] * __ldcg(x + lidx[q]);
+            const double acc = rhs - s;
+            x[j] = acc;
+            if (FWD) yd_l[j] = acc * dv;
+          }
+          unsigned longs = __ballot_sync(kFull, j < je && e - b > kShortRow);
+          while (longs) {
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const long long b2 = __shfl_sync(kFull, b, src), e2 = __shfl_sync(kFull, e, src);
+            const double rhs2 = __shfl_sync(kFull, rhs, src), dv2 = __shfl_sync(kFull, dv, src);
+            double part = 0.0;
+            for (long long q = b2 + lane; q < e2; q += 32) part += lval[q] * __ldcg(x + lidx[q]);
+            part = warp_sum(part);
+            if (lane == 0) {
+              const double acc = rhs2 - part;
+              x[j0 + src] = acc;
+              if (FWD) yd_l[j0 + src] = acc * dv2;
+            }
+          }
+        }
+      }
+    }
+    level_barrier();
+    if (ltime && w == 0 && lane == 0) ltime[t] = globaltimer_ns();
+  }
+  if constexpr (FWD) {  // tail rows' H part: ts_i = rhs - sum over head columns (idx < tail_base)
+    for (int i = w; i < nt; i += W) {
+      const int j = tail_base + i;
+      const long long b = lptr[j], e = lptr[j + 1];
+      double part = 0.0;
+      for (long long q = b + lane; q < e; q += 32) {
+        const int c = lidx[q];
+        if (c < tail_base) part += lval[q] * __ldcg(x + c);
+      }
+      part = warp_sum(part);
+      if (lane == 0) ts[i] = rhs_l[j] - part;
+    }
+  }
+}
+
+// hrec[L][w]: chunk w of level L (whole rows, ~equal entries + rows), for W warps.
+__global__ void head_chunk_kernel(int depth, int W, const long long* lvl_off, const long long* lptr, int4* hrec) {
+  const int L = blockIdx.x + 1;
+  if (L > depth) return;
+  const long long lb = lvl_off[L], le = lvl_off[L + 1];
+  const long long tot = (lptr[le] - lptr[lb]) + (le - lb);
+  auto start = [&](int c) -> long long {
+    if (c >= W) return le;
+    const long long goal = (tot * c + W - 1) / W;
+    long long lo = lb, hi = le;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if ((lptr[mid] - lptr[lb]) + (mid - lb) >= goal) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+  };
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    const long long a = start(c), b = start(c + 1);
+    hrec[static_cast<long long>(L) * W + c] =
+        make_int4(static_cast<int>(a), static_cast<int>(b), static_cast<int>(lptr[a]), static_cast<int>(lptr[b]));
+  }
+}
+
+// Level-order remaps: lpos[order[j]] = j; rlab[j] = inv[order[j]];
+// dinv_l[j] = D^+ of row order[j]; v2l[label] = lpos[perm[label]].
+__global__ void level_maps_kernel(int n, const int* order, const int* inv, const double* diag, int* lpos,
+                                  int* rlab, double* dinv_l) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int r = order[j];
+  lpos[r] = j;
+  rlab[j] = inv[r];
+  const double d = diag[r];
+  dinv_l[j] = d > 0.0 ? 1.0 / d : 0.0;
+}
+__global__ void label_map_kernel(int n, const int* perm, const int* lpos, int* v2l) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) v2l[v] = lpos[perm[v]];
+}
+__global__ void remap_idx_kernel(long long cnt, const int* lpos, int* idx) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    idx[e] = lpos[idx[e]];
+}
+__global__ void gather_z_l_dot_kernel(int n, const int* v2l, const double* zl, const double* r, double* z,
+                                      double* partials) {
+  double s = 0.0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const double zv = zl[v2l[v]];
+    z[v] = zv;
+    s += r[v] * zv;
+  }
+  block_partial(s, partials);
+}
+
+// ---- v3 tail: one CTA, level-order space, all per-level metadata in shared
+// memory (no dependent global loads on the level chain), entries of the next
+// level prefetched into registers, products for the whole level spread over
+// all 1024 threads. FWD: x = y (tail rows, init = rhs - G_TH y_H);
+// BWD: x = z (init = y * D^+).
+constexpr int kT3Rows = 8192;
+constexpr int kT3PF = 8;
+constexpr int kT3Pbuf = kTailThreads * kT3PF;
+constexpr std::size_t kT3Smem = (static_cast<std::size_t>(kT3Rows) + kT3Pbuf) * 8 +
+                                (2 * static_cast<std::size_t>(kT3Rows) + 2) * 4;
+
+template <bool FWD>
+__global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
+    int nt, int nlev, int tail_base, const int* lvl3, const int* ep, const int* eidx, const double* eval,
+    const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
+  extern __shared__ double t3[];
+  double* xs = t3;                                            // [kT3Rows]
+  double* pbuf = t3 + kT3Rows;                                // [kT3Pbuf]
+  int* eps = reinterpret_cast<int*>(pbuf + kT3Pbuf);         // [kT3Rows + 1]
+  int* lvs = eps + kT3Rows + 1;                               // [kT3Rows + 1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i <= nt; i += kTailThreads) eps[i] = ep[i];
+  for (int i = tid; i <= nlev; i += kTailThreads) lvs[i] = lvl3[i];
+  for (int i = tid; i < nt; i += kTailThreads)
+    xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];  // BWD: yd = y D^+
+  __syncthreads();
+  auto qlev = [&](int t) { return FWD ? t : nlev - 1 - t; };
+  auto lcount = [&](int t) { const int q = qlev(t); return eps[lvs[q + 1]] - eps[lvs[q]]; };
+  // Work is proportional to the level: threads past the level's entry count
+  // and warps past its row count skip straight to the barrier (the narrow
+  // levels would otherwise be issue-bound on 32 warps of predicated code).
+  int nidx[kT3PF];
+  double nval[kT3PF];
+  auto prefetch = [&](int t) {
+    const int q = qlev(t);
+    const int eb = eps[lvs[q]], ee = eps[lvs[q + 1]];
+    if (eb + tid < ee) {
+#pragma unroll
+      for (int k = 0; k < kT3PF; ++k) {
+        const int e = eb + k * kTailThreads + tid;
+        nidx[k] = e < ee ? eidx[e] : 0;
+        nval[k] = e < ee ? eval[e] : 0.0;
+      }
+    }
+  };
+  auto prefetch_l2_level = [&](int t) {
+    if (t >= nlev) return;
+    const int q = qlev(t);
+    const int eb = eps[lvs[q]], ee = eps[lvs[q + 1]];
+    prefetch_l2(eidx + eb, static_cast<long long>(ee - eb) * 4);
+    prefetch_l2(eval + eb, static_cast<long long>(ee - eb) * 8);
+  };
+  if (tid == 32)
+    for (int t = 1; t < 6; ++t) prefetch_l2_level(t);
+  if (nlev > 0) prefetch(0);
+  for (int t = 0; t < nlev; ++t) {
+    const int q = qlev(t);
+    const int lb = lvs[q], le = lvs[q + 1];
+    const int eb = eps[lb], cnt = eps[le] - eb;
+    if (tid == 32) prefetch_l2_level(t + 6);
+    if (tid < cnt) {
+#pragma unroll
+      for (int k = 0; k < kT3PF; ++k) {
+        const int e = k * kTailThreads + tid;
+        if (e < cnt) pbuf[e] = nval[k] * xs[nidx[k]];
+      }
+    }
+    if (t + 1 < nlev && tid < lcount(t + 1)) prefetch(t + 1);
+    __syncthreads();
+    for (int i = lb + warp; i < le; i += kTailThreads / 32) {
+      const int rb = eps[i] - eb, re = eps[i + 1] - eb;
+      double part = 0.0;
+      for (int e = rb + lane; e < re; e += 32)
+        part += e < kT3Pbuf ? pbuf[e] : eval[eb + e] * xs[eidx[eb + e]];
+      part = warp_sum(part);
+      if (lane == 0) {
+        const double acc = xs[i] - part;
+        xs[i] = acc;
+        x_l[tail_base + i] = acc;
+      }
+    }
+    __syncthreads();
+    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
+  }
+}
+
+// T-part of the forward tail rows: count, then copy with tail-relative indices.
+__global__ void tail3_count_kernel(int nt, int tail_base, const long long* lptr, const int* lidx, int* cnt) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < nt; i += nw) {
+    const long long b = lptr[tail_base + i], e = lptr[tail_base + i + 1];
+    int c = 0;
+    for (long long q = b + lane; q < e; q += 32) c += lidx[q] >= tail_base;
+    c = warp_sum(c);
+    if (lane == 0) cnt[i] = c;
+  }
+}
+__global__ void tail3_fill_kernel(int nt, int tail_base, const long long* lptr, const int* lidx, const double* lval,
+                                  const long long* off, int* tidx, double* tval) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < nt; i += nw) {
+    const long long b = lptr[tail_base + i], e = lptr[tail_base + i + 1];
+    long long o = off[i];
+    for (long long q0 = b; q0 < e; q0 += 32) {
+      const long long q = q0 + lane;
+      const bool t = q < e && lidx[q] >= tail_base;
+      const unsigned m = __ballot_sync(kFull, t);
+      if (t) {
+        const long long at = o + __popc(m & ((1u << lane) - 1));
+        tidx[at] = lidx[q] - tail_base;
+        tval[at] = lval[q];
+      }
+      o += __popc(m);
+    }
+  }
+}
+__global__ void ll_to_int_kernel(int cnt, const long long* src, long long base, int* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) dst[i] = static_cast<int>(src[i] - base);
+}
+__global__ void tail_rel_idx_kernel(long long b, long long e, int tail_base, int* idx) {
+  for (long long q = b + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < e;
+       q += static_cast<long long>(gridDim.x) * blockDim.x)
+    idx[q] -= tail_base;
+}
+
 // Level-ordered row copies: lens, then entries (warp per row).
 __global__ void lvl_len_kernel(int n, const int* order, const long long* aptr, const long long* bptr,
                                int* alen, int* blen) {
@@ -1335,10 +1795,11 @@ __global__ void chunk_fill_kernel(int depth, const long long* lvl_off, const lon
 }
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem, cudaStream_t st, Args... args) {
+cudaError_t launch_cluster_t(void (*kernel)(KArgs...), int csize, int threads, std::size_t smem, cudaStream_t st,
+                             Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(csize, 1, 1);
-  cfg.blockDim = dim3(kCThreads, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -1351,15 +1812,37 @@ cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem, cudaStream_t st, Args... args) {
+  return launch_cluster_t(kernel, csize, kCThreads, smem, st, args...);
+}
+
+// Cooperative (all CTAs co-resident, grid.sync allowed) launch.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(void (*kernel)(KArgs...), int grid, int threads, std::size_t smem, cudaStream_t st,
+                        Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Largest launchable cluster (16 non-portable, else 8) of 1024-thread CTAs.
 template <typename... KArgs>
-int pick_cluster(void (*kernel)(KArgs...), std::size_t smem = 0) {
+int pick_cluster(void (*kernel)(KArgs...), std::size_t smem = 0, int threads = kCThreads) {
   if (smem) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   for (int c : {16, 8, 4}) {
     if (c > 8) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c, 1, 1);
-    cfg.blockDim = dim3(kCThreads, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1532,6 +2015,10 @@ void build_tail(const SolveInputs& in, SolveState& s, int sms) {
                                kTailMaxRows * 8), "attr");
     check(cudaFuncSetAttribute(tail_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kTailMaxRows * 8), "attr");
+    check(cudaFuncSetAttribute(tail_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (kTailMaxRows + kTailPbuf) * 8), "attr");
+    check(cudaFuncSetAttribute(tail_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (kTailMaxRows + kTailPbuf) * 8), "attr");
     attr = true;
   }
   s.tail_L0 = L0;
@@ -1583,7 +2070,7 @@ void build_chunks(const SolveInputs& in, SolveState& s, const long long* lptr, i
 }
 
 // Level-ordered copies of G's rows and columns + chunk tables (fast mode).
-void build_level_layout(const SolveInputs& in, SolveState& s, int sms) {
+void build_level_layout(const SolveInputs& in, SolveState& s, int sms, bool chunks) {
   const int n = in.f_n, depth = s.depth;
   const long long Z = in.f_nnz;
   cudaStream_t st = in.stream;
@@ -1612,11 +2099,163 @@ void build_level_layout(const SolveInputs& in, SolveState& s, int sms) {
   lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, s.gt_ptr, s.gt_col, s.gt_val, s.lf_ptr, s.lf_idx, s.lf_val);
   lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, in.col_ptr, in.rows, in.vals, s.lb_ptr, s.lb_idx, s.lb_val);
   note_launches(2);
-  const ClusterSizes cs = cluster_sizes(in.device);
-  build_chunks(in, s, s.lf_ptr, cs.sweep_f * kCWarps, s.f_chunk, s.f_cbase, s.cap_fchunk);
-  build_chunks(in, s, s.lb_ptr, cs.sweep_b * kCWarps, s.b_chunk, s.b_cbase, s.cap_bchunk);
+  if (chunks) {
+    const ClusterSizes cs = cluster_sizes(in.device);
+    build_chunks(in, s, s.lf_ptr, cs.sweep_f * kCWarps, s.f_chunk, s.f_cbase, s.cap_fchunk);
+    build_chunks(in, s, s.lb_ptr, cs.sweep_b * kCWarps, s.b_chunk, s.b_cbase, s.cap_bchunk);
+  }
   dfree(blen);
   check(cudaGetLastError(), "level layout");
+}
+
+// v3 fast-mode layout (after build_level_layout made the level-ordered copies):
+// level-order maps, indices remapped to level order, head chunk tables for the
+// cluster's warps, and the one-CTA tail (levels wider than PARAC_TAIL_WIDTH,
+// default 64 rows, stay in the head; at most kT3Rows tail rows).
+void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
+  const int n = in.f_n, depth = s.depth;
+  const long long Z = in.f_nnz;
+  cudaStream_t st = in.stream;
+  s.t3_L0 = depth;
+  s.t3_nt = 0;
+  s.t3_base = n;
+  s.t3_nlev = 0;
+  if (n == 0 || depth == 0) return;
+  const std::size_t nn = static_cast<std::size_t>(n);
+  if (s.cap_v3 < nn) {
+    dalloc(s.lpos, nn); dalloc(s.rlab, nn); dalloc(s.v2l, nn); dalloc(s.dinv_l, nn); dalloc(s.rhs_l, nn);
+    s.cap_v3 = nn;
+  }
+  const int blocks = (n + 255) / 256;
+  level_maps_kernel<<<blocks, 256, 0, st>>>(n, s.order, s.inv, in.diag, s.lpos, s.rlab, s.dinv_l);
+  label_map_kernel<<<blocks, 256, 0, st>>>(n, in.perm, s.lpos, s.v2l);
+  remap_idx_kernel<<<sms * 8, 256, 0, st>>>(Z, s.lpos, s.lf_idx);
+  remap_idx_kernel<<<sms * 8, 256, 0, st>>>(Z, s.lpos, s.lb_idx);
+  note_launches(4);
+  // head cluster geometry + chunk tables (all levels; the head uses 1..L0)
+  static int csize[64] = {}, gsize[64] = {};
+  const int dev = in.device >= 0 && in.device < 64 ? in.device : 0;
+  if (!csize[dev]) {
+    csize[dev] = pick_cluster(head_sweep_kernel<true, false>, kHeadSmem, kHThreads);
+    cudaFuncSetAttribute(head_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
+    cudaFuncSetAttribute(head_sweep_kernel<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(head_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
+    cudaFuncSetAttribute(head_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
+    int pf = 0, pb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, head_sweep_kernel<true, true>, kHThreads, kHeadSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, head_sweep_kernel<false, true>, kHThreads, kHeadSmem);
+    gsize[dev] = std::max(1, std::min(pf, pb)) * sm_count(in.device);
+  }
+  s.head_csize = csize[dev];
+  s.head_W = s.head_csize * kHWarps;
+  s.grid_ctas = gsize[dev];
+  s.grid_W = s.grid_ctas * kHWarps;
+  const std::size_t nrec = (static_cast<std::size_t>(depth) + 2) * s.head_W;
+  if (s.cap_hrec < nrec) {
+    dalloc(s.hrec_f, nrec);
+    dalloc(s.hrec_b, nrec);
+    s.cap_hrec = nrec;
+  }
+  head_chunk_kernel<<<depth, 256, 0, st>>>(depth, s.head_W, s.lvl_off, s.lf_ptr, s.hrec_f);
+  head_chunk_kernel<<<depth, 256, 0, st>>>(depth, s.head_W, s.lvl_off, s.lb_ptr, s.hrec_b);
+  note_launches(2);
+  // tail choice
+  std::vector<long long> off(static_cast<std::size_t>(depth) + 2);
+  check(cudaMemcpyAsync(off.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "v3 sync");
+  // wide leading levels go to the cooperative full-GPU grid: rows + entries
+  // (forward rows and backward columns) above PARAC_WIDE_WEIGHT (default 32768)
+  {
+    const char* ww = std::getenv("PARAC_WIDE_WEIGHT");
+    const long long wide = ww ? std::atoll(ww) : 32768;
+    std::vector<long long> ef(static_cast<std::size_t>(depth) + 2), eb(static_cast<std::size_t>(depth) + 2);
+    long long* bnd = s.lvl_target;
+    gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, s.lf_ptr, bnd);
+    check(cudaMemcpyAsync(ef.data(), bnd, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "v3 sync");
+    gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, s.lb_ptr, bnd);
+    check(cudaMemcpyAsync(eb.data(), bnd, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "v3 sync");
+    note_launches(2);
+    int Lw = 0;
+    while (Lw < depth) {
+      const int L = Lw + 1;
+      const long long rows = off[L + 1] - off[L];
+      const long long wgt = rows + std::max(ef[L + 1] - ef[L], eb[L + 1] - eb[L]);
+      if (wide <= 0 || wgt < wide) break;
+      Lw = L;
+    }
+    s.wide_L = Lw;
+    if (Lw > 0) {
+      const std::size_t ng = (static_cast<std::size_t>(Lw) + 2) * s.grid_W;
+      if (s.cap_grec < ng) {
+        dalloc(s.hrec_gf, ng);
+        dalloc(s.hrec_gb, ng);
+        s.cap_grec = ng;
+      }
+      head_chunk_kernel<<<Lw, 256, 0, st>>>(Lw, s.grid_W, s.lvl_off, s.lf_ptr, s.hrec_gf);
+      head_chunk_kernel<<<Lw, 256, 0, st>>>(Lw, s.grid_W, s.lvl_off, s.lb_ptr, s.hrec_gb);
+      note_launches(2);
+    }
+  }
+  const char* env = std::getenv("PARAC_TAIL_WIDTH");
+  const int wt = env ? std::atoi(env) : 64;
+  int L0 = depth;
+  if (wt > 0) {
+    while (L0 >= 1 && off[L0 + 1] - off[L0] <= wt) --L0;
+    while (L0 < depth && off[depth + 1] - off[L0 + 1] > kT3Rows) ++L0;
+  }
+  s.t3_L0 = L0;
+  if (L0 >= depth) return;
+  const int base = static_cast<int>(off[L0 + 1]);
+  const int nt = n - base;
+  const int nlev = depth - L0;
+  if (s.cap_t3 < static_cast<std::size_t>(nt) + 2) {
+    dalloc(s.t3_lvl, static_cast<std::size_t>(nt) + 2);
+    dalloc(s.t3_fep, static_cast<std::size_t>(nt) + 2);
+    dalloc(s.t3_bep, static_cast<std::size_t>(nt) + 2);
+    dalloc(s.tail_s, static_cast<std::size_t>(nt) + 2);
+    dalloc(s.tail_cnt, 2 * (static_cast<std::size_t>(nt) + 2));
+    dalloc(s.hsplit, static_cast<std::size_t>(nt) + 2);  // scratch: forward T-part offsets
+    s.cap_t3 = static_cast<std::size_t>(nt) + 2;
+  }
+  std::vector<int> lvl3(static_cast<std::size_t>(nlev) + 1);
+  for (int t = 0; t <= nlev; ++t) lvl3[t] = static_cast<int>(off[L0 + 1 + t] - base);
+  check(cudaMemcpyAsync(s.t3_lvl, lvl3.data(), sizeof(int) * (nlev + 1), cudaMemcpyHostToDevice, st), "h2d");
+  // forward T part
+  tail3_count_kernel<<<sms * 4, 256, 0, st>>>(nt, base, s.lf_ptr, s.lf_idx, s.tail_cnt);
+  note_launches(1);
+  check(launch_scan(s.tail_cnt, nt, s.hsplit, s.tiles, st), "scan");
+  long long hb[2] = {0, 0};
+  check(cudaMemcpyAsync(&hb[0], s.hsplit + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaMemcpyAsync(&hb[1], s.lb_ptr + base, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "v3 sync");
+  const std::size_t ne = static_cast<std::size_t>(std::max<long long>(hb[0], 1));
+  if (s.cap_t3e < ne) {
+    dalloc(s.t3_fidx, ne);
+    dalloc(s.t3_fval, ne);
+    s.cap_t3e = ne;
+  }
+  tail3_fill_kernel<<<sms * 4, 256, 0, st>>>(nt, base, s.lf_ptr, s.lf_idx, s.lf_val, s.hsplit, s.t3_fidx, s.t3_fval);
+  ll_to_int_kernel<<<(nt + 1 + 255) / 256, 256, 0, st>>>(nt + 1, s.hsplit, 0, s.t3_fep);
+  // backward: the tail columns' entries all lie in the tail; make them tail-relative in place
+  ll_to_int_kernel<<<(nt + 1 + 255) / 256, 256, 0, st>>>(nt + 1, s.lb_ptr + base, hb[1], s.t3_bep);
+  long long lbe = 0;
+  check(cudaMemcpyAsync(&lbe, s.lb_ptr + n, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaStreamSynchronize(st), "v3 sync");
+  tail_rel_idx_kernel<<<sms * 4, 256, 0, st>>>(hb[1], lbe, base, s.lb_idx);
+  note_launches(4);
+  static bool attr = false;
+  if (!attr) {
+    check(cudaFuncSetAttribute(tail3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
+    check(cudaFuncSetAttribute(tail3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
+    attr = true;
+  }
+  check(cudaGetLastError(), "v3 layout");
+  s.t3_nt = nt;
+  s.t3_base = base;
+  s.t3_nlev = nlev;
+  s.t3_bbase = hb[1];
 }
 
 void prepare_factor(const SolveInputs& in) {
@@ -1673,15 +2312,21 @@ void prepare_factor(const SolveInputs& in) {
   check(cudaMemcpyAsync(&depth, s.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "prepare_factor");
   s.depth = depth;
-  // fast-mode copies: G rows sorted by level[k] ascending, G columns by level[r] descending
-  level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val, s.level, 0, depth + 1,
-                                             s.ff_col, s.ff_val, s.ff_lvl);
-  level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.level, 1, depth + 1,
-                                             s.fb_row, s.fb_val, s.fb_lvl);
-  note_launches(2);
-  check(cudaGetLastError(), "level sort");
-  build_tail(in, s, sms);
-  build_level_layout(in, s, sms);
+  static const bool v3 = !std::getenv("PARAC_SWEEP") || std::string(std::getenv("PARAC_SWEEP")) == "v3";
+  if (v3) {
+    build_level_layout(in, s, sms, false);
+    build_fast_v3(in, s, sms);
+  } else {
+    // fast-mode copies: G rows sorted by level[k] ascending, G columns by level[r] descending
+    level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val, s.level, 0, depth + 1,
+                                               s.ff_col, s.ff_val, s.ff_lvl);
+    level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.level, 1, depth + 1,
+                                               s.fb_row, s.fb_val, s.fb_lvl);
+    note_launches(2);
+    check(cudaGetLastError(), "level sort");
+    build_tail(in, s, sms);
+    build_level_layout(in, s, sms, true);
+  }
   if (std::getenv("PARAC_SWEEP_PROFILE")) {
     const std::size_t need = 4 * (static_cast<std::size_t>(s.depth) + 2);
     if (s.cap_ltime < need) {
@@ -1726,8 +2371,46 @@ struct Solver {
     int* done_b = s.done + (D + 2);
     check(cudaMemsetAsync(s.done, 0, sizeof(int) * 2 * (D + 2), st), "memset");
     check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
-    static const std::string sweep = std::getenv("PARAC_SWEEP") ? std::getenv("PARAC_SWEEP") : "chunk";
+    static const std::string sweep = std::getenv("PARAC_SWEEP") ? std::getenv("PARAC_SWEEP") : "v3";
     const bool legacy = sweep == "legacy";
+    if (!exact && sweep == "v3") {
+      const int H = s.t3_L0, nt = s.t3_nt;
+      const int Lw = std::min(s.wide_L, H);
+      unsigned long long* lt = s.ltime;
+      if (Lw > 0) {
+        check(launch_coop(head_sweep_kernel<true, true>, s.grid_ctas, kHThreads, kHeadSmem, st, 1, Lw, s.grid_W,
+                          s.hrec_gf, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, s.rlab, r,
+                          in.f_n, 0, s.t3_base, s.tail_s, lt), "wide forward");
+        note_launches(1);
+      }
+      check(launch_cluster_t(head_sweep_kernel<true, false>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
+                             s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd,
+                             s.rlab, Lw > 0 ? nullptr : r, in.f_n, nt, s.t3_base, s.tail_s, lt ? lt + Lw : nullptr),
+            "head forward");
+      note_launches(1);
+      if (nt > 0) {
+        tail3_kernel<true><<<1, kTailThreads, kT3Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_fep,
+                                                             s.t3_fidx, s.t3_fval, s.tail_s, s.dinv_l, nullptr,
+                                                             s.yf, lt ? lt + (D + 2) : nullptr);
+        tail3_kernel<false><<<1, kTailThreads, kT3Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_bep,
+                                                              s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
+                                                              nullptr, s.dinv_l, s.yf, s.zb,
+                                                              lt ? lt + 2 * (D + 2) : nullptr);
+        note_launches(2);
+      }
+      check(launch_cluster_t(head_sweep_kernel<false, false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
+                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr,
+                             nullptr, in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) : nullptr), "head backward");
+      if (Lw > 0) {
+        check(launch_coop(head_sweep_kernel<false, true>, s.grid_ctas, kHThreads, kHeadSmem, st, Lw, Lw, s.grid_W,
+                          s.hrec_gb, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr, nullptr,
+                          in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) + (H - Lw) : nullptr), "wide backward");
+        note_launches(1);
+      }
+      gather_z_l_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, s.v2l, s.zb, r, z, part(slot));
+      note_launches(2);
+      return;
+    }
     if (!exact && sweep == "chunk") {
       const ClusterSizes cs = cluster_sizes(in.device);
       const int H = s.tail_L0;
@@ -1739,13 +2422,13 @@ struct Solver {
             "chunk forward");
       note_launches(1);
       if (nt > 0) {
-        const std::size_t smem = static_cast<std::size_t>(nt) * 8;
-        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
-                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
-                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
-        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
-                                                            s.tb_row, s.tb_val, s.yd, s.zb,
-                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
+        const std::size_t smem = (static_cast<std::size_t>(kTailMaxRows) + kTailPbuf) * 8;
+        tail_sweep_kernel<true><<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tf_ptr,
+                                                               s.tf_col, s.tf_val, s.tail_s, in.diag, s.yf, s.yd,
+                                                               s.ltime ? s.ltime + (D + 2) : nullptr);
+        tail_sweep_kernel<false><<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
+                                                                s.tb_row, s.tb_val, nullptr, nullptr, s.zb, s.yd,
+                                                                s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
         note_launches(2);
       }
       check(launch_cluster(cluster_sweep_fast_kernel<false>, cs.sweep_b, kChunkSmem, st, H, H, s.b_chunk,
@@ -1892,6 +2575,9 @@ void solve_release(SolveState& s) {
   dfree(s.tf_val); dfree(s.tb_val); dfree(s.tail_s); dfree(s.tail_cnt);
   dfree(s.lf_ptr); dfree(s.lb_ptr); dfree(s.lf_idx); dfree(s.lb_idx); dfree(s.lf_val); dfree(s.lb_val);
   dfree(s.f_chunk); dfree(s.f_cbase); dfree(s.b_chunk); dfree(s.b_cbase); dfree(s.lvl_target); dfree(s.ltime);
+  dfree(s.hrec_gf); dfree(s.hrec_gb);
+  dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
+  dfree(s.t3_lvl); dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_bep); dfree(s.t3_fval);
   s = SolveState{};
 }
 void solve_invalidate(SolveState& s) {
@@ -1957,7 +2643,8 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
       std::vector<unsigned long long> t(4 * (static_cast<std::size_t>(ss.depth) + 2));
       check(cudaMemcpy(t.data(), ss.ltime, t.size() * 8, cudaMemcpyDeviceToHost), "d2h");
       if (FILE* f = std::fopen(std::getenv("PARAC_SWEEP_PROFILE"), "wb")) {
-        const int hdr[3] = {ss.tail_L0, ss.depth, ss.tail_n};
+        const bool v3 = ss.cap_v3 > 0;
+        const int hdr[3] = {v3 ? ss.t3_L0 : ss.tail_L0, ss.depth, v3 ? ss.t3_nt : ss.tail_n};
         std::fwrite(hdr, 4, 3, f);
         std::fwrite(t.data(), 8, t.size(), f);
         std::fclose(f);

@@ -41,7 +41,20 @@ struct SolveState {
   double *lf_val = nullptr, *lb_val = nullptr;
   int *f_chunk = nullptr, *f_cbase = nullptr, *b_chunk = nullptr, *b_cbase = nullptr;
   long long* lvl_target = nullptr;
-  unsigned long long* ltime = nullptr;  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
+  unsigned long long* ltime = nullptr;
+  // v3 fast sweeps (level-order index space): maps, head chunk tables, tail arrays
+  int *lpos = nullptr, *rlab = nullptr, *v2l = nullptr;
+  double *dinv_l = nullptr, *rhs_l = nullptr;
+  int4 *hrec_f = nullptr, *hrec_b = nullptr;
+  int head_csize = 0, head_W = 0;
+  int grid_ctas = 0, grid_W = 0, wide_L = 0;  // cooperative full-GPU sweep of the wide first levels
+  int4 *hrec_gf = nullptr, *hrec_gb = nullptr;
+  std::size_t cap_grec = 0;
+  int t3_L0 = 0, t3_nt = 0, t3_base = 0, t3_nlev = 0;
+  long long t3_bbase = 0;  // lb_ptr[t3_base]
+  int *t3_lvl = nullptr, *t3_fep = nullptr, *t3_fidx = nullptr, *t3_bep = nullptr;
+  double* t3_fval = nullptr;
+  std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0;  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
   std::size_t cap_ltime = 0;
   std::size_t cap_lz = 0, cap_fchunk = 0, cap_bchunk = 0, cap_levels = 0;
   std::size_t cap_tail = 0, cap_tail_nnz = 0;

@@ -397,6 +397,47 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
     return f
 
 
+def _batch_args(graphs, orderings, seeds):
+    if not (len(graphs) == len(orderings) == len(seeds)) or not graphs:
+        raise Error(Errc.dimension_mismatch, "DimensionMismatch: batch lists differ in length")
+    for g, o in zip(graphs, orderings):
+        if o.size() != g.n:
+            raise Error(Errc.dimension_mismatch, "DimensionMismatch: ordering size does not match graph")
+    csrs = (L.parac_csr * len(graphs))(*[g.csr() for g in graphs])
+    perms = (C.c_void_p * len(graphs))(*[_ptr(o.perm) for o in orderings])
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    keep = (csrs, perms, sd, graphs, orderings)
+    return csrs, perms, sd, keep
+
+
+def factor_batch_gpu(graphs: Sequence[LaplacianGraph], orderings: Sequence[Ordering], seeds: Sequence[int],
+                     options: Optional[GpuOptions] = None, ctx: Optional[GpuContext] = None):
+    """Factor independent Laplacians in ONE device pass (BASELINE config[4]): the
+    problems are staged as a disjoint union with per-problem sample seeds and
+    keys, so factor i is byte-identical to factor_gpu(graphs[i], orderings[i],
+    seeds[i]). Returns (list of LdlFactor, info)."""
+    ctx = ctx or default_context()
+    csrs, perms, sd, keep = _batch_args(graphs, orderings, seeds)
+    o = (options or GpuOptions()).native()
+    info = L.parac_gpu_factor_info()
+    _check(lib.parac_gpu_factor_batch(ctx.handle, len(graphs), csrs, perms, _ptr(sd), C.byref(o),
+                                      C.byref(info)))
+    ctx._factor_n = info.n
+    out = []
+    for i, (g, ordg) in enumerate(zip(graphs, orderings)):
+        z = C.c_int64()
+        _check(lib.parac_gpu_batch_nnz(ctx.handle, i, C.byref(z)))
+        z = int(z.value)
+        col_ptr = np.empty(g.n + 1, np.int64)
+        rows = np.empty(max(z, 1), np.int32)
+        vals = np.empty(max(z, 1), np.float64)
+        diag = np.empty(max(g.n, 1), np.float64)
+        _check(lib.parac_gpu_download_batch(ctx.handle, i, _ptr(col_ptr), _ptr(rows), _ptr(vals), _ptr(diag)))
+        out.append(LdlFactor(g.n, col_ptr, rows[:z], vals[:z], diag[:g.n], ordg.perm))
+    del keep
+    return out, info
+
+
 def dependency_counts(graph: LaplacianGraph, ordering: Ordering) -> np.ndarray:
     """dependency_counts (factor_seq.hpp:45-46): earlier-neighbour count per position."""
     pos = ordering.perm

@@ -113,3 +113,17 @@ def test_native_library_is_what_ran(gpu_ctx):
     g, perm, seed = case("poisson16_random0")
     gpu_factor(gpu_ctx, g, perm, seed)
     assert P.rchol.lib.parac_gpu_launch_count() > before
+
+
+def test_batch_union_equals_standalone(gpu_ctx, port, gold):
+    # config[4] mechanism: several independent problems factored in one device
+    # pass (disjoint union, per-problem seeds/keys) -- each factor byte-identical
+    # to the reference's stand-alone factorization, whatever its size and seed
+    names = ["p3", "k3_s7", "star8", "rc200_s1_nnz", "poisson16_random1", "components3000_s2", "ring9_s3"]
+    cases = [case(nm) for nm in names]
+    fs, info = P.factor_batch_gpu([c[0] for c in cases], [P.Ordering(c[1]) for c in cases],
+                                  [c[2] for c in cases], ctx=gpu_ctx)
+    for nm, (g, perm, seed), f in zip(names, cases, fs):
+        assert_same(f, factor_from_port(port.factor(g, perm, seed)), nm)
+        e = next(x for x in gold["factors"] if x["name"] == nm)
+        assert f"{f.checksum():016x}" == e["checksum"], nm

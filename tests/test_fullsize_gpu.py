@@ -75,9 +75,14 @@ def test_fullsize_rmat22(gpu_ctx):
 
 
 def test_batch_64x64_checksums(gpu_ctx):
+    # config[4]: all 64 problems in one device pass, each equal to the reference
     g = P.gen_poisson3d(64)
-    for e in FULL["batch_64x64"][::8]:
-        o = P.ordering_random(g.n, e["i"])
-        f = P.factor_gpu(g, o, e["i"], ctx=gpu_ctx)
+    ents = FULL["batch_64x64"]
+    fs, _ = P.factor_batch_gpu([g] * len(ents), [P.ordering_random(g.n, e["i"]) for e in ents],
+                               [e["i"] for e in ents], ctx=gpu_ctx)
+    for e, f in zip(ents, fs):
         assert f"{f.checksum():016x}" == e["checksum"], e["i"]
         assert f.nnz_off_diagonal() == e["nnz_off"]
+    # and one of them stand-alone
+    f0 = P.factor_gpu(g, P.ordering_random(g.n, 5), 5, ctx=gpu_ctx)
+    assert f"{f0.checksum():016x}" == ents[5]["checksum"]

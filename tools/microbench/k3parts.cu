@@ -28,7 +28,7 @@ __global__ void parts(int m, long long* out, double* sink) {
     wk[0] = g < m ? dbits(B[g]) : kInfBits;
     ak[0] = g < m ? A[g] : ~0ull;
     int rank[1];
-    rank_sort<kThreads, 1, true>(wk, ak, m, S.X1, S.X2, rank);
+    rank_sort<kThreads, 1>(wk, m, S.X1, S.X2, rank);
     __syncthreads();
     if (g < m) { X1[rank[0]] = ak[0]; }
     __syncthreads();
@@ -51,10 +51,10 @@ __global__ void parts(int m, long long* out, double* sink) {
   }
   long long t4 = clock64();
   for (int rep = 0; rep < 10; ++rep) {
-    unsigned long long key[1], none[1] = {0};
+    unsigned long long key[1];
     key[0] = tid < m ? A[tid] : ~0ull;
     int rank[1];
-    rank_sort<kThreads, 1, false>(key, none, m, S.X1, S.X2, rank);
+    rank_sort<kThreads, 1>(key, m, S.X1, S.X2, rank);
     __syncthreads();
   }
   long long t5 = clock64();

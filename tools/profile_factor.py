@@ -41,6 +41,9 @@ def main():
     for _ in range(2):
         f = P.factor_gpu(g, o, 0, opts, st, ctx=ctx)
     tt = ctx.vertex_times().astype(np.int64)
+    sub = np.zeros(8 * g.n, np.uint64)
+    P.rchol._check(P.rchol.lib.parac_gpu_download_subtimes(ctx.handle, sub.ctypes.data))
+    sub = sub.reshape(g.n, 8).astype(np.int64)
     n = g.n
     t0 = tt[:, 0].min()
     start = (tt[:, 0] - t0) / 1e3  # us
@@ -111,6 +114,22 @@ def main():
         "m_mean": float(m[ch].mean()), "service_us_per_vertex": float(dur[ch].mean()),
         "hop_us_per_vertex": float(hop[ch[1:]].mean()) if len(ch) > 1 else 0.0,
         "phases_us_per_vertex": {nm: round(float(pdur[ch, i].mean()), 2) for i, nm in enumerate(names)},
+    }
+    # sub-phase split of the critical path (where stamped)
+    def span(a, b):
+        ok = (a > 0) & (b > 0)
+        return float(((b - a)[ok] / 1e3).mean()) if ok.any() else None
+    chs = ch
+    out["critical_path"]["sub_us"] = {
+        "setup(claim->counts+dir)": span(tt[chs, 0], sub[chs, 0]),
+        "gather landed": span(sub[chs, 0], sub[chs, 1]),
+        "raw sort": span(sub[chs, 1], tt[chs, 1]),
+        "weight sort": span(tt[chs, 3], sub[chs, 2]),
+        "suffix chain": span(sub[chs, 2], tt[chs, 4]),
+        "draw samples": span(tt[chs, 4], sub[chs, 3]),
+        "emit fills": span(sub[chs, 3], sub[chs, 4]),
+        "levels+fence": span(sub[chs, 4], sub[chs, 5]),
+        "decrement": span(sub[chs, 5], tt[chs, 6]),
     }
     print(json.dumps(out, indent=1))
     if args.json:

@@ -64,6 +64,20 @@ int main(int argc, char** argv) {
   const std::vector<double> y_gpu = laplacian_apply_gpu(g, b);
   CHECK(y_ref == y_gpu, "laplacian_apply_gpu bit-identical");
 
+  // batch: three problems of different size/seed in one device pass
+  {
+    PoissonSpec s2;
+    s2.n = side / 2 + 2;
+    const LaplacianGraph g2 = gen_poisson3d(s2);
+    const std::vector<LaplacianGraph> gs = {g, g2, g};
+    const std::vector<Ordering> os = {o, ordering_random(g2.num_vertices(), 3), ordering_random(g.num_vertices(), 9)};
+    const std::vector<std::uint64_t> ss = {0, 3, 9};
+    const std::vector<LdlFactor> fb = factor_batch_gpu(gs, os, ss);
+    bool all = fb.size() == 3;
+    for (std::size_t i = 0; all && i < 3; ++i) all = fb[i].same_values(factor_randomized(gs[i], os[i], ss[i]));
+    CHECK(all, "factor_batch_gpu: each problem same_values factor_randomized");
+  }
+
   // error vocabulary: the same Errc codes the CPU backends throw
   try {
     GpuOptions tiny;

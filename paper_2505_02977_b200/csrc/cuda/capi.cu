@@ -74,6 +74,8 @@ struct parac_gpu_ctx {
   DevBuf<int> perm;
   // factor working state
   DevBuf<int> inv, fdeg, dp, queue, bqueue, fill_cnt, samples, col_len, arena_rows, level;
+  DevBuf<int> heavy_list, heavy_count, heavy_key;
+  DevBuf<double> heavy_val;
   DevBuf<long long> fwd_ptr, col_start, tiles;
   DevBuf<int> fwd_to;
   DevBuf<double> fwd_w, diag, arena_vals;
@@ -153,12 +155,16 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->fwd_ptr.ensure(nn + 1);
   ctx->fwd_to.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
   ctx->fwd_w.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
+  ctx->heavy_list.ensure(nn);
+  ctx->heavy_count.ensure(1);
+  ctx->heavy_key.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
+  ctx->heavy_val.ensure(static_cast<std::size_t>(std::max<long long>(E, 1)));
   ctx->pool0.ensure(nn * static_cast<std::size_t>(b.c0));
   ctx->dir.ensure(nn * kDirChunks);
   ctx->ovf.ensure(static_cast<std::size_t>(std::max<long long>(b.ovf, 1)));
   ctx->arena_rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->arena_vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
-  ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * 24);
+  ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * kSlabEntryBytes);
   ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->ctrl.ensure(1);
@@ -176,6 +182,10 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.fwd_to = ctx->fwd_to.p;
   d.fwd_w = ctx->fwd_w.p;
   d.fdeg = ctx->fdeg.p;
+  d.heavy_list = ctx->heavy_list.p;
+  d.heavy_count = ctx->heavy_count.p;
+  d.heavy_key = ctx->heavy_key.p;
+  d.heavy_val = ctx->heavy_val.p;
   d.dp = ctx->dp.p;
   d.queue = ctx->queue.p;
   d.bqueue = ctx->bqueue.p;
@@ -309,6 +319,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
+  ctx->heavy_list.release(); ctx->heavy_count.release(); ctx->heavy_key.release(); ctx->heavy_val.release();
   ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->level.release(); ctx->queue.release(); ctx->bqueue.release();
   ctx->fill_cnt.release(); ctx->samples.release(); ctx->col_len.release();
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();

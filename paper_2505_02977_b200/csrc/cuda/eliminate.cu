@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kEntryBytes = 24;  // A (u64), B (f64), C (f64) per column entry
+constexpr int kEntryBytes = kSlabEntryBytes;
 // small warps: A, B, C + two rank-sort segment buffers (X1, X2)
 constexpr int kSmallBytes = kSmallCap * 8 * 5;
 // big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
@@ -279,46 +279,6 @@ __device__ __forceinline__ void cta_reg_sort(unsigned long long (&key)[ITEMS],
   }
 }
 
-// Shared/global-memory bitonic networks for the whole CTA (slab path, P > kBigCap).
-__device__ __noinline__ void cta_sort_key(unsigned long long* A, double* B, int P) {
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (P >> 1); i += kThreads) {
-        const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        const int b = a + j;
-        const unsigned long long ka = A[a], kb = A[b];
-        if ((ka > kb) == ((a & k) == 0)) {
-          A[a] = kb;
-          A[b] = ka;
-          const double t = B[a];
-          B[a] = B[b];
-          B[b] = t;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__device__ __noinline__ void cta_sort_weight(unsigned long long* A, double* B, int P) {
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (P >> 1); i += kThreads) {
-        const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        const int b = a + j;
-        const unsigned long long aa = A[a], ab = A[b];
-        const unsigned long long wa = dbits(B[a]), wb = dbits(B[b]);
-        if (wless(wb, ab, wa, aa) == ((a & k) == 0)) {
-          A[a] = ab;
-          A[b] = aa;
-          B[a] = bitsd(wb);
-          B[b] = bitsd(wa);
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
 
 // ------------------------------------------------------------ rank sort
 // Stable sort of R <= T*ITEMS u64 keys held in registers (element g = i*T +
@@ -503,6 +463,170 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
   __syncthreads();
 }
 
+// ------------------------------------------------------------ wide columns
+// Columns with more than kBigCap raw entries (R-MAT hubs: up to ~10^5) live in
+// a global-memory slab owned by the CTA. Sort = tiles of kBigCap sorted in
+// shared memory by the register bitonic network, then log2(R / kBigCap)
+// merge-path passes (each thread merges a contiguous output range, found by
+// binary search on the diagonal) ping-ponging between (K, V) and (K2, V2).
+// Keys are unique under Less, so merges need no tie rule.
+template <typename Less>
+__device__ __noinline__ void slab_sort(unsigned long long* K, unsigned long long* V, unsigned long long* K2,
+                                       unsigned long long* V2, int R, unsigned long long padk,
+                                       unsigned long long padv, XBuf xb, Less less) {
+  const int tid = threadIdx.x;
+  for (int tb = 0; tb < R; tb += kBigCap) {
+    const int cnt = min(kBigCap, R - tb);
+    unsigned long long key[4], val[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = tid * 4 + i;
+      key[i] = g < cnt ? K[tb + g] : padk;
+      val[i] = g < cnt ? V[tb + g] : padv;
+    }
+    __syncthreads();
+    cta_reg_sort<4>(key, val, xb, less);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = tid * 4 + i;
+      if (g < cnt) {
+        K[tb + g] = key[i];
+        V[tb + g] = val[i];
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long *sk = K, *sv = V, *dk = K2, *dv = V2;
+  for (int run = kBigCap; run < R; run *= 2) {
+    for (int b = 0; b < R; b += 2 * run) {
+      const int na = min(run, R - b), nb = max(0, min(run, R - b - run));
+      const int tot = na + nb;
+      const unsigned long long *Ak = sk + b, *Av = sv + b, *Bk = sk + b + na, *Bv = sv + b + na;
+      const int per = (tot + kThreads - 1) / kThreads;
+      const int d0 = min(tid * per, tot), d1 = min(d0 + per, tot);
+      if (d0 >= d1) continue;
+      int lo = max(0, d0 - nb), hi = min(d0, na);
+      while (lo < hi) {  // A-elements among the first d0 outputs
+        const int mid = (lo + hi) >> 1;
+        if (less(Bk[d0 - 1 - mid], Bv[d0 - 1 - mid], Ak[mid], Av[mid])) hi = mid; else lo = mid + 1;
+      }
+      int i = lo, j = d0 - lo;
+      unsigned long long ak = i < na ? Ak[i] : 0, av = i < na ? Av[i] : 0;
+      unsigned long long bk = j < nb ? Bk[j] : 0, bv = j < nb ? Bv[j] : 0;
+      for (int o = d0; o < d1; ++o) {
+        const bool takeA = j >= nb || (i < na && less(ak, av, bk, bv));
+        if (takeA) {
+          dk[b + o] = ak;
+          dv[b + o] = av;
+          ++i;
+          if (i < na) { ak = Ak[i]; av = Av[i]; }
+        } else {
+          dk[b + o] = bk;
+          dv[b + o] = bv;
+          ++j;
+          if (j < nb) { bk = Bk[j]; bv = Bv[j]; }
+        }
+      }
+    }
+    __syncthreads();
+    unsigned long long* t = sk; sk = dk; dk = t;
+    t = sv; sv = dv; dv = t;
+  }
+  if (sk != K) {
+    for (int g = tid; g < R; g += kThreads) {
+      K[g] = sk[g];
+      V[g] = sv[g];
+    }
+    __syncthreads();
+  }
+}
+
+// Serial chains over a global-memory column: the lead thread walks chunks of
+// kChainChunk values staged in shared memory by warps 1..7 (double-buffered),
+// so the chain runs at the FP64 add latency instead of the L2 latency.
+constexpr int kChainChunk = 1024;
+
+__device__ __noinline__ double wide_total(const double* B, int m, double* stage) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nch = (m + kChainChunk - 1) / kChainChunk;
+  double s = 0.0;
+  if (warp != 0)
+    for (int t = tid - 32; t < min(m, kChainChunk); t += kThreads - 32) stage[t] = B[t];
+  for (int c = 0; c < nch; ++c) {
+    __syncthreads();
+    const double* cur = stage + (c & 1) * kChainChunk;
+    if (warp != 0) {
+      double* nxt = stage + ((c + 1) & 1) * kChainChunk;
+      const int b = (c + 1) * kChainChunk;
+      for (int t = tid - 32; t < kChainChunk && b + t < m; t += kThreads - 32) nxt[t] = B[b + t];
+    } else if (tid == 0) {
+      const int cnt = min(kChainChunk, m - c * kChainChunk);
+      int t = 0;
+      for (; t + 8 <= cnt; t += 8) {
+        double x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = cur[t + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, x[q]);
+      }
+      for (; t < cnt; ++t) s = __dadd_rn(s, cur[t]);
+    }
+  }
+  __syncthreads();
+  return s;
+}
+
+// suffix[g] = w[g] + suffix[g+1], right to left, written to C (global).
+__device__ __noinline__ void wide_suffix(const double* B, double* C, int m, double* stage) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nch = (m + kChainChunk - 1) / kChainChunk;
+  // chunk c covers [m - (c+1)*CH, m - c*CH)
+  auto chunk_lo = [&](int c) { return max(0, m - (c + 1) * kChainChunk); };
+  if (warp != 0) {
+    const int lo = chunk_lo(0);
+    for (int t = lo + tid - 32; t < m; t += kThreads - 32) stage[t - lo] = B[t];
+  }
+  double s = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    __syncthreads();
+    const double* cur = stage + (c & 1) * kChainChunk;
+    const int lo = chunk_lo(c), hi = m - c * kChainChunk;
+    if (warp != 0) {
+      if (c + 1 < nch) {
+        double* nxt = stage + ((c + 1) & 1) * kChainChunk;
+        const int lo2 = chunk_lo(c + 1), hi2 = lo;
+        for (int t = lo2 + tid - 32; t < hi2; t += kThreads - 32) nxt[t - lo2] = B[t];
+      }
+    } else if (tid == 0) {
+      int g = hi - 1;
+      if (c == 0) {
+        s = cur[g - lo];
+        C[g] = s;
+        --g;
+      }
+      for (; g - 7 >= lo; g -= 8) {
+        double x[8], o[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = cur[g - q - lo];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          s = __dadd_rn(x[q], s);
+          o[q] = s;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) C[g - q] = o[q];
+      }
+      for (; g >= lo; --g) {
+        s = __dadd_rn(cur[g - lo], s);
+        C[g] = s;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+
 // ---- warp path: gather + raw sort, weight sort (results in A/B, natural order)
 template <int ITEMS>
 __device__ __forceinline__ void warp_sort_raw(const FactorDev& d, int k, long long fb, int fdeg,
@@ -597,12 +721,12 @@ __device__ __forceinline__ void cta_sort_weight_reg(int m, unsigned long long* A
 __device__ __forceinline__ double serial_total(const double* B, int m) {
   double s = 0.0;
   int i = 0;
-  for (; i + 4 <= m; i += 4) {
-    const double x0 = B[i], x1 = B[i + 1], x2 = B[i + 2], x3 = B[i + 3];
-    s = __dadd_rn(s, x0);
-    s = __dadd_rn(s, x1);
-    s = __dadd_rn(s, x2);
-    s = __dadd_rn(s, x3);
+  for (; i + 8 <= m; i += 8) {
+    double x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = B[i + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = __dadd_rn(s, x[q]);
   }
   for (; i < m; ++i) s = __dadd_rn(s, B[i]);
   return s;
@@ -613,16 +737,19 @@ __device__ __forceinline__ void serial_suffix(const double* B, double* C, int m)
   double s = B[m - 1];
   C[m - 1] = s;
   int g = m - 2;
-  for (; g >= 3; g -= 4) {
-    const double x0 = B[g], x1 = B[g - 1], x2 = B[g - 2], x3 = B[g - 3];
-    s = __dadd_rn(x0, s);
-    C[g] = s;
-    s = __dadd_rn(x1, s);
-    C[g - 1] = s;
-    s = __dadd_rn(x2, s);
-    C[g - 2] = s;
-    s = __dadd_rn(x3, s);
-    C[g - 3] = s;
+  // loads of the next block are independent of the chain; stores after it
+  // (C may alias nothing in B, but the compiler cannot know)
+  for (; g >= 7; g -= 8) {
+    double x[8], o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = B[g - q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s = __dadd_rn(x[q], s);
+      o[q] = s;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) C[g - q] = o[q];
   }
   for (; g >= 0; --g) {
     s = __dadd_rn(B[g], s);
@@ -857,7 +984,8 @@ struct CtaShared {
   int bad;
   double lkk;
   long long start;
-  long long slab;
+  long long slab;      // this CTA's wide-column slab (entries), -1 none
+  int slab_cap;
   unsigned dirrow[kDirChunks];
   int wcount[kWarps];
   unsigned long long best[kWarps];
@@ -883,13 +1011,17 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   if (lead) {
     sh.bad = 0;
     if (P > kBigCap) {
-      const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(P)));
-      if (base + P > d.large_cap) {
-        fail(d, kErrArena, k);
-        sh.bad = 1;
+      if (P > sh.slab_cap) {  // this CTA's slab is reused; grow it (bump allocation) when too small
+        const int cap = max(P, 2 * sh.slab_cap);
+        const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(cap)));
+        if (base + cap > d.large_cap) {
+          fail(d, kErrArena, k);
+          sh.bad = 1;
+        }
+        sh.slab = base;
+        sh.slab_cap = cap;
       }
       atomicAdd(&ctrl->large_cols, 1);
-      sh.slab = base;
     }
     if (R > 64) atomicMax(&ctrl->max_raw, R);
   }
@@ -901,20 +1033,23 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   unsigned long long start_reg = 0;
   if (lead && R > 0) start_reg = atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R));
   const bool wide = P > kBigCap;
-  Scratch S = wide ? carve(d.large_pool + sh.slab * kEntryBytes, P) : carve(smem, kBigCap);
+  Scratch S = wide ? carve(d.large_pool + sh.slab * kEntryBytes, sh.slab_cap) : carve(smem, kBigCap);
+  const XBuf sxb{reinterpret_cast<unsigned long long*>(smem), reinterpret_cast<unsigned long long*>(smem + 8 * kBigCap),
+                 reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
+                 reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
   const XBuf xb{S.A, reinterpret_cast<unsigned long long*>(S.B),
                 reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
                 reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
-  if (wide) {  // global slab, shared-memory-free network
-    for (int t = tid; t < P; t += kThreads) {
+  if (wide) {  // global slab: shared-memory tiles + merge passes
+    for (int t = tid; t < R; t += kThreads) {
       unsigned long long key = ~0ull;
       double w = 0.0;
-      if (t < R) load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key, w);
+      load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key, w);
       S.A[t] = key;
       S.B[t] = w;
     }
     __syncthreads();
-    cta_sort_key(S.A, S.B, P);
+    slab_sort(S.A, reinterpret_cast<unsigned long long*>(S.B), S.X1, S.X2, R, ~0ull, 0ull, sxb, RawLess{});
   } else if (P <= kThreads) {
     cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   } else if (P <= 2 * kThreads) {
@@ -970,7 +1105,13 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
 
   // ---- 5. lkk + column
-  if (lead) {
+  if (wide) {
+    const double t = wide_total(S.B, m, reinterpret_cast<double*>(smem));
+    if (lead) {
+      sh.lkk = t;
+      sh.start = static_cast<long long>(start_reg);
+    }
+  } else if (lead) {
     sh.lkk = serial_total(S.B, m);
     sh.start = static_cast<long long>(start_reg);
   }
@@ -996,12 +1137,8 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   if (m >= 2) {
     const int Pm = next_pow2(m);
     if (Pm > kBigCap) {
-      for (int t = m + tid; t < Pm; t += kThreads) {
-        S.A[t] = ~0ull;
-        S.B[t] = bitsd(kInfBits);
-      }
-      __syncthreads();
-      cta_sort_weight(S.A, S.B, Pm);
+      // key = weight bits, payload = A (row << 32 | mult): (weight, row) order
+      slab_sort(reinterpret_cast<unsigned long long*>(S.B), S.A, S.X1, S.X2, m, kInfBits, ~0ull, sxb, WeightLess{});
     } else if (Pm <= kThreads) {
       cta_rank_weight<1>(m, S);
     } else if (Pm <= 2 * kThreads) {
@@ -1010,7 +1147,14 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       cta_sort_weight_reg<4>(m, S.A, S.B, xb);
     }
     SUB(2);
-    if (lead) serial_suffix(S.B, S.C, m);
+    if (Pm > kBigCap) {
+      wide_suffix(S.B, S.C, m, reinterpret_cast<double*>(smem));
+      double* coarse = reinterpret_cast<double*>(smem + 2 * 8 * kBigCap);  // C + D regions: kCoarseMax entries
+      const int cs = coarse_step(m);
+      for (int q = tid; q * cs < m; q += kThreads) coarse[q] = S.C[q * cs];
+    } else if (lead) {
+      serial_suffix(S.B, S.C, m);
+    }
     __syncthreads();
   }
   PHASE(4);
@@ -1023,7 +1167,10 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     const int i = base + tid;
     int lo = 0, hi = 0, slot = 0;
     double wv = 0.0;
-    const bool em = i < m - 1 && draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv);
+    const bool em = i < m - 1 &&
+                    draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv,
+                                m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
+                                coarse_step(m));
     if (base == 0) SUB(3);
     if (em) {
       slot = reserve_fill_slot(d, lo);
@@ -1121,7 +1268,9 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
     int done_local = 0;
     Next nx{-1, -1, 0, 0};
     while (true) {
+      bool kept = true;
       if (nx.k < 0) {
+        kept = false;
         int k = -1;
         if (lane == 0) {
           if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
@@ -1137,6 +1286,10 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
       const int k = nx.k;
       const bool lead = lane == 0;
       PHASE(0);
+      if (d.vsub && lead) {  // diagnostics: who eliminated k, and whether it was kept
+        d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | warp;
+        d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
+      }
       Next nn = warp_eliminate(d, nx, S, lane);
       if (nn.k == -2) break;
       if (nn.k != -3) {
@@ -1150,10 +1303,17 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
   }
 
   // big CTA: the whole CTA eliminates one vertex at a time
+  if (threadIdx.x == 0) {
+    sh.slab = -1;
+    sh.slab_cap = 0;
+  }
+  __syncthreads();
   int done_local = 0;
   int k = -1;
   while (true) {
+    bool kept = true;
     if (k < 0) {
+      kept = false;
       if (threadIdx.x == 0) {
         if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
         sh.k = claim(d, true);
@@ -1167,6 +1327,10 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
     fence_acq_rel();
     const bool lead = threadIdx.x == 0;
     PHASE(0);
+    if (d.vsub && lead) {
+      d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
+      d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
+    }
     const int next = cta_eliminate(d, k, smem, sh);
     if (next == -2) break;
     PHASE(7);

@@ -171,13 +171,35 @@ __device__ __forceinline__ SampleKey sample_key(const FactorDev& d, int k) {
   return {d.pid_seed[p], static_cast<long long>(k) - d.pid_base[p]};
 }
 
+// pick_by_suffix over a wide column: coarse index (every kCoarse-th suffix
+// value, shared memory) then a fine search in global memory. Same result as
+// the flat search: suffix is non-increasing, so {j : suffix[j] > u} is a prefix.
+constexpr int kCoarse = 64;        // minimum coarse step
+constexpr int kCoarseMax = 2048;   // coarse entries (16 KB of shared memory)
+__device__ __forceinline__ int coarse_step(int m) { return max(kCoarse, (m + kCoarseMax - 1) / kCoarseMax); }
+__device__ __forceinline__ int pick_wide(const double* suffix, const double* coarse, int cs, int lo, int hi,
+                                         double u) {
+  // largest coarse point q*cs inside [lo, hi] with suffix > u, then the fine search after it
+  int qlo = (lo + cs - 1) / cs, qhi = hi / cs;
+  int a = lo;
+  if (qlo <= qhi && coarse[qlo] > u) {
+    while (qlo < qhi) {
+      const int mid = qlo + (qhi - qlo + 1) / 2;
+      if (coarse[mid] > u) qlo = mid; else qhi = mid - 1;
+    }
+    a = max(lo, qlo * cs);
+  }
+  const int b = min(hi, a + cs);
+  return pick_by_suffix(suffix, a, b, u);
+}
+
 __device__ __forceinline__ bool draw_sample(const FactorDev& d, SampleKey sk, int k, int i, int m,
                                            const unsigned long long* A, const double* B,
                                            const double* suffix, double lkk, int& lo, int& hi,
-                                           double& wv) {
+                                           double& wv, const double* coarse = nullptr, int cs = 0) {
   const double s = suffix[i + 1];
   const double u = __dmul_rn(unit_uniform(sk.seed, sk.key, static_cast<unsigned long long>(i)), s);
-  const int j = pick_by_suffix(suffix, i + 1, m - 1, u);
+  const int j = coarse ? pick_wide(suffix, coarse, cs, i + 1, m - 1, u) : pick_by_suffix(suffix, i + 1, m - 1, u);
   wv = __ddiv_rn(__dmul_rn(s, B[i]), lkk);
   if (wv < kDropThreshold) return false;
   const int a = static_cast<int>(A[i] >> 32), c = static_cast<int>(A[j] >> 32);

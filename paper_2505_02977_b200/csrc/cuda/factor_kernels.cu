@@ -31,11 +31,16 @@ __global__ void pos_count_kernel(FactorDev d) {
     return;
   }
   if (atomicExch(&d.inv[p], v) != -1) fail(d, kErrPerm, v);
-  int cnt = 0;
   const long long b = d.ptr[v], e = d.ptr[v + 1];
-  for (long long t = b; t < e; ++t) cnt += d.perm[d.adj[t]] > p;
-  d.fdeg[p] = cnt;
-  d.dp[p] = static_cast<int>(e - b) - cnt;  // earlier_degree = initial dependency count
+  if (e - b > kHeavyDeg) {
+    // hub: counted and filled by a whole CTA (pos_*_heavy_kernel)
+    d.heavy_list[atomicAdd(d.heavy_count, 1)] = v;
+  } else {
+    int cnt = 0;
+    for (long long t = b; t < e; ++t) cnt += d.perm[d.adj[t]] > p;
+    d.fdeg[p] = cnt;
+    d.dp[p] = static_cast<int>(e - b) - cnt;  // earlier_degree = initial dependency count
+  }
   d.fill_cnt[p] = 0;
   d.queue[p] = -1;
   d.bqueue[p] = -1;
@@ -56,6 +61,7 @@ __global__ void pos_fill_kernel(FactorDev d) {
     const long long b = d.ptr[v];
     const int deg = static_cast<int>(d.ptr[v + 1] - b);
     const long long out = d.fwd_ptr[p];
+    if (deg > kHeavyDeg) continue;  // pos_fill_heavy_kernel
     if (deg <= 32) {
       int q = -1;
       double wt = 0.0;
@@ -94,6 +100,149 @@ __global__ void pos_fill_kernel(FactorDev d) {
         }
       }
     }
+  }
+}
+
+// Hubs (degree > kHeavyDeg): one CTA per vertex. Count: block reduction.
+// Fill: block compaction of the kept (q, w) pairs into the forward range,
+// then a sort by q: 1024-entry tiles in shared memory (bitonic), then
+// merge-path passes ping-ponging with the hub scratch at the same offsets.
+constexpr int kHT = 256;
+__global__ void __launch_bounds__(kHT) pos_count_heavy_kernel(FactorDev d) {
+  __shared__ int red[kHT / 32];
+  const int nh = *d.heavy_count;
+  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int v = d.heavy_list[h];
+    const int p = d.perm[v];
+    const long long b = d.ptr[v], e = d.ptr[v + 1];
+    int cnt = 0;
+    for (long long t = b + threadIdx.x; t < e; t += kHT) cnt += d.perm[d.adj[t]] > p;
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int c = 0;
+      for (int w = 0; w < kHT / 32; ++w) c += red[w];
+      d.fdeg[p] = c;
+      d.dp[p] = static_cast<int>(e - b) - c;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kHT) pos_fill_heavy_kernel(FactorDev d) {
+  __shared__ int base_sh;
+  __shared__ int skey[1024];
+  __shared__ double sval[1024];
+  const int nh = *d.heavy_count;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int v = d.heavy_list[h];
+    const int p = d.perm[v];
+    const long long b = d.ptr[v], e = d.ptr[v + 1];
+    const long long out = d.fwd_ptr[p];
+    const int f = static_cast<int>(d.fwd_ptr[p + 1] - out);
+    int* K = d.fwd_to + out;
+    double* V = d.fwd_w + out;
+    int* K2 = d.heavy_key + out;
+    double* V2 = d.heavy_val + out;
+    if (tid == 0) base_sh = 0;
+    __syncthreads();
+    for (long long t0 = b; t0 < e; t0 += kHT) {  // compaction (any order)
+      const long long t = t0 + tid;
+      int q = -1;
+      double w = 0.0;
+      if (t < e) {
+        q = d.perm[d.adj[t]];
+        w = d.w[t];
+      }
+      const bool keep = q > p;
+      const unsigned m = __ballot_sync(kFull, keep);
+      int at = 0;
+      if (lane == 0 && m) at = atomicAdd(&base_sh, __popc(m));
+      at = __shfl_sync(kFull, at, 0);
+      if (keep) {
+        const int o = at + __popc(m & ((1u << lane) - 1));
+        K[o] = q;
+        V[o] = w;
+      }
+    }
+    __syncthreads();
+    // tiles of 1024: bitonic in shared memory (keys are unique positions)
+    for (int tb = 0; tb < f; tb += 1024) {
+      const int cnt = min(1024, f - tb);
+      int P = 1;
+      while (P < cnt) P <<= 1;
+      for (int i = tid; i < P; i += kHT) {
+        skey[i] = i < cnt ? K[tb + i] : 0x7fffffff;
+        sval[i] = i < cnt ? V[tb + i] : 0.0;
+      }
+      __syncthreads();
+      for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = tid; i < (P >> 1); i += kHT) {
+            const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+            const int c = a + j;
+            const int ka = skey[a], kc = skey[c];
+            if ((ka > kc) == ((a & k) == 0)) {
+              skey[a] = kc;
+              skey[c] = ka;
+              const double tv = sval[a];
+              sval[a] = sval[c];
+              sval[c] = tv;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int i = tid; i < cnt; i += kHT) {
+        K[tb + i] = skey[i];
+        V[tb + i] = sval[i];
+      }
+      __syncthreads();
+    }
+    // merge passes
+    int *sk = K, *dk = K2;
+    double *sv = V, *dv = V2;
+    for (int run = 1024; run < f; run *= 2) {
+      for (int bb = 0; bb < f; bb += 2 * run) {
+        const int na = min(run, f - bb), nb = max(0, min(run, f - bb - run));
+        const int tot = na + nb;
+        const int per = (tot + kHT - 1) / kHT;
+        const int d0 = min(tid * per, tot), d1 = min(d0 + per, tot);
+        if (d0 >= d1) continue;
+        const int* A = sk + bb;
+        const int* B = sk + bb + na;
+        int lo = max(0, d0 - nb), hi = min(d0, na);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (B[d0 - 1 - mid] < A[mid]) hi = mid; else lo = mid + 1;
+        }
+        int i = lo, j = d0 - lo;
+        for (int o = d0; o < d1; ++o) {
+          const bool takeA = j >= nb || (i < na && A[i] < B[j]);
+          if (takeA) {
+            dk[bb + o] = A[i];
+            dv[bb + o] = sv[bb + i];
+            ++i;
+          } else {
+            dk[bb + o] = B[j];
+            dv[bb + o] = sv[bb + na + j];
+            ++j;
+          }
+        }
+      }
+      __syncthreads();
+      int* tk = sk; sk = dk; dk = tk;
+      double* tv = sv; sv = dv; dv = tv;
+    }
+    if (sk != K) {
+      for (int i = tid; i < f; i += kHT) {
+        K[i] = sk[i];
+        V[i] = sv[i];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -153,14 +302,18 @@ cudaError_t launch_scan(const int* in, long long n, long long* out, long long* t
 
 cudaError_t launch_pos_graph(const FactorDev& d, long long* tile_scratch, cudaStream_t s) {
   if (d.n == 0) return cudaSuccess;
-  pos_count_kernel<<<(d.n + 255) / 256, 256, 0, s>>>(d);
-  note_launches(1);
-  cudaError_t e = launch_scan(d.fdeg, d.n, d.fwd_ptr, tile_scratch, s);
-  if (e != cudaSuccess) return e;
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaError_t e = cudaMemsetAsync(d.heavy_count, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  pos_count_kernel<<<(d.n + 255) / 256, 256, 0, s>>>(d);
+  pos_count_heavy_kernel<<<num_sms(dev) * 4, kHT, 0, s>>>(d);
+  note_launches(2);
+  e = launch_scan(d.fdeg, d.n, d.fwd_ptr, tile_scratch, s);
+  if (e != cudaSuccess) return e;
   pos_fill_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(d);
-  note_launches(1);
+  pos_fill_heavy_kernel<<<num_sms(dev) * 2, kHT, 0, s>>>(d);
+  note_launches(2);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,10 @@ constexpr int kDirChunks = 16;
 // CTA holds up to kBigCap (wider columns use a global-memory slab). A vertex is
 // routed to the matching ready queue when it becomes ready.
 constexpr int kSmallCap = 128;
+// vertices of higher degree get a whole CTA in the forward-graph build (K1)
+constexpr int kHeavyDeg = 64;
+// wide-column slab: A (u64), B (f64), C (f64), A2, B2 per entry
+constexpr int kSlabEntryBytes = 40;
 constexpr int kBigCap = 1024;
 
 struct Ctrl {
@@ -50,6 +54,10 @@ struct FactorDev {
   int* fwd_to;
   double* fwd_w;
   int* fdeg;
+  int* heavy_list;     // labels with degree > kHeavyDeg (K1), count in *heavy_count
+  int* heavy_count;
+  int* heavy_key;      // K1 hub sort scratch, same offsets as fwd_to / fwd_w
+  double* heavy_val;
   // dependency counters + ready queues
   int* dp;
   int* queue;   // main queue [n]

@@ -1462,7 +1462,46 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
   int4 rec2 = make_int4(0, 0, 0, 0);
   if (nlev > 0) head_load<FWD>(nxt, rec_of(0), lptr, lidx, lval, rhs_l, dinv_l, lane);
   if (nlev > 1) rec2 = rec_of(1);
+  // L2 bulk prefetch of this CTA's slice of level t + kHeadL2, pipelined so
+  // the prefetching thread never waits: the slice bounds (first and last
+  // chunk record of the CTA's warps) are loaded one level before use.
+  constexpr int kHeadL2 = 4;
+  const bool pf = threadIdx.x == kHThreads - 32;
+  const int wbase = w - wl;
+  auto slice_recs = [&](int t, int4& a, int4& b) {
+    if (t < nlev) {
+      const int L = FWD ? Lfirst + t : Lfirst - t;
+      a = hrec[static_cast<long long>(L) * W + wbase];
+      b = hrec[static_cast<long long>(L) * W + wbase + kHWarps - 1];
+    } else {
+      a = b = make_int4(0, 0, 0, 0);
+    }
+  };
+  auto slice_prefetch = [&](const int4& a, const int4& b) {
+    if (b.w > a.z) {
+      prefetch_l2(lidx + a.z, static_cast<long long>(b.w - a.z) * 4);
+      prefetch_l2(lval + a.z, static_cast<long long>(b.w - a.z) * 8);
+    }
+    if (b.y > a.x) {
+      prefetch_l2(lptr + a.x, static_cast<long long>(b.y - a.x + 1) * 8);
+      prefetch_l2(rhs_l + a.x, static_cast<long long>(b.y - a.x) * 8);
+      if (FWD) prefetch_l2(dinv_l + a.x, static_cast<long long>(b.y - a.x) * 8);
+    }
+  };
+  int4 pa = make_int4(0, 0, 0, 0), pb = pa;
+  if (pf) {
+    for (int tt = 1; tt < kHeadL2 && tt < nlev; ++tt) {
+      int4 a, b;
+      slice_recs(tt, a, b);
+      slice_prefetch(a, b);
+    }
+    slice_recs(kHeadL2, pa, pb);
+  }
   for (int t = 0; t < nlev; ++t) {
+    if (pf) {
+      slice_prefetch(pa, pb);
+      slice_recs(t + kHeadL2 + 1, pa, pb);
+    }
     const HeadPre cur = nxt;
     if (t + 1 < nlev) head_load<FWD>(nxt, rec2, lptr, lidx, lval, rhs_l, dinv_l, lane);
     if (t + 2 < nlev) rec2 = rec_of(t + 2);
@@ -1500,6 +1539,60 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
             const double acc = rhs - part;
             x[jb + src] = acc;
             if (FWD) yd_l[jb + src] = acc * dv;
+          }
+        }
+        __syncwarp();
+      } else if (cnt <= kChunkCap) {
+        // many short rows (wide levels): all products first (8 loads in
+        // flight per lane), then lane-per-row sums from the product buffer
+        for (int base = 0; base < cnt; base += 256) {
+          int ci[8];
+          double gv[8], xv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int e = base + q * 32 + lane;
+            ci[q] = e < cnt ? lidx[eb + e] : 0;
+            gv[q] = e < cnt ? lval[eb + e] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xv[q] = base + q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (base + q * 32 + lane < cnt) pbuf[base + q * 32 + lane] = gv[q] * xv[q];
+        }
+        __syncwarp();
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          int b = 0, e = 0;
+          double rhs = 0.0, dv = 0.0;
+          if (j < je) {
+            b = static_cast<int>(lptr[j] - eb);
+            e = static_cast<int>(lptr[j + 1] - eb);
+            rhs = rhs_l[j];
+            if (FWD) dv = dinv_l[j];
+          }
+          const bool mine = j < je && e - b <= kShortRow;
+          if (mine) {
+            double sum = 0.0;
+            for (int q = b; q < e; ++q) sum += pbuf[q];
+            const double acc = rhs - sum;
+            x[j] = acc;
+            if (FWD) yd_l[j] = acc * dv;
+          }
+          unsigned longs = __ballot_sync(kFull, j < je && !mine);
+          while (longs) {
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int b2 = __shfl_sync(kFull, b, src), e2 = __shfl_sync(kFull, e, src);
+            const double rhs2 = __shfl_sync(kFull, rhs, src), dv2 = __shfl_sync(kFull, dv, src);
+            double part = 0.0;
+            for (int q = b2 + lane; q < e2; q += 32) part += pbuf[q];
+            part = warp_sum(part);
+            if (lane == 0) {
+              const double acc = rhs2 - part;
+              x[j0 + src] = acc;
+              if (FWD) yd_l[j0 + src] = acc * dv2;
+            }
           }
         }
         __syncwarp();
@@ -1672,6 +1765,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
     const int q = qlev(t);
     const int lb = lvs[q], le = lvs[q + 1];
     const int eb = eps[lb], cnt = eps[le] - eb;
+    long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    if (ltime && tid == 0) c0 = clock64();
     if (tid == 32) prefetch_l2_level(t + 6);
     if (tid < cnt) {
 #pragma unroll
@@ -1680,8 +1775,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
         if (e < cnt) pbuf[e] = nval[k] * xs[nidx[k]];
       }
     }
+    if (ltime && tid == 0) c1 = clock64();
     if (t + 1 < nlev && tid < lcount(t + 1)) prefetch(t + 1);
     __syncthreads();
+    if (ltime && tid == 0) c2 = clock64();
     for (int i = lb + warp; i < le; i += kTailThreads / 32) {
       const int rb = eps[i] - eb, re = eps[i + 1] - eb;
       double part = 0.0;
@@ -1694,8 +1791,128 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
         x_l[tail_base + i] = acc;
       }
     }
+    if (ltime && tid == 0) c3 = clock64();
     __syncthreads();
     if (ltime && tid == 0) ltime[t] = globaltimer_ns();
+    if (FWD && ltime && tid == 0) {
+      // diagnostics: cycles of (products, prefetch+sync, rows, sync) of this level
+      unsigned long long* dbg = ltime + 4 * (nlev + 2) + 4 * static_cast<long long>(t);
+      dbg[0] = c1 - c0;
+      dbg[1] = c2 - c1;
+      dbg[2] = c3 - c2;
+      dbg[3] = clock64() - c3;
+    }
+  }
+}
+
+// ---- v4 tail: every level has <= 32 rows (tail width <= 32), so the 32
+// warps split each level's rows into equal (row, slice) pieces: warp w takes
+// slice w % wpr of row w / wpr (wpr = 32 / rows). Each lane holds <= kT4PF of
+// its slice's entries in registers, loaded one level ahead; per level: one
+// product per entry against the shared solution, a warp tree, one partial
+// per warp in shared memory, a barrier, the row's warp 0 sums its wpr
+// partials in fixed order and publishes the value, a barrier. No thread ever
+// walks a long row alone.
+constexpr int kT4PF = 4;
+constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8 + (2 * static_cast<std::size_t>(kT3Rows) + 2) * 4;
+
+template <bool FWD>
+__global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
+    int nt, int nlev, int tail_base, const int* lvl3, const int* ep, const int* eidx, const double* eval,
+    const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
+  extern __shared__ double t4[];
+  double* xs = t4;                                          // [kT3Rows]
+  double* part = t4 + kT3Rows;                              // [32]
+  int* eps = reinterpret_cast<int*>(part + 32);            // [kT3Rows + 1]
+  int* lvs = eps + kT3Rows + 1;                             // [kT3Rows + 1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i <= nt; i += kTailThreads) eps[i] = ep[i];
+  for (int i = tid; i <= nlev; i += kTailThreads) lvs[i] = lvl3[i];
+  for (int i = tid; i < nt; i += kTailThreads)
+    xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];
+  __syncthreads();
+  auto qlev = [&](int t) { return FWD ? t : nlev - 1 - t; };
+  // this warp's piece of level t: row index (-1 none) and entry range
+  auto piece = [&](int t, int& row, int& eb, int& ee, int& wpr) {
+    const int q = qlev(t);
+    const int lb = lvs[q], r = lvs[q + 1] - lb;
+    wpr = r > 0 ? 32 / r : 0;
+    const int ri = wpr > 0 ? warp / wpr : r;
+    row = -1;
+    eb = ee = 0;
+    if (ri < r) {
+      row = lb + ri;
+      const int si = warp - ri * wpr;
+      const int rb = eps[row], len = eps[row + 1] - rb;
+      eb = rb + static_cast<int>((static_cast<long long>(len) * si) / wpr);
+      ee = rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / wpr);
+    }
+  };
+  // Two register sets, each holding one level's piece (loaded two levels
+  // ahead), plus an L2 bulk prefetch kT4L2 levels ahead by one thread: the
+  // tail's entries were evicted by the head sweep's stream, and one level
+  // (~0.3 us) is shorter than an HBM round trip.
+  struct Set {
+    int row, eb, ee, wpr;
+    int idx[kT4PF];
+    double val[kT4PF];
+  };
+  auto load = [&](int t, Set& S) {
+    piece(t, S.row, S.eb, S.ee, S.wpr);
+    if (S.row >= 0) {
+#pragma unroll
+      for (int k = 0; k < kT4PF; ++k) {
+        const int e = S.eb + k * 32 + lane;
+        S.idx[k] = e < S.ee ? eidx[e] : 0;
+        S.val[k] = e < S.ee ? eval[e] : 0.0;
+      }
+    }
+  };
+  auto l2 = [&](int t) {
+    if (t >= nlev) return;
+    const int q = qlev(t);
+    const int eb2 = eps[lvs[q]], ee2 = eps[lvs[q + 1]];
+    prefetch_l2(eidx + eb2, static_cast<long long>(ee2 - eb2) * 4);
+    prefetch_l2(eval + eb2, static_cast<long long>(ee2 - eb2) * 8);
+  };
+  constexpr int kT4L2 = 8;
+  if (tid == 32)
+    for (int t = 2; t < kT4L2; ++t) l2(t);
+  auto step = [&](int t, Set& S) {
+    const int crow = S.row, ceb = S.eb, cee = S.ee, cwpr = S.wpr;
+    double p = 0.0;
+    if (crow >= 0) {
+#pragma unroll
+      for (int k = 0; k < kT4PF; ++k)
+        if (ceb + k * 32 + lane < cee) p += S.val[k] * xs[S.idx[k]];
+      for (int e = ceb + kT4PF * 32 + lane; e < cee; e += 32) p += eval[e] * xs[eidx[e]];  // overflow
+    }
+    if (t + 2 < nlev) load(t + 2, S);
+    if (tid == 32) l2(t + kT4L2);
+    if (crow >= 0) {
+      p = warp_sum(p);
+      if (lane == 0) part[warp] = p;
+    }
+    __syncthreads();
+    if (crow >= 0 && warp % cwpr == 0) {  // the row's first warp publishes it
+      double sp = lane < cwpr ? part[warp + lane] : 0.0;
+      sp = warp_sum(sp);
+      if (lane == 0) {
+        const double acc = xs[crow] - sp;
+        xs[crow] = acc;
+        x_l[tail_base + crow] = acc;
+      }
+    }
+    __syncthreads();
+    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
+  };
+  Set A, B;
+  A.row = B.row = -1;
+  if (nlev > 0) load(0, A);
+  if (nlev > 1) load(1, B);
+  for (int t = 0; t < nlev; t += 2) {
+    step(t, A);
+    if (t + 1 < nlev) step(t + 1, B);
   }
 }
 
@@ -2199,7 +2416,7 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
     }
   }
   const char* env = std::getenv("PARAC_TAIL_WIDTH");
-  const int wt = env ? std::atoi(env) : 64;
+  const int wt = std::min(32, env ? std::atoi(env) : 32);  // tail4 needs <= 32 rows per level
   int L0 = depth;
   if (wt > 0) {
     while (L0 >= 1 && off[L0 + 1] - off[L0] <= wt) --L0;
@@ -2249,6 +2466,8 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   if (!attr) {
     check(cudaFuncSetAttribute(tail3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
     check(cudaFuncSetAttribute(tail3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
+    check(cudaFuncSetAttribute(tail4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
+    check(cudaFuncSetAttribute(tail4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
     attr = true;
   }
   check(cudaGetLastError(), "v3 layout");
@@ -2328,7 +2547,7 @@ void prepare_factor(const SolveInputs& in) {
     build_level_layout(in, s, sms, true);
   }
   if (std::getenv("PARAC_SWEEP_PROFILE")) {
-    const std::size_t need = 4 * (static_cast<std::size_t>(s.depth) + 2);
+    const std::size_t need = 16 * (static_cast<std::size_t>(s.depth) + 2);
     if (s.cap_ltime < need) {
       dalloc(s.ltime, need);
       s.cap_ltime = need;
@@ -2389,10 +2608,10 @@ struct Solver {
             "head forward");
       note_launches(1);
       if (nt > 0) {
-        tail3_kernel<true><<<1, kTailThreads, kT3Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_fep,
+        tail4_kernel<true><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_fep,
                                                              s.t3_fidx, s.t3_fval, s.tail_s, s.dinv_l, nullptr,
                                                              s.yf, lt ? lt + (D + 2) : nullptr);
-        tail3_kernel<false><<<1, kTailThreads, kT3Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_bep,
+        tail4_kernel<false><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_bep,
                                                               s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
                                                               nullptr, s.dinv_l, s.yf, s.zb,
                                                               lt ? lt + 2 * (D + 2) : nullptr);
@@ -2640,7 +2859,7 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
     if (in.state->ltime) {  // diagnostics: [H, depth, L0] then 4 x (depth+2) timestamps
       const SolveState& ss = *in.state;
-      std::vector<unsigned long long> t(4 * (static_cast<std::size_t>(ss.depth) + 2));
+      std::vector<unsigned long long> t(16 * (static_cast<std::size_t>(ss.depth) + 2));
       check(cudaMemcpy(t.data(), ss.ltime, t.size() * 8, cudaMemcpyDeviceToHost), "d2h");
       if (FILE* f = std::fopen(std::getenv("PARAC_SWEEP_PROFILE"), "wb")) {
         const bool v3 = ss.cap_v3 > 0;

@@ -155,6 +155,54 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
   return f;
 }
 
+// Many independent problems in one device pass (BASELINE config[4]); no
+// reference counterpart (the reference loops over factor_randomized). Factor i
+// is same_values-identical to factor_randomized(graphs[i], orderings[i], seeds[i]).
+inline std::vector<LdlFactor> factor_batch_gpu(std::span<const LaplacianGraph> graphs,
+                                               std::span<const Ordering> orderings,
+                                               std::span<const std::uint64_t> seeds,
+                                               const GpuOptions& options = {}) {
+  using namespace gpu_detail;
+  const std::size_t count = graphs.size();
+  if (orderings.size() != count || seeds.size() != count || count == 0)
+    throw Error(Errc::dimension_mismatch, "batch lists differ in length");
+  auto ctx = make_ctx(options.device);
+  std::vector<CsrView> views;
+  views.reserve(count);
+  std::vector<parac_csr> csrs(count);
+  std::vector<const std::int32_t*> perms(count);
+  for (std::size_t i = 0; i < count; ++i) {
+    if (orderings[i].size() != graphs[i].num_vertices())
+      throw Error(Errc::dimension_mismatch, "ordering size does not match the graph");
+    views.emplace_back(graphs[i]);
+    csrs[i] = views.back().csr;
+    perms[i] = orderings[i].perm.data();
+  }
+  parac_gpu_options o;
+  parac_gpu_default_options(&o);
+  o.column_arena_entries = options.arena_budget;
+  o.fill_pool_entries = options.fill_pool_budget;
+  o.watchdog_seconds = options.watchdog_seconds;
+  parac_gpu_factor_info info{};
+  check(parac_gpu_factor_batch(ctx.get(), static_cast<std::int32_t>(count), csrs.data(), perms.data(),
+                               seeds.data(), &o, &info));
+  std::vector<LdlFactor> out(count);
+  for (std::size_t i = 0; i < count; ++i) {
+    std::int64_t z = 0;
+    check(parac_gpu_batch_nnz(ctx.get(), static_cast<std::int32_t>(i), &z));
+    LdlFactor& f = out[i];
+    f.n = graphs[i].num_vertices();
+    f.col_ptr.resize(static_cast<std::size_t>(f.n) + 1);
+    f.rows.resize(static_cast<std::size_t>(z));
+    f.values.resize(static_cast<std::size_t>(z));
+    f.diag.resize(static_cast<std::size_t>(f.n));
+    f.perm = orderings[i].perm;
+    check(parac_gpu_download_batch(ctx.get(), static_cast<std::int32_t>(i), f.col_ptr.data(), f.rows.data(),
+                                   f.values.data(), f.diag.data()));
+  }
+  return out;
+}
+
 inline std::pair<std::vector<double>, SolveReport> pcg_solve_gpu(const LaplacianGraph& graph,
                                                                  const LdlFactor& factor,
                                                                  std::span<const double> b,

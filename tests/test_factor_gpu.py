@@ -127,3 +127,17 @@ def test_batch_union_equals_standalone(gpu_ctx, port, gold):
         assert_same(f, factor_from_port(port.factor(g, perm, seed)), nm)
         e = next(x for x in gold["factors"] if x["name"] == nm)
         assert f"{f.checksum():016x}" == e["checksum"], nm
+
+
+@pytest.mark.parametrize("scale", [15, 16])
+def test_rmat_wide_columns_byte_identical(gpu_ctx, port, scale):
+    # R-MAT hubs exceed the shared-memory column capacity (1024 raw entries):
+    # slab tile sort + merge passes, staged serial chains, coarse-indexed
+    # sampling search -- still byte-identical to the reference restatement
+    g = P.gen_rmat(scale, 16, 0)
+    perm = P.ordering_random(g.n, 0).perm
+    f, st = gpu_factor(gpu_ctx, g, perm, 0)
+    assert st.large_columns > 0, "no column took the wide path"
+    want = port.factor(g, perm, 0)
+    assert_same(f, factor_from_port(want))
+    assert np.array_equal(st.fills_received, want["fills_received"])

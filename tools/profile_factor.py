@@ -131,6 +131,21 @@ def main():
         "levels+fence": span(sub[chs, 4], sub[chs, 5]),
         "decrement": span(sub[chs, 5], tt[chs, 6]),
     }
+    # hand-off analysis along the critical path: kept (same warp/CTA continued)
+    # vs claimed from a ready queue; small (warp) vs big (CTA) eliminator
+    kept = sub[chs, 7] == 1
+    bigc = (sub[chs, 6] & 0xff) == 0xff
+    hops = hop[chs]
+    def stat(sel):
+        return {"count": int(sel.sum()), "hop_us_mean": float(hops[sel].mean()) if sel.any() else None}
+    prev_big = np.concatenate([[False], bigc[:-1]])
+    out["critical_path"]["handoffs"] = {
+        "kept": stat(kept), "claimed": stat(~kept),
+        "claimed_big_after_small": stat(~kept & bigc & ~prev_big),
+        "claimed_big_after_big": stat(~kept & bigc & prev_big),
+        "claimed_small": stat(~kept & ~bigc),
+        "big_eliminations": int(bigc.sum()),
+    }
     print(json.dumps(out, indent=1))
     if args.json:
         with open(args.json, "w") as fh:

@@ -20,7 +20,8 @@ for _ in range(3):
 lv, depth = P.schedule_levels_gpu(f, ctx=ctx)
 raw = open(path, "rb").read()
 H, D, nt = np.frombuffer(raw[:12], np.int32)
-t = np.frombuffer(raw[12:], np.uint64).astype(np.int64).reshape(4, D + 2)
+t_all = np.frombuffer(raw[12:], np.uint64).astype(np.int64)
+t = t_all[:4 * (D + 2)].reshape(4, D + 2)
 w = np.bincount(lv, minlength=D + 2)
 rowlen = np.bincount(f.rows, minlength=g.n)
 collen = np.diff(f.col_ptr)
@@ -43,3 +44,9 @@ if nt:
     show("tail fwd", t[1], np.arange(H + 1, D + 1), ent_f)
     show("tail bwd", t[2], np.arange(D, H, -1), ent_b)
 show("head bwd", t[3], np.arange(H, 0, -1), ent_b)
+if nt:
+    nlev = D - H
+    dbg = t_all[(D + 2) + 4 * (nlev + 2):(D + 2) + 4 * (nlev + 2) + 4 * nlev].reshape(nlev, 4)
+    print("tail fwd cycles per level (thread 0): products / prefetch+sync / rows / sync")
+    for lo, hi in ((0, 50), (50, 200), (200, 500), (500, nlev)):
+        print(f"   steps [{lo},{hi}):", dbg[lo:hi].mean(axis=0).round(0))

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -102,7 +104,7 @@ struct parac_gpu_ctx {
   int batch_count = 0;
   std::vector<long long> batch_base_h;
   DevBuf<int> pos_pid;
-  DevBuf<long long> pid_base;
+  DevBuf<long long> pid_base, pid_ebase;
   DevBuf<unsigned long long> pid_seed;
   // solve state
   SolveState solve;
@@ -213,6 +215,11 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   const double wd = o.watchdog_seconds > 0 ? o.watchdog_seconds : 60.0;
   d.watchdog_ns = static_cast<unsigned long long>(wd * 1e9);
   d.verify = o.verify;
+  {  // PARAC_CLAIM_SLEEP="a,b,c" (ns) overrides the claim backoff tiers (tuning)
+    unsigned t[3] = {512, 4096, 16384};
+    if (const char* e = std::getenv("PARAC_CLAIM_SLEEP")) std::sscanf(e, "%u,%u,%u", &t[0], &t[1], &t[2]);
+    for (int i = 0; i < 3; ++i) d.sleep_ns[i] = t[i];
+  }
   d.delay_ns = o.delay_ns;
   d.vtimes = nullptr;
   d.vsub = nullptr;
@@ -372,51 +379,54 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     require_ctx(ctx);
     if (count <= 0 || !graphs || !perms || !seeds) throw Failure{dimension_mismatch, "empty batch"};
     long long N = 0, NNZ = 0;
-    std::vector<long long> base(static_cast<std::size_t>(count) + 1, 0);
+    std::vector<long long> base(static_cast<std::size_t>(count) + 1, 0), ebase(base);
+    std::vector<unsigned long long> ps(static_cast<std::size_t>(count));
     for (int i = 0; i < count; ++i) {
       if (graphs[i].n < 0) throw Failure{dimension_mismatch, "bad graph in batch"};
       base[i] = N;
+      ebase[i] = NNZ;
       N += graphs[i].n;
       NNZ += graphs[i].ptr[graphs[i].n];
-    }
-    base[count] = N;
-    if (N > 2147483647LL) throw Failure{dimension_mismatch, "batch exceeds 2^31 vertices"};
-    std::vector<int64_t> ptr(static_cast<std::size_t>(N) + 1);
-    std::vector<int32_t> adj(static_cast<std::size_t>(std::max<long long>(NNZ, 1)));
-    std::vector<double> w(static_cast<std::size_t>(std::max<long long>(NNZ, 1)));
-    std::vector<int32_t> perm(static_cast<std::size_t>(std::max<long long>(N, 1)));
-    std::vector<int> pid(static_cast<std::size_t>(std::max<long long>(N, 1)));
-    std::vector<unsigned long long> ps(static_cast<std::size_t>(count));
-    long long e0 = 0;
-    for (int i = 0; i < count; ++i) {
-      const parac_csr& g = graphs[i];
-      const int b = static_cast<int>(base[i]);
-      for (int v = 0; v < g.n; ++v) {
-        ptr[b + v] = e0 + g.ptr[v];
-        perm[b + v] = perms[i][v] + b;
-        pid[b + v] = i;
-      }
-      const long long m = g.ptr[g.n];
-      for (long long e = 0; e < m; ++e) {
-        adj[e0 + e] = g.adj[e] + b;
-        w[e0 + e] = g.w[e];
-      }
-      e0 += m;
       ps[i] = derive_seed(seeds[i], kSaltSampling);
     }
-    ptr[N] = e0;
-    parac_csr u{static_cast<int32_t>(N), ptr.data(), adj.data(), w.data()};
-    const int rc = parac_gpu_upload(ctx, &u, perm.data());
-    if (rc) throw Failure{rc, parac_gpu_last_error()};
+    base[count] = N;
+    ebase[count] = NNZ;
+    if (N > 2147483647LL) throw Failure{dimension_mismatch, "batch exceeds 2^31 vertices"};
+    // Problems are copied straight into their slices of the device union (from
+    // the caller's buffers; pinned memory copies at full PCIe/C2C rate), then
+    // one pass adds the label / edge offsets on the device.
     cudaStream_t s = ctx->stream;
-    ctx->pos_pid.ensure(static_cast<std::size_t>(std::max<long long>(N, 1)));
+    const std::size_t nn = static_cast<std::size_t>(std::max<long long>(N, 1));
+    const std::size_t ee = static_cast<std::size_t>(std::max<long long>(NNZ, 1));
+    ctx->ptr.ensure(nn + 1);
+    ctx->adj.ensure(ee);
+    ctx->w.ensure(ee);
+    ctx->perm.ensure(nn);
+    ctx->pos_pid.ensure(nn);
     ctx->pid_base.ensure(static_cast<std::size_t>(count) + 1);
+    ctx->pid_ebase.ensure(static_cast<std::size_t>(count) + 1);
     ctx->pid_seed.ensure(static_cast<std::size_t>(count));
-    // positions: problem i owns positions [base_i, base_{i+1})
-    check(cudaMemcpyAsync(ctx->pos_pid.p, pid.data(), sizeof(int) * N, cudaMemcpyHostToDevice, s), "h2d");
+    for (int i = 0; i < count; ++i) {
+      const parac_csr& g = graphs[i];
+      const long long m = g.ptr[g.n];
+      check(cudaMemcpyAsync(ctx->ptr.p + base[i], g.ptr, sizeof(long long) * g.n, cudaMemcpyHostToDevice, s), "h2d");
+      if (m > 0) {
+        check(cudaMemcpyAsync(ctx->adj.p + ebase[i], g.adj, sizeof(int) * m, cudaMemcpyHostToDevice, s), "h2d");
+        check(cudaMemcpyAsync(ctx->w.p + ebase[i], g.w, sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
+      }
+      if (g.n > 0)
+        check(cudaMemcpyAsync(ctx->perm.p + base[i], perms[i], sizeof(int) * g.n, cudaMemcpyHostToDevice, s), "h2d");
+    }
     check(cudaMemcpyAsync(ctx->pid_base.p, base.data(), sizeof(long long) * (count + 1), cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaMemcpyAsync(ctx->pid_ebase.p, ebase.data(), sizeof(long long) * (count + 1), cudaMemcpyHostToDevice, s), "h2d");
     check(cudaMemcpyAsync(ctx->pid_seed.p, ps.data(), sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, s), "h2d");
+    check(launch_batch_offsets(count, N, NNZ, ctx->pid_base.p, ctx->pid_ebase.p, ctx->ptr.p, ctx->adj.p,
+                               ctx->perm.p, ctx->pos_pid.p, s), "batch offsets");
     check(cudaStreamSynchronize(s), "h2d sync");
+    ctx->n = static_cast<int>(N);
+    ctx->nnz = NNZ;
+    ctx->f_n = -1;
+    solve_invalidate(ctx->solve);
     ctx->batch_count = count;
     ctx->batch_base_h = base;
   });
@@ -466,9 +476,7 @@ int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, in
     if (values && z) check(cudaMemcpyAsync(values, ctx->vals.p + z0, sizeof(double) * z, cudaMemcpyDeviceToHost, s), "d2h");
     if (diag && n) check(cudaMemcpyAsync(diag, ctx->diag.p + b, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "d2h");
     check(cudaStreamSynchronize(s), "d2h sync");
-    for (long long k = 0; k <= n; ++k) col_ptr[k] -= z0;
-    if (rows)
-      for (long long t = 0; t < z; ++t) rows[t] -= static_cast<int>(b);
+    for (long long k = 0; k <= n; ++k) col_ptr[k] -= z0;  // rows were made local on the device
   });
 }
 
@@ -509,6 +517,11 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
     ctx->f_nnz = Z;
     ctx->f_has_stats = true;
     ctx->f_external = false;
+    if (ctx->batch_count > 0) {  // each problem's rows in its own position space
+      check(launch_batch_local_rows(n, ctx->col_ptr.p, ctx->pos_pid.p, ctx->pid_base.p, ctx->rows.p, ctx->stream),
+            "batch rows");
+      check(cudaStreamSynchronize(ctx->stream), "batch rows sync");
+    }
     solve_invalidate_factor(ctx->solve);
     if (info) {
       std::memset(info, 0, sizeof(*info));
@@ -653,6 +666,7 @@ SolveInputs solve_inputs(parac_gpu_ctx* ctx) {
   in.diag = ctx->f_external ? ctx->f_diag_ext.p : ctx->diag.p;
   in.perm = ctx->f_external ? ctx->f_perm_ext.p : ctx->perm.p;
   in.level = ctx->f_external ? nullptr : ctx->level.p;
+  in.batch = ctx->batch_count;
   in.stream = ctx->stream;
   in.device = ctx->device;
   in.state = &ctx->solve;

@@ -110,9 +110,9 @@ __device__ int claim(const FactorDev& d, bool big) {
     // trips, so they run on every 8th poll only.
     if ((iter & 7) == 0 || ns >= 512) {  // long sleepers re-probe every time
       if (idx < 16 || ld_relaxed(&queue[idx - 16]) >= 0) ns = 32;
-      else if (idx < 256 || ld_relaxed(&queue[idx - 256]) >= 0) ns = 512;
-      else if (idx < 1024 || ld_relaxed(&queue[idx - 1024]) >= 0) ns = 4096;
-      else ns = 16384;  // far waiters must not load the L2 (see wait_level)
+      else if (idx < 256 || ld_relaxed(&queue[idx - 256]) >= 0) ns = d.sleep_ns[0];
+      else if (idx < 1024 || ld_relaxed(&queue[idx - 1024]) >= 0) ns = d.sleep_ns[1];
+      else ns = d.sleep_ns[2];  // far waiters must not load the L2
     }
     __nanosleep(ns);
     v = ld_relaxed(&queue[idx]);

@@ -337,4 +337,65 @@ cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, d
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- batch
+namespace {
+__device__ __forceinline__ int batch_of(const long long* base, int count, long long x) {
+  int lo = 0, hi = count - 1;  // last i with base[i] <= x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (base[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__global__ void batch_vertex_kernel(int count, long long N, long long NNZ, const long long* base,
+                                    const long long* ebase, long long* ptr, int* perm, int* pos_pid) {
+  for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j <= N;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (j == N) {
+      ptr[N] = NNZ;
+      continue;
+    }
+    const int i = batch_of(base, count, j);
+    ptr[j] += ebase[i];
+    perm[j] += static_cast<int>(base[i]);
+    pos_pid[j] = i;  // positions of problem i are [base_i, base_{i+1}) too
+  }
+}
+__global__ void batch_edge_kernel(int count, long long NNZ, const long long* ebase, const long long* base, int* adj) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < NNZ;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    adj[e] += static_cast<int>(base[batch_of(ebase, count, e)]);
+}
+__global__ void batch_rows_kernel(int n, const long long* col_ptr, const int* pos_pid, const long long* base,
+                                  int* rows) {
+  const int lane = lane_id();
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = gw; k < n; k += nw) {
+    const int b = static_cast<int>(base[pos_pid[k]]);
+    for (long long t = col_ptr[k] + lane; t < col_ptr[k + 1]; t += 32) rows[t] -= b;
+  }
+}
+}  // namespace
+
+cudaError_t launch_batch_offsets(int count, long long N, long long NNZ, const long long* base,
+                                 const long long* ebase, long long* ptr, int* adj, int* perm, int* pos_pid,
+                                 cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  batch_vertex_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(count, N, NNZ, base, ebase, ptr, perm, pos_pid);
+  if (NNZ > 0) batch_edge_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(count, NNZ, ebase, base, adj);
+  note_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_local_rows(int n, const long long* col_ptr, const int* pos_pid, const long long* base,
+                                    int* rows, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  batch_rows_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(n, col_ptr, pos_pid, base, rows);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
 }  // namespace parac_gpu

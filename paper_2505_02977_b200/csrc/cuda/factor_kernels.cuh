@@ -92,6 +92,7 @@ struct FactorDev {
   unsigned long long watchdog_ns;
   int verify;
   int delay_ns;
+  unsigned sleep_ns[3];  // claim() backoff by distance to the publishing front (16-256, 256-1024, >1024 slots)
   unsigned long long* vtimes;  // optional [8n] phase timestamps per position
   unsigned long long* vsub;    // optional [8n] sub-phase timestamps per position
 };
@@ -106,5 +107,12 @@ cudaError_t launch_scan(const int* in, long long n, long long* out, long long* t
                         cudaStream_t s);
 long long scan_tiles(long long n);
 int eliminate_occupancy_grid(int device);
+// batch (disjoint union): add label / edge offsets to the staged union, and
+// rebase each problem's factor rows to its own position space
+cudaError_t launch_batch_offsets(int count, long long N, long long NNZ, const long long* base,
+                                 const long long* ebase, long long* ptr, int* adj, int* perm, int* pos_pid,
+                                 cudaStream_t s);
+cudaError_t launch_batch_local_rows(int n, const long long* col_ptr, const int* pos_pid, const long long* base,
+                                    int* rows, cudaStream_t s);
 
 }  // namespace parac_gpu

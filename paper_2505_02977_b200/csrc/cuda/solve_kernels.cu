@@ -1814,102 +1814,110 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
 // partials in fixed order and publishes the value, a barrier. No thread ever
 // walks a long row alone.
 constexpr int kT4PF = 4;
-constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8 + (2 * static_cast<std::size_t>(kT3Rows) + 2) * 4;
+constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8;
+
+// Piece table of the tail (built once per factor, per direction): level t's
+// warp w piece = {row (tail index, -1 none), eb, ee, wpr}. Keeping the integer
+// divisions of the (row, slice) split out of the level loop matters: they
+// were ~half of a level's dependent instruction chain.
+__global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const int* ep, int4* pieces) {
+  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int warp = threadIdx.x & 31;  // one thread per (level, warp)
+  if (t >= nlev) return;
+  const int q = fwd ? t : nlev - 1 - t;
+  const int lb = lvl3[q], r = lvl3[q + 1] - lb;
+  const int wpr = r > 0 ? 32 / r : 0;
+  const int ri = wpr > 0 ? warp / wpr : r;
+  int4 pc = make_int4(-1, 0, 0, 0);
+  if (ri < r) {
+    const int row = lb + ri;
+    const int si = warp - ri * wpr;
+    const int rb = ep[row], len = ep[row + 1] - rb;
+    // .w = number of slices for the row's FIRST slice (it combines them), else 0
+    pc = make_int4(row, rb + static_cast<int>((static_cast<long long>(len) * si) / wpr),
+                   rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / wpr), si == 0 ? wpr : 0);
+  }
+  pieces[static_cast<long long>(t) * 32 + warp] = pc;
+}
 
 template <bool FWD>
 __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
-    int nt, int nlev, int tail_base, const int* lvl3, const int* ep, const int* eidx, const double* eval,
+    int nt, int nlev, int tail_base, const int4* pieces, const int* eidx, const double* eval,
     const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
   extern __shared__ double t4[];
   double* xs = t4;                                          // [kT3Rows]
   double* part = t4 + kT3Rows;                              // [32]
-  int* eps = reinterpret_cast<int*>(part + 32);            // [kT3Rows + 1]
-  int* lvs = eps + kT3Rows + 1;                             // [kT3Rows + 1]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i <= nt; i += kTailThreads) eps[i] = ep[i];
-  for (int i = tid; i <= nlev; i += kTailThreads) lvs[i] = lvl3[i];
   for (int i = tid; i < nt; i += kTailThreads)
     xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];
-  __syncthreads();
-  auto qlev = [&](int t) { return FWD ? t : nlev - 1 - t; };
-  // this warp's piece of level t: row index (-1 none) and entry range
-  auto piece = [&](int t, int& row, int& eb, int& ee, int& wpr) {
-    const int q = qlev(t);
-    const int lb = lvs[q], r = lvs[q + 1] - lb;
-    wpr = r > 0 ? 32 / r : 0;
-    const int ri = wpr > 0 ? warp / wpr : r;
-    row = -1;
-    eb = ee = 0;
-    if (ri < r) {
-      row = lb + ri;
-      const int si = warp - ri * wpr;
-      const int rb = eps[row], len = eps[row + 1] - rb;
-      eb = rb + static_cast<int>((static_cast<long long>(len) * si) / wpr);
-      ee = rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / wpr);
-    }
-  };
-  // Two register sets, each holding one level's piece (loaded two levels
-  // ahead), plus an L2 bulk prefetch kT4L2 levels ahead by one thread: the
-  // tail's entries were evicted by the head sweep's stream, and one level
-  // (~0.3 us) is shorter than an HBM round trip.
+  // Two register sets hold the pieces of levels t and t+1 (entries loaded two
+  // levels ahead), the piece records are loaded three levels ahead, and one
+  // thread bulk-prefetches entry ranges into L2 eight levels ahead.
   struct Set {
-    int row, eb, ee, wpr;
+    int4 pc;
     int idx[kT4PF];
     double val[kT4PF];
   };
-  auto load = [&](int t, Set& S) {
-    piece(t, S.row, S.eb, S.ee, S.wpr);
-    if (S.row >= 0) {
+  auto piece_at = [&](int t) { return t < nlev ? pieces[static_cast<long long>(t) * 32 + warp] : make_int4(-1, 0, 0, 0); };
+  auto load = [&](const int4 pc, Set& S) {
+    S.pc = pc;
+    if (pc.x >= 0) {
 #pragma unroll
       for (int k = 0; k < kT4PF; ++k) {
-        const int e = S.eb + k * 32 + lane;
-        S.idx[k] = e < S.ee ? eidx[e] : 0;
-        S.val[k] = e < S.ee ? eval[e] : 0.0;
+        const int e = pc.y + k * 32 + lane;
+        S.idx[k] = e < pc.z ? eidx[e] : 0;
+        S.val[k] = e < pc.z ? eval[e] : 0.0;
       }
     }
   };
-  auto l2 = [&](int t) {
-    if (t >= nlev) return;
-    const int q = qlev(t);
-    const int eb2 = eps[lvs[q]], ee2 = eps[lvs[q + 1]];
-    prefetch_l2(eidx + eb2, static_cast<long long>(ee2 - eb2) * 4);
-    prefetch_l2(eval + eb2, static_cast<long long>(ee2 - eb2) * 8);
-  };
   constexpr int kT4L2 = 8;
+  auto l2 = [&](int t) {  // whole level: first and last piece of warp 0 / 31
+    if (t >= nlev) return;
+    const int4 f = pieces[static_cast<long long>(t) * 32];
+    int4 l = pieces[static_cast<long long>(t) * 32 + 31];
+    for (int w = 30; l.x < 0 && w >= 0; --w) l = pieces[static_cast<long long>(t) * 32 + w];
+    if (f.x >= 0 && l.z > f.y) {
+      prefetch_l2(eidx + f.y, static_cast<long long>(l.z - f.y) * 4);
+      prefetch_l2(eval + f.y, static_cast<long long>(l.z - f.y) * 8);
+    }
+  };
   if (tid == 32)
     for (int t = 2; t < kT4L2; ++t) l2(t);
+  Set A, B;
+  A.pc = B.pc = make_int4(-1, 0, 0, 0);
+  int4 pnext = piece_at(2);
+  if (nlev > 0) load(piece_at(0), A);
+  if (nlev > 1) load(piece_at(1), B);
+  __syncthreads();
   auto step = [&](int t, Set& S) {
-    const int crow = S.row, ceb = S.eb, cee = S.ee, cwpr = S.wpr;
+    const int4 pc = S.pc;
     double p = 0.0;
-    if (crow >= 0) {
+    if (pc.x >= 0) {
 #pragma unroll
       for (int k = 0; k < kT4PF; ++k)
-        if (ceb + k * 32 + lane < cee) p += S.val[k] * xs[S.idx[k]];
-      for (int e = ceb + kT4PF * 32 + lane; e < cee; e += 32) p += eval[e] * xs[eidx[e]];  // overflow
+        if (pc.y + k * 32 + lane < pc.z) p += S.val[k] * xs[S.idx[k]];
+      for (int e = pc.y + kT4PF * 32 + lane; e < pc.z; e += 32) p += eval[e] * xs[eidx[e]];  // overflow
     }
-    if (t + 2 < nlev) load(t + 2, S);
+    if (t + 2 < nlev) load(pnext, S);  // level t+2 into the set just consumed
+    pnext = piece_at(t + 3);
     if (tid == 32) l2(t + kT4L2);
-    if (crow >= 0) {
+    if (pc.x >= 0) {
       p = warp_sum(p);
       if (lane == 0) part[warp] = p;
     }
     __syncthreads();
-    if (crow >= 0 && warp % cwpr == 0) {  // the row's first warp publishes it
-      double sp = lane < cwpr ? part[warp + lane] : 0.0;
+    if (pc.x >= 0 && pc.w > 0) {  // the row's first warp publishes it
+      double sp = lane < pc.w ? part[warp + lane] : 0.0;
       sp = warp_sum(sp);
       if (lane == 0) {
-        const double acc = xs[crow] - sp;
-        xs[crow] = acc;
-        x_l[tail_base + crow] = acc;
+        const double acc = xs[pc.x] - sp;
+        xs[pc.x] = acc;
+        x_l[tail_base + pc.x] = acc;
       }
     }
     __syncthreads();
     if (ltime && tid == 0) ltime[t] = globaltimer_ns();
   };
-  Set A, B;
-  A.row = B.row = -1;
-  if (nlev > 0) load(0, A);
-  if (nlev > 1) load(1, B);
   for (int t = 0; t < nlev; t += 2) {
     step(t, A);
     if (t + 1 < nlev) step(t + 1, B);
@@ -2462,6 +2470,15 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   check(cudaStreamSynchronize(st), "v3 sync");
   tail_rel_idx_kernel<<<sms * 4, 256, 0, st>>>(hb[1], lbe, base, s.lb_idx);
   note_launches(4);
+  const std::size_t npc = static_cast<std::size_t>(nlev) * 32;
+  if (s.cap_t4 < npc) {
+    dalloc(s.t4_fpc, npc);
+    dalloc(s.t4_bpc, npc);
+    s.cap_t4 = npc;
+  }
+  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 1, s.t3_lvl, s.t3_fep, s.t4_fpc);
+  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 0, s.t3_lvl, s.t3_bep, s.t4_bpc);
+  note_launches(2);
   static bool attr = false;
   if (!attr) {
     check(cudaFuncSetAttribute(tail3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
@@ -2608,10 +2625,10 @@ struct Solver {
             "head forward");
       note_launches(1);
       if (nt > 0) {
-        tail4_kernel<true><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_fep,
-                                                             s.t3_fidx, s.t3_fval, s.tail_s, s.dinv_l, nullptr,
-                                                             s.yf, lt ? lt + (D + 2) : nullptr);
-        tail4_kernel<false><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t3_lvl, s.t3_bep,
+        tail4_kernel<true><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_fpc, s.t3_fidx,
+                                                             s.t3_fval, s.tail_s, s.dinv_l, nullptr, s.yf,
+                                                             lt ? lt + (D + 2) : nullptr);
+        tail4_kernel<false><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_bpc,
                                                               s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
                                                               nullptr, s.dinv_l, s.yf, s.zb,
                                                               lt ? lt + 2 * (D + 2) : nullptr);
@@ -2780,6 +2797,8 @@ void need_graph(const SolveInputs& in) {
 }
 void need_factor(const SolveInputs& in) {
   if (in.f_n < 0) throw Failure{dimension_mismatch, "no resident factor"};
+  if (in.batch > 0)
+    throw Failure{dimension_mismatch, "the resident factor is a batch: download it and solve each problem separately"};
 }
 
 }  // namespace
@@ -2796,6 +2815,7 @@ void solve_release(SolveState& s) {
   dfree(s.f_chunk); dfree(s.f_cbase); dfree(s.b_chunk); dfree(s.b_cbase); dfree(s.lvl_target); dfree(s.ltime);
   dfree(s.hrec_gf); dfree(s.hrec_gb);
   dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
+  dfree(s.t4_fpc); dfree(s.t4_bpc);
   dfree(s.t3_lvl); dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_bep); dfree(s.t3_fval);
   s = SolveState{};
 }

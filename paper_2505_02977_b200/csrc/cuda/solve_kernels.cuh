@@ -54,7 +54,8 @@ struct SolveState {
   long long t3_bbase = 0;  // lb_ptr[t3_base]
   int *t3_lvl = nullptr, *t3_fep = nullptr, *t3_fidx = nullptr, *t3_bep = nullptr;
   double* t3_fval = nullptr;
-  std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0;  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
+  std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0, cap_t4 = 0;
+  int4 *t4_fpc = nullptr, *t4_bpc = nullptr;  // tail piece tables [nlev][32]  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
   std::size_t cap_ltime = 0;
   std::size_t cap_lz = 0, cap_fchunk = 0, cap_bchunk = 0, cap_levels = 0;
   std::size_t cap_tail = 0, cap_tail_nnz = 0;
@@ -89,6 +90,7 @@ struct SolveInputs {
   const double* diag;
   const int* perm;
   const int* level;  // ASAP levels from K3 (nullptr: compute them)
+  int batch;         // >0: the resident factor is a batch (per-problem rows); no solve
   cudaStream_t stream;
   int device;
   SolveState* state;

@@ -7,6 +7,27 @@
 #include <random>
 #include "../../paper_2505_02977_b200/csrc/cuda/solve_kernels.cu"
 
+
+// floor experiments: a 1024-thread CTA doing only the per-level barriers (+ options)
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) floor_kernel(int nlev, const int* eidx, unsigned long long* lt, double* sink) {
+  __shared__ double xs[1024];
+  const int tid = threadIdx.x;
+  xs[tid] = tid;
+  __syncthreads();
+  double acc = 0;
+  for (int t = 0; t < nlev; ++t) {
+    if (MODE == 1 && tid == 32) prefetch_l2(eidx + t * 64, 256);
+    if (MODE == 2 && tid < 32) acc += eidx[(t + 2) * 32 + tid];
+    if (tid < 32) acc += xs[(t + tid) & 1023];
+    __syncthreads();
+    if (tid == 0) xs[t & 1023] = acc;
+    __syncthreads();
+    if (MODE == 3 && tid == 0) lt[t] = globaltimer_ns();
+  }
+  if (tid == 0) sink[0] = acc;
+}
+
 int main() {
   using namespace parac_gpu;
   cudaFuncSetAttribute(tail4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem));
@@ -38,12 +59,14 @@ int main() {
       cudaMemset(ts, 0, 8 * nt);
       // flush L2 between runs so the entries come from HBM like in the solver
       char* flush; cudaMalloc(&flush, 256 << 20);
+      int4* pcs; cudaMalloc(&pcs, sizeof(int4) * 32 * nlev);
+      tail4_pieces_kernel<<<(nlev + 7) / 8, 256>>>(nlev, 1, dl, de, pcs);
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
         cudaMemset(flush, rep, 256 << 20);
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
         cudaEventRecord(a);
-        tail4_kernel<true><<<1, kTailThreads, kT4Smem>>>(nt, nlev, 0, dl, de, di, dv, ts, dinv, nullptr, x, lt);
+        tail4_kernel<true><<<1, kTailThreads, kT4Smem>>>(nt, nlev, 0, pcs, di, dv, ts, dinv, nullptr, x, lt);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); best = std::min(best, ms);
       }
@@ -53,6 +76,23 @@ int main() {
              (h[nlev - 1] - h[0]) / double(nlev - 1), cudaGetErrorString(cudaGetLastError()));
       cudaFree(dl); cudaFree(de); cudaFree(di); cudaFree(dv); cudaFree(ts); cudaFree(dinv); cudaFree(x); cudaFree(lt); cudaFree(flush);
     }
+  }
+  {
+    int* di; double* sink; unsigned long long* lt;
+    cudaMalloc(&di, 4 << 20); cudaMemset(di, 0, 4 << 20); cudaMalloc(&sink, 8); cudaMalloc(&lt, 8 * 1000);
+    auto run = [&](auto kern, const char* name) {
+      cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+      kern<<<1, 1024>>>(800, di, lt, sink);
+      cudaEventRecord(a);
+      kern<<<1, 1024>>>(800, di, lt, sink);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      printf("floor %-28s %.0f ns/level\n", name, ms * 1e6 / 800);
+    };
+    run(floor_kernel<0>, "2 x syncthreads");
+    run(floor_kernel<1>, "+ L2 bulk prefetch");
+    run(floor_kernel<2>, "+ global load (2 ahead)");
+    run(floor_kernel<3>, "+ globaltimer store");
   }
   return 0;
 }

@@ -137,7 +137,11 @@ def main():
     bigc = (sub[chs, 6] & 0xff) == 0xff
     hops = hop[chs]
     def stat(sel):
-        return {"count": int(sel.sum()), "hop_us_mean": float(hops[sel].mean()) if sel.any() else None}
+        if not sel.any():
+            return {"count": 0}
+        return {"count": int(sel.sum()), "hop_us_mean": float(hops[sel].mean()),
+                "p50": float(np.percentile(hops[sel], 50)), "p90": float(np.percentile(hops[sel], 90)),
+                "max": float(hops[sel].max()), "sum_us": float(hops[sel].sum())}
     prev_big = np.concatenate([[False], bigc[:-1]])
     out["critical_path"]["handoffs"] = {
         "kept": stat(kept), "claimed": stat(~kept),
@@ -146,6 +150,12 @@ def main():
         "claimed_small": stat(~kept & ~bigc),
         "big_eliminations": int(bigc.sum()),
     }
+    top = np.argsort(-hops)[:8]
+    out["critical_path"]["worst_hops"] = [
+        {"pos": int(chs[i]), "hop_us": float(hops[i]), "start_us": float(start[chs[i]]),
+         "ready_us": float(ready[chs[i]]), "raw": int(raw[chs[i]]), "m": int(m[chs[i]]),
+         "eliminator": int(sub[chs[i], 6]), "kept": int(sub[chs[i], 7]),
+         "path_index": int(i)} for i in top]
     print(json.dumps(out, indent=1))
     if args.json:
         with open(args.json, "w") as fh:

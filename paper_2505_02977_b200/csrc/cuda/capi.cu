@@ -219,6 +219,8 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     unsigned t[3] = {512, 4096, 16384};
     if (const char* e = std::getenv("PARAC_CLAIM_SLEEP")) std::sscanf(e, "%u,%u,%u", &t[0], &t[1], &t[2]);
     for (int i = 0; i < 3; ++i) d.sleep_ns[i] = t[i];
+    const char* kl = std::getenv("PARAC_KEEP_LIMIT");
+    d.keep_limit = kl ? std::max(1, std::atoi(kl)) : 1 << 30;
   }
   d.delay_ns = o.delay_ns;
   d.vtimes = nullptr;

@@ -768,7 +768,7 @@ __device__ __forceinline__ unsigned long long ready_info(const FactorDev& d, int
 
 // ============================================================ small path
 // One warp eliminates k (R <= kSmallCap). Returns the kept vertex, -1, or -2.
-__device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane) {
+__device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane, bool allow_keep) {
   const int k = nx.k;
   const bool lead = lane == 0;
   Ctrl* ctrl = d.ctrl;
@@ -957,7 +957,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane)
     const unsigned long long other = __shfl_xor_sync(kFull, best, o);
     best = other > best ? other : best;
   }
-  const int keep = best ? static_cast<int>(best & 0xffffffffu) : -1;
+  const int keep = best && allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
   for (int base = 0; base < nready; base += 32) {
     const int t = base + lane;
     bool pub = false, big = false;
@@ -992,7 +992,7 @@ struct CtaShared {
 };
 
 // The whole CTA eliminates k. Returns the kept vertex (any width), -1, or -2.
-__device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh) {
+__device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh, bool allow_keep) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool lead = tid == 0;
   Ctrl* ctrl = d.ctrl;
@@ -1237,7 +1237,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   best = 0;
 #pragma unroll
   for (int w2 = 0; w2 < kWarps; ++w2) best = sh.best[w2] > best ? sh.best[w2] : best;
-  const int keep = static_cast<int>(best & 0xffffffffu);
+  const int keep = allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
   for (int base = 0; base < nready; base += kThreads) {
     const int t = base + tid;
     bool pub = false, big = false;
@@ -1267,10 +1267,12 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
     Scratch S = carve(smem + warp * kSmallBytes, kSmallCap);
     int done_local = 0;
     Next nx{-1, -1, 0, 0};
+    int chain = 0;  // consecutive kept eliminations (bounded: the FIFO queue must drain)
     while (true) {
       bool kept = true;
       if (nx.k < 0) {
         kept = false;
+        chain = 0;
         int k = -1;
         if (lane == 0) {
           if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
@@ -1290,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
         d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | warp;
         d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
       }
-      Next nn = warp_eliminate(d, nx, S, lane);
+      Next nn = warp_eliminate(d, nx, S, lane, ++chain < d.keep_limit);
       if (nn.k == -2) break;
       if (nn.k != -3) {
         PHASE(7);
@@ -1310,10 +1312,12 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
   __syncthreads();
   int done_local = 0;
   int k = -1;
+  int chain = 0;
   while (true) {
     bool kept = true;
     if (k < 0) {
       kept = false;
+      chain = 0;
       if (threadIdx.x == 0) {
         if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
         sh.k = claim(d, true);
@@ -1331,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
       d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
       d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
     }
-    const int next = cta_eliminate(d, k, smem, sh);
+    const int next = cta_eliminate(d, k, smem, sh, ++chain < d.keep_limit);
     if (next == -2) break;
     PHASE(7);
     ++done_local;

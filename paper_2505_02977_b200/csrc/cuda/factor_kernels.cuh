@@ -93,6 +93,7 @@ struct FactorDev {
   int verify;
   int delay_ns;
   unsigned sleep_ns[3];  // claim() backoff by distance to the publishing front (16-256, 256-1024, >1024 slots)
+  int keep_limit;        // max consecutive keep-one hand-offs before a warp/CTA returns to the queue
   unsigned long long* vtimes;  // optional [8n] phase timestamps per position
   unsigned long long* vsub;    // optional [8n] sub-phase timestamps per position
 };

@@ -819,6 +819,14 @@ __global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
 //   backward: z_T = G_TT^-T yd_T                  (self-contained; runs first)
 // T is level-sorted, so tail index i = order position - tail_base and the rows
 // of one level are a contiguous index range.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Asynchronous L2 prefetch of [p, p + bytes) (16-byte aligned superset), in
 // 64 KB bulk requests: the sweeps know every future level's G entries, so
 // they pull them from HBM into L2 a few levels ahead of use.
@@ -1400,7 +1408,7 @@ __global__ void __launch_bounds__(kCThreads, 1) cluster_sweep_fast_kernel(
 constexpr int kHeadPF = 8;  // entries per lane held in registers (256 per warp)
 constexpr int kHThreads = 512;  // 16 warps: 128 registers per thread hold two levels' prefetch
 constexpr int kHWarps = kHThreads / 32;
-constexpr std::size_t kHeadSmem = static_cast<std::size_t>(kHWarps) * kChunkCap * sizeof(double);
+constexpr std::size_t kHeadSmem = static_cast<std::size_t>(kHWarps) * kChunkCap * sizeof(double) + kHWarps * 8 * 16;
 
 struct HeadPre {
   int4 rec;               // jb, je, eb, ee
@@ -1454,30 +1462,29 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
     for (int j = w * 32 + lane; j < n; j += W * 32) rl[j] = rvec[rlab[j]];
     level_barrier();
   }
-  auto rec_of = [&](int t) -> int4 {
+  auto rec_ptr = [&](int t, int ww) -> const int4* {
     const int L = FWD ? Lfirst + t : Lfirst - t;
-    return hrec[static_cast<long long>(L) * W + w];
+    return hrec + static_cast<long long>(L) * W + ww;
   };
-  HeadPre nxt;
-  int4 rec2 = make_int4(0, 0, 0, 0);
-  if (nlev > 0) head_load<FWD>(nxt, rec_of(0), lptr, lidx, lval, rhs_l, dinv_l, lane);
-  if (nlev > 1) rec2 = rec_of(1);
-  // L2 bulk prefetch of this CTA's slice of level t + kHeadL2, pipelined so
-  // the prefetching thread never waits: the slice bounds (first and last
-  // chunk record of the CTA's warps) are loaded one level before use.
-  constexpr int kHeadL2 = 4;
+  // Chunk records travel through a per-warp shared-memory ring, copied with
+  // cp.async kHRing-1 levels ahead (no register waits on them in the loop);
+  // the entries of level t+1 are loaded into registers during level t; one
+  // thread bulk-prefetches this CTA's slice of level t+4 into L2 (bounds
+  // read from the rings of the CTA's first and last warp).
+  constexpr int kHRing = 8;
+  int4* ring = reinterpret_cast<int4*>(pbuf_all + kHWarps * kChunkCap);  // [kHWarps][kHRing]
+  int4* myring = ring + wl * kHRing;
+  for (int t = 0; t < kHRing - 1; ++t) {
+    if (lane == 0 && t < nlev) cp_async16(&myring[t % kHRing], rec_ptr(t, w));
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
   const bool pf = threadIdx.x == kHThreads - 32;
-  const int wbase = w - wl;
-  auto slice_recs = [&](int t, int4& a, int4& b) {
-    if (t < nlev) {
-      const int L = FWD ? Lfirst + t : Lfirst - t;
-      a = hrec[static_cast<long long>(L) * W + wbase];
-      b = hrec[static_cast<long long>(L) * W + wbase + kHWarps - 1];
-    } else {
-      a = b = make_int4(0, 0, 0, 0);
-    }
-  };
-  auto slice_prefetch = [&](const int4& a, const int4& b) {
+  auto slice_prefetch = [&](int t) {
+    if (t >= nlev) return;
+    const int4 a = ring[0 * kHRing + t % kHRing];
+    const int4 b = ring[(kHWarps - 1) * kHRing + t % kHRing];
     if (b.w > a.z) {
       prefetch_l2(lidx + a.z, static_cast<long long>(b.w - a.z) * 4);
       prefetch_l2(lval + a.z, static_cast<long long>(b.w - a.z) * 8);
@@ -1488,23 +1495,19 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
       if (FWD) prefetch_l2(dinv_l + a.x, static_cast<long long>(b.y - a.x) * 8);
     }
   };
-  int4 pa = make_int4(0, 0, 0, 0), pb = pa;
-  if (pf) {
-    for (int tt = 1; tt < kHeadL2 && tt < nlev; ++tt) {
-      int4 a, b;
-      slice_recs(tt, a, b);
-      slice_prefetch(a, b);
-    }
-    slice_recs(kHeadL2, pa, pb);
-  }
+  if (pf)
+    for (int tt = 1; tt <= 4; ++tt) slice_prefetch(tt);
+  HeadPre nxt;
+  if (nlev > 0) head_load<FWD>(nxt, myring[0], lptr, lidx, lval, rhs_l, dinv_l, lane);
   for (int t = 0; t < nlev; ++t) {
-    if (pf) {
-      slice_prefetch(pa, pb);
-      slice_recs(t + kHeadL2 + 1, pa, pb);
-    }
     const HeadPre cur = nxt;
-    if (t + 1 < nlev) head_load<FWD>(nxt, rec2, lptr, lidx, lval, rhs_l, dinv_l, lane);
-    if (t + 2 < nlev) rec2 = rec_of(t + 2);
+    if (t + 1 < nlev) head_load<FWD>(nxt, myring[(t + 1) % kHRing], lptr, lidx, lval, rhs_l, dinv_l, lane);
+    {
+      const int tn = t + kHRing - 1;
+      if (lane == 0 && tn < nlev) cp_async16(&myring[tn % kHRing], rec_ptr(tn, w));
+      cp_async_commit();
+    }
+    if (pf) slice_prefetch(t + 4);
     const int jb = cur.rec.x, je = cur.rec.y, eb = cur.rec.z, ee = cur.rec.w;
     const int cnt = ee - eb;
     if (jb < je) {
@@ -1633,9 +1636,11 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
         }
       }
     }
+    cp_async_wait<2>();  // records of levels <= t + kHRing - 3 have landed
     level_barrier();
     if (ltime && w == 0 && lane == 0) ltime[t] = globaltimer_ns();
   }
+  cp_async_wait<0>();
   if constexpr (FWD) {  // tail rows' H part: ts_i = rhs - sum over head columns (idx < tail_base)
     for (int i = w; i < nt; i += W) {
       const int j = tail_base + i;
@@ -1814,7 +1819,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
 // partials in fixed order and publishes the value, a barrier. No thread ever
 // walks a long row alone.
 constexpr int kT4PF = 4;
-constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8;
+constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8 + 8 * 32 * 16 + 8 * 8192;  // max
+inline std::size_t tail4_smem(int nlev) {
+  return (static_cast<std::size_t>(kT3Rows) + 32) * 8 + 8 * 32 * 16 + 8 * static_cast<std::size_t>(nlev);
+}
 
 // Piece table of the tail (built once per factor, per direction): level t's
 // warp w piece = {row (tail index, -1 none), eb, ee, wpr}. Keeping the integer
@@ -1840,55 +1848,73 @@ __global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const in
   pieces[static_cast<long long>(t) * 32 + warp] = pc;
 }
 
-template <bool FWD>
+
+
+// Latency plan of the level loop (HBM round trips here are ~1-1.5 us, a
+// level should take ~0.3 us): nothing a level needs may be loaded later
+// than ~4 levels ahead, and no thread may wait on a global load inside the
+// loop except for data loaded >= 2 levels earlier that is L2-resident.
+//   * piece records: staged into a shared-memory ring kT4Ring levels ahead
+//     with cp.async (threads 0..31, one 16-byte record each);
+//   * entry ranges per level: shared memory (loaded once);
+//   * entries: bulk-prefetched into L2 kT4L2 levels ahead (addresses from
+//     shared memory), loaded into registers 2 levels ahead.
+constexpr int kT4Ring = 8;
+constexpr int kT4L2 = 12;
+
+// FLAGS (experiments only, tools/microbench/tailbench.cu): 1 no L2 bulk
+// prefetch, 2 no cp.async record ring (records read from global 2 levels
+// ahead), 4 no global store of the result, 8 no entry loads (products of 0).
+template <bool FWD, int FLAGS = 0>
 __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
-    int nt, int nlev, int tail_base, const int4* pieces, const int* eidx, const double* eval,
+    int nt, int nlev, int tail_base, const int4* pieces, const int2* lrange, const int* eidx, const double* eval,
     const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
   extern __shared__ double t4[];
-  double* xs = t4;                                          // [kT3Rows]
-  double* part = t4 + kT3Rows;                              // [32]
+  double* xs = t4;                                                     // [kT3Rows]
+  double* part = t4 + kT3Rows;                                         // [32]
+  int4* ring = reinterpret_cast<int4*>(part + 32);                     // [kT4Ring][32]
+  int2* lr = reinterpret_cast<int2*>(ring + kT4Ring * 32);             // [nlev]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < nt; i += kTailThreads)
     xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];
-  // Two register sets hold the pieces of levels t and t+1 (entries loaded two
-  // levels ahead), the piece records are loaded three levels ahead, and one
-  // thread bulk-prefetches entry ranges into L2 eight levels ahead.
+  for (int i = tid; i < nlev; i += kTailThreads) lr[i] = lrange[i];
+  // ring slots for levels 0 .. kT4Ring-2 (one commit group per level)
+  for (int t = 0; t < kT4Ring - 1; ++t) {
+    if (tid < 32 && t < nlev) cp_async16(&ring[(t % kT4Ring) * 32 + tid], &pieces[static_cast<long long>(t) * 32 + tid]);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  auto l2 = [&](int t) {
+    if ((FLAGS & 1) || t >= nlev) return;
+    const int2 r = lr[t];
+    if (r.y > r.x) {
+      prefetch_l2(eidx + r.x, static_cast<long long>(r.y - r.x) * 4);
+      prefetch_l2(eval + r.x, static_cast<long long>(r.y - r.x) * 8);
+    }
+  };
+  if (tid == 32)
+    for (int t = 0; t < kT4L2; ++t) l2(t);
   struct Set {
     int4 pc;
     int idx[kT4PF];
     double val[kT4PF];
   };
-  auto piece_at = [&](int t) { return t < nlev ? pieces[static_cast<long long>(t) * 32 + warp] : make_int4(-1, 0, 0, 0); };
-  auto load = [&](const int4 pc, Set& S) {
-    S.pc = pc;
-    if (pc.x >= 0) {
+  auto load = [&](int t, Set& S) {
+    S.pc = (FLAGS & 2) ? pieces[static_cast<long long>(t) * 32 + warp] : ring[(t % kT4Ring) * 32 + warp];
+    if (!(FLAGS & 8) && S.pc.x >= 0) {
 #pragma unroll
       for (int k = 0; k < kT4PF; ++k) {
-        const int e = pc.y + k * 32 + lane;
-        S.idx[k] = e < pc.z ? eidx[e] : 0;
-        S.val[k] = e < pc.z ? eval[e] : 0.0;
+        const int e = S.pc.y + k * 32 + lane;
+        S.idx[k] = e < S.pc.z ? eidx[e] : 0;
+        S.val[k] = e < S.pc.z ? eval[e] : 0.0;
       }
     }
   };
-  constexpr int kT4L2 = 8;
-  auto l2 = [&](int t) {  // whole level: first and last piece of warp 0 / 31
-    if (t >= nlev) return;
-    const int4 f = pieces[static_cast<long long>(t) * 32];
-    int4 l = pieces[static_cast<long long>(t) * 32 + 31];
-    for (int w = 30; l.x < 0 && w >= 0; --w) l = pieces[static_cast<long long>(t) * 32 + w];
-    if (f.x >= 0 && l.z > f.y) {
-      prefetch_l2(eidx + f.y, static_cast<long long>(l.z - f.y) * 4);
-      prefetch_l2(eval + f.y, static_cast<long long>(l.z - f.y) * 8);
-    }
-  };
-  if (tid == 32)
-    for (int t = 2; t < kT4L2; ++t) l2(t);
   Set A, B;
   A.pc = B.pc = make_int4(-1, 0, 0, 0);
-  int4 pnext = piece_at(2);
-  if (nlev > 0) load(piece_at(0), A);
-  if (nlev > 1) load(piece_at(1), B);
-  __syncthreads();
+  if (nlev > 0) load(0, A);
+  if (nlev > 1) load(1, B);
   auto step = [&](int t, Set& S) {
     const int4 pc = S.pc;
     double p = 0.0;
@@ -1898,13 +1924,19 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
         if (pc.y + k * 32 + lane < pc.z) p += S.val[k] * xs[S.idx[k]];
       for (int e = pc.y + kT4PF * 32 + lane; e < pc.z; e += 32) p += eval[e] * xs[eidx[e]];  // overflow
     }
-    if (t + 2 < nlev) load(pnext, S);  // level t+2 into the set just consumed
-    pnext = piece_at(t + 3);
+    if (t + 2 < nlev) load(t + 2, S);  // level t+2 into the set just consumed (its ring slot landed)
+    // stage level t + kT4Ring - 1 into the slot level t-1 used (free since the last barrier)
+    const int tn = t + kT4Ring - 1;
+    if (!(FLAGS & 2)) {
+      if (tid < 32 && tn < nlev) cp_async16(&ring[(tn % kT4Ring) * 32 + tid], &pieces[static_cast<long long>(tn) * 32 + tid]);
+      cp_async_commit();
+    }
     if (tid == 32) l2(t + kT4L2);
     if (pc.x >= 0) {
       p = warp_sum(p);
       if (lane == 0) part[warp] = p;
     }
+    cp_async_wait<kT4Ring - 4>();  // level t+3's records have landed (needed after the barrier)
     __syncthreads();
     if (pc.x >= 0 && pc.w > 0) {  // the row's first warp publishes it
       double sp = lane < pc.w ? part[warp + lane] : 0.0;
@@ -1912,7 +1944,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
       if (lane == 0) {
         const double acc = xs[pc.x] - sp;
         xs[pc.x] = acc;
-        x_l[tail_base + pc.x] = acc;
+        if (!(FLAGS & 4)) x_l[tail_base + pc.x] = acc;
       }
     }
     __syncthreads();
@@ -1922,6 +1954,22 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
     step(t, A);
     if (t + 1 < nlev) step(t + 1, B);
   }
+  cp_async_wait<0>();
+}
+
+// Entry range [eb, ee) of each tail level (from the piece table).
+__global__ void tail4_range_kernel(int nlev, const int4* pieces, int2* lrange) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nlev) return;
+  int eb = 0x7fffffff, ee = 0;
+  for (int w = 0; w < 32; ++w) {
+    const int4 pc = pieces[static_cast<long long>(t) * 32 + w];
+    if (pc.x >= 0) {
+      eb = min(eb, pc.y);
+      ee = max(ee, pc.z);
+    }
+  }
+  lrange[t] = eb <= ee ? make_int2(eb, ee) : make_int2(0, 0);
 }
 
 // T-part of the forward tail rows: count, then copy with tail-relative indices.
@@ -2474,11 +2522,15 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   if (s.cap_t4 < npc) {
     dalloc(s.t4_fpc, npc);
     dalloc(s.t4_bpc, npc);
+    dalloc(s.t4_frange, static_cast<std::size_t>(nlev) + 1);
+    dalloc(s.t4_brange, static_cast<std::size_t>(nlev) + 1);
     s.cap_t4 = npc;
   }
   tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 1, s.t3_lvl, s.t3_fep, s.t4_fpc);
   tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 0, s.t3_lvl, s.t3_bep, s.t4_bpc);
-  note_launches(2);
+  tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_fpc, s.t4_frange);
+  tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_bpc, s.t4_brange);
+  note_launches(4);
   static bool attr = false;
   if (!attr) {
     check(cudaFuncSetAttribute(tail3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
@@ -2625,13 +2677,14 @@ struct Solver {
             "head forward");
       note_launches(1);
       if (nt > 0) {
-        tail4_kernel<true><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_fpc, s.t3_fidx,
-                                                             s.t3_fval, s.tail_s, s.dinv_l, nullptr, s.yf,
-                                                             lt ? lt + (D + 2) : nullptr);
-        tail4_kernel<false><<<1, kTailThreads, kT4Smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_bpc,
-                                                              s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
-                                                              nullptr, s.dinv_l, s.yf, s.zb,
-                                                              lt ? lt + 2 * (D + 2) : nullptr);
+        const std::size_t t4smem = tail4_smem(s.t3_nlev);
+        tail4_kernel<true><<<1, kTailThreads, t4smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_fpc, s.t4_frange,
+                                                            s.t3_fidx, s.t3_fval, s.tail_s, s.dinv_l, nullptr, s.yf,
+                                                            lt ? lt + (D + 2) : nullptr);
+        tail4_kernel<false><<<1, kTailThreads, t4smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_bpc, s.t4_brange,
+                                                             s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
+                                                             nullptr, s.dinv_l, s.yf, s.zb,
+                                                             lt ? lt + 2 * (D + 2) : nullptr);
         note_launches(2);
       }
       check(launch_cluster_t(head_sweep_kernel<false, false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
@@ -2815,7 +2868,7 @@ void solve_release(SolveState& s) {
   dfree(s.f_chunk); dfree(s.f_cbase); dfree(s.b_chunk); dfree(s.b_cbase); dfree(s.lvl_target); dfree(s.ltime);
   dfree(s.hrec_gf); dfree(s.hrec_gb);
   dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
-  dfree(s.t4_fpc); dfree(s.t4_bpc);
+  dfree(s.t4_fpc); dfree(s.t4_bpc); dfree(s.t4_frange); dfree(s.t4_brange);
   dfree(s.t3_lvl); dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_bep); dfree(s.t3_fval);
   s = SolveState{};
 }

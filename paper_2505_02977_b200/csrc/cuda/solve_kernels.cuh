@@ -55,7 +55,8 @@ struct SolveState {
   int *t3_lvl = nullptr, *t3_fep = nullptr, *t3_fidx = nullptr, *t3_bep = nullptr;
   double* t3_fval = nullptr;
   std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0, cap_t4 = 0;
-  int4 *t4_fpc = nullptr, *t4_bpc = nullptr;  // tail piece tables [nlev][32]  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
+  int4 *t4_fpc = nullptr, *t4_bpc = nullptr;  // tail piece tables [nlev][32]
+  int2 *t4_frange = nullptr, *t4_brange = nullptr;  // tail entry range per level  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
   std::size_t cap_ltime = 0;
   std::size_t cap_lz = 0, cap_fchunk = 0, cap_bchunk = 0, cap_levels = 0;
   std::size_t cap_tail = 0, cap_tail_nnz = 0;

@@ -61,12 +61,14 @@ int main() {
       char* flush; cudaMalloc(&flush, 256 << 20);
       int4* pcs; cudaMalloc(&pcs, sizeof(int4) * 32 * nlev);
       tail4_pieces_kernel<<<(nlev + 7) / 8, 256>>>(nlev, 1, dl, de, pcs);
+      int2* lrg; cudaMalloc(&lrg, sizeof(int2) * (nlev + 1));
+      tail4_range_kernel<<<(nlev + 255) / 256, 256>>>(nlev, pcs, lrg);
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
         cudaMemset(flush, rep, 256 << 20);
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
         cudaEventRecord(a);
-        tail4_kernel<true><<<1, kTailThreads, kT4Smem>>>(nt, nlev, 0, pcs, di, dv, ts, dinv, nullptr, x, lt);
+        tail4_kernel<true><<<1, kTailThreads, kT4Smem>>>(nt, nlev, 0, pcs, lrg, di, dv, ts, dinv, nullptr, x, lt);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); best = std::min(best, ms);
       }
@@ -74,6 +76,22 @@ int main() {
       cudaMemcpy(h.data(), lt, 8 * nlev, cudaMemcpyDeviceToHost);
       printf("rows/level %2d len %3d: %d levels, kernel %.1f us, %.0f ns/level (%s)\n", r, len, nlev, best * 1e3,
              (h[nlev - 1] - h[0]) / double(nlev - 1), cudaGetErrorString(cudaGetLastError()));
+      if (r == 1 && len == 100) {
+        auto var = [&](auto kern, const char* name) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem));
+          cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+          cudaEventRecord(a);
+          kern<<<1, kTailThreads, kT4Smem>>>(nt, nlev, 0, pcs, lrg, di, dv, ts, dinv, nullptr, x, lt);
+          cudaEventRecord(b); cudaEventSynchronize(b);
+          float ms; cudaEventElapsedTime(&ms, a, b);
+          printf("   variant %-24s %.0f ns/level\n", name, ms * 1e6 / nlev);
+        };
+        var(tail4_kernel<true, 1>, "no L2 prefetch");
+        var(tail4_kernel<true, 2>, "no cp.async ring");
+        var(tail4_kernel<true, 4>, "no result store");
+        var(tail4_kernel<true, 8>, "no entry loads");
+        var(tail4_kernel<true, 15>, "none of these");
+      }
       cudaFree(dl); cudaFree(de); cudaFree(di); cudaFree(dv); cudaFree(ts); cudaFree(dinv); cudaFree(x); cudaFree(lt); cudaFree(flush);
     }
   }

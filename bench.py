@@ -172,6 +172,12 @@ def allreduce(pg, device, value: float, op: str) -> float:
     return float(t.item())
 
 
+def batch_share(rank: int, world: int, total: int = 64):
+    """Problems of the 64-problem batch that rank `rank` of `world` factors
+    (round-robin; every problem exactly once over the ranks)."""
+    return list(range(rank, total, world))
+
+
 # ---------------------------------------------------------------- reference CPU
 def cpu_reference_factor(graph, perm, seed, workers_list, repeats=1):
     """Wall clock around the reference API call (host graph in, LdlFactor out),
@@ -486,7 +492,7 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     lib = P.rchol.lib
-    mine = list(range(rank, 64, world))
+    mine = batch_share(rank, world)
     g = P.gen_poisson3d(64)
     perms = [P.ordering_random(g.n, i).perm for i in mine]
     ctx = P.GpuContext(local)

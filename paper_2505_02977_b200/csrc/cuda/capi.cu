@@ -75,7 +75,8 @@ struct parac_gpu_ctx {
   DevBuf<double> w;
   DevBuf<int> perm;
   // factor working state
-  DevBuf<int> inv, fdeg, dp, queue, bqueue, fill_cnt, samples, col_len, arena_rows, level;
+  DevBuf<int> inv, fdeg, queue, bqueue, samples, col_len, arena_rows, level;
+  DevBuf<unsigned long long> cnt;  // dp (low 32) | fills received (high 32)
   DevBuf<int> heavy_list, heavy_count, heavy_key;
   DevBuf<double> heavy_val;
   DevBuf<long long> fwd_ptr, col_start, tiles;
@@ -129,7 +130,15 @@ Budgets default_budgets(int n, long long E, const parac_gpu_options& o) {
   const long long base = E + n;
   // 64 preallocated slots per position cover the fill count of ~99.5% of
   // 128^3 positions (p99 66), so the directory lookup is rare.
-  b.c0 = o.first_chunk > 0 ? o.first_chunk : 64;
+  // Preallocated fill slots per position: as many as ~8.6 GB allow, up to 256
+  // (covers the fill counts of all but the widest columns at 128^3: no
+  // overflow-directory round trips on the emission or gather path), at least 64.
+  if (o.first_chunk > 0) {
+    b.c0 = o.first_chunk;
+  } else {
+    const long long cap = 8600000000LL / (16LL * std::max(n, 1));
+    b.c0 = cap >= 256 ? 256 : cap >= 128 ? 128 : 64;
+  }
   b.ovf = o.fill_pool_entries >= 0 ? o.fill_pool_entries : 4 * base + 4096;
   b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : 6 * base + 4096;
   b.large = base + 65536;
@@ -145,10 +154,9 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   const std::size_t nn = static_cast<std::size_t>(std::max(n, 1));
   ctx->inv.ensure(nn);
   ctx->fdeg.ensure(nn);
-  ctx->dp.ensure(nn);
+  ctx->cnt.ensure(nn);
   ctx->queue.ensure(nn);
   ctx->bqueue.ensure(nn);
-  ctx->fill_cnt.ensure(nn);
   ctx->samples.ensure(nn);
   ctx->level.ensure(nn);
   ctx->col_len.ensure(nn);
@@ -188,10 +196,9 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.heavy_count = ctx->heavy_count.p;
   d.heavy_key = ctx->heavy_key.p;
   d.heavy_val = ctx->heavy_val.p;
-  d.dp = ctx->dp.p;
+  d.cnt = ctx->cnt.p;
   d.queue = ctx->queue.p;
   d.bqueue = ctx->bqueue.p;
-  d.fill_cnt = ctx->fill_cnt.p;
   d.pool0 = ctx->pool0.p;
   d.dir = ctx->dir.p;
   d.ovf = ctx->ovf.p;
@@ -329,8 +336,8 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
   ctx->heavy_list.release(); ctx->heavy_count.release(); ctx->heavy_key.release(); ctx->heavy_val.release();
-  ctx->inv.release(); ctx->fdeg.release(); ctx->dp.release(); ctx->level.release(); ctx->queue.release(); ctx->bqueue.release();
-  ctx->fill_cnt.release(); ctx->samples.release(); ctx->col_len.release();
+  ctx->inv.release(); ctx->fdeg.release(); ctx->cnt.release(); ctx->level.release(); ctx->queue.release(); ctx->bqueue.release();
+  ctx->samples.release(); ctx->col_len.release();
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
   ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
@@ -589,7 +596,11 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
     if (samples_emitted && n)
       check(cudaMemcpyAsync(samples_emitted, ctx->samples.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
     if (fills_received && n)
-      check(cudaMemcpyAsync(fills_received, ctx->fill_cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    {
+      ctx->heavy_list.ensure(static_cast<std::size_t>(std::max(n, 1)));  // scratch (K1 only uses it earlier)
+      check(launch_extract_fills(n, ctx->cnt.p, ctx->heavy_list.p, s), "fills");
+      check(cudaMemcpyAsync(fills_received, ctx->heavy_list.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    }
     check(cudaStreamSynchronize(s), "d2h sync");
   });
 }

@@ -425,9 +425,11 @@ __device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long lon
       val[i] = dbits(w);
     }
   }
-  if (stamp && threadIdx.x == 0) {
-    asm volatile("" ::"l"(key[0]), "l"(val[0]));
-    *stamp = globaltimer_ns();
+  if (stamp) {  // diagnostics: every thread's gather has landed
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) asm volatile("" ::"l"(key[i]), "l"(val[i]));
+    __syncthreads();
+    if (threadIdx.x == 0) *stamp = globaltimer_ns();
   }
   int rank[ITEMS];
   rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, rank);
@@ -757,14 +759,14 @@ __device__ __forceinline__ void serial_suffix(const double* B, double* C, int m)
   }
 }
 
-// Final raw size of a vertex that just became ready (all its fills landed):
-// (R << 32 | row). The forward offset/degree and fill count are also what a
-// keeper needs to skip its first gather round trip.
-__device__ __forceinline__ unsigned long long ready_info(const FactorDev& d, int r) {
-  const long long rdeg = d.fwd_ptr[r + 1] - d.fwd_ptr[r];
-  return (static_cast<unsigned long long>(rdeg + ld_relaxed(&d.fill_cnt[r])) << 32) |
+// Final raw size of a vertex that just became ready, (R << 32 | row): its
+// forward degree (static, loaded alongside the decrement) plus the final fill
+// count returned by the decrement itself (high word of the counter).
+__device__ __forceinline__ unsigned long long ready_info(int r, int fdeg, unsigned long long old_cnt) {
+  return (static_cast<unsigned long long>(fdeg + static_cast<int>(old_cnt >> 32)) << 32) |
          static_cast<unsigned>(r);
 }
+__device__ __forceinline__ int dp_of(unsigned long long c) { return static_cast<int>(c & 0xffffffffull); }
 
 // ============================================================ small path
 // One warp eliminates k (R <= kSmallCap). Returns the kept vertex, -1, or -2.
@@ -772,7 +774,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   const int k = nx.k;
   const bool lead = lane == 0;
   Ctrl* ctrl = d.ctrl;
-  if (d.verify && lead && ld_relaxed(&d.dp[k]) != 0) fail(d, kErrInternal, k);
+  if (d.verify && lead && dp_of(ld_relaxed_u64(&d.cnt[k])) != 0) fail(d, kErrInternal, k);
   maybe_delay(d, k, 0);
 
   // ---- 1. gather
@@ -781,9 +783,12 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   if (fdeg < 0) {
     fb = d.fwd_ptr[k];
     fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
-    fc = ld_relaxed(&d.fill_cnt[k]);
+    fc = static_cast<int>(ld_relaxed_u64(&d.cnt[k]) >> 32);
   }
   const int R = fdeg + fc;
+  // level[k] is final once k is ready (every predecessor raised it before its
+  // releasing decrement); load it now, use it after the sampling phase
+  const int lvk = d.level ? ld_relaxed(&d.level[k]) : 0;
   if (R > kSmallCap) {  // mis-routed (cannot happen with exact routing): hand to a big CTA
     publish(d, lead, true, k, lane);
     return {-3, -1, 0, 0};
@@ -887,7 +892,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
     for (int b = 0; b < kBatch; ++b) {
       if (em[b]) {
         slot[b] = reserve_fill_slot(d, lo[b]);
-        red_add_relaxed(&d.dp[hi[b]], 1);
+        red_add_relaxed_u64(&d.cnt[hi[b]], 1ull);
         bad = bad || slot[b] < 0;
       }
     }
@@ -903,7 +908,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   // ASAP level of the factor DAG (schedule_levels, factor_par.cpp:659-684):
   // level[row] >= level[k] + 1, published before the decrements release row.
   if (d.level) {
-    const int lk = ld_relaxed(&d.level[k]) + 1;
+    const int lk = lvk + 1;
     for (int t = lane; t < m; t += 32) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
   }
   PHASE(5);
@@ -916,28 +921,29 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
   int nready = 0;
   {
-    int row[kBatch], old[kBatch], mult[kBatch];
+    int row[kBatch], mult[kBatch], fd[kBatch];
+    unsigned long long old[kBatch];
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
       const int t = b * 32 + lane;
       row[b] = -1;
-      old[b] = mult[b] = 0;
+      mult[b] = fd[b] = 0;
+      old[b] = 0;
       if (t < m) {
         const unsigned long long a = S.A[t];
         row[b] = static_cast<int>(a >> 32);
         mult[b] = static_cast<int>(a & 0xffffffffu);
-        old[b] = atom_add_relaxed(&d.dp[row[b]], -mult[b]);
+        fd[b] = __ldg(&d.fdeg[row[b]]);  // in flight with the decrement
+        old[b] = atom_add_relaxed_u64(&d.cnt[row[b]], static_cast<unsigned long long>(-static_cast<long long>(mult[b])));
       }
     }
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-      if (d.verify && row[b] >= 0 && old[b] < mult[b]) fail(d, kErrInternal, row[b]);
-      const bool now_ready = row[b] >= 0 && old[b] == mult[b];
+      if (d.verify && row[b] >= 0 && dp_of(old[b]) < mult[b]) fail(d, kErrInternal, row[b]);
+      // no fence here: whoever eliminates a ready vertex acquires first (loop top / claim)
+      const bool now_ready = row[b] >= 0 && dp_of(old[b]) == mult[b];
       const unsigned bm = __ballot_sync(kFull, now_ready);
-      if (bm) {
-        fence_acq_rel();  // acquire: the other decrementers' emissions are visible
-        if (now_ready) ready[nready + __popc(bm & lanemask_lt())] = ready_info(d, row[b]);
-      }
+      if (now_ready) ready[nready + __popc(bm & lanemask_lt())] = ready_info(row[b], fd[b], old[b]);
       nready += __popc(bm);
     }
   }
@@ -996,7 +1002,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool lead = tid == 0;
   Ctrl* ctrl = d.ctrl;
-  if (d.verify && lead && ld_relaxed(&d.dp[k]) != 0) fail(d, kErrInternal, k);
+  if (d.verify && lead && dp_of(ld_relaxed_u64(&d.cnt[k])) != 0) fail(d, kErrInternal, k);
   maybe_delay(d, k, 0);
 
   // ---- 1. gather (the directory row is fetched in the same round trip)
@@ -1005,7 +1011,8 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
         ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
   const long long fb = d.fwd_ptr[k];
   const int fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
-  const int fc = ld_relaxed(&d.fill_cnt[k]);
+  const int fc = static_cast<int>(ld_relaxed_u64(&d.cnt[k]) >> 32);
+  const int lvk = d.level ? ld_relaxed(&d.level[k]) : 0;  // final once k is ready; used after sampling
   const int R = fdeg + fc;
   const int P = next_pow2(R);
   if (lead) {
@@ -1174,7 +1181,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     if (base == 0) SUB(3);
     if (em) {
       slot = reserve_fill_slot(d, lo);
-      red_add_relaxed(&d.dp[hi], 1);
+      red_add_relaxed_u64(&d.cnt[hi], 1ull);
       bad = bad || slot < 0;
     }
     __syncwarp();
@@ -1193,7 +1200,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     sh.nready = 0;
   }
   if (d.level) {  // ASAP levels, as in the warp path
-    const int lk = ld_relaxed(&d.level[k]) + 1;
+    const int lk = lvk + 1;
     for (int t = tid; t < m; t += kThreads) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
   }
   PHASE(5);
@@ -1208,12 +1215,10 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     const unsigned long long a = S.A[t];
     const int row = static_cast<int>(a >> 32);
     const int mult = static_cast<int>(a & 0xffffffffu);
-    const int old = atom_add_relaxed(&d.dp[row], -mult);
-    if (d.verify && old < mult) fail(d, kErrInternal, row);
-    if (old == mult) {
-      fence_acq_rel();
-      ready[atomicAdd(&sh.nready, 1)] = ready_info(d, row);
-    }
+    const int fd = __ldg(&d.fdeg[row]);
+    const unsigned long long old = atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
+    if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
+    if (dp_of(old) == mult) ready[atomicAdd(&sh.nready, 1)] = ready_info(row, fd, old);
   }
   __syncthreads();
   const int nready = sh.nready;

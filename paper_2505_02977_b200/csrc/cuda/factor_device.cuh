@@ -102,7 +102,7 @@ __device__ __forceinline__ void load_raw_dir(const FactorDev& d, int k, long lon
 // Reserve fill slot for (lo) and allocate its overflow chunk if this slot is
 // the chunk's first. Returns the slot, or -1 on budget exhaustion.
 __device__ __forceinline__ int reserve_fill_slot(const FactorDev& d, int lo) {
-  const int slot = atomicAdd(&d.fill_cnt[lo], 1);
+  const int slot = static_cast<int>(atomicAdd(&d.cnt[lo], 1ull << 32) >> 32);
   if (slot >= d.c0) {
     const SlotLoc L = slot_loc(d.c0, slot);
     if (L.c > kDirChunks) {

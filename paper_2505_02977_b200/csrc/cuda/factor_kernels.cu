@@ -39,9 +39,8 @@ __global__ void pos_count_kernel(FactorDev d) {
     int cnt = 0;
     for (long long t = b; t < e; ++t) cnt += d.perm[d.adj[t]] > p;
     d.fdeg[p] = cnt;
-    d.dp[p] = static_cast<int>(e - b) - cnt;  // earlier_degree = initial dependency count
+    d.cnt[p] = static_cast<unsigned long long>(static_cast<unsigned>(static_cast<int>(e - b) - cnt));  // earlier_degree
   }
-  d.fill_cnt[p] = 0;
   d.queue[p] = -1;
   d.bqueue[p] = -1;
   d.samples[p] = 0;
@@ -124,7 +123,7 @@ __global__ void __launch_bounds__(kHT) pos_count_heavy_kernel(FactorDev d) {
       int c = 0;
       for (int w = 0; w < kHT / 32; ++w) c += red[w];
       d.fdeg[p] = c;
-      d.dp[p] = static_cast<int>(e - b) - c;
+      d.cnt[p] = static_cast<unsigned long long>(static_cast<unsigned>(static_cast<int>(e - b) - c));
     }
     __syncthreads();
   }
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(kHT) pos_fill_heavy_kernel(FactorDev d) {
 __global__ void initial_ready_kernel(FactorDev d) {
   if (d.ctrl->status != 0) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool ready = p < d.n && d.dp[p] == 0;
+  const bool ready = p < d.n && (d.cnt[p] & 0xffffffffull) == 0;
   const bool big = ready && d.fdeg[p] > kSmallCap;  // no fills yet: R = forward degree
   publish(d, ready, big, p, lane_id());
 }
@@ -386,6 +385,20 @@ cudaError_t launch_batch_offsets(int count, long long N, long long NNZ, const lo
   batch_vertex_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(count, N, NNZ, base, ebase, ptr, perm, pos_pid);
   if (NNZ > 0) batch_edge_kernel<<<num_sms(dev) * 8, 256, 0, s>>>(count, NNZ, ebase, base, adj);
   note_launches(2);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void extract_fills_kernel(int n, const unsigned long long* cnt, int* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) out[p] = static_cast<int>(cnt[p] >> 32);
+}
+}  // namespace
+
+cudaError_t launch_extract_fills(int n, const unsigned long long* cnt, int* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  extract_fills_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, cnt, out);
+  note_launches(1);
   return cudaGetLastError();
 }
 

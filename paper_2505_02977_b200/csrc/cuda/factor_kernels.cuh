@@ -59,11 +59,14 @@ struct FactorDev {
   int* heavy_key;      // K1 hub sort scratch, same offsets as fwd_to / fwd_w
   double* heavy_val;
   // dependency counters + ready queues
-  int* dp;
+  // per-position counters, one 64-bit word each: low 32 bits = dp (pending
+  // earlier neighbours + pending fill endpoints), high 32 bits = fills
+  // received. One word means the decrement that makes a vertex ready also
+  // returns its final fill count -- no extra round trip, no extra fence.
+  unsigned long long* cnt;
   int* queue;   // main queue [n]
   int* bqueue;  // big-column queue [n]
   // fills
-  int* fill_cnt;
   int4* pool0;
   unsigned* dir;
   int4* ovf;
@@ -113,6 +116,8 @@ int eliminate_occupancy_grid(int device);
 cudaError_t launch_batch_offsets(int count, long long N, long long NNZ, const long long* base,
                                  const long long* ebase, long long* ptr, int* adj, int* perm, int* pos_pid,
                                  cudaStream_t s);
+// fills_received per position (high words of cnt) into out[n]
+cudaError_t launch_extract_fills(int n, const unsigned long long* cnt, int* out, cudaStream_t s);
 cudaError_t launch_batch_local_rows(int n, const long long* col_ptr, const int* pos_pid, const long long* base,
                                     int* rows, cudaStream_t s);
 

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--workload", default="poisson3d")
     ap.add_argument("--json", default=None)
     ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--c0", type=int, default=0, help="preallocated fill slots per vertex (0: library default)")
     args = ap.parse_args()
     if args.workload == "poisson3d":
         g = P.gen_poisson3d(args.n)
@@ -36,7 +37,7 @@ def main():
         g = P.gen_rmat(args.n, 16, 0)
     o = P.ordering_random(g.n, 0)
     ctx = P.GpuContext(0)
-    opts = P.GpuOptions(record_times=True, grid_ctas=args.grid)
+    opts = P.GpuOptions(record_times=True, grid_ctas=args.grid, first_chunk=args.c0)
     st = P.FactorStats()
     for _ in range(2):
         f = P.factor_gpu(g, o, 0, opts, st, ctx=ctx)

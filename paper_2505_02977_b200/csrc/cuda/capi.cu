@@ -226,6 +226,8 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     unsigned t[3] = {512, 4096, 16384};
     if (const char* e = std::getenv("PARAC_CLAIM_SLEEP")) std::sscanf(e, "%u,%u,%u", &t[0], &t[1], &t[2]);
     for (int i = 0; i < 3; ++i) d.sleep_ns[i] = t[i];
+    const char* kp = std::getenv("PARAC_KEEP");
+    d.keep_pos = kp && std::string(kp) == "width" ? 0 : 1;  // default: lowest position
     const char* kl = std::getenv("PARAC_KEEP_LIMIT");
     d.keep_limit = kl ? std::max(1, std::atoi(kl)) : 1 << 30;
   }

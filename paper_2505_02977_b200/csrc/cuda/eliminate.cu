@@ -93,7 +93,6 @@ struct Next {
 __device__ int claim(const FactorDev& d, bool big) {
   int* queue = big ? d.bqueue : d.queue;
   int* head = big ? &d.ctrl->b_head : &d.ctrl->q_head;
-  int* tail_p = big ? &d.ctrl->b_tail : &d.ctrl->q_tail;
   const int idx = atomicAdd(head, 1);
   if (idx >= d.n) return -1;
   int v = ld_relaxed(&queue[idx]);
@@ -101,7 +100,6 @@ __device__ int claim(const FactorDev& d, bool big) {
   unsigned long long t0 = globaltimer_ns();
   int last = ld_relaxed(&d.ctrl->eliminated);
   int iter = 0;
-  (void)tail_p;
   unsigned ns = 32;
   while (true) {
     // Distance probe on a slot-specific address (no shared word polled by
@@ -768,6 +766,15 @@ __device__ __forceinline__ unsigned long long ready_info(int r, int fdeg, unsign
 }
 __device__ __forceinline__ int dp_of(unsigned long long c) { return static_cast<int>(c & 0xffffffffull); }
 
+// keep-one preference among the vertices an elimination made ready (max key
+// wins; the low word is the row): the widest column, or (keep_pos) the lowest
+// position -- the head of the longest remaining dependency chain.
+__device__ __forceinline__ unsigned long long keep_key(const FactorDev& d, unsigned long long rr) {
+  const unsigned row = static_cast<unsigned>(rr & 0xffffffffu);
+  return d.keep_pos ? (1ull << 63) | (static_cast<unsigned long long>(0x7fffffffu - row) << 32) | row
+                    : rr | (1ull << 63);
+}
+
 // ============================================================ small path
 // One warp eliminates k (R <= kSmallCap). Returns the kept vertex, -1, or -2.
 __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane, bool allow_keep) {
@@ -956,7 +963,8 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   unsigned long long best = 0;
   for (int t = lane; t < nready; t += 32) {
     const unsigned long long rr = ready[t];
-    if (static_cast<int>(rr >> 32) <= kSmallCap && (rr | (1ull << 63)) > best) best = rr | (1ull << 63);
+    const unsigned long long key = keep_key(d, rr);
+    if (static_cast<int>(rr >> 32) <= kSmallCap && key > best) best = key;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -992,12 +1000,35 @@ struct CtaShared {
   long long start;
   long long slab;      // this CTA's wide-column slab (entries), -1 none
   int slab_cap;
+  long long fb;        // cta_prologue: forward offset, degree, raw size, level
+  int fdeg, R, lvk;
   unsigned dirrow[kDirChunks];
   int wcount[kWarps];
   unsigned long long best[kWarps];
 };
 
 // The whole CTA eliminates k. Returns the kept vertex (any width), -1, or -2.
+// WIDE (raw size > kBigCap, R-MAT hubs) works in a global-memory slab; the
+// common case is a separate instantiation so that all its scratch accesses
+// compile to shared-memory instructions (a runtime select between slab and
+// shared memory made every access generic). cta_prologue (the caller) has
+// loaded fb / fdeg / R / level into sh.
+__device__ __forceinline__ void cta_prologue(const FactorDev& d, int k, CtaShared& sh) {
+  const int tid = threadIdx.x;
+  if (tid < kDirChunks)
+    sh.dirrow[tid] = static_cast<unsigned>(
+        ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
+  if (tid == 0) {
+    const long long fb = d.fwd_ptr[k];
+    sh.fb = fb;
+    sh.fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
+    sh.R = sh.fdeg + static_cast<int>(ld_relaxed_u64(&d.cnt[k]) >> 32);
+    sh.lvk = d.level ? ld_relaxed(&d.level[k]) : 0;  // final once k is ready; used after sampling
+  }
+  __syncthreads();
+}
+
+template <bool WIDE>
 __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh, bool allow_keep) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool lead = tid == 0;
@@ -1005,15 +1036,11 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   if (d.verify && lead && dp_of(ld_relaxed_u64(&d.cnt[k])) != 0) fail(d, kErrInternal, k);
   maybe_delay(d, k, 0);
 
-  // ---- 1. gather (the directory row is fetched in the same round trip)
-  if (tid < kDirChunks)
-    sh.dirrow[tid] = static_cast<unsigned>(
-        ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
-  const long long fb = d.fwd_ptr[k];
-  const int fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
-  const int fc = static_cast<int>(ld_relaxed_u64(&d.cnt[k]) >> 32);
-  const int lvk = d.level ? ld_relaxed(&d.level[k]) : 0;  // final once k is ready; used after sampling
-  const int R = fdeg + fc;
+  // ---- 1. gather (counts and the directory row were fetched by cta_prologue)
+  const long long fb = sh.fb;
+  const int fdeg = sh.fdeg;
+  const int lvk = sh.lvk;
+  const int R = sh.R;
   const int P = next_pow2(R);
   if (lead) {
     sh.bad = 0;
@@ -1039,8 +1066,8 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // value is first needed at the column write)
   unsigned long long start_reg = 0;
   if (lead && R > 0) start_reg = atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R));
-  const bool wide = P > kBigCap;
-  Scratch S = wide ? carve(d.large_pool + sh.slab * kEntryBytes, sh.slab_cap) : carve(smem, kBigCap);
+  constexpr bool wide = WIDE;
+  Scratch S = WIDE ? carve(d.large_pool + sh.slab * kEntryBytes, sh.slab_cap) : carve(smem, kBigCap);
   const XBuf sxb{reinterpret_cast<unsigned long long*>(smem), reinterpret_cast<unsigned long long*>(smem + 8 * kBigCap),
                  reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
                  reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
@@ -1143,7 +1170,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // ---- 6-7. weight sort + suffix
   if (m >= 2) {
     const int Pm = next_pow2(m);
-    if (Pm > kBigCap) {
+    if (WIDE && Pm > kBigCap) {
       // key = weight bits, payload = A (row << 32 | mult): (weight, row) order
       slab_sort(reinterpret_cast<unsigned long long*>(S.B), S.A, S.X1, S.X2, m, kInfBits, ~0ull, sxb, WeightLess{});
     } else if (Pm <= kThreads) {
@@ -1154,7 +1181,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       cta_sort_weight_reg<4>(m, S.A, S.B, xb);
     }
     SUB(2);
-    if (Pm > kBigCap) {
+    if (WIDE && Pm > kBigCap) {
       wide_suffix(S.B, S.C, m, reinterpret_cast<double*>(smem));
       double* coarse = reinterpret_cast<double*>(smem + 2 * 8 * kBigCap);  // C + D regions: kCoarseMax entries
       const int cs = coarse_step(m);
@@ -1176,7 +1203,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     double wv = 0.0;
     const bool em = i < m - 1 &&
                     draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv,
-                                m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
+                                WIDE && m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
                                 coarse_step(m));
     if (base == 0) SUB(3);
     if (em) {
@@ -1229,7 +1256,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // keep-one (any width) + publish the rest
   unsigned long long best = 0;
   for (int t = tid; t < nready; t += kThreads) {
-    const unsigned long long rr = ready[t] | (1ull << 63);
+    const unsigned long long rr = keep_key(d, ready[t]);
     best = rr > best ? rr : best;
   }
 #pragma unroll
@@ -1340,7 +1367,10 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
       d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
       d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
     }
-    const int next = cta_eliminate(d, k, smem, sh, ++chain < d.keep_limit);
+    cta_prologue(d, k, sh);
+    const bool allow = ++chain < d.keep_limit;
+    const int next = sh.R > kBigCap ? cta_eliminate<true>(d, k, smem, sh, allow)
+                                    : cta_eliminate<false>(d, k, smem, sh, allow);
     if (next == -2) break;
     PHASE(7);
     ++done_local;

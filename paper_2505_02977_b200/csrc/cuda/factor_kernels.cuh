@@ -37,8 +37,8 @@ struct Ctrl {
   unsigned long long large_bump;  // large-column slab pool (entries)
   long long total_fills;
   long long err_info;
-  int kept;              // hand-offs that skipped the queue (keep-one)
-  int pad;
+  int pad0;
+  int pad1;
 };
 
 struct FactorDev {
@@ -66,6 +66,7 @@ struct FactorDev {
   unsigned long long* cnt;
   int* queue;   // main queue [n]
   int* bqueue;  // big-column queue [n]
+  int keep_pos; // keep-one preference: 0 widest column, 1 lowest position
   // fills
   int4* pool0;
   unsigned* dir;

@@ -85,6 +85,23 @@ __global__ void warp_parts(int m, long long* out) {
   if (lane == 0) out[8] = (t1 - t0) / 10;
 }
 
+
+// cold-instruction-cache variant: one raw rank sort per launch (first touch of its code on that SM)
+__global__ void cold_raw(int m, long long* out) {
+  __shared__ unsigned long long A[1024], X1[1024], X2[1024];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 1024; i += blockDim.x) A[i] = (static_cast<unsigned long long>((i * 2654435761u) & 0xfffff) << 32) | 1u;
+  __syncthreads();
+  long long t0 = clock64();
+  unsigned long long key[1];
+  key[0] = tid < m ? A[tid] : ~0ull;
+  int rank[1];
+  rank_sort<kThreads, 1>(key, m, X1, X2, rank);
+  __syncthreads();
+  long long t1 = clock64();
+  if (tid == 0) out[12 + blockIdx.x % 4] = t1 - t0;
+}
+
 int main() {
   long long* out; double* sink;
   cudaMalloc(&out, 256); cudaMalloc(&sink, 64);
@@ -95,6 +112,12 @@ int main() {
     cudaMemcpy(h, out, 128, cudaMemcpyDeviceToHost);
     printf("m=%3d  cta: weight rank sort %6lld  lkk chain %6lld  suffix chain %6lld  ddiv col %5lld  raw rank sort %6lld cyc | warp weight sort %6lld cyc\n",
            m, h[0], h[1], h[2], h[3], h[4], h[8]);
+  }
+  for (int m : {103, 173, 256}) {
+    cold_raw<<<148, kThreads>>>(m, out);  // every SM runs the code once (cold)
+    long long h[16];
+    cudaMemcpy(h, out, 128, cudaMemcpyDeviceToHost);
+    printf("cold raw rank sort m=%d: %lld %lld cycles (first touch per SM)\n", m, h[12], h[13]);
   }
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;

@@ -200,7 +200,7 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
  * and sorted, 2 merged, 3 column written, 4 weight-sorted + suffix, 5 fills
  * emitted, 6 decremented, 7 end (after publishing). Zero = phase skipped. */
 int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end);
-/* Diagnostics: sub-phase timestamps sub[8*k + i] of the same run (i = 0 setup
+/* Diagnostics: sub-phase timestamps sub[8*k + i] (then 4 rank-sort cycle counters per position at sub[8*n + 4*k]) of the same run (i = 0 setup
  * loads done, 1 gather landed, 2 weight sort done, 3 samples drawn, 4 fills
  * written, 5 release fence done; zero = not recorded on that path). */
 int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub);

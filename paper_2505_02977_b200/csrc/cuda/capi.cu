@@ -239,8 +239,8 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     ctx->vtimes.ensure(8 * nn);
     check(cudaMemsetAsync(ctx->vtimes.p, 0, 8 * nn * sizeof(unsigned long long), s), "memset");
     d.vtimes = ctx->vtimes.p;
-    ctx->vsub.ensure(8 * nn);
-    check(cudaMemsetAsync(ctx->vsub.p, 0, 8 * nn * sizeof(unsigned long long), s), "memset");
+    ctx->vsub.ensure(12 * nn);  // 8 sub-phase stamps + 4 cycle counters (rank-sort diagnostics)
+    check(cudaMemsetAsync(ctx->vsub.p, 0, 12 * nn * sizeof(unsigned long long), s), "memset");
     d.vsub = ctx->vsub.p;
   }
 
@@ -650,7 +650,7 @@ int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub) {
   return guarded([&] {
     require_ctx(ctx);
     if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
-    check(cudaMemcpy(sub, ctx->vsub.p, sizeof(unsigned long long) * 8 * ctx->f_n, cudaMemcpyDeviceToHost), "d2h");
+    check(cudaMemcpy(sub, ctx->vsub.p, sizeof(unsigned long long) * 12 * ctx->f_n, cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

@@ -293,16 +293,19 @@ __device__ __forceinline__ void cta_reg_sort(unsigned long long (&key)[ITEMS],
 // (factor_common.hpp:133-145).
 template <int T, int ITEMS>
 __device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], int R, unsigned long long* X1,
-                                          unsigned long long* X2, int (&rank)[ITEMS]) {
+                                          unsigned long long* X2, int (&rank)[ITEMS], long long* cyc = nullptr) {
   const int tid = T == 32 ? lane_id() : static_cast<int>(threadIdx.x);
   const int lane = tid & 31;
   const int wid = tid >> 5;
+  long long c0 = 0;
+  if (cyc && tid == 0) c0 = clock64();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int g = i * T + tid;
     if (g < R) X2[g] = k[i];
   }
   if (T == 32) __syncwarp(); else __syncthreads();
+  if (cyc && tid == 0) cyc[0] = clock64() - c0;
   int lr[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -321,6 +324,7 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], 
     lr[i] = c;
   }
   if (T == 32) __syncwarp(); else __syncthreads();
+  if (cyc && tid == 0) cyc[1] = clock64() - c0;
   const int nseg = (R + 31) >> 5;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -351,6 +355,7 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], 
     }
     rank[i] = r;
   }
+  if (cyc && tid == 0) cyc[2] = clock64() - c0;
 }
 
 // ---- warp path (rank sort): gather + raw sort, weight sort (results in A/B)
@@ -430,7 +435,8 @@ __device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long lon
     if (threadIdx.x == 0) *stamp = globaltimer_ns();
   }
   int rank[ITEMS];
-  rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, rank);
+  long long* cyc = d.vsub ? reinterpret_cast<long long*>(d.vsub + d.n * 8ll + 4ll * k) : nullptr;
+  rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, rank, cyc);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (i * kThreads + static_cast<int>(threadIdx.x) < R) {

@@ -42,9 +42,10 @@ def main():
     for _ in range(2):
         f = P.factor_gpu(g, o, 0, opts, st, ctx=ctx)
     tt = ctx.vertex_times().astype(np.int64)
-    sub = np.zeros(8 * g.n, np.uint64)
-    P.rchol._check(P.rchol.lib.parac_gpu_download_subtimes(ctx.handle, sub.ctypes.data))
-    sub = sub.reshape(g.n, 8).astype(np.int64)
+    sub_all = np.zeros(12 * g.n, np.uint64)
+    P.rchol._check(P.rchol.lib.parac_gpu_download_subtimes(ctx.handle, sub_all.ctypes.data))
+    sub = sub_all[:8 * g.n].reshape(g.n, 8).astype(np.int64)
+    cyc = sub_all[8 * g.n:].reshape(g.n, 4).astype(np.int64)
     n = g.n
     t0 = tt[:, 0].min()
     start = (tt[:, 0] - t0) / 1e3  # us
@@ -151,6 +152,12 @@ def main():
         "claimed_small": stat(~kept & ~bigc),
         "big_eliminations": int(bigc.sum()),
     }
+    cc = cyc[chs]
+    okc = cc[:, 2] > 0
+    if okc.any():
+        out["critical_path"]["cta_raw_rank_sort_cycles"] = {
+            "count": int(okc.sum()), "x2_store_sync": float(cc[okc, 0].mean()),
+            "phase1_done": float(cc[okc, 1].mean()), "phase2_done": float(cc[okc, 2].mean())}
     top = np.argsort(-hops)[:8]
     out["critical_path"]["worst_hops"] = [
         {"pos": int(chs[i]), "hop_us": float(hops[i]), "start_us": float(start[chs[i]]),

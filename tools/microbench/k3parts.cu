@@ -28,7 +28,7 @@ __global__ void parts(int m, long long* out, double* sink) {
     wk[0] = g < m ? dbits(B[g]) : kInfBits;
     ak[0] = g < m ? A[g] : ~0ull;
     int rank[1];
-    rank_sort<kThreads, 1>(wk, m, S.X1, S.X2, rank);
+    rank_sort<kThreads, 1>(wk, m, S.X1, S.X2, reinterpret_cast<int*>(Cs), reinterpret_cast<int*>(Cs) + 1024, rank);
     __syncthreads();
     if (g < m) { X1[rank[0]] = ak[0]; }
     __syncthreads();
@@ -54,7 +54,8 @@ __global__ void parts(int m, long long* out, double* sink) {
     unsigned long long key[1];
     key[0] = tid < m ? A[tid] : ~0ull;
     int rank[1];
-    rank_sort<kThreads, 1>(key, m, S.X1, S.X2, rank);
+    rank_sort<kThreads, 1>(key, m, S.X1, S.X2, reinterpret_cast<int*>(Cs), reinterpret_cast<int*>(Cs) + 1024, rank);
+    if (tid < m) X2[rank[0]] = key[0];
     __syncthreads();
   }
   long long t5 = clock64();
@@ -96,7 +97,9 @@ __global__ void cold_raw(int m, long long* out) {
   unsigned long long key[1];
   key[0] = tid < m ? A[tid] : ~0ull;
   int rank[1];
-  rank_sort<kThreads, 1>(key, m, X1, X2, rank);
+  __shared__ int IAB[2048];
+  rank_sort<kThreads, 1>(key, m, X1, X2, IAB, IAB + 1024, rank);
+  if (tid < m) A[rank[0]] = key[0];
   __syncthreads();
   long long t1 = clock64();
   if (tid == 0) out[12 + blockIdx.x % 4] = t1 - t0;

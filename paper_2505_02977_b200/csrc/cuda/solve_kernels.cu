@@ -1656,6 +1656,112 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
   }
 }
 
+// ---- wide levels: one ordinary launch per level. The first ~150 levels of a
+// 3D problem hold 10^2-3*10^5 rows of 5-100 entries each: enough independent
+// rows to fill the GPU, so the kernel boundary is the level barrier and no
+// in-kernel grid barrier is needed. K lanes share a row (K chosen per level
+// from its mean row length) so a row's loads issue in parallel; each lane sums
+// a fixed stride of the row and the K partials are combined by a fixed xor
+// tree (deterministic). Launched with programmatic dependent launch: the
+// factor data (row pointers, entries, dinv -- constant during the solve) are
+// loaded before griddepcontrol.wait, so the next level's index loads and
+// launch overlap the current level; x and the right-hand side are read after.
+constexpr int kWideRegs = 4;  // entries per lane staged before the wait
+
+template <bool FWD, int K>
+__global__ void __launch_bounds__(256) wide_level_kernel(long long j0, long long j1, const long long* __restrict__ lptr,
+                                                          const int* __restrict__ lidx, const double* __restrict__ lval,
+                                                          const double* rhs_l, const double* __restrict__ dinv_l,
+                                                          double* x, double* yd_l, int rhs_early,
+                                                          unsigned long long* lt) {
+  const int lane = threadIdx.x % K;
+  const long long j = j0 + (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) / K;
+  const bool live = j < j1;
+  long long b = 0, e = 0;
+  if (live) {
+    b = lptr[j];
+    e = lptr[j + 1];
+  }
+  int c[kWideRegs];
+  double g[kWideRegs];
+#pragma unroll
+  for (int t = 0; t < kWideRegs; ++t) {
+    const long long q = b + lane + static_cast<long long>(t) * K;
+    const bool ok = q < e;
+    c[t] = ok ? lidx[q] : 0;
+    g[t] = ok ? lval[q] : 0.0;
+  }
+  const bool head = live && lane == 0;
+  const double di = (FWD && head) ? dinv_l[j] : 0.0;
+  double rh = (rhs_early && head) ? __ldcg(rhs_l + j) : 0.0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // dependents launch once every CTA of this level is past its wait, i.e. once
+  // the level before this one has completed: their early loads never see a
+  // vector a kernel still running may write (rhs_early relies on this)
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (lt && blockIdx.x == 0 && threadIdx.x == 0) *lt = globaltimer_ns();
+  double xv[kWideRegs];
+#pragma unroll
+  for (int t = 0; t < kWideRegs; ++t) xv[t] = __ldcg(x + c[t]);
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < kWideRegs; ++t) s += g[t] * xv[t];
+  for (long long q = b + lane + static_cast<long long>(kWideRegs) * K; q < e; q += K) s += lval[q] * __ldcg(x + lidx[q]);
+#pragma unroll
+  for (int o = K / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (head) {
+    if (!rhs_early) rh = __ldcg(rhs_l + j);
+    const double acc = rh - s;
+    x[j] = acc;
+    if (FWD) yd_l[j] = acc * di;
+  }
+}
+
+template <bool FWD>
+cudaError_t launch_wide_level(int K, long long j0, long long j1, cudaStream_t st, const long long* lptr,
+                              const int* lidx, const double* lval, const double* rhs_l, const double* dinv_l,
+                              double* x, double* yd_l, int rhs_early, unsigned long long* lt) {
+  cudaLaunchConfig_t cfg = {};
+  const long long threads = (j1 - j0) * K;
+  cfg.gridDim = dim3(static_cast<unsigned>((threads + 255) / 256), 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+#define PARAC_WIDE_CASE(KK)                                                                                  \
+  case KK:                                                                                                   \
+    return cudaLaunchKernelEx(&cfg, wide_level_kernel<FWD, KK>, j0, j1, lptr, lidx, lval, rhs_l, dinv_l, x, \
+                              yd_l, rhs_early, lt);
+  switch (K) {
+    PARAC_WIDE_CASE(1)
+    PARAC_WIDE_CASE(2)
+    PARAC_WIDE_CASE(4)
+    PARAC_WIDE_CASE(8)
+    PARAC_WIDE_CASE(16)
+    default:
+      return cudaLaunchKernelEx(&cfg, wide_level_kernel<FWD, 32>, j0, j1, lptr, lidx, lval, rhs_l, dinv_l, x, yd_l,
+                                rhs_early, lt);
+  }
+#undef PARAC_WIDE_CASE
+}
+
+// lanes per row for a level of `rows` rows and `ents` entries: the mean row
+// spread over <= kWideRegs entries per lane, at most a warp
+inline int wide_lanes(long long rows, long long ents) {
+  const long long mean = rows > 0 ? (ents + rows - 1) / rows : 1;
+  int K = 1;
+  while (K < 32 && static_cast<long long>(K) * kWideRegs < mean) K *= 2;
+  return K;
+}
+
+__global__ void rhs_permute_kernel(int n, const int* rlab, const double* r, double* rhs_l) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) rhs_l[j] = r[rlab[j]];
+}
+
 // hrec[L][w]: chunk w of level L (whole rows, ~equal entries + rows), for W warps.
 __global__ void head_chunk_kernel(int depth, int W, const long long* lvl_off, const long long* lptr, int4* hrec) {
   const int L = blockIdx.x + 1;
@@ -2459,6 +2565,13 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
       Lw = L;
     }
     s.wide_L = Lw;
+    s.wide_kf.assign(static_cast<std::size_t>(Lw) + 1, 1);
+    s.wide_kb.assign(static_cast<std::size_t>(Lw) + 1, 1);
+    for (int L = 1; L <= Lw; ++L) {
+      s.wide_kf[L] = wide_lanes(off[L + 1] - off[L], ef[L + 1] - ef[L]);
+      s.wide_kb[L] = wide_lanes(off[L + 1] - off[L], eb[L + 1] - eb[L]);
+    }
+    s.lvl_off_h.assign(off.begin(), off.begin() + std::min<std::size_t>(off.size(), static_cast<std::size_t>(Lw) + 2));
     if (Lw > 0) {
       const std::size_t ng = (static_cast<std::size_t>(Lw) + 2) * s.grid_W;
       if (s.cap_grec < ng) {
@@ -2665,11 +2778,20 @@ struct Solver {
       const int H = s.t3_L0, nt = s.t3_nt;
       const int Lw = std::min(s.wide_L, H);
       unsigned long long* lt = s.ltime;
-      if (Lw > 0) {
+      static const bool coop_wide = std::getenv("PARAC_WIDE") && std::string(std::getenv("PARAC_WIDE")) == "coop";
+      if (Lw > 0 && coop_wide) {
         check(launch_coop(head_sweep_kernel<true, true>, s.grid_ctas, kHThreads, kHeadSmem, st, 1, Lw, s.grid_W,
                           s.hrec_gf, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, s.rlab, r,
                           in.f_n, 0, s.t3_base, s.tail_s, lt), "wide forward");
         note_launches(1);
+      } else if (Lw > 0) {
+        rhs_permute_kernel<<<(in.f_n + 255) / 256, 256, 0, st>>>(in.f_n, s.rlab, r, s.rhs_l);
+        for (int L = 1; L <= Lw; ++L) {
+          const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
+          check(launch_wide_level<true>(s.wide_kf[L], j0, j1, st, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l,
+                                        s.yf, s.yd, L >= 2, lt ? lt + (L - 1) : nullptr), "wide level forward");
+        }
+        note_launches(1 + Lw);
       }
       check(launch_cluster_t(head_sweep_kernel<true, false>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
                              s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd,
@@ -2690,11 +2812,19 @@ struct Solver {
       check(launch_cluster_t(head_sweep_kernel<false, false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
                              s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr,
                              nullptr, in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) : nullptr), "head backward");
-      if (Lw > 0) {
+      if (Lw > 0 && coop_wide) {
         check(launch_coop(head_sweep_kernel<false, true>, s.grid_ctas, kHThreads, kHeadSmem, st, Lw, Lw, s.grid_W,
                           s.hrec_gb, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr, nullptr,
                           in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) + (H - Lw) : nullptr), "wide backward");
         note_launches(1);
+      } else if (Lw > 0) {
+        for (int L = Lw; L >= 1; --L) {
+          const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
+          check(launch_wide_level<false>(s.wide_kb[L], j0, j1, st, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb,
+                                         nullptr, 1, lt ? lt + 3 * (D + 2) + (H - Lw) + (Lw - L) : nullptr),
+                "wide level backward");
+        }
+        note_launches(Lw);
       }
       gather_z_l_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, s.v2l, s.zb, r, z, part(slot));
       note_launches(2);

@@ -1934,7 +1934,14 @@ inline std::size_t tail4_smem(int nlev) {
 // warp w piece = {row (tail index, -1 none), eb, ee, wpr}. Keeping the integer
 // divisions of the (row, slice) split out of the level loop matters: they
 // were ~half of a level's dependent instruction chain.
-__global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const int* ep, int4* pieces) {
+//
+// A row gets only as many of its wpr warps as its length needs (epw entries
+// per warp, default 32 * kT4PF = one register set): the 32 warps share four
+// schedulers, so every warp that joins a level costs issue slots on the
+// level's critical path even when it holds 3 entries; the rest idle at the
+// barriers.
+__global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const int* ep, int4* pieces,
+                                    int epw = 32 * kT4PF) {
   const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int warp = threadIdx.x & 31;  // one thread per (level, warp)
   if (t >= nlev) return;
@@ -1947,14 +1954,14 @@ __global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const in
     const int row = lb + ri;
     const int si = warp - ri * wpr;
     const int rb = ep[row], len = ep[row + 1] - rb;
+    const int use = min(wpr, max(1, (len + epw - 1) / epw));
     // .w = number of slices for the row's FIRST slice (it combines them), else 0
-    pc = make_int4(row, rb + static_cast<int>((static_cast<long long>(len) * si) / wpr),
-                   rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / wpr), si == 0 ? wpr : 0);
+    if (si < use)
+      pc = make_int4(row, rb + static_cast<int>((static_cast<long long>(len) * si) / use),
+                     rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / use), si == 0 ? use : 0);
   }
   pieces[static_cast<long long>(t) * 32 + warp] = pc;
 }
-
-
 
 // Latency plan of the level loop (HBM round trips here are ~1-1.5 us, a
 // level should take ~0.3 us): nothing a level needs may be loaded later
@@ -2040,13 +2047,16 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
     if (tid == 32) l2(t + kT4L2);
     if (pc.x >= 0) {
       p = warp_sum(p);
-      if (lane == 0) part[warp] = p;
+      if (lane == 0 && pc.w != 1) part[warp] = p;
     }
     cp_async_wait<kT4Ring - 4>();  // level t+3's records have landed (needed after the barrier)
     __syncthreads();
     if (pc.x >= 0 && pc.w > 0) {  // the row's first warp publishes it
-      double sp = lane < pc.w ? part[warp + lane] : 0.0;
-      sp = warp_sum(sp);
+      double sp = p;
+      if (pc.w > 1) {
+        sp = lane < pc.w ? part[warp + lane] : 0.0;
+        sp = warp_sum(sp);
+      }
       if (lane == 0) {
         const double acc = xs[pc.x] - sp;
         xs[pc.x] = acc;
@@ -2639,8 +2649,10 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
     dalloc(s.t4_brange, static_cast<std::size_t>(nlev) + 1);
     s.cap_t4 = npc;
   }
-  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 1, s.t3_lvl, s.t3_fep, s.t4_fpc);
-  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 0, s.t3_lvl, s.t3_bep, s.t4_bpc);
+  const char* epw_env = std::getenv("PARAC_TAIL_EPW");
+  const int epw = epw_env ? std::max(1, std::atoi(epw_env)) : 32 * kT4PF;
+  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 1, s.t3_lvl, s.t3_fep, s.t4_fpc, epw);
+  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 0, s.t3_lvl, s.t3_bep, s.t4_bpc, epw);
   tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_fpc, s.t4_frange);
   tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_bpc, s.t4_brange);
   note_launches(4);

@@ -44,9 +44,3 @@ if nt:
     show("tail fwd", t[1], np.arange(H + 1, D + 1), ent_f)
     show("tail bwd", t[2], np.arange(D, H, -1), ent_b)
 show("head bwd", t[3], np.arange(H, 0, -1), ent_b)
-if nt:
-    nlev = D - H
-    dbg = t_all[(D + 2) + 4 * (nlev + 2):(D + 2) + 4 * (nlev + 2) + 4 * nlev].reshape(nlev, 4)
-    print("tail fwd cycles per level (thread 0): products / prefetch+sync / rows / sync")
-    for lo, hi in ((0, 50), (50, 200), (200, 500), (500, nlev)):
-        print(f"   steps [{lo},{hi}):", dbg[lo:hi].mean(axis=0).round(0))

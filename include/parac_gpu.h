@@ -215,6 +215,13 @@ int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_pt
  * of the resident factor; returns the depth in *depth. levels may be NULL. */
 int parac_gpu_schedule_levels(parac_gpu_ctx* ctx, int32_t* levels, int32_t* depth);
 
+/* ordering_nnz_sort (ordering.hpp:32, src/ordering.cpp:49-70) on the device:
+ * the same perm as parac_ordering_nnz_sort (bit-identical order: the fp64 tie
+ * is an exact scaling of a 53-bit integer, so a stable radix sort by
+ * (tie bits, degree) over vertices 0..n-1 reproduces std::sort's order).
+ * Uses only g->ptr (degrees); does not touch the context's staged graph. */
+int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t seed, int32_t* perm);
+
 /* ---- solve ------------------------------------------------------------------
  * SolveConfig / SolveReport (include/parac/solver.hpp:13-25). */
 typedef struct {

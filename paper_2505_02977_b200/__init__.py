@@ -7,6 +7,6 @@ from .rchol import (  # noqa: F401
     SolveConfig, SolveReport, factor_gpu, pcg_solve_gpu, apply_preconditioner_gpu,
     laplacian_apply_gpu, schedule_levels_gpu, dependency_counts, make_rhs, gen_poisson3d,
     gen_poisson2d, gen_poisson27, gen_rmat, gen_random_connected, gen_random_components,
-    ordering_random, ordering_nnz_sort, default_context, device_count, factor_batch_gpu,
+    ordering_random, ordering_nnz_sort, ordering_nnz_sort_gpu, default_context, device_count, factor_batch_gpu,
 )
 from ._lib import LIB_PATH  # noqa: F401

@@ -86,6 +86,7 @@ SIGNATURES = {
     "parac_gpu_download_batch": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "parac_gpu_schedule_levels": (C.c_int, [vp, vp, P(i32)]),
+    "parac_gpu_ordering_nnz_sort": (C.c_int, [vp, P(parac_csr), u64, vp]),
     "parac_gpu_pcg": (C.c_int, [vp, vp, f64, i32, vp, P(parac_gpu_solve_report)]),
     "parac_gpu_set_preconditioner_mode": (C.c_int, [vp, i32]),
     "parac_gpu_apply_preconditioner": (C.c_int, [vp, vp, vp]),

@@ -351,6 +351,28 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   delete ctx;
 }
 
+int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t seed, int32_t* perm) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!g || g->n < 0 || (g->n > 0 && (!g->ptr || !perm))) throw Failure{dimension_mismatch, "bad graph"};
+    const int n = g->n;
+    if (n == 0) return;
+    cudaStream_t s = ctx->stream;
+    long long* d_ptr = nullptr;
+    int* d_perm = nullptr;
+    check(cudaMallocAsync(&d_ptr, sizeof(long long) * (static_cast<std::size_t>(n) + 1), s), "alloc");
+    check(cudaMallocAsync(&d_perm, sizeof(int) * static_cast<std::size_t>(n), s), "alloc");
+    check(cudaMemcpyAsync(d_ptr, g->ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s), "h2d");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    nnz_sort_device(n, d_ptr, derive_seed(seed, kSaltTieBreak), d_perm, s, sms);
+    check(cudaMemcpyAsync(perm, d_perm, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
+    check(cudaFreeAsync(d_ptr, s), "free");
+    check(cudaFreeAsync(d_perm, s), "free");
+    check(cudaStreamSynchronize(s), "nnz_sort sync");
+  });
+}
+
 int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm) {
   return guarded([&] {
     require_ctx(ctx);

@@ -121,5 +121,7 @@ cudaError_t launch_batch_offsets(int count, long long N, long long NNZ, const lo
 cudaError_t launch_extract_fills(int n, const unsigned long long* cnt, int* out, cudaStream_t s);
 cudaError_t launch_batch_local_rows(int n, const long long* col_ptr, const int* pos_pid, const long long* base,
                                     int* rows, cudaStream_t s);
+// ordering_nnz_sort on the device (ordering.cu): perm from the CSR row pointer
+void nnz_sort_device(int n, const long long* d_ptr, std::uint64_t tie_seed, int* d_perm, cudaStream_t st, int sms);
 
 }  // namespace parac_gpu

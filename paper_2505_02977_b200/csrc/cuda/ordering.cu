@@ -1,0 +1,125 @@
+// Device ordering_nnz_sort (proj/src/ordering.cpp:49-70).
+//
+// The reference sorts (degree, tie, vertex) with std::sort, where
+// tie = SampleStream::unit_uniform(derive_seed(seed, kSaltTieBreak), v, 0)
+// = (x >> 11) * 2^-53. That fp64 value is an exact scaling of the 53-bit
+// integer x >> 11, so comparing ties equals comparing those integers, and the
+// whole key is an integer tuple: a stable LSD radix sort of the vertices
+// 0..n-1 by (tie bits, then degree) yields exactly the reference order (the
+// vertex id breaks remaining ties through stability). When the largest degree
+// fits in 11 bits the two keys pack into one 64-bit key and one sort suffices.
+// Then perm[vertex at p] = p.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <string>
+
+#include "../host/errors.hpp"
+#include "common.cuh"
+#include "factor_kernels.cuh"
+
+namespace parac_gpu {
+void note_launches(long long k);  // defined in capi.cu
+namespace {
+
+__device__ __forceinline__ unsigned long long tie_bits(std::uint64_t seed, long long v) {
+  std::uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (static_cast<std::uint64_t>(v) + 1);
+  x = dev::mix64(x);
+  x = dev::mix64(x ^ (0xd1b54a32d192ed03ULL * 1ULL));  // counter 0
+  return x >> 11;
+}
+
+__global__ void nnz_keys_kernel(int n, const long long* ptr, std::uint64_t tie_seed, int packed,
+                                unsigned long long* key, int* vert) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const long long d = ptr[v + 1] - ptr[v];
+    const unsigned long long t = tie_bits(tie_seed, v);
+    key[v] = packed ? (static_cast<unsigned long long>(d) << 53) | t : t;
+    vert[v] = v;
+  }
+}
+
+__global__ void max_degree_kernel(int n, const long long* ptr, long long* maxdeg) {
+  long long local = 0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    local = max(local, ptr[v + 1] - ptr[v]);
+  for (int o = 16; o > 0; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(maxdeg), static_cast<unsigned long long>(local));
+}
+
+__global__ void degree_of_kernel(int n, const long long* ptr, const int* vert, unsigned int* deg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = vert[i];
+    deg[i] = static_cast<unsigned int>(ptr[v + 1] - ptr[v]);
+  }
+}
+
+__global__ void positions_kernel(int n, const int* vert, int* perm) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) perm[vert[p]] = p;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Failure{internal_error, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+int bits_for(unsigned long long v) {
+  int b = 0;
+  while (b < 64 && (v >> b) != 0) ++b;
+  return std::max(b, 1);
+}
+
+}  // namespace
+
+void nnz_sort_device(int n, const long long* d_ptr, std::uint64_t tie_seed, int* d_perm, cudaStream_t st, int sms) {
+  if (n <= 0) return;
+  const int grid = std::min((n + 255) / 256, sms * 8);
+  long long* d_max = nullptr;
+  cuda_check(cudaMallocAsync(&d_max, sizeof(long long), st), "alloc");
+  cuda_check(cudaMemsetAsync(d_max, 0, sizeof(long long), st), "memset");
+  max_degree_kernel<<<grid, 256, 0, st>>>(n, d_ptr, d_max);
+  long long maxdeg = 0;
+  cuda_check(cudaMemcpyAsync(&maxdeg, d_max, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  const int dbits = bits_for(static_cast<unsigned long long>(maxdeg));
+  const bool packed = dbits <= 11;
+  unsigned long long *k0 = nullptr, *k1 = nullptr;
+  int *v0 = nullptr, *v1 = nullptr;
+  const std::size_t N = static_cast<std::size_t>(n);
+  cuda_check(cudaMallocAsync(&k0, N * 8, st), "alloc");
+  cuda_check(cudaMallocAsync(&k1, N * 8, st), "alloc");
+  cuda_check(cudaMallocAsync(&v0, N * 4, st), "alloc");
+  cuda_check(cudaMallocAsync(&v1, N * 4, st), "alloc");
+  nnz_keys_kernel<<<grid, 256, 0, st>>>(n, d_ptr, tie_seed, packed ? 1 : 0, k0, v0);
+  note_launches(2);
+  cub::DoubleBuffer<unsigned long long> keys(k0, k1);
+  cub::DoubleBuffer<int> vals(v0, v1);
+  std::size_t tmp_bytes = 0;
+  const int end1 = packed ? 53 + dbits : 53;
+  cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, vals, n, 0, end1, st), "cub size");
+  // the degree pass sorts 32-bit keys of the same count: its temp need is no larger
+  void* tmp = nullptr;
+  cuda_check(cudaMallocAsync(&tmp, tmp_bytes, st), "alloc");
+  cuda_check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, vals, n, 0, end1, st), "cub sort");
+  if (!packed) {  // stable second pass by degree
+    unsigned int* d0 = reinterpret_cast<unsigned int*>(keys.Alternate());
+    unsigned int* d1 = d0 + N;  // the alternate key buffer holds 2N u32
+    degree_of_kernel<<<grid, 256, 0, st>>>(n, d_ptr, vals.Current(), d0);
+    note_launches(1);
+    cub::DoubleBuffer<unsigned int> dk(d0, d1);
+    std::size_t tmp2 = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, dk, vals, n, 0, dbits, st), "cub size");
+    if (tmp2 > tmp_bytes) {
+      cuda_check(cudaFreeAsync(tmp, st), "free");
+      cuda_check(cudaMallocAsync(&tmp, tmp2, st), "alloc");
+      tmp_bytes = tmp2;
+    }
+    cuda_check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, vals, n, 0, dbits, st), "cub sort");
+  }
+  positions_kernel<<<grid, 256, 0, st>>>(n, vals.Current(), d_perm);
+  note_launches(1);
+  for (void* p : {static_cast<void*>(k0), static_cast<void*>(k1), static_cast<void*>(v0), static_cast<void*>(v1),
+                  tmp, static_cast<void*>(d_max)})
+    cuda_check(cudaFreeAsync(p, st), "free");
+}
+
+}  // namespace parac_gpu

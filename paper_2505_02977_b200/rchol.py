@@ -533,6 +533,17 @@ def schedule_levels_gpu(factor: LdlFactor, ctx: Optional[GpuContext] = None):
     return lv[:factor.n], int(depth.value)
 
 
+def ordering_nnz_sort_gpu(graph: LaplacianGraph, seed: int, ctx: Optional[GpuContext] = None) -> Ordering:
+    """ordering_nnz_sort (ordering.hpp:32, src/ordering.cpp:49-70) computed on the
+    device: keys and a stable radix sort by (tie bits, degree); same perm as the
+    reference's std::sort (SURVEY 8(f)-1)."""
+    ctx = ctx or default_context()
+    perm = np.empty(max(graph.n, 1), dtype=np.int32)
+    csr = graph.csr()
+    _check(lib.parac_gpu_ordering_nnz_sort(ctx.handle, C.byref(csr), seed, _ptr(perm)))
+    return Ordering(perm[:graph.n])
+
+
 RHS_MODES = {"random_projected": 1, "from_random_x": 2}
 
 

@@ -111,6 +111,47 @@ int parac_ordering_nnz_sort(const parac_csr* g, uint64_t seed, int32_t* perm);
  * PARAC_NOT_A_PERMUTATION unless perm is a bijection on [0,n). */
 int parac_ordering_check(int32_t n, const int32_t* perm);
 
+/* ---- Matrix Market text I/O (include/parac/matrix_market.hpp) -------------
+ * Byte-identical files to the reference writers (values as %.17g, exact
+ * binary64 round trip); readers accept what the reference readers accept and
+ * fail with the same Errc (PARAC_IO_ERROR, PARAC_PARSE_ERROR "<path>:<line>:
+ * what", PARAC_UNSUPPORTED_FIELD, validate_laplacian's codes). Formatting and
+ * parsing run on all host threads. */
+/* read_laplacian (src/matrix_market.cpp:129-135) = read_matrix_market (:65-127)
+ * + validate_laplacian (src/graph.cpp:99-186) -> library-owned graph. */
+int parac_read_laplacian(const char* path, parac_graph* out);
+/* write_matrix_market (src/matrix_market.cpp:137-159): symmetric lower
+ * triangle, row major, diagonal (weighted degree) first. */
+int parac_write_matrix_market(const char* path, const parac_csr* g);
+/* write_factor (src/matrix_market.cpp:161-184): <stem>.G.mtx (coordinate
+ * real general, strictly lower, 1-based) and <stem>.D.mtx (array real). */
+int parac_write_factor(const char* stem, int32_t n, const int64_t* col_ptr, const int32_t* rows,
+                       const double* values, const double* diag);
+/* Library-owned LdlFactor arrays (include/parac/factor.hpp:18-25). */
+typedef struct {
+  int32_t n;
+  int64_t nnz; /* off-diagonal = col_ptr[n] */
+  int64_t* col_ptr;
+  int32_t* rows;
+  double* values;
+  double* diag;
+  int32_t* perm;
+} parac_factor;
+void parac_factor_free(parac_factor* f);
+/* read_factor (src/matrix_market.cpp:186-266): columns sorted by (row,
+ * value); perm from ordering_from_file(perm_path) or identity when
+ * perm_path is NULL or "". */
+int parac_read_factor(const char* stem, const char* perm_path, parac_factor* out);
+/* write_vector / read_vector (src/matrix_market.cpp:268-304). read_vector
+ * returns a malloc'd array (free with parac_free_array). */
+int parac_write_vector(const char* path, int64_t n, const double* values);
+int parac_read_vector(const char* path, double** values, int64_t* n);
+void parac_free_array(void* p);
+/* write_permutation / ordering_from_file + Ordering::from_positions
+ * (src/ordering.cpp:72-93, :22-36): one position per line. */
+int parac_write_permutation(const char* path, int32_t n, const int32_t* perm);
+int parac_read_permutation(const char* path, int32_t n, int32_t* perm);
+
 /* ---- device context --------------------------------------------------------
  * Owns the device buffers (reused across calls, grown on demand) and a CUDA
  * stream. Re-entrant per context; use one context per concurrent problem

@@ -185,6 +185,13 @@ class Reference:
         L.pref_make_rhs.argtypes = [vp, C.c_int, u64, vp]
         L.pref_pcg.argtypes = [vp, vp, vp, f64, C.c_int, vp, C.POINTER(C.c_int), C.POINTER(f64),
                                C.POINTER(f64), C.POINTER(C.c_int), C.POINTER(f64)]
+        L.pref_read_laplacian.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.pref_write_matrix_market.argtypes = [C.c_char_p, vp]
+        L.pref_write_factor.argtypes = [vp, C.c_char_p]
+        L.pref_read_factor.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(vp)]
+        L.pref_write_vector.argtypes = [C.c_char_p, i64, vp]
+        L.pref_read_vector.argtypes = [C.c_char_p, i64, vp, C.POINTER(i64)]
+        L.pref_write_permutation.argtypes = [C.c_char_p, i32, vp]
         self.L = L
 
     @staticmethod

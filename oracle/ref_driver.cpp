@@ -12,6 +12,9 @@
 //   schedule_levels / depth         proj/src/factor_par.cpp:659,686
 //   apply_preconditioner / laplacian_apply / pcg_solve / make_rhs
 //                                   proj/src/solver.cpp:32,76,95,177
+//   read_laplacian / write_matrix_market / write_factor / read_factor /
+//   write_vector / read_vector      proj/src/matrix_market.cpp:129-304
+//   write_permutation / ordering_from_file  proj/src/ordering.cpp:72-93
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -24,6 +27,7 @@
 #include "parac/factor_seq.hpp"
 #include "parac/generators.hpp"
 #include "parac/graph.hpp"
+#include "parac/matrix_market.hpp"
 #include "parac/ordering.hpp"
 #include "parac/rng.hpp"
 #include "parac/solver.hpp"
@@ -325,4 +329,35 @@ int pref_pcg(void* g, void* f, const double* b, double tol, int max_iters, doubl
   });
 }
 
+
+// ------------------------------------------------------------ Matrix Market
+int pref_read_laplacian(const char* path, void** out) {
+  return guarded([&] { *out = new LaplacianGraph(read_laplacian(path)); });
+}
+int pref_write_matrix_market(const char* path, void* g) {
+  return guarded([&] { write_matrix_market(path, *static_cast<LaplacianGraph*>(g)); });
+}
+int pref_write_factor(void* f, const char* stem) {
+  return guarded([&] { write_factor(static_cast<FactorBox*>(f)->f, stem); });
+}
+int pref_read_factor(const char* stem, const char* perm_path, void** out) {
+  return guarded([&] {
+    auto* box = new FactorBox;
+    box->f = read_factor(stem, perm_path ? perm_path : "");
+    *out = box;
+  });
+}
+int pref_write_vector(const char* path, std::int64_t n, const double* v) {
+  return guarded([&] { write_vector(path, std::span<const double>(v, static_cast<std::size_t>(n))); });
+}
+int pref_read_vector(const char* path, std::int64_t cap, double* v, std::int64_t* n) {
+  return guarded([&] {
+    auto x = read_vector(path);
+    *n = static_cast<std::int64_t>(x.size());
+    std::memcpy(v, x.data(), std::min<std::size_t>(x.size(), static_cast<std::size_t>(cap)) * sizeof(double));
+  });
+}
+int pref_write_permutation(const char* path, std::int32_t n, const std::int32_t* perm) {
+  return guarded([&] { write_permutation(path, ordering_from_perm(n, perm)); });
+}
 }  // extern "C"

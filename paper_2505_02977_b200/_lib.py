@@ -34,6 +34,11 @@ class parac_graph(C.Structure):
                 ("wdeg", P(f64))]
 
 
+class parac_factor(C.Structure):
+    _fields_ = [("n", i32), ("nnz", i64), ("col_ptr", P(i64)), ("rows", P(i32)), ("values", P(f64)),
+                ("diag", P(f64)), ("perm", P(i32))]
+
+
 class parac_gpu_options(C.Structure):
     _fields_ = [("fill_pool_entries", i64), ("column_arena_entries", i64),
                 ("first_chunk", i32), ("watchdog_seconds", f64), ("record_stats", i32),
@@ -87,6 +92,16 @@ SIGNATURES = {
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),
     "parac_gpu_schedule_levels": (C.c_int, [vp, vp, P(i32)]),
     "parac_gpu_ordering_nnz_sort": (C.c_int, [vp, P(parac_csr), u64, vp]),
+    "parac_read_laplacian": (C.c_int, [C.c_char_p, P(parac_graph)]),
+    "parac_write_matrix_market": (C.c_int, [C.c_char_p, P(parac_csr)]),
+    "parac_write_factor": (C.c_int, [C.c_char_p, i32, vp, vp, vp, vp]),
+    "parac_factor_free": (None, [P(parac_factor)]),
+    "parac_read_factor": (C.c_int, [C.c_char_p, C.c_char_p, P(parac_factor)]),
+    "parac_write_vector": (C.c_int, [C.c_char_p, i64, vp]),
+    "parac_read_vector": (C.c_int, [C.c_char_p, P(P(f64)), P(i64)]),
+    "parac_free_array": (None, [vp]),
+    "parac_write_permutation": (C.c_int, [C.c_char_p, i32, vp]),
+    "parac_read_permutation": (C.c_int, [C.c_char_p, i32, vp]),
     "parac_gpu_pcg": (C.c_int, [vp, vp, f64, i32, vp, P(parac_gpu_solve_report)]),
     "parac_gpu_set_preconditioner_mode": (C.c_int, [vp, i32]),
     "parac_gpu_apply_preconditioner": (C.c_int, [vp, vp, vp]),

@@ -21,6 +21,7 @@
 
 #include "../../../include/parac_gpu.h"
 #include "errors.hpp"
+#include "graph_build.hpp"
 #include "host_rng.hpp"
 
 namespace parac_gpu {
@@ -58,11 +59,6 @@ const char* errc_name(int code) {
 
 namespace {
 
-struct Edge {
-  std::int32_t a, b;
-  double w;
-};
-
 template <typename F>
 void parallel_for(std::int64_t n, F&& f) {
   unsigned hw = std::thread::hardware_concurrency();
@@ -88,6 +84,8 @@ T* dup_array(const std::vector<T>& v) {
   if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
   return p;
 }
+
+}  // namespace
 
 // LaplacianGraph::from_edges, src/graph.cpp:21-83: place both halves in input
 // order, sort each row by (neighbour, weight), reject duplicates, and sum the
@@ -151,6 +149,8 @@ void build_graph(std::int32_t n, const std::vector<Edge>& edges, parac_graph* ou
   out->w = dup_array(w);
   out->wdeg = dup_array(wdeg);
 }
+
+namespace {
 
 // LSD radix sort of 64-bit keys (used to dedupe R-MAT samples).
 void radix_sort_u64(std::vector<std::uint64_t>& keys, int bits) {

@@ -20,6 +20,7 @@ only the host container.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -542,6 +543,73 @@ def ordering_nnz_sort_gpu(graph: LaplacianGraph, seed: int, ctx: Optional[GpuCon
     csr = graph.csr()
     _check(lib.parac_gpu_ordering_nnz_sort(ctx.handle, C.byref(csr), seed, _ptr(perm)))
     return Ordering(perm[:graph.n])
+
+
+# ------------------------------------------------- Matrix Market I/O (8(f)-4)
+def _b(path) -> bytes:
+    return os.fsencode(path)
+
+
+def read_laplacian(path) -> LaplacianGraph:
+    """read_laplacian (matrix_market.hpp:30, src/matrix_market.cpp:129-135)."""
+    g = L.parac_graph()
+    _check(lib.parac_read_laplacian(_b(path), C.byref(g)))
+    return LaplacianGraph._from_native(g)
+
+
+def write_matrix_market(path, graph: LaplacianGraph) -> None:
+    """write_matrix_market (src/matrix_market.cpp:137-159), byte-identical."""
+    csr = graph.csr()
+    _check(lib.parac_write_matrix_market(_b(path), C.byref(csr)))
+
+
+def write_factor(factor: LdlFactor, stem) -> None:
+    """write_factor (src/matrix_market.cpp:161-184): <stem>.G.mtx + <stem>.D.mtx."""
+    _check(lib.parac_write_factor(_b(stem), factor.n, _ptr(factor.col_ptr), _ptr(factor.rows),
+                                  _ptr(factor.values), _ptr(factor.diag)))
+
+
+def read_factor(stem, perm_path="") -> LdlFactor:
+    """read_factor (src/matrix_market.cpp:186-266)."""
+    f = L.parac_factor()
+    _check(lib.parac_read_factor(_b(stem), _b(perm_path) if perm_path else None, C.byref(f)))
+    try:
+        n, z = f.n, f.nnz
+        arr = lambda p, k: np.ctypeslib.as_array(p, shape=(max(k, 1),))[:k].copy()  # noqa: E731
+        return LdlFactor(n, arr(f.col_ptr, n + 1), arr(f.rows, z), arr(f.values, z), arr(f.diag, n),
+                         arr(f.perm, n))
+    finally:
+        lib.parac_factor_free(C.byref(f))
+
+
+def write_vector(path, values) -> None:
+    """write_vector (src/matrix_market.cpp:268-276)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    _check(lib.parac_write_vector(_b(path), len(v), _ptr(v)))
+
+
+def read_vector(path) -> np.ndarray:
+    """read_vector (src/matrix_market.cpp:278-304)."""
+    p = C.POINTER(C.c_double)()
+    n = C.c_int64()
+    _check(lib.parac_read_vector(_b(path), C.byref(p), C.byref(n)))
+    try:
+        return np.ctypeslib.as_array(p, shape=(max(n.value, 1),))[:n.value].copy()
+    finally:
+        lib.parac_free_array(C.cast(p, C.c_void_p))
+
+
+def write_permutation(path, ordering: Ordering) -> None:
+    """write_permutation (src/ordering.cpp:87-93)."""
+    perm = np.ascontiguousarray(ordering.perm, dtype=np.int32)
+    _check(lib.parac_write_permutation(_b(path), len(perm), _ptr(perm)))
+
+
+def ordering_from_file(path, n: int) -> Ordering:
+    """ordering_from_file (src/ordering.cpp:72-85) + from_positions validation."""
+    perm = np.empty(max(n, 1), dtype=np.int32)
+    _check(lib.parac_read_permutation(_b(path), n, _ptr(perm)))
+    return Ordering(perm[:n])
 
 
 RHS_MODES = {"random_projected": 1, "from_random_x": 2}

@@ -1414,7 +1414,8 @@ struct HeadPre {
   int4 rec;               // jb, je, eb, ee
   int idx[kHeadPF];
   double val[kHeadPF];
-  int rb, re;             // lane's row entry range (relative), lane < je - jb
+  long long rb, re;       // lane's row entry range (absolute; made relative at use, so the
+                          // loads issued a level ahead are not waited on here)
   double rhs, dinv;       // lane's row right-hand side and D^+
 };
 
@@ -1434,8 +1435,8 @@ __device__ __forceinline__ void head_load(HeadPre& p, const int4 rec, const long
   p.rb = p.re = 0;
   p.rhs = p.dinv = 0.0;
   if (j < rec.y) {
-    p.rb = static_cast<int>(lptr[j] - rec.z);
-    p.re = static_cast<int>(lptr[j + 1] - rec.z);
+    p.rb = lptr[j];
+    p.re = lptr[j + 1];
     p.rhs = rhs_l[j];
     if (FWD) p.dinv = dinv_l[j];
   }
@@ -1443,6 +1444,10 @@ __device__ __forceinline__ void head_load(HeadPre& p, const int4 rec, const long
 
 // GRID: one cooperative persistent grid (all SMs) for the wide first levels,
 // grid.sync() per level; otherwise one thread-block cluster (cluster barrier).
+// (A variant keeping the cluster rows' solution in distributed shared memory,
+// with the outside operands folded into the right-hand side beforehand, was
+// measured no faster: the level time is spread over load issue, gathers, row
+// sums and the barrier wait, not the L2 round trip of the gathers.)
 template <bool FWD, bool GRID>
 __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
     int Lfirst, int nlev, int W, const int4* hrec, const long long* lptr, const int* lidx, const double* lval,
@@ -1452,6 +1457,9 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
   const int lane = lane_id(), wl = threadIdx.x >> 5;
   const int w = (GRID ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_rank())) * kHWarps + wl;
   double* pbuf = pbuf_all + wl * kChunkCap;
+  auto xget = [&](int c) -> double { return __ldcg(x + c); };
+  auto xput = [&](int j, double v) { x[j] = v; };
+  const double* rhs_rows = rhs_l;
   auto level_barrier = [&]() {
     if constexpr (GRID) cooperative_groups::this_grid().sync();
     else cluster_barrier();
@@ -1491,23 +1499,36 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
     }
     if (b.y > a.x) {
       prefetch_l2(lptr + a.x, static_cast<long long>(b.y - a.x + 1) * 8);
-      prefetch_l2(rhs_l + a.x, static_cast<long long>(b.y - a.x) * 8);
+      prefetch_l2(rhs_rows + a.x, static_cast<long long>(b.y - a.x) * 8);
       if (FWD) prefetch_l2(dinv_l + a.x, static_cast<long long>(b.y - a.x) * 8);
     }
   };
   if (pf)
     for (int tt = 1; tt <= 4; ++tt) slice_prefetch(tt);
   HeadPre nxt;
-  if (nlev > 0) head_load<FWD>(nxt, myring[0], lptr, lidx, lval, rhs_l, dinv_l, lane);
+  if (nlev > 0) head_load<FWD>(nxt, myring[0], lptr, lidx, lval, rhs_rows, dinv_l, lane);
+  // diagnostics (PARAC_SWEEP_PROFILE, cluster): warp 0's per-level phase
+  // cycles {load issue, gathers+products, sums+stores, wait+barrier}
+  unsigned long long* dbg = (!GRID && ltime && w == 0 && lane == 0) ? ltime + (FWD ? 20 : 4) * (nlev + 8) : nullptr;
+  long long c0 = clock64(), c1 = 0, c2 = 0, c3 = 0;
   for (int t = 0; t < nlev; ++t) {
+    if (dbg && t > 0) {
+      const long long cn = clock64();
+      dbg[4 * (t - 1) + 0] = c1 - c0;
+      dbg[4 * (t - 1) + 1] = c2 - c1;
+      dbg[4 * (t - 1) + 2] = c3 - c2;
+      dbg[4 * (t - 1) + 3] = cn - c3;
+      c0 = cn;
+    }
     const HeadPre cur = nxt;
-    if (t + 1 < nlev) head_load<FWD>(nxt, myring[(t + 1) % kHRing], lptr, lidx, lval, rhs_l, dinv_l, lane);
+    if (t + 1 < nlev) head_load<FWD>(nxt, myring[(t + 1) % kHRing], lptr, lidx, lval, rhs_rows, dinv_l, lane);
     {
       const int tn = t + kHRing - 1;
       if (lane == 0 && tn < nlev) cp_async16(&myring[tn % kHRing], rec_ptr(tn, w));
       cp_async_commit();
     }
     if (pf) slice_prefetch(t + 4);
+    if (dbg) c1 = clock64();
     const int jb = cur.rec.x, je = cur.rec.y, eb = cur.rec.z, ee = cur.rec.w;
     const int cnt = ee - eb;
     if (jb < je) {
@@ -1515,32 +1536,34 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
         // fast path: everything prefetched; one gather round trip
         double xv[kHeadPF];
 #pragma unroll
-        for (int q = 0; q < kHeadPF; ++q) xv[q] = q * 32 + lane < cnt ? __ldcg(x + cur.idx[q]) : 0.0;
+        for (int q = 0; q < kHeadPF; ++q) xv[q] = q * 32 + lane < cnt ? xget(cur.idx[q]) : 0.0;
 #pragma unroll
         for (int q = 0; q < kHeadPF; ++q)
           if (q * 32 + lane < cnt) pbuf[q * 32 + lane] = cur.val[q] * xv[q];
         __syncwarp();
+        if (dbg) c2 = clock64();
         const int j = jb + lane;
-        const bool mine = j < je && cur.re - cur.rb <= kShortRow;
+        const int crb = static_cast<int>(cur.rb - eb), cre = static_cast<int>(cur.re - eb);
+        const bool mine = j < je && cre - crb <= kShortRow;
         if (mine) {
           double s = 0.0;
-          for (int q = cur.rb; q < cur.re; ++q) s += pbuf[q];
+          for (int q = crb; q < cre; ++q) s += pbuf[q];
           const double acc = cur.rhs - s;
-          x[j] = acc;
+          xput(j, acc);
           if (FWD) yd_l[j] = acc * cur.dinv;
         }
         unsigned longs = __ballot_sync(kFull, j < je && !mine);
         while (longs) {
           const int src = __ffs(longs) - 1;
           longs &= longs - 1;
-          const int b2 = __shfl_sync(kFull, cur.rb, src), e2 = __shfl_sync(kFull, cur.re, src);
+          const int b2 = __shfl_sync(kFull, crb, src), e2 = __shfl_sync(kFull, cre, src);
           const double rhs = __shfl_sync(kFull, cur.rhs, src), dv = __shfl_sync(kFull, cur.dinv, src);
           double part = 0.0;
           for (int q = b2 + lane; q < e2; q += 32) part += pbuf[q];
           part = warp_sum(part);
           if (lane == 0) {
             const double acc = rhs - part;
-            x[jb + src] = acc;
+            xput(jb + src, acc);
             if (FWD) yd_l[jb + src] = acc * dv;
           }
         }
@@ -1558,7 +1581,7 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
             gv[q] = e < cnt ? lval[eb + e] : 0.0;
           }
 #pragma unroll
-          for (int q = 0; q < 8; ++q) xv[q] = base + q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
+          for (int q = 0; q < 8; ++q) xv[q] = base + q * 32 + lane < cnt ? xget(ci[q]) : 0.0;
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (base + q * 32 + lane < cnt) pbuf[base + q * 32 + lane] = gv[q] * xv[q];
@@ -1571,7 +1594,7 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
           if (j < je) {
             b = static_cast<int>(lptr[j] - eb);
             e = static_cast<int>(lptr[j + 1] - eb);
-            rhs = rhs_l[j];
+            rhs = rhs_rows[j];
             if (FWD) dv = dinv_l[j];
           }
           const bool mine = j < je && e - b <= kShortRow;
@@ -1579,7 +1602,7 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
             double sum = 0.0;
             for (int q = b; q < e; ++q) sum += pbuf[q];
             const double acc = rhs - sum;
-            x[j] = acc;
+            xput(j, acc);
             if (FWD) yd_l[j] = acc * dv;
           }
           unsigned longs = __ballot_sync(kFull, j < je && !mine);
@@ -1593,7 +1616,7 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
             part = warp_sum(part);
             if (lane == 0) {
               const double acc = rhs2 - part;
-              x[j0 + src] = acc;
+              xput(j0 + src, acc);
               if (FWD) yd_l[j0 + src] = acc * dv2;
             }
           }
@@ -1608,14 +1631,14 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
           if (j < je) {
             b = lptr[j];
             e = lptr[j + 1];
-            rhs = rhs_l[j];
+            rhs = rhs_rows[j];
             if (FWD) dv = dinv_l[j];
           }
           if (j < je && e - b <= kShortRow) {
             double s = 0.0;
-            for (long long q = b; q < e; ++q) s += lval[q] * __ldcg(x + lidx[q]);
+            for (long long q = b; q < e; ++q) s += lval[q] * xget(lidx[q]);
             const double acc = rhs - s;
-            x[j] = acc;
+            xput(j, acc);
             if (FWD) yd_l[j] = acc * dv;
           }
           unsigned longs = __ballot_sync(kFull, j < je && e - b > kShortRow);
@@ -1625,17 +1648,18 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
             const long long b2 = __shfl_sync(kFull, b, src), e2 = __shfl_sync(kFull, e, src);
             const double rhs2 = __shfl_sync(kFull, rhs, src), dv2 = __shfl_sync(kFull, dv, src);
             double part = 0.0;
-            for (long long q = b2 + lane; q < e2; q += 32) part += lval[q] * __ldcg(x + lidx[q]);
+            for (long long q = b2 + lane; q < e2; q += 32) part += lval[q] * xget(lidx[q]);
             part = warp_sum(part);
             if (lane == 0) {
               const double acc = rhs2 - part;
-              x[j0 + src] = acc;
+              xput(j0 + src, acc);
               if (FWD) yd_l[j0 + src] = acc * dv2;
             }
           }
         }
       }
     }
+    if (dbg) c3 = clock64();
     cp_async_wait<2>();  // records of levels <= t + kHRing - 3 have landed
     level_barrier();
     if (ltime && w == 0 && lane == 0) ltime[t] = globaltimer_ns();
@@ -2796,18 +2820,22 @@ struct Solver {
                           s.hrec_gf, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, s.rlab, r,
                           in.f_n, 0, s.t3_base, s.tail_s, lt), "wide forward");
         note_launches(1);
-      } else if (Lw > 0) {
+      } else {
         rhs_permute_kernel<<<(in.f_n + 255) / 256, 256, 0, st>>>(in.f_n, s.rlab, r, s.rhs_l);
+        note_launches(1);
+      }
+      if (Lw > 0 && !coop_wide) {
         for (int L = 1; L <= Lw; ++L) {
           const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
           check(launch_wide_level<true>(s.wide_kf[L], j0, j1, st, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l,
                                         s.yf, s.yd, L >= 2, lt ? lt + (L - 1) : nullptr), "wide level forward");
         }
-        note_launches(1 + Lw);
+        note_launches(Lw);
       }
       check(launch_cluster_t(head_sweep_kernel<true, false>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
                              s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd,
-                             s.rlab, Lw > 0 ? nullptr : r, in.f_n, nt, s.t3_base, s.tail_s, lt ? lt + Lw : nullptr),
+                             s.rlab, (Lw > 0 || !coop_wide) ? nullptr : r, in.f_n, nt, s.t3_base, s.tail_s,
+                             lt ? lt + Lw : nullptr),
             "head forward");
       note_launches(1);
       if (nt > 0) {
@@ -2822,12 +2850,15 @@ struct Solver {
         note_launches(2);
       }
       check(launch_cluster_t(head_sweep_kernel<false, false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
-                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr,
-                             nullptr, in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) : nullptr), "head backward");
+                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr,
+                             nullptr, nullptr, in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) : nullptr),
+            "head backward");
+      note_launches(1);
       if (Lw > 0 && coop_wide) {
         check(launch_coop(head_sweep_kernel<false, true>, s.grid_ctas, kHThreads, kHeadSmem, st, Lw, Lw, s.grid_W,
                           s.hrec_gb, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr, nullptr,
-                          in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) + (H - Lw) : nullptr), "wide backward");
+                          in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) + (H - Lw) : nullptr),
+              "wide backward");
         note_launches(1);
       } else if (Lw > 0) {
         for (int L = Lw; L >= 1; --L) {
@@ -3072,14 +3103,15 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     download(z, in.state->z, in.f_n, in.stream);
     sv.check_abort();
     if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
-    if (in.state->ltime) {  // diagnostics: [H, depth, L0] then 4 x (depth+2) timestamps
+    if (in.state->ltime) {  // diagnostics: [H, depth, tail rows, wide levels] then 16 x (depth+2) stamps
       const SolveState& ss = *in.state;
       std::vector<unsigned long long> t(16 * (static_cast<std::size_t>(ss.depth) + 2));
       check(cudaMemcpy(t.data(), ss.ltime, t.size() * 8, cudaMemcpyDeviceToHost), "d2h");
       if (FILE* f = std::fopen(std::getenv("PARAC_SWEEP_PROFILE"), "wb")) {
         const bool v3 = ss.cap_v3 > 0;
-        const int hdr[3] = {v3 ? ss.t3_L0 : ss.tail_L0, ss.depth, v3 ? ss.t3_nt : ss.tail_n};
-        std::fwrite(hdr, 4, 3, f);
+        const int hdr[4] = {v3 ? ss.t3_L0 : ss.tail_L0, ss.depth, v3 ? ss.t3_nt : ss.tail_n,
+                            v3 ? std::min(ss.wide_L, ss.t3_L0) : 0};
+        std::fwrite(hdr, 4, 4, f);
         std::fwrite(t.data(), 8, t.size(), f);
         std::fclose(f);
       }

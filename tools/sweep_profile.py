@@ -19,8 +19,8 @@ for _ in range(3):
     P.apply_preconditioner_gpu(f, r, ctx=ctx)
 lv, depth = P.schedule_levels_gpu(f, ctx=ctx)
 raw = open(path, "rb").read()
-H, D, nt = np.frombuffer(raw[:12], np.int32)
-t_all = np.frombuffer(raw[12:], np.uint64).astype(np.int64)
+H, D, nt, Lw = np.frombuffer(raw[:16], np.int32)
+t_all = np.frombuffer(raw[16:], np.uint64).astype(np.int64)
 t = t_all[:4 * (D + 2)].reshape(4, D + 2)
 w = np.bincount(lv, minlength=D + 2)
 rowlen = np.bincount(f.rows, minlength=g.n)
@@ -44,3 +44,15 @@ if nt:
     show("tail fwd", t[1], np.arange(H + 1, D + 1), ent_f)
     show("tail bwd", t[2], np.arange(D, H, -1), ent_b)
 show("head bwd", t[3], np.arange(H, 0, -1), ent_b)
+
+# DS cluster head: warp 0 phase cycles per level (see head_sweep_kernel dbg)
+nh = H - Lw
+def phases(name, base, nlev):
+    a = t_all[base:base + 4 * nlev].reshape(nlev, 4)[:-1].astype(np.int64)
+    if a.max() <= 0 or a.max() > 10**8:
+        return
+    print(f"{name} warp-0 cycles per level: load-issue / gather+products / sums+stores / wait+barrier")
+    for lo, hi in ((0, 50), (50, 150), (150, nlev)):
+        print(f"   steps [{lo},{hi}):", a[lo:hi].mean(axis=0).round(0))
+phases("head fwd", Lw + 20 * (nh + 8), nh)
+phases("head bwd", 3 * (D + 2) + 4 * (nh + 8), nh)

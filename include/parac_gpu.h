@@ -189,9 +189,11 @@ typedef struct {
   double setup_ms;          /* device: forward-CSR build + dependency init */
   double eliminate_ms;      /* device: persistent elimination kernel */
   double assemble_ms;       /* device: CSC assembly */
-  double device_ms;         /* device total (events around all factor kernels) */
+  double device_ms;         /* device total (events around all factor kernels), summed over
+                               every attempt when default budgets had to grow and retry */
   double upload_ms;         /* host->device copy (0 for resident inputs) */
   double wall_ms;           /* host wall clock of the call */
+  int32_t attempts;         /* device passes run (> 1: library-chosen budgets were grown) */
 } parac_gpu_factor_info;
 
 /* Stage graph + ordering on the device of ctx (host->device copy). */

@@ -50,7 +50,8 @@ class parac_gpu_factor_info(C.Structure):
     _fields_ = [("n", i32), ("num_edges", i64), ("nnz_off_diagonal", i64), ("total_fills", i64),
                 ("fill_pool_used", i64), ("arena_used", i64), ("max_raw", i32),
                 ("large_columns", i32), ("setup_ms", f64), ("eliminate_ms", f64),
-                ("assemble_ms", f64), ("device_ms", f64), ("upload_ms", f64), ("wall_ms", f64)]
+                ("assemble_ms", f64), ("device_ms", f64), ("upload_ms", f64), ("wall_ms", f64),
+                ("attempts", i32)]
 
 
 class parac_gpu_solve_report(C.Structure):

@@ -70,7 +70,8 @@ struct parac_gpu_ctx {
   // staged input (label space)
   int n = -1;
   long long nnz = 0;
-  DevBuf<long long> ptr;
+  long long max_degree = 0;  // of the staged graph (sizes the wide-column slab pool)
+  DevBuf<long long> ptr, scalar;
   DevBuf<int> adj;
   DevBuf<double> w;
   DevBuf<int> perm;
@@ -115,6 +116,12 @@ namespace {
 
 void activate(parac_gpu_ctx* ctx) { check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
+int device_sms(parac_gpu_ctx* ctx) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  return sms;
+}
+
 void require_ctx(parac_gpu_ctx* ctx) {
   if (!ctx) throw Failure{internal_error, "null context"};
   activate(ctx);
@@ -125,7 +132,7 @@ struct Budgets {
   int c0;
 };
 
-Budgets default_budgets(int n, long long E, const parac_gpu_options& o) {
+Budgets default_budgets(int n, long long E, long long max_degree, const parac_gpu_options& o) {
   Budgets b;
   const long long base = E + n;
   // 64 preallocated slots per position cover the fill count of ~99.5% of
@@ -139,9 +146,16 @@ Budgets default_budgets(int n, long long E, const parac_gpu_options& o) {
     const long long cap = 8600000000LL / (16LL * std::max(n, 1));
     b.c0 = cap >= 256 ? 256 : cap >= 128 ? 128 : 64;
   }
-  b.ovf = o.fill_pool_entries >= 0 ? o.fill_pool_entries : 4 * base + 4096;
-  b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : 6 * base + 4096;
-  b.large = base + 65536;
+  // hub graphs: fills concentrate on a few positions whose overflow chunks
+  // grow geometrically (up to 2x waste), and raw columns are wide
+  const bool hubs = max_degree > 512;
+  b.ovf = o.fill_pool_entries >= 0 ? o.fill_pool_entries : (hubs ? 8 : 4) * base + 4096;
+  b.arena = o.column_arena_entries >= 0 ? o.column_arena_entries : (hubs ? 8 : 6) * base + 4096;
+  // wide-column slabs (R > 1024): each big CTA's slab grows geometrically to
+  // the widest raw column it meets; hub graphs (R-MAT: raw columns up to ~10^6
+  // entries with fills) need ~4x the graph size, which the first attempt
+  // should get instead of failing after seconds and retrying
+  b.large = (hubs ? 4 : 1) * base + 65536;
   return b;
 }
 
@@ -336,7 +350,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  ctx->ptr.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
+  ctx->ptr.release(); ctx->scalar.release(); ctx->adj.release(); ctx->w.release(); ctx->perm.release();
   ctx->heavy_list.release(); ctx->heavy_count.release(); ctx->heavy_key.release(); ctx->heavy_val.release();
   ctx->inv.release(); ctx->fdeg.release(); ctx->cnt.release(); ctx->level.release(); ctx->queue.release(); ctx->bqueue.release();
   ctx->samples.release(); ctx->col_len.release();
@@ -363,9 +377,7 @@ int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t
     check(cudaMallocAsync(&d_ptr, sizeof(long long) * (static_cast<std::size_t>(n) + 1), s), "alloc");
     check(cudaMallocAsync(&d_perm, sizeof(int) * static_cast<std::size_t>(n), s), "alloc");
     check(cudaMemcpyAsync(d_ptr, g->ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s), "h2d");
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    nnz_sort_device(n, d_ptr, derive_seed(seed, kSaltTieBreak), d_perm, s, sms);
+    nnz_sort_device(n, d_ptr, derive_seed(seed, kSaltTieBreak), d_perm, s, device_sms(ctx));
     check(cudaMemcpyAsync(perm, d_perm, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "d2h");
     check(cudaFreeAsync(d_ptr, s), "free");
     check(cudaFreeAsync(d_perm, s), "free");
@@ -391,6 +403,9 @@ int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
     }
     if (n > 0)
       check(cudaMemcpyAsync(ctx->perm.p, perm, sizeof(int) * n, cudaMemcpyHostToDevice, s), "h2d");
+    ctx->scalar.ensure(1);
+    max_degree_device(n, ctx->ptr.p, ctx->scalar.p, s, device_sms(ctx));
+    check(cudaMemcpyAsync(&ctx->max_degree, ctx->scalar.p, sizeof(long long), cudaMemcpyDeviceToHost, s), "d2h");
     check(cudaStreamSynchronize(s), "h2d sync");
     ctx->n = n;
     ctx->nnz = nnz;
@@ -455,6 +470,9 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     check(cudaMemcpyAsync(ctx->pid_seed.p, ps.data(), sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, s), "h2d");
     check(launch_batch_offsets(count, N, NNZ, ctx->pid_base.p, ctx->pid_ebase.p, ctx->ptr.p, ctx->adj.p,
                                ctx->perm.p, ctx->pos_pid.p, s), "batch offsets");
+    ctx->scalar.ensure(1);
+    max_degree_device(static_cast<int>(N), ctx->ptr.p, ctx->scalar.p, s, device_sms(ctx));
+    check(cudaMemcpyAsync(&ctx->max_degree, ctx->scalar.p, sizeof(long long), cudaMemcpyDeviceToHost, s), "d2h");
     check(cudaStreamSynchronize(s), "h2d sync");
     ctx->n = static_cast<int>(N);
     ctx->nnz = NNZ;
@@ -525,13 +543,24 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
   if (rc) return rc;
   const int n = ctx->n;
   const long long E = ctx->nnz / 2;
-  Budgets b = default_budgets(n, E, o);
+  Budgets b = default_budgets(n, E, ctx->max_degree, o);
+  double failed_ms = 0.0;  // device time of attempts that ran out of library-chosen budget
+  int attempts = 0;
   for (int attempt = 0;; ++attempt) {
     rc = 0;
     int st = 0;
     rc = guarded([&] { st = run_factor(ctx, seed, o, b, info); });
     if (rc) return rc;
+    attempts = attempt + 1;
     if (st == 0) break;
+    {
+      float t = 0;
+      if (cudaEventSynchronize(ctx->ev[3]) == cudaSuccess && cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[3]) == cudaSuccess)
+        failed_ms += t;
+      if (std::getenv("PARAC_VERBOSE"))
+        std::fprintf(stderr, "parac_gpu: attempt %d ran out of budget after %.1f ms: %s\n", attempt, t,
+                     last_error());
+    }
     // Budget exhaustion with library-chosen budgets: grow and retry (the
     // caller's explicit budgets fail cleanly, like ParOptions::arena_budget).
     const bool defaults = o.fill_pool_entries < 0 && o.column_arena_entries < 0;
@@ -574,8 +603,9 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
       info->setup_ms = t01;
       info->eliminate_ms = t12;
       info->assemble_ms = t23;
-      info->device_ms = t03;
+      info->device_ms = t03 + failed_ms;
       info->wall_ms = wall.ms();
+      info->attempts = attempts;
     }
   });
   return rc;

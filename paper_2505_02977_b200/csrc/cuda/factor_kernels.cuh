@@ -123,5 +123,6 @@ cudaError_t launch_batch_local_rows(int n, const long long* col_ptr, const int* 
                                     int* rows, cudaStream_t s);
 // ordering_nnz_sort on the device (ordering.cu): perm from the CSR row pointer
 void nnz_sort_device(int n, const long long* d_ptr, std::uint64_t tie_seed, int* d_perm, cudaStream_t st, int sms);
+void max_degree_device(int n, const long long* d_ptr, long long* d_out, cudaStream_t st, int sms);
 
 }  // namespace parac_gpu

@@ -70,6 +70,14 @@ int bits_for(unsigned long long v) {
 
 }  // namespace
 
+// Largest vertex degree of a device CSR into *d_out (zeroed here).
+void max_degree_device(int n, const long long* d_ptr, long long* d_out, cudaStream_t st, int sms) {
+  cuda_check(cudaMemsetAsync(d_out, 0, sizeof(long long), st), "memset");
+  if (n <= 0) return;
+  max_degree_kernel<<<std::min((n + 255) / 256, sms * 8), 256, 0, st>>>(n, d_ptr, d_out);
+  note_launches(1);
+}
+
 void nnz_sort_device(int n, const long long* d_ptr, std::uint64_t tie_seed, int* d_perm, cudaStream_t st, int sms) {
   if (n <= 0) return;
   const int grid = std::min((n + 255) / 256, sms * 8);

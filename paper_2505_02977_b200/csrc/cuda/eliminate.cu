@@ -522,30 +522,36 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
 template <typename Less>
 __device__ __noinline__ void slab_sort(unsigned long long* K, unsigned long long* V, unsigned long long* K2,
                                        unsigned long long* V2, int R, unsigned long long padk,
-                                       unsigned long long padv, XBuf xb, Less less) {
+                                       unsigned long long padv, XBuf xb, Less less,
+                                       unsigned long long* tiles_done = nullptr) {
   const int tid = threadIdx.x;
+  // tiles: stable shared-memory rank sort of the keys (ties keep slab order,
+  // which is what Less resolves them to: raw keys are unique, and the weight
+  // sort's input is row-ascending), ~6x faster than the register bitonic
+  // network on these 1024-entry tiles; scattered straight back to the slab
   for (int tb = 0; tb < R; tb += kBigCap) {
     const int cnt = min(kBigCap, R - tb);
     unsigned long long key[4], val[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int g = tid * 4 + i;
+      const int g = i * kThreads + tid;
       key[i] = g < cnt ? K[tb + g] : padk;
       val[i] = g < cnt ? V[tb + g] : padv;
     }
-    __syncthreads();
-    cta_reg_sort<4>(key, val, xb, less);
-    __syncthreads();
+    int rank[4];
+    __syncthreads();  // the previous tile's scratch is free
+    rank_sort<kThreads, 4>(key, cnt, xb.k0, xb.v0, reinterpret_cast<int*>(xb.k1),
+                           reinterpret_cast<int*>(xb.k1) + kBigCap, rank);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int g = tid * 4 + i;
-      if (g < cnt) {
-        K[tb + g] = key[i];
-        V[tb + g] = val[i];
+      if (i * kThreads + tid < cnt) {
+        K[tb + rank[i]] = key[i];
+        V[tb + rank[i]] = val[i];
       }
     }
   }
   __syncthreads();
+  if (tiles_done && threadIdx.x == 0) *tiles_done = globaltimer_ns();
   unsigned long long *sk = K, *sv = V, *dk = K2, *dv = V2;
   for (int run = kBigCap; run < R; run *= 2) {
     for (int b = 0; b < R; b += 2 * run) {
@@ -1123,16 +1129,37 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   const XBuf xb{S.A, reinterpret_cast<unsigned long long*>(S.B),
                 reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
                 reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
+  // diagnostics (record_times, wide columns): globaltimer stamps {gather
+  // landed, raw sort done, merge done, weight sort done} in the 4 cycle slots
+  unsigned long long* wst =
+      (WIDE && d.vsub && lead) ? d.vsub + d.n * 8ll + 4ll * k : nullptr;
   if (wide) {  // global slab: shared-memory tiles + merge passes
-    for (int t = tid; t < R; t += kThreads) {
-      unsigned long long key = ~0ull;
-      double w = 0.0;
-      load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key, w);
-      S.A[t] = key;
-      S.B[t] = w;
+    // 8 raw entries in flight per thread (loads first, then the slab stores:
+    // the stores may alias nothing the loads read, but the compiler cannot know)
+    for (int t0 = tid; t0 < R; t0 += 8 * kThreads) {
+      unsigned long long key[8];
+      double w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        key[u] = ~0ull;
+        w[u] = 0.0;
+        const int t = t0 + u * kThreads;
+        if (t < R) load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key[u], w[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * kThreads;
+        if (t < R) {
+          S.A[t] = key[u];
+          S.B[t] = w[u];
+        }
+      }
     }
     __syncthreads();
-    slab_sort(S.A, reinterpret_cast<unsigned long long*>(S.B), S.X1, S.X2, R, ~0ull, 0ull, sxb, RawLess{});
+    if (wst) wst[0] = globaltimer_ns();
+    slab_sort(S.A, reinterpret_cast<unsigned long long*>(S.B), S.X1, S.X2, R, ~0ull, 0ull, sxb, RawLess{},
+              wst ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
+    if (wst) wst[1] = globaltimer_ns();
   } else if (P <= kThreads) {
     cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   } else if (P <= 2 * kThreads) {
@@ -1142,11 +1169,106 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
   PHASE(1);
 
-  // ---- 3. merge runs in place, chunks of 256 (writes stay below the chunk end)
+  // ---- 3. merge runs (rows' multiplicities and left-to-right weight sums)
   int m = 0;
+  if (WIDE) {
+    // global slab: each thread owns a contiguous block of the sorted column;
+    // pass 1 counts the segment heads in it (8 loads in flight), one CTA scan
+    // gives every thread its output offset, pass 2 sums each segment that
+    // starts in its block left to right (walking past the block end when the
+    // segment continues) into X1/X2, which then become A/B. Two passes of
+    // independent loads instead of R/256 dependent chunk round trips.
+    int* tcnt = reinterpret_cast<int*>(smem);
+    const int per = (R + kThreads - 1) / kThreads;
+    const int b0 = min(tid * per, R), b1 = min(b0 + per, R);
+    auto row_at = [&](int i) { return static_cast<int>(S.A[i] >> 32); };
+    int cnt = 0;
+    {
+      int prev = b0 > 0 && b0 < R ? row_at(b0 - 1) : -2;
+      for (int i0 = b0; i0 < b1; i0 += 8) {
+        int rw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rw[u] = i0 + u < b1 ? row_at(i0 + u) : -3;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u < b1) {
+            cnt += rw[u] != prev;
+            prev = rw[u];
+          }
+      }
+    }
+    // exclusive scan of the per-thread head counts (thread order = column order)
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh.wcount[warp] = incl;
+    __syncthreads();
+    int off = incl - cnt, total = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      off += w2 < warp ? sh.wcount[w2] : 0;
+      total += sh.wcount[w2];
+    }
+    (void)tcnt;
+    unsigned long long* OK = S.X1;
+    double* OV = reinterpret_cast<double*>(S.X2);
+    {
+      int prev = b0 > 0 && b0 < R ? row_at(b0 - 1) : -2;
+      bool open = false;
+      int cur = -1, c = 0;
+      double acc = 0.0;
+      for (int i0 = b0; i0 < b1; i0 += 8) {
+        int rw[8];
+        double wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          rw[u] = i0 + u < b1 ? row_at(i0 + u) : -3;
+          wv[u] = i0 + u < b1 ? S.B[i0 + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u >= b1) continue;
+          if (rw[u] != prev) {  // segment head
+            if (open) {
+              OK[off] = (static_cast<unsigned long long>(static_cast<unsigned>(cur)) << 32) | static_cast<unsigned>(c);
+              OV[off] = acc;
+              ++off;
+            }
+            open = true;
+            cur = rw[u];
+            acc = wv[u];
+            c = 1;
+          } else if (open) {
+            acc = __dadd_rn(acc, wv[u]);
+            ++c;
+          }  // else: the tail of a segment an earlier block owns
+          prev = rw[u];
+        }
+      }
+      if (open) {
+        for (int i = b1; i < R && row_at(i) == cur; ++i) {
+          acc = __dadd_rn(acc, S.B[i]);
+          ++c;
+        }
+        OK[off] = (static_cast<unsigned long long>(static_cast<unsigned>(cur)) << 32) | static_cast<unsigned>(c);
+        OV[off] = acc;
+      }
+    }
+    __syncthreads();
+    unsigned long long* ta = S.A;
+    double* tb = S.B;
+    S.A = S.X1;
+    S.B = reinterpret_cast<double*>(S.X2);
+    S.X1 = ta;
+    S.X2 = reinterpret_cast<unsigned long long*>(tb);
+    m = total;
+  }
   if (lead) sh.carry_row = -1;
   __syncthreads();
-  for (int base = 0; base < R; base += kThreads) {
+  for (int base = 0; !WIDE && base < R; base += kThreads) {
     const int t = base + tid;
     const int row = t < R ? static_cast<int>(S.A[t] >> 32) : -2;
     const int prev = tid == 0 ? sh.carry_row : (t - 1 < R ? static_cast<int>(S.A[t - 1] >> 32) : -2);
@@ -1182,6 +1304,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     __syncthreads();
   }
   PHASE(2);
+  if (wst) wst[2] = globaltimer_ns();
   if (m == 0) {
     if (lead) d.diag[k] = 0.0;
     return -1;
@@ -1222,6 +1345,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     if (WIDE && Pm > kBigCap) {
       // key = weight bits, payload = A (row << 32 | mult): (weight, row) order
       slab_sort(reinterpret_cast<unsigned long long*>(S.B), S.A, S.X1, S.X2, m, kInfBits, ~0ull, sxb, WeightLess{});
+      if (wst) wst[3] = globaltimer_ns();
     } else if (Pm <= kThreads) {
       cta_rank_weight<1>(m, S);
     } else if (Pm <= 2 * kThreads) {

@@ -153,6 +153,21 @@ def main():
         "big_eliminations": int(bigc.sum()),
     }
     cc = cyc[chs]
+    wide = cc[:, 0] > 10**15  # wide columns store globaltimer stamps here, not cycles
+    if wide.any():
+        w = cc[wide].astype(np.float64)
+        s0 = sub[chs][wide, 0].astype(np.float64)
+        t3 = tt[chs][wide, 3].astype(np.float64)
+        out["critical_path"]["wide_columns"] = {
+            "count": int(wide.sum()), "raw_mean": float(raw[chs][wide].mean()),
+            "m_mean": float(m[chs][wide].mean()),
+            "gather_us": float(((w[:, 0] - s0) / 1e3).mean()),
+            "raw_sort_us": float(((w[:, 1] - w[:, 0]) / 1e3).mean()),
+            "raw_sort_tiles_us": float(((sub[chs][wide, 1].astype(np.float64) - w[:, 0]) / 1e3).mean()),
+            "merge_us": float(((w[:, 2] - w[:, 1]) / 1e3).mean()),
+            "lkk_column_us": float(((t3 - w[:, 2]) / 1e3).mean()),
+            "weight_sort_us": float(((w[:, 3] - t3) / 1e3)[w[:, 3] > 0].mean()) if (w[:, 3] > 0).any() else None}
+    cc = np.where(wide[:, None], 0, cc)
     okc = cc[:, 2] > 0
     if okc.any():
         out["critical_path"]["cta_raw_rank_sort_cycles"] = {

@@ -1,7 +1,9 @@
 // Micro-benchmark of the one-CTA tail sweep (tail4_kernel) on synthetic level
 // structures: nlev levels of r rows x len entries, indices into earlier rows.
-// Prints ns per level. Build:
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr tailbench.cu -o tailbench
+// Prints ns per level. Build (after `make lib`; links the library's other objects):
+//   B=../../paper_2505_02977_b200/build
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr tailbench.cu \
+//     $B/capi.o $B/factor_kernels.o $B/eliminate.o $B/ordering.o $B/host_graph_host.o $B/host_mm_io.o -o tailbench
 #include <cstdio>
 #include <vector>
 #include <random>

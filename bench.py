@@ -424,11 +424,13 @@ def run_ours(args):
     if not args.no_pcg and workload != "rmat_22":
         check(lib.parac_gpu_factor_resident(ctx.handle, seed, C.byref(opts), C.byref(info)))
         b = P.make_rhs(g, "random_projected", 0)
-        P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))  # warm (builds G rows + levels)
+        # first call on a new factor also builds the solve layout (G transpose,
+        # level order, tail tables): reported as first_call_wall_ms
+        _, rep0 = P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))
         x, rep = P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))
         pcg = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
                "converged": rep.converged, "solve_ms": rep.device_ms, "wall_ms": rep.solve_seconds * 1e3,
-               "tol": 1e-8}
+               "first_call_wall_ms": rep0.solve_seconds * 1e3, "tol": 1e-8}
 
     peak, peak_src = read_peaks()
     by = algorithmic_bytes(n, E, Z, F)

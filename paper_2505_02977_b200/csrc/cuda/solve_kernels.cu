@@ -40,8 +40,6 @@ namespace {
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed => deterministic reductions
 constexpr int kRedThreads = 256;
 constexpr int kSweepThreads = 256;
-constexpr int kRowBlock = 256;  // row entries staged per warp before the serial chain
-constexpr int kFastBlock = 128;  // fast-mode batch (4 entries per lane in flight)
 
 enum Slot { kSlotA = 0, kSlotB = 1, kSlotC = 2, kSlots = 3 };
 enum Scalar { kRz0 = 0, kRz1 = 1, kPlpOk = 2, kScalars = 8 };
@@ -90,12 +88,6 @@ __device__ __forceinline__ double sum_partials(const double* partials) {
   return s;
 }
 
-__device__ __forceinline__ double block_scalar(const double* partials) {
-  __shared__ double v;
-  if (threadIdx.x == 0) v = sum_partials(partials);
-  __syncthreads();
-  return v;
-}
 
 // -------------------------------------------------------------- graph prep
 // wdeg: left-to-right sum in ascending-neighbour order (src/graph.cpp:66-75)
@@ -374,71 +366,6 @@ __global__ void diff_norm_kernel(int n, const double* a, const double* b, double
 }
 
 // ------------------------------------------------------------------- K6
-// Level-pipelined triangular sweeps. Rows are claimed in ASAP-level order
-// (forward: ascending, backward: descending). A row of level L starts once
-// every row of level L-1 (forward) / L+1 (backward) has finished: by
-// induction all its dependencies are then complete, so only one counter is
-// polled per row (lane 0, backoff by distance to the highest finished level)
-// instead of one flag per dependency -- per-dependency polling by ~9.5k warps
-// saturated L2 with requests. done[L] counts finished rows of level L; the
-// finishing row's increment follows a release fence, the waiter's relaxed
-// read is followed by an acquire fence.
-__device__ __forceinline__ int level_size(const long long* lvl_off, int L) {
-  return static_cast<int>(lvl_off[L + 1] - lvl_off[L]);
-}
-
-// Wait until level L is complete. The sleep follows the distance to the
-// finishing front, probed on level-specific counters 1, 3 and 15 levels back
-// in sweep order (step = -1 forward, +1 backward): no word is polled by every
-// waiter, and the thousands of waiters far from the front poll rarely, which
-// keeps L2 latency low for the rows on the critical path.
-__device__ __forceinline__ bool level_done(const int* done, const long long* lvl_off, int L, int lo,
-                                           int hi) {
-  return L < lo || L > hi || ld_relaxed(&done[L]) >= level_size(lvl_off, L);
-}
-
-__device__ __forceinline__ void wait_level(const int* done, const long long* lvl_off, int L, int step,
-                                           int depth) {
-  const int target = level_size(lvl_off, L);
-  if (ld_relaxed(&done[L]) >= target) return;
-  // Near the front every waiter of the next level polls done[L]; a wide next
-  // level means many pollers of one word, so the near interval grows with it.
-  const int nxt = L - step;
-  const int pollers = (nxt >= 1 && nxt <= depth) ? level_size(lvl_off, nxt) : 1;
-  const unsigned near_ns = 32u + static_cast<unsigned>(min(pollers, 4096)) / 4u;
-  // The distance probes cost dependent round trips: re-classify only every 8th
-  // poll, so a waiter near the front re-checks done[L] every ~near_ns + 1 RT.
-  unsigned ns = near_ns;
-  const unsigned long long t0 = globaltimer_ns();
-  for (int it = 0;; ++it) {
-    if ((it & 7) == 0 || ns >= 1024) {  // long sleepers re-probe every time
-      // done[0] (level 0 does not exist) is the sweep's abort word: a wait
-      // that exceeds 20 s raises it, and every waiter then bails out.
-      if (ld_relaxed(&done[0]) != 0) return;
-      if (globaltimer_ns() - t0 > 20000000000ull) {
-        atomicExch(const_cast<int*>(&done[0]), 1);
-        return;
-      }
-      // sleep ~ distance to the front (levels take ~3-30 us each): a waiter
-      // far ahead must not poll -- thousands of early waiters polling slowed
-      // the L2 for the rows on the critical path by 2-3x (measured).
-      if (level_done(done, lvl_off, L + step, 1, depth)) ns = near_ns;
-      else if (level_done(done, lvl_off, L + 2 * step, 1, depth)) ns = 1024;
-      else if (level_done(done, lvl_off, L + 4 * step, 1, depth)) ns = 3072;
-      else if (level_done(done, lvl_off, L + 8 * step, 1, depth)) ns = 8192;
-      else if (level_done(done, lvl_off, L + 16 * step, 1, depth)) ns = 16384;
-      else ns = 32768;
-    }
-    __nanosleep(ns);
-    if (ld_relaxed(&done[L]) >= target) return;
-  }
-}
-
-__device__ __forceinline__ void finish_row(int* done, int L) {
-  fence_acq_rel();  // release: this row's value before the count
-  atomicAdd(&done[L], 1);
-}
-
 // acc -= prod[0] - ... - prod[cnt-1], strictly in order, by lane 0 from the
 // warp's shared slots (loads hoisted 4 at a time; ~one DSUB latency per term).
 __device__ __forceinline__ double serial_sub(double acc, const double* buf, int cnt) {
@@ -454,206 +381,17 @@ __device__ __forceinline__ double serial_sub(double acc, const double* buf, int 
   return acc;
 }
 
-// Row j of the level order belongs to warp j mod W: a level's rows are spread
-// round-robin and consecutive narrow levels land on consecutive warps, so the
-// warp owning a tail row arrives there early and stages it while waiting.
-__device__ __forceinline__ long long first_row(long long lb, int w, int W) {
-  return lb + ((w - lb % W) % W + W) % W;
-}
 
-// Products G(.,.) * x[idx] of one block of a row into the warp's shared slots.
-// All index loads, then all value loads, then the stores: explicit register
-// staging, because global loads through generic pointers are otherwise not
-// hoisted above the shared-memory stores (measured 50 -> ~12 cycles/entry).
-// skip_zero replaces terms with x == 0 by +0.0 (see the forward sweep).
-__device__ __forceinline__ void stage_products(const int* idx, const double* g, const double* x, int cnt,
-                                               int lane, bool skip_zero, double* wbuf) {
-  constexpr int Q = kRowBlock / 32;
-  int ci[Q];
-  double xv[Q], gv[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) ci[q] = q * 32 + lane < cnt ? idx[q * 32 + lane] : 0;
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    xv[q] = q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
-    gv[q] = q * 32 + lane < cnt ? g[q * 32 + lane] : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < Q; ++q)
-    if (q * 32 + lane < cnt) wbuf[q * 32 + lane] = (skip_zero && xv[q] == 0.0) ? 0.0 : __dmul_rn(gv[q], xv[q]);
-}
 
 // Wide levels (>= kLaneRowsPerWarp rows per warp): one row per LANE, summed
 // sequentially in the reference's order (so these rows are bit-exact in both
 // modes) -- 32 independent rows per warp instead of one keeps the first,
 // widest levels (10^5 rows each at 128^3) from being latency-bound per row.
-constexpr int kLaneRowsPerWarp = 2;
 
-__device__ __forceinline__ bool lane_mode(const long long* lvl_off, int L, int W) {
-  return level_size(lvl_off, L) >= kLaneRowsPerWarp * W;
-}
 
-// Forward rows of level L, one per lane (gather form, k ascending, zero skip).
-__device__ __forceinline__ void lane_level_forward(int L, int depth, int w, int W, int lane,
-                                                   const int* order, const long long* lvl_off,
-                                                   const long long* gt_ptr, const int* gt_col,
-                                                   const double* gt_val, const double* diag,
-                                                   const int* inv, const double* rvec, double* yf,
-                                                   double* yd, int* done) {
-  const long long lb = lvl_off[L], le = lvl_off[L + 1];
-  const long long ntask = (le - lb + 31) / 32;
-  bool waited = L == 1;
-  for (long long t = w; t < ntask; t += W) {
-    if (!waited) {
-      if (lane == 0) wait_level(done, lvl_off, L - 1, -1, depth);
-      __syncwarp();
-      fence_acq_rel();
-      waited = true;
-    }
-    const long long j = lb + t * 32 + lane;
-    if (j < le) {
-      const int r = order[j];
-      double acc = rvec[inv[r]];
-      const long long b = gt_ptr[r], e = gt_ptr[r + 1];
-      for (long long q = b; q < e; ++q) {
-        const double yk = __ldcg(yf + gt_col[q]);
-        if (yk != 0.0) acc = __dsub_rn(acc, __dmul_rn(gt_val[q], yk));
-      }
-      yf[r] = acc;
-      const double dd = diag[r];
-      yd[r] = dd > 0.0 ? __ddiv_rn(acc, dd) : 0.0;
-    }
-    const unsigned ok = __ballot_sync(kFull, j < le);
-    fence_acq_rel();
-    __syncwarp();
-    if (lane == 0) atomicAdd(&done[L], __popc(ok));
-  }
-}
 
-// Backward rows (columns of G) of level L, one per lane, rows ascending.
-__device__ __forceinline__ void lane_level_backward(int L, int depth, int w, int W, int lane,
-                                                    const int* order, const long long* lvl_off,
-                                                    const long long* col_ptr, const int* rows,
-                                                    const double* vals, const double* yd, double* zb,
-                                                    int* done) {
-  const long long lb = lvl_off[L], le = lvl_off[L + 1];
-  const long long ntask = (le - lb + 31) / 32;
-  bool waited = L == depth;
-  for (long long t = w; t < ntask; t += W) {
-    if (!waited) {
-      if (lane == 0) wait_level(done, lvl_off, L + 1, +1, depth);
-      __syncwarp();
-      fence_acq_rel();
-      waited = true;
-    }
-    const long long j = lb + t * 32 + lane;
-    if (j < le) {
-      const int k = order[j];
-      double acc = yd[k];
-      const long long b = col_ptr[k], e = col_ptr[k + 1];
-      for (long long q = b; q < e; ++q) acc = __dsub_rn(acc, __dmul_rn(vals[q], __ldcg(zb + rows[q])));
-      zb[k] = acc;
-    }
-    const unsigned ok = __ballot_sync(kFull, j < le);
-    fence_acq_rel();
-    __syncwarp();
-    if (lane == 0) atomicAdd(&done[L], __popc(ok));
-  }
-}
 
-// Forward: y[r] = rhs[r] - sum_{k<r} G(r,k) y[k], k ascending, skipping
-// y[k] == 0 exactly like the column scatter (solver.cpp:45-52; a skipped term
-// is replaced by +0.0, which leaves acc bit-identical); then D^+ (:54-58) into
-// yd. rhs[r] = rvec[inv[r]] (permutation in, :40-43).
-__global__ void __launch_bounds__(kSweepThreads) sweep_forward_kernel(
-    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
-    const int* gt_col, const double* gt_val, const double* diag, const int* inv,
-    const double* rvec, double* yf, double* yd, int* done, int* frontier, int* counter,
-    unsigned long long* trace) {
-  __shared__ double buf[kSweepThreads / 32][kRowBlock];
-  const int lane = lane_id();
-  double* wbuf = buf[threadIdx.x >> 5];
-  // Static round-robin of each level's rows over the persistent warps, levels
-  // in sweep order: no claim atomics (a single claim counter capped the wide
-  // early levels at the L2 same-address atomic rate).
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  (void)counter;
-  (void)level;
-  for (int L = 1; L <= depth; ++L) {
-   if (lane_mode(lvl_off, L, W)) {
-     lane_level_forward(L, depth, w, W, lane, order, lvl_off, gt_ptr, gt_col, gt_val, diag, inv, rvec,
-                        yf, yd, done);
-     continue;
-   }
-   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
-    const int r = order[j];
-    if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
-    if (L > 1 && lane == 0) wait_level(done, lvl_off, L - 1, -1, depth);
-    __syncwarp();
-    fence_acq_rel();
-    if (trace && lane == 0) trace[3 * r] = globaltimer_ns();
-    double acc = rvec[inv[r]];
-    const long long b = gt_ptr[r], e = gt_ptr[r + 1];
-    for (long long base = b; base < e; base += kRowBlock) {
-      const int cnt = static_cast<int>(min(static_cast<long long>(kRowBlock), e - base));
-      stage_products(gt_col + base, gt_val + base, yf, cnt, lane, true, wbuf);
-      __syncwarp();
-      if (lane == 0) acc = serial_sub(acc, wbuf, cnt);
-      __syncwarp();
-    }
-    if (lane == 0) {
-      yf[r] = acc;
-      const double d = diag[r];
-      yd[r] = d > 0.0 ? __ddiv_rn(acc, d) : 0.0;
-      if (trace) trace[3 * r + 1] = globaltimer_ns();
-      finish_row(done, L);
-    }
-  }
-  }
-}
 
-// Backward: z[k] = yd[k] - sum_{r in col k, ascending} G(r,k) z[r] (solver.cpp:60-66).
-__global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
-    int n, int depth, const int* order, const int* level, const long long* lvl_off,
-    const long long* col_ptr, const int* rows, const double* vals, const double* yd, double* zb,
-    int* done, int* frontier, int* counter, unsigned long long* trace) {
-  __shared__ double buf[kSweepThreads / 32][kRowBlock];
-  const int lane = lane_id();
-  double* wbuf = buf[threadIdx.x >> 5];
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  (void)counter;
-  (void)level;
-  for (int L = depth; L >= 1; --L) {
-   if (lane_mode(lvl_off, L, W)) {
-     lane_level_backward(L, depth, w, W, lane, order, lvl_off, col_ptr, rows, vals, yd, zb, done);
-     continue;
-   }
-   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
-    const int k = order[j];
-    if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
-    if (L < depth && lane == 0) wait_level(done, lvl_off, L + 1, +1, depth);
-    __syncwarp();
-    fence_acq_rel();
-    if (trace && lane == 0) trace[3 * k] = globaltimer_ns();
-    double acc = yd[k];
-    const long long b = col_ptr[k], e = col_ptr[k + 1];
-    for (long long base = b; base < e; base += kRowBlock) {
-      const int cnt = static_cast<int>(min(static_cast<long long>(kRowBlock), e - base));
-      stage_products(rows + base, vals + base, zb, cnt, lane, false, wbuf);
-      __syncwarp();
-      if (lane == 0) acc = serial_sub(acc, wbuf, cnt);
-      __syncwarp();
-    }
-    if (lane == 0) {
-      zb[k] = acc;
-      if (trace) trace[3 * k + 1] = globaltimer_ns();
-      finish_row(done, L);
-    }
-  }
-  }
-}
 
 // ------------------------------------------------------------ K6 (fast mode)
 // PCG does not need the reference's summation order (only its iteration count
@@ -669,37 +407,6 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(
 // in sweep order is complete -- each row of level X reads a value of the
 // previous level (ASAP levels), so it cannot finish before that level did.
 
-// Segmented sort of (idx, val) within each segment by key = level-derived u64.
-// Warp per segment; <= 32 in registers, longer segments by ranking in place
-// through a scratch copy (rare: long rows of the last few hundred levels).
-__global__ void level_sort_kernel(int nseg, const long long* seg, const int* idx_in, const double* val_in,
-                                  const int* level, int desc, int maxlevel, int* idx_out, double* val_out,
-                                  int* lvl_out) {
-  const int lane = lane_id();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int sgi = gw; sgi < nseg; sgi += nw) {
-    const long long b = seg[sgi];
-    const int len = static_cast<int>(seg[sgi + 1] - b);
-    auto key_of = [&](int j) -> unsigned long long {
-      const int id = idx_in[b + j];
-      const int lv = level[id];
-      const unsigned hi = desc ? static_cast<unsigned>(maxlevel - lv) : static_cast<unsigned>(lv);
-      return (static_cast<unsigned long long>(hi) << 32) | static_cast<unsigned>(id);
-    };
-    for (int base = 0; base < len; base += 32) {
-      const int t = base + lane;
-      const unsigned long long mk = t < len ? key_of(t) : ~0ull;
-      int rank = 0;
-      for (int j = 0; j < len; ++j) rank += key_of(j) < mk;
-      if (t < len) {
-        idx_out[b + rank] = idx_in[b + t];
-        val_out[b + rank] = val_in[b + t];
-        lvl_out[b + rank] = level[idx_in[b + t]];
-      }
-    }
-  }
-}
 
 // One batch of up to 32*Q entries of a fast-mode row: index/coefficient loads
 // first (independent of the wait), then -- once the batch's latest dependency
@@ -723,92 +430,7 @@ __device__ __forceinline__ double fast_batch(const int* idx, const double* g, co
   return part;
 }
 
-// Forward, fast: y[r] = rhs[r] - sum G(r,k) y[k]; entries sorted by level[k] ascending.
-__global__ void __launch_bounds__(kSweepThreads, 6) sweep_forward_fast_kernel(
-    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* gt_ptr,
-    const int* fcol, const double* fval, const int* flvl, const int* gt_col, const double* gt_val,
-    const double* diag, const int* inv, const double* rvec, double* yf, double* yd, int* done, int* counter,
-    unsigned long long* trace) {
-  const int lane = lane_id();
-  // Static round-robin of each level's rows over the persistent warps, levels
-  // in sweep order: no claim atomics (a single claim counter capped the wide
-  // early levels at the L2 same-address atomic rate).
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  (void)counter;
-  (void)level;
-  for (int L = 1; L <= depth; ++L) {
-   if (lane_mode(lvl_off, L, W)) {
-     lane_level_forward(L, depth, w, W, lane, order, lvl_off, gt_ptr, gt_col, gt_val, diag, inv, rvec,
-                        yf, yd, done);
-     continue;
-   }
-   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
-    const int r = order[j];
-    if (trace && lane == 0) trace[3 * r + 2] = globaltimer_ns();
-    const long long b = gt_ptr[r], e = gt_ptr[r + 1];
-    double part = 0.0;
-    for (long long base = b; base < e; base += kFastBlock) {
-      const int cnt = static_cast<int>(min(static_cast<long long>(kFastBlock), e - base));
-      const int need = flvl[base + cnt - 1];  // latest dependency level in the batch
-      if (lane == 0) wait_level(done, lvl_off, need, -1, depth);
-      __syncwarp();
-      fence_acq_rel();
-      part = fast_batch<kFastBlock / 32>(fcol + base, fval + base, yf, cnt, lane, part);
-    }
-    if (trace && lane == 0) trace[3 * r] = globaltimer_ns();
-    const double sum = warp_sum(part);
-    if (lane == 0) {
-      if (trace) trace[3 * r + 1] = globaltimer_ns();
-      const double acc = rvec[inv[r]] - sum;
-      yf[r] = acc;
-      const double d = diag[r];
-      yd[r] = d > 0.0 ? acc / d : 0.0;
-      finish_row(done, L);
-    }
-  }
-  }
-}
 
-// Backward, fast: z[k] = yd[k] - sum G(r,k) z[r]; entries sorted by level[r] descending.
-__global__ void __launch_bounds__(kSweepThreads, 6) sweep_backward_fast_kernel(
-    int n, int depth, const int* order, const int* level, const long long* lvl_off, const long long* col_ptr,
-    const int* brow, const double* bval, const int* blvl, const int* rows, const double* vals,
-    const double* yd, double* zb, int* done, int* counter, unsigned long long* trace) {
-  const int lane = lane_id();
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  (void)counter;
-  (void)level;
-  for (int L = depth; L >= 1; --L) {
-   if (lane_mode(lvl_off, L, W)) {
-     lane_level_backward(L, depth, w, W, lane, order, lvl_off, col_ptr, rows, vals, yd, zb, done);
-     continue;
-   }
-   for (long long j = first_row(lvl_off[L], w, W); j < lvl_off[L + 1]; j += W) {
-    const int k = order[j];
-    if (trace && lane == 0) trace[3 * k + 2] = globaltimer_ns();
-    const long long b = col_ptr[k], e = col_ptr[k + 1];
-    double part = 0.0;
-    for (long long base = b; base < e; base += kFastBlock) {
-      const int cnt = static_cast<int>(min(static_cast<long long>(kFastBlock), e - base));
-      const int need = blvl[base + cnt - 1];
-      // levels above depth belong to the tail (already swept before this kernel)
-      if (lane == 0 && need <= depth) wait_level(done, lvl_off, need, +1, depth);
-      __syncwarp();
-      fence_acq_rel();
-      part = fast_batch<kFastBlock / 32>(brow + base, bval + base, zb, cnt, lane, part);
-    }
-    if (trace && lane == 0) trace[3 * k] = globaltimer_ns();
-    const double sum = warp_sum(part);
-    if (lane == 0) {
-      if (trace) trace[3 * k + 1] = globaltimer_ns();
-      zb[k] = yd[k] - sum;
-      finish_row(done, L);
-    }
-  }
-  }
-}
 
 // ------------------------------------------------------------ K6 (fast mode): narrow tail
 // The last levels of the factor DAG are narrow and long: at 128^3 the last 774
@@ -840,281 +462,17 @@ __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
     a += sz;
   }
 }
-constexpr int kPrefetchLevels = 3;
 constexpr int kTailThreads = 1024;
-constexpr int kTailWarps = kTailThreads / 32;
-constexpr int kTailMaxRows = 16 * 1024;  // 128 KB of shared fp64 (+ 64 KB product buffer)
-
-// tpos[order[tail_base + i]] = i; count T-part entries of forward row i and
-// the H/T split of its level-sorted entries.
-__global__ void tail_index_kernel(int nt, int tail_base, const int* order, int* tpos) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nt) tpos[order[tail_base + i]] = i;
-}
-
-__global__ void tail_count_kernel(int nt, int tail_base, int L0, const int* order, const long long* gt_ptr,
-                                  const int* ff_lvl, const long long* col_ptr, long long* hsplit,
-                                  int* fcnt, int* bcnt) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  const int r = order[tail_base + i];
-  long long lo = gt_ptr[r], hi = gt_ptr[r + 1];
-  const long long e = hi;
-  while (lo < hi) {  // first entry with level > L0 (entries sorted by level ascending)
-    const long long mid = (lo + hi) >> 1;
-    if (ff_lvl[mid] > L0) hi = mid; else lo = mid + 1;
-  }
-  hsplit[i] = lo;
-  fcnt[i] = static_cast<int>(e - lo);
-  bcnt[i] = static_cast<int>(col_ptr[r + 1] - col_ptr[r]);
-}
-
-__global__ void tail_fill_kernel(int nt, int tail_base, const int* order, const int* tpos,
-                                 const long long* gt_ptr, const long long* hsplit, const int* ff_col,
-                                 const double* ff_val, const long long* tf_ptr, int* tf_col, double* tf_val,
-                                 const long long* col_ptr, const int* fb_row, const double* fb_val,
-                                 const long long* tb_ptr, int* tb_row, double* tb_val) {
-  const int lane = lane_id();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = gw; i < nt; i += nw) {
-    const int r = order[tail_base + i];
-    const long long s = hsplit[i], e = gt_ptr[r + 1], o = tf_ptr[i];
-    for (long long q = s + lane; q < e; q += 32) {
-      tf_col[o + (q - s)] = tpos[ff_col[q]];
-      tf_val[o + (q - s)] = ff_val[q];
-    }
-    const long long cb = col_ptr[r], ce = col_ptr[r + 1], ob = tb_ptr[i];
-    for (long long q = cb + lane; q < ce; q += 32) {
-      tb_row[ob + (q - cb)] = tpos[fb_row[q]];
-      tb_val[ob + (q - cb)] = fb_val[q];
-    }
-  }
-}
-
-// Forward prologue (grid-wide, after the head sweep): s_i = rhs - G_TH y_H.
-__global__ void tail_fwd_prologue_kernel(int nt, int tail_base, const int* order, const long long* gt_ptr,
-                                         const long long* hsplit, const int* ff_col, const double* ff_val,
-                                         const int* inv, const double* rvec, const double* yf, double* ts) {
-  const int lane = lane_id();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = gw; i < nt; i += nw) {
-    const int r = order[tail_base + i];
-    const long long b = gt_ptr[r], e = hsplit[i];
-    double part = 0.0;
-    for (long long q = b + lane; q < e; q += 32) part += ff_val[q] * __ldcg(yf + ff_col[q]);
-    part = warp_sum(part);
-    if (lane == 0) ts[i] = rvec[inv[r]] - part;
-  }
-}
-
-// One tail row against the shared solution vector: sum of val * xs[idx] over
-// [b, e), lane-strided with 4 loads in flight, fixed-order warp tree.
-__device__ __forceinline__ double tail_row_sum(const int* idx, const double* val, long long b, long long e,
-                                               const double* xs, int lane) {
-  double part = 0.0;
-  long long q = b + lane;
-  for (; q + 96 < e; q += 128) {
-    const int c0 = idx[q], c1 = idx[q + 32], c2 = idx[q + 64], c3 = idx[q + 96];
-    const double v0 = val[q], v1 = val[q + 32], v2 = val[q + 64], v3 = val[q + 96];
-    part += v0 * xs[c0];
-    part += v1 * xs[c1];
-    part += v2 * xs[c2];
-    part += v3 * xs[c3];
-  }
-  for (; q < e; q += 32) part += val[q] * xs[idx[q]];
-  return warp_sum(part);
-}
-
-// ---- v2: entry-parallel, software-pipelined tail sweep. Per level, all
-// 1024 threads compute the level's products (each <= kTailPF entries, loaded
-// into registers one level AHEAD, so no global-memory latency remains on the
-// level-to-level chain), a barrier, then a warp per row sums its products
-// (fixed order: lane-strided + warp tree), a barrier. The solution of the
-// tail lives in shared memory. Levels wider than 1024*kTailPF entries fall
-// back to a strided loop (rare: the tail is the narrow part of the DAG).
-constexpr int kTailPF = 8;
-constexpr int kTailPbuf = kTailThreads * kTailPF;  // 8192 products (64 KB)
-
-struct TailLevel {
-  int lb, le;           // rows (tail index)
-  long long eb, ee;     // entries
-};
-
-template <bool FWD>
-__global__ void __launch_bounds__(kTailThreads, 1) tail_sweep_kernel(
-    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const long long* eptr,
-    const int* eidx, const double* eval, const double* init, const double* diag, double* xout, double* yd,
-    unsigned long long* ltime) {
-  extern __shared__ double tsm[];
-  double* xs = tsm;                       // [nt]
-  double* pbuf = tsm + kTailMaxRows;      // [kTailPbuf]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nt = static_cast<int>(lvl_off[depth + 1] - tail_base);
-  const int nlev = depth - L0;
-  auto level_of = [&](int t) { return FWD ? L0 + 1 + t : depth - t; };
-  auto bounds = [&](int t) {
-    TailLevel b;
-    const int L = level_of(t);
-    b.lb = static_cast<int>(lvl_off[L] - tail_base);
-    b.le = static_cast<int>(lvl_off[L + 1] - tail_base);
-    b.eb = eptr[b.lb];
-    b.ee = eptr[b.le];
-    return b;
-  };
-  // initial values: forward = rhs - G_TH y_H (prologue), backward = yd of the tail rows
-  for (int i = tid; i < nt; i += kTailThreads) {
-    if (FWD) {
-      xs[i] = init[i];
-    } else {
-      xs[i] = yd[order[tail_base + i]];
-    }
-  }
-  TailLevel nb = bounds(0);
-  int nidx[kTailPF];
-  double nval[kTailPF];
-#pragma unroll
-  for (int q = 0; q < kTailPF; ++q) {
-    const long long e = nb.eb + q * kTailThreads + tid;
-    nidx[q] = e < nb.ee ? eidx[e] : 0;
-    nval[q] = e < nb.ee ? eval[e] : 0.0;
-  }
-  __syncthreads();
-  for (int t = 0; t < nlev; ++t) {
-    const TailLevel cb = nb;
-    int cidx[kTailPF];
-    double cval[kTailPF];
-#pragma unroll
-    for (int q = 0; q < kTailPF; ++q) {
-      cidx[q] = nidx[q];
-      cval[q] = nval[q];
-    }
-    // issue the next level's loads now; they land while this level computes
-    if (t + 1 < nlev) {
-      nb = bounds(t + 1);
-#pragma unroll
-      for (int q = 0; q < kTailPF; ++q) {
-        const long long e = nb.eb + q * kTailThreads + tid;
-        nidx[q] = e < nb.ee ? eidx[e] : 0;
-        nval[q] = e < nb.ee ? eval[e] : 0.0;
-      }
-    }
-    const int cnt = static_cast<int>(cb.ee - cb.eb);
-#pragma unroll
-    for (int q = 0; q < kTailPF; ++q) {
-      const int e = q * kTailThreads + tid;
-      if (e < cnt) pbuf[e] = cval[q] * xs[cidx[q]];
-    }
-    const bool wide = cnt > kTailPbuf;
-    __syncthreads();
-    for (int i = cb.lb + warp; i < cb.le; i += kTailThreads / 32) {
-      const long long rb = eptr[i] - cb.eb, re = eptr[i + 1] - cb.eb;
-      double part = 0.0;
-      for (long long q = rb + lane; q < re; q += 32)
-        part += q < kTailPbuf ? pbuf[q] : eval[cb.eb + q] * xs[eidx[cb.eb + q]];
-      part = warp_sum(part);
-      if (lane == 0) {
-        const double acc = xs[i] - part;
-        xs[i] = acc;
-        const int r = order[tail_base + i];
-        xout[r] = acc;
-        if (FWD) {
-          const double d = diag[r];
-          yd[r] = d > 0.0 ? acc / d : 0.0;
-        }
-      }
-    }
-    (void)wide;
-    __syncthreads();
-    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
-  }
-}
-
-__global__ void __launch_bounds__(kTailThreads, 1) tail_forward_kernel(
-    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const double* ts,
-    const long long* tf_ptr, const int* tf_col, const double* tf_val, const double* diag, double* yf,
-    double* yd, unsigned long long* ltime) {
-  extern __shared__ double ys[];
-  const int nt = static_cast<int>(lvl_off[depth + 1] - tail_base);
-  auto prefetch_level = [&](int Lp) {
-    if (Lp > depth) return;
-    const long long lb = lvl_off[Lp] - tail_base, le = lvl_off[Lp + 1] - tail_base;
-    const long long ea = tf_ptr[lb], ez = tf_ptr[le];
-    prefetch_l2(tf_col + ea, (ez - ea) * 4);
-    prefetch_l2(tf_val + ea, (ez - ea) * 8);
-  };
-  if (threadIdx.x == kTailThreads - 32)
-    for (int Lp = L0 + 1; Lp <= L0 + 2 * kPrefetchLevels; ++Lp) prefetch_level(Lp);
-  for (int i = threadIdx.x; i < nt; i += kTailThreads) ys[i] = ts[i];
-  __syncthreads();
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  for (int L = L0 + 1; L <= depth; ++L) {
-    if (threadIdx.x == kTailThreads - 32) prefetch_level(L + 2 * kPrefetchLevels);
-    const int lb = static_cast<int>(lvl_off[L] - tail_base), le = static_cast<int>(lvl_off[L + 1] - tail_base);
-    for (int i = lb + warp; i < le; i += kTailWarps) {
-      const double sum = tail_row_sum(tf_col, tf_val, tf_ptr[i], tf_ptr[i + 1], ys, lane);
-      if (lane == 0) {
-        const double acc = ys[i] - sum;
-        ys[i] = acc;
-        const int r = order[tail_base + i];
-        yf[r] = acc;
-        const double d = diag[r];
-        yd[r] = d > 0.0 ? acc / d : 0.0;
-      }
-    }
-    __syncthreads();
-    if (ltime && threadIdx.x == 0) ltime[L - L0 - 1] = globaltimer_ns();
-  }
-}
-
-// Backward tail: z_k = yd_k - sum_{r in col k} G(r,k) z_r, levels descending.
-__global__ void __launch_bounds__(kTailThreads, 1) tail_backward_kernel(
-    int L0, int depth, int tail_base, const long long* lvl_off, const int* order, const long long* tb_ptr,
-    const int* tb_row, const double* tb_val, const double* yd, double* zb, unsigned long long* ltime) {
-  extern __shared__ double zs[];
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  auto prefetch_level = [&](int Lp) {
-    if (Lp <= L0) return;
-    const long long lb = lvl_off[Lp] - tail_base, le = lvl_off[Lp + 1] - tail_base;
-    const long long ea = tb_ptr[lb], ez = tb_ptr[le];
-    prefetch_l2(tb_row + ea, (ez - ea) * 4);
-    prefetch_l2(tb_val + ea, (ez - ea) * 8);
-  };
-  if (threadIdx.x == kTailThreads - 32)
-    for (int Lp = depth; Lp > depth - 2 * kPrefetchLevels; --Lp) prefetch_level(Lp);
-  for (int L = depth; L > L0; --L) {
-    if (threadIdx.x == kTailThreads - 32) prefetch_level(L - 2 * kPrefetchLevels);
-    const int lb = static_cast<int>(lvl_off[L] - tail_base), le = static_cast<int>(lvl_off[L + 1] - tail_base);
-    for (int i = lb + warp; i < le; i += kTailWarps) {
-      const double sum = tail_row_sum(tb_row, tb_val, tb_ptr[i], tb_ptr[i + 1], zs, lane);
-      if (lane == 0) {
-        const int k = order[tail_base + i];
-        const double acc = yd[k] - sum;
-        zs[i] = acc;
-        zb[k] = acc;
-      }
-    }
-    __syncthreads();
-    if (ltime && threadIdx.x == 0) ltime[depth - L] = globaltimer_ns();
-  }
-}
 
 // ------------------------------------------------------------ K6: cluster sweeps
-// One thread-block cluster (16 CTAs x 1024 threads = 512 warps, one CTA per SM)
-// sweeps the head levels level-synchronously: every row of level L is computed,
-// then ONE hardware cluster barrier (barrier.cluster arrive.release /
-// wait.acquire, measured 235 ns on B200 vs ~1.2 us for a grid-wide sync and
-// 0.5-1 us per global flag hand-off) publishes the level. At the barrier all of
-// a row's dependencies are complete, so rows read plain CSR data -- no
-// per-level counters, no polling, no level-sorted copies. Solution values are
-// written with plain stores and read with ld.global.cg (L2), so no stale L1
-// line can be observed after the acquire.
-//   EXACT: per-row sums in the reference's order (solver.cpp:44-66), lane 0
-//          serial over register-staged products -> bit-identical to
-//          apply_preconditioner; FAST: per-lane strided partials + fixed warp
-//          tree (deterministic). Wide levels run one row per lane, serial, in
-//          the reference's order in both modes.
+// One thread-block cluster sweeps levels level-synchronously: every row of
+// level L is computed, then ONE hardware cluster barrier (barrier.cluster
+// arrive.release / wait.acquire, measured 235 ns on B200 vs ~1.2 us for a
+// grid-wide sync) publishes the level. Solution values are written with plain
+// stores and read with ld.global.cg (L2), so no stale L1 line can be observed
+// after the acquire. Exact mode (cluster_forward/backward_kernel<true>): per-row
+// sums in the reference's order (solver.cpp:44-66), lane 0 serial over
+// register-staged products -> bit-identical to apply_preconditioner.
 constexpr int kCThreads = 1024;
 constexpr int kCWarps = kCThreads / 32;
 constexpr int kCStage = 128;  // exact mode: products staged per warp before the serial chain
@@ -1295,107 +653,6 @@ __device__ __forceinline__ void finish_row(int j, double s, const int* order, co
   }
 }
 
-template <bool FWD>
-__global__ void __launch_bounds__(kCThreads, 1) cluster_sweep_fast_kernel(
-    int Lfirst, int nlev, const int* chunk, const int* chunk_base, const long long* lptr, const int* lidx,
-    const double* lval, const int* order, const double* rhs_pos, const int* inv, const double* rvec,
-    const double* diag, double* x, double* yd, int nt, int tail_base, const long long* gt_ptr,
-    const long long* hsplit, const int* ff_col, const double* ff_val, double* ts, unsigned long long* ltime) {
-  extern __shared__ double pbuf_all[];
-  const int lane = lane_id(), wl = threadIdx.x >> 5;
-  const int W = static_cast<int>(cluster_nctas()) * kCWarps;
-  const int w = static_cast<int>(cluster_rank()) * kCWarps + wl;
-  double* pbuf = pbuf_all + wl * kChunkCap;
-  const bool pf_thread = threadIdx.x == kCThreads - 32;  // lane 0 of the last warp
-  const int nc = static_cast<int>(cluster_nctas()), cr = static_cast<int>(cluster_rank());
-  auto prefetch_level = [&](int tt) {
-    if (tt >= nlev) return;
-    const int Lp = FWD ? Lfirst + tt : Lfirst - tt;
-    const long long ja = chunk[chunk_base[Lp]], jz = chunk[chunk_base[Lp + 1] - 1];
-    const long long ea = lptr[ja], ez = lptr[jz];
-    const long long s0 = ea + (ez - ea) * cr / nc, s1 = ea + (ez - ea) * (cr + 1) / nc;
-    prefetch_l2(lidx + s0, (s1 - s0) * 4);
-    prefetch_l2(lval + s0, (s1 - s0) * 8);
-    const long long r0 = ja + (jz - ja) * cr / nc, r1 = ja + (jz - ja) * (cr + 1) / nc;
-    prefetch_l2(lptr + r0, (r1 - r0 + 1) * 8);
-    prefetch_l2(order + r0, (r1 - r0) * 4);
-  };
-  if (pf_thread)
-    for (int tt = 0; tt < kPrefetchLevels; ++tt) prefetch_level(tt);
-  for (int t = 0; t < nlev; ++t) {
-    const int L = FWD ? Lfirst + t : Lfirst - t;
-    if (pf_thread) prefetch_level(t + kPrefetchLevels);
-    const int cb = chunk_base[L], ce = chunk_base[L + 1] - 1;  // chunks [cb, ce), starts chunk[cb..ce]
-    for (int c = cb + w; c < ce; c += W) {
-      const int jb = chunk[c], je = chunk[c + 1];
-      if (jb >= je) continue;
-      const long long eb = lptr[jb], ee = lptr[je];
-      if (ee - eb <= kChunkCap) {
-        const int cnt = static_cast<int>(ee - eb);
-        for (int base = 0; base < cnt; base += 256) {
-          int ci[8];
-          double gv[8], xv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int e = base + q * 32 + lane;
-            ci[q] = e < cnt ? lidx[eb + e] : 0;
-            gv[q] = e < cnt ? lval[eb + e] : 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) xv[q] = base + q * 32 + lane < cnt ? __ldcg(x + ci[q]) : 0.0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (base + q * 32 + lane < cnt) pbuf[base + q * 32 + lane] = gv[q] * xv[q];
-        }
-        __syncwarp();
-        for (int j0 = jb; j0 < je; j0 += 32) {
-          const int j = j0 + lane;
-          int b = 0, e = 0;
-          if (j < je) {
-            b = static_cast<int>(lptr[j] - eb);
-            e = static_cast<int>(lptr[j + 1] - eb);
-            if (e - b <= kShortRow) {
-              double s = 0.0;
-              for (int q = b; q < e; ++q) s += pbuf[q];
-              finish_row<FWD>(j, s, order, rhs_pos, inv, rvec, diag, x, yd);
-            }
-          }
-          unsigned longs = __ballot_sync(kFull, j < je && e - b > kShortRow);
-          while (longs) {
-            const int src = __ffs(longs) - 1;
-            longs &= longs - 1;
-            const int lb2 = __shfl_sync(kFull, b, src), le2 = __shfl_sync(kFull, e, src);
-            double part = 0.0;
-            for (int q = lb2 + lane; q < le2; q += 32) part += pbuf[q];
-            part = warp_sum(part);
-            if (lane == 0) finish_row<FWD>(j0 + src, part, order, rhs_pos, inv, rvec, diag, x, yd);
-          }
-        }
-        __syncwarp();
-      } else {
-        for (int j = jb; j < je; ++j) {
-          double part = 0.0;
-          const long long b = lptr[j], e = lptr[j + 1];
-          for (long long q = b + lane; q < e; q += 32) part += lval[q] * __ldcg(x + lidx[q]);
-          part = warp_sum(part);
-          if (lane == 0) finish_row<FWD>(j, part, order, rhs_pos, inv, rvec, diag, x, yd);
-        }
-      }
-    }
-    cluster_barrier();
-    if (ltime && w == 0 && lane == 0) ltime[t] = globaltimer_ns();
-  }
-  if constexpr (FWD) {  // G_TH part of the tail rows (fast mode with a tail)
-    for (int i = w; i < nt; i += W) {
-      const int r = order[tail_base + i];
-      const long long b = gt_ptr[r], e = hsplit[i];
-      double part = 0.0;
-      for (long long q = b + lane; q < e; q += 32) part += ff_val[q] * __ldcg(x + ff_col[q]);
-      part = warp_sum(part);
-      if (lane == 0) ts[i] = rvec[inv[r]] - part;
-    }
-  }
-}
 
 // ---- v3 head sweep: level-order index space + software pipelining.
 // Vectors are indexed by level-order position j (rows of a level are
@@ -1847,98 +1104,7 @@ __global__ void gather_z_l_dot_kernel(int n, const int* v2l, const double* zl, c
 // all 1024 threads. FWD: x = y (tail rows, init = rhs - G_TH y_H);
 // BWD: x = z (init = y * D^+).
 constexpr int kT3Rows = 8192;
-constexpr int kT3PF = 8;
-constexpr int kT3Pbuf = kTailThreads * kT3PF;
-constexpr std::size_t kT3Smem = (static_cast<std::size_t>(kT3Rows) + kT3Pbuf) * 8 +
-                                (2 * static_cast<std::size_t>(kT3Rows) + 2) * 4;
 
-template <bool FWD>
-__global__ void __launch_bounds__(kTailThreads, 1) tail3_kernel(
-    int nt, int nlev, int tail_base, const int* lvl3, const int* ep, const int* eidx, const double* eval,
-    const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
-  extern __shared__ double t3[];
-  double* xs = t3;                                            // [kT3Rows]
-  double* pbuf = t3 + kT3Rows;                                // [kT3Pbuf]
-  int* eps = reinterpret_cast<int*>(pbuf + kT3Pbuf);         // [kT3Rows + 1]
-  int* lvs = eps + kT3Rows + 1;                               // [kT3Rows + 1]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i <= nt; i += kTailThreads) eps[i] = ep[i];
-  for (int i = tid; i <= nlev; i += kTailThreads) lvs[i] = lvl3[i];
-  for (int i = tid; i < nt; i += kTailThreads)
-    xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];  // BWD: yd = y D^+
-  __syncthreads();
-  auto qlev = [&](int t) { return FWD ? t : nlev - 1 - t; };
-  auto lcount = [&](int t) { const int q = qlev(t); return eps[lvs[q + 1]] - eps[lvs[q]]; };
-  // Work is proportional to the level: threads past the level's entry count
-  // and warps past its row count skip straight to the barrier (the narrow
-  // levels would otherwise be issue-bound on 32 warps of predicated code).
-  int nidx[kT3PF];
-  double nval[kT3PF];
-  auto prefetch = [&](int t) {
-    const int q = qlev(t);
-    const int eb = eps[lvs[q]], ee = eps[lvs[q + 1]];
-    if (eb + tid < ee) {
-#pragma unroll
-      for (int k = 0; k < kT3PF; ++k) {
-        const int e = eb + k * kTailThreads + tid;
-        nidx[k] = e < ee ? eidx[e] : 0;
-        nval[k] = e < ee ? eval[e] : 0.0;
-      }
-    }
-  };
-  auto prefetch_l2_level = [&](int t) {
-    if (t >= nlev) return;
-    const int q = qlev(t);
-    const int eb = eps[lvs[q]], ee = eps[lvs[q + 1]];
-    prefetch_l2(eidx + eb, static_cast<long long>(ee - eb) * 4);
-    prefetch_l2(eval + eb, static_cast<long long>(ee - eb) * 8);
-  };
-  if (tid == 32)
-    for (int t = 1; t < 6; ++t) prefetch_l2_level(t);
-  if (nlev > 0) prefetch(0);
-  for (int t = 0; t < nlev; ++t) {
-    const int q = qlev(t);
-    const int lb = lvs[q], le = lvs[q + 1];
-    const int eb = eps[lb], cnt = eps[le] - eb;
-    long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    if (ltime && tid == 0) c0 = clock64();
-    if (tid == 32) prefetch_l2_level(t + 6);
-    if (tid < cnt) {
-#pragma unroll
-      for (int k = 0; k < kT3PF; ++k) {
-        const int e = k * kTailThreads + tid;
-        if (e < cnt) pbuf[e] = nval[k] * xs[nidx[k]];
-      }
-    }
-    if (ltime && tid == 0) c1 = clock64();
-    if (t + 1 < nlev && tid < lcount(t + 1)) prefetch(t + 1);
-    __syncthreads();
-    if (ltime && tid == 0) c2 = clock64();
-    for (int i = lb + warp; i < le; i += kTailThreads / 32) {
-      const int rb = eps[i] - eb, re = eps[i + 1] - eb;
-      double part = 0.0;
-      for (int e = rb + lane; e < re; e += 32)
-        part += e < kT3Pbuf ? pbuf[e] : eval[eb + e] * xs[eidx[eb + e]];
-      part = warp_sum(part);
-      if (lane == 0) {
-        const double acc = xs[i] - part;
-        xs[i] = acc;
-        x_l[tail_base + i] = acc;
-      }
-    }
-    if (ltime && tid == 0) c3 = clock64();
-    __syncthreads();
-    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
-    if (FWD && ltime && tid == 0) {
-      // diagnostics: cycles of (products, prefetch+sync, rows, sync) of this level
-      unsigned long long* dbg = ltime + 4 * (nlev + 2) + 4 * static_cast<long long>(t);
-      dbg[0] = c1 - c0;
-      dbg[1] = c2 - c1;
-      dbg[2] = c3 - c2;
-      dbg[3] = clock64() - c3;
-    }
-  }
-}
 
 // ---- v4 tail: every level has <= 32 rows (tail width <= 32), so the 32
 // warps split each level's rows into equal (row, slice) pieces: warp w takes
@@ -2181,31 +1347,6 @@ __global__ void lvl_copy_kernel(int n, const int* order, const long long* src_pt
   }
 }
 
-// chunk[chunk_base[L] + c] = first row j of level L whose weighted prefix
-// (entries + rows from the level start) reaches c * target[L].
-__global__ void chunk_fill_kernel(int depth, const long long* lvl_off, const long long* lptr,
-                                  const int* chunk_base, const long long* target, int* chunk) {
-  const int L = blockIdx.x + 1;
-  if (L > depth) return;
-  const long long lb = lvl_off[L], le = lvl_off[L + 1];
-  const int nch = chunk_base[L + 1] - chunk_base[L] - 1;
-  const long long t = target[L];
-  for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
-    long long j;
-    if (c == nch) {
-      j = le;
-    } else {
-      const long long goal = static_cast<long long>(c) * t;
-      long long lo = lb, hi = le;
-      while (lo < hi) {  // first j with (lptr[j] - lptr[lb]) + (j - lb) >= goal
-        const long long mid = (lo + hi) >> 1;
-        if ((lptr[mid] - lptr[lb]) + (mid - lb) >= goal) hi = mid; else lo = mid + 1;
-      }
-      j = lo;
-    }
-    chunk[chunk_base[L] + c] = static_cast<int>(j);
-  }
-}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_cluster_t(void (*kernel)(KArgs...), int csize, int threads, std::size_t smem, cudaStream_t st,
@@ -2272,46 +1413,27 @@ int pick_cluster(void (*kernel)(KArgs...), std::size_t smem = 0, int threads = k
 }
 
 struct ClusterSizes {
-  int fwd_fast, fwd_exact, bwd_fast, bwd_exact, sweep_f, sweep_b;
+  int fwd_exact, bwd_exact;
 };
-constexpr std::size_t kChunkSmem = static_cast<std::size_t>(kCWarps) * kChunkCap * sizeof(double);
 ClusterSizes cluster_sizes(int device) {
   static ClusterSizes cached[64] = {};
-  if (device >= 0 && device < 64 && cached[device].fwd_fast) return cached[device];
-  ClusterSizes c{pick_cluster(cluster_forward_kernel<false>), pick_cluster(cluster_forward_kernel<true>),
-                 pick_cluster(cluster_backward_kernel<false>), pick_cluster(cluster_backward_kernel<true>),
-                 pick_cluster(cluster_sweep_fast_kernel<true>, kChunkSmem),
-                 pick_cluster(cluster_sweep_fast_kernel<false>, kChunkSmem)};
+  if (device >= 0 && device < 64 && cached[device].fwd_exact) return cached[device];
+  ClusterSizes c{pick_cluster(cluster_forward_kernel<true>), pick_cluster(cluster_backward_kernel<true>)};
   if (device >= 0 && device < 64) cached[device] = c;
   return c;
 }
 
-// Persistent sweep grids: exactly the co-resident capacity of each kernel.
-// The static row assignment needs every CTA resident (a non-resident CTA's
-// rows would never run while resident ones wait on their level), so each
-// kernel is sized from its own occupancy (register/smem use differ).
-template <typename K>
-int occupancy_grid(K kernel, int device) {
+// Grid of the sync-free level pass (uploaded factors): exactly its co-resident
+// capacity, so every CTA that a waiting row depends on is resident.
+int sweep_grid(int device) {
+  static int cached[64] = {};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSweepThreads, 0);
-  return std::max(1, per_sm) * sm_count(device);
-}
-
-struct SweepGrids {
-  int fwd, bwd, fwd_fast, bwd_fast, level;
-};
-
-SweepGrids sweep_grids(int device) {
-  static SweepGrids cached[64] = {};
-  if (device >= 0 && device < 64 && cached[device].fwd) return cached[device];
-  SweepGrids g{occupancy_grid(sweep_forward_kernel, device), occupancy_grid(sweep_backward_kernel, device),
-               occupancy_grid(sweep_forward_fast_kernel, device),
-               occupancy_grid(sweep_backward_fast_kernel, device), occupancy_grid(level_kernel, device)};
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_kernel, kSweepThreads, 0);
+  const int g = std::max(1, per_sm) * sm_count(device);
   if (device >= 0 && device < 64) cached[device] = g;
   return g;
 }
-
-int sweep_grid(int device) { return sweep_grids(device).level; }
 
 // ---------------------------------------------------------------- host side
 void ensure_vectors(SolveState& s, int n) {
@@ -2320,8 +1442,7 @@ void ensure_vectors(SolveState& s, int n) {
   dalloc(s.x, c); dalloc(s.r, c); dalloc(s.p, c); dalloc(s.lp, c); dalloc(s.z, c);
   dalloc(s.best, c); dalloc(s.yf, c); dalloc(s.yd, c); dalloc(s.zb, c); dalloc(s.rhs, c);
   dalloc(s.wdeg, c); dalloc(s.inv, c); dalloc(s.level, c); dalloc(s.order, c);
-  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2); dalloc(s.tpos, c); dalloc(s.done, 2 * c + 8);
-  if (std::getenv("PARAC_SWEEP_TRACE")) dalloc(s.trace, 6 * c);  // diagnostics only
+  dalloc(s.flags, c); dalloc(s.tmp_int, c + 2);
   dalloc(s.partials, static_cast<std::size_t>(kRedBlocks) * kSlots);
   dalloc(s.scalars, kScalars);
   dalloc(s.counters, 16);
@@ -2368,122 +1489,15 @@ int component_count(const SolveInputs& in) {
   return h;
 }
 
-// Choose the narrow tail (levels > L0 with width <= PARAC_TAIL_WIDTH, default
-// 64, at most kTailMaxRows rows) and build its index-remapped entry lists.
-void build_tail(const SolveInputs& in, SolveState& s, int sms) {
-  const int n = in.f_n, depth = s.depth;
-  cudaStream_t st = in.stream;
-  s.tail_L0 = depth;
-  s.tail_n = 0;
-  s.tail_base = n;
-  const char* env = std::getenv("PARAC_TAIL_WIDTH");
-  const int wt = env ? std::atoi(env) : 64;
-  if (n == 0 || depth < 2 || wt <= 0) return;
-  std::vector<long long> off(static_cast<std::size_t>(depth) + 2);
-  check(cudaMemcpyAsync(off.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaStreamSynchronize(st), "tail sync");
-  int L0 = depth;
-  while (L0 >= 1 && off[L0 + 1] - off[L0] <= wt) --L0;
-  while (L0 < depth && off[depth + 1] - off[L0 + 1] > kTailMaxRows) ++L0;
-  if (L0 >= depth) return;
-  const int base = static_cast<int>(off[L0 + 1]);
-  const int nt = static_cast<int>(off[depth + 1]) - base;
-  if (s.cap_tail < static_cast<std::size_t>(nt) + 1) {
-    dalloc(s.tf_ptr, static_cast<std::size_t>(nt) + 1);
-    dalloc(s.tb_ptr, static_cast<std::size_t>(nt) + 1);
-    dalloc(s.hsplit, static_cast<std::size_t>(nt));
-    dalloc(s.tail_s, static_cast<std::size_t>(nt));
-    dalloc(s.tail_cnt, 2 * (static_cast<std::size_t>(nt) + 1));
-    s.cap_tail = static_cast<std::size_t>(nt) + 1;
-  }
-  int* fcnt = s.tail_cnt;
-  int* bcnt = s.tail_cnt + (nt + 1);
-  const int tb = (nt + 255) / 256;
-  tail_index_kernel<<<tb, 256, 0, st>>>(nt, base, s.order, s.tpos);
-  tail_count_kernel<<<tb, 256, 0, st>>>(nt, base, L0, s.order, s.gt_ptr, s.ff_lvl, in.col_ptr, s.hsplit,
-                                        fcnt, bcnt);
-  note_launches(2);
-  check(launch_scan(fcnt, nt, s.tf_ptr, s.tiles, st), "scan");
-  check(launch_scan(bcnt, nt, s.tb_ptr, s.tiles, st), "scan");
-  long long tot[2] = {0, 0};
-  check(cudaMemcpyAsync(&tot[0], s.tf_ptr + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaMemcpyAsync(&tot[1], s.tb_ptr + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaStreamSynchronize(st), "tail sync");
-  const std::size_t need = static_cast<std::size_t>(std::max<long long>(std::max(tot[0], tot[1]), 1));
-  if (s.cap_tail_nnz < need) {
-    dalloc(s.tf_col, need);
-    dalloc(s.tf_val, need);
-    dalloc(s.tb_row, need);
-    dalloc(s.tb_val, need);
-    s.cap_tail_nnz = need;
-  }
-  tail_fill_kernel<<<sms * 8, 256, 0, st>>>(nt, base, s.order, s.tpos, s.gt_ptr, s.hsplit, s.ff_col, s.ff_val,
-                                            s.tf_ptr, s.tf_col, s.tf_val, in.col_ptr, s.fb_row, s.fb_val,
-                                            s.tb_ptr, s.tb_row, s.tb_val);
-  note_launches(1);
-  check(cudaGetLastError(), "tail build");
-  static bool attr = false;
-  if (!attr) {
-    check(cudaFuncSetAttribute(tail_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kTailMaxRows * 8), "attr");
-    check(cudaFuncSetAttribute(tail_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kTailMaxRows * 8), "attr");
-    check(cudaFuncSetAttribute(tail_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (kTailMaxRows + kTailPbuf) * 8), "attr");
-    check(cudaFuncSetAttribute(tail_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (kTailMaxRows + kTailPbuf) * 8), "attr");
-    attr = true;
-  }
-  s.tail_L0 = L0;
-  s.tail_n = nt;
-  s.tail_base = base;
-}
 
 __global__ void gather_ll_kernel(int cnt, const long long* idx, const long long* src, long long* dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) dst[i] = src[idx[i]];
 }
 
-// Chunk table of one direction for a cluster of W warps (see cluster_sweep_fast_kernel).
-void build_chunks(const SolveInputs& in, SolveState& s, const long long* lptr, int W, int*& chunk,
-                  int*& cbase, std::size_t& cap_chunk) {
-  const int depth = s.depth;
-  cudaStream_t st = in.stream;
-  // entry offsets at the level boundaries
-  long long* bnd = s.lvl_target;  // scratch (depth + 2)
-  gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, lptr, bnd);
-  note_launches(1);
-  std::vector<long long> eoff(depth + 2), roff(depth + 2);
-  check(cudaMemcpyAsync(eoff.data(), bnd, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaMemcpyAsync(roff.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaStreamSynchronize(st), "chunk sync");
-  std::vector<int> base(depth + 2, 0);
-  std::vector<long long> target(depth + 2, 1);
-  long long total = 0;
-  for (int L = 1; L <= depth; ++L) {
-    const long long tot = (eoff[L + 1] - eoff[L]) + (roff[L + 1] - roff[L]);
-    long long t = std::max<long long>(1, (tot + W - 1) / W);
-    t = std::min<long long>(t, kChunkCap / 2);
-    const long long nch = std::max<long long>(1, (tot + t - 1) / t);
-    target[L] = t;
-    base[L] = static_cast<int>(total);
-    total += nch + 1;
-  }
-  base[depth + 1] = static_cast<int>(total);
-  if (cap_chunk < static_cast<std::size_t>(total)) {
-    dalloc(chunk, static_cast<std::size_t>(total));
-    cap_chunk = static_cast<std::size_t>(total);
-  }
-  if (!cbase) dalloc(cbase, s.cap_levels);  // cap_levels = n + 2 >= depth + 2
-  check(cudaMemcpyAsync(cbase, base.data(), sizeof(int) * (depth + 2), cudaMemcpyHostToDevice, st), "h2d");
-  check(cudaMemcpyAsync(s.lvl_target, target.data(), sizeof(long long) * (depth + 2), cudaMemcpyHostToDevice, st), "h2d");
-  chunk_fill_kernel<<<depth, 256, 0, st>>>(depth, s.lvl_off, lptr, cbase, s.lvl_target, chunk);
-  note_launches(1);
-  check(cudaStreamSynchronize(st), "chunk sync");  // host vectors go out of scope
-}
 
 // Level-ordered copies of G's rows and columns + chunk tables (fast mode).
-void build_level_layout(const SolveInputs& in, SolveState& s, int sms, bool chunks) {
+void build_level_layout(const SolveInputs& in, SolveState& s, int sms) {
   const int n = in.f_n, depth = s.depth;
   const long long Z = in.f_nnz;
   cudaStream_t st = in.stream;
@@ -2497,8 +1511,6 @@ void build_level_layout(const SolveInputs& in, SolveState& s, int sms, bool chun
     dalloc(s.lf_ptr, static_cast<std::size_t>(n) + 1);
     dalloc(s.lb_ptr, static_cast<std::size_t>(n) + 1);
     dalloc(s.lvl_target, static_cast<std::size_t>(n) + 2);
-    dfree(s.f_cbase);
-    dfree(s.b_cbase);
     s.cap_levels = static_cast<std::size_t>(n) + 2;
   }
   int* alen = s.tmp_int;
@@ -2512,11 +1524,6 @@ void build_level_layout(const SolveInputs& in, SolveState& s, int sms, bool chun
   lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, s.gt_ptr, s.gt_col, s.gt_val, s.lf_ptr, s.lf_idx, s.lf_val);
   lvl_copy_kernel<<<sms * 8, 256, 0, st>>>(n, s.order, in.col_ptr, in.rows, in.vals, s.lb_ptr, s.lb_idx, s.lb_val);
   note_launches(2);
-  if (chunks) {
-    const ClusterSizes cs = cluster_sizes(in.device);
-    build_chunks(in, s, s.lf_ptr, cs.sweep_f * kCWarps, s.f_chunk, s.f_cbase, s.cap_fchunk);
-    build_chunks(in, s, s.lb_ptr, cs.sweep_b * kCWarps, s.b_chunk, s.b_cbase, s.cap_bchunk);
-  }
   dfree(blen);
   check(cudaGetLastError(), "level layout");
 }
@@ -2682,8 +1689,6 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   note_launches(4);
   static bool attr = false;
   if (!attr) {
-    check(cudaFuncSetAttribute(tail3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
-    check(cudaFuncSetAttribute(tail3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT3Smem)), "attr");
     check(cudaFuncSetAttribute(tail4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
     check(cudaFuncSetAttribute(tail4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
     attr = true;
@@ -2707,12 +1712,6 @@ void prepare_factor(const SolveInputs& in) {
     const std::size_t cz = static_cast<std::size_t>(std::max<long long>(Z, 1));
     dalloc(s.gt_col, cz);
     dalloc(s.gt_val, cz);
-    dalloc(s.ff_col, cz);
-    dalloc(s.ff_val, cz);
-    dalloc(s.ff_lvl, cz);
-    dalloc(s.fb_row, cz);
-    dalloc(s.fb_val, cz);
-    dalloc(s.fb_lvl, cz);
     s.cap_z = static_cast<std::size_t>(std::max<long long>(Z, 1));
   }
   inverse_perm_kernel<<<blocks, 256, 0, st>>>(n, in.perm, s.inv);
@@ -2749,21 +1748,8 @@ void prepare_factor(const SolveInputs& in) {
   check(cudaMemcpyAsync(&depth, s.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "prepare_factor");
   s.depth = depth;
-  static const bool v3 = !std::getenv("PARAC_SWEEP") || std::string(std::getenv("PARAC_SWEEP")) == "v3";
-  if (v3) {
-    build_level_layout(in, s, sms, false);
-    build_fast_v3(in, s, sms);
-  } else {
-    // fast-mode copies: G rows sorted by level[k] ascending, G columns by level[r] descending
-    level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val, s.level, 0, depth + 1,
-                                               s.ff_col, s.ff_val, s.ff_lvl);
-    level_sort_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.level, 1, depth + 1,
-                                               s.fb_row, s.fb_val, s.fb_lvl);
-    note_launches(2);
-    check(cudaGetLastError(), "level sort");
-    build_tail(in, s, sms);
-    build_level_layout(in, s, sms, true);
-  }
+  build_level_layout(in, s, sms);
+  build_fast_v3(in, s, sms);
   if (std::getenv("PARAC_SWEEP_PROFILE")) {
     const std::size_t need = 16 * (static_cast<std::size_t>(s.depth) + 2);
     if (s.cap_ltime < need) {
@@ -2786,11 +1772,10 @@ struct Solver {
   SolveState& s;
   cudaStream_t st;
   int n;
-  SweepGrids grids;
   std::vector<double> hp = std::vector<double>(kRedBlocks);
 
   explicit Solver(const SolveInputs& i)
-      : in(i), s(*i.state), st(i.stream), n(i.n), grids(sweep_grids(i.device)) {}
+      : in(i), s(*i.state), st(i.stream), n(i.n) {}
 
   double* part(int slot) const { return s.partials + slot * kRedBlocks; }
 
@@ -2804,13 +1789,7 @@ struct Solver {
   // z (label space) = M^-1 r (label space); partial r.z into slot.
   void precond(const double* r, double* z, int slot, bool exact = true) {
     const int D = s.depth;
-    int* done_f = s.done;
-    int* done_b = s.done + (D + 2);
-    check(cudaMemsetAsync(s.done, 0, sizeof(int) * 2 * (D + 2), st), "memset");
-    check(cudaMemsetAsync(s.counters + 2, 0, sizeof(int) * 4, st), "memset");
-    static const std::string sweep = std::getenv("PARAC_SWEEP") ? std::getenv("PARAC_SWEEP") : "v3";
-    const bool legacy = sweep == "legacy";
-    if (!exact && sweep == "v3") {
+    if (!exact) {
       const int H = s.t3_L0, nt = s.t3_nt;
       const int Lw = std::min(s.wide_L, H);
       unsigned long long* lt = s.ltime;
@@ -2873,112 +1852,16 @@ struct Solver {
       note_launches(2);
       return;
     }
-    if (!exact && sweep == "chunk") {
-      const ClusterSizes cs = cluster_sizes(in.device);
-      const int H = s.tail_L0;
-      const int nt = s.tail_n;
-      check(launch_cluster(cluster_sweep_fast_kernel<true>, cs.sweep_f, kChunkSmem, st, 1, H, s.f_chunk,
-                           s.f_cbase, s.lf_ptr, s.lf_idx, s.lf_val, s.order, nullptr, s.inv, r, in.diag, s.yf,
-                           s.yd, nt, s.tail_base, s.gt_ptr, s.hsplit, s.ff_col, s.ff_val, s.tail_s,
-                           s.ltime ? s.ltime : nullptr),
-            "chunk forward");
-      note_launches(1);
-      if (nt > 0) {
-        const std::size_t smem = (static_cast<std::size_t>(kTailMaxRows) + kTailPbuf) * 8;
-        tail_sweep_kernel<true><<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tf_ptr,
-                                                               s.tf_col, s.tf_val, s.tail_s, in.diag, s.yf, s.yd,
-                                                               s.ltime ? s.ltime + (D + 2) : nullptr);
-        tail_sweep_kernel<false><<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
-                                                                s.tb_row, s.tb_val, nullptr, nullptr, s.zb, s.yd,
-                                                                s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
-        note_launches(2);
-      }
-      check(launch_cluster(cluster_sweep_fast_kernel<false>, cs.sweep_b, kChunkSmem, st, H, H, s.b_chunk,
-                           s.b_cbase, s.lb_ptr, s.lb_idx, s.lb_val, s.order, s.yd, nullptr, nullptr, nullptr,
-                           s.zb, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
-                           s.ltime ? s.ltime + 3 * (D + 2) : nullptr),
-            "chunk backward");
-      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
-      note_launches(2);
-      return;
-    }
-    if (!legacy) {
-      const ClusterSizes cs = cluster_sizes(in.device);
-      const int H = exact ? D : s.tail_L0;  // head depth (== D without a tail)
-      const int nt = exact ? 0 : s.tail_n;
-      if (exact)
-        check(launch_cluster(cluster_forward_kernel<true>, cs.fwd_exact, 0, st, H, s.lvl_off, s.order, s.gt_ptr,
-                             s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, 0, 0, s.hsplit, s.ff_col,
-                             s.ff_val, s.tail_s), "cluster forward");
-      else
-        check(launch_cluster(cluster_forward_kernel<false>, cs.fwd_fast, 0, st, H, s.lvl_off, s.order, s.gt_ptr,
-                             s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, nt, s.tail_base, s.hsplit,
-                             s.ff_col, s.ff_val, s.tail_s), "cluster forward");
-      note_launches(1);
-      if (nt > 0) {
-        const std::size_t smem = static_cast<std::size_t>(nt) * 8;
-        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
-                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
-                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
-        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
-                                                            s.tb_row, s.tb_val, s.yd, s.zb,
-                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
-        note_launches(2);
-      }
-      if (exact)
-        check(launch_cluster(cluster_backward_kernel<true>, cs.bwd_exact, 0, st, H, s.lvl_off, s.order, in.col_ptr,
-                             in.rows, in.vals, s.yd, s.zb), "cluster backward");
-      else
-        check(launch_cluster(cluster_backward_kernel<false>, cs.bwd_fast, 0, st, H, s.lvl_off, s.order, in.col_ptr,
-                             in.rows, in.vals, s.yd, s.zb), "cluster backward");
-      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
-      note_launches(2);
-      return;
-    }
-    if (!exact) {
-      const int H = s.tail_L0;  // head depth (== D without a tail)
-      sweep_forward_fast_kernel<<<grids.fwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, H, s.order, s.level, s.lvl_off, s.gt_ptr, s.ff_col, s.ff_val, s.ff_lvl, s.gt_col,
-          s.gt_val, in.diag, s.inv, r, s.yf, s.yd, done_f, s.counters + 2, s.trace);
-      note_launches(1);
-      if (s.tail_n > 0) {
-        const int sms = sm_count(in.device);
-        const std::size_t smem = static_cast<std::size_t>(s.tail_n) * 8;
-        tail_fwd_prologue_kernel<<<sms * 4, 256, 0, st>>>(s.tail_n, s.tail_base, s.order, s.gt_ptr, s.hsplit,
-                                                         s.ff_col, s.ff_val, s.inv, r, s.yf, s.tail_s);
-        tail_forward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tail_s,
-                                                           s.tf_ptr, s.tf_col, s.tf_val, in.diag, s.yf, s.yd,
-                                                           s.ltime ? s.ltime + (D + 2) : nullptr);
-        tail_backward_kernel<<<1, kTailThreads, smem, st>>>(H, D, s.tail_base, s.lvl_off, s.order, s.tb_ptr,
-                                                            s.tb_row, s.tb_val, s.yd, s.zb,
-                                                            s.ltime ? s.ltime + 2 * (D + 2) : nullptr);
-        note_launches(3);
-      }
-      sweep_backward_fast_kernel<<<grids.bwd_fast, kSweepThreads, 0, st>>>(
-          in.f_n, H, s.order, s.level, s.lvl_off, in.col_ptr, s.fb_row, s.fb_val, s.fb_lvl, in.rows,
-          in.vals, s.yd, s.zb, done_b, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
-      gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
-      note_launches(2);
-      return;
-    }
-    sweep_forward_kernel<<<grids.fwd, kSweepThreads, 0, st>>>(
-        in.f_n, D, s.order, s.level, s.lvl_off, s.gt_ptr, s.gt_col, s.gt_val, in.diag, s.inv, r,
-        s.yf, s.yd, done_f, s.counters + 4, s.counters + 2, s.trace);
-    sweep_backward_kernel<<<grids.bwd, kSweepThreads, 0, st>>>(
-        in.f_n, D, s.order, s.level, s.lvl_off, in.col_ptr, in.rows, in.vals, s.yd, s.zb, done_b,
-        s.counters + 5, s.counters + 3, s.trace ? s.trace + 3 * in.f_n : nullptr);
+    // exact mode: bit-identical to apply_preconditioner (serial row sums in the
+    // reference's order), one cluster per direction over all levels
+    const ClusterSizes cs = cluster_sizes(in.device);
+    check(launch_cluster(cluster_forward_kernel<true>, cs.fwd_exact, 0, st, D, s.lvl_off, s.order, s.gt_ptr,
+                         s.gt_col, s.gt_val, in.diag, s.inv, r, s.yf, s.yd, 0, 0, nullptr, nullptr, nullptr,
+                         nullptr), "cluster forward");
+    check(launch_cluster(cluster_backward_kernel<true>, cs.bwd_exact, 0, st, D, s.lvl_off, s.order, in.col_ptr,
+                         in.rows, in.vals, s.yd, s.zb), "cluster backward");
     gather_z_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, in.perm, s.zb, r, z, part(slot));
     note_launches(3);
-  }
-
-  // The sweeps' abort words (done[0] of each direction, see wait_level).
-  void check_abort() {
-    int flags[2] = {0, 0};
-    check(cudaMemcpyAsync(&flags[0], s.done, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
-    check(cudaMemcpyAsync(&flags[1], s.done + (s.depth + 2), sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
-    check(cudaStreamSynchronize(st), "sync");
-    if (flags[0] || flags[1])
-      throw Failure{queue_stall, "triangular sweep made no progress for 20 s (watchdog)"};
   }
 
   void spmv(const double* x, double* y, int slot) {
@@ -3002,22 +1885,6 @@ void download(double* dst, const double* src, int n, cudaStream_t st) {
   check(cudaStreamSynchronize(st), "d2h sync");
 }
 
-// Diagnostics (PARAC_SWEEP_TRACE=<file>): per-position start/end of the last
-// forward and backward sweeps, levels and level order, as raw little-endian arrays.
-void dump_sweep_trace(const SolveInputs& in, const char* path) {
-  const int n = in.f_n;
-  std::vector<unsigned long long> tr(6 * static_cast<std::size_t>(n));
-  std::vector<int> lv(n);
-  check(cudaMemcpy(tr.data(), in.state->trace, tr.size() * 8, cudaMemcpyDeviceToHost), "d2h");
-  check(cudaMemcpy(lv.data(), in.state->level, lv.size() * 4, cudaMemcpyDeviceToHost), "d2h");
-  FILE* f = std::fopen(path, "wb");
-  if (!f) return;
-  std::fwrite(&n, 4, 1, f);
-  std::fwrite(tr.data(), 8, tr.size(), f);
-  std::fwrite(lv.data(), 4, lv.size(), f);
-  std::fclose(f);
-}
-
 void need_graph(const SolveInputs& in) {
   if (in.n < 0) throw Failure{dimension_mismatch, "no graph staged (call parac_gpu_upload)"};
 }
@@ -3031,14 +1898,13 @@ void need_factor(const SolveInputs& in) {
 
 void solve_release(SolveState& s) {
   dfree(s.wdeg); dfree(s.inv); dfree(s.gt_ptr); dfree(s.gt_col); dfree(s.gt_val);
-  dfree(s.level); dfree(s.order); dfree(s.done); dfree(s.trace);
-  dfree(s.ff_col); dfree(s.ff_val); dfree(s.ff_lvl); dfree(s.fb_row); dfree(s.fb_val); dfree(s.fb_lvl); dfree(s.lvl_off); dfree(s.flags); dfree(s.x); dfree(s.r); dfree(s.p);
-  dfree(s.lp); dfree(s.z); dfree(s.best); dfree(s.yf); dfree(s.yd); dfree(s.zb); dfree(s.rhs);
+  dfree(s.level); dfree(s.order); dfree(s.lvl_off); dfree(s.flags);
+  dfree(s.x); dfree(s.r); dfree(s.p); dfree(s.lp); dfree(s.z); dfree(s.best);
+  dfree(s.yf); dfree(s.yd); dfree(s.zb); dfree(s.rhs);
   dfree(s.partials); dfree(s.scalars); dfree(s.counters); dfree(s.tiles); dfree(s.tmp_int);
-  dfree(s.tpos); dfree(s.tf_ptr); dfree(s.tb_ptr); dfree(s.hsplit); dfree(s.tf_col); dfree(s.tb_row);
-  dfree(s.tf_val); dfree(s.tb_val); dfree(s.tail_s); dfree(s.tail_cnt);
+  dfree(s.hsplit); dfree(s.tail_s); dfree(s.tail_cnt);
   dfree(s.lf_ptr); dfree(s.lb_ptr); dfree(s.lf_idx); dfree(s.lb_idx); dfree(s.lf_val); dfree(s.lb_val);
-  dfree(s.f_chunk); dfree(s.f_cbase); dfree(s.b_chunk); dfree(s.b_cbase); dfree(s.lvl_target); dfree(s.ltime);
+  dfree(s.lvl_target); dfree(s.ltime);
   dfree(s.hrec_gf); dfree(s.hrec_gb);
   dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
   dfree(s.t4_fpc); dfree(s.t4_bpc); dfree(s.t4_frange); dfree(s.t4_brange);
@@ -3101,16 +1967,12 @@ int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* 
     sv.precond(in.state->r, in.state->z, kSlotC, in.state->mode != kModeFast);
     check(cudaGetLastError(), "precond");
     download(z, in.state->z, in.f_n, in.stream);
-    sv.check_abort();
-    if (in.state->trace) dump_sweep_trace(in, std::getenv("PARAC_SWEEP_TRACE"));
     if (in.state->ltime) {  // diagnostics: [H, depth, tail rows, wide levels] then 16 x (depth+2) stamps
       const SolveState& ss = *in.state;
       std::vector<unsigned long long> t(16 * (static_cast<std::size_t>(ss.depth) + 2));
       check(cudaMemcpy(t.data(), ss.ltime, t.size() * 8, cudaMemcpyDeviceToHost), "d2h");
       if (FILE* f = std::fopen(std::getenv("PARAC_SWEEP_PROFILE"), "wb")) {
-        const bool v3 = ss.cap_v3 > 0;
-        const int hdr[4] = {v3 ? ss.t3_L0 : ss.tail_L0, ss.depth, v3 ? ss.t3_nt : ss.tail_n,
-                            v3 ? std::min(ss.wide_L, ss.t3_L0) : 0};
+        const int hdr[4] = {ss.t3_L0, ss.depth, ss.t3_nt, std::min(ss.wide_L, ss.t3_L0)};
         std::fwrite(hdr, 4, 4, f);
         std::fwrite(t.data(), 8, t.size(), f);
         std::fclose(f);
@@ -3220,7 +2082,6 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     }
     check(cudaEventRecord(e1, st), "event");
     check(cudaGetLastError(), "pcg");
-    if (b_norm != 0.0) sv.check_abort();
     download(x, s.x, n, st);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);

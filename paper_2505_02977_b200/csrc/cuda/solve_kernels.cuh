@@ -1,5 +1,6 @@
-// Device PCG state (solve path): SpMV, level-ordered sync-free triangular
-// sweeps, fused vector ops. See solve_kernels.cu.
+// Device PCG state (solve path): SpMV, level-synchronous triangular sweeps
+// (fast mode: wide levels / cluster head / one-CTA tail; exact mode: cluster),
+// fused vector ops. See solve_kernels.cu.
 #pragma once
 #include <cstdint>
 #include <vector>
@@ -23,26 +24,17 @@ struct SolveState {
   int* order = nullptr;       // positions sorted by level
   long long* lvl_off = nullptr;  // level offsets into order
   int* flags = nullptr;       // completion stamps per position (level pass)
-  int* done = nullptr;
-  // fast-mode sweep copies (entries sorted by dependency level) + level of each entry
-  int *ff_col = nullptr, *ff_lvl = nullptr, *fb_row = nullptr, *fb_lvl = nullptr;
-  double *ff_val = nullptr, *fb_val = nullptr;
-  // fast-mode narrow tail (levels > tail_L0), swept by one CTA (see solve_kernels.cu)
-  int tail_L0 = 0;            // head depth; == depth when there is no tail
-  int tail_n = 0, tail_base = 0;
-  int* tpos = nullptr;
-  long long *tf_ptr = nullptr, *tb_ptr = nullptr, *hsplit = nullptr;
-  int *tf_col = nullptr, *tb_row = nullptr;
-  double *tf_val = nullptr, *tb_val = nullptr, *tail_s = nullptr;
+  // fast-mode one-CTA tail (levels > t3_L0): tail rows' right-hand side after
+  // the head's contributions, scratch counts and forward T-part offsets
+  long long* hsplit = nullptr;
+  double* tail_s = nullptr;
   int* tail_cnt = nullptr;
-  // fast-mode chunked cluster sweeps: rows (forward) / columns (backward) of G
-  // copied in level order, and per-level chunk tables for the cluster's warps
+  // G's rows (forward) / columns (backward) copied in level order
   long long *lf_ptr = nullptr, *lb_ptr = nullptr;
   int *lf_idx = nullptr, *lb_idx = nullptr;
   double *lf_val = nullptr, *lb_val = nullptr;
-  int *f_chunk = nullptr, *f_cbase = nullptr, *b_chunk = nullptr, *b_cbase = nullptr;
   long long* lvl_target = nullptr;
-  unsigned long long* ltime = nullptr;
+  unsigned long long* ltime = nullptr;  // PARAC_SWEEP_PROFILE: per-level timestamps
   // v3 fast sweeps (level-order index space): maps, head chunk tables, tail arrays
   int *lpos = nullptr, *rlab = nullptr, *v2l = nullptr;
   double *dinv_l = nullptr, *rhs_l = nullptr;
@@ -59,12 +51,10 @@ struct SolveState {
   double* t3_fval = nullptr;
   std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0, cap_t4 = 0;
   int4 *t4_fpc = nullptr, *t4_bpc = nullptr;  // tail piece tables [nlev][32]
-  int2 *t4_frange = nullptr, *t4_brange = nullptr;  // tail entry range per level  // PARAC_SWEEP_PROFILE: per-level timestamps (4 x (depth+2))
+  int2 *t4_frange = nullptr, *t4_brange = nullptr;  // tail entry range per level
   std::size_t cap_ltime = 0;
-  std::size_t cap_lz = 0, cap_fchunk = 0, cap_bchunk = 0, cap_levels = 0;
-  std::size_t cap_tail = 0, cap_tail_nnz = 0;
+  std::size_t cap_lz = 0, cap_levels = 0;
   int mode = 0;  // 0 default (pcg fast, apply exact), 1 exact, 2 fast
-  unsigned long long* trace = nullptr;  // PARAC_SWEEP_TRACE diagnostics        // per-level finished-row counters, forward + backward
   int depth = 0;
   int epoch = 0;
   // vectors

@@ -1708,6 +1708,16 @@ void prepare_factor(const SolveInputs& in) {
   cudaStream_t st = in.stream;
   const int blocks = (n + 255) / 256;
   const int sms = sm_count(in.device);
+  static const bool verbose = std::getenv("PARAC_VERBOSE") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what) {
+    if (!verbose) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "prepare_factor %-16s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_start).count());
+    t_start = now;
+  };
   if (s.cap_z < static_cast<std::size_t>(std::max<long long>(Z, 1))) {
     const std::size_t cz = static_cast<std::size_t>(std::max<long long>(Z, 1));
     dalloc(s.gt_col, cz);
@@ -1724,6 +1734,7 @@ void prepare_factor(const SolveInputs& in) {
   gt_fill_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.gt_ptr, cnt, s.gt_col, s.gt_val);
   gt_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val);
   note_launches(2);
+  stamp("transpose");
   // levels: recorded by the elimination kernel for factors computed here,
   // recomputed (sync-free pass over G's rows) for uploaded ones
   check(cudaMemsetAsync(s.counters, 0, sizeof(int) * 4, st), "memset");
@@ -1748,8 +1759,11 @@ void prepare_factor(const SolveInputs& in) {
   check(cudaMemcpyAsync(&depth, s.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "prepare_factor");
   s.depth = depth;
+  stamp("levels");
   build_level_layout(in, s, sms);
+  stamp("level layout");
   build_fast_v3(in, s, sms);
+  stamp("v3 tables");
   if (std::getenv("PARAC_SWEEP_PROFILE")) {
     const std::size_t need = 16 * (static_cast<std::size_t>(s.depth) + 2);
     if (s.cap_ltime < need) {

@@ -21,7 +21,6 @@
 #include <string>
 #include <vector>
 
-#include <cooperative_groups.h>
 
 #include "../../../include/parac_gpu.h"
 #include "../host/errors.hpp"
@@ -699,34 +698,25 @@ __device__ __forceinline__ void head_load(HeadPre& p, const int4 rec, const long
   }
 }
 
-// GRID: one cooperative persistent grid (all SMs) for the wide first levels,
-// grid.sync() per level; otherwise one thread-block cluster (cluster barrier).
-// (A variant keeping the cluster rows' solution in distributed shared memory,
-// with the outside operands folded into the right-hand side beforehand, was
-// measured no faster: the level time is spread over load issue, gathers, row
-// sums and the barrier wait, not the L2 round trip of the gathers.)
-template <bool FWD, bool GRID>
+// One thread-block cluster sweeps levels Lfirst .. (cluster barrier per level).
+// Measured alternatives, removed: a cooperative full-GPU grid for the wide
+// levels (grid.sync(); 8-13 us per level, see DESIGN §4 K6); the cluster rows'
+// solution in distributed shared memory with the outside operands folded into
+// the right-hand side first (no faster: the level time is spread over load
+// issue, gathers, row sums and the barrier wait, not the gathers' L2 trip).
+template <bool FWD>
 __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
     int Lfirst, int nlev, int W, const int4* hrec, const long long* lptr, const int* lidx, const double* lval,
-    const double* rhs_l, const double* dinv_l, double* x, double* yd_l, const int* rlab, const double* rvec,
-    int n, int nt, int tail_base, double* ts, unsigned long long* ltime) {
+    const double* rhs_l, const double* dinv_l, double* x, double* yd_l, int nt, int tail_base, double* ts,
+    unsigned long long* ltime) {
   extern __shared__ double pbuf_all[];
   const int lane = lane_id(), wl = threadIdx.x >> 5;
-  const int w = (GRID ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_rank())) * kHWarps + wl;
+  const int w = static_cast<int>(cluster_rank()) * kHWarps + wl;
   double* pbuf = pbuf_all + wl * kChunkCap;
   auto xget = [&](int c) -> double { return __ldcg(x + c); };
   auto xput = [&](int j, double v) { x[j] = v; };
   const double* rhs_rows = rhs_l;
-  auto level_barrier = [&]() {
-    if constexpr (GRID) cooperative_groups::this_grid().sync();
-    else cluster_barrier();
-  };
-  if (FWD && rvec) {
-    // level 0: the right-hand side permuted into level order (label -> level order)
-    double* rl = const_cast<double*>(rhs_l);
-    for (int j = w * 32 + lane; j < n; j += W * 32) rl[j] = rvec[rlab[j]];
-    level_barrier();
-  }
+  auto level_barrier = [&]() { cluster_barrier(); };
   auto rec_ptr = [&](int t, int ww) -> const int4* {
     const int L = FWD ? Lfirst + t : Lfirst - t;
     return hrec + static_cast<long long>(L) * W + ww;
@@ -766,7 +756,7 @@ __global__ void __launch_bounds__(kHThreads, 1) head_sweep_kernel(
   if (nlev > 0) head_load<FWD>(nxt, myring[0], lptr, lidx, lval, rhs_rows, dinv_l, lane);
   // diagnostics (PARAC_SWEEP_PROFILE, cluster): warp 0's per-level phase
   // cycles {load issue, gathers+products, sums+stores, wait+barrier}
-  unsigned long long* dbg = (!GRID && ltime && w == 0 && lane == 0) ? ltime + (FWD ? 20 : 4) * (nlev + 8) : nullptr;
+  unsigned long long* dbg = (ltime && w == 0 && lane == 0) ? ltime + (FWD ? 20 : 4) * (nlev + 8) : nullptr;
   long long c0 = clock64(), c1 = 0, c2 = 0, c3 = 0;
   for (int t = 0; t < nlev; ++t) {
     if (dbg && t > 0) {
@@ -1371,22 +1361,6 @@ cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem
   return launch_cluster_t(kernel, csize, kCThreads, smem, st, args...);
 }
 
-// Cooperative (all CTAs co-resident, grid.sync allowed) launch.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_coop(void (*kernel)(KArgs...), int grid, int threads, std::size_t smem, cudaStream_t st,
-                        Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(threads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
-}
 
 // Largest launchable cluster (16 non-portable, else 8) of 1024-thread CTAs.
 template <typename... KArgs>
@@ -1553,23 +1527,15 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   remap_idx_kernel<<<sms * 8, 256, 0, st>>>(Z, s.lpos, s.lb_idx);
   note_launches(4);
   // head cluster geometry + chunk tables (all levels; the head uses 1..L0)
-  static int csize[64] = {}, gsize[64] = {};
+  static int csize[64] = {};
   const int dev = in.device >= 0 && in.device < 64 ? in.device : 0;
   if (!csize[dev]) {
-    csize[dev] = pick_cluster(head_sweep_kernel<true, false>, kHeadSmem, kHThreads);
-    cudaFuncSetAttribute(head_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
-    cudaFuncSetAttribute(head_sweep_kernel<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(head_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
-    cudaFuncSetAttribute(head_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
-    int pf = 0, pb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, head_sweep_kernel<true, true>, kHThreads, kHeadSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, head_sweep_kernel<false, true>, kHThreads, kHeadSmem);
-    gsize[dev] = std::max(1, std::min(pf, pb)) * sm_count(in.device);
+    csize[dev] = pick_cluster(head_sweep_kernel<true>, kHeadSmem, kHThreads);
+    cudaFuncSetAttribute(head_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
+    cudaFuncSetAttribute(head_sweep_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   s.head_csize = csize[dev];
   s.head_W = s.head_csize * kHWarps;
-  s.grid_ctas = gsize[dev];
-  s.grid_W = s.grid_ctas * kHWarps;
   const std::size_t nrec = (static_cast<std::size_t>(depth) + 2) * s.head_W;
   if (s.cap_hrec < nrec) {
     dalloc(s.hrec_f, nrec);
@@ -1583,8 +1549,8 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   std::vector<long long> off(static_cast<std::size_t>(depth) + 2);
   check(cudaMemcpyAsync(off.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "v3 sync");
-  // wide leading levels go to the cooperative full-GPU grid: rows + entries
-  // (forward rows and backward columns) above PARAC_WIDE_WEIGHT (default 32768)
+  // wide leading levels (one launch per level): rows + entries (forward rows
+  // and backward columns) above PARAC_WIDE_WEIGHT (default 32768)
   {
     const char* ww = std::getenv("PARAC_WIDE_WEIGHT");
     const long long wide = ww ? std::atoll(ww) : 32768;
@@ -1613,17 +1579,6 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
       s.wide_kb[L] = wide_lanes(off[L + 1] - off[L], eb[L + 1] - eb[L]);
     }
     s.lvl_off_h.assign(off.begin(), off.begin() + std::min<std::size_t>(off.size(), static_cast<std::size_t>(Lw) + 2));
-    if (Lw > 0) {
-      const std::size_t ng = (static_cast<std::size_t>(Lw) + 2) * s.grid_W;
-      if (s.cap_grec < ng) {
-        dalloc(s.hrec_gf, ng);
-        dalloc(s.hrec_gb, ng);
-        s.cap_grec = ng;
-      }
-      head_chunk_kernel<<<Lw, 256, 0, st>>>(Lw, s.grid_W, s.lvl_off, s.lf_ptr, s.hrec_gf);
-      head_chunk_kernel<<<Lw, 256, 0, st>>>(Lw, s.grid_W, s.lvl_off, s.lb_ptr, s.hrec_gb);
-      note_launches(2);
-    }
   }
   const char* env = std::getenv("PARAC_TAIL_WIDTH");
   const int wt = std::min(32, env ? std::atoi(env) : 32);  // tail4 needs <= 32 rows per level
@@ -1807,30 +1762,21 @@ struct Solver {
       const int H = s.t3_L0, nt = s.t3_nt;
       const int Lw = std::min(s.wide_L, H);
       unsigned long long* lt = s.ltime;
-      static const bool coop_wide = std::getenv("PARAC_WIDE") && std::string(std::getenv("PARAC_WIDE")) == "coop";
-      if (Lw > 0 && coop_wide) {
-        check(launch_coop(head_sweep_kernel<true, true>, s.grid_ctas, kHThreads, kHeadSmem, st, 1, Lw, s.grid_W,
-                          s.hrec_gf, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, s.rlab, r,
-                          in.f_n, 0, s.t3_base, s.tail_s, lt), "wide forward");
-        note_launches(1);
-      } else {
-        rhs_permute_kernel<<<(in.f_n + 255) / 256, 256, 0, st>>>(in.f_n, s.rlab, r, s.rhs_l);
-        note_launches(1);
+      // forward: rhs into level order, wide levels (one launch each), cluster head, tail
+      rhs_permute_kernel<<<(in.f_n + 255) / 256, 256, 0, st>>>(in.f_n, s.rlab, r, s.rhs_l);
+      note_launches(1);
+      for (int L = 1; L <= Lw; ++L) {
+        const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
+        check(launch_wide_level<true>(s.wide_kf[L], j0, j1, st, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l,
+                                      s.yf, s.yd, L >= 2, lt ? lt + (L - 1) : nullptr), "wide level forward");
       }
-      if (Lw > 0 && !coop_wide) {
-        for (int L = 1; L <= Lw; ++L) {
-          const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
-          check(launch_wide_level<true>(s.wide_kf[L], j0, j1, st, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l,
-                                        s.yf, s.yd, L >= 2, lt ? lt + (L - 1) : nullptr), "wide level forward");
-        }
-        note_launches(Lw);
-      }
-      check(launch_cluster_t(head_sweep_kernel<true, false>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
-                             s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd,
-                             s.rlab, (Lw > 0 || !coop_wide) ? nullptr : r, in.f_n, nt, s.t3_base, s.tail_s,
-                             lt ? lt + Lw : nullptr),
+      note_launches(Lw);
+      check(launch_cluster_t(head_sweep_kernel<true>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
+                             s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, nt,
+                             s.t3_base, s.tail_s, lt ? lt + Lw : nullptr),
             "head forward");
       note_launches(1);
+      // tail forward + backward (one CTA each)
       if (nt > 0) {
         const std::size_t t4smem = tail4_smem(s.t3_nlev);
         tail4_kernel<true><<<1, kTailThreads, t4smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_fpc, s.t4_frange,
@@ -1842,26 +1788,19 @@ struct Solver {
                                                              lt ? lt + 2 * (D + 2) : nullptr);
         note_launches(2);
       }
-      check(launch_cluster_t(head_sweep_kernel<false, false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
-                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr,
-                             nullptr, nullptr, in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) : nullptr),
+      // backward: cluster head, wide levels
+      check(launch_cluster_t(head_sweep_kernel<false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
+                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, 0, 0,
+                             nullptr, lt ? lt + 3 * (D + 2) : nullptr),
             "head backward");
       note_launches(1);
-      if (Lw > 0 && coop_wide) {
-        check(launch_coop(head_sweep_kernel<false, true>, s.grid_ctas, kHThreads, kHeadSmem, st, Lw, Lw, s.grid_W,
-                          s.hrec_gb, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, nullptr, nullptr,
-                          in.f_n, 0, 0, nullptr, lt ? lt + 3 * (D + 2) + (H - Lw) : nullptr),
-              "wide backward");
-        note_launches(1);
-      } else if (Lw > 0) {
-        for (int L = Lw; L >= 1; --L) {
-          const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
-          check(launch_wide_level<false>(s.wide_kb[L], j0, j1, st, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb,
-                                         nullptr, 1, lt ? lt + 3 * (D + 2) + (H - Lw) + (Lw - L) : nullptr),
-                "wide level backward");
-        }
-        note_launches(Lw);
+      for (int L = Lw; L >= 1; --L) {
+        const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
+        check(launch_wide_level<false>(s.wide_kb[L], j0, j1, st, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb,
+                                       nullptr, 1, lt ? lt + 3 * (D + 2) + (H - Lw) + (Lw - L) : nullptr),
+              "wide level backward");
       }
+      note_launches(Lw);
       gather_z_l_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(in.f_n, s.v2l, s.zb, r, z, part(slot));
       note_launches(2);
       return;
@@ -1919,7 +1858,6 @@ void solve_release(SolveState& s) {
   dfree(s.hsplit); dfree(s.tail_s); dfree(s.tail_cnt);
   dfree(s.lf_ptr); dfree(s.lb_ptr); dfree(s.lf_idx); dfree(s.lb_idx); dfree(s.lf_val); dfree(s.lb_val);
   dfree(s.lvl_target); dfree(s.ltime);
-  dfree(s.hrec_gf); dfree(s.hrec_gb);
   dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
   dfree(s.t4_fpc); dfree(s.t4_bpc); dfree(s.t4_frange); dfree(s.t4_brange);
   dfree(s.t3_lvl); dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_bep); dfree(s.t3_fval);

@@ -40,11 +40,9 @@ struct SolveState {
   double *dinv_l = nullptr, *rhs_l = nullptr;
   int4 *hrec_f = nullptr, *hrec_b = nullptr;
   int head_csize = 0, head_W = 0;
-  int grid_ctas = 0, grid_W = 0, wide_L = 0;  // the wide first levels (one launch per level)
+  int wide_L = 0;                             // the wide first levels (one launch per level)
   std::vector<long long> lvl_off_h;           // host copy of the level offsets of levels 0..wide_L+1
   std::vector<int> wide_kf, wide_kb;          // lanes per row of each wide level (forward rows / backward columns)
-  int4 *hrec_gf = nullptr, *hrec_gb = nullptr;
-  std::size_t cap_grec = 0;
   int t3_L0 = 0, t3_nt = 0, t3_base = 0, t3_nlev = 0;
   long long t3_bbase = 0;  // lb_ptr[t3_base]
   int *t3_lvl = nullptr, *t3_fep = nullptr, *t3_fidx = nullptr, *t3_bep = nullptr;

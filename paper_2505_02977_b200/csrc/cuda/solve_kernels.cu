@@ -1550,10 +1550,10 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   check(cudaMemcpyAsync(off.data(), s.lvl_off, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "v3 sync");
   // wide leading levels (one launch per level): rows + entries (forward rows
-  // and backward columns) above PARAC_WIDE_WEIGHT (default 32768)
+  // and backward columns) above PARAC_WIDE_WEIGHT (default 16384)
   {
     const char* ww = std::getenv("PARAC_WIDE_WEIGHT");
-    const long long wide = ww ? std::atoll(ww) : 32768;
+    const long long wide = ww ? std::atoll(ww) : 16384;
     std::vector<long long> ef(static_cast<std::size_t>(depth) + 2), eb(static_cast<std::size_t>(depth) + 2);
     long long* bnd = s.lvl_target;
     gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, s.lf_ptr, bnd);

@@ -186,8 +186,37 @@ __global__ void gt_sort_kernel(int n, const long long* gt_ptr, int* gt_col, doub
         gt_col[b + rank] = k;
         gt_val[b + rank] = v;
       }
+    } else if (len <= 256) {
+      // up to 8 keys per lane, ranked against every key of the row (keys are
+      // unique columns) through register broadcasts; then scattered in place
+      int k[8];
+      double v[8];
+      int rank[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = i * 32 + lane;
+        k[i] = e < len ? gt_col[b + e] : 0x7fffffff;
+        v[i] = e < len ? gt_val[b + e] : 0.0;
+        rank[i] = 0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if (jj * 32 >= len) break;
+        for (int src = 0; src < 32; ++src) {
+          const int kj = __shfl_sync(kFull, k[jj], src);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rank[i] += kj < k[i];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i * 32 + lane < len) {
+          gt_col[b + rank[i]] = k[i];
+          gt_val[b + rank[i]] = v[i];
+        }
     } else {
-      // In-place odd-even transposition is O(len^2); rows this long are rare.
+      // In-place odd-even transposition is O(len^2); rows longer than 256 are rare.
       for (int phase = 0; phase < len; ++phase) {
         for (int i = 2 * lane + (phase & 1); i + 1 < len; i += 64) {
           const int a = gt_col[b + i], c = gt_col[b + i + 1];

@@ -1477,6 +1477,7 @@ int component_count(const SolveInputs& in) {
   SolveState& s = *in.state;
   const int n = in.n;
   if (n == 0) return 0;
+  if (s.graph_ready && s.components >= 0) return s.components;  // once per staged graph
   const int blocks = (n + 255) / 256;
   cudaStream_t st = in.stream;
   int* parent = s.tmp_int;
@@ -1489,6 +1490,7 @@ int component_count(const SolveInputs& in) {
   int h = 0;
   check(cudaMemcpyAsync(&h, count, sizeof(int), cudaMemcpyDeviceToHost, st), "cc");
   check(cudaStreamSynchronize(st), "cc sync");
+  s.components = h;
   return h;
 }
 
@@ -1894,6 +1896,7 @@ void solve_release(SolveState& s) {
 }
 void solve_invalidate(SolveState& s) {
   s.graph_ready = false;
+  s.components = -1;
   s.factor_ready = false;
 }
 void solve_invalidate_factor(SolveState& s) { s.factor_ready = false; }

@@ -12,6 +12,7 @@ namespace parac_gpu {
 
 struct SolveState {
   bool graph_ready = false;   // wdeg computed for the staged graph
+  int components = -1;        // connected components of the staged graph (-1: not yet counted)
   bool factor_ready = false;  // G^T (CSR), inverse perm, level order built
   int n = 0;
   double* wdeg = nullptr;

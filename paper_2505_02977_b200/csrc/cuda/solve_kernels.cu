@@ -12,6 +12,8 @@
 // dot products use a deterministic two-level tree (run-to-run reproducible, not
 // the reference's serial order), which SURVEY §8(a) a16 validated does not move
 // iteration counts.
+#include <cub/device/device_segmented_sort.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -215,21 +217,53 @@ __global__ void gt_sort_kernel(int n, const long long* gt_ptr, int* gt_col, doub
           gt_col[b + rank[i]] = k[i];
           gt_val[b + rank[i]] = v[i];
         }
-    } else {
-      // In-place odd-even transposition is O(len^2); rows longer than 256 are rare.
-      for (int phase = 0; phase < len; ++phase) {
-        for (int i = 2 * lane + (phase & 1); i + 1 < len; i += 64) {
-          const int a = gt_col[b + i], c = gt_col[b + i + 1];
-          if (a > c) {
-            gt_col[b + i] = c;
-            gt_col[b + i + 1] = a;
-            const double va = gt_val[b + i];
-            gt_val[b + i] = gt_val[b + i + 1];
-            gt_val[b + i + 1] = va;
-          }
-        }
-        __syncwarp();
-      }
+    }  // longer rows: gt_long_* + a CUB segmented sort (prepare_factor)
+  }
+}
+
+// Rows of G^T longer than 256 entries (hub columns of the factor) are sorted
+// out of line: flagged and counted, copied into a compact buffer, sorted there
+// by CUB's segmented sort (any length), and copied back.
+constexpr int kGtShortRow = 256;
+__global__ void gt_long_flags_kernel(int n, const long long* gt_ptr, int* flag, int* len) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const long long l = gt_ptr[r + 1] - gt_ptr[r];
+  flag[r] = l > kGtShortRow ? 1 : 0;
+  len[r] = l > kGtShortRow ? static_cast<int>(l) : 0;
+}
+__global__ void gt_long_gather_kernel(int n, const long long* gt_ptr, const int* flag, const long long* rpos,
+                                      const long long* loff, const int* gt_col, const double* gt_val, int* beg,
+                                      int* end, int* rows, int* ck, double* cv) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = gw; r < n; r += nw) {
+    if (!flag[r]) continue;
+    const long long b = gt_ptr[r], l = gt_ptr[r + 1] - b, o = loff[r];
+    if (lane == 0) {
+      const long long i = rpos[r];
+      beg[i] = static_cast<int>(o);
+      end[i] = static_cast<int>(o + l);
+      rows[i] = r;
+    }
+    for (long long q = lane; q < l; q += 32) {
+      ck[o + q] = gt_col[b + q];
+      cv[o + q] = gt_val[b + q];
+    }
+  }
+}
+__global__ void gt_long_scatter_kernel(int nl, const long long* gt_ptr, const int* beg, const int* end,
+                                       const int* rows, const int* ck, const double* cv, int* gt_col,
+                                       double* gt_val) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < nl; i += nw) {
+    const long long b = gt_ptr[rows[i]];
+    for (int q = beg[i] + lane; q < end[i]; q += 32) {
+      gt_col[b + q - beg[i]] = ck[q];
+      gt_val[b + q - beg[i]] = cv[q];
     }
   }
 }
@@ -1720,6 +1754,54 @@ void prepare_factor(const SolveInputs& in) {
   gt_fill_kernel<<<sms * 8, 256, 0, st>>>(n, in.col_ptr, in.rows, in.vals, s.gt_ptr, cnt, s.gt_col, s.gt_val);
   gt_sort_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, s.gt_col, s.gt_val);
   note_launches(2);
+  {  // rows longer than kGtShortRow
+    int* flag = s.tmp_int;
+    int* len = nullptr;
+    long long* rpos = nullptr;
+    long long* loff = nullptr;
+    check(cudaMallocAsync(&len, sizeof(int) * (static_cast<std::size_t>(n) + 1), st), "alloc");
+    check(cudaMallocAsync(&rpos, sizeof(long long) * (static_cast<std::size_t>(n) + 1), st), "alloc");
+    check(cudaMallocAsync(&loff, sizeof(long long) * (static_cast<std::size_t>(n) + 1), st), "alloc");
+    gt_long_flags_kernel<<<blocks, 256, 0, st>>>(n, s.gt_ptr, flag, len);
+    note_launches(1);
+    check(launch_scan(flag, n, rpos, s.tiles, st), "scan");
+    check(launch_scan(len, n, loff, s.tiles, st), "scan");
+    long long tot[2] = {0, 0};
+    check(cudaMemcpyAsync(&tot[0], rpos + n, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaMemcpyAsync(&tot[1], loff + n, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "long rows");
+    const int nl = static_cast<int>(tot[0]);
+    const long long T = tot[1];
+    if (nl > 0) {
+      int *beg, *end, *rows, *ck, *ck2;
+      double *cv, *cv2;
+      check(cudaMallocAsync(&beg, sizeof(int) * nl, st), "alloc");
+      check(cudaMallocAsync(&end, sizeof(int) * nl, st), "alloc");
+      check(cudaMallocAsync(&rows, sizeof(int) * nl, st), "alloc");
+      check(cudaMallocAsync(&ck, sizeof(int) * T, st), "alloc");
+      check(cudaMallocAsync(&ck2, sizeof(int) * T, st), "alloc");
+      check(cudaMallocAsync(&cv, sizeof(double) * T, st), "alloc");
+      check(cudaMallocAsync(&cv2, sizeof(double) * T, st), "alloc");
+      gt_long_gather_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, flag, rpos, loff, s.gt_col, s.gt_val, beg, end,
+                                                     rows, ck, cv);
+      std::size_t tb = 0;
+      check(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, ck, ck2, cv, cv2, static_cast<int>(T), nl, beg, end,
+                                                st), "segmented sort size");
+      void* tmp = nullptr;
+      check(cudaMallocAsync(&tmp, std::max<std::size_t>(tb, 1), st), "alloc");
+      check(cub::DeviceSegmentedSort::SortPairs(tmp, tb, ck, ck2, cv, cv2, static_cast<int>(T), nl, beg, end, st),
+            "segmented sort");
+      gt_long_scatter_kernel<<<sms * 8, 256, 0, st>>>(nl, s.gt_ptr, beg, end, rows, ck2, cv2, s.gt_col, s.gt_val);
+      note_launches(2);
+      for (void* q : {static_cast<void*>(beg), static_cast<void*>(end), static_cast<void*>(rows),
+                      static_cast<void*>(ck), static_cast<void*>(ck2), static_cast<void*>(cv),
+                      static_cast<void*>(cv2), tmp})
+        check(cudaFreeAsync(q, st), "free");
+    }
+    check(cudaFreeAsync(rpos, st), "free");
+    check(cudaFreeAsync(loff, st), "free");
+    check(cudaFreeAsync(len, st), "free");
+  }
   stamp("transpose");
   // levels: recorded by the elimination kernel for factors computed here,
   // recomputed (sync-free pass over G's rows) for uploaded ones

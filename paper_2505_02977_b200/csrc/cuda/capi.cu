@@ -237,7 +237,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.watchdog_ns = static_cast<unsigned long long>(wd * 1e9);
   d.verify = o.verify;
   {  // PARAC_CLAIM_SLEEP="a,b,c" (ns) overrides the claim backoff tiers (tuning)
-    unsigned t[3] = {512, 4096, 16384};
+    unsigned t[3] = {128, 1024, 4096};  // measured: 2D 256^2 1.77 -> 1.40 ms, 128^3 -1% vs 512,4096,16384
     if (const char* e = std::getenv("PARAC_CLAIM_SLEEP")) std::sscanf(e, "%u,%u,%u", &t[0], &t[1], &t[2]);
     for (int i = 0; i < 3; ++i) d.sleep_ns[i] = t[i];
     const char* kp = std::getenv("PARAC_KEEP");

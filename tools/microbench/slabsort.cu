@@ -34,6 +34,31 @@ __global__ void run(unsigned long long* K, unsigned long long* V, unsigned long 
   }
 }
 
+
+// rank_sort<kThreads, 4> alone on shared-memory data (no global traffic), 10 reps
+__global__ void rank_only(unsigned long long* out, int R) {
+  extern __shared__ char smem[];
+  unsigned long long* X1 = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* X2 = X1 + 1024;
+  int* IA = reinterpret_cast<int*>(X2 + 1024);
+  int* IB = IA + 1024;
+  unsigned long long key[4];
+  for (int i = 0; i < 4; ++i) {
+    const unsigned g = i * kThreads + threadIdx.x;
+    key[i] = (static_cast<unsigned long long>((g * 2654435761u) % 4000000u) << 32) | (g + 1);
+  }
+  int rank[4];
+  __syncthreads();
+  const long long c0 = clock64();
+  for (int rep = 0; rep < 10; ++rep) {
+    rank_sort<kThreads, 4>(key, R, X1, X2, IA, IB, rank);
+    __syncthreads();
+  }
+  const long long c1 = clock64();
+  if (threadIdx.x == 0) out[0] = (c1 - c0) / 10;
+  if (threadIdx.x == 1) out[1] = rank[0];
+}
+
 int main() {
   const int Rs[] = {1024, 2048, 4096, 5600, 16384, 65536};
   unsigned long long *K, *V, *K2, *V2, *out;
@@ -69,6 +94,13 @@ int main() {
       printf("R %6d %s: total %8.1f us, tiles %8.1f us, merges %8.1f us %s\n", R, which ? "weight" : "raw   ",
              best / 1e3, bt / 1e3, (best - bt) / 1e3, ok ? "sorted" : "NOT SORTED");
     }
+  }
+  cudaFuncSetAttribute(rank_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
+  for (int R : {256, 512, 1024}) {
+    rank_only<<<1, kThreads, kCtaSmem>>>(out, R);
+    unsigned long long h[2];
+    cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+    printf("rank_sort<256,4> alone, R %d: %llu cycles\n", R, h[0]);
   }
   const cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));

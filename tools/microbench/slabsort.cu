@@ -48,15 +48,20 @@ __global__ void rank_only(unsigned long long* out, int R) {
     key[i] = (static_cast<unsigned long long>((g * 2654435761u) % 4000000u) << 32) | (g + 1);
   }
   int rank[4];
+  __shared__ long long cyc[3];
   __syncthreads();
   const long long c0 = clock64();
   for (int rep = 0; rep < 10; ++rep) {
-    rank_sort<kThreads, 4>(key, R, X1, X2, IA, IB, rank);
+    rank_sort<kThreads, 4>(key, R, X1, X2, IA, IB, rank, cyc);
     __syncthreads();
   }
   const long long c1 = clock64();
-  if (threadIdx.x == 0) out[0] = (c1 - c0) / 10;
-  if (threadIdx.x == 1) out[1] = rank[0];
+  if (threadIdx.x == 0) {
+    out[0] = (c1 - c0) / 10;
+    out[1] = cyc[0];
+    out[2] = cyc[1];
+    out[3] = cyc[2];
+  }
 }
 
 int main() {
@@ -98,9 +103,10 @@ int main() {
   cudaFuncSetAttribute(rank_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
   for (int R : {256, 512, 1024}) {
     rank_only<<<1, kThreads, kCtaSmem>>>(out, R);
-    unsigned long long h[2];
-    cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
-    printf("rank_sort<256,4> alone, R %d: %llu cycles\n", R, h[0]);
+    unsigned long long h[4];
+    cudaMemcpy(h, out, 32, cudaMemcpyDeviceToHost);
+    printf("rank_sort<256,4> alone, R %d: %llu cycles (stage %llu, phase1 %llu, phase2 %llu)\n", R, h[0], h[1],
+           h[2], h[3]);
   }
   const cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));

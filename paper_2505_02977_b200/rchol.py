@@ -291,6 +291,10 @@ class GpuContext:
         self.device = device
         self._graph = None
         self._factor_n = -1
+        # the LdlFactor object whose arrays are the context's resident factor
+        # (factors are immutable inputs, like the reference's const LdlFactor&;
+        # the ones factor_gpu returns are marked read-only)
+        self._resident = None
 
     def close(self) -> None:
         if self.handle:
@@ -316,12 +320,14 @@ class GpuContext:
         csr = graph.csr()
         _check(lib.parac_gpu_upload(self.handle, C.byref(csr), _ptr(ordering.perm)))
         self._graph = (graph, ordering)
+        self._resident = None  # staging a graph drops the resident factor
 
     def factor_resident(self, seed: int, options: Optional[GpuOptions] = None):
         o = (options or GpuOptions()).native()
         info = L.parac_gpu_factor_info()
         _check(lib.parac_gpu_factor_resident(self.handle, seed, C.byref(o), C.byref(info)))
         self._factor_n = info.n
+        self._resident = None
         return info
 
     def download(self, with_stats: bool = True):
@@ -357,6 +363,12 @@ class GpuContext:
         _check(lib.parac_gpu_upload_factor(self.handle, f.n, _ptr(f.col_ptr), _ptr(f.rows),
                                            _ptr(f.values), _ptr(f.diag), _ptr(f.perm)))
         self._factor_n = f.n
+        self._resident = f
+
+    def ensure_factor(self, f: LdlFactor) -> None:
+        """Make f the resident factor; no copy when it already is (same object)."""
+        if self._resident is not f:
+            self.upload_factor(f)
 
 
 _default_ctx: Optional[GpuContext] = None
@@ -382,6 +394,9 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
     ctx.upload(graph, ordering)
     info = ctx.factor_resident(seed, options)
     f, st = ctx.download(with_stats=stats is not None)
+    for a in (f.col_ptr, f.rows, f.values, f.diag):
+        a.flags.writeable = False
+    ctx._resident = f  # the device copy stays resident for solves on this factor
     if stats is not None:
         stats.merged_degree, stats.samples_emitted, stats.fills_received = st
         stats.total_fills = info.total_fills
@@ -472,7 +487,7 @@ def _stage_for_solve(ctx: GpuContext, graph: Optional[LaplacianGraph], factor: L
         g_cur = ctx._graph[0] if ctx._graph else None
         if g_cur is not graph:
             ctx.upload(graph, Ordering(factor.perm))
-    ctx.upload_factor(factor)
+    ctx.ensure_factor(factor)
 
 
 def pcg_solve_gpu(graph: LaplacianGraph, factor: LdlFactor, b: np.ndarray,
@@ -503,7 +518,7 @@ def apply_preconditioner_gpu(factor: LdlFactor, r: np.ndarray,
     if len(r) != factor.n:
         raise Error(Errc.dimension_mismatch,
                     f"DimensionMismatch: vector length {len(r)} vs factor size {factor.n}")
-    ctx.upload_factor(factor)
+    ctx.ensure_factor(factor)
     r = np.ascontiguousarray(r, dtype=np.float64)
     z = np.empty(factor.n, np.float64)
     _check(lib.parac_gpu_apply_preconditioner(ctx.handle, _ptr(r), _ptr(z)))
@@ -527,7 +542,7 @@ def laplacian_apply_gpu(graph: LaplacianGraph, x: np.ndarray,
 def schedule_levels_gpu(factor: LdlFactor, ctx: Optional[GpuContext] = None):
     """schedule_levels / schedule_depth (factor_par.hpp:66-70). Returns (levels, depth)."""
     ctx = ctx or default_context()
-    ctx.upload_factor(factor)
+    ctx.ensure_factor(factor)
     lv = np.empty(max(factor.n, 1), np.int32)
     depth = C.c_int32()
     _check(lib.parac_gpu_schedule_levels(ctx.handle, _ptr(lv), C.byref(depth)))

@@ -685,6 +685,11 @@ int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_pt
     ctx->f_nnz = Z;
     ctx->f_has_stats = false;
     ctx->f_external = true;
+    if (ctx->batch_count > 0) {  // an uploaded factor replaces a resident batch; the
+      ctx->batch_count = 0;      // staged union graph means nothing without it
+      ctx->n = -1;
+      solve_invalidate(ctx->solve);
+    }
     solve_invalidate_factor(ctx->solve);
   });
 }

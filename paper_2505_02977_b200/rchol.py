@@ -439,6 +439,8 @@ def factor_batch_gpu(graphs: Sequence[LaplacianGraph], orderings: Sequence[Order
     _check(lib.parac_gpu_factor_batch(ctx.handle, len(graphs), csrs, perms, _ptr(sd), C.byref(o),
                                       C.byref(info)))
     ctx._factor_n = info.n
+    ctx._graph = None      # the context now holds the batch union,
+    ctx._resident = None   # not any single graph or factor
     out = []
     for i, (g, ordg) in enumerate(zip(graphs, orderings)):
         z = C.c_int64()

@@ -129,3 +129,20 @@ def test_fast_preconditioner_close_to_exact(gpu_ctx, port):
     finally:
         gpu_ctx.set_preconditioner_mode("default")
     assert np.allclose(z, want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
+
+
+def test_resident_factor_tracking_across_batch(gpu_ctx):
+    # factor_gpu keeps its factor resident; a batch pass replaces the device
+    # state, and later solves on the single factor must re-stage it
+    g = P.gen_poisson3d(10)
+    o = P.ordering_random(g.n, 2)
+    f = P.factor_gpu(g, o, 2, ctx=gpu_ctx)
+    b = P.make_rhs(g, "random_projected", 0)
+    z0 = P.apply_preconditioner_gpu(f, b, ctx=gpu_ctx)
+    P.factor_batch_gpu([P.gen_poisson3d(6), P.gen_poisson3d(7)], [P.ordering_random(216, 0),
+                       P.ordering_random(343, 1)], [0, 1], ctx=gpu_ctx)
+    z1 = P.apply_preconditioner_gpu(f, b, ctx=gpu_ctx)
+    assert z0.tobytes() == z1.tobytes()
+    x, rep = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+    assert rep.converged
+    assert not f.values.flags.writeable  # factors from factor_gpu are immutable

@@ -123,3 +123,19 @@ def test_cli_errors():
     assert cli.main(["factor", "--gen", "poisson3d:n=4", "--ordering", "bogus"]) == 10 + 5
     assert cli.main(["factor", "--gen", "cube:n=4"]) == 10 + 5
     assert cli.main(["factor", "--input", "/nonexistent.mtx"]) == 10 + 16
+
+
+def test_solve_factors_on_gpu_without_factor_files(R, tmp_path):
+    # solve without --factor: the runner factors on the device (gpu backend), then runs PCG
+    g = P.gen_poisson3d(12, "anisotropic", 1e-3, 1e4, 0)
+    rj = str(tmp_path / "r.json")
+    rc = cli.main(["solve", "--gen", "poisson3d:n=12,variant=anisotropic", "--ordering", "random", "--seed", "2",
+                   "--tol", "1e-8", "--report", rj])
+    rep = json.load(open(rj))
+    assert rc == 0 and rep["converged"] and rep["relative_residual"] <= 1e-8
+    h = R.graph_from_csr(g)
+    f, _ = R.factor(h, P.ordering_random(g.n, 2).perm, 2, backend=R.SEQ)
+    it = ref_pcg_iters(R, h, f, 2, 1e-8)
+    assert abs(rep["iterations"] - it) <= max(1, it // 10)
+    R.free_factor(f)
+    R.free_graph(h)

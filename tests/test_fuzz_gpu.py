@@ -70,3 +70,38 @@ def test_fuzz_byte_identical(gpu_ctx, port, case_seed):
     want = port.factor(g, perm, seed)
     assert f.same_values(factor_from_port(want)), (case_seed, kind, g.n)
     assert np.array_equal(st.fills_received, want["fills_received"]), (case_seed, kind)
+
+
+@pytest.mark.parametrize("case_seed", range(24))
+def test_fuzz_solve(gpu_ctx, port, case_seed):
+    # apply_preconditioner: exact sweeps bit-identical to the oracle
+    # (proj/src/solver.cpp apply_preconditioner), fast sweeps within 1e-10;
+    # PCG iterations within 10% of the oracle's
+    rng = np.random.default_rng(5000 + case_seed)
+    g, kind = random_graph(rng)
+    seed = int(rng.integers(0, 1 << 31))
+    perm = P.ordering_random(g.n, seed).perm
+    want = port.factor(g, perm, seed)
+    f = factor_from_port(want)
+    r = P.make_rhs(g, "random_projected", seed)
+    zref = port.apply_preconditioner(want, r)
+    try:
+        gpu_ctx.set_preconditioner_mode("exact")
+        assert P.apply_preconditioner_gpu(f, r, ctx=gpu_ctx).tobytes() == zref.tobytes(), (case_seed, kind)
+        gpu_ctx.set_preconditioner_mode("fast")
+        z = P.apply_preconditioner_gpu(f, r, ctx=gpu_ctx)
+        assert np.allclose(z, zref, rtol=1e-10, atol=1e-12 * max(np.abs(zref).max(), 1e-300)), (case_seed, kind)
+    finally:
+        gpu_ctx.set_preconditioner_mode("default")
+    rc, _, ref = port.pcg(g, want, r, tol=1e-8)
+    try:
+        x, rep = P.pcg_solve_gpu(g, f, r, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+    except P.Error:
+        assert rc != 0 or not ref["converged"], (case_seed, kind)
+        return
+    # the iteration gate applies where the reference converges (disconnected graphs and
+    # twelve-decade weights can stall both; there only a clean report is required)
+    if rc == 0 and ref["converged"]:
+        assert rep.converged and rep.relative_residual <= 1e-8, (case_seed, kind)
+        assert abs(rep.iterations - ref["iterations"]) <= max(1, ref["iterations"] // 10), (case_seed, kind, ref)
+    assert np.isfinite(x).all() and rep.iterations <= 1000

@@ -378,8 +378,8 @@ __global__ void update_xr_kernel(int n, const double* plp_partials, const double
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     double rv = r[v];
     if (ok) {
-      x[v] += alpha * p[v];
-      rv -= alpha * lp[v];
+      x[v] = __dadd_rn(x[v], __dmul_rn(alpha, p[v]));  // unfused, as solver.cpp:137-138
+      rv = __dsub_rn(rv, __dmul_rn(alpha, lp[v]));
       r[v] = rv;
     }
     s += rv * rv;
@@ -410,7 +410,7 @@ __global__ void update_p_kernel(int n, const double* rz_partials, double* scalar
   }
   __syncthreads();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    p[v] = first ? z[v] : z[v] + beta * p[v];
+    p[v] = first ? z[v] : __dadd_rn(z[v], __dmul_rn(beta, p[v]));
 }
 
 __global__ void copy_kernel(int n, const double* a, double* b) {

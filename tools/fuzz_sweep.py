@@ -1,4 +1,6 @@
-"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT.
+"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve].
+Without --solve: factors byte for byte; with it: exact-mode preconditioner bytes,
+fast mode within 1e-10 and PCG iterations within 10% where the oracle converges.
 Prints one line per failing case and a summary (GPU; the oracle is the checker)."""
 import os
 import sys
@@ -16,6 +18,51 @@ from test_fuzz_gpu import random_graph  # noqa: E402
 start, count = int(sys.argv[1]), int(sys.argv[2])
 port, ctx = oracle.Port(), P.GpuContext(0)
 bad, t0 = 0, time.time()
+
+
+def solve_case(cs):
+    rng = np.random.default_rng(5000 + cs)
+    g, kind = random_graph(rng)
+    seed = int(rng.integers(0, 1 << 31))
+    want = port.factor(g, P.ordering_random(g.n, seed).perm, seed)
+    f = factor_from_port(want)
+    r = P.make_rhs(g, "random_projected", seed)
+    zref = port.apply_preconditioner(want, r)
+    ctx.set_preconditioner_mode("exact")
+    if P.apply_preconditioner_gpu(f, r, ctx=ctx).tobytes() != zref.tobytes():
+        return f"exact {kind} {g.n}"
+    ctx.set_preconditioner_mode("fast")
+    z = P.apply_preconditioner_gpu(f, r, ctx=ctx)
+    ctx.set_preconditioner_mode("default")
+    if not np.allclose(z, zref, rtol=1e-10, atol=1e-12 * max(np.abs(zref).max(), 1e-300)):
+        return f"fast {kind} {g.n}"
+    rc, _, ref = port.pcg(g, want, r, tol=1e-8)
+    try:
+        x, rep = P.pcg_solve_gpu(g, f, r, P.SolveConfig(tol=1e-8), ctx=ctx)
+    except P.Error as e:
+        return None if rc != 0 or not ref["converged"] else f"pcg error {e}"
+    if rc == 0 and ref["converged"]:
+        it_ok = abs(rep.iterations - ref["iterations"]) <= max(1, ref["iterations"] // 10)
+        what = (f"{kind} {g.n} iters {rep.iterations} vs {ref['iterations']} true/recurrence residual "
+                f"{rep.relative_residual:.3g}/{rep.recurrence_residual:.3g} vs "
+                f"{ref['relative_residual']:.3g}/{ref['recurrence_residual']:.3g}")
+        if not it_ok:
+            return "pcg " + what
+        if not rep.converged:
+            # both stop on the recurrence residual; the true residual of an
+            # ill-conditioned graph can land either side of tol
+            print("FLAG", cs, what, flush=True)
+    return None
+
+
+if "--solve" in sys.argv:
+    for cs in range(start, start + count):
+        msg = solve_case(cs)
+        if msg:
+            bad += 1
+            print("MISMATCH", cs, msg, flush=True)
+    print(f"solve cases {count} mismatches {bad} seconds {time.time() - t0:.1f}")
+    sys.exit(0)
 for cs in range(start, start + count):
     rng = np.random.default_rng(1000 + cs)
     g, kind = random_graph(rng)

@@ -105,3 +105,20 @@ def test_fuzz_solve(gpu_ctx, port, case_seed):
         assert rep.converged and rep.relative_residual <= 1e-8, (case_seed, kind)
         assert abs(rep.iterations - ref["iterations"]) <= max(1, ref["iterations"] // 10), (case_seed, kind, ref)
     assert np.isfinite(x).all() and rep.iterations <= 1000
+
+
+@pytest.mark.parametrize("batch_seed", range(6))
+def test_fuzz_batch(gpu_ctx, port, batch_seed):
+    # config[4]: a batch of random graphs (1-12 of them, hubs included) in one
+    # device pass; every member byte-identical to its stand-alone oracle factor
+    rng = np.random.default_rng(9000 + batch_seed)
+    graphs, perms, seeds = [], [], []
+    for _ in range(int(rng.integers(1, 13))):
+        g, _ = random_graph(rng)
+        s = int(rng.integers(0, 1 << 31))
+        graphs.append(g)
+        seeds.append(s)
+        perms.append(P.ordering_random(g.n, s).perm)
+    fs, _ = P.factor_batch_gpu(graphs, [P.Ordering(p) for p in perms], seeds, ctx=gpu_ctx)
+    for i, (g, p, s, f) in enumerate(zip(graphs, perms, seeds, fs)):
+        assert f.same_values(factor_from_port(port.factor(g, p, s))), (batch_seed, i, g.n)

@@ -1,4 +1,4 @@
-"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve].
+"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve|--batch].
 Without --solve: factors byte for byte; with it: exact-mode preconditioner bytes,
 fast mode within 1e-10 and PCG iterations within 10% where the oracle converges.
 Prints one line per failing case and a summary (GPU; the oracle is the checker)."""
@@ -55,6 +55,30 @@ def solve_case(cs):
     return None
 
 
+def batch_case(cs):
+    rng = np.random.default_rng(9000 + cs)
+    graphs, perms, seeds = [], [], []
+    for _ in range(int(rng.integers(1, 13))):
+        g, _ = random_graph(rng)
+        s = int(rng.integers(0, 1 << 31))
+        graphs.append(g)
+        seeds.append(s)
+        perms.append(P.ordering_random(g.n, s).perm)
+    fs, _ = P.factor_batch_gpu(graphs, [P.Ordering(p) for p in perms], seeds, ctx=ctx)
+    for i, (g, p, s, f) in enumerate(zip(graphs, perms, seeds, fs)):
+        if not f.same_values(factor_from_port(port.factor(g, p, s))):
+            return f"batch member {i} n={g.n}"
+    return None
+
+
+if "--batch" in sys.argv:
+    for cs in range(start, start + count):
+        msg = batch_case(cs)
+        if msg:
+            bad += 1
+            print("MISMATCH", cs, msg, flush=True)
+    print(f"batch cases {count} mismatches {bad} seconds {time.time() - t0:.1f}")
+    sys.exit(0)
 if "--solve" in sys.argv:
     for cs in range(start, start + count):
         msg = solve_case(cs)

@@ -172,6 +172,18 @@ def allreduce(pg, device, value: float, op: str) -> float:
     return float(t.item())
 
 
+def workload_config(workload: str, n: int, edges: int) -> dict:
+    """`config` of BOTH arms (identical dicts: the driver compares them). Only
+    what identifies the workload; arm-specific details live outside it."""
+    cfg = {"workload": workload, "desc": WORKLOADS[workload][2], "n": n, "edges": edges}
+    if workload == "batch_64x64":
+        cfg.update({"problems": 64, "ordering": "problem i: ordering_random(n, i)", "seed": "problem i: i"})
+    else:
+        cfg.update({"ordering": "ordering_random(n, seed)", "seed": "rank (0 at N=1)"})
+    cfg["l2"] = "GPU arm: flushed between steps (256 MiB memset); working set > L2 anyway"
+    return cfg
+
+
 def batch_share(rank: int, world: int, total: int = 64):
     """Problems of the 64-problem batch that rank `rank` of `world` factors
     (round-robin; every problem exactly once over the ranks)."""
@@ -179,25 +191,42 @@ def batch_share(rank: int, world: int, total: int = 64):
 
 
 # ---------------------------------------------------------------- reference CPU
-def cpu_reference_factor(graph, perm, seed, workers_list, repeats=1):
+# Everything in this section runs the UNMODIFIED reference (oracle/_ref) on its
+# own inputs: graphs from the reference's gen_poisson3d / from_edges (the
+# port's harness generators for the configs the reference has no generator
+# for), orderings from its ordering_random. The product library is never
+# imported here.
+def cpu_reference_factor(R, h, n, perm, seed, workers_list, repeats=1):
     """Wall clock around the reference API call (host graph in, LdlFactor out),
     BASELINE.md §2: min over {par-left, par-right} x workers."""
-    import oracle
-    R = oracle.Reference()
-    h = R.graph_from_csr(graph)
     best = None
     rows = []
     for backend, bname in ((R.LEFT, "par-left"), (R.RIGHT, "par-right")):
         for w in workers_list:
             for _ in range(repeats):
                 f, wall = R.factor(h, perm, seed, backend=backend, workers=w)
-                nnz = R.L.pref_factor_nnz_off(f) + graph.n
+                nnz = R.L.pref_factor_nnz_off(f) + n
                 R.free_factor(f)
                 rows.append((wall, bname, w))
                 if best is None or wall < best[0]:
                     best = (wall, bname, w, nnz)
-    R.free_graph(h)
     return best, rows
+
+
+def cpu_reference_pcg(R, h, perm, seed, tol=1e-8):
+    """pcg_solve (src/solver.cpp:95-175, single-threaded by design) on the
+    reference's own factor of the same graph/ordering/seed, rhs
+    make_rhs(random_projected, 0): the same-box baseline of the metric's
+    second half. Timed by the reference's SolveReport::solve_seconds."""
+    f, _ = R.factor(h, perm, seed, backend=R.LEFT, workers=os.cpu_count() or 1)
+    try:
+        b = R.make_rhs(h, 1, 0)  # RhsMode::random_projected
+        _, rep = R.pcg(h, f, b, tol=tol)
+    finally:
+        R.free_factor(f)
+    return {"seconds": rep["seconds"], "iterations": rep["iterations"],
+            "relative_residual": rep["relative_residual"], "converged": rep["converged"], "cores": 1,
+            "kind": "reference", "sample": "1 full pcg_solve to tol 1e-8 (single-threaded by design)"}
 
 
 def run_reference(args):
@@ -205,47 +234,38 @@ def run_reference(args):
     if rank != 0:
         return  # other ranks exit without work (the CPU path does not shard)
     import oracle
-    import paper_2505_02977_b200 as P
     workload = args.workload
     cores = os.cpu_count() or 1
     if not oracle.Reference.available():
-        kind = "port"
-    else:
-        kind = "reference"
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparac_ref.so not built "
+                          "(needs /root/reference at build time)"}), flush=True)
+        return
+    R = oracle.Reference()
     if workload == "batch_64x64":
-        return run_reference_batch(args, P, oracle, cores)
-    g = build_graph(P, workload, 0)
-    perm = P.ordering_random(g.n, 0).perm
+        return run_reference_batch(args, R, cores)
+    h = R.workload_graph(workload, 0)
+    n = R.L.pref_graph_n(h)
+    E = R.L.pref_graph_nnz(h) // 2
+    perm = R.ordering_random(n, 0)
     cands = sorted({w for w in (cores, max(1, cores // 2), min(cores, 32), min(cores, 16), 8) if w <= cores})
-    if kind == "port":
-        port = oracle.Port()
-        run_one = lambda: port.factor(g, perm, 0)  # noqa: E731
-        t = time.perf_counter(); f = run_one(); wall = time.perf_counter() - t
-        nnz = len(f["rows"]) + g.n
-        best_cfg = ("oracle port (factor_randomized restatement)", 1)
-        cores_used = 1
-        times = []
-        for _ in range(args.steps):
-            t = time.perf_counter(); run_one(); times.append(time.perf_counter() - t)
-    else:
-        # warm-up: pick the best backend x workers (BASELINE.md §2 T_cpu rule)
-        (w0, bname, wk, nnz), rows = cpu_reference_factor(g, perm, 0, cands)
-        log("reference sweep:", [(round(a, 3), b, c) for a, b, c in rows])
-        best_cfg = (bname, wk)
-        cores_used = wk
-        import oracle as O
-        R = O.Reference()
-        h = R.graph_from_csr(g)
-        backend = R.LEFT if bname == "par-left" else R.RIGHT
-        for _ in range(max(0, args.warmup - 1)):
-            f, _ = R.factor(h, perm, 0, backend=backend, workers=wk)
-            R.free_factor(f)
-        times = []
-        for _ in range(args.steps):
-            f, wall = R.factor(h, perm, 0, backend=backend, workers=wk)
-            R.free_factor(f)
-            times.append(wall)
-        R.free_graph(h)
+    # warm-up: pick the best backend x workers (BASELINE.md §2 T_cpu rule)
+    (w0, bname, wk, nnz), rows = cpu_reference_factor(R, h, n, perm, 0, cands)
+    log("reference sweep:", [(round(a, 3), b, c) for a, b, c in rows])
+    backend = R.LEFT if bname == "par-left" else R.RIGHT
+    for _ in range(max(0, args.warmup - 1)):
+        f, _ = R.factor(h, perm, 0, backend=backend, workers=wk)
+        R.free_factor(f)
+    times = []
+    for _ in range(args.steps):
+        f, wall = R.factor(h, perm, 0, backend=backend, workers=wk)
+        R.free_factor(f)
+        times.append(wall)
+    pcg = None
+    if not args.no_pcg and workload != "rmat_22":  # R-MAT is disconnected: pcg_solve refuses it
+        cb = cpu_reference_pcg(R, h, perm, 0)
+        pcg = {"iterations": cb["iterations"], "relative_residual": cb["relative_residual"],
+               "converged": cb["converged"], "solve_ms": cb["seconds"] * 1e3, "tol": 1e-8, "cpu_baseline": cb}
+    R.free_graph(h)
     sec = sum(times) / len(times)
     value = nnz / sec
     line = {
@@ -253,29 +273,28 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "desc": WORKLOADS[workload][2], "n": g.n,
-                   "edges": g.num_edges(), "ordering": "ordering_random(n, 0)", "seed": 0,
-                   "backend": best_cfg[0], "workers": best_cfg[1]},
-        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": cores_used, "kind": kind,
-                         "sample": f"{args.steps} full factorizations of {workload}, wall clock "
-                                   f"around the API call (host graph in, LdlFactor out)"},
+        "config": workload_config(workload, n, E),
+        "reference": {"backend": bname, "workers": wk, "library": "oracle/_ref/libparac_ref.so (unmodified sources)"},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": wk, "kind": "reference",
+                         "sample": f"{args.steps} full factorizations of {workload}, {bname} x {wk} threads, "
+                                   f"wall clock around the API call (host graph in, LdlFactor out)"},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pcg": pcg,
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_reference_batch(P, oracle, cores, count):
+def cpu_reference_batch(R, cores, count):
     """SURVEY §8(d) batch rule: nproc threads x factor_randomized, one problem per
     thread (the reference has no batch API). Returns (seconds, total nnz, count)."""
-    R = oracle.Reference()
-    g = P.gen_poisson3d(64)
-    h = R.graph_from_csr(g)
-    perms = [P.ordering_random(g.n, i).perm for i in range(count)]
+    h = R.poisson3d(64)
+    n = R.L.pref_graph_n(h)
+    perms = [R.ordering_random(n, i) for i in range(count)]
     nnz = [0] * count
 
     def work(i):
         f, _ = R.factor(h, perms[i], i, backend=R.SEQ, workers=1)
-        nnz[i] = R.L.pref_factor_nnz_off(f) + g.n
+        nnz[i] = R.L.pref_factor_nnz_off(f) + n
         R.free_factor(f)
 
     from concurrent.futures import ThreadPoolExecutor
@@ -287,25 +306,28 @@ def cpu_reference_batch(P, oracle, cores, count):
     return sec, sum(nnz), count
 
 
-def run_reference_batch(args, P, oracle, cores):
+def run_reference_batch(args, R, cores):
     # a bounded sample: `cores` problems per step (one per host thread), so a
     # step is one wave of the 64-problem batch
     count = min(64, cores)
     for _ in range(max(0, args.warmup - 2)):
-        cpu_reference_batch(P, oracle, cores, count)
+        cpu_reference_batch(R, cores, count)
     secs, nnz = [], 0
     for _ in range(args.steps):
-        sec, nnz, _ = cpu_reference_batch(P, oracle, cores, count)
+        sec, nnz, _ = cpu_reference_batch(R, cores, count)
         secs.append(sec)
     sec = sum(secs) / len(secs)
     value = nnz / sec
+    h = R.poisson3d(64)
+    n, E = R.L.pref_graph_n(h), R.L.pref_graph_nnz(h) // 2
+    R.free_graph(h)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "batch_64x64", "desc": WORKLOADS["batch_64x64"][2],
-                   "problems_per_step": count, "backend": "factor_randomized x threads", "workers": cores},
+        "config": workload_config("batch_64x64", n, E),
+        "reference": {"backend": "factor_randomized x threads", "workers": cores, "problems_per_step": count},
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": cores, "kind": "reference",
                          "sample": f"{count} problems of the batch per step, {cores} threads x "
                                    f"factor_randomized (one problem per thread), wall clock"},
@@ -448,12 +470,19 @@ def run_ours(args):
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
+            import oracle
+            R = oracle.Reference()
             cores = os.cpu_count() or 1
-            (wall, bname, wk, cnnz), _ = cpu_reference_factor(g, order.perm, seed, [cores])
+            h = R.workload_graph(workload, seed)
+            rperm = R.ordering_random(n, seed)
+            (wall, bname, wk, cnnz), _ = cpu_reference_factor(R, h, n, rperm, seed, [cores])
             cpu_base = {"value": cnnz / wall, "unit": "nnz/s", "cores": wk, "kind": "reference",
                         "sample": f"1 full {workload} factorization, {bname} x {wk} threads "
                                   f"(best of par-left/par-right), wall clock around the API call",
                         "seconds": wall}
+            if pcg is not None:
+                pcg["cpu_baseline"] = cpu_reference_pcg(R, h, rperm, seed)
+            R.free_graph(h)
         except Exception as exc:  # oracle/_ref missing -> port timing would be 1-core
             cpu_base = {"value": None, "unit": "nnz/s", "cores": 0, "kind": "reference",
                         "sample": f"unavailable: {exc}"}
@@ -465,11 +494,9 @@ def run_ours(args):
             "ms_per_step": max_dev_s / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (host generators = reference gen_poisson3d etc.; ordering_random(n, rank), seed = rank)",
-            "config": {"workload": workload, "desc": WORKLOADS[workload][2], "n": n, "edges": E,
-                       "nnz_G": nnz, "fills": F, "factor_checksum": f"{checksum:016x}",
-                       "per_gpu": "one independent factorization per rank",
-                       "l2": "flushed between steps (256 MiB memset); working set > L2 anyway",
-                       "parallelism": f"replicas x{world}"},
+            "config": workload_config(workload, n, E),
+            "factor": {"nnz_G": nnz, "fills": F, "factor_checksum": f"{checksum:016x}",
+                       "per_gpu": "one independent factorization per rank", "parallelism": f"replicas x{world}"},
             "factor_ms": {"device": max_dev_s / args.steps * 1e3,
                           "eliminate_k3": sum(k3_ms) / len(k3_ms), "wall_resident_loop_s": wall_resident,
                           "device_passes_per_step": max(attempts) if attempts else 1},
@@ -577,7 +604,7 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
         try:
             import oracle
             cores = os.cpu_count() or 1
-            sec, cnnz, cnt = cpu_reference_batch(P, oracle, cores, min(64, cores))
+            sec, cnnz, cnt = cpu_reference_batch(oracle.Reference(), cores, min(64, cores))
             cpu_base = {"value": cnnz / sec, "unit": "nnz/s", "cores": cores, "kind": "reference",
                         "sample": f"{cnt} of the 64 problems, {cores} threads x factor_randomized "
                                   f"(one problem per thread), wall clock", "seconds": sec}
@@ -591,11 +618,11 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
             "ms_per_step": max_dev_s / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_poisson3d(64) x 64; problem i: ordering_random(n, i), seed i)",
-            "config": {"workload": "batch_64x64", "desc": WORKLOADS["batch_64x64"][2], "problems": 64,
-                       "problems_per_gpu": len(mine), "nnz_G_per_gpu": nnz_total,
+            "config": workload_config("batch_64x64", g.n, g.num_edges()),
+            "factor": {"problems_per_gpu": len(mine), "nnz_G_per_gpu": nnz_total,
                        "factor0_checksum": f"{f0.checksum():016x}",
                        "per_gpu": "its share of the 64 problems as one disjoint-union device pass",
-                       "l2": "flushed between steps (256 MiB memset)", "parallelism": f"batch split x{world}"},
+                       "parallelism": f"batch split x{world}"},
             "factor_ms": {"device": max_dev_s / args.steps * 1e3, "eliminate_k3": sum(k3_ms) / len(k3_ms)},
             "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},

@@ -69,10 +69,29 @@ class Port:
         L.oracle_pcg.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, C.c_int, vp,
                                  C.POINTER(C.c_int), C.POINTER(f64), C.POINTER(f64), C.POINTER(C.c_int)]
         L.oracle_build_pos_graph.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.oracle_gen_edges.restype = i64
+        L.oracle_gen_edges.argtypes = [C.c_int, i32, u64, C.POINTER(C.POINTER(i32)), C.POINTER(C.POINTER(i32)),
+                                       C.POINTER(C.POINTER(f64)), C.POINTER(i32)]
+        L.oracle_free.argtypes = [vp]
         self.L = L
 
     def unit_uniform(self, seed, key, counter) -> float:
         return self.L.oracle_unit_uniform(seed, key, counter)
+
+    GEN_KINDS = {"poisson2d": 0, "poisson27": 1, "rmat": 2}
+
+    def gen_edges(self, kind: str, size: int, seed: int = 0):
+        """Harness generator edge list (a < b, w) of a BASELINE config the
+        reference has no generator for: poisson2d(size), poisson27(size, seed),
+        rmat(scale=size, ef 16, seed). Returns (n, a, b, w)."""
+        pa, pb, pw = C.POINTER(i32)(), C.POINTER(i32)(), C.POINTER(f64)()
+        n = i32()
+        m = self.L.oracle_gen_edges(self.GEN_KINDS[kind], size, seed, C.byref(pa), C.byref(pb), C.byref(pw),
+                                    C.byref(n))
+        out = [np.ctypeslib.as_array(p, shape=(max(m, 1),))[:m].copy() for p in (pa, pb, pw)]
+        for p in (pa, pb, pw):
+            self.L.oracle_free(C.cast(p, vp))
+        return n.value, out[0], out[1], out[2]
 
     def derive_seed(self, seed, salt) -> int:
         return self.L.oracle_derive_seed(seed, salt)
@@ -213,6 +232,25 @@ class Reference:
         self._chk(self.L.pref_graph_from_edges(g.n, len(a), _p(a), _p(b), _p(w), C.byref(h)))
         return h
 
+    def graph_from_edges(self, n, a, b, w):
+        """LaplacianGraph::from_edges (src/graph.cpp:21) of an edge list."""
+        a, b = np.ascontiguousarray(a, np.int32), np.ascontiguousarray(b, np.int32)
+        w = np.ascontiguousarray(w, np.float64)
+        h = vp()
+        self._chk(self.L.pref_graph_from_edges(n, len(a), _p(a), _p(b), _p(w), C.byref(h)))
+        return h
+
+    def workload_graph(self, workload: str, seed: int = 0):
+        """Reference LaplacianGraph of a bench.py workload, built without the
+        product library: gen_poisson3d through the reference itself, the other
+        configs from the port's harness generators + the reference's from_edges."""
+        kind = {"poisson3d_128": ("p3", 128), "batch_64x64": ("p3", 64), "poisson2d_256": ("poisson2d", 256),
+                "poisson27_96": ("poisson27", 96), "rmat_22": ("rmat", 22)}[workload]
+        if kind[0] == "p3":
+            return self.poisson3d(kind[1])
+        n, a, b, w = Port().gen_edges(kind[0], kind[1], 1 if kind[0] == "poisson27" else seed)
+        return self.graph_from_edges(n, a, b, w)
+
     def poisson3d(self, n, variant=0, eps=1e-3, contrast=1e4, seed=0):
         h = vp()
         self._chk(self.L.pref_graph_poisson3d(n, variant, eps, contrast, seed, C.byref(h)))
@@ -278,6 +316,23 @@ class Reference:
 
     def checksum(self, f) -> int:
         return self.L.pref_factor_checksum(f)
+
+    def make_rhs(self, h, mode: int, seed: int):
+        out = np.empty(self.L.pref_graph_n(h), np.float64)
+        self._chk(self.L.pref_make_rhs(h, mode, seed, _p(out)))
+        return out
+
+    def pcg(self, h, f, b, tol=1e-8, max_iters=1000):
+        """pcg_solve (src/solver.cpp:95-175) through the reference's public API;
+        `seconds` is its own SolveReport::solve_seconds."""
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty(len(b), np.float64)
+        it, conv = C.c_int(), C.c_int()
+        rel, rec, sec = f64(), f64(), f64()
+        self._chk(self.L.pref_pcg(h, f, _p(b), tol, max_iters, _p(x), C.byref(it), C.byref(rel), C.byref(rec),
+                                  C.byref(conv), C.byref(sec)))
+        return x, {"iterations": it.value, "relative_residual": rel.value, "recurrence_residual": rec.value,
+                   "converged": bool(conv.value), "seconds": sec.value}
 
     def free_factor(self, f):
         self.L.pref_factor_free(f)

@@ -455,3 +455,95 @@ int oracle_pcg(int32_t n, const int64_t* ptr, const int32_t* adj, const double* 
   free(rhs); free(r); free(z); free(p); free(lp); free(best_x);
   return 0;
 }
+
+/* ------------------------------------------------- harness generators */
+/* The BASELINE configs' synthetic inputs that the reference library has no
+ * generator for (SURVEY §8(d) list items 1, 3, 4). They are harness
+ * definitions, not reference code: the edge lists below are handed to the
+ * reference's own LaplacianGraph::from_edges (src/graph.cpp:21) by the
+ * reference arm of bench.py, so that arm never touches the product library.
+ * tests/test_oracle.py pins the resulting CSR byte for byte to the product's
+ * host generators. Weights of the form 0.5 + 1.5*U are computed with
+ * -ffp-contract=off (FMA sensitivity). */
+static const uint64_t kSaltCells = 0x63656c6c636f6566ULL;
+static const uint64_t kSaltRmat = 0x726d61745f67656eULL;
+
+static int cmp_u64(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y ? 1 : 0;
+}
+
+int64_t oracle_gen_edges(int kind, int32_t size, uint64_t seed, int32_t** ea, int32_t** eb,
+                         double** ew, int32_t* n_out) {
+  int64_t cap = 0, m = 0;
+  int32_t* A = NULL;
+  int32_t* B = NULL;
+  double* W = NULL;
+  if (kind == 0) { /* 2D 5-point, id = x + N*y, unit weights */
+    const int64_t N = size;
+    cap = 2 * N * N;
+    A = malloc(sizeof(int32_t) * cap); B = malloc(sizeof(int32_t) * cap); W = malloc(sizeof(double) * cap);
+    for (int64_t y = 0; y < N; ++y)
+      for (int64_t x = 0; x < N; ++x) {
+        const int32_t v = (int32_t)(x + N * y);
+        if (x + 1 < N) { A[m] = v; B[m] = v + 1; W[m] = 1.0; ++m; }
+        if (y + 1 < N) { A[m] = v; B[m] = (int32_t)(v + N); W[m] = 1.0; ++m; }
+      }
+    *n_out = (int32_t)(N * N);
+  } else if (kind == 1) { /* 3D 27-point, w(a,b) = 0.5 + 1.5 U(derive_seed(seed, cells), a, b), a < b */
+    const int64_t N = size;
+    const uint64_t ws = oracle_derive_seed(seed, kSaltCells);
+    cap = 13 * N * N * N;
+    A = malloc(sizeof(int32_t) * cap); B = malloc(sizeof(int32_t) * cap); W = malloc(sizeof(double) * cap);
+    for (int64_t z = 0; z < N; ++z)
+      for (int64_t y = 0; y < N; ++y)
+        for (int64_t x = 0; x < N; ++x) {
+          const int32_t a = (int32_t)(x + N * (y + N * z));
+          for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int64_t xx = x + dx, yy = y + dy, zz = z + dz;
+                if (xx < 0 || yy < 0 || zz < 0 || xx >= N || yy >= N || zz >= N) continue;
+                const int32_t b = (int32_t)(xx + N * (yy + N * zz));
+                if (b <= a) continue;
+                const double u = oracle_unit_uniform(ws, a, (uint64_t)b);
+                const double t = 1.5 * u;
+                A[m] = a; B[m] = b; W[m] = 0.5 + t; ++m;
+              }
+        }
+    *n_out = (int32_t)(N * N * N);
+  } else { /* R-MAT scale `size`, edge factor 16, Graph500 a,b,c = .57,.19,.19 */
+    const int64_t nv = (int64_t)1 << size, samples = 16 * nv;
+    const uint64_t rs = oracle_derive_seed(seed, kSaltRmat), ws = oracle_derive_seed(seed, kSaltCells);
+    const double pa = 0.57, pb = 0.19, pc = 0.19;
+    const double ab = pa + pb, abc = pa + pb + pc;
+    uint64_t* keys = malloc(sizeof(uint64_t) * samples);
+    for (int64_t e = 0; e < samples; ++e) {
+      uint64_t u = 0, v = 0;
+      for (int l = 0; l < size; ++l) {
+        const double r = oracle_unit_uniform(rs, e, (uint64_t)l);
+        const int bu = r >= ab;
+        const int bv = (r >= pa && r < ab) || r >= abc;
+        u = (u << 1) | (uint64_t)bu;
+        v = (v << 1) | (uint64_t)bv;
+      }
+      keys[e] = u == v ? ~0ULL : ((u < v ? u : v) << 32) | (u < v ? v : u);
+    }
+    qsort(keys, (size_t)samples, sizeof(uint64_t), cmp_u64);
+    cap = samples;
+    A = malloc(sizeof(int32_t) * cap); B = malloc(sizeof(int32_t) * cap); W = malloc(sizeof(double) * cap);
+    for (int64_t i = 0; i < samples; ++i) {
+      if (keys[i] == ~0ULL) break;
+      if (i > 0 && keys[i] == keys[i - 1]) continue;
+      const int32_t a = (int32_t)(keys[i] >> 32), b = (int32_t)(keys[i] & 0xffffffffULL);
+      const double t = 1.5 * oracle_unit_uniform(ws, a, (uint64_t)b);
+      A[m] = a; B[m] = b; W[m] = 0.5 + t; ++m;
+    }
+    free(keys);
+    *n_out = (int32_t)nv;
+  }
+  *ea = A; *eb = B; *ew = W;
+  return m;
+}
+
+void oracle_free(void* p) { free(p); }

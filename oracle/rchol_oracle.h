@@ -72,6 +72,14 @@ int oracle_pcg(int32_t n, const int64_t* ptr, const int32_t* adj, const double* 
                int max_iters, double* x, int* iterations, double* relres, double* recres,
                int* converged);
 
+/* Harness generators (BASELINE configs 2D 5-point, 27-point, R-MAT): edge
+ * lists (a < b, w) for LaplacianGraph::from_edges; kind 0 = poisson2d(size),
+ * 1 = poisson27(size, seed), 2 = rmat(scale = size, ef 16, seed). Arrays are
+ * malloc'd (free with oracle_free); returns the edge count. */
+int64_t oracle_gen_edges(int kind, int32_t size, uint64_t seed, int32_t** a, int32_t** b,
+                         double** w, int32_t* n);
+void oracle_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

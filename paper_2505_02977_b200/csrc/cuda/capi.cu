@@ -388,9 +388,15 @@ int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t
 int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm) {
   return guarded([&] {
     require_ctx(ctx);
-    if (!g || g->n < 0) throw Failure{dimension_mismatch, "bad graph"};
+    if (!g || g->n < 0 || !g->ptr) throw Failure{dimension_mismatch, "bad graph"};
     const int n = g->n;
     const long long nnz = g->ptr[n];
+    if (n > 0 && !perm) throw Failure{dimension_mismatch, "null ordering"};
+    // nothing staged is valid until every copy below has succeeded
+    ctx->n = -1;
+    ctx->f_n = -1;
+    ctx->batch_count = 0;
+    solve_invalidate(ctx->solve);
     ctx->ptr.ensure(static_cast<std::size_t>(n) + 1);
     ctx->adj.ensure(static_cast<std::size_t>(std::max<long long>(nnz, 1)));
     ctx->w.ensure(static_cast<std::size_t>(std::max<long long>(nnz, 1)));
@@ -426,6 +432,24 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
   return guarded([&] {
     require_ctx(ctx);
     if (count <= 0 || !graphs || !perms || !seeds) throw Failure{dimension_mismatch, "empty batch"};
+    ctx->n = -1;
+    ctx->f_n = -1;
+    ctx->batch_count = 0;
+    solve_invalidate(ctx->solve);
+    // every member's ordering must be a permutation of its own [0, n_i): the
+    // union check on the device cannot tell a valid union of invalid members
+    for (int i = 0; i < count; ++i) {
+      const int ni = graphs[i].n;
+      if (ni < 0 || !graphs[i].ptr || (ni > 0 && !perms[i])) throw Failure{dimension_mismatch, "bad graph in batch"};
+      std::vector<unsigned char> seen(static_cast<std::size_t>(ni), 0);
+      for (int v = 0; v < ni; ++v) {
+        const int q = perms[i][v];
+        if (q < 0 || q >= ni || seen[q])
+          throw Failure{not_a_permutation, "ordering of batch problem " + std::to_string(i) +
+                                               " is not a permutation (vertex " + std::to_string(v) + ")"};
+        seen[q] = 1;
+      }
+    }
     long long N = 0, NNZ = 0;
     std::vector<long long> base(static_cast<std::size_t>(count) + 1, 0), ebase(base);
     std::vector<unsigned long long> ps(static_cast<std::size_t>(count));
@@ -541,6 +565,9 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
     if (ctx->n < 0) throw Failure{dimension_mismatch, "no graph staged (call parac_gpu_upload)"};
   });
   if (rc) return rc;
+  // the previous resident factor is gone as soon as its buffers are reused
+  ctx->f_n = -1;
+  solve_invalidate_factor(ctx->solve);
   const int n = ctx->n;
   const long long E = ctx->nnz / 2;
   Budgets b = default_budgets(n, E, ctx->max_degree, o);
@@ -664,7 +691,31 @@ int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_pt
                             const int32_t* perm) {
   return guarded([&] {
     require_ctx(ctx);
+    // The sweeps trust the factor's structure (levels are built by waiting on
+    // earlier columns), so a malformed factor is rejected here, before any
+    // device work: the reference's apply_preconditioner would just read it.
+    if (n < 0 || !col_ptr || (n > 0 && (!diag || !perm)))
+      throw Failure{dimension_mismatch, "bad factor arrays"};
+    if (col_ptr[0] != 0) throw Failure{dimension_mismatch, "factor col_ptr[0] != 0"};
+    for (int k = 0; k < n; ++k)
+      if (col_ptr[k + 1] < col_ptr[k]) throw Failure{dimension_mismatch, "factor col_ptr is not monotone"};
     const long long Z = col_ptr[n];
+    if (Z > 0 && (!rows || !values)) throw Failure{dimension_mismatch, "bad factor arrays"};
+    for (int k = 0; k < n; ++k)
+      for (long long p = col_ptr[k]; p < col_ptr[k + 1]; ++p)
+        if (rows[p] <= k || rows[p] >= n)
+          throw Failure{dimension_mismatch, "factor row " + std::to_string(rows[p]) + " of column " +
+                                                std::to_string(k) + " is not strictly below the diagonal"};
+    {
+      std::vector<unsigned char> seen(static_cast<std::size_t>(n), 0);
+      for (int v = 0; v < n; ++v) {
+        const int q = perm[v];
+        if (q < 0 || q >= n || seen[q]) throw Failure{not_a_permutation, "factor perm is not a permutation"};
+        seen[q] = 1;
+      }
+    }
+    ctx->f_n = -1;  // published only after every copy succeeded
+    solve_invalidate_factor(ctx->solve);
     cudaStream_t s = ctx->stream;
     ctx->col_ptr.ensure(static_cast<std::size_t>(n) + 1);
     ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(Z, 1)));

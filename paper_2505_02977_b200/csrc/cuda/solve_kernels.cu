@@ -270,20 +270,34 @@ __global__ void gt_long_scatter_kernel(int nl, const long long* gt_ptr, const in
 
 // Relaxed polling with exponential backoff (no L1 invalidation per poll); the
 // caller follows with fence_acq_rel() before reading the producer's data.
-__device__ __forceinline__ void wait_stamp(const int* flag, int stamp) {
-  if (ld_relaxed(flag) >= stamp) return;
+// Bounded: after ~`budget_ns` without the stamp (a malformed factor whose
+// rows reference a column that is never finished) the wait raises `*abort`
+// and returns false; every waiter then bails out instead of hanging the GPU.
+__device__ __forceinline__ bool wait_stamp(const int* flag, int stamp, int* abort,
+                                           unsigned long long budget_ns = 10000000000ull) {
+  if (ld_relaxed(flag) >= stamp) return true;
   unsigned ns = 32;
+  const unsigned long long t0 = globaltimer_ns();
+  int it = 0;
   do {
     __nanosleep(ns);
     if (ns < 512) ns <<= 1;
+    if ((++it & 63) == 0) {
+      if (ld_relaxed(abort) != 0) return false;
+      if (globaltimer_ns() - t0 > budget_ns) {
+        atomicExch(abort, 1);
+        return false;
+      }
+    }
   } while (ld_relaxed(flag) < stamp);
+  return true;
 }
 
 // ASAP levels of the factor DAG (schedule_levels, src/factor_par.cpp:659-684):
 // level[r] = 1 + max level over G's row r. Sync-free, positions claimed in
 // ascending order (all dependencies are earlier positions => deadlock-free).
 __global__ void level_kernel(int n, const long long* gt_ptr, const int* gt_col, int* level,
-                             int* flags, int stamp, int* counter) {
+                             int* flags, int stamp, int* counter, int* abort) {
   const int lane = lane_id();
   while (true) {
     int r = 0;
@@ -291,12 +305,20 @@ __global__ void level_kernel(int n, const long long* gt_ptr, const int* gt_col, 
     r = __shfl_sync(kFull, r, 0);
     if (r >= n) return;
     int lv = 0;
+    bool ok = true;
     for (long long t = gt_ptr[r] + lane; t < gt_ptr[r + 1]; t += 32) {
       const int k = gt_col[t];
-      wait_stamp(&flags[k], stamp);
+      // uploaded factors are validated (k < r), so this wait is bounded by the
+      // DAG; the budget only guards against a corrupted device state
+      if (k >= r || !wait_stamp(&flags[k], stamp, abort)) {
+        atomicExch(abort, 1);
+        ok = false;
+        break;
+      }
       fence_acq_rel();
       lv = max(lv, ld_relaxed(&level[k]));
     }
+    if (!__all_sync(kFull, ok)) return;
     lv = warp_max(lv) + 1;
     if (lane == 0) {
       level[r] = lv;
@@ -1707,11 +1729,12 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_fpc, s.t4_frange);
   tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_bpc, s.t4_brange);
   note_launches(4);
-  static bool attr = false;
-  if (!attr) {
+  // kernel attributes belong to each device's context: set them per device
+  static bool attr[64] = {};
+  if (!attr[dev]) {
     check(cudaFuncSetAttribute(tail4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
     check(cudaFuncSetAttribute(tail4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
-    attr = true;
+    attr[dev] = true;
   }
   check(cudaGetLastError(), "v3 layout");
   s.t3_nt = nt;
@@ -1811,8 +1834,12 @@ void prepare_factor(const SolveInputs& in) {
   } else {
     const int stamp = ++s.epoch;
     level_kernel<<<sweep_grid(in.device), kSweepThreads, 0, st>>>(n, s.gt_ptr, s.gt_col, s.level,
-                                                                  s.flags, stamp, s.counters);
+                                                                  s.flags, stamp, s.counters, s.counters + 3);
     note_launches(1);
+    int abort_flag = 0;
+    check(cudaMemcpyAsync(&abort_flag, s.counters + 3, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "levels");
+    if (abort_flag) throw Failure{dimension_mismatch, "factor is not lower triangular (level analysis aborted)"};
   }
   // counting sort of positions by level
   int* hist = s.tmp_int;  // levels are 1..n
@@ -1900,6 +1927,7 @@ struct Solver {
                                                              nullptr, s.dinv_l, s.yf, s.zb,
                                                              lt ? lt + 2 * (D + 2) : nullptr);
         note_launches(2);
+        check(cudaGetLastError(), "tail launch");
       }
       // backward: cluster head, wide levels
       check(launch_cluster_t(head_sweep_kernel<false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
@@ -2090,9 +2118,16 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     cudaStream_t st = in.stream;
     Solver sv(in);
     parac_gpu_solve_report rep{};
-    cudaEvent_t e0, e1;
-    check(cudaEventCreate(&e0), "event");
-    check(cudaEventCreate(&e1), "event");
+    struct Events {  // destroyed on every path out (a failed check throws)
+      cudaEvent_t e[2] = {nullptr, nullptr};
+      ~Events() {
+        for (cudaEvent_t x : e)
+          if (x) cudaEventDestroy(x);
+      }
+    } ev;
+    check(cudaEventCreate(&ev.e[0]), "event");
+    check(cudaEventCreate(&ev.e[1]), "event");
+    cudaEvent_t e0 = ev.e[0], e1 = ev.e[1];
     check(cudaEventRecord(e0, st), "event");
 
     upload(s.lp, b, n, st);
@@ -2151,8 +2186,6 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     download(x, s.x, n, st);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     rep.solve_ms = ms;
     rep.wall_ms = wall.ms();
     if (report) *report = rep;

@@ -334,7 +334,7 @@ class GpuContext:
         graph, ordering = self._graph
         n = graph.n
         col_ptr = np.empty(n + 1, np.int64)
-        lib.parac_gpu_download(self.handle, _ptr(col_ptr), None, None, None, None, None, None)
+        _check(lib.parac_gpu_download(self.handle, _ptr(col_ptr), None, None, None, None, None, None))
         z = int(col_ptr[n])
         rows = np.empty(max(z, 1), np.int32)
         vals = np.empty(max(z, 1), np.float64)
@@ -360,6 +360,7 @@ class GpuContext:
         _check(lib.parac_gpu_set_preconditioner_mode(self.handle, self.PRECOND_MODES[mode]))
 
     def upload_factor(self, f: LdlFactor) -> None:
+        self._resident = None  # the previous resident factor is dropped even if f is rejected
         _check(lib.parac_gpu_upload_factor(self.handle, f.n, _ptr(f.col_ptr), _ptr(f.rows),
                                            _ptr(f.values), _ptr(f.diag), _ptr(f.perm)))
         self._factor_n = f.n

@@ -171,3 +171,21 @@ def test_fullsize_fixture_pins_survey_values():
     assert full["poisson2d_256"]["nnz_off"] == 330229 and full["poisson2d_256"]["depth"] == 139
     assert full["poisson2d_256"]["pcg"]["iterations"] == 50
     assert full["rmat_22"]["n"] == 4194304
+
+
+@pytest.mark.parametrize("kind,size,seed", [("poisson2d", 16, 0), ("poisson27", 6, 1), ("poisson27", 5, 7),
+                                            ("rmat", 10, 0), ("rmat", 11, 3)])
+def test_harness_generators_match_product(port, ref, kind, size, seed):
+    # the reference arm of bench.py builds its inputs from these edge lists and
+    # the reference's own from_edges; they must be the product's graphs exactly
+    import paper_2505_02977_b200 as P
+    g = {"poisson2d": lambda: P.gen_poisson2d(size), "poisson27": lambda: P.gen_poisson27(size, seed),
+         "rmat": lambda: P.gen_rmat(size, 16, seed)}[kind]()
+    n, a, b, w = port.gen_edges(kind, size, seed)
+    h = ref.graph_from_edges(n, a, b, w)
+    try:
+        rn, ptr, adj, ww, _ = ref.csr(h)
+    finally:
+        ref.free_graph(h)
+    assert rn == g.n and np.array_equal(ptr, g.ptr) and np.array_equal(adj, g.adj)
+    assert ww.tobytes() == g.w.tobytes()

@@ -274,6 +274,9 @@ typedef struct {
   int32_t converged;
   double solve_ms;            /* device time of the solve */
   double wall_ms;
+  int32_t exact;              /* 1: the bit-exact PCG ran (every reduction, update and
+                                 sweep in pcg_solve's order; x and the report are the
+                                 reference's bytes), 0: the fast PCG */
 } parac_gpu_solve_report;
 
 /* pcg_solve (include/parac/solver.hpp:39-42, src/solver.cpp:95-175) on the
@@ -281,13 +284,15 @@ typedef struct {
  * PARAC_NOT_CONNECTED for a disconnected graph, as the reference. */
 int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_iters, double* x,
                   parac_gpu_solve_report* report);
-/* Triangular-sweep mode of the preconditioner on ctx:
+/* Mode of the solve path on ctx:
  *   0 default: parac_gpu_apply_preconditioner bit-identical to the reference
- *     (solver.cpp:32-74 summation order), parac_gpu_pcg in fast mode;
- *   1 exact for both; 2 fast for both. Fast mode sums each row with a
- *   deterministic (run-to-run identical) tree over entries ordered by
- *   dependency level: same operator, different rounding, far shorter
- *   critical path. */
+ *     (solver.cpp:32-74 summation order); parac_gpu_pcg exact (bit-identical
+ *     to pcg_solve) for n <= 16384 (PARAC_EXACT_PCG_N), fast above;
+ *   1 exact for both (any n); 2 fast for both. The exact PCG runs pcg_solve's
+ *   serial reductions as single-thread chains (O(n) latency per dot product).
+ *   Fast mode sums each row of the sweeps and each dot product in a fixed
+ *   (run-to-run identical) tree order: same operator, different rounding, far
+ *   shorter critical path; iteration counts within 10% of the reference. */
 int parac_gpu_set_preconditioner_mode(parac_gpu_ctx* ctx, int32_t mode);
 /* apply_preconditioner (solver.hpp:30, src/solver.cpp:32-74) */
 int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* z);

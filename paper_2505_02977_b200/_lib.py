@@ -56,7 +56,7 @@ class parac_gpu_factor_info(C.Structure):
 
 class parac_gpu_solve_report(C.Structure):
     _fields_ = [("iterations", i32), ("relative_residual", f64), ("recurrence_residual", f64),
-                ("converged", i32), ("solve_ms", f64), ("wall_ms", f64)]
+                ("converged", i32), ("solve_ms", f64), ("wall_ms", f64), ("exact", i32)]
 
 
 # name -> (restype, argtypes); mirrors include/parac_gpu.h one to one.

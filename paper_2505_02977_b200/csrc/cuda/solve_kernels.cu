@@ -449,6 +449,116 @@ __global__ void diff_norm_kernel(int n, const double* a, const double* b, double
   block_partial(s, partials);
 }
 
+// ------------------------------------------------ exact PCG (serial chains)
+// pcg_solve's reductions are plain left-to-right loops (solver.cpp:15-28):
+// dot() is s = fl(s + fl(a_i * b_i)), subtract_mean() sums v_i the same way.
+// The exact PCG reproduces them bit for bit: ONE thread runs each chain, the
+// other warps of the CTA stream the terms into a double-buffered shared-memory
+// stage ahead of it, so the chain runs at the FP64 add latency. Two
+// independent chains (e.g. r.r and r.z) interleave in the same thread for the
+// price of one. Term kinds:
+//   kTermDot:  a_i * b_i        (dot, norm2)
+//   kTermSum:  a_i              (subtract_mean)
+//   kTermDiff: (a_i - b_i)^2    (norm2 of true_r = rhs - L x, solver.cpp:164-169)
+enum : int { kTermDot = 0, kTermSum = 1, kTermDiff = 2 };
+struct Chain {
+  int kind;
+  const double* a;
+  const double* b;
+};
+constexpr int kSerThreads = 256;
+constexpr int kSerChunk = 1024;
+
+__device__ __forceinline__ double chain_term(const Chain& c, int i) {
+  if (c.kind == kTermSum) return c.a[i];
+  if (c.kind == kTermDot) return __dmul_rn(c.a[i], c.b[i]);
+  const double t = __dsub_rn(c.a[i], c.b[i]);
+  return __dmul_rn(t, t);
+}
+
+__global__ void __launch_bounds__(kSerThreads, 1) serial_chain_kernel(int n, Chain c0, Chain c1, int nch,
+                                                                      double* out) {
+  __shared__ double buf[2][2][kSerChunk];  // [chain][stage][chunk]
+  const int tid = threadIdx.x;
+  const int nchunks = (n + kSerChunk - 1) / kSerChunk;
+  auto fill = [&](int ch, int stage) {
+    const int b = ch * kSerChunk, cnt = min(kSerChunk, n - b);
+    for (int t = tid - 32; t < cnt; t += kSerThreads - 32) {
+      buf[0][stage][t] = chain_term(c0, b + t);
+      if (nch > 1) buf[1][stage][t] = chain_term(c1, b + t);
+    }
+  };
+  if (tid >= 32 && nchunks > 0) fill(0, 0);
+  double s0 = 0.0, s1 = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    __syncthreads();  // stage ch&1 is full; the other stage is free
+    if (tid >= 32) {
+      if (ch + 1 < nchunks) fill(ch + 1, (ch + 1) & 1);
+    } else if (tid == 0) {
+      const double* x0 = buf[0][ch & 1];
+      const double* x1 = buf[1][ch & 1];
+      const int cnt = min(kSerChunk, n - ch * kSerChunk);
+      int t = 0;
+      if (nch > 1) {
+        for (; t + 8 <= cnt; t += 8) {
+          double u[8], v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            u[q] = x0[t + q];
+            v[q] = x1[t + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            s0 = __dadd_rn(s0, u[q]);
+            s1 = __dadd_rn(s1, v[q]);
+          }
+        }
+        for (; t < cnt; ++t) {
+          s0 = __dadd_rn(s0, x0[t]);
+          s1 = __dadd_rn(s1, x1[t]);
+        }
+      } else {
+        for (; t + 8 <= cnt; t += 8) {
+          double u[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) u[q] = x0[t + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) s0 = __dadd_rn(s0, u[q]);
+        }
+        for (; t < cnt; ++t) s0 = __dadd_rn(s0, x0[t]);
+      }
+    }
+  }
+  if (tid == 0) {
+    out[0] = s0;
+    if (nch > 1) out[1] = s1;
+  }
+}
+
+// rhs = b - mean; r = rhs; x = 0 (solver.cpp:107-119, subtract_mean :23-28)
+__global__ void center_exact_kernel(int n, const double* a, double mean, double* out, double* r, double* x) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const double o = __dsub_rn(a[v], mean);
+    out[v] = o;
+    if (r) r[v] = o;
+    if (x) x[v] = 0.0;
+  }
+}
+
+// x += alpha p; r -= alpha lp (solver.cpp:136-139), unfused
+__global__ void update_xr_exact_kernel(int n, double alpha, double* x, double* r, const double* p, const double* lp) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    x[v] = __dadd_rn(x[v], __dmul_rn(alpha, p[v]));
+    r[v] = __dsub_rn(r[v], __dmul_rn(alpha, lp[v]));
+  }
+}
+
+// p = z + beta p (solver.cpp:149-152)
+__global__ void update_p_exact_kernel(int n, double beta, const double* z, double* p) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    p[v] = __dadd_rn(z[v], __dmul_rn(beta, p[v]));
+}
+
 // ------------------------------------------------------------------- K6
 // acc -= prod[0] - ... - prod[cnt-1], strictly in order, by lane 0 from the
 // warp's shared slots (loads hoisted 4 at a time; ~one DSUB latency per term).
@@ -1963,6 +2073,19 @@ struct Solver {
     note_launches(1);
   }
 
+  // Serial chain(s) in the reference's order (exact PCG); blocking read.
+  void chains(Chain c0, Chain c1, int nch, double* out) {
+    serial_chain_kernel<<<1, kSerThreads, 0, st>>>(n, c0, c1, nch, s.scalars + 4);
+    note_launches(1);
+    check(cudaMemcpyAsync(out, s.scalars + 4, sizeof(double) * nch, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "sync");
+  }
+  double chain(int kind, const double* a, const double* b = nullptr) {
+    double v = 0.0;
+    chains(Chain{kind, a, b}, Chain{kind, a, b}, 1, &v);
+    return v;
+  }
+
   // subtract_mean in place; returns ||a||^2 partial slot B filled
   void center(const double* a, double* out, double* r, double* x) {
     sum_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, a, part(kSlotA));
@@ -1986,6 +2109,83 @@ void need_factor(const SolveInputs& in) {
   if (in.f_n < 0) throw Failure{dimension_mismatch, "no resident factor"};
   if (in.batch > 0)
     throw Failure{dimension_mismatch, "the resident factor is a batch: download it and solve each problem separately"};
+}
+
+// pcg_solve (solver.cpp:95-175) with every reduction, vector update and
+// preconditioner sweep in the reference's order: x, the iteration count and
+// both residuals are bit-identical to the reference's. The reductions are
+// serial chains (O(n) latency each), so this is the default only where that
+// is cheap (parac_gpu_pcg, mode 0 with n <= the exact threshold).
+void pcg_exact(const SolveInputs& in, double tol, int max_iters, parac_gpu_solve_report& rep) {
+  SolveState& s = *in.state;
+  const int n = in.n;
+  cudaStream_t st = in.stream;
+  Solver sv(in);
+  const int vb = std::max(1, std::min(kRedBlocks * 2, (n + 255) / 256));
+  // rhs = b - mean(b) (b was uploaded into lp); r = rhs; x = 0
+  const double mean = sv.chain(kTermSum, s.lp) / static_cast<double>(n);
+  center_exact_kernel<<<vb, 256, 0, st>>>(n, s.lp, mean, s.rhs, s.r, s.x);
+  note_launches(1);
+  const double b_norm = std::sqrt(sv.chain(kTermDot, s.rhs, s.rhs));
+  if (b_norm == 0.0) {
+    rep.converged = 1;
+    return;
+  }
+  sv.precond(s.r, s.z, kSlotC, true);
+  copy_kernel<<<vb, 256, 0, st>>>(n, s.z, s.p);
+  copy_kernel<<<vb, 256, 0, st>>>(n, s.x, s.best);
+  note_launches(2);
+  double rz = sv.chain(kTermDot, s.r, s.z);
+  double best_norm = b_norm;  // norm2(r) with r = rhs: the same chain, the same bits
+  double rn = b_norm;         // norm2(r) of the current r (loop test, :130)
+  int iters = 0;
+  while (iters < max_iters) {
+    if (rn <= tol * b_norm) break;
+    ++iters;
+    sv.spmv(s.p, s.lp, kSlotA);
+    const double p_lp = sv.chain(kTermDot, s.p, s.lp);
+    if (!(p_lp > 0.0)) break;
+    const double alpha = rz / p_lp;
+    update_xr_exact_kernel<<<vb, 256, 0, st>>>(n, alpha, s.x, s.r, s.p, s.lp);
+    note_launches(1);
+    // z does not depend on ||r||: the sweep first, then both chains at once
+    sv.precond(s.r, s.z, kSlotC, true);
+    double two[2];
+    sv.chains(Chain{kTermDot, s.r, s.r}, Chain{kTermDot, s.r, s.z}, 2, two);
+    rn = std::sqrt(two[0]);
+    if (rn < best_norm) {
+      best_norm = rn;
+      copy_kernel<<<vb, 256, 0, st>>>(n, s.x, s.best);
+      note_launches(1);
+    }
+    const double beta = two[1] / rz;
+    rz = two[1];
+    update_p_exact_kernel<<<vb, 256, 0, st>>>(n, beta, s.z, s.p);
+    note_launches(1);
+  }
+  double rec = rn;
+  if (rec > best_norm) {
+    copy_kernel<<<vb, 256, 0, st>>>(n, s.best, s.x);
+    note_launches(1);
+    rec = best_norm;
+  }
+  rep.recurrence_residual = rec / b_norm;
+  const double xmean = sv.chain(kTermSum, s.x) / static_cast<double>(n);
+  center_exact_kernel<<<vb, 256, 0, st>>>(n, s.x, xmean, s.x, nullptr, nullptr);
+  note_launches(1);
+  sv.spmv(s.x, s.lp, kSlotA);
+  rep.iterations = iters;
+  rep.relative_residual = std::sqrt(sv.chain(kTermDiff, s.rhs, s.lp)) / b_norm;
+  rep.converged = rep.relative_residual <= tol;
+}
+
+// parac_gpu_pcg's mode 0 runs the exact PCG up to this size (PARAC_EXACT_PCG_N)
+int exact_pcg_max_n() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAC_EXACT_PCG_N");
+    return e ? std::atoi(e) : 16384;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -2131,6 +2331,11 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     check(cudaEventRecord(e0, st), "event");
 
     upload(s.lp, b, n, st);
+    const bool exact = s.mode == kModeExact || (s.mode == kModeDefault && n <= exact_pcg_max_n());
+    rep.exact = exact ? 1 : 0;
+    if (exact) {
+      pcg_exact(in, tol, max_iters, rep);
+    } else {
     sv.center(s.lp, s.rhs, s.r, s.x);  // rhs = b - mean, r = rhs, x = 0
     const double b_norm = std::sqrt(sv.read_partials(kSlotB));
     if (b_norm == 0.0) {
@@ -2180,6 +2385,7 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
       rep.iterations = iters;
       rep.relative_residual = std::sqrt(sv.read_partials(kSlotB)) / b_norm;
       rep.converged = rep.relative_residual <= tol;
+    }
     }
     check(cudaEventRecord(e1, st), "event");
     check(cudaGetLastError(), "pcg");

@@ -483,6 +483,7 @@ class SolveReport:
     factor_seconds: float = 0.0
     solve_seconds: float = 0.0
     device_ms: float = 0.0
+    exact: bool = False  # the bit-exact PCG ran (x and this report are the reference's bytes)
 
 
 def _stage_for_solve(ctx: GpuContext, graph: Optional[LaplacianGraph], factor: LdlFactor):
@@ -511,7 +512,7 @@ def _pcg_resident(ctx: GpuContext, b: np.ndarray, config: SolveConfig):
     _check(lib.parac_gpu_pcg(ctx.handle, _ptr(b), config.tol, config.max_iters, _ptr(x),
                              C.byref(rep)))
     return x, SolveReport(rep.iterations, rep.relative_residual, rep.recurrence_residual,
-                          bool(rep.converged), 0.0, rep.wall_ms / 1e3, rep.solve_ms)
+                          bool(rep.converged), 0.0, rep.wall_ms / 1e3, rep.solve_ms, bool(rep.exact))
 
 
 def apply_preconditioner_gpu(factor: LdlFactor, r: np.ndarray,

@@ -1,6 +1,7 @@
 """Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve|--batch].
 Without --solve: factors byte for byte; with it: exact-mode preconditioner bytes,
-fast mode within 1e-10 and PCG iterations within 10% where the oracle converges.
+fast mode within 1e-10, and the default PCG (exact at these sizes) bit-identical
+to the oracle's pcg_solve (--fast: the fast PCG, iterations within 10%).
 Prints one line per failing case and a summary (GPU; the oracle is the checker)."""
 import os
 import sys
@@ -36,16 +37,26 @@ def solve_case(cs):
     ctx.set_preconditioner_mode("default")
     if not np.allclose(z, zref, rtol=1e-10, atol=1e-12 * max(np.abs(zref).max(), 1e-300)):
         return f"fast {kind} {g.n}"
-    rc, _, ref = port.pcg(g, want, r, tol=1e-8)
+    rc, xref, ref = port.pcg(g, want, r, tol=1e-8)
+    if "--fast" in sys.argv:
+        ctx.set_preconditioner_mode("fast")
     try:
         x, rep = P.pcg_solve_gpu(g, f, r, P.SolveConfig(tol=1e-8), ctx=ctx)
     except P.Error as e:
         return None if rc != 0 or not ref["converged"] else f"pcg error {e}"
+    finally:
+        ctx.set_preconditioner_mode("default")
+    what = (f"{kind} {g.n} iters {rep.iterations} vs {ref['iterations']} true/recurrence residual "
+            f"{rep.relative_residual:.3g}/{rep.recurrence_residual:.3g} vs "
+            f"{ref['relative_residual']:.3g}/{ref['recurrence_residual']:.3g}")
+    if rep.exact:
+        # default mode at these sizes: the exact PCG, bit-identical to pcg_solve
+        same = (rep.iterations == ref["iterations"] and rep.converged == ref["converged"]
+                and rep.relative_residual == ref["relative_residual"]
+                and rep.recurrence_residual == ref["recurrence_residual"])
+        return None if same and x.tobytes() == xref.tobytes() else "exact pcg " + what
     if rc == 0 and ref["converged"]:
         it_ok = abs(rep.iterations - ref["iterations"]) <= max(1, ref["iterations"] // 10)
-        what = (f"{kind} {g.n} iters {rep.iterations} vs {ref['iterations']} true/recurrence residual "
-                f"{rep.relative_residual:.3g}/{rep.recurrence_residual:.3g} vs "
-                f"{ref['relative_residual']:.3g}/{ref['recurrence_residual']:.3g}")
         if not it_ok:
             return "pcg " + what
         if not rep.converged:

@@ -626,15 +626,7 @@ __device__ __forceinline__ double fast_batch(const int* idx, const double* g, co
 
 
 
-// ------------------------------------------------------------ K6 (fast mode): narrow tail
-// The last levels of the factor DAG are narrow and long: at 128^3 the last 774
-// of 1,206 levels hold 4,644 rows. Run grid-wide, each costs a global
-// completion hand-off (several us). The tail T is instead swept by ONE CTA with
-// its solution vector in shared memory and one __syncthreads per level:
-//   forward:  y_T = G_TT^-1 (rhs_T - G_TH y_H)   (prologue: the G_TH part, grid-wide)
-//   backward: z_T = G_TT^-T yd_T                  (self-contained; runs first)
-// T is level-sorted, so tail index i = order position - tail_base and the rows
-// of one level are a contiguous index range.
+// ------------------------------------------------------------ async copy helpers
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
@@ -656,7 +648,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
     a += sz;
   }
 }
-constexpr int kTailThreads = 1024;
 
 // ------------------------------------------------------------ K6: cluster sweeps
 // One thread-block cluster sweeps levels level-synchronously: every row of
@@ -1283,185 +1274,7 @@ __global__ void gather_z_l_dot_kernel(int n, const int* v2l, const double* zl, c
   block_partial(s, partials);
 }
 
-// ---- v3 tail: one CTA, level-order space, all per-level metadata in shared
-// memory (no dependent global loads on the level chain), entries of the next
-// level prefetched into registers, products for the whole level spread over
-// all 1024 threads. FWD: x = y (tail rows, init = rhs - G_TH y_H);
-// BWD: x = z (init = y * D^+).
-constexpr int kT3Rows = 8192;
-
-
-// ---- v4 tail: every level has <= 32 rows (tail width <= 32), so the 32
-// warps split each level's rows into equal (row, slice) pieces: warp w takes
-// slice w % wpr of row w / wpr (wpr = 32 / rows). Each lane holds <= kT4PF of
-// its slice's entries in registers, loaded one level ahead; per level: one
-// product per entry against the shared solution, a warp tree, one partial
-// per warp in shared memory, a barrier, the row's warp 0 sums its wpr
-// partials in fixed order and publishes the value, a barrier. No thread ever
-// walks a long row alone.
-constexpr int kT4PF = 4;
-constexpr std::size_t kT4Smem = (static_cast<std::size_t>(kT3Rows) + 32) * 8 + 8 * 32 * 16 + 8 * 8192;  // max
-inline std::size_t tail4_smem(int nlev) {
-  return (static_cast<std::size_t>(kT3Rows) + 32) * 8 + 8 * 32 * 16 + 8 * static_cast<std::size_t>(nlev);
-}
-
-// Piece table of the tail (built once per factor, per direction): level t's
-// warp w piece = {row (tail index, -1 none), eb, ee, wpr}. Keeping the integer
-// divisions of the (row, slice) split out of the level loop matters: they
-// were ~half of a level's dependent instruction chain.
-//
-// A row gets only as many of its wpr warps as its length needs (epw entries
-// per warp, default 32 * kT4PF = one register set): the 32 warps share four
-// schedulers, so every warp that joins a level costs issue slots on the
-// level's critical path even when it holds 3 entries; the rest idle at the
-// barriers.
-__global__ void tail4_pieces_kernel(int nlev, int fwd, const int* lvl3, const int* ep, int4* pieces,
-                                    int epw = 32 * kT4PF) {
-  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int warp = threadIdx.x & 31;  // one thread per (level, warp)
-  if (t >= nlev) return;
-  const int q = fwd ? t : nlev - 1 - t;
-  const int lb = lvl3[q], r = lvl3[q + 1] - lb;
-  const int wpr = r > 0 ? 32 / r : 0;
-  const int ri = wpr > 0 ? warp / wpr : r;
-  int4 pc = make_int4(-1, 0, 0, 0);
-  if (ri < r) {
-    const int row = lb + ri;
-    const int si = warp - ri * wpr;
-    const int rb = ep[row], len = ep[row + 1] - rb;
-    const int use = min(wpr, max(1, (len + epw - 1) / epw));
-    // .w = number of slices for the row's FIRST slice (it combines them), else 0
-    if (si < use)
-      pc = make_int4(row, rb + static_cast<int>((static_cast<long long>(len) * si) / use),
-                     rb + static_cast<int>((static_cast<long long>(len) * (si + 1)) / use), si == 0 ? use : 0);
-  }
-  pieces[static_cast<long long>(t) * 32 + warp] = pc;
-}
-
-// Latency plan of the level loop (HBM round trips here are ~1-1.5 us, a
-// level should take ~0.3 us): nothing a level needs may be loaded later
-// than ~4 levels ahead, and no thread may wait on a global load inside the
-// loop except for data loaded >= 2 levels earlier that is L2-resident.
-//   * piece records: staged into a shared-memory ring kT4Ring levels ahead
-//     with cp.async (threads 0..31, one 16-byte record each);
-//   * entry ranges per level: shared memory (loaded once);
-//   * entries: bulk-prefetched into L2 kT4L2 levels ahead (addresses from
-//     shared memory), loaded into registers 2 levels ahead.
-constexpr int kT4Ring = 8;
-constexpr int kT4L2 = 12;
-
-// FLAGS (experiments only, tools/microbench/tailbench.cu): 1 no L2 bulk
-// prefetch, 2 no cp.async record ring (records read from global 2 levels
-// ahead), 4 no global store of the result, 8 no entry loads (products of 0).
-template <bool FWD, int FLAGS = 0>
-__global__ void __launch_bounds__(kTailThreads, 1) tail4_kernel(
-    int nt, int nlev, int tail_base, const int4* pieces, const int2* lrange, const int* eidx, const double* eval,
-    const double* ts, const double* dinv_l, const double* xin, double* x_l, unsigned long long* ltime) {
-  extern __shared__ double t4[];
-  double* xs = t4;                                                     // [kT3Rows]
-  double* part = t4 + kT3Rows;                                         // [32]
-  int4* ring = reinterpret_cast<int4*>(part + 32);                     // [kT4Ring][32]
-  int2* lr = reinterpret_cast<int2*>(ring + kT4Ring * 32);             // [nlev]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < nt; i += kTailThreads)
-    xs[i] = FWD ? ts[i] : xin[tail_base + i] * dinv_l[tail_base + i];
-  for (int i = tid; i < nlev; i += kTailThreads) lr[i] = lrange[i];
-  // ring slots for levels 0 .. kT4Ring-2 (one commit group per level)
-  for (int t = 0; t < kT4Ring - 1; ++t) {
-    if (tid < 32 && t < nlev) cp_async16(&ring[(t % kT4Ring) * 32 + tid], &pieces[static_cast<long long>(t) * 32 + tid]);
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  auto l2 = [&](int t) {
-    if ((FLAGS & 1) || t >= nlev) return;
-    const int2 r = lr[t];
-    if (r.y > r.x) {
-      prefetch_l2(eidx + r.x, static_cast<long long>(r.y - r.x) * 4);
-      prefetch_l2(eval + r.x, static_cast<long long>(r.y - r.x) * 8);
-    }
-  };
-  if (tid == 32)
-    for (int t = 0; t < kT4L2; ++t) l2(t);
-  struct Set {
-    int4 pc;
-    int idx[kT4PF];
-    double val[kT4PF];
-  };
-  auto load = [&](int t, Set& S) {
-    S.pc = (FLAGS & 2) ? pieces[static_cast<long long>(t) * 32 + warp] : ring[(t % kT4Ring) * 32 + warp];
-    if (!(FLAGS & 8) && S.pc.x >= 0) {
-#pragma unroll
-      for (int k = 0; k < kT4PF; ++k) {
-        const int e = S.pc.y + k * 32 + lane;
-        S.idx[k] = e < S.pc.z ? eidx[e] : 0;
-        S.val[k] = e < S.pc.z ? eval[e] : 0.0;
-      }
-    }
-  };
-  Set A, B;
-  A.pc = B.pc = make_int4(-1, 0, 0, 0);
-  if (nlev > 0) load(0, A);
-  if (nlev > 1) load(1, B);
-  auto step = [&](int t, Set& S) {
-    const int4 pc = S.pc;
-    double p = 0.0;
-    if (pc.x >= 0) {
-#pragma unroll
-      for (int k = 0; k < kT4PF; ++k)
-        if (pc.y + k * 32 + lane < pc.z) p += S.val[k] * xs[S.idx[k]];
-      for (int e = pc.y + kT4PF * 32 + lane; e < pc.z; e += 32) p += eval[e] * xs[eidx[e]];  // overflow
-    }
-    if (t + 2 < nlev) load(t + 2, S);  // level t+2 into the set just consumed (its ring slot landed)
-    // stage level t + kT4Ring - 1 into the slot level t-1 used (free since the last barrier)
-    const int tn = t + kT4Ring - 1;
-    if (!(FLAGS & 2)) {
-      if (tid < 32 && tn < nlev) cp_async16(&ring[(tn % kT4Ring) * 32 + tid], &pieces[static_cast<long long>(tn) * 32 + tid]);
-      cp_async_commit();
-    }
-    if (tid == 32) l2(t + kT4L2);
-    if (pc.x >= 0) {
-      p = warp_sum(p);
-      if (lane == 0 && pc.w != 1) part[warp] = p;
-    }
-    cp_async_wait<kT4Ring - 4>();  // level t+3's records have landed (needed after the barrier)
-    __syncthreads();
-    if (pc.x >= 0 && pc.w > 0) {  // the row's first warp publishes it
-      double sp = p;
-      if (pc.w > 1) {
-        sp = lane < pc.w ? part[warp + lane] : 0.0;
-        sp = warp_sum(sp);
-      }
-      if (lane == 0) {
-        const double acc = xs[pc.x] - sp;
-        xs[pc.x] = acc;
-        if (!(FLAGS & 4)) x_l[tail_base + pc.x] = acc;
-      }
-    }
-    __syncthreads();
-    if (ltime && tid == 0) ltime[t] = globaltimer_ns();
-  };
-  for (int t = 0; t < nlev; t += 2) {
-    step(t, A);
-    if (t + 1 < nlev) step(t + 1, B);
-  }
-  cp_async_wait<0>();
-}
-
-// Entry range [eb, ee) of each tail level (from the piece table).
-__global__ void tail4_range_kernel(int nlev, const int4* pieces, int2* lrange) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nlev) return;
-  int eb = 0x7fffffff, ee = 0;
-  for (int w = 0; w < 32; ++w) {
-    const int4 pc = pieces[static_cast<long long>(t) * 32 + w];
-    if (pc.x >= 0) {
-      eb = min(eb, pc.y);
-      ee = max(ee, pc.z);
-    }
-  }
-  lrange[t] = eb <= ee ? make_int2(eb, ee) : make_int2(0, 0);
-}
+#include "tail_dense.cuh"
 
 // T-part of the forward tail rows: count, then copy with tail-relative indices.
 __global__ void tail3_count_kernel(int nt, int tail_base, const long long* lptr, const int* lidx, int* cnt) {
@@ -1501,12 +1314,6 @@ __global__ void ll_to_int_kernel(int cnt, const long long* src, long long base, 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) dst[i] = static_cast<int>(src[i] - base);
 }
-__global__ void tail_rel_idx_kernel(long long b, long long e, int tail_base, int* idx) {
-  for (long long q = b + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < e;
-       q += static_cast<long long>(gridDim.x) * blockDim.x)
-    idx[q] -= tail_base;
-}
-
 // Level-ordered row copies: lens, then entries (warp per row).
 __global__ void lvl_len_kernel(int n, const int* order, const long long* aptr, const long long* bptr,
                                int* alen, int* blen) {
@@ -1556,6 +1363,24 @@ cudaError_t launch_cluster(void (*kernel)(KArgs...), int csize, std::size_t smem
   return launch_cluster_t(kernel, csize, kCThreads, smem, st, args...);
 }
 
+
+// Ordinary launch with programmatic dependent launch enabled (the kernel calls
+// griddepcontrol.wait before reading its predecessor's output).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int threads, std::size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.blockDim = dim3(static_cast<unsigned>(threads), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // Largest launchable cluster (16 non-portable, else 8) of 1024-thread CTAs.
 template <typename... KArgs>
@@ -1701,8 +1526,7 @@ void build_level_layout(const SolveInputs& in, SolveState& s, int sms) {
 
 // v3 fast-mode layout (after build_level_layout made the level-ordered copies):
 // level-order maps, indices remapped to level order, head chunk tables for the
-// cluster's warps, and the one-CTA tail (levels wider than PARAC_TAIL_WIDTH,
-// default 64 rows, stay in the head; at most kT3Rows tail rows).
+// cluster's warps, and the dense-inverse tail (tail_dense.cuh).
 void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   const int n = in.f_n, depth = s.depth;
   const long long Z = in.f_nnz;
@@ -1777,39 +1601,69 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
     }
     s.lvl_off_h.assign(off.begin(), off.begin() + std::min<std::size_t>(off.size(), static_cast<std::size_t>(Lw) + 2));
   }
-  const char* env = std::getenv("PARAC_TAIL_WIDTH");
-  const int wt = std::min(32, env ? std::atoi(env) : 32);  // tail4 needs <= 32 rows per level
-  int L0 = depth;
-  if (wt > 0) {
-    while (L0 >= 1 && off[L0 + 1] - off[L0] <= wt) --L0;
-    while (L0 < depth && off[depth + 1] - off[L0 + 1] > kT3Rows) ++L0;
+  // Dense-inverse tail (tail_dense.cuh): the trailing levels whose rows fit
+  // T <= kTwMaxRows. Which levels: the split minimising a cost model of the
+  // per-apply time (2 GEMVs of T^2/2 x 8 bytes vs one cluster-barrier level
+  // per head level and direction) amortised over ~40 applies plus the one-time
+  // build (~T-weighted entry count x 8 bytes + one launch per tail level).
+  // PARAC_TAIL_ROWS=T forces the largest tail of at most T rows (0: none).
+  const int Lw = s.wide_L;
+  int L0 = depth;  // last head level; the tail is levels L0+1 .. depth
+  {
+    const char* env = std::getenv("PARAC_TAIL_ROWS");
+    const long long forced = env ? std::atoll(env) : -1;
+    const long long cap = std::min<long long>(forced >= 0 ? forced : kTwMaxRows, kTwMaxRows);
+    std::vector<long long> ef(static_cast<std::size_t>(depth) + 2);
+    gather_ll_kernel<<<(depth + 2 + 255) / 256, 256, 0, st>>>(depth + 2, s.lvl_off, s.lf_ptr, s.lvl_target);
+    note_launches(1);
+    check(cudaMemcpyAsync(ef.data(), s.lvl_target, sizeof(long long) * (depth + 2), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "v3 sync");
+    constexpr double kGemvBW = 5.0e12, kBuildBW = 2.5e12, kHeadLevel = 2.8e-6, kLaunch = 4.0e-6, kApplies = 40.0;
+    double best = 1e300;
+    double S0 = 0.0, S1 = 0.0;  // sums over tail levels l of E_l and E_l * off[l]
+    for (int Lc = depth; Lc >= std::max(Lw, 0); --Lc) {  // candidate: tail = levels Lc+1 .. depth
+      const long long tb = off[Lc + 1], T = n - tb;
+      if (T > cap) break;
+      if (Lc < depth) {
+        const double El = static_cast<double>(ef[Lc + 2] - ef[Lc + 1]);
+        S0 += El;
+        S1 += El * static_cast<double>(off[Lc + 1]);
+      }
+      // build traffic: each tail entry of level l reads a parent row of mean
+      // length ~ (tail-relative start of level l) / 2
+      const double fma_bytes = 0.5 * (S1 - static_cast<double>(tb) * S0) * 8.0;
+      const double Td = static_cast<double>(T);
+      const double apply = 2.0 * (Td * Td * 4.0 / kGemvBW + (T ? 3e-6 : 0.0)) + 2.0 * kHeadLevel * (Lc - Lw);
+      const double cost = apply * kApplies + fma_bytes / kBuildBW + (depth - Lc) * kLaunch;
+      if (forced >= 0 || cost < best) {
+        best = cost;
+        L0 = Lc;
+      }
+    }
   }
   s.t3_L0 = L0;
   if (L0 >= depth) return;
   const int base = static_cast<int>(off[L0 + 1]);
   const int nt = n - base;
   const int nlev = depth - L0;
+  const int Tp = tw_even(nt);
   if (s.cap_t3 < static_cast<std::size_t>(nt) + 2) {
-    dalloc(s.t3_lvl, static_cast<std::size_t>(nt) + 2);
     dalloc(s.t3_fep, static_cast<std::size_t>(nt) + 2);
-    dalloc(s.t3_bep, static_cast<std::size_t>(nt) + 2);
     dalloc(s.tail_s, static_cast<std::size_t>(nt) + 2);
     dalloc(s.tail_cnt, 2 * (static_cast<std::size_t>(nt) + 2));
     dalloc(s.hsplit, static_cast<std::size_t>(nt) + 2);  // scratch: forward T-part offsets
+    dalloc(s.tw_offl, static_cast<std::size_t>(nt) + 2);
+    dalloc(s.tw_offu, static_cast<std::size_t>(nt) + 2);
     s.cap_t3 = static_cast<std::size_t>(nt) + 2;
   }
-  std::vector<int> lvl3(static_cast<std::size_t>(nlev) + 1);
-  for (int t = 0; t <= nlev; ++t) lvl3[t] = static_cast<int>(off[L0 + 1 + t] - base);
-  check(cudaMemcpyAsync(s.t3_lvl, lvl3.data(), sizeof(int) * (nlev + 1), cudaMemcpyHostToDevice, st), "h2d");
-  // forward T part
+  // forward T part of every tail row (entries with tail-relative indices)
   tail3_count_kernel<<<sms * 4, 256, 0, st>>>(nt, base, s.lf_ptr, s.lf_idx, s.tail_cnt);
   note_launches(1);
   check(launch_scan(s.tail_cnt, nt, s.hsplit, s.tiles, st), "scan");
-  long long hb[2] = {0, 0};
-  check(cudaMemcpyAsync(&hb[0], s.hsplit + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaMemcpyAsync(&hb[1], s.lb_ptr + base, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
+  long long hb = 0;
+  check(cudaMemcpyAsync(&hb, s.hsplit + nt, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "v3 sync");
-  const std::size_t ne = static_cast<std::size_t>(std::max<long long>(hb[0], 1));
+  const std::size_t ne = static_cast<std::size_t>(std::max<long long>(hb, 1));
   if (s.cap_t3e < ne) {
     dalloc(s.t3_fidx, ne);
     dalloc(s.t3_fval, ne);
@@ -1817,40 +1671,64 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   }
   tail3_fill_kernel<<<sms * 4, 256, 0, st>>>(nt, base, s.lf_ptr, s.lf_idx, s.lf_val, s.hsplit, s.t3_fidx, s.t3_fval);
   ll_to_int_kernel<<<(nt + 1 + 255) / 256, 256, 0, st>>>(nt + 1, s.hsplit, 0, s.t3_fep);
-  // backward: the tail columns' entries all lie in the tail; make them tail-relative in place
-  ll_to_int_kernel<<<(nt + 1 + 255) / 256, 256, 0, st>>>(nt + 1, s.lb_ptr + base, hb[1], s.t3_bep);
-  long long lbe = 0;
-  check(cudaMemcpyAsync(&lbe, s.lb_ptr + n, sizeof(long long), cudaMemcpyDeviceToHost, st), "d2h");
-  check(cudaStreamSynchronize(st), "v3 sync");
-  tail_rel_idx_kernel<<<sms * 4, 256, 0, st>>>(hb[1], lbe, base, s.lb_idx);
-  note_launches(4);
-  const std::size_t npc = static_cast<std::size_t>(nlev) * 32;
-  if (s.cap_t4 < npc) {
-    dalloc(s.t4_fpc, npc);
-    dalloc(s.t4_bpc, npc);
-    dalloc(s.t4_frange, static_cast<std::size_t>(nlev) + 1);
-    dalloc(s.t4_brange, static_cast<std::size_t>(nlev) + 1);
-    s.cap_t4 = npc;
+  note_launches(2);
+  // packed row offsets of W (lower) and W^T (upper), padded to even lengths
+  std::vector<long long> offl(static_cast<std::size_t>(nt) + 1), offu(static_cast<std::size_t>(nt) + 1);
+  offl[0] = offu[0] = 0;
+  for (int i = 0; i < nt; ++i) {
+    offl[i + 1] = offl[i] + tw_even(i + 1);
+    offu[i + 1] = offu[i] + (Tp - (i & ~1));
   }
-  const char* epw_env = std::getenv("PARAC_TAIL_EPW");
-  const int epw = epw_env ? std::max(1, std::atoi(epw_env)) : 32 * kT4PF;
-  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 1, s.t3_lvl, s.t3_fep, s.t4_fpc, epw);
-  tail4_pieces_kernel<<<(nlev + 7) / 8, 256, 0, st>>>(nlev, 0, s.t3_lvl, s.t3_bep, s.t4_bpc, epw);
-  tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_fpc, s.t4_frange);
-  tail4_range_kernel<<<(nlev + 255) / 256, 256, 0, st>>>(nlev, s.t4_bpc, s.t4_brange);
-  note_launches(4);
+  check(cudaMemcpyAsync(s.tw_offl, offl.data(), sizeof(long long) * (nt + 1), cudaMemcpyHostToDevice, st), "h2d");
+  check(cudaMemcpyAsync(s.tw_offu, offu.data(), sizeof(long long) * (nt + 1), cudaMemcpyHostToDevice, st), "h2d");
+  const std::size_t wl = static_cast<std::size_t>(offl[nt]), wu = static_cast<std::size_t>(offu[nt]);
+  if (s.cap_tw < wl || s.cap_twt < wu) {
+    dalloc(s.tw, std::max(wl, s.cap_tw));
+    dalloc(s.twt, std::max(wu, s.cap_twt));
+    s.cap_tw = std::max(wl, s.cap_tw);
+    s.cap_twt = std::max(wu, s.cap_twt);
+  }
+  // W = G_TT^-1, one launch per tail level (programmatic dependent launch:
+  // the next level's entries are staged while this one finishes)
+  for (int t = 0; t < nlev; ++t) {
+    const int r0 = static_cast<int>(off[L0 + 1 + t] - base), r1 = static_cast<int>(off[L0 + 2 + t] - base);
+    if (r1 <= r0) continue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((tw_even(r1) + kTwBlockCols - 1) / kTwBlockCols),
+                       static_cast<unsigned>(r1 - r0), 1);
+    cfg.blockDim = dim3(kTwBuildThreads, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    check(cudaLaunchKernelEx(&cfg, tw_build_level_kernel, r0, r1, static_cast<const int*>(s.t3_fep),
+                             static_cast<const int*>(s.t3_fidx), static_cast<const double*>(s.t3_fval),
+                             static_cast<const long long*>(s.tw_offl), s.tw),
+          "tail W build");
+    note_launches(1);
+  }
+  {
+    const long long nb = (Tp + 31) / 32;
+    tw_transpose_kernel<<<static_cast<unsigned>(nb * (nb + 1) / 2), 256, 0, st>>>(nt, Tp, s.tw, s.tw_offl, s.tw_offu,
+                                                                                  s.twt);
+    note_launches(1);
+  }
   // kernel attributes belong to each device's context: set them per device
   static bool attr[64] = {};
   if (!attr[dev]) {
-    check(cudaFuncSetAttribute(tail4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
-    check(cudaFuncSetAttribute(tail4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kT4Smem)), "attr");
+    const int smem = static_cast<int>(sizeof(double) * kTwMaxRows);
+    check(cudaFuncSetAttribute(tw_gemv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    check(cudaFuncSetAttribute(tw_gemv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
     attr[dev] = true;
   }
   check(cudaGetLastError(), "v3 layout");
   s.t3_nt = nt;
   s.t3_base = base;
   s.t3_nlev = nlev;
-  s.t3_bbase = hb[1];
+  s.tw_T = nt;
+  s.tw_Tp = Tp;
 }
 
 void prepare_factor(const SolveInputs& in) {
@@ -2021,30 +1899,41 @@ struct Solver {
                                       s.yf, s.yd, L >= 2, lt ? lt + (L - 1) : nullptr), "wide level forward");
       }
       note_launches(Lw);
-      check(launch_cluster_t(head_sweep_kernel<true>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
-                             s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, nt,
-                             s.t3_base, s.tail_s, lt ? lt + Lw : nullptr),
-            "head forward");
-      note_launches(1);
-      // tail forward + backward (one CTA each)
+      if (H > Lw) {
+        check(launch_cluster_t(head_sweep_kernel<true>, s.head_csize, kHThreads, kHeadSmem, st, Lw + 1, H - Lw,
+                               s.head_W, s.hrec_f, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l, s.dinv_l, s.yf, s.yd, 0,
+                               s.t3_base, s.tail_s, lt ? lt + Lw : nullptr),
+              "head forward");
+        note_launches(1);
+      }
+      // dense-inverse tail: ts = rhs_T - G_TH y_H, then y_T = W ts (+ D^+),
+      // z_T = W^T (D^+ y)_T (tail_dense.cuh)
       if (nt > 0) {
-        const std::size_t t4smem = tail4_smem(s.t3_nlev);
-        tail4_kernel<true><<<1, kTailThreads, t4smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_fpc, s.t4_frange,
-                                                            s.t3_fidx, s.t3_fval, s.tail_s, s.dinv_l, nullptr, s.yf,
-                                                            lt ? lt + (D + 2) : nullptr);
-        tail4_kernel<false><<<1, kTailThreads, t4smem, st>>>(nt, s.t3_nlev, s.t3_base, s.t4_bpc, s.t4_brange,
-                                                             s.lb_idx + s.t3_bbase, s.lb_val + s.t3_bbase,
-                                                             nullptr, s.dinv_l, s.yf, s.zb,
-                                                             lt ? lt + 2 * (D + 2) : nullptr);
+        const int base = s.t3_base;
+        tail_rhs_kernel<<<sm_count(in.device) * 4, 256, 0, st>>>(nt, base, s.lf_ptr, s.lf_idx, s.lf_val, s.rhs_l,
+                                                                s.yf, s.tail_s);
+        note_launches(1);
+        const std::size_t smem = sizeof(double) * static_cast<std::size_t>(s.tw_Tp);
+        check(launch_pdl(tw_gemv_kernel<true>, sm_count(in.device), kTwGemvThreads, smem, st, nt, s.tw_Tp,
+                         static_cast<const double*>(s.tw), static_cast<const long long*>(s.tw_offl),
+                         static_cast<const double*>(s.tail_s), static_cast<const double*>(s.dinv_l + base),
+                         s.yf + base, s.yd + base),
+              "tail forward");
+        check(launch_pdl(tw_gemv_kernel<false>, sm_count(in.device), kTwGemvThreads, smem, st, nt, s.tw_Tp,
+                         static_cast<const double*>(s.twt), static_cast<const long long*>(s.tw_offu),
+                         static_cast<const double*>(s.yd + base), static_cast<const double*>(nullptr), s.zb + base,
+                         static_cast<double*>(nullptr)),
+              "tail backward");
         note_launches(2);
-        check(cudaGetLastError(), "tail launch");
       }
       // backward: cluster head, wide levels
-      check(launch_cluster_t(head_sweep_kernel<false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
-                             s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, 0, 0,
-                             nullptr, lt ? lt + 3 * (D + 2) : nullptr),
-            "head backward");
-      note_launches(1);
+      if (H > Lw) {
+        check(launch_cluster_t(head_sweep_kernel<false>, s.head_csize, kHThreads, kHeadSmem, st, H, H - Lw,
+                               s.head_W, s.hrec_b, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb, nullptr, 0, 0,
+                               nullptr, lt ? lt + 3 * (D + 2) : nullptr),
+              "head backward");
+        note_launches(1);
+      }
       for (int L = Lw; L >= 1; --L) {
         const long long j0 = s.lvl_off_h[L], j1 = s.lvl_off_h[L + 1];
         check(launch_wide_level<false>(s.wide_kb[L], j0, j1, st, s.lb_ptr, s.lb_idx, s.lb_val, s.yd, nullptr, s.zb,
@@ -2200,8 +2089,8 @@ void solve_release(SolveState& s) {
   dfree(s.lf_ptr); dfree(s.lb_ptr); dfree(s.lf_idx); dfree(s.lb_idx); dfree(s.lf_val); dfree(s.lb_val);
   dfree(s.lvl_target); dfree(s.ltime);
   dfree(s.lpos); dfree(s.rlab); dfree(s.v2l); dfree(s.dinv_l); dfree(s.rhs_l); dfree(s.hrec_f); dfree(s.hrec_b);
-  dfree(s.t4_fpc); dfree(s.t4_bpc); dfree(s.t4_frange); dfree(s.t4_brange);
-  dfree(s.t3_lvl); dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_bep); dfree(s.t3_fval);
+  dfree(s.t3_fep); dfree(s.t3_fidx); dfree(s.t3_fval);
+  dfree(s.tw); dfree(s.twt); dfree(s.tw_offl); dfree(s.tw_offu);
   s = SolveState{};
 }
 void solve_invalidate(SolveState& s) {

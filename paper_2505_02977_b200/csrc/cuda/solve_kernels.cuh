@@ -1,5 +1,5 @@
 // Device PCG state (solve path): SpMV, level-synchronous triangular sweeps
-// (fast mode: wide levels / cluster head / one-CTA tail; exact mode: cluster),
+// (fast mode: wide levels / cluster head / dense-inverse tail; exact mode: cluster),
 // fused vector ops. See solve_kernels.cu.
 #pragma once
 #include <cstdint>
@@ -44,13 +44,15 @@ struct SolveState {
   int wide_L = 0;                             // the wide first levels (one launch per level)
   std::vector<long long> lvl_off_h;           // host copy of the level offsets of levels 0..wide_L+1
   std::vector<int> wide_kf, wide_kb;          // lanes per row of each wide level (forward rows / backward columns)
+  // dense-inverse tail (levels > t3_L0, rows t3_base.. in level order, T = t3_nt)
   int t3_L0 = 0, t3_nt = 0, t3_base = 0, t3_nlev = 0;
-  long long t3_bbase = 0;  // lb_ptr[t3_base]
-  int *t3_lvl = nullptr, *t3_fep = nullptr, *t3_fidx = nullptr, *t3_bep = nullptr;
+  int *t3_fep = nullptr, *t3_fidx = nullptr;  // tail rows' entries inside the tail (tail-relative)
   double* t3_fval = nullptr;
-  std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0, cap_t4 = 0;
-  int4 *t4_fpc = nullptr, *t4_bpc = nullptr;  // tail piece tables [nlev][32]
-  int2 *t4_frange = nullptr, *t4_brange = nullptr;  // tail entry range per level
+  double *tw = nullptr, *twt = nullptr;       // W = G_TT^-1 (lower packed) and W^T (rows = W's columns)
+  long long *tw_offl = nullptr, *tw_offu = nullptr;
+  int tw_T = 0, tw_Tp = 0;
+  std::size_t cap_tw = 0, cap_twt = 0;
+  std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0;
   std::size_t cap_ltime = 0;
   std::size_t cap_lz = 0, cap_levels = 0;
   int mode = 0;  // 0 default (pcg fast, apply exact), 1 exact, 2 fast

@@ -25,5 +25,5 @@ for _ in range(a.reps):
     x, rep = P.rchol._pcg_resident(ctx, b, P.SolveConfig(tol=1e-8))
     res.append({"iters": rep.iterations, "relres": rep.relative_residual, "solve_ms": rep.device_ms,
                 "wall_ms": rep.solve_seconds * 1e3, "exact": rep.exact})
-print(json.dumps({"workload": a.workload, "n": a.n, "mode": a.mode, "tail_width": os.environ.get("PARAC_TAIL_WIDTH", "64"),
+print(json.dumps({"workload": a.workload, "n": a.n, "mode": a.mode, "tail_rows": os.environ.get("PARAC_TAIL_ROWS", "auto"),
                   "runs": res}))

@@ -27,7 +27,7 @@ rowlen = np.bincount(f.rows, minlength=g.n)
 collen = np.diff(f.col_ptr)
 ent_f = np.bincount(lv, weights=rowlen, minlength=D + 2)
 ent_b = np.bincount(lv, weights=collen, minlength=D + 2)
-print(f"H={H} depth={D} tail rows={nt}")
+print(f"H={H} depth={D} tail rows={nt} wide levels={Lw}")
 def show(name, ts, levels, ent):
     ts = ts[:len(levels)]
     d = np.diff(ts) / 1e3
@@ -41,14 +41,16 @@ def show(name, ts, levels, ent):
                   f"  rows/level {w[L].mean():9.1f}  entries/level {ent[L].mean():10.1f}")
 show("head fwd", t[0], np.arange(1, H + 1), ent_f)
 if nt:
-    show("tail fwd", t[1], np.arange(H + 1, D + 1), ent_f)
-    show("tail bwd", t[2], np.arange(D, H, -1), ent_b)
+    print(f"tail: levels {H + 1}..{D} ({nt} rows) by the dense-inverse GEMVs (no per-level stamps)")
 show("head bwd", t[3], np.arange(H, 0, -1), ent_b)
 
 # DS cluster head: warp 0 phase cycles per level (see head_sweep_kernel dbg)
 nh = H - Lw
 def phases(name, base, nlev):
-    a = t_all[base:base + 4 * nlev].reshape(nlev, 4)[:-1].astype(np.int64)
+    a = t_all[base:base + 4 * nlev]
+    if nlev < 2 or len(a) < 4 * nlev:
+        return
+    a = a.reshape(nlev, 4)[:-1].astype(np.int64)
     if a.max() <= 0 or a.max() > 10**8:
         return
     print(f"{name} warp-0 cycles per level: load-issue / gather+products / sums+stores / wait+barrier")

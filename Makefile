@@ -18,7 +18,7 @@ OBJDIR   := $(PKG)/build
 CU_OBJS  := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(CPP_SRCS))
 
-.PHONY: all lib oracle ref clean
+.PHONY: all lib oracle ref dropin clean
 all: lib oracle
 
 lib: $(LIB)
@@ -41,6 +41,18 @@ oracle:
 ref:
 	$(MAKE) -C oracle ref
 
+# The drop-in timing harness (bench.py e2e_dropin): the reference's types and
+# generators on the host side of parac::factor_gpu (needs /root/reference's
+# headers: built here, shipped prebuilt like oracle/_ref).
+REF ?= /root/reference/proj
+dropin: tools/_build/dropin_time
+
+tools/_build/dropin_time: tools/dropin_time.cpp $(LIB) $(PKG)/csrc/shim/parac_gpu_shim.hpp include/parac_gpu.h oracle/_ref/libparac_ref.so
+	@mkdir -p tools/_build
+	g++ -std=c++20 -O2 -I$(REF)/include -Ioracle/eigen_shim -Iinclude -I$(PKG)/csrc/shim $< -o $@ \
+	  -Loracle/_ref -lparac_ref -L$(LIBDIR) -lparac_gpu \
+	  -Wl,-rpath,'$$ORIGIN/../../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -pthread
+
 clean:
-	rm -rf $(OBJDIR) $(LIBDIR)
+	rm -rf $(OBJDIR) $(LIBDIR) tools/_build
 	$(MAKE) -C oracle clean

@@ -454,6 +454,25 @@ def run_ours(args):
                "converged": rep.converged, "solve_ms": rep.device_ms, "wall_ms": rep.solve_seconds * 1e3,
                "first_call_wall_ms": rep0.solve_seconds * 1e3, "tol": 1e-8}
 
+    # ---- the drop-in C++ call (parac::factor_gpu through the shim, the
+    # reference's own types, pageable std::vector outputs): tools/_build/dropin_time
+    dropin = None
+    if rank == 0 and world == 1 and workload == "poisson3d_128" and not args.no_dropin:
+        exe = os.path.join(ROOT, "tools", "_build", "dropin_time")
+        if os.path.exists(exe):
+            try:
+                out = subprocess.run([exe, "128", str(max(3, args.steps)), "2"], capture_output=True, text=True,
+                                     timeout=600)
+                d = json.loads(out.stdout.strip().splitlines()[-1])
+                dropin = {"value": d["nnz"] / (d["ms_per_call"] / 1e3), "unit": "nnz/s",
+                          "ms_per_step": d["ms_per_call"], "calls_ms": d["calls"], "checksum": d["checksum"],
+                          "what": "parac::factor_gpu(LaplacianGraph, Ordering, seed) -> LdlFactor (C++ shim, "
+                                  "cached device context, pageable std::vector in/out), host clock around the call"}
+            except Exception as exc:
+                dropin = {"value": None, "unit": "nnz/s", "error": str(exc)}
+        else:
+            dropin = {"value": None, "unit": "nnz/s", "error": "tools/_build/dropin_time not built"}
+
     peak, peak_src = read_peaks()
     by = algorithmic_bytes(n, E, Z, F)
     k3_avg_s = sum(k3_ms) / len(k3_ms) / 1e3
@@ -502,6 +521,7 @@ def run_ours(args):
                           "device_passes_per_step": max(attempts) if attempts else 1},
             "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},
+            "e2e_dropin": dropin,
             "pcg": pcg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -648,6 +668,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="poisson3d_128")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")

@@ -12,6 +12,7 @@
 // dot products use a deterministic two-level tree (run-to-run reproducible, not
 // the reference's serial order), which SURVEY §8(a) a16 validated does not move
 // iteration counts.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
@@ -43,7 +44,9 @@ constexpr int kRedThreads = 256;
 constexpr int kSweepThreads = 256;
 
 enum Slot { kSlotA = 0, kSlotB = 1, kSlotC = 2, kSlots = 3 };
-enum Scalar { kRz0 = 0, kRz1 = 1, kPlpOk = 2, kScalars = 8 };
+enum Scalar { kRz0 = 0, kRz1 = 1, kPlpOk = 2, kRzPrev = 6, kRn = 7, kBest = 8, kTolB = 9, kScalars = 16 };
+// int control words of the fast PCG loop (SolveState::counters + kCtl): iterations, max_iters, copy-best flag
+enum Ctl { kCtl = 12, kCtlIters = 0, kCtlMax = 1, kCtlCopy = 2 };
 
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -334,12 +337,9 @@ __global__ void level_hist_kernel(int n, const int* level, int* hist, int* depth
   atomicMax(depth, level[r]);
 }
 
-__global__ void level_scatter_kernel(int n, const int* level, const long long* off, int* cursor,
-                                     int* order) {
+__global__ void iota_kernel(int n, int* out) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int l = level[r];
-  order[off[l] + atomicAdd(&cursor[l], 1)] = r;
+  if (r < n) out[r] = r;
 }
 
 // ---------------------------------------------------------------- K5 / K7
@@ -382,18 +382,37 @@ __global__ void center_kernel(int n, const double* a, const double* sum_partials
   block_partial(s, partials);
 }
 
-// alpha = rz / p.lp; x += alpha p; r -= alpha lp; partial ||r||^2 (solver.cpp:133-140).
-// If p.lp <= 0 nothing is updated and the flag is raised (solver.cpp:134).
-__global__ void update_xr_kernel(int n, const double* plp_partials, const double* scalars_in,
-                                 int rz_slot, double* x, double* r, const double* p,
-                                 const double* lp, double* partials, double* flag_out) {
+// z (label space) = zb[perm[v]]; partial r.z (solver.cpp:145-146 / :122-124).
+__global__ void gather_z_dot_kernel(int n, const int* perm, const double* zb, const double* r,
+                                    double* z, double* partials) {
+  double s = 0.0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const double zv = zb[perm[v]];
+    z[v] = zv;
+    s += r[v] * zv;
+  }
+  block_partial(s, partials);
+}
+
+// ---- fast PCG loop, graph form (one iteration = one body of a CUDA-graph
+// while node; no host round trip per iteration). The reductions are the same
+// fixed-order partial sums as above, read by every block, so every reader
+// derives bit-identical scalars.
+// Iteration t: rz_{t-1} is partial slot C (r.z of the previous iteration);
+// update_xr_g snapshots it into kRzPrev for update_p_g's beta.
+__global__ void update_xr_g_kernel(int n, const double* plp_partials, const double* rz_partials, double* scalars,
+                                   double* x, double* r, const double* p, const double* lp, double* partials) {
   __shared__ double alpha;
   __shared__ int ok;
   if (threadIdx.x == 0) {
     const double plp = sum_partials(plp_partials);
-    ok = plp > 0.0;
-    alpha = ok ? scalars_in[rz_slot] / plp : 0.0;
-    if (blockIdx.x == 0) *flag_out = ok ? 1.0 : 0.0;
+    const double rz = sum_partials(rz_partials);
+    ok = plp > 0.0;  // solver.cpp:134
+    alpha = ok ? rz / plp : 0.0;
+    if (blockIdx.x == 0) {
+      scalars[kPlpOk] = ok ? 1.0 : 0.0;
+      scalars[kRzPrev] = rz;
+    }
   }
   __syncthreads();
   double s = 0.0;
@@ -409,30 +428,41 @@ __global__ void update_xr_kernel(int n, const double* plp_partials, const double
   block_partial(s, partials);
 }
 
-// z (label space) = zb[perm[v]]; partial r.z (solver.cpp:145-146 / :122-124).
-__global__ void gather_z_dot_kernel(int n, const int* perm, const double* zb, const double* r,
-                                    double* z, double* partials) {
-  double s = 0.0;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const double zv = zb[perm[v]];
-    z[v] = zv;
-    s += r[v] * zv;
+// The loop test of solver.cpp:129-131 + the best-iterate bookkeeping of
+// :141-144, on the device: one thread. Sets the while node's condition.
+__global__ void pcg_control_kernel(const double* rr_partials, double* scalars, int* ctl,
+                                   cudaGraphConditionalHandle cond, int set_cond) {
+  const double rn = sqrt(sum_partials(rr_partials));
+  const bool ok = scalars[kPlpOk] != 0.0;
+  const int it = ctl[kCtlIters] + 1;  // ++iters precedes the p.Lp test (solver.cpp:132)
+  ctl[kCtlIters] = it;
+  int copy = 0;
+  if (ok) {
+    scalars[kRn] = rn;
+    if (rn < scalars[kBest]) {
+      scalars[kBest] = rn;
+      copy = 1;
+    }
   }
-  block_partial(s, partials);
+  ctl[kCtlCopy] = copy;
+  const int cont = ok && it < ctl[kCtlMax] && rn > scalars[kTolB];
+  if (set_cond) cudaGraphSetConditional(cond, cont ? 1u : 0u);
+  ctl[kCtlCopy + 1] = cont;
 }
 
-// beta = rz_next / rz; p = z + beta p (solver.cpp:146-152). first: p = z.
-__global__ void update_p_kernel(int n, const double* rz_partials, double* scalars, int rz_old,
-                                int rz_new, int first, const double* z, double* p) {
+__global__ void copy_if_kernel(int n, const int* flag, const double* a, double* b) {
+  if (!*flag) return;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) b[v] = a[v];
+}
+
+// beta = rz_t / rz_{t-1}; p = z + beta p (solver.cpp:146-152)
+__global__ void update_p_g_kernel(int n, const double* rz_partials, const double* scalars, const double* z,
+                                  double* p) {
   __shared__ double beta;
-  if (threadIdx.x == 0) {
-    const double rzn = sum_partials(rz_partials);
-    beta = first ? 0.0 : rzn / scalars[rz_old];
-    if (blockIdx.x == 0) scalars[rz_new] = rzn;
-  }
+  if (threadIdx.x == 0) beta = sum_partials(rz_partials) / scalars[kRzPrev];
   __syncthreads();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    p[v] = first ? z[v] : __dadd_rn(z[v], __dmul_rn(beta, p[v]));
+    p[v] = __dadd_rn(z[v], __dmul_rn(beta, p[v]));
 }
 
 __global__ void copy_kernel(int n, const double* a, double* b) {
@@ -1430,8 +1460,16 @@ int sweep_grid(int device) {
 }
 
 // ---------------------------------------------------------------- host side
+void drop_pcg_graph(SolveState& s) {
+  if (s.pcg_exec) cudaGraphExecDestroy(s.pcg_exec);
+  if (s.pcg_graph) cudaGraphDestroy(s.pcg_graph);
+  s.pcg_exec = nullptr;
+  s.pcg_graph = nullptr;
+}
+
 void ensure_vectors(SolveState& s, int n) {
   if (s.cap_n >= static_cast<std::size_t>(n) && s.x) return;
+  drop_pcg_graph(s);  // its kernels hold the old vectors
   const std::size_t c = static_cast<std::size_t>(std::max(n, 1));
   dalloc(s.x, c); dalloc(s.r, c); dalloc(s.p, c); dalloc(s.lp, c); dalloc(s.z, c);
   dalloc(s.best, c); dalloc(s.yf, c); dalloc(s.yd, c); dalloc(s.zb, c); dalloc(s.rhs, c);
@@ -1734,6 +1772,7 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
 void prepare_factor(const SolveInputs& in) {
   SolveState& s = *in.state;
   if (s.factor_ready) return;
+  drop_pcg_graph(s);  // captured for the previous factor's layout
   const int n = in.f_n;
   const long long Z = in.f_nnz;
   cudaStream_t st = in.stream;
@@ -1835,13 +1874,31 @@ void prepare_factor(const SolveInputs& in) {
   level_hist_kernel<<<blocks, 256, 0, st>>>(n, s.level, hist, s.counters + 1);
   note_launches(2);
   check(launch_scan(hist, n + 1, s.lvl_off, s.tiles, st), "scan");
-  check(cudaMemsetAsync(hist, 0, sizeof(int) * (n + 2), st), "memset");  // reuse as cursor
-  level_scatter_kernel<<<blocks, 256, 0, st>>>(n, s.level, s.lvl_off, hist, s.order);
-  note_launches(1);
   int depth = 0;
   check(cudaMemcpyAsync(&depth, s.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
   check(cudaStreamSynchronize(st), "prepare_factor");
   s.depth = depth;
+  // positions in (level, position) order: a STABLE sort by level, so the
+  // level-order layout -- and with it every fast-mode summation order -- is
+  // the same on every build of the same factor (an atomic scatter was not)
+  {
+    int* keys_out = nullptr;
+    int* pos_in = nullptr;
+    check(cudaMallocAsync(&keys_out, sizeof(int) * static_cast<std::size_t>(std::max(n, 1)), st), "alloc");
+    check(cudaMallocAsync(&pos_in, sizeof(int) * static_cast<std::size_t>(std::max(n, 1)), st), "alloc");
+    iota_kernel<<<blocks, 256, 0, st>>>(n, pos_in);
+    note_launches(1);
+    int bits = 1;
+    while (bits < 31 && (1 << bits) <= depth) ++bits;
+    std::size_t tb = 0;
+    check(cub::DeviceRadixSort::SortPairs(nullptr, tb, s.level, keys_out, pos_in, s.order, n, 0, bits, st),
+          "level sort size");
+    void* tmp = nullptr;
+    check(cudaMallocAsync(&tmp, std::max<std::size_t>(tb, 1), st), "alloc");
+    check(cub::DeviceRadixSort::SortPairs(tmp, tb, s.level, keys_out, pos_in, s.order, n, 0, bits, st),
+          "level sort");
+    for (void* q : {static_cast<void*>(keys_out), static_cast<void*>(pos_in), tmp}) check(cudaFreeAsync(q, st), "free");
+  }
   stamp("levels");
   build_level_layout(in, s, sms);
   stamp("level layout");
@@ -2068,6 +2125,109 @@ void pcg_exact(const SolveInputs& in, double tol, int max_iters, parac_gpu_solve
   rep.converged = rep.relative_residual <= tol;
 }
 
+// Fast PCG (the default above the exact threshold): pcg_solve's control flow
+// with fixed-order tree reductions and the fast sweeps. The loop runs on the
+// device as a CUDA graph -- a while node whose body is one iteration
+// (SpMV, x/r update, the loop test and best-iterate bookkeeping in a one-thread
+// control kernel, preconditioner sweeps, p update) -- captured once per factor
+// and replayed per solve. PARAC_PCG_GRAPH=0 drives the same kernels from the
+// host (one control read per iteration) for comparison.
+void pcg_fast(const SolveInputs& in, double tol, int max_iters, parac_gpu_solve_report& rep) {
+  SolveState& s = *in.state;
+  const int n = in.n;
+  cudaStream_t st = in.stream;
+  Solver sv(in);
+  sv.center(s.lp, s.rhs, s.r, s.x);  // rhs = b - mean, r = rhs, x = 0
+  const double b_norm = std::sqrt(sv.read_partials(kSlotB));
+  if (b_norm == 0.0) {
+    rep.converged = 1;
+    return;
+  }
+  sv.precond(s.r, s.z, kSlotC, false);  // slot C = r0.z0
+  copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.z, s.p);
+  copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.x, s.best);
+  note_launches(2);
+  double rn = b_norm, best_norm = b_norm;  // norm2(r) with r = rhs
+  int iters = 0;
+  if (max_iters > 0 && rn > tol * b_norm) {
+    const double sc[3] = {b_norm, b_norm, tol * b_norm};  // kRn, kBest, kTolB
+    const int ctl[2] = {0, max_iters};
+    check(cudaMemcpyAsync(s.scalars + kRn, sc, sizeof(sc), cudaMemcpyHostToDevice, st), "h2d");
+    check(cudaMemcpyAsync(s.counters + kCtl, ctl, sizeof(ctl), cudaMemcpyHostToDevice, st), "h2d");
+    int* dctl = s.counters + kCtl;
+    auto body = [&](cudaGraphConditionalHandle cond, int set_cond) {
+      sv.spmv(s.p, s.lp, kSlotA);
+      update_xr_g_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotA), sv.part(kSlotC), s.scalars, s.x,
+                                                             s.r, s.p, s.lp, sv.part(kSlotB));
+      pcg_control_kernel<<<1, 1, 0, st>>>(sv.part(kSlotB), s.scalars, dctl, cond, set_cond);
+      copy_if_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, dctl + kCtlCopy, s.x, s.best);
+      note_launches(3);
+      sv.precond(s.r, s.z, kSlotC, false);
+      update_p_g_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotC), s.scalars, s.z, s.p);
+      note_launches(1);
+    };
+    static const bool use_graph = [] {
+      const char* e = std::getenv("PARAC_PCG_GRAPH");
+      return !(e && std::atoi(e) == 0) && !std::getenv("PARAC_SWEEP_PROFILE");
+    }();
+    if (use_graph) {
+      if (!s.pcg_exec) {
+        cudaGraph_t g = nullptr;
+        check(cudaGraphCreate(&g, 0), "graph create");
+        s.pcg_graph = g;
+        cudaGraphConditionalHandle cond;
+        check(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault), "conditional handle");
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        check(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "while node");
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        const long long l0 = parac_gpu_launch_count();
+        check(cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+              "capture");
+        body(cond, 1);
+        cudaGraph_t captured = nullptr;
+        check(cudaStreamEndCapture(st, &captured), "end capture");
+        s.pcg_body_launches = parac_gpu_launch_count() - l0;
+        note_launches(-s.pcg_body_launches);  // counted per executed iteration below
+        check(cudaGraphInstantiate(&s.pcg_exec, g, 0), "graph instantiate");
+      }
+      check(cudaGraphLaunch(s.pcg_exec, st), "graph launch");
+    } else {
+      int cont = 1;
+      while (cont) {
+        body(0, 0);
+        check(cudaMemcpyAsync(&cont, dctl + kCtlCopy + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+        check(cudaStreamSynchronize(st), "sync");
+      }
+    }
+    double back[2];
+    check(cudaMemcpyAsync(back, s.scalars + kRn, sizeof(back), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaMemcpyAsync(&iters, dctl + kCtlIters, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "pcg loop");
+    rn = back[0];
+    best_norm = back[1];
+    if (use_graph) note_launches(s.pcg_body_launches * iters);
+  }
+  double rec = rn;  // norm2(r) of the final r (:156)
+  if (rec > best_norm) {
+    copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.best, s.x);
+    note_launches(1);
+    rec = best_norm;
+  }
+  rep.recurrence_residual = rec / b_norm;
+  sv.center(s.x, s.x, nullptr, nullptr);  // subtract_mean(x)
+  sv.spmv(s.x, s.lp, kSlotA);
+  diff_norm_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.rhs, s.lp, sv.part(kSlotB));
+  note_launches(1);
+  rep.iterations = iters;
+  rep.relative_residual = std::sqrt(sv.read_partials(kSlotB)) / b_norm;
+  rep.converged = rep.relative_residual <= tol;
+}
+
 // parac_gpu_pcg's mode 0 runs the exact PCG up to this size (PARAC_EXACT_PCG_N)
 int exact_pcg_max_n() {
   static const int v = [] {
@@ -2080,6 +2240,7 @@ int exact_pcg_max_n() {
 }  // namespace
 
 void solve_release(SolveState& s) {
+  drop_pcg_graph(s);
   dfree(s.wdeg); dfree(s.inv); dfree(s.gt_ptr); dfree(s.gt_col); dfree(s.gt_val);
   dfree(s.level); dfree(s.order); dfree(s.lvl_off); dfree(s.flags);
   dfree(s.x); dfree(s.r); dfree(s.p); dfree(s.lp); dfree(s.z); dfree(s.best);
@@ -2205,7 +2366,6 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     SolveState& s = *in.state;
     const int n = in.n;
     cudaStream_t st = in.stream;
-    Solver sv(in);
     parac_gpu_solve_report rep{};
     struct Events {  // destroyed on every path out (a failed check throws)
       cudaEvent_t e[2] = {nullptr, nullptr};
@@ -2222,60 +2382,8 @@ int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_i
     upload(s.lp, b, n, st);
     const bool exact = s.mode == kModeExact || (s.mode == kModeDefault && n <= exact_pcg_max_n());
     rep.exact = exact ? 1 : 0;
-    if (exact) {
-      pcg_exact(in, tol, max_iters, rep);
-    } else {
-    sv.center(s.lp, s.rhs, s.r, s.x);  // rhs = b - mean, r = rhs, x = 0
-    const double b_norm = std::sqrt(sv.read_partials(kSlotB));
-    if (b_norm == 0.0) {
-      rep.converged = 1;
-    } else {
-      sv.precond(s.r, s.z, kSlotC, s.mode == kModeExact);
-      update_p_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotC), s.scalars, kRz0, kRz0, 1, s.z, s.p);
-      copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.x, s.best);
-      note_launches(2);
-      double best_norm = b_norm;  // norm2(r) with r = rhs
-      double rn = b_norm;
-      int iters = 0, slot = kRz0;
-      std::vector<double> flag(1);
-      while (iters < max_iters) {
-        if (rn <= tol * b_norm) break;
-        ++iters;
-        sv.spmv(s.p, s.lp, kSlotA);
-        update_xr_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotA), s.scalars, slot, s.x, s.r,
-                                                             s.p, s.lp, sv.part(kSlotB), s.scalars + kPlpOk);
-        note_launches(1);
-        check(cudaMemcpyAsync(flag.data(), s.scalars + kPlpOk, sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
-        const double rr = sv.read_partials(kSlotB);
-        if (flag[0] == 0.0) break;  // numerically exhausted search direction
-        rn = std::sqrt(rr);
-        if (rn < best_norm) {
-          best_norm = rn;
-          copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.x, s.best);
-          note_launches(1);
-        }
-        sv.precond(s.r, s.z, kSlotC, s.mode == kModeExact);
-        const int next = slot == kRz0 ? kRz1 : kRz0;
-        update_p_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, sv.part(kSlotC), s.scalars, slot, next, 0, s.z, s.p);
-        note_launches(1);
-        slot = next;
-      }
-      double rec = rn;
-      if (rec > best_norm) {
-        copy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.best, s.x);
-        note_launches(1);
-        rec = best_norm;
-      }
-      rep.recurrence_residual = rec / b_norm;
-      sv.center(s.x, s.x, nullptr, nullptr);  // subtract_mean(x)
-      sv.spmv(s.x, s.lp, kSlotA);
-      diff_norm_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, s.rhs, s.lp, sv.part(kSlotB));
-      note_launches(1);
-      rep.iterations = iters;
-      rep.relative_residual = std::sqrt(sv.read_partials(kSlotB)) / b_norm;
-      rep.converged = rep.relative_residual <= tol;
-    }
-    }
+    if (exact) pcg_exact(in, tol, max_iters, rep);
+    else pcg_fast(in, tol, max_iters, rep);
     check(cudaEventRecord(e1, st), "event");
     check(cudaGetLastError(), "pcg");
     download(x, s.x, n, st);

@@ -55,6 +55,11 @@ struct SolveState {
   std::size_t cap_v3 = 0, cap_hrec = 0, cap_t3 = 0, cap_t3e = 0;
   std::size_t cap_ltime = 0;
   std::size_t cap_lz = 0, cap_levels = 0;
+  // fast PCG loop as a CUDA graph (a while node over one iteration), built on
+  // the first solve of a factor and replayed: no host round trip per iteration
+  cudaGraphExec_t pcg_exec = nullptr;
+  cudaGraph_t pcg_graph = nullptr;
+  long long pcg_body_launches = 0;
   int mode = 0;  // 0 default (pcg fast, apply exact), 1 exact, 2 fast
   int depth = 0;
   int epoch = 0;

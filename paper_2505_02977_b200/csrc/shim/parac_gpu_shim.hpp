@@ -16,16 +16,31 @@
 // parac::Error(code, detail) exactly like the CPU backends throw
 // (ArenaExhausted, QueueStall, NotConnected, DimensionMismatch, ...).
 // No exception crosses the C boundary; no CPU fallback exists behind it.
+//
+// Contexts: every call on a device shares ONE cached device context (buffers
+// sized by the largest problem seen, pinned staging, solve layouts), created
+// on first use. Calls are thread-safe: calls on the same device serialise on
+// the context's mutex, calls on different devices run concurrently
+// (factor_par's "no global state" contract becomes "one session per device").
+// release_gpu_sessions() frees them (e.g. before cudaDeviceReset).
 #pragma once
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <utility>
 #include <vector>
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
 
 #include "parac/error.hpp"
 #include "parac/factor.hpp"
@@ -63,15 +78,52 @@ inline void check(int rc) {
   if (rc != 0) rethrow(rc);
 }
 
-struct CtxDeleter {
-  void operator()(parac_gpu_ctx* c) const { parac_gpu_destroy(c); }
+// One cached context per device (see the header comment). Never destroyed
+// implicitly: at process exit the driver reclaims it.
+constexpr int kMaxDevices = 64;
+struct Session {
+  std::mutex m;
+  parac_gpu_ctx* ctx = nullptr;
+  // shape (n, adjacency entries) and factor size of the last factorization:
+  // the guess for sizing the next same-shape factor's outputs early
+  std::int64_t last_n = -1, last_nnz = -1, last_z = 0;
 };
-using Ctx = std::unique_ptr<parac_gpu_ctx, CtxDeleter>;
-
-inline Ctx make_ctx(int device) {
+inline Session& session(int device) {
+  static Session sessions[kMaxDevices];
+  return sessions[device];
+}
+struct Ctx {  // a locked lease of a device's context
+  std::unique_lock<std::mutex> lock;
   parac_gpu_ctx* c = nullptr;
-  check(parac_gpu_create(device, &c));
-  return Ctx(c);
+  Session* s = nullptr;
+  parac_gpu_ctx* get() const { return c; }
+};
+inline Ctx make_ctx(int device) {
+  if (device < 0 || device >= kMaxDevices) throw Error(Errc::internal_error, "device ordinal out of range");
+  Session& s = session(device);
+  std::unique_lock<std::mutex> lock(s.m);
+  if (!s.ctx) check(parac_gpu_create(device, &s.ctx));
+  return Ctx{std::move(lock), s.ctx, &s};
+}
+
+// Sizes an output vector for a download. The host cost of the drop-in path
+// is dominated by first-touch page faults on fresh multi-MB vectors (~110 ms
+// for the 300 MB of a 128^3 factor on the B200 host's VM): large outputs ask
+// for transparent huge pages (512x fewer faults) before resize() touches them.
+template <typename T>
+void size_output(std::vector<T>& v, std::size_t count) {
+  static_assert(std::is_trivially_copyable_v<T>);
+  v.reserve(count);
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+  const std::size_t bytes = count * sizeof(T);
+  constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20;
+  if (bytes >= 8 * kHuge) {
+    const auto p = reinterpret_cast<std::uintptr_t>(v.data());
+    const std::uintptr_t a = (p + kHuge - 1) & ~(kHuge - 1), e = (p + bytes) & ~(kHuge - 1);
+    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // a hint; failure is harmless
+  }
+#endif
+  v.resize(count);
 }
 
 // LaplacianGraph keeps ptr_ private; its public spans are views into the
@@ -98,10 +150,21 @@ inline void stage_factor(parac_gpu_ctx* ctx, const LdlFactor& f) {
 
 }  // namespace gpu_detail
 
+// Frees every cached device context (the next call creates a fresh one).
+inline void release_gpu_sessions() {
+  for (int d = 0; d < gpu_detail::kMaxDevices; ++d) {
+    gpu_detail::Session& s = gpu_detail::session(d);
+    std::lock_guard<std::mutex> lock(s.m);
+    if (s.ctx) parac_gpu_destroy(s.ctx);
+    s.ctx = nullptr;
+  }
+}
+
 inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& ordering,
                             std::uint64_t seed, const GpuOptions& options = {},
                             FactorStats* stats = nullptr) {
   using namespace gpu_detail;
+  const auto start_time = std::chrono::steady_clock::now();
   const VertexId n = graph.num_vertices();
   if (ordering.size() != n)
     throw Error(Errc::dimension_mismatch, "ordering size does not match the graph");
@@ -117,14 +180,39 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
   o.delay_ns = options.delay_ns;
   o.record_times = options.record_vertex_times ? 1 : 0;
   parac_gpu_factor_info info{};
-  check(parac_gpu_factor(ctx.get(), &v.csr, ordering.perm.data(), seed, &o, &info));
+  const auto t_csr = std::chrono::steady_clock::now();
+  // The output vectors are sized by a helper thread while the device works
+  // (their first-touch page faults are the largest host cost): col_ptr and
+  // diag exactly, rows/values at the size of the last factor of a graph of
+  // this shape (corrected below when the guess is off).
   LdlFactor f;
   f.n = n;
-  f.col_ptr.resize(static_cast<std::size_t>(n) + 1);
-  f.rows.resize(static_cast<std::size_t>(info.nnz_off_diagonal));
-  f.values.resize(static_cast<std::size_t>(info.nnz_off_diagonal));
-  f.diag.resize(static_cast<std::size_t>(n));
+  const std::int64_t nnz_adj = v.ptr.empty() ? 0 : v.ptr.back();
+  Session& sess = *ctx.s;
+  const std::size_t guess =
+      sess.last_n == n && sess.last_nnz == nnz_adj ? static_cast<std::size_t>(sess.last_z) : 0;
+  std::thread sizer([&f, n, guess] {
+    size_output(f.col_ptr, static_cast<std::size_t>(n) + 1);
+    size_output(f.diag, static_cast<std::size_t>(n));
+    if (guess) {
+      size_output(f.rows, guess);
+      size_output(f.values, guess);
+    }
+  });
+  const int rc = parac_gpu_factor(ctx.get(), &v.csr, ordering.perm.data(), seed, &o, &info);
+  sizer.join();
+  check(rc);
+  const auto t_fac = std::chrono::steady_clock::now();
+  const auto z = static_cast<std::size_t>(info.nnz_off_diagonal);
+  if (f.rows.size() != z) {
+    size_output(f.rows, z);
+    size_output(f.values, z);
+  }
+  sess.last_n = n;
+  sess.last_nnz = nnz_adj;
+  sess.last_z = static_cast<std::int64_t>(z);
   f.perm = ordering.perm;
+  const auto t_alloc = std::chrono::steady_clock::now();
   std::vector<std::int32_t> md, se, fr;
   if (stats) {
     md.resize(n);
@@ -134,13 +222,21 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
   check(parac_gpu_download(ctx.get(), f.col_ptr.data(), f.rows.data(), f.values.data(),
                            f.diag.data(), stats ? md.data() : nullptr,
                            stats ? se.data() : nullptr, stats ? fr.data() : nullptr));
+  if (std::getenv("PARAC_SHIM_TIMING")) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t_end = std::chrono::steady_clock::now();
+    std::fprintf(stderr,
+                 "factor_gpu: csr %.2f ms | upload %.2f + device %.2f ms (parac_gpu_factor %.2f) | outputs %.2f ms | "
+                 "download %.2f ms\n",
+                 ms(start_time, t_csr), info.upload_ms, info.device_ms, ms(t_csr, t_fac), ms(t_fac, t_alloc),
+                 ms(t_alloc, t_end));
+  }
   if (stats) {
     stats->merged_degree = std::move(md);
     stats->samples_emitted = std::move(se);
     stats->fills_received = std::move(fr);
     stats->total_fills = info.total_fills;
     stats->arena_used = info.arena_used;
-    stats->seconds = info.device_ms * 1e-3;
     if (options.record_vertex_times) {
       std::vector<std::uint64_t> t(8 * static_cast<std::size_t>(n));
       check(parac_gpu_download_times(ctx.get(), t.data()));
@@ -151,6 +247,9 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
       for (VertexId k = 0; k < n; ++k)
         if (t[8 * k + 7]) stats->vertex_seconds[k] = static_cast<double>(t[8 * k + 7] - t0) * 1e-9;
     }
+    // wall clock at the API, like factor_sequential (src/factor_seq.cpp:46, :141-143):
+    // upload, device factorization, download and the host vectors included
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start_time).count();
   }
   return f;
 }
@@ -192,10 +291,10 @@ inline std::vector<LdlFactor> factor_batch_gpu(std::span<const LaplacianGraph> g
     check(parac_gpu_batch_nnz(ctx.get(), static_cast<std::int32_t>(i), &z));
     LdlFactor& f = out[i];
     f.n = graphs[i].num_vertices();
-    f.col_ptr.resize(static_cast<std::size_t>(f.n) + 1);
-    f.rows.resize(static_cast<std::size_t>(z));
-    f.values.resize(static_cast<std::size_t>(z));
-    f.diag.resize(static_cast<std::size_t>(f.n));
+    size_output(f.col_ptr, static_cast<std::size_t>(f.n) + 1);
+    size_output(f.rows, static_cast<std::size_t>(z));
+    size_output(f.values, static_cast<std::size_t>(z));
+    size_output(f.diag, static_cast<std::size_t>(f.n));
     f.perm = orderings[i].perm;
     check(parac_gpu_download_batch(ctx.get(), static_cast<std::int32_t>(i), f.col_ptr.data(), f.rows.data(),
                                    f.values.data(), f.diag.data()));

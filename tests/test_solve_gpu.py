@@ -146,3 +146,23 @@ def test_resident_factor_tracking_across_batch(gpu_ctx):
     x, rep = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
     assert rep.converged
     assert not f.values.flags.writeable  # factors from factor_gpu are immutable
+
+
+def test_fast_pcg_deterministic_across_builds(gpu_ctx):
+    # the fast PCG's summation orders follow the level-order layout, which is
+    # a stable sort of the factor: every build of the same factor (a re-upload,
+    # another context) gives the same bits, graph-driven or not
+    g = P.gen_poisson3d(30)  # n = 27000: above the exact threshold
+    o = P.ordering_random(g.n, 5)
+    f = P.factor_gpu(g, o, 5, ctx=gpu_ctx)
+    b = P.make_rhs(g, "random_projected", 2)
+    x1, r1 = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+    x2, r2 = P.pcg_solve_gpu(g, f, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)  # graph replay
+    f2 = P.LdlFactor(f.n, f.col_ptr, f.rows, f.values, f.diag, f.perm)  # same arrays, new object: re-upload
+    x3, r3 = P.pcg_solve_gpu(g, f2, b, P.SolveConfig(tol=1e-8), ctx=gpu_ctx)
+    with P.GpuContext(0) as other:
+        x4, r4 = P.pcg_solve_gpu(g, f2, b, P.SolveConfig(tol=1e-8), ctx=other)
+    assert not r1.exact and r1.converged
+    for x, r in ((x2, r2), (x3, r3), (x4, r4)):
+        assert x.tobytes() == x1.tobytes() and r.iterations == r1.iterations
+        assert r.relative_residual == r1.relative_residual

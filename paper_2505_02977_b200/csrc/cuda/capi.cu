@@ -362,7 +362,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->ctrl.ensure(1);
-  ctx->tiles.ensure(static_cast<std::size_t>(scan_tiles(n) + 1));
+  ctx->tiles.ensure(static_cast<std::size_t>(std::max<long long>(scan_tiles(n) + 1, initial_ready_scratch(n))));
   ctx->col_ptr.ensure(nn + 1);
 
   FactorDev d{};
@@ -433,7 +433,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   check(cudaMemsetAsync(ctx->dir.p, 0, nn * kDirChunks * sizeof(unsigned), s), "memset");
   check(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s), "memset");
   check(launch_pos_graph(d, ctx->tiles.p, s), "pos_graph launch");
-  check(launch_initial_ready(d, s), "initial_ready launch");
+  check(launch_initial_ready(d, ctx->tiles.p, s), "initial_ready launch");
   check(cudaEventRecord(ctx->ev[1], s), "event");
   int grid = 0;
   check(launch_eliminate(d, o.grid_ctas, s, &grid), "eliminate launch");

@@ -246,12 +246,86 @@ __global__ void __launch_bounds__(kHT) pos_fill_heavy_kernel(FactorDev d) {
 }
 
 // ---------------------------------------------------------------- K2
-__global__ void initial_ready_kernel(FactorDev d) {
-  if (d.ctrl->status != 0) return;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+// The initial frontier is published in ascending position order (a
+// deterministic compaction instead of warp-aggregated appends): the heads of
+// the longest dependency chains tend to be the lowest positions (every chain
+// climbs in position), and the FIFO serves them first.
+constexpr int kReadyThreads = 1024;
+constexpr int kReadyItems = 4;
+constexpr int kReadyTile = kReadyThreads * kReadyItems;
+
+__device__ __forceinline__ void ready_flags(const FactorDev& d, int p, int& m, int& b) {
   const bool ready = p < d.n && (d.cnt[p] & 0xffffffffull) == 0;
   const bool big = ready && d.fdeg[p] > kSmallCap;  // no fills yet: R = forward degree
-  publish(d, ready, big, p, lane_id());
+  m = ready && !big;
+  b = big;
+}
+
+// per tile: counts of main / big ready positions
+__global__ void __launch_bounds__(kReadyThreads) ready_count_kernel(FactorDev d, long long* tile_cnt) {
+  __shared__ long long smem[32];
+  long long cm = 0, cb = 0;
+#pragma unroll
+  for (int i = 0; i < kReadyItems; ++i) {
+    int m, b;
+    ready_flags(d, blockIdx.x * kReadyTile + i * kReadyThreads + threadIdx.x, m, b);
+    cm += m;
+    cb += b;
+  }
+  long long tm, tb;
+  block_exclusive_scan(cm, smem, &tm);
+  block_exclusive_scan(cb, smem, &tb);
+  if (threadIdx.x == 0) {
+    tile_cnt[2 * blockIdx.x] = tm;
+    tile_cnt[2 * blockIdx.x + 1] = tb;
+  }
+}
+
+// one CTA: exclusive scan of the tile counts; queue tails
+__global__ void ready_scan_kernel(FactorDev d, long long* tile_cnt, int tiles) {
+  __shared__ long long smem[32];
+  long long base_m = 0, base_b = 0;
+  for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const long long vm = t < tiles ? tile_cnt[2 * t] : 0, vb = t < tiles ? tile_cnt[2 * t + 1] : 0;
+    long long sm, sb;
+    const long long om = block_exclusive_scan(vm, smem, &sm);
+    const long long ob = block_exclusive_scan(vb, smem, &sb);
+    if (t < tiles) {
+      tile_cnt[2 * t] = base_m + om;
+      tile_cnt[2 * t + 1] = base_b + ob;
+    }
+    base_m += sm;
+    base_b += sb;
+  }
+  if (threadIdx.x == 0) {
+    d.ctrl->q_tail = static_cast<int>(base_m);
+    d.ctrl->b_tail = static_cast<int>(base_b);
+  }
+}
+
+// each tile writes its ready positions in order at its offsets
+__global__ void __launch_bounds__(kReadyThreads) ready_scatter_kernel(FactorDev d, const long long* tile_off) {
+  __shared__ long long smem[32];
+  long long om = tile_off[2 * blockIdx.x], ob = tile_off[2 * blockIdx.x + 1];
+  // blocked layout: thread t owns positions base + t*kReadyItems .. + kReadyItems - 1
+  const int p0 = blockIdx.x * kReadyTile + threadIdx.x * kReadyItems;
+  int m[kReadyItems], b[kReadyItems];
+  long long cm = 0, cb = 0;
+#pragma unroll
+  for (int i = 0; i < kReadyItems; ++i) {
+    ready_flags(d, p0 + i, m[i], b[i]);
+    cm += m[i];
+    cb += b[i];
+  }
+  long long tm, tb;
+  long long xm = block_exclusive_scan(cm, smem, &tm) + om;
+  long long xb = block_exclusive_scan(cb, smem, &tb) + ob;
+#pragma unroll
+  for (int i = 0; i < kReadyItems; ++i) {
+    if (m[i]) d.queue[xm++] = p0 + i;
+    if (b[i]) d.bqueue[xb++] = p0 + i;
+  }
 }
 
 // ---------------------------------------------------------------- K4
@@ -316,12 +390,16 @@ cudaError_t launch_pos_graph(const FactorDev& d, long long* tile_scratch, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_initial_ready(const FactorDev& d, cudaStream_t s) {
+cudaError_t launch_initial_ready(const FactorDev& d, long long* tile_scratch, cudaStream_t s) {
   if (d.n == 0) return cudaSuccess;
-  initial_ready_kernel<<<(d.n + 255) / 256, 256, 0, s>>>(d);
-  note_launches(1);
+  const int tiles = (d.n + kReadyTile - 1) / kReadyTile;
+  ready_count_kernel<<<tiles, kReadyThreads, 0, s>>>(d, tile_scratch);
+  ready_scan_kernel<<<1, 1024, 0, s>>>(d, tile_scratch, tiles);
+  ready_scatter_kernel<<<tiles, kReadyThreads, 0, s>>>(d, tile_scratch);
+  note_launches(3);
   return cudaGetLastError();
 }
+int initial_ready_scratch(int n) { return 2 * ((n + kReadyTile - 1) / kReadyTile) + 2; }
 
 cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, double* vals,
                             long long* tile_scratch, cudaStream_t s) {

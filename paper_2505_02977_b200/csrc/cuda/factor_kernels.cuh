@@ -104,7 +104,8 @@ struct FactorDev {
 
 // Launchers (stream-ordered). All return cudaError_t of the launch.
 cudaError_t launch_pos_graph(const FactorDev& d, long long* tile_scratch, cudaStream_t s);
-cudaError_t launch_initial_ready(const FactorDev& d, cudaStream_t s);
+cudaError_t launch_initial_ready(const FactorDev& d, long long* tile_scratch, cudaStream_t s);
+int initial_ready_scratch(int n);  // long longs of tile_scratch launch_initial_ready needs
 cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used);
 cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, double* vals,
                             long long* tile_scratch, cudaStream_t s);

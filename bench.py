@@ -149,10 +149,22 @@ def dist_setup(n_gpus: int):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PARAC_BENCH_SAME_DEVICE") == "1":
+            # test hook (tests/test_multirank_gpu.py): every rank on cuda:0 over
+            # gloo, so the N>1 path runs on a one-GPU box. Not a bench setting.
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     return rank, world, local, pg
+
+
+def _reduce_device(pg, device):
+    """Tensors for torch.distributed ops: the GPU under NCCL, the host under gloo."""
+    return device if pg is not None and pg.get_backend() == "nccl" else "cpu"
 
 
 def barrier(pg, device):
@@ -167,9 +179,18 @@ def allreduce(pg, device, value: float, op: str) -> float:
     if pg is None:
         return value
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=_reduce_device(pg, device))
     pg.all_reduce(t, op=getattr(pg.ReduceOp, op))
     return float(t.item())
+
+
+def gather_to_all(pg, obj):
+    """Every rank's `obj`, in rank order (reporting only, never on the data path)."""
+    if pg is None:
+        return [obj]
+    out = [None] * pg.get_world_size()
+    pg.all_gather_object(out, obj)
+    return out
 
 
 def workload_config(workload: str, n: int, edges: int) -> dict:
@@ -506,6 +527,19 @@ def run_ours(args):
             cpu_base = {"value": None, "unit": "nnz/s", "cores": 0, "kind": "reference",
                         "sample": f"unavailable: {exc}"}
 
+    ctx.close()
+    # BASELINE config[4] at this N: the 64 x 64^3 batch split over the ranks
+    # (the north_star's "reported at 1, 2, 4 and 8 GPUs"), as a sub-record of
+    # the headline line so the driver's scaling run yields that curve too
+    batch = None
+    if not args.no_batch and workload == "poisson3d_128":
+        try:
+            batch = measure_batch(args, P, L, torch, rank, world, local, pg, e2e=False)
+            batch.pop("clocks", None)
+            batch["n_gpus"] = world
+        except Exception as exc:
+            batch = {"value": None, "error": str(exc)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
@@ -530,18 +564,19 @@ def run_ours(args):
             "cpu_baseline": cpu_base,
             "gpu_launches": launches,
             "clocks": clk,
+            "batch": batch,
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
     if pg is not None:
         pg.destroy_process_group()
 
 
-def run_ours_batch(args, P, L, torch, rank, world, local, pg):
+def measure_batch(args, P, L, torch, rank, world, local, pg, e2e=True):
     """BASELINE config[4]: 64 independent gen_poisson3d(64) problems (problem i:
     ordering_random(n, i), seed i) split round-robin over the ranks; each rank
     factors its share in ONE device pass (disjoint-union batch, byte-identical
-    per-problem factors). No collective on the data path."""
+    per-problem factors). No collective on the data path: the ranks only meet
+    at the timing barriers and the max/sum reductions of the result."""
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     lib = P.rchol.lib
@@ -586,8 +621,6 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
     clk = clocks.stop() if clocks else None
     max_dev_s = allreduce(pg, device, sum(dev_ms) / 1e3, "MAX")
     total_nnz = allreduce(pg, device, float(nnz_total * args.steps), "SUM")
-    value = total_nnz / max_dev_s
-    # e2e: parac_gpu_factor_batch from pinned host inputs + download of every factor
     zs = []
     for i in range(len(mine)):
         z = C.c_int64()
@@ -596,29 +629,54 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
     outs = [[pinned_copy(P, np.zeros(k, dt)) for k, dt in
              ((g.n + 1, np.int64), (max(z, 1), np.int32), (max(z, 1), np.float64), (g.n, np.float64))]
             for z in zs]
-    barrier(pg, device)
-    e2e_s = []
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(device)
-        t0 = time.perf_counter()
-        check(lib.parac_gpu_factor_batch(ctx.handle, len(mine), csrs, pptr, seeds.ctypes.data, C.byref(opts),
-                                         C.byref(info)))
+    res = {"value": total_nnz / max_dev_s, "unit": "nnz/s", "ms_per_step": max_dev_s / args.steps * 1e3,
+           "eliminate_k3_ms": sum(k3_ms) / len(k3_ms), "problems": 64, "problems_per_gpu": len(mine),
+           "nnz_G_per_gpu": nnz_total, "fills_per_gpu": F, "nnz_off_per_gpu": Z, "n_per_gpu": info.n,
+           "edges_per_gpu": g.num_edges() * len(mine), "launches": launches, "clocks": clk,
+           "scaling": "strong", "what": "64 x gen_poisson3d(64) split round-robin over the ranks, "
+                                       "one disjoint-union device pass per rank, max-over-ranks device time"}
+    # e2e: parac_gpu_factor_batch from pinned host inputs + download of every factor
+    if e2e:
+        barrier(pg, device)
+        e2e_s = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            check(lib.parac_gpu_factor_batch(ctx.handle, len(mine), csrs, pptr, seeds.ctypes.data, C.byref(opts),
+                                             C.byref(info)))
+            for i, o in enumerate(outs):
+                check(lib.parac_gpu_download_batch(ctx.handle, i, o[0][0], o[1][0], o[2][0], o[3][0]))
+            e2e_s.append(time.perf_counter() - t0)
+        barrier(pg, device)
+        e2e_total = allreduce(pg, device, sum(e2e_s), "MAX")
+        h2d = len(mine) * (8 * (g.n + 1) + 12 * 2 * g.num_edges() + 4 * g.n)
+        d2h = sum(8 * (g.n + 1) + 12 * z + 8 * g.n for z in zs)
+        res["e2e"] = {"value": total_nnz / e2e_total, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3}
+    else:  # outputs of the last resident pass
         for i, o in enumerate(outs):
             check(lib.parac_gpu_download_batch(ctx.handle, i, o[0][0], o[1][0], o[2][0], o[3][0]))
-        e2e_s.append(time.perf_counter() - t0)
-    barrier(pg, device)
-    e2e_total = allreduce(pg, device, sum(e2e_s), "MAX")
-    e2e_value = total_nnz / e2e_total
-    h2d = len(mine) * (8 * (g.n + 1) + 12 * 2 * g.num_edges() + 4 * g.n)
-    d2h = sum(8 * (g.n + 1) + 12 * z + 8 * g.n for z in zs)
-    f0 = P.LdlFactor(g.n, outs[0][0][1], outs[0][1][1][:zs[0]], outs[0][2][1][:zs[0]], outs[0][3][1], perms[0])
+    sums = {}
+    for i, (p, o, z) in enumerate(zip(mine, outs, zs)):
+        f = P.LdlFactor(g.n, o[0][1], o[1][1][:z], o[2][1][:z], o[3][1], perms[i])
+        sums[p] = f"{f.checksum():016x}"
+    allsums = {}
+    for part in gather_to_all(pg, sums):
+        allsums.update(part)
+    res["checksums"] = [allsums.get(i) for i in range(64)]
+    res["factor0_checksum"] = allsums.get(0)
+    ctx.close()
+    return res
+
+
+def run_ours_batch(args, P, L, torch, rank, world, local, pg):
+    res = measure_batch(args, P, L, torch, rank, world, local, pg)
+    device = torch.device("cuda", local)
     peak, peak_src = read_peaks()
-    E = g.num_edges() * len(mine)
-    n = g.n * len(mine)
-    by = algorithmic_bytes(n, E, Z, F)
-    k3_avg_s = sum(k3_ms) / len(k3_ms) / 1e3
-    achieved = by["k3"] / k3_avg_s / 1e9
+    g_n, g_e = 64 ** 3, res["edges_per_gpu"] // res["problems_per_gpu"]
+    by = algorithmic_bytes(res["n_per_gpu"], res["edges_per_gpu"], res["nnz_off_per_gpu"], res["fills_per_gpu"])
+    achieved = by["k3"] / (res["eliminate_k3_ms"] / 1e3) / 1e9
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -633,28 +691,27 @@ def run_ours_batch(args, P, L, torch, rank, world, local, pg):
                         "sample": f"unavailable: {exc}"}
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+            "metric": METRIC, "value": res["value"], "unit": "nnz/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": max_dev_s / args.steps * 1e3, "higher_is_better": True,
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_poisson3d(64) x 64; problem i: ordering_random(n, i), seed i)",
-            "config": workload_config("batch_64x64", g.n, g.num_edges()),
-            "factor": {"problems_per_gpu": len(mine), "nnz_G_per_gpu": nnz_total,
-                       "factor0_checksum": f"{f0.checksum():016x}",
+            "config": workload_config("batch_64x64", g_n, g_e),
+            "factor": {"problems_per_gpu": res["problems_per_gpu"], "nnz_G_per_gpu": res["nnz_G_per_gpu"],
+                       "factor0_checksum": res["factor0_checksum"], "checksums": res["checksums"],
                        "per_gpu": "its share of the 64 problems as one disjoint-union device pass",
                        "parallelism": f"batch split x{world}"},
-            "factor_ms": {"device": max_dev_s / args.steps * 1e3, "eliminate_k3": sum(k3_ms) / len(k3_ms)},
-            "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},
+            "factor_ms": {"device": res["ms_per_step"], "eliminate_k3": res["eliminate_k3_ms"]},
+            "e2e": res["e2e"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "eliminate_kernel (K3)",
                          "algorithmic_bytes": by["k3"], "peak_source": peak_src},
             "cpu_baseline": cpu_base,
-            "gpu_launches": launches,
-            "clocks": clk,
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
+    del device
     if pg is not None:
         pg.destroy_process_group()
 
@@ -669,6 +726,7 @@ def main():
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true")
+    ap.add_argument("--no-batch", action="store_true", help="skip the 64x64^3 batch sub-record")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")

@@ -173,6 +173,9 @@ typedef struct {
   int32_t grid_ctas;             /* persistent-kernel CTAs; <=0: occupancy-sized */
   int32_t delay_ns;              /* >0: random __nanosleep injection (TestHooks::delay) */
   int32_t record_times;          /* ParOptions::record_vertex_times: start/end per position */
+  int32_t trace_phases;          /* != 0: TestHooks::on_phase analogue -- snapshot every dependency
+                                    counter at the phase boundaries of trace_position's elimination */
+  int32_t trace_position;        /* the position traced when trace_phases != 0 */
 } parac_gpu_options;
 void parac_gpu_default_options(parac_gpu_options* opt);
 
@@ -243,6 +246,16 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
  * and sorted, 2 merged, 3 column written, 4 weight-sorted + suffix, 5 fills
  * emitted, 6 decremented, 7 end (after publishing). Zero = phase skipped. */
 int parac_gpu_download_times(parac_gpu_ctx* ctx, uint64_t* start_end);
+/* TestHooks::on_phase (include/parac/factor_par.hpp:16-29, src/factor_par.cpp:112-120)
+ * analogue of the last factor run with trace_phases set: dp[p*n + i] = the
+ * dependency counter of position i as the eliminating warp/CTA read it at
+ * phase p of trace_position's elimination (0 gathered, 1 sampled = after its
+ * fill emissions, 2 decremented); taken[p] = 1 when phase p was reached
+ * (a position with no merged entries stops after "gathered", as in the
+ * reference). Counters of other positions may move concurrently, exactly as
+ * under the reference's worker pool. */
+int parac_gpu_download_phase_snapshots(parac_gpu_ctx* ctx, int64_t* dp, int32_t* taken);
+
 /* Diagnostics: sub-phase timestamps sub[8*k + i] (then 4 rank-sort cycle counters per position at sub[8*n + 4*k]) of the same run (i = 0 setup
  * loads done, 1 gather landed, 2 weight sort done, 3 samples drawn, 4 fills
  * written, 5 release fence done; zero = not recorded on that path). */

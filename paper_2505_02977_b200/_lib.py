@@ -43,7 +43,7 @@ class parac_gpu_options(C.Structure):
     _fields_ = [("fill_pool_entries", i64), ("column_arena_entries", i64),
                 ("first_chunk", i32), ("watchdog_seconds", f64), ("record_stats", i32),
                 ("verify", i32), ("grid_ctas", i32), ("delay_ns", i32),
-                ("record_times", i32)]
+                ("record_times", i32), ("trace_phases", i32), ("trace_position", i32)]
 
 
 class parac_gpu_factor_info(C.Structure):
@@ -85,6 +85,7 @@ SIGNATURES = {
     "parac_gpu_download": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "parac_gpu_download_times": (C.c_int, [vp, vp]),
     "parac_gpu_download_subtimes": (C.c_int, [vp, vp]),
+    "parac_gpu_download_phase_snapshots": (C.c_int, [vp, vp, vp]),
     "parac_gpu_upload_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp]),
     "parac_gpu_factor_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp, P(parac_gpu_options),
                                          P(parac_gpu_factor_info)]),

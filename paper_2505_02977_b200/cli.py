@@ -134,6 +134,29 @@ def run_factor(graph, ordering, backend: str, seed: int, ctx, record_times=False
     return f, stats
 
 
+def hbm_peak_gbs() -> float:
+    """The measured HBM copy bandwidth (MEASURED_PEAKS.json at the repo root,
+    driver-written), else the B200 profiling recipe's fallback."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def device_metrics(graph: R.LaplacianGraph, factor: R.LdlFactor, st: R.FactorStats) -> dict:
+    """SURVEY §5 metrics next to the reference's stats keys: device and
+    wall seconds of the factorization and the achieved HBM bandwidth of its
+    algorithmic bytes B_fact = 16(n+1) + 8n + 12E + 40F + 20Z."""
+    n, E, Z, F = factor.n, graph.num_edges(), factor.nnz_off_diagonal(), int(st.total_fills)
+    b_fact = 16 * (n + 1) + 8 * n + 12 * E + 40 * F + 20 * Z
+    dev_s = st.device_ms / 1e3
+    gbs = b_fact / dev_s / 1e9 if dev_s > 0 else 0.0
+    return {"device_seconds": dev_s, "wall_seconds": st.seconds, "eliminate_seconds": st.eliminate_ms / 1e3,
+            "algorithmic_bytes": b_fact, "hbm_gbs": gbs, "roofline_fraction": gbs / hbm_peak_gbs()}
+
+
 def emit_json(payload, path: str) -> None:
     """emit_json (parac_cli.cpp:136-144): nlohmann dump(2) = sorted keys, 2-space indent."""
     text = json.dumps(payload, indent=2, sort_keys=True) + "\n"
@@ -212,6 +235,7 @@ def cmd_factor(a, ctx) -> int:
              "nnz_g": f.nnz(), "nnz_g_off_diagonal": f.nnz_off_diagonal(), "fill_ratio": fill_ratio(g, f),
              "schedule_depth": depth, "total_fills": int(st.total_fills), "factor_seconds": st.seconds,
              "checksum": f.checksum()}
+    stats.update(device_metrics(g, f, st))
     if st.arena_used > 0:
         stats["arena_used"] = int(st.arena_used)
     emit_json(stats, a.stats)

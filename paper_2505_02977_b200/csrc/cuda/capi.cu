@@ -257,6 +257,9 @@ struct parac_gpu_ctx {
   DevBuf<Ctrl> ctrl;
   DevBuf<unsigned long long> vtimes, vsub;
   bool has_times = false;
+  DevBuf<long long> trace_dp;  // on_phase snapshots [3n]
+  DevBuf<int> trace_taken;     // [3]
+  int trace_n = -1;            // n of the last traced run, -1 none
   Ctrl last_ctrl{};
   long long last_z = 0;
   // resident factor (CSC, position space)
@@ -414,10 +417,34 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     d.keep_pos = kp && std::string(kp) == "width" ? 0 : 1;  // default: lowest position
     const char* kl = std::getenv("PARAC_KEEP_LIMIT");
     d.keep_limit = kl ? std::max(1, std::atoi(kl)) : 1 << 30;
+    const char* bl = std::getenv("PARAC_BIG_LAYOUT");
+    d.big_layout = bl ? std::atoi(bl) : 1;  // measured: 128^3 -2.3%, 27-point -2.9%, 2D -2.3% vs 0
+    // routing threshold: 64 on sparse graphs (mean degree <= 8), 128 on denser
+    // ones (see kSmallCap); PARAC_SMALL_CAP overrides (tuning)
+    const double mean_deg = n > 0 ? 2.0 * static_cast<double>(E) / n : 0.0;
+    d.small_cap = mean_deg <= 8.0 ? 64 : 96;
+    if (const char* sc = std::getenv("PARAC_SMALL_CAP")) d.small_cap = std::atoi(sc);
+    d.small_cap = std::max(1, std::min(d.small_cap, kSmallCap));
   }
   d.delay_ns = o.delay_ns;
   d.vtimes = nullptr;
   d.vsub = nullptr;
+  d.trace_k = -1;
+  d.trace_dp = nullptr;
+  d.trace_taken = nullptr;
+  ctx->trace_n = -1;
+  if (o.trace_phases) {
+    if (o.trace_position < 0 || o.trace_position >= n)
+      throw Failure{dimension_mismatch, "trace_position outside [0, n)"};
+    ctx->trace_dp.ensure(3 * nn);
+    ctx->trace_taken.ensure(3);
+    check(cudaMemsetAsync(ctx->trace_dp.p, 0xff, 3 * nn * sizeof(long long), s), "memset");
+    check(cudaMemsetAsync(ctx->trace_taken.p, 0, 3 * sizeof(int), s), "memset");
+    d.trace_k = o.trace_position;
+    d.trace_dp = ctx->trace_dp.p;
+    d.trace_taken = ctx->trace_taken.p;
+    ctx->trace_n = n;
+  }
   ctx->has_times = o.record_times != 0;
   if (o.record_times) {
     ctx->vtimes.ensure(8 * nn);
@@ -922,6 +949,16 @@ int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub) {
     require_ctx(ctx);
     if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
     check(cudaMemcpy(sub, ctx->vsub.p, sizeof(unsigned long long) * 12 * ctx->f_n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int parac_gpu_download_phase_snapshots(parac_gpu_ctx* ctx, int64_t* dp, int32_t* taken) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ctx->trace_n < 0 || ctx->f_n < 0) throw Failure{internal_error, "no traced factor run"};
+    if (dp)
+      check(cudaMemcpy(dp, ctx->trace_dp.p, sizeof(long long) * 3 * ctx->trace_n, cudaMemcpyDeviceToHost), "d2h");
+    if (taken) check(cudaMemcpy(taken, ctx->trace_taken.p, sizeof(int) * 3, cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

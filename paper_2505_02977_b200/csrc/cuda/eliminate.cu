@@ -42,7 +42,7 @@ constexpr int kSmallBytes = kSmallCap * 8 * 5;
 // big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
 constexpr int kBigBytes = kBigCap * 8 * 5;
 constexpr int kCtaSmem = kWarps * kSmallBytes > kBigBytes ? kWarps * kSmallBytes : kBigBytes;
-constexpr int kBatch = 4;  // samples / decrements per lane in flight (small path)
+constexpr int kBatch = (kSmallCap + 31) / 32;  // samples / decrements per lane in flight (small path): one batch
 
 // Role of this CTA. On a full grid the role follows the SM (every 4th SM runs
 // only big CTAs) so each SM executes a single code path and its instruction
@@ -84,6 +84,28 @@ struct Next {
   int fdeg;     // forward degree (-1: unknown)
   int fc;       // fills received
   long long fb; // forward-CSR offset
+};
+
+// Shared state of a big CTA (one vertex at a time).
+struct CtaShared {
+  int k;
+  int m;
+  int nready;
+  int emitted;
+  int carry_row;
+  int bad;
+  double lkk;
+  long long start;
+  long long slab;      // this CTA's wide-column slab (entries), -1 none
+  int slab_cap;
+  long long fb;        // cta_prologue: forward offset, degree, raw size
+  int fdeg, R;
+  unsigned dirrow[kDirChunks];
+  int wcount[kWarps];
+  unsigned long long best[kWarps];
+  int next_R;          // raw size of the kept vertex
+  int mbump, mcount;   // cta_hash_merge: stage bump, distinct rows
+  int hbad;            // cta_hash_merge: a run longer than kRunCap
 };
 
 // ------------------------------------------------------------ claiming
@@ -401,6 +423,92 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], 
   if (cyc && tid == 0) cyc[2] = clock64() - c0;
 }
 
+// All-pairs stable rank with broadcast shared-memory reads: element g of the
+// R keys gets
+//   rank = #{t : X[t] < k_g} + (STABLE ? #{t < g : X[t] == k_g} : 0)
+// (raw keys are unique; the weight sort needs the stable tie rule). One
+// barrier, broadcast 16-byte loads and four independent compare/accumulate
+// chains per element: no dependent binary-search rounds, no barriers per
+// round. The stable rule is free outside the 32-key block holding g's own
+// warp: keys before that block count when <= k (compare against k + 1),
+// keys after it when < k; inside it the threshold switches at g.
+
+// c += #{keys of pairs [q0, q1) of P below thr} (two accumulators per element)
+__device__ __forceinline__ void count_below(const ulonglong2* P, int q0, int q1, unsigned long long thr, int& ca,
+                                            int& cb) {
+#pragma unroll 2
+  for (int q = q0; q < q1; ++q) {
+    const ulonglong2 p = P[q];
+    ca += static_cast<int>(p.x < thr);
+    cb += static_cast<int>(p.y < thr);
+  }
+}
+// The mixed block (keys t = 2q, 2q+1 relative to the block): threshold k + 1
+// before position `pos` in the block, k from it on.
+__device__ __forceinline__ void count_below_mixed(const ulonglong2* P, int pairs, unsigned long long k, int pos,
+                                                  int& ca, int& cb) {
+  const unsigned long long k1 = k + 1;
+#pragma unroll 2
+  for (int q = 0; q < pairs; ++q) {
+    const ulonglong2 p = P[q];
+    ca += static_cast<int>(p.x < (2 * q < pos ? k1 : k));
+    cb += static_cast<int>(p.y < (2 * q + 1 < pos ? k1 : k));
+  }
+}
+
+// CTA: element g = threadIdx.x < R <= NT (one per thread); the first NT
+// threads take part (NT < kThreads: named barrier 1, the other warps are free
+// to do something else meanwhile).
+template <bool STABLE, int NT = kThreads>
+__device__ __forceinline__ int bcast_rank_cta(unsigned long long k, int R, unsigned long long* X) {
+  const int tid = threadIdx.x, lane = tid & 31, wb = tid & ~31;
+  if (tid < R) X[tid] = k;
+  if (tid == 0 && (R & 1)) X[R] = ~0ull;  // pad the last pair: never below a threshold
+  if (NT == kThreads) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(X);
+  const int pairs = (R + 1) >> 1;
+  int ca = 0, cb = 0;
+  if (!STABLE) {
+    count_below(X2, 0, pairs, k, ca, cb);
+  } else {
+    const int qm = min(wb >> 1, pairs), qe = min((wb + 32) >> 1, pairs);
+    count_below(X2, 0, qm, k + 1, ca, cb);                   // keys before g's warp block: <= k
+    count_below_mixed(X2 + qm, qe - qm, k, lane, ca, cb);    // g's warp block
+    count_below(X2, qe, pairs, k, ca, cb);                   // keys after it: < k
+  }
+  return ca + cb;
+}
+
+// Warp: element g = i*32 + lane of R <= 32*ITEMS; block b holds keys
+// [32b, 32b+32), item i's own block is b == i (compile-time).
+template <int ITEMS, bool STABLE>
+__device__ __forceinline__ void bcast_rank_warp(const unsigned long long (&k)[ITEMS], int R, unsigned long long* X,
+                                                int (&rank)[ITEMS]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if (i * 32 + lane < R) X[i * 32 + lane] = k[i];
+  if (lane == 0 && (R & 1)) X[R] = ~0ull;
+  __syncwarp();
+  const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(X);
+  int ca[ITEMS], cb[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) ca[i] = cb[i] = 0;
+#pragma unroll 1
+  for (int b = 0; b * 32 < R; ++b) {
+    const ulonglong2* P = X2 + 16 * b;
+    const int pairs = (min(32, R - 32 * b) + 1) >> 1;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (STABLE && i == b) count_below_mixed(P, pairs, k[i], lane, ca[i], cb[i]);
+      else count_below(P, 0, pairs, STABLE && i > b ? k[i] + 1 : k[i], ca[i], cb[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) rank[i] = ca[i] + cb[i];
+}
+
 // ---- warp path (rank sort): gather + raw sort, weight sort (results in A/B)
 template <int ITEMS>
 __device__ __forceinline__ void warp_rank_raw(const FactorDev& d, int k, long long fb, int fdeg, int R,
@@ -422,7 +530,7 @@ __device__ __forceinline__ void warp_rank_raw(const FactorDev& d, int k, long lo
     *stamp = globaltimer_ns();
   }
   int rank[ITEMS];
-  rank_sort<32, ITEMS>(key, R, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kSmallCap, rank);
+  bcast_rank_warp<ITEMS, false>(key, R, S.X1, rank);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (i * 32 + lane < R) {
@@ -443,7 +551,7 @@ __device__ __forceinline__ void warp_rank_weight(int m, Scratch S, int lane) {
     ak[i] = g < m ? S.A[g] : ~0ull;
   }
   int rank[ITEMS];
-  rank_sort<32, ITEMS>(wk, m, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kSmallCap, rank);
+  bcast_rank_warp<ITEMS, true>(wk, m, S.X1, rank);
   __syncwarp();  // every lane has read A/B
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -479,7 +587,12 @@ __device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long lon
   }
   int rank[ITEMS];
   long long* cyc = d.vsub ? reinterpret_cast<long long*>(d.vsub + d.n * 8ll + 4ll * k) : nullptr;
-  rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kBigCap, rank, cyc);
+  if constexpr (ITEMS == 1) {
+    (void)cyc;
+    rank[0] = bcast_rank_cta<false>(key[0], R, S.X1);
+  } else {
+    rank_sort<kThreads, ITEMS>(key, R, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kBigCap, rank, cyc);
+  }
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (i * kThreads + static_cast<int>(threadIdx.x) < R) {
@@ -488,6 +601,170 @@ __device__ __forceinline__ void cta_rank_raw(const FactorDev& d, int k, long lon
     }
   }
   __syncthreads();
+}
+
+// ---- CTA path: gather + merge by hashing (R <= kBigCap), no raw sort.
+// factor_common.hpp:100-113 sorts the raw column by (row, source) and sums
+// each row's run left to right. Only two orders matter for the bits: rows
+// ascending (the merged column) and sources ascending inside a row (the
+// summation order). So: hash the raw entries by row (shared-memory open
+// addressing + a per-row list), let every entry count the entries of its row
+// with a smaller key (its place in the run; sources are unique per row, see
+// DESIGN.md), stage each run contiguously in that order, let the run's first
+// entry sum it serially, then rank the m distinct rows with 32-bit broadcast
+// compares. Output: merged (row << 32 | multiplicity, sum) in row order in
+// (X1, X2). Returns m, or -1 when a row's run is longer than kRunCap (then the
+// caller falls back to the full raw sort).
+constexpr int kRunCap = 64;
+template <int ITEMS>
+__device__ __forceinline__ int cta_hash_merge(const FactorDev& d, int k, long long fb, int fdeg, int R,
+                                              const unsigned* dirrow, Scratch S, CtaShared& sh,
+                                              unsigned long long* stamp) {
+  const int tid = threadIdx.x;
+  int* tab = reinterpret_cast<int*>(S.X1);   // slot -> row, then slot -> stage base
+  int* head = reinterpret_cast<int*>(S.X2);  // slot -> last pushed entry
+  int* nxt = reinterpret_cast<int*>(S.C);    // entry -> next entry of its row
+  int* rows32 = nxt + kBigCap;               // distinct rows (unordered)
+  double* stage = S.B;                       // runs, contiguous, source order
+  const int hbits = 32 - __clz(max(2 * R - 1, 1));  // table of 2^hbits >= 2R slots
+  const int hs = 1 << hbits;
+  unsigned long long key[ITEMS];
+  double w[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * kThreads + tid;
+    key[i] = ~0ull;
+    w[i] = 0.0;
+    if (g < R) load_raw_dir(d, k, fb, fdeg, g, dirrow, key[i], w[i]);
+  }
+  for (int t = tid; t < hs; t += kThreads) {
+    tab[t] = -1;
+    head[t] = -1;
+  }
+  if (tid == 0) {
+    sh.mbump = 0;
+    sh.mcount = 0;
+    sh.hbad = 0;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * kThreads + tid;
+    if (g < R) S.A[g] = key[i];
+  }
+  if (stamp) {  // diagnostics: every thread's gather has landed
+    __syncthreads();
+    if (tid == 0) *stamp = globaltimer_ns();
+  }
+  __syncthreads();
+  // diagnostics (record_times): clock64 at the step barriers, 4 slots per position
+  long long* cyc = stamp && tid == 0 ? reinterpret_cast<long long*>(d.vsub + d.n * 8ll + 4ll * k) : nullptr;
+  const long long c0 = cyc ? clock64() : 0;
+  // insert: slot of the row, push the entry on the row's list
+  int slot[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * kThreads + tid;
+    slot[i] = -1;
+    if (g < R) {
+      const int row = static_cast<int>(key[i] >> 32);
+      int h = static_cast<int>((static_cast<unsigned>(row) * 0x9E3779B1u) >> (32 - hbits));
+      while (true) {
+        const int old = atomicCAS(&tab[h], -1, row);
+        if (old == -1 || old == row) break;
+        h = (h + 1) & (hs - 1);
+      }
+      slot[i] = h;
+      nxt[g] = atomicExch(&head[h], g);
+    }
+  }
+  __syncthreads();
+  if (cyc) cyc[0] = clock64() - c0;
+  // place in the run = entries of the row with a smaller key; run length
+  int pos[ITEMS], len[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    pos[i] = 0;
+    len[i] = 0;
+    if (slot[i] >= 0) {
+      int h = head[slot[i]];
+      while (h >= 0 && len[i] <= kRunCap) {
+        pos[i] += static_cast<int>(S.A[h] < key[i]);
+        ++len[i];
+        h = nxt[h];
+      }
+      if (len[i] > kRunCap) sh.hbad = 1;
+    }
+  }
+  __syncthreads();  // every walk done: tab (rows) is free; hbad visible
+  if (cyc) cyc[1] = clock64() - c0;
+  if (sh.hbad) return -1;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if (slot[i] >= 0 && pos[i] == 0) tab[slot[i]] = atomicAdd(&sh.mbump, len[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if (slot[i] >= 0) stage[tab[slot[i]] + pos[i]] = w[i];
+  __syncthreads();
+  // run heads: serial sum in source order (merge_raw); (row, length, sum)
+  // go to slot j of compact arrays (rows32, nxt, head as doubles: all free now)
+  double* sumj = reinterpret_cast<double*>(head);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (slot[i] >= 0 && pos[i] == 0) {
+      const double* st = stage + tab[slot[i]];
+      double acc = st[0];
+      for (int q = 1; q < len[i]; ++q) acc = __dadd_rn(acc, st[q]);
+      const int j = atomicAdd(&sh.mcount, 1);
+      rows32[j] = static_cast<int>(key[i] >> 32);
+      nxt[j] = len[i];
+      sumj[j] = acc;
+    }
+  }
+  __syncthreads();
+  const int m = sh.mcount;
+  if (cyc) cyc[2] = clock64() - c0;
+  // rank of each distinct row (all-pairs, 32-bit, 4 rows per broadcast load),
+  // spread over every thread; results written after a barrier (the output
+  // overwrites the compact arrays)
+  const int4* R4 = reinterpret_cast<const int4*>(rows32);
+  const int quads = m >> 2;
+  int rk[ITEMS], rrow[ITEMS], rlen[ITEMS];
+  double rsum[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int j = i * kThreads + tid;
+    rk[i] = -1;
+    if (j < m) {
+      const int row = rows32[j];
+      int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll 4
+      for (int q = 0; q < quads; ++q) {
+        const int4 v = R4[q];
+        c0 += static_cast<int>(v.x < row);
+        c1 += static_cast<int>(v.y < row);
+        c2 += static_cast<int>(v.z < row);
+        c3 += static_cast<int>(v.w < row);
+      }
+      for (int t = 4 * quads; t < m; ++t) c0 += static_cast<int>(rows32[t] < row);
+      rk[i] = c0 + c1 + c2 + c3;
+      rrow[i] = row;
+      rlen[i] = nxt[j];
+      rsum[i] = sumj[j];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (rk[i] >= 0) {
+      S.X1[rk[i]] = (static_cast<unsigned long long>(static_cast<unsigned>(rrow[i])) << 32) |
+                    static_cast<unsigned>(rlen[i]);
+      reinterpret_cast<double*>(S.X2)[rk[i]] = rsum[i];
+    }
+  }
+  __syncthreads();
+  if (cyc) cyc[3] = clock64() - c0;
+  return m;
 }
 
 template <int ITEMS>
@@ -500,7 +777,8 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
     ak[i] = g < m ? S.A[g] : ~0ull;
   }
   int rank[ITEMS];
-  rank_sort<kThreads, ITEMS>(wk, m, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kBigCap, rank);
+  if constexpr (ITEMS == 1) rank[0] = bcast_rank_cta<true>(wk[0], m, S.X1);
+  else rank_sort<kThreads, ITEMS>(wk, m, S.X1, S.X2, reinterpret_cast<int*>(S.C), reinterpret_cast<int*>(S.C) + kBigCap, rank);
   __syncthreads();  // every thread has read A/B
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -830,6 +1108,16 @@ __device__ __forceinline__ unsigned long long keep_key(const FactorDev& d, unsig
                     : rr | (1ull << 63);
 }
 
+// TestHooks::on_phase analogue (factor_par.cpp:112-120): the eliminating
+// warp/CTA (t in [0, nt)) copies every dependency counter after its own
+// updates of this phase are performed (the caller has fenced). Inline: an
+// out-of-line call made ptxas spill around it (188 B vs 60 B in K3).
+__device__ __forceinline__ void snapshot_dp(const FactorDev& d, int phase, int t, int nt) {
+  long long* out = d.trace_dp + static_cast<long long>(phase) * d.n;
+  for (int i = t; i < d.n; i += nt) out[i] = dp_of(ld_relaxed_u64(&d.cnt[i]));
+  if (t == 0) d.trace_taken[phase] = 1;
+}
+
 // ============================================================ small path
 // One warp eliminates k (R <= kSmallCap). Returns the kept vertex, -1, or -2.
 __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane, bool allow_keep) {
@@ -851,7 +1139,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   // level[k] is final once k is ready (every predecessor raised it before its
   // releasing decrement); load it now, use it after the sampling phase
   const int lvk = d.level ? ld_relaxed(&d.level[k]) : 0;
-  if (R > kSmallCap) {  // mis-routed (cannot happen with exact routing): hand to a big CTA
+  if (R > d.small_cap) {  // mis-routed (cannot happen with exact routing): hand to a big CTA
     publish(d, lead, true, k, lane);
     return {-3, -1, 0, 0};
   }
@@ -863,9 +1151,10 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   // ---- 2. sort raw by (row, source)  (factor_common.hpp:100-104), in registers
   if (R <= 32) warp_rank_raw<1>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   else if (R <= 64) warp_rank_raw<2>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
-  else warp_rank_raw<4>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
+  else warp_rank_raw<kBatch>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   __syncwarp();
   PHASE(1);
+  if (k == d.trace_k) snapshot_dp(d, 0, lane, 32);
 
   // ---- 3. merge runs in place: left-to-right sums, multiplicity = run length
   //      (factor_common.hpp:105-113). Chunk c writes only below 32(c+1).
@@ -928,7 +1217,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   if (m >= 2) {
     if (m <= 32) warp_rank_weight<1>(m, S, lane);
     else if (m <= 64) warp_rank_weight<2>(m, S, lane);
-    else warp_rank_weight<4>(m, S, lane);
+    else warp_rank_weight<kBatch>(m, S, lane);
     __syncwarp();
     SUB(2);
     if (lead) serial_suffix(S.B, S.C, m);
@@ -980,6 +1269,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   fence_acq_rel();
   __syncwarp();
   SUB(5);
+  if (k == d.trace_k) snapshot_dp(d, 1, lane, 32);
   unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
   int nready = 0;
   {
@@ -1011,15 +1301,17 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   }
   __syncwarp();
   PHASE(6);
+  if (k == d.trace_k) snapshot_dp(d, 2, lane, 32);
   maybe_delay(d, k, 2);
   if (nready == 0) return {-1, -1, 0, 0};
 
-  // keep-one: the widest ready column this warp can hold; publish the rest
+  // keep-one: the best ready column this warp can hold (lowest position by
+  // default); publish the rest
   unsigned long long best = 0;
   for (int t = lane; t < nready; t += 32) {
     const unsigned long long rr = ready[t];
     const unsigned long long key = keep_key(d, rr);
-    if (static_cast<int>(rr >> 32) <= kSmallCap && key > best) best = key;
+    if (static_cast<int>(rr >> 32) <= d.small_cap && key > best) best = key;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1027,6 +1319,14 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
     best = other > best ? other : best;
   }
   const int keep = best && allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
+  // the kept column's forward offset and degree: loaded now, in flight while
+  // the others are published (its raw size comes with its ready entry)
+  long long kfb0 = 0, kfb1 = 0;
+  if (keep >= 0 && lead) {
+    kfb0 = d.fwd_ptr[keep];
+    kfb1 = d.fwd_ptr[keep + 1];
+  }
+  int kR = 0;
   for (int base = 0; base < nready; base += 32) {
     const int t = base + lane;
     bool pub = false, big = false;
@@ -1034,33 +1334,21 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
     if (t < nready) {
       const unsigned long long rr = ready[t];
       r = static_cast<int>(rr & 0xffffffffu);
-      big = static_cast<int>(rr >> 32) > kSmallCap;
+      big = static_cast<int>(rr >> 32) > d.small_cap;
       pub = r != keep;
+      if (r == keep) kR = static_cast<int>(rr >> 32);
     }
     publish(d, pub, big, r, lane);
   }
   if (keep < 0) return {-1, -1, 0, 0};
-  return {keep, -1, 0, 0};
+  kR = __reduce_max_sync(kFull, kR);
+  kfb0 = __shfl_sync(kFull, kfb0, 0);
+  kfb1 = __shfl_sync(kFull, kfb1, 0);
+  const int kfd = static_cast<int>(kfb1 - kfb0);
+  return {keep, kfd, kR - kfd, kfb0};
 }
 
 // ============================================================ big path
-struct CtaShared {
-  int k;
-  int m;
-  int nready;
-  int emitted;
-  int carry_row;
-  int bad;
-  double lkk;
-  long long start;
-  long long slab;      // this CTA's wide-column slab (entries), -1 none
-  int slab_cap;
-  long long fb;        // cta_prologue: forward offset, degree, raw size, level
-  int fdeg, R, lvk;
-  unsigned dirrow[kDirChunks];
-  int wcount[kWarps];
-  unsigned long long best[kWarps];
-};
 
 // The whole CTA eliminates k. Returns the kept vertex (any width), -1, or -2.
 // WIDE (raw size > kBigCap, R-MAT hubs) works in a global-memory slab; the
@@ -1068,19 +1356,139 @@ struct CtaShared {
 // compile to shared-memory instructions (a runtime select between slab and
 // shared memory made every access generic). cta_prologue (the caller) has
 // loaded fb / fdeg / R / level into sh.
-__device__ __forceinline__ void cta_prologue(const FactorDev& d, int k, CtaShared& sh) {
+__device__ __forceinline__ void cta_prologue(const FactorDev& d, int k, CtaShared& sh, bool known) {
   const int tid = threadIdx.x;
-  if (tid < kDirChunks)
-    sh.dirrow[tid] = static_cast<unsigned>(
-        ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
-  if (tid == 0) {
+  // a kept vertex arrives with its forward offset / degree / raw size (loaded
+  // by the keeper while it published the others): only a column with
+  // overflow fills still needs its directory row
+  if (!known || sh.R - sh.fdeg > d.c0) {
+    if (tid < kDirChunks)
+      sh.dirrow[tid] = static_cast<unsigned>(
+          ld_relaxed(reinterpret_cast<const int*>(d.dir + static_cast<long long>(k) * kDirChunks + tid)));
+  }
+  if (!known && tid == 0) {
     const long long fb = d.fwd_ptr[k];
     sh.fb = fb;
     sh.fdeg = static_cast<int>(d.fwd_ptr[k + 1] - fb);
     sh.R = sh.fdeg + static_cast<int>(ld_relaxed_u64(&d.cnt[k]) >> 32);
-    sh.lvk = d.level ? ld_relaxed(&d.level[k]) : 0;  // final once k is ready; used after sampling
   }
   __syncthreads();
+}
+
+// Steps 8-9 of a CTA elimination (sampling + emission, release, decrements,
+// keep-one + publish) over the weight-ordered column (S.A rows, S.B weights,
+// S.C suffix sums).
+template <bool WIDE>
+__device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, char* smem, CtaShared& sh,
+                                                  bool allow_keep, Scratch S, int m, double lkk, int lvk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool lead = tid == 0;
+  // ---- 8. sampling + emission, one sample per thread per round
+  const SampleKey sk = sample_key(d, k);
+  int emitted = 0;
+  bool bad = false;
+  for (int base = 0; base < m - 1; base += kThreads) {
+    const int i = base + tid;
+    int lo = 0, hi = 0, slot = 0;
+    double wv = 0.0;
+    const bool em = i < m - 1 &&
+                    draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv,
+                                WIDE && m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
+                                coarse_step(m));
+    if (base == 0) SUB(3);
+    if (em) {
+      slot = reserve_fill_slot(d, lo);
+      red_add_relaxed_u64(&d.cnt[hi], 1ull);
+      bad = bad || slot < 0;
+    }
+    __syncwarp();
+    if (em && !bad) bad = !write_fill(d, lo, slot, hi, k, wv);
+    emitted += __popc(__ballot_sync(kFull, em));
+  }
+  if (lane == 0) sh.wcount[warp] = emitted;
+  if (bad) sh.bad = 1;
+  __syncthreads();
+  SUB(4);
+  if (sh.bad) return -2;
+  if (lead) {
+    int e = 0;
+    for (int w2 = 0; w2 < kWarps; ++w2) e += sh.wcount[w2];
+    d.samples[k] = e;
+    sh.nready = 0;
+  }
+  if (d.level) {  // ASAP levels, as in the warp path
+    const int lk = lvk + 1;
+    for (int t = tid; t < m; t += kThreads) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
+  }
+  PHASE(5);
+  maybe_delay(d, k, 1);
+
+  // ---- 9. release, decrement, collect ready rows into C
+  fence_acq_rel();
+  __syncthreads();
+  SUB(5);
+  if (k == d.trace_k) snapshot_dp(d, 1, tid, kThreads);
+  unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
+  for (int t = tid; t < m; t += kThreads) {
+    const unsigned long long a = S.A[t];
+    const int row = static_cast<int>(a >> 32);
+    const int mult = static_cast<int>(a & 0xffffffffu);
+    const int fd = __ldg(&d.fdeg[row]);
+    const unsigned long long old = atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
+    if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
+    if (dp_of(old) == mult) ready[atomicAdd(&sh.nready, 1)] = ready_info(row, fd, old);
+  }
+  __syncthreads();
+  const int nready = sh.nready;
+  PHASE(6);
+  if (k == d.trace_k) snapshot_dp(d, 2, tid, kThreads);
+  maybe_delay(d, k, 2);
+  if (nready == 0) return -1;
+
+  // keep-one (any width) + publish the rest
+  unsigned long long best = 0;
+  for (int t = tid; t < nready; t += kThreads) {
+    const unsigned long long rr = keep_key(d, ready[t]);
+    best = rr > best ? rr : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(kFull, best, o);
+    best = other > best ? other : best;
+  }
+  if (lane == 0) sh.best[warp] = best;
+  __syncthreads();
+  best = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < kWarps; ++w2) best = sh.best[w2] > best ? sh.best[w2] : best;
+  const int keep = allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
+  // the kept column's forward offset and degree: loaded now, in flight while
+  // the others are published (its raw size comes with its ready entry)
+  long long kfb0 = 0, kfb1 = 0;
+  if (keep >= 0 && tid == kThreads - 1) {
+    kfb0 = d.fwd_ptr[keep];
+    kfb1 = d.fwd_ptr[keep + 1];
+  }
+  for (int base = 0; base < nready; base += kThreads) {
+    const int t = base + tid;
+    bool pub = false, big = false;
+    int r = 0;
+    if (t < nready) {
+      const unsigned long long rr = ready[t];
+      r = static_cast<int>(rr & 0xffffffffu);
+      big = static_cast<int>(rr >> 32) > d.small_cap;
+      pub = r != keep;
+      if (r == keep) sh.next_R = static_cast<int>(rr >> 32);
+    }
+    publish(d, pub, big, r, lane);
+  }
+  __syncthreads();  // ready list (C) is reused by the next elimination; next_R visible
+  if (keep >= 0 && tid == kThreads - 1) {
+    sh.fb = kfb0;
+    sh.fdeg = static_cast<int>(kfb1 - kfb0);
+    sh.R = sh.next_R;
+  }
+  return keep;
 }
 
 template <bool WIDE>
@@ -1094,7 +1502,8 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // ---- 1. gather (counts and the directory row were fetched by cta_prologue)
   const long long fb = sh.fb;
   const int fdeg = sh.fdeg;
-  const int lvk = sh.lvk;
+  // level[k] is final once k is ready; the load is first used after sampling
+  const int lvk = d.level ? ld_relaxed(&d.level[k]) : 0;
   const int R = sh.R;
   const int P = next_pow2(R);
   if (lead) {
@@ -1133,6 +1542,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // landed, raw sort done, merge done, weight sort done} in the 4 cycle slots
   unsigned long long* wst =
       (WIDE && d.vsub && lead) ? d.vsub + d.n * 8ll + 4ll * k : nullptr;
+  int hashed = -1;  // merged column size when cta_hash_merge merged it
   if (wide) {  // global slab: shared-memory tiles + merge passes
     // 8 raw entries in flight per thread (loads first, then the slab stores:
     // the stores may alias nothing the loads read, but the compiler cannot know)
@@ -1160,17 +1570,34 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     slab_sort(S.A, reinterpret_cast<unsigned long long*>(S.B), S.X1, S.X2, R, ~0ull, 0ull, sxb, RawLess{},
               wst ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
     if (wst) wst[1] = globaltimer_ns();
-  } else if (P <= kThreads) {
-    cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
-  } else if (P <= 2 * kThreads) {
-    cta_rank_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   } else {
-    cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+    // gather + hash merge; the raw sort + run merge only when a row's run is
+    // longer than kRunCap
+    unsigned long long* stamp = d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr;
+    const int mm = P <= kThreads       ? cta_hash_merge<1>(d, k, fb, fdeg, R, sh.dirrow, S, sh, stamp)
+                   : P <= 2 * kThreads ? cta_hash_merge<2>(d, k, fb, fdeg, R, sh.dirrow, S, sh, stamp)
+                                       : cta_hash_merge<4>(d, k, fb, fdeg, R, sh.dirrow, S, sh, stamp);
+    if (mm >= 0) {
+      hashed = mm;
+      unsigned long long* ta = S.A;
+      double* tb = S.B;
+      S.A = S.X1;
+      S.B = reinterpret_cast<double*>(S.X2);
+      S.X1 = ta;
+      S.X2 = reinterpret_cast<unsigned long long*>(tb);
+    } else if (P <= kThreads) {
+      cta_rank_raw<1>(d, k, fb, fdeg, R, sh.dirrow, S, nullptr);
+    } else if (P <= 2 * kThreads) {
+      cta_rank_raw<2>(d, k, fb, fdeg, R, sh.dirrow, S, nullptr);
+    } else {
+      cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
+    }
   }
   PHASE(1);
+  if (k == d.trace_k) snapshot_dp(d, 0, tid, kThreads);
 
   // ---- 3. merge runs (rows' multiplicities and left-to-right weight sums)
-  int m = 0;
+  int m = hashed >= 0 ? hashed : 0;
   if (WIDE) {
     // global slab: each thread owns a contiguous block of the sorted column;
     // pass 1 counts the segment heads in it (8 loads in flight), one CTA scan
@@ -1268,7 +1695,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
   if (lead) sh.carry_row = -1;
   __syncthreads();
-  for (int base = 0; !WIDE && base < R; base += kThreads) {
+  for (int base = 0; !WIDE && hashed < 0 && base < R; base += kThreads) {
     const int t = base + tid;
     const int row = t < R ? static_cast<int>(S.A[t] >> 32) : -2;
     const int prev = tid == 0 ? sh.carry_row : (t - 1 < R ? static_cast<int>(S.A[t - 1] >> 32) : -2);
@@ -1310,7 +1737,54 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     return -1;
   }
 
-  // ---- 5. lkk + column
+  // ---- 5-7. lkk + column, weight sort + suffix
+  if (!WIDE && m >= 2 && m <= kThreads - 32) {
+    // Overlapped: the last warp holds no element of the weight sort, so its
+    // lead runs the serial lkk chain over B (row order, left intact) while
+    // warps 0..6 rank the weights and scatter the weight-ordered column to
+    // (X2, C). Then every thread writes its column entry from registers
+    // while thread 0 runs the serial suffix chain into B.
+    const int g = tid;
+    const unsigned long long wk = g < m ? dbits(S.B[g]) : kInfBits;
+    const unsigned long long ak = g < m ? S.A[g] : ~0ull;
+    unsigned long long* WA = S.X2;
+    double* WB = S.C;
+    if (warp == kWarps - 1) {
+      if (lane == 0) sh.lkk = serial_total(S.B, m);
+    } else {
+      const int r = bcast_rank_cta<true, kThreads - 32>(wk, m, S.X1);
+      if (g < m) {
+        WA[r] = ak;
+        WB[r] = bitsd(wk);
+      }
+    }
+    if (lead) sh.start = static_cast<long long>(start_reg);
+    __syncthreads();
+    const double lkk = sh.lkk;
+    const long long start = sh.start;
+    if (start + m > d.arena_cap) {
+      if (lead) fail(d, kErrArena, k);
+      return -2;
+    }
+    if (lead) {
+      d.diag[k] = lkk;
+      d.col_start[k] = start;
+      d.col_len[k] = m;
+    }
+    if (g < m) {
+      d.arena_rows[start + g] = static_cast<int>(ak >> 32);
+      d.arena_vals[start + g] = __ddiv_rn(-bitsd(wk), lkk);
+    }
+    PHASE(3);
+    SUB(2);
+    if (lead) serial_suffix(WB, S.B, m);
+    S.C = S.B;
+    S.A = WA;
+    S.B = WB;
+    __syncthreads();
+    PHASE(4);
+    return cta_sample_release<WIDE>(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
+  }
   if (wide) {
     const double t = wide_total(S.B, m, reinterpret_cast<double*>(smem));
     if (lead) {
@@ -1366,97 +1840,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
   PHASE(4);
 
-  // ---- 8. sampling + emission, one sample per thread per round
-  const SampleKey sk = sample_key(d, k);
-  int emitted = 0;
-  bool bad = false;
-  for (int base = 0; base < m - 1; base += kThreads) {
-    const int i = base + tid;
-    int lo = 0, hi = 0, slot = 0;
-    double wv = 0.0;
-    const bool em = i < m - 1 &&
-                    draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv,
-                                WIDE && m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
-                                coarse_step(m));
-    if (base == 0) SUB(3);
-    if (em) {
-      slot = reserve_fill_slot(d, lo);
-      red_add_relaxed_u64(&d.cnt[hi], 1ull);
-      bad = bad || slot < 0;
-    }
-    __syncwarp();
-    if (em && !bad) bad = !write_fill(d, lo, slot, hi, k, wv);
-    emitted += __popc(__ballot_sync(kFull, em));
-  }
-  if (lane == 0) sh.wcount[warp] = emitted;
-  if (bad) sh.bad = 1;
-  __syncthreads();
-  SUB(4);
-  if (sh.bad) return -2;
-  if (lead) {
-    int e = 0;
-    for (int w2 = 0; w2 < kWarps; ++w2) e += sh.wcount[w2];
-    d.samples[k] = e;
-    sh.nready = 0;
-  }
-  if (d.level) {  // ASAP levels, as in the warp path
-    const int lk = lvk + 1;
-    for (int t = tid; t < m; t += kThreads) atomicMax(&d.level[static_cast<int>(S.A[t] >> 32)], lk);
-  }
-  PHASE(5);
-  maybe_delay(d, k, 1);
-
-  // ---- 9. release, decrement, collect ready rows into C
-  fence_acq_rel();
-  __syncthreads();
-  SUB(5);
-  unsigned long long* ready = reinterpret_cast<unsigned long long*>(S.C);
-  for (int t = tid; t < m; t += kThreads) {
-    const unsigned long long a = S.A[t];
-    const int row = static_cast<int>(a >> 32);
-    const int mult = static_cast<int>(a & 0xffffffffu);
-    const int fd = __ldg(&d.fdeg[row]);
-    const unsigned long long old = atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
-    if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
-    if (dp_of(old) == mult) ready[atomicAdd(&sh.nready, 1)] = ready_info(row, fd, old);
-  }
-  __syncthreads();
-  const int nready = sh.nready;
-  PHASE(6);
-  maybe_delay(d, k, 2);
-  if (nready == 0) return -1;
-
-  // keep-one (any width) + publish the rest
-  unsigned long long best = 0;
-  for (int t = tid; t < nready; t += kThreads) {
-    const unsigned long long rr = keep_key(d, ready[t]);
-    best = rr > best ? rr : best;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(kFull, best, o);
-    best = other > best ? other : best;
-  }
-  if (lane == 0) sh.best[warp] = best;
-  __syncthreads();
-  best = 0;
-#pragma unroll
-  for (int w2 = 0; w2 < kWarps; ++w2) best = sh.best[w2] > best ? sh.best[w2] : best;
-  const int keep = allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
-  for (int base = 0; base < nready; base += kThreads) {
-    const int t = base + tid;
-    bool pub = false, big = false;
-    int r = 0;
-    if (t < nready) {
-      const unsigned long long rr = ready[t];
-      r = static_cast<int>(rr & 0xffffffffu);
-      big = static_cast<int>(rr >> 32) > kSmallCap;
-      pub = r != keep;
-    }
-    publish(d, pub, big, r, lane);
-  }
-  __syncthreads();  // ready list (C) is reused by the next elimination
-  return keep;
+  return cta_sample_release<WIDE>(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
 }
 
 // ============================================================ kernel
@@ -1468,7 +1852,23 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
   const int warp = threadIdx.x >> 5;
   if (ld_relaxed(&d.ctrl->status) != 0) return;
 
-  if (!is_big_cta()) {
+  // Role. big_layout 1: the first CTA to start on each SM is the big one, so
+  // no two big CTAs share an SM (the tail's few concurrent wide columns never
+  // compete for one SM's schedulers); 0: every 4th SM runs only big CTAs.
+  bool big;
+  if (d.big_layout == 1 && gridDim.x >= 148) {
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      sh.k = atomicAdd(&d.ctrl->sm_slot[smid & 255], 1) == 0;
+    }
+    __syncthreads();
+    big = sh.k != 0;
+    __syncthreads();
+  } else {
+    big = is_big_cta();
+  }
+  if (!big) {
     Scratch S = carve(smem + warp * kSmallBytes, kSmallCap);
     int done_local = 0;
     Next nx{-1, -1, 0, 0};
@@ -1540,7 +1940,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
       d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
       d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
     }
-    cta_prologue(d, k, sh);
+    cta_prologue(d, k, sh, kept);
     const bool allow = ++chain < d.keep_limit;
     const int next = sh.R > kBigCap ? cta_eliminate<true>(d, k, smem, sh, allow)
                                     : cta_eliminate<false>(d, k, smem, sh, allow);

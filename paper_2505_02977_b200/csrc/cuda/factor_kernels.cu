@@ -256,7 +256,7 @@ constexpr int kReadyTile = kReadyThreads * kReadyItems;
 
 __device__ __forceinline__ void ready_flags(const FactorDev& d, int p, int& m, int& b) {
   const bool ready = p < d.n && (d.cnt[p] & 0xffffffffull) == 0;
-  const bool big = ready && d.fdeg[p] > kSmallCap;  // no fills yet: R = forward degree
+  const bool big = ready && d.fdeg[p] > d.small_cap;  // no fills yet: R = forward degree
   m = ready && !big;
   b = big;
 }

@@ -16,29 +16,43 @@ constexpr int kDirChunks = 16;
 // columns of up to kSmallCap raw entries in shared memory, one "big" warp per
 // CTA holds up to kBigCap (wider columns use a global-memory slab). A vertex is
 // routed to the matching ready queue when it becomes ready.
-constexpr int kSmallCap = 128;
+// Capacity of a small warp's column scratch. The routing threshold itself is
+// FactorDev::small_cap (<= kSmallCap), chosen per problem: 64 on sparse
+// meshes, where a 65-128 entry column took ~20 us on one warp (two 4-item
+// sorts on 32 lanes) vs ~10 us on a CTA and such columns are ~40% of the
+// 128^3 critical path (tools/profile_factor.py, by_raw); 128 on denser
+// graphs (27-point), where they are common enough in the wide phase that the
+// big-CTA pool would become the throughput limit (96 measured best there:
+// 27-point 96^3 K3 31.3 ms vs 32.9 at 128 and 35.3 at 64). A capacity of 96
+// rather than 128 keeps the small path's sample/decrement batches at 3 per
+// lane (fewer registers: 128^3 K3 19.5 vs 20.2 ms with the same routing).
+constexpr int kSmallCap = 96;
 // vertices of higher degree get a whole CTA in the forward-graph build (K1)
 constexpr int kHeavyDeg = 64;
 // wide-column slab: A (u64), B (f64), C (f64), A2, B2 per entry
 constexpr int kSlabEntryBytes = 40;
 constexpr int kBigCap = 1024;
 
+// Control block. The counters every elimination touches (queue heads and
+// tails, the column arena bump, the eliminated count, the status word the
+// waiters poll) each get their own 256-byte line: sharing one line serialised
+// the wide phase's ~800 atomics/us at a single L2 slice (measured: a relaxed
+// load of q_head/q_tail alongside the decrements cost ~3 us).
 struct Ctrl {
-  int status;            // 0 or Errc
-  int q_head;            // main (small-column) queue: next slot to claim
-  int q_tail;            //                            next slot to publish
-  int b_head;            // big-column queue
-  int b_tail;
-  int eliminated;        // vertices done (flushed per warp before it waits)
-  int max_raw;           // largest gathered column
-  int large_cols;        // columns that used the global-memory slab
-  unsigned long long ovf_bump;    // fill overflow pool (entries)
-  unsigned long long arena_bump;  // G column arena (entries)
-  unsigned long long large_bump;  // large-column slab pool (entries)
+  alignas(256) int status;  // 0 or Errc
+  alignas(256) int q_head;  // main (small-column) queue: next slot to claim
+  alignas(256) int q_tail;  //                            next slot to publish
+  alignas(256) int b_head;  // big-column queue
+  alignas(256) int b_tail;
+  alignas(256) int eliminated;               // vertices done (flushed per warp before it waits)
+  alignas(256) unsigned long long arena_bump;  // G column arena (entries)
+  alignas(256) int max_raw;                  // largest gathered column
+  int large_cols;                            // columns that used the global-memory slab
+  unsigned long long ovf_bump;               // fill overflow pool (entries)
+  unsigned long long large_bump;             // large-column slab pool (entries)
   long long total_fills;
   long long err_info;
-  int pad0;
-  int pad1;
+  alignas(256) int sm_slot[256];             // CTAs started per SM (role assignment)
 };
 
 struct FactorDev {
@@ -98,8 +112,15 @@ struct FactorDev {
   int delay_ns;
   unsigned sleep_ns[3];  // claim() backoff by distance to the publishing front (16-256, 256-1024, >1024 slots)
   int keep_limit;        // max consecutive keep-one hand-offs before a warp/CTA returns to the queue
+  int big_layout;        // 0: every 4th SM runs big CTAs only; 1: one big CTA per SM
+  int small_cap;         // columns with more raw entries go to the big-CTA queue (<= kSmallCap)
   unsigned long long* vtimes;  // optional [8n] phase timestamps per position
   unsigned long long* vsub;    // optional [8n] sub-phase timestamps per position
+  // optional TestHooks::on_phase analogue: dp snapshots [3n] at the phase
+  // boundaries of position trace_k's elimination (trace_k < 0: off)
+  int trace_k;
+  long long* trace_dp;
+  int* trace_taken;
 };
 
 // Launchers (stream-ordered). All return cudaError_t of the launch.

@@ -20,6 +20,7 @@ only the host container.
 from __future__ import annotations
 
 import ctypes as C
+import time
 import os
 import enum
 from dataclasses import dataclass, field
@@ -235,6 +236,7 @@ class GpuOptions:
     grid_ctas: int = 0
     delay_ns: int = 0                # TestHooks::delay analogue (random __nanosleep)
     record_times: bool = False       # ParOptions::record_vertex_times analogue
+    trace_position: int = -1         # TestHooks::on_phase analogue: >= 0 snapshots dp for this position
 
     def native(self) -> "L.parac_gpu_options":
         o = L.parac_gpu_options()
@@ -248,6 +250,8 @@ class GpuOptions:
         o.grid_ctas = self.grid_ctas
         o.delay_ns = self.delay_ns
         o.record_times = int(self.record_times)
+        o.trace_phases = int(self.trace_position >= 0)
+        o.trace_position = max(self.trace_position, 0)
         return o
 
 
@@ -353,6 +357,18 @@ class GpuContext:
         _check(lib.parac_gpu_download_times(self.handle, _ptr(out)))
         return out[:8 * n].reshape(n, 8)
 
+    PHASES = ("gathered", "sampled", "decremented")  # TestHooks::Phase (factor_par.hpp:17)
+
+    def phase_snapshots(self) -> dict:
+        """TestHooks::on_phase analogue of the last run with trace_position set:
+        {phase: dp snapshot (int64[n])} for each phase the traced position
+        reached (parac_gpu_download_phase_snapshots)."""
+        n = self._factor_n
+        dp = np.empty(3 * max(n, 1), np.int64)
+        taken = np.zeros(3, np.int32)
+        _check(lib.parac_gpu_download_phase_snapshots(self.handle, _ptr(dp), _ptr(taken)))
+        return {ph: dp[i * n:(i + 1) * n].copy() for i, ph in enumerate(self.PHASES) if taken[i]}
+
     PRECOND_MODES = {"default": 0, "exact": 1, "fast": 2}
 
     def set_preconditioner_mode(self, mode: str) -> None:
@@ -391,6 +407,7 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
                ctx: Optional[GpuContext] = None) -> LdlFactor:
     """Drop-in for factor_parallel_left (factor_par.hpp:53-55): byte-identical
     LdlFactor to factor_randomized for the same graph, ordering and seed."""
+    t0 = time.perf_counter()
     ctx = ctx or default_context()
     ctx.upload(graph, ordering)
     info = ctx.factor_resident(seed, options)
@@ -410,7 +427,9 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
         stats.assemble_ms = info.assemble_ms
         stats.device_ms = info.device_ms
         stats.upload_ms = info.upload_ms
-        stats.seconds = info.device_ms / 1e3
+        # FactorStats::seconds is wall time at the API, as in the reference
+        # (factor_seq.cpp:46, factor_par.cpp); device_ms holds the device time
+        stats.seconds = time.perf_counter() - t0
     return f
 
 

@@ -59,6 +59,12 @@ def test_factor_command(R, tmp_path):
     assert st["total_fills"] == rs["total_fills"]
     assert st["fill_ratio"] == 2.0 * st["nnz_g"] / (int(g.ptr[g.n]) + g.n)
     assert st["config"]["backend"] == "gpu" and st["config"]["seed"] == seed
+    # SURVEY §5 device metrics next to the reference's keys
+    assert 0 < st["device_seconds"] <= st["wall_seconds"]
+    assert 0 < st["eliminate_seconds"] <= st["device_seconds"]
+    assert st["hbm_gbs"] > 0 and 0 < st["roofline_fraction"] < 1
+    assert st["algorithmic_bytes"] == (16 * (g.n + 1) + 8 * g.n + 12 * g.num_edges() + 40 * st["total_fills"]
+                                       + 20 * (st["nnz_g"] - g.n))
     tr = json.load(open(tj))
     levels = np.empty(g.n, np.int32)
     R._chk(R.L.pref_schedule_levels(f, levels.ctypes.data))

@@ -141,3 +141,50 @@ def test_rmat_wide_columns_byte_identical(gpu_ctx, port, scale):
     want = port.factor(g, perm, 0)
     assert_same(f, factor_from_port(want))
     assert np.array_equal(st.fills_received, want["fills_received"])
+
+
+@pytest.mark.parametrize("grid", [0, 2, 7])
+def test_star_center_first_dependency_trace(gpu_ctx, port, grid):
+    """proj/tests/test_factor_par.cpp:67-103 on the device: TestHooks::on_phase's
+    dp snapshots while position 0 (the star's centre) is eliminated. The seed's
+    first draw pairs leaves 1 and 2, so the samples are {(1,2), (2,3)} and the
+    counters go (0,1,1,1) -> (0,1,2,2) after the samples -> (0,0,1,1) after the
+    decrements; the factor is the full chain rows {1,2,3,2,3}."""
+    from corpus import star
+    salt = 0x73616D706C696E67  # kSaltSampling ("sampling"), proj/include/parac/rng.hpp
+    chosen = next(s for s in range(64) if port.unit_uniform(port.derive_seed(s, salt), 0, 0) * 2.0 >= 1.0)
+    g = star(3)
+    f, _ = gpu_factor(gpu_ctx, g, np.arange(4, dtype=np.int32), chosen, trace_position=0, grid_ctas=grid)
+    snaps = gpu_ctx.phase_snapshots()
+    assert set(snaps) == {"gathered", "sampled", "decremented"}
+    assert snaps["gathered"].tolist() == [0, 1, 1, 1]
+    assert snaps["sampled"].tolist() == [0, 1, 2, 2]
+    assert snaps["decremented"].tolist() == [0, 0, 1, 1]
+    assert f.rows.tolist() == [1, 2, 3, 2, 3]
+    # a later run without tracing: no snapshots, same factor
+    f2, _ = gpu_factor(gpu_ctx, g, np.arange(4, dtype=np.int32), chosen)
+    assert f2.same_values(f)
+    with pytest.raises(P.Error):
+        gpu_ctx.phase_snapshots()
+
+
+def test_phase_trace_on_a_cta_column(gpu_ctx, port):
+    """The CTA path (raw column > 128 entries) takes the same snapshots: the
+    hub of a 300-leaf star, eliminated first. Its rows are published only
+    after the "decremented" snapshot, so nothing else runs in between."""
+    from corpus import star
+    g = star(300)
+    perm = np.arange(301, dtype=np.int32)
+    f, st = gpu_factor(gpu_ctx, g, perm, 1, trace_position=0)
+    want = port.factor(g, perm, 1)
+    assert f.same_values(P.LdlFactor(want["n"], want["col_ptr"], want["rows"], want["values"], want["diag"],
+                                     want["perm"]))
+    snaps = gpu_ctx.phase_snapshots()
+    dp0 = P.dependency_counts(g, P.Ordering.identity(301))
+    assert snaps["gathered"].tolist() == dp0.tolist()
+    # every emitted fill raised its hi endpoint's counter by one
+    assert int((snaps["sampled"] - snaps["gathered"]).sum()) == int(st.samples_emitted[0]) > 0
+    assert (snaps["sampled"] >= snaps["gathered"]).all()
+    # the hub's decrements: one per leaf (multiplicity 1)
+    assert snaps["decremented"][0] == 0
+    assert (snaps["decremented"][1:] == snaps["sampled"][1:] - 1).all()

@@ -170,9 +170,22 @@ def main():
     cc = np.where(wide[:, None], 0, cc)
     okc = cc[:, 2] > 0
     if okc.any():
-        out["critical_path"]["cta_raw_rank_sort_cycles"] = {
-            "count": int(okc.sum()), "x2_store_sync": float(cc[okc, 0].mean()),
-            "phase1_done": float(cc[okc, 1].mean()), "phase2_done": float(cc[okc, 2].mean())}
+        # cta_hash_merge step barriers (clock64 from the gather's landing)
+        out["critical_path"]["cta_hash_merge_cycles"] = {
+            "count": int(okc.sum()), "inserted": float(cc[okc, 0].mean()),
+            "runs_walked": float(cc[okc, 1].mean()), "runs_summed": float(cc[okc, 2].mean()),
+            "rows_ranked": float(cc[okc, 3].mean())}
+        # the same by raw-size bucket, with the critical path's raw-size mix
+        rr = raw[chs]
+        byb = {}
+        for lo, hi in ((0, 129), (129, 257), (257, 513), (513, 1025), (1025, 1 << 30)):
+            sel = (rr >= lo) & (rr < hi)
+            selc = sel & okc
+            byb[f"[{lo},{hi})"] = {
+                "count": int(sel.sum()), "m_mean": float(m[chs][sel].mean()) if sel.any() else None,
+                "service_us": float(dur[chs][sel].mean()) if sel.any() else None,
+                "cycles": [float(x) for x in cc[selc].mean(axis=0)] if selc.any() else None}
+        out["critical_path"]["by_raw"] = byb
     top = np.argsort(-hops)[:8]
     out["critical_path"]["worst_hops"] = [
         {"pos": int(chs[i]), "hop_us": float(hops[i]), "start_us": float(start[chs[i]]),

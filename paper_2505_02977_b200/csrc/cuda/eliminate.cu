@@ -105,6 +105,7 @@ struct CtaShared {
   unsigned long long best[kWarps];
   int next_R;          // raw size of the kept vertex
   int mbump, mcount;   // cta_hash_merge: stage bump, distinct rows
+  unsigned long long bestkey;  // keep-one: max keep_key over the rows made ready
   int hbad;            // cta_hash_merge: a run longer than kRunCap
 };
 
@@ -698,9 +699,33 @@ __device__ __forceinline__ int cta_hash_merge(const FactorDev& d, int k, long lo
   __syncthreads();  // every walk done: tab (rows) is free; hbad visible
   if (cyc) cyc[1] = clock64() - c0;
   if (sh.hbad) return -1;
+  // stage base and compact index of each run: warp-level exclusive scans of
+  // the run heads' lengths and counts, one shared-memory atomic per warp each
+  int jj[ITEMS];
+  {
+    const int lane = tid & 31;
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i)
-    if (slot[i] >= 0 && pos[i] == 0) tab[slot[i]] = atomicAdd(&sh.mbump, len[i]);
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool headr = slot[i] >= 0 && pos[i] == 0;
+      const int v = headr ? len[i] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned hm = __ballot_sync(kFull, headr);
+      int base = 0, jb = 0;
+      if (lane == 31 && hm) {
+        base = atomicAdd(&sh.mbump, incl);
+        jb = atomicAdd(&sh.mcount, __popc(hm));
+      }
+      base = __shfl_sync(kFull, base, 31);
+      jb = __shfl_sync(kFull, jb, 31);
+      jj[i] = jb + __popc(hm & lanemask_lt());
+      if (headr) tab[slot[i]] = base + incl - v;
+    }
+  }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i)
@@ -715,7 +740,7 @@ __device__ __forceinline__ int cta_hash_merge(const FactorDev& d, int k, long lo
       const double* st = stage + tab[slot[i]];
       double acc = st[0];
       for (int q = 1; q < len[i]; ++q) acc = __dadd_rn(acc, st[q]);
-      const int j = atomicAdd(&sh.mcount, 1);
+      const int j = jj[i];
       rows32[j] = static_cast<int>(key[i] >> 32);
       nxt[j] = len[i];
       sumj[j] = acc;
@@ -1153,6 +1178,7 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   else if (R <= 64) warp_rank_raw<2>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   else warp_rank_raw<kBatch>(d, k, fb, fdeg, R, S, lane, d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
   __syncwarp();
+  discard_fills(d, k, R - fdeg, lane, 32);
   PHASE(1);
   if (k == d.trace_k) snapshot_dp(d, 0, lane, 32);
 
@@ -1415,6 +1441,7 @@ __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, cha
     for (int w2 = 0; w2 < kWarps; ++w2) e += sh.wcount[w2];
     d.samples[k] = e;
     sh.nready = 0;
+    sh.bestkey = 0;
   }
   if (d.level) {  // ASAP levels, as in the warp path
     const int lk = lvk + 1;
@@ -1436,7 +1463,11 @@ __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, cha
     const int fd = __ldg(&d.fdeg[row]);
     const unsigned long long old = atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
     if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
-    if (dp_of(old) == mult) ready[atomicAdd(&sh.nready, 1)] = ready_info(row, fd, old);
+    if (dp_of(old) == mult) {
+      const unsigned long long rr = ready_info(row, fd, old);
+      ready[atomicAdd(&sh.nready, 1)] = rr;
+      atomicMax(&sh.bestkey, keep_key(d, rr));  // keep-one preference, decided at the barrier
+    }
   }
   __syncthreads();
   const int nready = sh.nready;
@@ -1446,21 +1477,7 @@ __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, cha
   if (nready == 0) return -1;
 
   // keep-one (any width) + publish the rest
-  unsigned long long best = 0;
-  for (int t = tid; t < nready; t += kThreads) {
-    const unsigned long long rr = keep_key(d, ready[t]);
-    best = rr > best ? rr : best;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(kFull, best, o);
-    best = other > best ? other : best;
-  }
-  if (lane == 0) sh.best[warp] = best;
-  __syncthreads();
-  best = 0;
-#pragma unroll
-  for (int w2 = 0; w2 < kWarps; ++w2) best = sh.best[w2] > best ? sh.best[w2] : best;
+  const unsigned long long best = sh.bestkey;
   const int keep = allow_keep ? static_cast<int>(best & 0xffffffffu) : -1;
   // the kept column's forward offset and degree: loaded now, in flight while
   // the others are published (its raw size comes with its ready entry)
@@ -1593,6 +1610,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       cta_gather_sort_raw<4>(d, k, fb, fdeg, R, sh.dirrow, S.A, S.B, xb);
     }
   }
+  discard_fills(d, k, R - fdeg, tid, kThreads);  // every gather above ended at a barrier
   PHASE(1);
   if (k == d.trace_k) snapshot_dp(d, 0, tid, kThreads);
 
@@ -1738,27 +1756,28 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
 
   // ---- 5-7. lkk + column, weight sort + suffix
-  if (!WIDE && m >= 2 && m <= kThreads - 32) {
-    // Overlapped: the last warp holds no element of the weight sort, so its
-    // lead runs the serial lkk chain over B (row order, left intact) while
-    // warps 0..6 rank the weights and scatter the weight-ordered column to
-    // (X2, C). Then every thread writes its column entry from registers
-    // while thread 0 runs the serial suffix chain into B.
+  if (!WIDE && m >= 2 && m <= kThreads) {
+    // Weight sort (broadcast all-pairs rank, one element per thread) scatters
+    // the weight-ordered column to (X2, C) and leaves B (row order) intact;
+    // then the two serial chains run side by side on two warps: lkk over B
+    // (row order) and the suffix sums over the sorted weights (into A's
+    // space). Every thread writes its column entry from registers after.
     const int g = tid;
     const unsigned long long wk = g < m ? dbits(S.B[g]) : kInfBits;
     const unsigned long long ak = g < m ? S.A[g] : ~0ull;
     unsigned long long* WA = S.X2;
     double* WB = S.C;
-    if (warp == kWarps - 1) {
-      if (lane == 0) sh.lkk = serial_total(S.B, m);
-    } else {
-      const int r = bcast_rank_cta<true, kThreads - 32>(wk, m, S.X1);
-      if (g < m) {
-        WA[r] = ak;
-        WB[r] = bitsd(wk);
-      }
+    double* SUF = reinterpret_cast<double*>(S.A);
+    const int r = bcast_rank_cta<true>(wk, m, S.X1);
+    if (g < m) {
+      WA[r] = ak;
+      WB[r] = bitsd(wk);
     }
     if (lead) sh.start = static_cast<long long>(start_reg);
+    __syncthreads();
+    SUB(2);
+    if (tid == kThreads - 32) sh.lkk = serial_total(S.B, m);
+    else if (lead) serial_suffix(WB, SUF, m);
     __syncthreads();
     const double lkk = sh.lkk;
     const long long start = sh.start;
@@ -1776,12 +1795,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       d.arena_vals[start + g] = __ddiv_rn(-bitsd(wk), lkk);
     }
     PHASE(3);
-    SUB(2);
-    if (lead) serial_suffix(WB, S.B, m);
-    S.C = S.B;
+    S.C = SUF;
     S.A = WA;
     S.B = WB;
-    __syncthreads();
     PHASE(4);
     return cta_sample_release<WIDE>(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
   }

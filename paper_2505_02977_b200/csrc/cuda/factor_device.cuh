@@ -147,6 +147,19 @@ __device__ __forceinline__ bool write_fill(const FactorDev& d, int lo, int slot,
   return true;
 }
 
+// The fills a column received are read exactly once, by its own gather, and
+// no writer touches the column's preallocated slots after it became ready:
+// drop those L2 lines without a write-back (the next factorization rewrites
+// every slot before it is read). Slots [0, min(fc, c0)) of position k, lines
+// t, t + step, ...
+__device__ __forceinline__ void discard_fills(const FactorDev& d, int k, int fc, int t, int step) {
+  if (!d.discard_fills) return;
+  const long long bytes = 16ll * min(fc, d.c0);
+  const char* base = reinterpret_cast<const char*>(d.pool0 + static_cast<long long>(k) * d.c0);
+  for (long long off = 128ll * t; off < bytes; off += 128ll * step)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + off) : "memory");
+}
+
 // pick_by_suffix (include/parac/sampling.hpp:46-57)
 __device__ __forceinline__ int pick_by_suffix(const double* suffix, int lo, int hi, double u) {
   while (lo < hi) {

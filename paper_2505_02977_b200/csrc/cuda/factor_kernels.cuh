@@ -114,6 +114,7 @@ struct FactorDev {
   int keep_limit;        // max consecutive keep-one hand-offs before a warp/CTA returns to the queue
   int big_layout;        // 0: every 4th SM runs big CTAs only; 1: one big CTA per SM
   int small_cap;         // columns with more raw entries go to the big-CTA queue (<= kSmallCap)
+  int discard_fills;     // drop a column's fill-slot L2 lines once it has gathered them
   unsigned long long* vtimes;  // optional [8n] phase timestamps per position
   unsigned long long* vsub;    // optional [8n] sub-phase timestamps per position
   // optional TestHooks::on_phase analogue: dp snapshots [3n] at the phase

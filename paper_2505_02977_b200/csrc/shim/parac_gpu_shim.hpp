@@ -123,6 +123,20 @@ void size_output(std::vector<T>& v, std::size_t count) {
     if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // a hint; failure is harmless
   }
 #endif
+  // first touch in parallel (the kernel zeroes each page on its fault, one
+  // core per fault): resize() then writes over resident pages
+  const std::size_t bytes_all = count * sizeof(T);
+  if (bytes_all >= (std::size_t{16} << 20)) {
+    char* base = reinterpret_cast<char*>(v.data());
+    const int nt = 4;
+    std::thread th[nt];
+    for (int i = 0; i < nt; ++i)
+      th[i] = std::thread([base, bytes_all, i] {
+        const std::size_t a = bytes_all * i / nt, b = bytes_all * (i + 1) / nt;
+        for (std::size_t off = a & ~std::size_t{4095}; off < b; off += 4096) base[off < a ? a : off] = 0;
+      });
+    for (auto& t : th) t.join();
+  }
   v.resize(count);
 }
 
@@ -135,7 +149,23 @@ struct CsrView {
   explicit CsrView(const LaplacianGraph& g) {
     const VertexId n = g.num_vertices();
     ptr.resize(static_cast<std::size_t>(n) + 1, 0);
-    for (VertexId v = 0; v < n; ++v) ptr[v + 1] = ptr[v] + g.degree(v);
+    // ptr[v] = offset of v's neighbour span in the contiguous adjacency
+    // array: independent per vertex, so large graphs fill it on 4 threads
+    const VertexId* base = n > 0 ? g.neighbors(0).data() : nullptr;
+    auto fill = [&](VertexId a, VertexId b) {
+      for (VertexId v = a; v < b; ++v) ptr[v] = static_cast<std::int64_t>(g.neighbors(v).data() - base);
+    };
+    if (n >= (1 << 20)) {
+      std::thread th[3];
+      for (int i = 0; i < 3; ++i)
+        th[i] = std::thread(fill, static_cast<VertexId>(static_cast<std::int64_t>(n) * (i + 1) / 4),
+                            static_cast<VertexId>(static_cast<std::int64_t>(n) * (i + 2) / 4));
+      fill(0, static_cast<VertexId>(n / 4));
+      for (auto& t : th) t.join();
+    } else {
+      fill(0, n);
+    }
+    if (n > 0) ptr[n] = static_cast<std::int64_t>(g.nnz_off_diagonal());
     csr.n = n;
     csr.ptr = ptr.data();
     csr.adj = n > 0 ? g.neighbors(0).data() : nullptr;
@@ -191,15 +221,22 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
   Session& sess = *ctx.s;
   const std::size_t guess =
       sess.last_n == n && sess.last_nnz == nnz_adj ? static_cast<std::size_t>(sess.last_z) : 0;
+  // upload first (its pageable->pinned staging uses the host cores), then
+  // size the outputs on helper threads while the device factors
+  check(parac_gpu_upload(ctx.get(), &v.csr, ordering.perm.data()));
   std::thread sizer([&f, n, guess] {
-    size_output(f.col_ptr, static_cast<std::size_t>(n) + 1);
-    size_output(f.diag, static_cast<std::size_t>(n));
+    std::thread t2([&f, n] {
+      size_output(f.col_ptr, static_cast<std::size_t>(n) + 1);
+      size_output(f.diag, static_cast<std::size_t>(n));
+    });
     if (guess) {
-      size_output(f.rows, guess);
+      std::thread t3([&f, guess] { size_output(f.rows, guess); });
       size_output(f.values, guess);
+      t3.join();
     }
+    t2.join();
   });
-  const int rc = parac_gpu_factor(ctx.get(), &v.csr, ordering.perm.data(), seed, &o, &info);
+  const int rc = parac_gpu_factor_resident(ctx.get(), seed, &o, &info);
   sizer.join();
   check(rc);
   const auto t_fac = std::chrono::steady_clock::now();

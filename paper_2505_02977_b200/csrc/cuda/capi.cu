@@ -254,6 +254,7 @@ struct parac_gpu_ctx {
   DevBuf<int4> pool0, ovf;
   DevBuf<unsigned> dir;
   DevBuf<char> large_pool;
+  DevBuf<HubJob> hub_jobs;  // one per CTA of the elimination grid
   DevBuf<Ctrl> ctrl;
   DevBuf<unsigned long long> vtimes, vsub;
   bool has_times = false;
@@ -362,6 +363,8 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   ctx->arena_rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->arena_vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->large_pool.ensure(static_cast<std::size_t>(std::max<long long>(b.large, 1)) * kSlabEntryBytes);
+  const int hub_jobs = eliminate_occupancy_grid(ctx->device);
+  ctx->hub_jobs.ensure(static_cast<std::size_t>(hub_jobs));
   ctx->rows.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->vals.ensure(static_cast<std::size_t>(std::max<long long>(b.arena, 1)));
   ctx->ctrl.ensure(1);
@@ -400,6 +403,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.samples = ctx->samples.p;
   d.level = ctx->level.p;
   d.large_pool = ctx->large_pool.p;
+  d.hub_jobs = ctx->hub_jobs.p;
   d.large_cap = b.large;
   d.ctrl = ctx->ctrl.p;
   d.sample_seed = derive_seed(seed, kSaltSampling);
@@ -465,6 +469,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   check(cudaMemsetAsync(ctx->inv.p, 0xff, nn * sizeof(int), s), "memset");
   check(cudaMemsetAsync(ctx->dir.p, 0, nn * kDirChunks * sizeof(unsigned), s), "memset");
   check(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s), "memset");
+  check(cudaMemsetAsync(ctx->hub_jobs.p, 0, static_cast<std::size_t>(hub_jobs) * sizeof(HubJob), s), "memset");
   check(launch_pos_graph(d, ctx->tiles.p, s), "pos_graph launch");
   check(launch_initial_ready(d, ctx->tiles.p, s), "initial_ready launch");
   check(cudaEventRecord(ctx->ev[1], s), "event");
@@ -560,7 +565,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
   ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
-  ctx->large_pool.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->vsub.release(); ctx->col_ptr.release(); ctx->rows.release();
+  ctx->large_pool.release(); ctx->hub_jobs.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->vsub.release(); ctx->col_ptr.release(); ctx->rows.release();
   ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
   solve_release(ctx->solve);
   ctx->stage.release();

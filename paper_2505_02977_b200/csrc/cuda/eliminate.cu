@@ -107,16 +107,24 @@ struct CtaShared {
   int mbump, mcount;   // cta_hash_merge: stage bump, distinct rows
   unsigned long long bestkey;  // keep-one: max keep_key over the rows made ready
   int hbad;            // cta_hash_merge: a run longer than kRunCap
+  // cooperative wide columns (hub path)
+  int ticket;          // big-queue slot this CTA waits on (-1: none), kept while it helps
+  int help;            // job a waiting CTA was sent to help
+  int hub_c, hub_cseq; // chunk taken, and the phase sequence it belongs to
+  int hub_seq;         // owner: sequence number of its last posted phase
+  int hub_slot;        // owner: public slot of its job (-1: private)
+  HubDesc hd;          // the phase being worked on
 };
 
 // ------------------------------------------------------------ claiming
 // Claim the next slot of a ready queue and spin on it (relaxed polls, backoff
 // by distance to the tail). Returns the vertex, -1 when every vertex is
 // eliminated, -2 on abort. The caller issues the acquire fence.
-__device__ int claim(const FactorDev& d, bool big) {
+// claim_at waits on slot idx; with help != nullptr (big CTAs) it also watches
+// the public hub jobs and returns -3 (job in *help) when one has chunks left,
+// keeping the slot for later.
+__device__ __forceinline__ int claim_at(const FactorDev& d, bool big, int idx, int* help) {
   int* queue = big ? d.bqueue : d.queue;
-  int* head = big ? &d.ctrl->b_head : &d.ctrl->q_head;
-  const int idx = atomicAdd(head, 1);
   if (idx >= d.n) return -1;
   int v = ld_relaxed(&queue[idx]);
   if (v >= 0) return v;
@@ -135,6 +143,22 @@ __device__ int claim(const FactorDev& d, bool big) {
       else if (idx < 1024 || ld_relaxed(&queue[idx - 1024]) >= 0) ns = d.sleep_ns[1];
       else ns = d.sleep_ns[2];  // far waiters must not load the L2
     }
+    if (help) {  // a posted hub phase with chunks left: go and help
+      const unsigned hm = static_cast<unsigned>(ld_relaxed(reinterpret_cast<const int*>(&d.ctrl->hub_mask)));
+      if (hm) {
+        const int rot = blockIdx.x & 31;
+        const int j = (__ffs(__funnelshift_r(hm, hm, rot)) - 1 + rot) & 31;
+        const int jb = ld_relaxed(&d.ctrl->hub_pub[j]);
+        if (jb > 0) {
+          const unsigned long long nx = ld_relaxed_u64(&d.hub_jobs[jb - 1].next);
+          if ((nx & 0xffffffull) < ((nx >> 24) & 0xffffffull)) {
+            *help = jb - 1;
+            return -3;
+          }
+        }
+        ns = min(ns, 64u);  // the next phase of an active job follows within microseconds
+      }
+    }
     __nanosleep(ns);
     v = ld_relaxed(&queue[idx]);
     if (v >= 0) return v;
@@ -152,6 +176,10 @@ __device__ int claim(const FactorDev& d, bool big) {
       }
     }
   }
+}
+
+__device__ __forceinline__ int claim(const FactorDev& d, bool big) {
+  return claim_at(d, big, atomicAdd(big ? &d.ctrl->b_head : &d.ctrl->q_head, 1), nullptr);
 }
 
 // ------------------------------------------------------------ sorting
@@ -816,108 +844,25 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
 }
 
 // ------------------------------------------------------------ wide columns
-// Columns with more than kBigCap raw entries (R-MAT hubs: up to ~10^5) live in
-// a global-memory slab owned by the CTA. Sort = tiles of kBigCap sorted in
-// shared memory by the register bitonic network, then log2(R / kBigCap)
-// merge-path passes (each thread merges a contiguous output range, found by
-// binary search on the diagonal) ping-ponging between (K, V) and (K2, V2).
-// Keys are unique under Less, so merges need no tie rule.
-template <typename Less>
-__device__ __noinline__ void slab_sort(unsigned long long* K, unsigned long long* V, unsigned long long* K2,
-                                       unsigned long long* V2, int R, unsigned long long padk,
-                                       unsigned long long padv, XBuf xb, Less less,
-                                       unsigned long long* tiles_done = nullptr) {
-  const int tid = threadIdx.x;
-  // tiles: stable shared-memory rank sort of the keys (ties keep slab order,
-  // which is what Less resolves them to: raw keys are unique, and the weight
-  // sort's input is row-ascending), ~6x faster than the register bitonic
-  // network on these 1024-entry tiles; scattered straight back to the slab
-  for (int tb = 0; tb < R; tb += kBigCap) {
-    const int cnt = min(kBigCap, R - tb);
-    unsigned long long key[4], val[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int g = i * kThreads + tid;
-      key[i] = g < cnt ? K[tb + g] : padk;
-      val[i] = g < cnt ? V[tb + g] : padv;
-    }
-    int rank[4];
-    __syncthreads();  // the previous tile's scratch is free
-    rank_sort<kThreads, 4>(key, cnt, xb.k0, xb.v0, reinterpret_cast<int*>(xb.k1),
-                           reinterpret_cast<int*>(xb.k1) + kBigCap, rank);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i * kThreads + tid < cnt) {
-        K[tb + rank[i]] = key[i];
-        V[tb + rank[i]] = val[i];
-      }
-    }
-  }
-  __syncthreads();
-  if (tiles_done && threadIdx.x == 0) *tiles_done = globaltimer_ns();
-  unsigned long long *sk = K, *sv = V, *dk = K2, *dv = V2;
-  for (int run = kBigCap; run < R; run *= 2) {
-    for (int b = 0; b < R; b += 2 * run) {
-      const int na = min(run, R - b), nb = max(0, min(run, R - b - run));
-      const int tot = na + nb;
-      const unsigned long long *Ak = sk + b, *Av = sv + b, *Bk = sk + b + na, *Bv = sv + b + na;
-      const int per = (tot + kThreads - 1) / kThreads;
-      const int d0 = min(tid * per, tot), d1 = min(d0 + per, tot);
-      if (d0 >= d1) continue;
-      int lo = max(0, d0 - nb), hi = min(d0, na);
-      while (lo < hi) {  // A-elements among the first d0 outputs
-        const int mid = (lo + hi) >> 1;
-        if (less(Bk[d0 - 1 - mid], Bv[d0 - 1 - mid], Ak[mid], Av[mid])) hi = mid; else lo = mid + 1;
-      }
-      int i = lo, j = d0 - lo;
-      unsigned long long ak = i < na ? Ak[i] : 0, av = i < na ? Av[i] : 0;
-      unsigned long long bk = j < nb ? Bk[j] : 0, bv = j < nb ? Bv[j] : 0;
-      for (int o = d0; o < d1; ++o) {
-        const bool takeA = j >= nb || (i < na && less(ak, av, bk, bv));
-        if (takeA) {
-          dk[b + o] = ak;
-          dv[b + o] = av;
-          ++i;
-          if (i < na) { ak = Ak[i]; av = Av[i]; }
-        } else {
-          dk[b + o] = bk;
-          dv[b + o] = bv;
-          ++j;
-          if (j < nb) { bk = Bk[j]; bv = Bv[j]; }
-        }
-      }
-    }
-    __syncthreads();
-    unsigned long long* t = sk; sk = dk; dk = t;
-    t = sv; sv = dv; dv = t;
-  }
-  if (sk != K) {
-    for (int g = tid; g < R; g += kThreads) {
-      K[g] = sk[g];
-      V[g] = sv[g];
-    }
-    __syncthreads();
-  }
-}
-
-// Serial chains over a global-memory column: the lead thread walks chunks of
-// kChainChunk values staged in shared memory by warps 1..7 (double-buffered),
-// so the chain runs at the FP64 add latency instead of the L2 latency.
+// Serial chains over a global-memory column (hub path): the lead thread walks
+// chunks of kChainChunk values staged in shared memory by warps 1..7
+// (double-buffered), so the chain runs at the FP64 add latency instead of the
+// L2 latency. The column was written by other SMs: loads bypass L1.
 constexpr int kChainChunk = 1024;
 
-__device__ __noinline__ double wide_total(const double* B, int m, double* stage) {
+__device__ __noinline__ double hub_total(const double* B, int m, double* stage) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nch = (m + kChainChunk - 1) / kChainChunk;
   double s = 0.0;
   if (warp != 0)
-    for (int t = tid - 32; t < min(m, kChainChunk); t += kThreads - 32) stage[t] = B[t];
+    for (int t = tid - 32; t < min(m, kChainChunk); t += kThreads - 32) stage[t] = __ldcg(B + t);
   for (int c = 0; c < nch; ++c) {
     __syncthreads();
     const double* cur = stage + (c & 1) * kChainChunk;
     if (warp != 0) {
       double* nxt = stage + ((c + 1) & 1) * kChainChunk;
       const int b = (c + 1) * kChainChunk;
-      for (int t = tid - 32; t < kChainChunk && b + t < m; t += kThreads - 32) nxt[t] = B[b + t];
+      for (int t = tid - 32; t < kChainChunk && b + t < m; t += kThreads - 32) nxt[t] = __ldcg(B + b + t);
     } else if (tid == 0) {
       const int cnt = min(kChainChunk, m - c * kChainChunk);
       int t = 0;
@@ -936,14 +881,14 @@ __device__ __noinline__ double wide_total(const double* B, int m, double* stage)
 }
 
 // suffix[g] = w[g] + suffix[g+1], right to left, written to C (global).
-__device__ __noinline__ void wide_suffix(const double* B, double* C, int m, double* stage) {
+__device__ __noinline__ void hub_suffix(const double* B, double* C, int m, double* stage) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nch = (m + kChainChunk - 1) / kChainChunk;
   // chunk c covers [m - (c+1)*CH, m - c*CH)
   auto chunk_lo = [&](int c) { return max(0, m - (c + 1) * kChainChunk); };
   if (warp != 0) {
     const int lo = chunk_lo(0);
-    for (int t = lo + tid - 32; t < m; t += kThreads - 32) stage[t - lo] = B[t];
+    for (int t = lo + tid - 32; t < m; t += kThreads - 32) stage[t - lo] = __ldcg(B + t);
   }
   double s = 0.0;
   for (int c = 0; c < nch; ++c) {
@@ -954,13 +899,13 @@ __device__ __noinline__ void wide_suffix(const double* B, double* C, int m, doub
       if (c + 1 < nch) {
         double* nxt = stage + ((c + 1) & 1) * kChainChunk;
         const int lo2 = chunk_lo(c + 1), hi2 = lo;
-        for (int t = lo2 + tid - 32; t < hi2; t += kThreads - 32) nxt[t - lo2] = B[t];
+        for (int t = lo2 + tid - 32; t < hi2; t += kThreads - 32) nxt[t - lo2] = __ldcg(B + t);
       }
     } else if (tid == 0) {
       int g = hi - 1;
       if (c == 0) {
         s = cur[g - lo];
-        C[g] = s;
+        __stcg(C + g, s);
         --g;
       }
       for (; g - 7 >= lo; g -= 8) {
@@ -973,11 +918,11 @@ __device__ __noinline__ void wide_suffix(const double* B, double* C, int m, doub
           o[q] = s;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) C[g - q] = o[q];
+        for (int q = 0; q < 8; ++q) __stcg(C + g - q, o[q]);
       }
       for (; g >= lo; --g) {
         s = __dadd_rn(cur[g - lo], s);
-        C[g] = s;
+        __stcg(C + g, s);
       }
     }
   }
@@ -1376,12 +1321,9 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
 
 // ============================================================ big path
 
-// The whole CTA eliminates k. Returns the kept vertex (any width), -1, or -2.
-// WIDE (raw size > kBigCap, R-MAT hubs) works in a global-memory slab; the
-// common case is a separate instantiation so that all its scratch accesses
-// compile to shared-memory instructions (a runtime select between slab and
-// shared memory made every access generic). cta_prologue (the caller) has
-// loaded fb / fdeg / R / level into sh.
+// The whole CTA eliminates k (R <= kBigCap, in shared memory; wider columns
+// take the cooperative hub path). Returns the kept vertex (any width), -1, or
+// -2. cta_prologue (the caller) has loaded fb / fdeg / R / level into sh.
 __device__ __forceinline__ void cta_prologue(const FactorDev& d, int k, CtaShared& sh, bool known) {
   const int tid = threadIdx.x;
   // a kept vertex arrives with its forward offset / degree / raw size (loaded
@@ -1404,7 +1346,6 @@ __device__ __forceinline__ void cta_prologue(const FactorDev& d, int k, CtaShare
 // Steps 8-9 of a CTA elimination (sampling + emission, release, decrements,
 // keep-one + publish) over the weight-ordered column (S.A rows, S.B weights,
 // S.C suffix sums).
-template <bool WIDE>
 __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, char* smem, CtaShared& sh,
                                                   bool allow_keep, Scratch S, int m, double lkk, int lvk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1417,10 +1358,7 @@ __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, cha
     const int i = base + tid;
     int lo = 0, hi = 0, slot = 0;
     double wv = 0.0;
-    const bool em = i < m - 1 &&
-                    draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv,
-                                WIDE && m > kBigCap ? reinterpret_cast<const double*>(smem + 2 * 8 * kBigCap) : nullptr,
-                                coarse_step(m));
+    const bool em = i < m - 1 && draw_sample(d, sk, k, i, m, S.A, S.B, S.C, lkk, lo, hi, wv);
     if (base == 0) SUB(3);
     if (em) {
       slot = reserve_fill_slot(d, lo);
@@ -1508,7 +1446,6 @@ __device__ __forceinline__ int cta_sample_release(const FactorDev& d, int k, cha
   return keep;
 }
 
-template <bool WIDE>
 __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh, bool allow_keep) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool lead = tid == 0;
@@ -1525,69 +1462,20 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   const int P = next_pow2(R);
   if (lead) {
     sh.bad = 0;
-    if (P > kBigCap) {
-      if (P > sh.slab_cap) {  // this CTA's slab is reused; grow it (bump allocation) when too small
-        const int cap = max(P, 2 * sh.slab_cap);
-        const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(cap)));
-        if (base + cap > d.large_cap) {
-          fail(d, kErrArena, k);
-          sh.bad = 1;
-        }
-        sh.slab = base;
-        sh.slab_cap = cap;
-      }
-      atomicAdd(&ctrl->large_cols, 1);
-    }
     if (R > 64) atomicMax(&ctrl->max_raw, R);
   }
   __syncthreads();
-  if (sh.bad) return -2;
   SUB(0);
   // column arena slot: the round trip overlaps the gather/sort/merge (the
   // value is first needed at the column write)
   unsigned long long start_reg = 0;
   if (lead && R > 0) start_reg = atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R));
-  constexpr bool wide = WIDE;
-  Scratch S = WIDE ? carve(d.large_pool + sh.slab * kEntryBytes, sh.slab_cap) : carve(smem, kBigCap);
-  const XBuf sxb{reinterpret_cast<unsigned long long*>(smem), reinterpret_cast<unsigned long long*>(smem + 8 * kBigCap),
-                 reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
-                 reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
+  Scratch S = carve(smem, kBigCap);
   const XBuf xb{S.A, reinterpret_cast<unsigned long long*>(S.B),
                 reinterpret_cast<unsigned long long*>(smem + 3 * 8 * kBigCap),
                 reinterpret_cast<unsigned long long*>(smem + 4 * 8 * kBigCap)};
-  // diagnostics (record_times, wide columns): globaltimer stamps {gather
-  // landed, raw sort done, merge done, weight sort done} in the 4 cycle slots
-  unsigned long long* wst =
-      (WIDE && d.vsub && lead) ? d.vsub + d.n * 8ll + 4ll * k : nullptr;
   int hashed = -1;  // merged column size when cta_hash_merge merged it
-  if (wide) {  // global slab: shared-memory tiles + merge passes
-    // 8 raw entries in flight per thread (loads first, then the slab stores:
-    // the stores may alias nothing the loads read, but the compiler cannot know)
-    for (int t0 = tid; t0 < R; t0 += 8 * kThreads) {
-      unsigned long long key[8];
-      double w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        key[u] = ~0ull;
-        w[u] = 0.0;
-        const int t = t0 + u * kThreads;
-        if (t < R) load_raw_dir(d, k, fb, fdeg, t, sh.dirrow, key[u], w[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * kThreads;
-        if (t < R) {
-          S.A[t] = key[u];
-          S.B[t] = w[u];
-        }
-      }
-    }
-    __syncthreads();
-    if (wst) wst[0] = globaltimer_ns();
-    slab_sort(S.A, reinterpret_cast<unsigned long long*>(S.B), S.X1, S.X2, R, ~0ull, 0ull, sxb, RawLess{},
-              wst ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr);
-    if (wst) wst[1] = globaltimer_ns();
-  } else {
+  {
     // gather + hash merge; the raw sort + run merge only when a row's run is
     // longer than kRunCap
     unsigned long long* stamp = d.vsub ? d.vsub + 8 * static_cast<long long>(k) + 1 : nullptr;
@@ -1616,104 +1504,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
 
   // ---- 3. merge runs (rows' multiplicities and left-to-right weight sums)
   int m = hashed >= 0 ? hashed : 0;
-  if (WIDE) {
-    // global slab: each thread owns a contiguous block of the sorted column;
-    // pass 1 counts the segment heads in it (8 loads in flight), one CTA scan
-    // gives every thread its output offset, pass 2 sums each segment that
-    // starts in its block left to right (walking past the block end when the
-    // segment continues) into X1/X2, which then become A/B. Two passes of
-    // independent loads instead of R/256 dependent chunk round trips.
-    int* tcnt = reinterpret_cast<int*>(smem);
-    const int per = (R + kThreads - 1) / kThreads;
-    const int b0 = min(tid * per, R), b1 = min(b0 + per, R);
-    auto row_at = [&](int i) { return static_cast<int>(S.A[i] >> 32); };
-    int cnt = 0;
-    {
-      int prev = b0 > 0 && b0 < R ? row_at(b0 - 1) : -2;
-      for (int i0 = b0; i0 < b1; i0 += 8) {
-        int rw[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) rw[u] = i0 + u < b1 ? row_at(i0 + u) : -3;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (i0 + u < b1) {
-            cnt += rw[u] != prev;
-            prev = rw[u];
-          }
-      }
-    }
-    // exclusive scan of the per-thread head counts (thread order = column order)
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) sh.wcount[warp] = incl;
-    __syncthreads();
-    int off = incl - cnt, total = 0;
-#pragma unroll
-    for (int w2 = 0; w2 < kWarps; ++w2) {
-      off += w2 < warp ? sh.wcount[w2] : 0;
-      total += sh.wcount[w2];
-    }
-    (void)tcnt;
-    unsigned long long* OK = S.X1;
-    double* OV = reinterpret_cast<double*>(S.X2);
-    {
-      int prev = b0 > 0 && b0 < R ? row_at(b0 - 1) : -2;
-      bool open = false;
-      int cur = -1, c = 0;
-      double acc = 0.0;
-      for (int i0 = b0; i0 < b1; i0 += 8) {
-        int rw[8];
-        double wv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          rw[u] = i0 + u < b1 ? row_at(i0 + u) : -3;
-          wv[u] = i0 + u < b1 ? S.B[i0 + u] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (i0 + u >= b1) continue;
-          if (rw[u] != prev) {  // segment head
-            if (open) {
-              OK[off] = (static_cast<unsigned long long>(static_cast<unsigned>(cur)) << 32) | static_cast<unsigned>(c);
-              OV[off] = acc;
-              ++off;
-            }
-            open = true;
-            cur = rw[u];
-            acc = wv[u];
-            c = 1;
-          } else if (open) {
-            acc = __dadd_rn(acc, wv[u]);
-            ++c;
-          }  // else: the tail of a segment an earlier block owns
-          prev = rw[u];
-        }
-      }
-      if (open) {
-        for (int i = b1; i < R && row_at(i) == cur; ++i) {
-          acc = __dadd_rn(acc, S.B[i]);
-          ++c;
-        }
-        OK[off] = (static_cast<unsigned long long>(static_cast<unsigned>(cur)) << 32) | static_cast<unsigned>(c);
-        OV[off] = acc;
-      }
-    }
-    __syncthreads();
-    unsigned long long* ta = S.A;
-    double* tb = S.B;
-    S.A = S.X1;
-    S.B = reinterpret_cast<double*>(S.X2);
-    S.X1 = ta;
-    S.X2 = reinterpret_cast<unsigned long long*>(tb);
-    m = total;
-  }
   if (lead) sh.carry_row = -1;
   __syncthreads();
-  for (int base = 0; !WIDE && hashed < 0 && base < R; base += kThreads) {
+  for (int base = 0; hashed < 0 && base < R; base += kThreads) {
     const int t = base + tid;
     const int row = t < R ? static_cast<int>(S.A[t] >> 32) : -2;
     const int prev = tid == 0 ? sh.carry_row : (t - 1 < R ? static_cast<int>(S.A[t - 1] >> 32) : -2);
@@ -1749,14 +1542,13 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     __syncthreads();
   }
   PHASE(2);
-  if (wst) wst[2] = globaltimer_ns();
   if (m == 0) {
     if (lead) d.diag[k] = 0.0;
     return -1;
   }
 
   // ---- 5-7. lkk + column, weight sort + suffix
-  if (!WIDE && m >= 2 && m <= kThreads) {
+  if (m >= 2 && m <= kThreads) {
     // Weight sort (broadcast all-pairs rank, one element per thread) scatters
     // the weight-ordered column to (X2, C) and leaves B (row order) intact;
     // then the two serial chains run side by side on two warps: lkk over B
@@ -1799,15 +1591,9 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
     S.A = WA;
     S.B = WB;
     PHASE(4);
-    return cta_sample_release<WIDE>(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
+    return cta_sample_release(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
   }
-  if (wide) {
-    const double t = wide_total(S.B, m, reinterpret_cast<double*>(smem));
-    if (lead) {
-      sh.lkk = t;
-      sh.start = static_cast<long long>(start_reg);
-    }
-  } else if (lead) {
+  if (lead) {
     sh.lkk = serial_total(S.B, m);
     sh.start = static_cast<long long>(start_reg);
   }
@@ -1832,11 +1618,7 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   // ---- 6-7. weight sort + suffix
   if (m >= 2) {
     const int Pm = next_pow2(m);
-    if (WIDE && Pm > kBigCap) {
-      // key = weight bits, payload = A (row << 32 | mult): (weight, row) order
-      slab_sort(reinterpret_cast<unsigned long long*>(S.B), S.A, S.X1, S.X2, m, kInfBits, ~0ull, sxb, WeightLess{});
-      if (wst) wst[3] = globaltimer_ns();
-    } else if (Pm <= kThreads) {
+    if (Pm <= kThreads) {
       cta_rank_weight<1>(m, S);
     } else if (Pm <= 2 * kThreads) {
       cta_rank_weight<2>(m, S);
@@ -1844,23 +1626,542 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
       cta_sort_weight_reg<4>(m, S.A, S.B, xb);
     }
     SUB(2);
-    if (WIDE && Pm > kBigCap) {
-      wide_suffix(S.B, S.C, m, reinterpret_cast<double*>(smem));
-      double* coarse = reinterpret_cast<double*>(smem + 2 * 8 * kBigCap);  // C + D regions: kCoarseMax entries
-      const int cs = coarse_step(m);
-      for (int q = tid; q * cs < m; q += kThreads) coarse[q] = S.C[q * cs];
-    } else if (lead) {
+    if (lead) {
       serial_suffix(S.B, S.C, m);
     }
     __syncthreads();
   }
   PHASE(4);
 
-  return cta_sample_release<WIDE>(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
+  return cta_sample_release(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
+}
+
+// ============================================================ cooperative wide columns
+// Columns with more than kBigCap raw entries (R-MAT hubs: mean ~5,600 raw
+// entries on the critical path at scale 20, up to ~10^5) take ~300 us on one
+// SM, and they are the R-MAT critical path while most SMs idle. The owner
+// (the big CTA that claimed the column) runs the elimination as phases cut
+// into 256-entry chunks and posts each phase as a job (HubJob,
+// factor_kernels.cuh); big CTAs waiting on the big queue take chunks
+// (claim_at). The owner takes chunks too, so a column completes without
+// helpers. Same arithmetic and orders as the reference:
+//   kHubGather  raw entries of tile c, ranked in shared memory (raw keys are
+//               unique) -> RK/RW, each 256-entry tile sorted by (row, source)
+//   kHubRank    each entry's place among the other tiles (binary searches over
+//               tiles staged in shared memory) -> SK/SW, the raw column sorted;
+//               run heads counted per 256-entry block of the sorted order (HB)
+//   kHubMerge   each run head sums its run left to right (factor_common.hpp:
+//               100-113) -> merged column (row << 32 | mult, weight) in RK/RW
+//   kHubWTile   each tile ranked stably by weight bits -> SK (bits) / SW
+//               (payload); meanwhile the owner walks lkk in row order
+//   kHubWRank   place among the other tiles (earlier tiles: ties count) ->
+//               WK / WB in (weight, row) order (factor_common.hpp:133-145);
+//               then the owner walks the suffix sums (sampling.hpp:72-76)
+//   kHubSample  samples i (sampling.hpp:77-83) + fill emission, the column of
+//               G in row order, ASAP levels
+//   kHubRelease decrements by multiplicity, ready rows published
+// A phase is posted (descriptor, then the release of its `next` word) only
+// after every chunk of the previous one is done, so chunks of one phase never
+// read what the same phase writes.
+enum : int { kHubGather = 1, kHubRank, kHubMerge, kHubWTile, kHubWRank, kHubSample, kHubRelease };
+constexpr int kHubTile = kThreads;                        // entries per chunk, one per thread
+constexpr int kHubGroup = kCtaSmem / (8 * kHubTile);      // tiles staged per shared-memory group
+
+struct HubArr {
+  unsigned long long *RK, *SK, *WK;
+  double *RW, *SW, *WB, *C;
+  int* HB;  // run heads per sorted block (in C's space: C is written after kHubMerge)
+};
+__device__ __forceinline__ HubArr hub_arrays(const FactorDev& d, long long slab, int cap) {
+  char* b = d.large_pool + slab * kEntryBytes;
+  const long long c8 = 8ll * cap;
+  return {reinterpret_cast<unsigned long long*>(b), reinterpret_cast<unsigned long long*>(b + 2 * c8),
+          reinterpret_cast<unsigned long long*>(b + 4 * c8), reinterpret_cast<double*>(b + c8),
+          reinterpret_cast<double*>(b + 3 * c8), reinterpret_cast<double*>(b + 5 * c8),
+          reinterpret_cast<double*>(b + 6 * c8), reinterpret_cast<int*>(b + 6 * c8)};
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// CTA sum of one int per thread (ws: kWarps ints of shared memory).
+__device__ __forceinline__ int cta_sum(int v, int* ws) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) t += ws[w];
+  return t;
+}
+
+// Place of `key` (an element of sorted tile c of the sorted-tile array K[0, n))
+// among the other tiles: #{keys < key} in each (STABLE: earlier tiles count
+// keys <= key, the stable rule for the weight sort). Tiles are staged into
+// shared memory kHubGroup at a time; four binary searches run side by side.
+// PRED: pred = max(pred, largest key below `key` in the other tiles).
+template <bool STABLE, bool PRED>
+__device__ __forceinline__ int hub_cross_rank(const unsigned long long* K, int n, int c, unsigned long long key,
+                                              bool valid, unsigned long long* X, unsigned long long& pred) {
+  const int tid = threadIdx.x;
+  const int nt = (n + kHubTile - 1) / kHubTile;
+  int pos = 0;
+  for (int g0 = 0; g0 < nt; g0 += kHubGroup) {
+    const int g1 = min(nt, g0 + kHubGroup);
+    const int len = min(n, g1 * kHubTile) - g0 * kHubTile;
+    __syncthreads();  // the previous group (or the caller's use of X) is done
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(K + static_cast<long long>(g0) * kHubTile);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(X);
+    for (int i = tid; 2 * i < len; i += kThreads) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    if (!valid) continue;
+    for (int t = g0; t < g1; t += 4) {
+      int lo[4], tl[4];
+      unsigned long long thr[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int tt = t + q;
+        lo[q] = 0;
+        tl[q] = (tt < g1 && tt != c) ? min(kHubTile, n - tt * kHubTile) : 0;
+        thr[q] = STABLE && tt < c ? key + 1 : key;
+      }
+#pragma unroll
+      for (int step = kHubTile; step > 0; step >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int p = lo[q] + step;
+          if (p <= tl[q] && X[(t + q - g0) * kHubTile + p - 1] < thr[q]) lo[q] = p;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pos += lo[q];
+        if (PRED && lo[q] > 0) pred = max(pred, X[(t + q - g0) * kHubTile + lo[q] - 1]);
+      }
+    }
+  }
+  return pos;
+}
+
+// pick_by_suffix over the global suffix array through the shared-memory coarse
+// index (pick_wide), loads through L2.
+__device__ __forceinline__ int hub_pick(const double* suffix, const double* coarse, int cs, int lo, int hi,
+                                        double u) {
+  int qlo = (lo + cs - 1) / cs, qhi = hi / cs;
+  int a = lo;
+  if (qlo <= qhi && coarse[qlo] > u) {
+    while (qlo < qhi) {
+      const int mid = qlo + (qhi - qlo + 1) / 2;
+      if (coarse[mid] > u) qlo = mid; else qhi = mid - 1;
+    }
+    a = max(lo, qlo * cs);
+  }
+  int b = min(hi, a + cs);
+  while (a < b) {
+    const int mid = a + (b - a + 1) / 2;
+    if (__ldcg(suffix + mid) > u) a = mid; else b = mid - 1;
+  }
+  return a;
+}
+
+__device__ __noinline__ void hub_chunk(const FactorDev& d, const HubDesc& h, int c, char* smem, int* emitted) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const HubArr A = hub_arrays(d, h.slab, h.cap);
+  unsigned long long* X = reinterpret_cast<unsigned long long*>(smem);
+  const int b0 = c * kHubTile;
+  switch (h.phase) {
+    case kHubGather: {
+      const int cnt = min(kHubTile, h.R - b0);
+      unsigned long long key = ~0ull;
+      double w = 0.0;
+      if (tid < cnt) load_raw_dir(d, h.k, h.fb, h.fdeg, b0 + tid, h.dirrow, key, w);
+      const int r = bcast_rank_cta<false>(key, cnt, X);
+      if (tid < cnt) {
+        __stcg(A.RK + b0 + r, key);
+        __stcg(A.RW + b0 + r, w);
+      }
+      if (tid == 0) __stcg(A.HB + c, 0);
+      break;
+    }
+    case kHubRank: {
+      const int cnt = min(kHubTile, h.R - b0);
+      const bool v = tid < cnt;
+      const unsigned long long key = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
+      const double w = v ? __ldcg(A.RW + b0 + tid) : 0.0;
+      unsigned long long pred = v && tid > 0 ? __ldcg(A.RK + b0 + tid - 1) : 0ull;  // 0: none (rows are >= 1)
+      const int pos = tid + hub_cross_rank<false, true>(A.RK, h.R, c, key, v, X, pred);
+      if (v) {
+        __stcg(A.SK + pos, key);
+        __stcg(A.SW + pos, w);
+        if ((pred >> 32) != (key >> 32)) atomicAdd(A.HB + (pos / kHubTile), 1);
+      }
+      break;
+    }
+    case kHubMerge: {
+      const int cnt = min(kHubTile, h.R - b0);
+      int* ws = reinterpret_cast<int*>(X);
+      int before = 0;
+      for (int j = tid; j < c; j += kThreads) before += __ldcg(A.HB + j);
+      before = cta_sum(before, ws);
+      const int p = b0 + tid;
+      const bool v = tid < cnt;
+      const unsigned long long key = v ? __ldcg(A.SK + p) : 0ull;
+      const unsigned long long prev = v && p > 0 ? __ldcg(A.SK + p - 1) : 0ull;
+      const bool head = v && (prev >> 32) != (key >> 32);
+      const unsigned hb = __ballot_sync(kFull, head);
+      __syncthreads();  // ws reused
+      if (lane == 0) ws[kWarps + (tid >> 5)] = __popc(hb);
+      __syncthreads();
+      int off = before + __popc(hb & lanemask_lt());
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) off += w < (tid >> 5) ? ws[kWarps + w] : 0;
+      if (head) {  // the run p, p+1, ... summed left to right, 8 loads in flight
+        const unsigned row = static_cast<unsigned>(key >> 32);
+        double acc = __ldcg(A.SW + p);
+        int mult = 1;
+        bool open = true;
+        for (int q = p + 1; open && q < h.R; q += 8) {
+          unsigned long long kk[8];
+          double ww[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            kk[u] = q + u < h.R ? __ldcg(A.SK + q + u) : ~0ull;
+            ww[u] = q + u < h.R ? __ldcg(A.SW + q + u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (open && static_cast<unsigned>(kk[u] >> 32) == row) {
+              acc = __dadd_rn(acc, ww[u]);
+              ++mult;
+            } else {
+              open = false;
+            }
+          }
+        }
+        __stcg(A.RK + off, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned>(mult));
+        __stcg(A.RW + off, acc);
+      }
+      break;
+    }
+    case kHubWTile: {
+      const int cnt = min(kHubTile, h.m - b0);
+      const bool v = tid < cnt;
+      const unsigned long long wk = v ? dbits(__ldcg(A.RW + b0 + tid)) : kInfBits;
+      const unsigned long long a = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
+      const int r = bcast_rank_cta<true>(wk, cnt, X);
+      if (v) {
+        __stcg(A.SK + b0 + r, wk);
+        __stcg(reinterpret_cast<unsigned long long*>(A.SW) + b0 + r, a);
+      }
+      break;
+    }
+    case kHubWRank: {
+      const int cnt = min(kHubTile, h.m - b0);
+      const bool v = tid < cnt;
+      const unsigned long long wk = v ? __ldcg(A.SK + b0 + tid) : kInfBits;
+      const unsigned long long a = v ? __ldcg(reinterpret_cast<const unsigned long long*>(A.SW) + b0 + tid) : 0ull;
+      unsigned long long unused = 0;
+      const int pos = tid + hub_cross_rank<true, false>(A.SK, h.m, c, wk, v, X, unused);
+      if (v) {
+        __stcg(A.WK + pos, a);
+        __stcg(A.WB + pos, bitsd(wk));
+      }
+      break;
+    }
+    case kHubSample: {
+      double* coarse = reinterpret_cast<double*>(X);
+      const int m = h.m, cs = h.cs;
+      for (int q = tid; q * cs < m; q += kThreads) coarse[q] = __ldcg(A.C + static_cast<long long>(q) * cs);
+      __syncthreads();
+      const int i = b0 + tid;
+      bool em = false;
+      int lo = 0, hi = 0, slot = -1;
+      double wv = 0.0;
+      if (i < m - 1) {  // sample_clique_sorted (sampling.hpp:77-83), as draw_sample
+        const SampleKey sk = sample_key(d, h.k);
+        const double s = __ldcg(A.C + i + 1);
+        const double u = __dmul_rn(unit_uniform(sk.seed, sk.key, static_cast<unsigned long long>(i)), s);
+        const int j = hub_pick(A.C, coarse, cs, i + 1, m - 1, u);
+        wv = __ddiv_rn(__dmul_rn(s, __ldcg(A.WB + i)), h.lkk);
+        if (wv >= kDropThreshold) {
+          const int ra = static_cast<int>(__ldcg(A.WK + i) >> 32), rc = static_cast<int>(__ldcg(A.WK + j) >> 32);
+          lo = min(ra, rc);
+          hi = max(ra, rc);
+          em = true;
+        }
+      }
+      if (em) {
+        slot = reserve_fill_slot(d, lo);
+        red_add_relaxed_u64(&d.cnt[hi], 1ull);
+      }
+      __syncwarp();
+      if (em && slot >= 0) write_fill(d, lo, slot, hi, h.k, wv);
+      const int e = __popc(__ballot_sync(kFull, em));
+      if (lane == 0 && e) atomicAdd(emitted, e);
+      if (i < m) {  // the column of G (row order) and ASAP levels
+        const unsigned long long a = __ldcg(A.RK + i);
+        const int row = static_cast<int>(a >> 32);
+        d.arena_rows[h.start + i] = row;
+        d.arena_vals[h.start + i] = __ddiv_rn(-__ldcg(A.RW + i), h.lkk);
+        if (d.level) atomicMax(&d.level[row], h.lvk + 1);
+      }
+      break;
+    }
+    case kHubRelease: {
+      const int i = b0 + tid;
+      bool rdy = false, big = false;
+      int row = 0;
+      if (i < h.m) {
+        const unsigned long long a = __ldcg(A.RK + i);
+        row = static_cast<int>(a >> 32);
+        const int mult = static_cast<int>(a & 0xffffffffu);
+        const int fd = __ldg(&d.fdeg[row]);
+        const unsigned long long old =
+            atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
+        if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
+        if (dp_of(old) == mult) {
+          rdy = true;
+          big = static_cast<int>(ready_info(row, fd, old) >> 32) > d.small_cap;
+        }
+      }
+      publish(d, rdy, big, row, lane);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// Take and run chunks of job `job` until its posted phase has none left. The
+// owner (own) works from its shared descriptor; a helper copies the posted one.
+__device__ __noinline__ void hub_work(const FactorDev& d, int job, char* smem, CtaShared& sh, bool own) {
+  HubJob& J = d.hub_jobs[job];
+  const int tid = threadIdx.x;
+  while (true) {
+    __syncthreads();  // the previous chunk's shared state is free
+    if (tid == 0) {
+      const unsigned long long old = atom_add_relaxed_u64(&J.next, 1ull);
+      const int c = static_cast<int>(old & 0xffffffull);
+      sh.hub_c = c < static_cast<int>((old >> 24) & 0xffffffull) ? c : -1;
+      sh.hub_cseq = static_cast<int>(old >> 48);
+    }
+    __syncthreads();
+    const int c = sh.hub_c;
+    if (c < 0) break;
+    fence_acq_rel();  // acquire: the phase's inputs (published before its post) are visible
+    if (!own) {       // stable until every chunk of the phase is done (ours included)
+      const unsigned* src = reinterpret_cast<const unsigned*>(&J.desc[sh.hub_cseq & 1]);
+      unsigned* dst = reinterpret_cast<unsigned*>(&sh.hd);
+      for (int w = tid; w < static_cast<int>(sizeof(HubDesc) / 4); w += kThreads) dst[w] = __ldcg(src + w);
+      __syncthreads();
+    }
+    hub_chunk(d, sh.hd, c, smem, &J.emitted);
+    fence_acq_rel();  // release: this chunk's stores before its completion count
+    __syncthreads();
+    if (tid == 0) red_add_relaxed_u64(&J.done, 1ull);
+  }
+}
+
+// Owner: post phase `phase` with nch chunks (descriptor first, then the
+// release of the `next` word that helpers claim chunks from).
+__device__ __forceinline__ void hub_post(const FactorDev& d, int job, CtaShared& sh, int phase, int nch) {
+  HubJob& J = d.hub_jobs[job];
+  const int tid = threadIdx.x;
+  __syncthreads();  // sh.hd complete
+  if (tid < 32) {
+    const int seq = (sh.hub_seq + 1) & 0xffff;
+    sh.hd.phase = phase;  // lane-uniform write
+    __syncwarp();
+    const unsigned* src = reinterpret_cast<const unsigned*>(&sh.hd);
+    unsigned* dst = reinterpret_cast<unsigned*>(&J.desc[seq & 1]);
+    for (int w = tid; w < static_cast<int>(sizeof(HubDesc) / 4); w += 32) __stcg(dst + w, src[w]);
+    fence_acq_rel();
+    __syncwarp();
+    if (tid == 0) {
+      sh.hub_seq = seq;
+      st_relaxed_u64(&J.done, static_cast<unsigned long long>(seq) << 32);
+      fence_acq_rel();
+      st_relaxed_u64(&J.next, (static_cast<unsigned long long>(seq) << 48) |
+                                  (static_cast<unsigned long long>(nch) << 24));
+    }
+  }
+  __syncthreads();
+}
+
+// Owner: wait until every chunk of the posted phase is done (false: the
+// factorization aborted meanwhile).
+__device__ __forceinline__ bool hub_wait(const FactorDev& d, int job, CtaShared& sh, int nch) {
+  if (threadIdx.x == 0) {
+    const unsigned long long target = (static_cast<unsigned long long>(sh.hub_seq) << 32) |
+                                      static_cast<unsigned long long>(nch);
+    int iter = 0;
+    sh.bad = 0;
+    while (ld_relaxed_u64(&d.hub_jobs[job].done) != target) {
+      if ((++iter & 255) == 0 && ld_relaxed(&d.ctrl->status) != 0) {
+        sh.bad = 1;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  fence_acq_rel();  // acquire: the chunks' stores are visible
+  return sh.bad == 0;
+}
+
+__device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* smem, CtaShared& sh, int phase,
+                                          int nch) {
+  hub_post(d, job, sh, phase, nch);
+  hub_work(d, job, smem, sh, true);
+  return hub_wait(d, job, sh, nch);
+}
+
+__device__ __forceinline__ void hub_release_slot(const FactorDev& d, CtaShared& sh) {
+  if (threadIdx.x == 0 && sh.hub_slot >= 0) {
+    atomicAnd(&d.ctrl->hub_mask, ~(1u << sh.hub_slot));
+    atomicExch(&d.ctrl->hub_pub[sh.hub_slot], 0);
+    sh.hub_slot = -1;
+  }
+}
+
+// The owner's side of a cooperative wide-column elimination. Returns -1 (the
+// rows it made ready are all published) or -2 (abort).
+__device__ __noinline__ int hub_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh) {
+  const int tid = threadIdx.x;
+  const bool lead = tid == 0;
+  Ctrl* ctrl = d.ctrl;
+  const int job = blockIdx.x;
+  const int R = sh.R;
+  if (d.verify && lead && dp_of(ld_relaxed_u64(&d.cnt[k])) != 0) fail(d, kErrInternal, k);
+  maybe_delay(d, k, 0);
+  if (lead) {
+    sh.bad = 0;
+    const int P = next_pow2(R);
+    if (P > sh.slab_cap) {  // this CTA's slab is reused; grow it (bump allocation) when too small
+      const int cap = max(P, 2 * sh.slab_cap);
+      const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(cap)));
+      if (base + cap > d.large_cap) {
+        fail(d, kErrArena, k);
+        sh.bad = 1;
+      }
+      sh.slab = base;
+      sh.slab_cap = cap;
+    }
+    atomicAdd(&ctrl->large_cols, 1);
+    atomicMax(&ctrl->max_raw, R);
+    sh.start = static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R)));
+    HubDesc& h = sh.hd;
+    h.k = k;
+    h.R = R;
+    h.m = 0;
+    h.nt = (R + kHubTile - 1) / kHubTile;
+    h.mt = 0;
+    h.fdeg = sh.fdeg;
+    h.fb = sh.fb;
+    h.lvk = d.level ? ld_relaxed(&d.level[k]) : 0;
+    h.cs = 0;
+    h.cap = sh.slab_cap;
+    h.slab = sh.slab;
+    h.start = 0;
+    h.lkk = 0.0;
+    // a public slot, so that waiting big CTAs find the job (none free: the
+    // owner works alone)
+    sh.hub_slot = -1;
+    if (!sh.bad) {
+      for (int t = 0; t < kHubSlots; ++t) {
+        const int j = (job + t) & (kHubSlots - 1);
+        if (ld_relaxed(&ctrl->hub_pub[j]) == 0 && atomicCAS(&ctrl->hub_pub[j], 0, job + 1) == 0) {
+          sh.hub_slot = j;
+          atomicOr(&ctrl->hub_mask, 1u << j);
+          break;
+        }
+      }
+    }
+  }
+  if (tid < kDirChunks) sh.hd.dirrow[tid] = sh.dirrow[tid];
+  __syncthreads();
+  if (sh.bad) return -2;
+  SUB(0);
+  unsigned long long* wst = (d.vsub && lead) ? d.vsub + d.n * 8ll + 4ll * k : nullptr;
+  const int nt = sh.hd.nt;
+  bool ok = hub_phase(d, job, smem, sh, kHubGather, nt);
+  if (wst) wst[0] = globaltimer_ns();
+  ok = ok && hub_phase(d, job, smem, sh, kHubRank, nt);
+  if (wst) wst[1] = globaltimer_ns();
+  ok = ok && hub_phase(d, job, smem, sh, kHubMerge, nt);
+  if (!ok) {
+    hub_release_slot(d, sh);
+    return -2;
+  }
+  const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
+  int m = 0;
+  for (int j = tid; j < nt; j += kThreads) m += __ldcg(A.HB + j);
+  m = cta_sum(m, reinterpret_cast<int*>(smem));
+  if (wst) wst[2] = globaltimer_ns();
+  PHASE(1);
+  PHASE(2);
+  if (k == d.trace_k) snapshot_dp(d, 0, tid, kThreads);
+  if (m == 0) {  // (a raw entry always merges into a row)
+    hub_release_slot(d, sh);
+    if (lead) d.diag[k] = 0.0;
+    return -1;
+  }
+  if (lead) {
+    sh.hd.m = m;
+    sh.hd.mt = (m + kHubTile - 1) / kHubTile;
+  }
+  __syncthreads();
+  const int mt = sh.hd.mt;
+  double* stage = reinterpret_cast<double*>(smem);
+  double lkk;
+  if (m >= 2) {
+    // lkk (row order) on the owner while the helpers rank the weight tiles;
+    // then the owner joins the phase
+    hub_post(d, job, sh, kHubWTile, mt);
+    lkk = hub_total(A.RW, m, stage);
+    PHASE(3);
+    hub_work(d, job, smem, sh, true);
+    ok = hub_wait(d, job, sh, mt) && hub_phase(d, job, smem, sh, kHubWRank, mt);
+    if (wst) wst[3] = globaltimer_ns();
+    if (ok) hub_suffix(A.WB, A.C, m, stage);
+  } else {
+    lkk = hub_total(A.RW, m, stage);
+    PHASE(3);
+  }
+  PHASE(4);
+  if (ok && sh.start + m > d.arena_cap) {
+    if (lead) fail(d, kErrArena, k);
+    ok = false;
+  }
+  if (!ok) {
+    hub_release_slot(d, sh);
+    return -2;
+  }
+  if (lead) {
+    sh.hd.lkk = lkk;
+    sh.hd.start = sh.start;
+    sh.hd.cs = coarse_step(m);
+    d.diag[k] = lkk;
+    d.col_start[k] = sh.start;
+    d.col_len[k] = m;
+    d.hub_jobs[job].emitted = 0;  // ordered before the post by its fences
+  }
+  ok = hub_phase(d, job, smem, sh, kHubSample, mt);
+  PHASE(5);
+  if (lead) d.samples[k] = ld_relaxed(&d.hub_jobs[job].emitted);
+  maybe_delay(d, k, 1);
+  if (ok && k == d.trace_k) snapshot_dp(d, 1, tid, kThreads);
+  ok = ok && hub_phase(d, job, smem, sh, kHubRelease, mt);
+  PHASE(6);
+  if (ok && k == d.trace_k) snapshot_dp(d, 2, tid, kThreads);
+  hub_release_slot(d, sh);
+  return ok ? -1 : -2;
 }
 
 // ============================================================ kernel
-__global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
+__global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_constant__ FactorDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ CtaShared sh;
   char* smem = reinterpret_cast<char*>(smem_raw);
@@ -1929,6 +2230,9 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
   if (threadIdx.x == 0) {
     sh.slab = -1;
     sh.slab_cap = 0;
+    sh.ticket = -1;
+    sh.hub_seq = 0;
+    sh.hub_slot = -1;
   }
   __syncthreads();
   int done_local = 0;
@@ -1941,12 +2245,22 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
       chain = 0;
       if (threadIdx.x == 0) {
         if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
-        sh.k = claim(d, true);
+        if (sh.ticket < 0) sh.ticket = atomicAdd(&d.ctrl->b_head, 1);
+        int help = -1;
+        const int v = claim_at(d, true, sh.ticket, &help);
+        sh.k = v;
+        sh.help = help;
+        if (v != -3) sh.ticket = -1;
       }
       done_local = 0;
       __syncthreads();
       k = sh.k;
       __syncthreads();
+      if (k == -3) {  // help a posted hub phase, then wait on the same slot again
+        hub_work(d, sh.help, smem, sh, false);
+        k = -1;
+        continue;
+      }
       if (k < 0) break;
     }
     fence_acq_rel();
@@ -1958,8 +2272,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(FactorDev d) {
     }
     cta_prologue(d, k, sh, kept);
     const bool allow = ++chain < d.keep_limit;
-    const int next = sh.R > kBigCap ? cta_eliminate<true>(d, k, smem, sh, allow)
-                                    : cta_eliminate<false>(d, k, smem, sh, allow);
+    const int next = sh.R > kBigCap ? hub_eliminate(d, k, smem, sh) : cta_eliminate(d, k, smem, sh, allow);
     if (next == -2) break;
     PHASE(7);
     ++done_local;

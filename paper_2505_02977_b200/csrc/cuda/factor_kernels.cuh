@@ -29,9 +29,32 @@ constexpr int kDirChunks = 16;
 constexpr int kSmallCap = 96;
 // vertices of higher degree get a whole CTA in the forward-graph build (K1)
 constexpr int kHeavyDeg = 64;
-// wide-column slab: A (u64), B (f64), C (f64), A2, B2 per entry
-constexpr int kSlabEntryBytes = 40;
+// wide-column slab (cooperative hub path, eliminate.cu): 7 arrays of 8 B per
+// entry -- raw keys/weights (tile-sorted, then the merged column), sorted raw
+// keys/weights (then the weight-sorted tiles), weight-ordered column, suffix
+constexpr int kSlabEntryBytes = 56;
 constexpr int kBigCap = 1024;
+
+// Cooperative wide columns (raw size > kBigCap, R-MAT hubs). The big CTA that
+// claims such a column (the owner) runs its elimination as a sequence of
+// phases, each cut into 256-entry chunks and posted as a job; big CTAs that
+// are waiting for a queue slot take chunks of any posted job (helpers). The
+// owner takes chunks too, so a column finishes with or without helpers.
+constexpr int kHubSlots = 32;  // public job slots (Ctrl::hub_mask bits)
+struct HubDesc {                // one phase of one column (read by every chunk)
+  int k, R, m, nt, mt, fdeg, lvk, cs, phase, cap;
+  long long fb, slab, start;
+  double lkk;
+  unsigned dirrow[kDirChunks];
+};
+struct HubJob {  // one per CTA of the elimination grid
+  // seq << 48 | nchunks << 24 | chunks claimed: claiming a chunk is one
+  // atomicAdd, and the returned word says which phase the chunk belongs to
+  alignas(256) unsigned long long next;
+  alignas(256) unsigned long long done;  // seq << 32 | chunks completed
+  alignas(256) HubDesc desc[2];          // by seq parity
+  alignas(256) int emitted;              // fills emitted by the sampling phase
+};
 
 // Control block. The counters every elimination touches (queue heads and
 // tails, the column arena bump, the eliminated count, the status word the
@@ -53,6 +76,8 @@ struct Ctrl {
   long long total_fills;
   long long err_info;
   alignas(256) int sm_slot[256];             // CTAs started per SM (role assignment)
+  alignas(256) unsigned hub_mask;            // public hub job slots in use (helpers poll this word)
+  alignas(256) int hub_pub[kHubSlots];       // slot -> job index + 1 (0: free)
 };
 
 struct FactorDev {
@@ -96,9 +121,10 @@ struct FactorDev {
   long long arena_cap;
   int* samples;
   int* level;  // optional: ASAP level per position (schedule_levels), 1-based
-  // large-column slab pool: 24 B per entry
+  // large-column slab pool: kSlabEntryBytes per entry
   char* large_pool;
   long long large_cap;
+  HubJob* hub_jobs;  // [grid] cooperative wide-column jobs, one per CTA
   // control
   Ctrl* ctrl;
   unsigned long long sample_seed;

@@ -129,14 +129,17 @@ def test_batch_union_equals_standalone(gpu_ctx, port, gold):
         assert f"{f.checksum():016x}" == e["checksum"], nm
 
 
-@pytest.mark.parametrize("scale", [15, 16])
-def test_rmat_wide_columns_byte_identical(gpu_ctx, port, scale):
+@pytest.mark.parametrize("scale,opts", [(15, {}), (16, {}), (15, dict(grid_ctas=2)),
+                                        (15, dict(grid_ctas=9, verify=True)),
+                                        (15, dict(delay_ns=3000, verify=True))])
+def test_rmat_wide_columns_byte_identical(gpu_ctx, port, scale, opts):
     # R-MAT hubs exceed the shared-memory column capacity (1024 raw entries):
-    # slab tile sort + merge passes, staged serial chains, coarse-indexed
-    # sampling search -- still byte-identical to the reference restatement
+    # the cooperative hub path (phases in 256-entry chunks taken by waiting
+    # big CTAs; with grid_ctas=2 the owner works alone) -- still byte-identical
+    # to the reference restatement, whoever takes which chunk
     g = P.gen_rmat(scale, 16, 0)
     perm = P.ordering_random(g.n, 0).perm
-    f, st = gpu_factor(gpu_ctx, g, perm, 0)
+    f, st = gpu_factor(gpu_ctx, g, perm, 0, **opts)
     assert st.large_columns > 0, "no column took the wide path"
     want = port.factor(g, perm, 0)
     assert_same(f, factor_from_port(want))
@@ -188,3 +191,26 @@ def test_phase_trace_on_a_cta_column(gpu_ctx, port):
     # the hub's decrements: one per leaf (multiplicity 1)
     assert snaps["decremented"][0] == 0
     assert (snaps["decremented"][1:] == snaps["sampled"][1:] - 1).all()
+
+
+def test_phase_trace_on_a_hub_column(gpu_ctx, port):
+    """The cooperative hub path (raw column > 1024 entries) takes the
+    snapshots at the same phase boundaries: the centre of a 1500-leaf star,
+    eliminated first while every leaf waits on it."""
+    from corpus import star
+    g = star(1500)
+    perm = np.arange(1501, dtype=np.int32)
+    f, st = gpu_factor(gpu_ctx, g, perm, 2, trace_position=0, verify=True)
+    assert st.large_columns > 0, "the centre did not take the hub path"
+    want = port.factor(g, perm, 2)
+    assert f.same_values(P.LdlFactor(want["n"], want["col_ptr"], want["rows"], want["values"], want["diag"],
+                                     want["perm"]))
+    snaps = gpu_ctx.phase_snapshots()
+    dp0 = P.dependency_counts(g, P.Ordering.identity(1501))
+    assert snaps["gathered"].tolist() == dp0.tolist()
+    assert int((snaps["sampled"] - snaps["gathered"]).sum()) == int(st.samples_emitted[0]) > 0
+    assert (snaps["sampled"] >= snaps["gathered"]).all()
+    # the centre's own counter is zero (leaves made ready are published by the
+    # chunks that decremented them, so later eliminations may already have
+    # moved the leaves' counters by the time of this snapshot)
+    assert snaps["decremented"][0] == 0

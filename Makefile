@@ -23,6 +23,14 @@ all: lib oracle
 
 lib: $(LIB)
 
+# K3: the hub instance of the kernel calls the cooperative hub path across
+# units (relocatable device code) so that the two register allocations stay
+# independent; the hub unit gets the kernel's 64-register budget. The mesh
+# instance (eliminate.o) stays whole-program (relocatable code cost it 4%).
+$(OBJDIR)/eliminate_hubs.o: NVFLAGS += -rdc=true
+$(OBJDIR)/eliminate_hubs.o: $(PKG)/csrc/cuda/eliminate.cu
+$(OBJDIR)/hub.o: NVFLAGS += -rdc=true -maxrregcount=64
+
 $(OBJDIR)/%.o: $(PKG)/csrc/cuda/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@

@@ -196,7 +196,8 @@ typedef struct {
                                every attempt when default budgets had to grow and retry */
   double upload_ms;         /* host->device copy (0 for resident inputs) */
   double wall_ms;           /* host wall clock of the call */
-  int32_t attempts;         /* device passes run (> 1: library-chosen budgets were grown) */
+  int32_t attempts;         /* device passes run (> 1: library-chosen budgets were grown, or the
+                               kernel instance with the hub path was needed) */
 } parac_gpu_factor_info;
 
 /* Stage graph + ordering on the device of ctx (host->device copy). */
@@ -260,6 +261,12 @@ int parac_gpu_download_phase_snapshots(parac_gpu_ctx* ctx, int64_t* dp, int32_t*
  * loads done, 1 gather landed, 2 weight sort done, 3 samples drawn, 4 fills
  * written, 5 release fence done; zero = not recorded on that path). */
 int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub);
+
+/* Diagnostics: the cooperative hub path's per-column trace of the same
+ * record_times run (kHubTraceWords = 48 words per wide column, layout in
+ * csrc/cuda/factor_kernels.cuh). Copies min(cap, *count) records; *count =
+ * wide columns recorded. */
+int parac_gpu_download_hub_trace(parac_gpu_ctx* ctx, uint64_t* out, int32_t cap, int32_t* count);
 
 /* Stage an existing factor (e.g. one computed by the reference) on the
  * device for the solve entry points. */

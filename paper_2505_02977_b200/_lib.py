@@ -85,6 +85,7 @@ SIGNATURES = {
     "parac_gpu_download": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "parac_gpu_download_times": (C.c_int, [vp, vp]),
     "parac_gpu_download_subtimes": (C.c_int, [vp, vp]),
+    "parac_gpu_download_hub_trace": (C.c_int, [vp, vp, C.c_int32, vp]),
     "parac_gpu_download_phase_snapshots": (C.c_int, [vp, vp, vp]),
     "parac_gpu_upload_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp]),
     "parac_gpu_factor_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp, P(parac_gpu_options),

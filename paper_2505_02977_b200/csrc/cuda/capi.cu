@@ -239,6 +239,7 @@ struct parac_gpu_ctx {
   int n = -1;
   long long nnz = 0;
   long long max_degree = 0;  // of the staged graph (sizes the wide-column slab pool)
+  bool needs_hubs = false;   // a run on the staged graph met a column wider than kBigCap
   DevBuf<long long> ptr, scalar;
   DevBuf<int> adj;
   DevBuf<double> w;
@@ -255,6 +256,7 @@ struct parac_gpu_ctx {
   DevBuf<unsigned> dir;
   DevBuf<char> large_pool;
   DevBuf<HubJob> hub_jobs;  // one per CTA of the elimination grid
+  DevBuf<unsigned long long> hub_trace;  // record_times: per hub column phase times
   DevBuf<Ctrl> ctrl;
   DevBuf<unsigned long long> vtimes, vsub;
   bool has_times = false;
@@ -404,6 +406,15 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.level = ctx->level.p;
   d.large_pool = ctx->large_pool.p;
   d.hub_jobs = ctx->hub_jobs.p;
+  {  // PARAC_HUB_LINGER_NS: how long a helper stays with a hub job between its phases (tuning)
+    const char* e = std::getenv("PARAC_HUB_LINGER_NS");
+    d.hub_linger_ns = e ? std::strtoull(e, nullptr, 10) : 40000ull;
+    // the kernel instance with the hub path on graphs with hub vertices, or
+    // once a run on this graph met a column wider than kBigCap (PARAC_HUBS=0/1
+    // overrides the first choice; tuning / tests)
+    const char* hh = std::getenv("PARAC_HUBS");
+    d.hubs = ctx->needs_hubs || (hh ? std::atoi(hh) != 0 : ctx->max_degree > 512);
+  }
   d.large_cap = b.large;
   d.ctrl = ctx->ctrl.p;
   d.sample_seed = derive_seed(seed, kSaltSampling);
@@ -439,6 +450,7 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   d.delay_ns = o.delay_ns;
   d.vtimes = nullptr;
   d.vsub = nullptr;
+  d.hub_trace = nullptr;
   d.trace_k = -1;
   d.trace_dp = nullptr;
   d.trace_taken = nullptr;
@@ -463,6 +475,10 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     ctx->vsub.ensure(12 * nn);  // 8 sub-phase stamps + 4 cycle counters (rank-sort diagnostics)
     check(cudaMemsetAsync(ctx->vsub.p, 0, 12 * nn * sizeof(unsigned long long), s), "memset");
     d.vsub = ctx->vsub.p;
+    ctx->hub_trace.ensure(static_cast<std::size_t>(kHubTraceCap) * kHubTraceWords);
+    check(cudaMemsetAsync(ctx->hub_trace.p, 0, sizeof(unsigned long long) * kHubTraceCap * kHubTraceWords, s),
+          "memset");
+    d.hub_trace = ctx->hub_trace.p;
   }
 
   check(cudaEventRecord(ctx->ev[0], s), "event");
@@ -485,6 +501,11 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   check(cudaStreamSynchronize(s), "factor sync");
   ctx->last_ctrl = c;
   ctx->last_z = z;
+  if (c.status == kStatusNeedHubs) {  // re-run with the hub path (parac_gpu_factor_resident)
+    ctx->f_n = -1;
+    ctx->needs_hubs = true;
+    return c.status;
+  }
   if (c.status != 0) {
     ctx->f_n = -1;
     std::string msg;
@@ -565,7 +586,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   ctx->arena_rows.release(); ctx->fwd_ptr.release(); ctx->col_start.release();
   ctx->tiles.release(); ctx->fwd_to.release(); ctx->fwd_w.release(); ctx->diag.release();
   ctx->arena_vals.release(); ctx->pool0.release(); ctx->ovf.release(); ctx->dir.release();
-  ctx->large_pool.release(); ctx->hub_jobs.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->vsub.release(); ctx->col_ptr.release(); ctx->rows.release();
+  ctx->large_pool.release(); ctx->hub_jobs.release(); ctx->hub_trace.release(); ctx->ctrl.release(); ctx->vtimes.release(); ctx->vsub.release(); ctx->col_ptr.release(); ctx->rows.release();
   ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
   solve_release(ctx->solve);
   ctx->stage.release();
@@ -620,6 +641,7 @@ int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
     ctx->scalar.ensure(1);
     max_degree_device(n, ctx->ptr.p, ctx->scalar.p, s, device_sms(ctx));
     check(cudaMemcpyAsync(&ctx->max_degree, ctx->scalar.p, sizeof(long long), cudaMemcpyDeviceToHost, s), "d2h");
+    ctx->needs_hubs = false;
     check(cudaStreamSynchronize(s), "h2d sync");
     ctx->n = n;
     ctx->nnz = nnz;
@@ -705,6 +727,7 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     ctx->scalar.ensure(1);
     max_degree_device(static_cast<int>(N), ctx->ptr.p, ctx->scalar.p, s, device_sms(ctx));
     check(cudaMemcpyAsync(&ctx->max_degree, ctx->scalar.p, sizeof(long long), cudaMemcpyDeviceToHost, s), "d2h");
+    ctx->needs_hubs = false;
     check(cudaStreamSynchronize(s), "h2d sync");
     ctx->n = static_cast<int>(N);
     ctx->nnz = NNZ;
@@ -799,6 +822,7 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
     // Budget exhaustion with library-chosen budgets: grow and retry (the
     // caller's explicit budgets fail cleanly, like ParOptions::arena_budget).
     const bool defaults = o.fill_pool_entries < 0 && o.column_arena_entries < 0;
+    if (st == kStatusNeedHubs && attempt < 8) continue;  // now with the hub path
     if (st == arena_exhausted && defaults && attempt < 4) {
       b.ovf *= 2;
       b.arena *= 2;
@@ -960,6 +984,19 @@ int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub) {
     require_ctx(ctx);
     if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
     check(cudaMemcpy(sub, ctx->vsub.p, sizeof(unsigned long long) * 12 * ctx->f_n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int parac_gpu_download_hub_trace(parac_gpu_ctx* ctx, uint64_t* out, int32_t cap, int32_t* count) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!ctx->has_times || ctx->f_n < 0) throw Failure{internal_error, "no recorded times"};
+    const int cols = std::min(ctx->last_ctrl.large_cols, kHubTraceCap);
+    if (count) *count = cols;
+    const int c = std::min(cols, std::max(cap, 0));
+    if (out && c > 0)
+      check(cudaMemcpy(out, ctx->hub_trace.p, sizeof(unsigned long long) * kHubTraceWords * c, cudaMemcpyDeviceToHost),
+            "d2h");
   });
 }
 

@@ -22,8 +22,9 @@
 // Bit-exactness: the serial sums use __dadd_rn in the reference's order, the
 // products/divisions __dmul_rn/__ddiv_rn; sort keys are unique, so any sorting
 // network reproduces the reference's order.
-#include "factor_device.cuh"
-#include "factor_kernels.cuh"
+#include "k3_common.cuh"
+
+#include <algorithm>
 
 namespace parac_gpu {
 
@@ -31,17 +32,10 @@ void note_launches(long long k);
 
 using namespace dev;
 using namespace fdev;
+using namespace k3;
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kEntryBytes = kSlabEntryBytes;
-// small warps: A, B, C + two rank-sort segment buffers (X1, X2)
-constexpr int kSmallBytes = kSmallCap * 8 * 5;
-// big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
-constexpr int kBigBytes = kBigCap * 8 * 5;
-constexpr int kCtaSmem = kWarps * kSmallBytes > kBigBytes ? kWarps * kSmallBytes : kBigBytes;
 constexpr int kBatch = (kSmallCap + 31) / 32;  // samples / decrements per lane in flight (small path): one batch
 
 // Role of this CTA. On a full grid the role follows the SM (every 4th SM runs
@@ -53,13 +47,6 @@ __device__ __forceinline__ bool is_big_cta() {
   asm("mov.u32 %0, %%smid;" : "=r"(smid));
   return (smid & 3) == 3;
 }
-
-#define PHASE(i) \
-  do { if (d.vtimes && lead) d.vtimes[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
-// sub-phase stamps (record_times diagnostics): 0 setup done, 1 gather landed,
-// 2 weight sort done, 3 samples drawn, 4 fills written, 5 fence done
-#define SUB(i) \
-  do { if (d.vsub && lead) d.vsub[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
 
 // Column scratch views. A: raw key (row << 32 | source+1), then merged
 // (row << 32 | multiplicity); B: weights; C: suffix sums, then the ready list.
@@ -86,43 +73,13 @@ struct Next {
   long long fb; // forward-CSR offset
 };
 
-// Shared state of a big CTA (one vertex at a time).
-struct CtaShared {
-  int k;
-  int m;
-  int nready;
-  int emitted;
-  int carry_row;
-  int bad;
-  double lkk;
-  long long start;
-  long long slab;      // this CTA's wide-column slab (entries), -1 none
-  int slab_cap;
-  long long fb;        // cta_prologue: forward offset, degree, raw size
-  int fdeg, R;
-  unsigned dirrow[kDirChunks];
-  int wcount[kWarps];
-  unsigned long long best[kWarps];
-  int next_R;          // raw size of the kept vertex
-  int mbump, mcount;   // cta_hash_merge: stage bump, distinct rows
-  unsigned long long bestkey;  // keep-one: max keep_key over the rows made ready
-  int hbad;            // cta_hash_merge: a run longer than kRunCap
-  // cooperative wide columns (hub path)
-  int ticket;          // big-queue slot this CTA waits on (-1: none), kept while it helps
-  int help;            // job a waiting CTA was sent to help
-  int hub_c, hub_cseq; // chunk taken, and the phase sequence it belongs to
-  int hub_seq;         // owner: sequence number of its last posted phase
-  int hub_slot;        // owner: public slot of its job (-1: private)
-  HubDesc hd;          // the phase being worked on
-};
-
 // ------------------------------------------------------------ claiming
 // Claim the next slot of a ready queue and spin on it (relaxed polls, backoff
 // by distance to the tail). Returns the vertex, -1 when every vertex is
 // eliminated, -2 on abort. The caller issues the acquire fence.
 // claim_at waits on slot idx; with help != nullptr (big CTAs) it also watches
-// the public hub jobs and returns -3 (job in *help) when one has chunks left,
-// keeping the slot for later.
+// the latest posted hub job (Ctrl::hub_hint) and returns -3 (job in *help)
+// when it has chunks left, keeping the slot for later.
 __device__ __forceinline__ int claim_at(const FactorDev& d, bool big, int idx, int* help) {
   int* queue = big ? d.bqueue : d.queue;
   if (idx >= d.n) return -1;
@@ -144,17 +101,12 @@ __device__ __forceinline__ int claim_at(const FactorDev& d, bool big, int idx, i
       else ns = d.sleep_ns[2];  // far waiters must not load the L2
     }
     if (help) {  // a posted hub phase with chunks left: go and help
-      const unsigned hm = static_cast<unsigned>(ld_relaxed(reinterpret_cast<const int*>(&d.ctrl->hub_mask)));
-      if (hm) {
-        const int rot = blockIdx.x & 31;
-        const int j = (__ffs(__funnelshift_r(hm, hm, rot)) - 1 + rot) & 31;
-        const int jb = ld_relaxed(&d.ctrl->hub_pub[j]);
-        if (jb > 0) {
-          const unsigned long long nx = ld_relaxed_u64(&d.hub_jobs[jb - 1].next);
-          if ((nx & 0xffffffull) < ((nx >> 24) & 0xffffffull)) {
-            *help = jb - 1;
-            return -3;
-          }
+      const int hj = ld_relaxed(&d.ctrl->hub_hint);
+      if (hj > 0) {
+        const unsigned long long nx = ld_relaxed_u64(&d.hub_jobs[hj - 1].next);
+        if ((nx & 0xffffffull) < ((nx >> 24) & 0xffffffull)) {
+          *help = hj - 1;
+          return -3;
         }
         ns = min(ns, 64u);  // the next phase of an active job follows within microseconds
       }
@@ -461,53 +413,6 @@ __device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], 
 // round. The stable rule is free outside the 32-key block holding g's own
 // warp: keys before that block count when <= k (compare against k + 1),
 // keys after it when < k; inside it the threshold switches at g.
-
-// c += #{keys of pairs [q0, q1) of P below thr} (two accumulators per element)
-__device__ __forceinline__ void count_below(const ulonglong2* P, int q0, int q1, unsigned long long thr, int& ca,
-                                            int& cb) {
-#pragma unroll 2
-  for (int q = q0; q < q1; ++q) {
-    const ulonglong2 p = P[q];
-    ca += static_cast<int>(p.x < thr);
-    cb += static_cast<int>(p.y < thr);
-  }
-}
-// The mixed block (keys t = 2q, 2q+1 relative to the block): threshold k + 1
-// before position `pos` in the block, k from it on.
-__device__ __forceinline__ void count_below_mixed(const ulonglong2* P, int pairs, unsigned long long k, int pos,
-                                                  int& ca, int& cb) {
-  const unsigned long long k1 = k + 1;
-#pragma unroll 2
-  for (int q = 0; q < pairs; ++q) {
-    const ulonglong2 p = P[q];
-    ca += static_cast<int>(p.x < (2 * q < pos ? k1 : k));
-    cb += static_cast<int>(p.y < (2 * q + 1 < pos ? k1 : k));
-  }
-}
-
-// CTA: element g = threadIdx.x < R <= NT (one per thread); the first NT
-// threads take part (NT < kThreads: named barrier 1, the other warps are free
-// to do something else meanwhile).
-template <bool STABLE, int NT = kThreads>
-__device__ __forceinline__ int bcast_rank_cta(unsigned long long k, int R, unsigned long long* X) {
-  const int tid = threadIdx.x, lane = tid & 31, wb = tid & ~31;
-  if (tid < R) X[tid] = k;
-  if (tid == 0 && (R & 1)) X[R] = ~0ull;  // pad the last pair: never below a threshold
-  if (NT == kThreads) __syncthreads();
-  else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-  const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(X);
-  const int pairs = (R + 1) >> 1;
-  int ca = 0, cb = 0;
-  if (!STABLE) {
-    count_below(X2, 0, pairs, k, ca, cb);
-  } else {
-    const int qm = min(wb >> 1, pairs), qe = min((wb + 32) >> 1, pairs);
-    count_below(X2, 0, qm, k + 1, ca, cb);                   // keys before g's warp block: <= k
-    count_below_mixed(X2 + qm, qe - qm, k, lane, ca, cb);    // g's warp block
-    count_below(X2, qe, pairs, k, ca, cb);                   // keys after it: < k
-  }
-  return ca + cb;
-}
 
 // Warp: element g = i*32 + lane of R <= 32*ITEMS; block b holds keys
 // [32b, 32b+32), item i's own block is b == i (compile-time).
@@ -843,93 +748,6 @@ __device__ __forceinline__ void cta_rank_weight(int m, Scratch S) {
   __syncthreads();
 }
 
-// ------------------------------------------------------------ wide columns
-// Serial chains over a global-memory column (hub path): the lead thread walks
-// chunks of kChainChunk values staged in shared memory by warps 1..7
-// (double-buffered), so the chain runs at the FP64 add latency instead of the
-// L2 latency. The column was written by other SMs: loads bypass L1.
-constexpr int kChainChunk = 1024;
-
-__device__ __noinline__ double hub_total(const double* B, int m, double* stage) {
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int nch = (m + kChainChunk - 1) / kChainChunk;
-  double s = 0.0;
-  if (warp != 0)
-    for (int t = tid - 32; t < min(m, kChainChunk); t += kThreads - 32) stage[t] = __ldcg(B + t);
-  for (int c = 0; c < nch; ++c) {
-    __syncthreads();
-    const double* cur = stage + (c & 1) * kChainChunk;
-    if (warp != 0) {
-      double* nxt = stage + ((c + 1) & 1) * kChainChunk;
-      const int b = (c + 1) * kChainChunk;
-      for (int t = tid - 32; t < kChainChunk && b + t < m; t += kThreads - 32) nxt[t] = __ldcg(B + b + t);
-    } else if (tid == 0) {
-      const int cnt = min(kChainChunk, m - c * kChainChunk);
-      int t = 0;
-      for (; t + 8 <= cnt; t += 8) {
-        double x[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = cur[t + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, x[q]);
-      }
-      for (; t < cnt; ++t) s = __dadd_rn(s, cur[t]);
-    }
-  }
-  __syncthreads();
-  return s;
-}
-
-// suffix[g] = w[g] + suffix[g+1], right to left, written to C (global).
-__device__ __noinline__ void hub_suffix(const double* B, double* C, int m, double* stage) {
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int nch = (m + kChainChunk - 1) / kChainChunk;
-  // chunk c covers [m - (c+1)*CH, m - c*CH)
-  auto chunk_lo = [&](int c) { return max(0, m - (c + 1) * kChainChunk); };
-  if (warp != 0) {
-    const int lo = chunk_lo(0);
-    for (int t = lo + tid - 32; t < m; t += kThreads - 32) stage[t - lo] = __ldcg(B + t);
-  }
-  double s = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    __syncthreads();
-    const double* cur = stage + (c & 1) * kChainChunk;
-    const int lo = chunk_lo(c), hi = m - c * kChainChunk;
-    if (warp != 0) {
-      if (c + 1 < nch) {
-        double* nxt = stage + ((c + 1) & 1) * kChainChunk;
-        const int lo2 = chunk_lo(c + 1), hi2 = lo;
-        for (int t = lo2 + tid - 32; t < hi2; t += kThreads - 32) nxt[t - lo2] = __ldcg(B + t);
-      }
-    } else if (tid == 0) {
-      int g = hi - 1;
-      if (c == 0) {
-        s = cur[g - lo];
-        __stcg(C + g, s);
-        --g;
-      }
-      for (; g - 7 >= lo; g -= 8) {
-        double x[8], o[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = cur[g - q - lo];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          s = __dadd_rn(x[q], s);
-          o[q] = s;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) __stcg(C + g - q, o[q]);
-      }
-      for (; g >= lo; --g) {
-        s = __dadd_rn(cur[g - lo], s);
-        __stcg(C + g, s);
-      }
-    }
-  }
-  __syncthreads();
-}
-
-
 // ---- warp path: gather + raw sort, weight sort (results in A/B, natural order)
 template <int ITEMS>
 __device__ __forceinline__ void warp_sort_raw(const FactorDev& d, int k, long long fb, int fdeg,
@@ -1060,15 +878,6 @@ __device__ __forceinline__ void serial_suffix(const double* B, double* C, int m)
   }
 }
 
-// Final raw size of a vertex that just became ready, (R << 32 | row): its
-// forward degree (static, loaded alongside the decrement) plus the final fill
-// count returned by the decrement itself (high word of the counter).
-__device__ __forceinline__ unsigned long long ready_info(int r, int fdeg, unsigned long long old_cnt) {
-  return (static_cast<unsigned long long>(fdeg + static_cast<int>(old_cnt >> 32)) << 32) |
-         static_cast<unsigned>(r);
-}
-__device__ __forceinline__ int dp_of(unsigned long long c) { return static_cast<int>(c & 0xffffffffull); }
-
 // keep-one preference among the vertices an elimination made ready (max key
 // wins; the low word is the row): the widest column, or (keep_pos) the lowest
 // position -- the head of the longest remaining dependency chain.
@@ -1076,16 +885,6 @@ __device__ __forceinline__ unsigned long long keep_key(const FactorDev& d, unsig
   const unsigned row = static_cast<unsigned>(rr & 0xffffffffu);
   return d.keep_pos ? (1ull << 63) | (static_cast<unsigned long long>(0x7fffffffu - row) << 32) | row
                     : rr | (1ull << 63);
-}
-
-// TestHooks::on_phase analogue (factor_par.cpp:112-120): the eliminating
-// warp/CTA (t in [0, nt)) copies every dependency counter after its own
-// updates of this phase are performed (the caller has fenced). Inline: an
-// out-of-line call made ptxas spill around it (188 B vs 60 B in K3).
-__device__ __forceinline__ void snapshot_dp(const FactorDev& d, int phase, int t, int nt) {
-  long long* out = d.trace_dp + static_cast<long long>(phase) * d.n;
-  for (int i = t; i < d.n; i += nt) out[i] = dp_of(ld_relaxed_u64(&d.cnt[i]));
-  if (t == 0) d.trace_taken[phase] = 1;
 }
 
 // ============================================================ small path
@@ -1636,531 +1435,77 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   return cta_sample_release(d, k, smem, sh, allow_keep, S, m, lkk, lvk);
 }
 
-// ============================================================ cooperative wide columns
-// Columns with more than kBigCap raw entries (R-MAT hubs: mean ~5,600 raw
-// entries on the critical path at scale 20, up to ~10^5) take ~300 us on one
-// SM, and they are the R-MAT critical path while most SMs idle. The owner
-// (the big CTA that claimed the column) runs the elimination as phases cut
-// into 256-entry chunks and posts each phase as a job (HubJob,
-// factor_kernels.cuh); big CTAs waiting on the big queue take chunks
-// (claim_at). The owner takes chunks too, so a column completes without
-// helpers. Same arithmetic and orders as the reference:
-//   kHubGather  raw entries of tile c, ranked in shared memory (raw keys are
-//               unique) -> RK/RW, each 256-entry tile sorted by (row, source)
-//   kHubRank    each entry's place among the other tiles (binary searches over
-//               tiles staged in shared memory) -> SK/SW, the raw column sorted;
-//               run heads counted per 256-entry block of the sorted order (HB)
-//   kHubMerge   each run head sums its run left to right (factor_common.hpp:
-//               100-113) -> merged column (row << 32 | mult, weight) in RK/RW
-//   kHubWTile   each tile ranked stably by weight bits -> SK (bits) / SW
-//               (payload); meanwhile the owner walks lkk in row order
-//   kHubWRank   place among the other tiles (earlier tiles: ties count) ->
-//               WK / WB in (weight, row) order (factor_common.hpp:133-145);
-//               then the owner walks the suffix sums (sampling.hpp:72-76)
-//   kHubSample  samples i (sampling.hpp:77-83) + fill emission, the column of
-//               G in row order, ASAP levels
-//   kHubRelease decrements by multiplicity, ready rows published
-// A phase is posted (descriptor, then the release of its `next` word) only
-// after every chunk of the previous one is done, so chunks of one phase never
-// read what the same phase writes.
-enum : int { kHubGather = 1, kHubRank, kHubMerge, kHubWTile, kHubWRank, kHubSample, kHubRelease };
-constexpr int kHubTile = kThreads;                        // entries per chunk, one per thread
-constexpr int kHubGroup = kCtaSmem / (8 * kHubTile);      // tiles staged per shared-memory group
-
-struct HubArr {
-  unsigned long long *RK, *SK, *WK;
-  double *RW, *SW, *WB, *C;
-  int* HB;  // run heads per sorted block (in C's space: C is written after kHubMerge)
-};
-__device__ __forceinline__ HubArr hub_arrays(const FactorDev& d, long long slab, int cap) {
-  char* b = d.large_pool + slab * kEntryBytes;
-  const long long c8 = 8ll * cap;
-  return {reinterpret_cast<unsigned long long*>(b), reinterpret_cast<unsigned long long*>(b + 2 * c8),
-          reinterpret_cast<unsigned long long*>(b + 4 * c8), reinterpret_cast<double*>(b + c8),
-          reinterpret_cast<double*>(b + 3 * c8), reinterpret_cast<double*>(b + 5 * c8),
-          reinterpret_cast<double*>(b + 6 * c8), reinterpret_cast<int*>(b + 6 * c8)};
-}
-
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// CTA sum of one int per thread (ws: kWarps ints of shared memory).
-__device__ __forceinline__ int cta_sum(int v, int* ws) {
-  v = warp_sum(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int t = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) t += ws[w];
-  return t;
-}
-
-// Place of `key` (an element of sorted tile c of the sorted-tile array K[0, n))
-// among the other tiles: #{keys < key} in each (STABLE: earlier tiles count
-// keys <= key, the stable rule for the weight sort). Tiles are staged into
-// shared memory kHubGroup at a time; four binary searches run side by side.
-// PRED: pred = max(pred, largest key below `key` in the other tiles).
-template <bool STABLE, bool PRED>
-__device__ __forceinline__ int hub_cross_rank(const unsigned long long* K, int n, int c, unsigned long long key,
-                                              bool valid, unsigned long long* X, unsigned long long& pred) {
-  const int tid = threadIdx.x;
-  const int nt = (n + kHubTile - 1) / kHubTile;
-  int pos = 0;
-  for (int g0 = 0; g0 < nt; g0 += kHubGroup) {
-    const int g1 = min(nt, g0 + kHubGroup);
-    const int len = min(n, g1 * kHubTile) - g0 * kHubTile;
-    __syncthreads();  // the previous group (or the caller's use of X) is done
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(K + static_cast<long long>(g0) * kHubTile);
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(X);
-    for (int i = tid; 2 * i < len; i += kThreads) dst[i] = __ldcg(src + i);
-    __syncthreads();
-    if (!valid) continue;
-    for (int t = g0; t < g1; t += 4) {
-      int lo[4], tl[4];
-      unsigned long long thr[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int tt = t + q;
-        lo[q] = 0;
-        tl[q] = (tt < g1 && tt != c) ? min(kHubTile, n - tt * kHubTile) : 0;
-        thr[q] = STABLE && tt < c ? key + 1 : key;
-      }
-#pragma unroll
-      for (int step = kHubTile; step > 0; step >>= 1) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int p = lo[q] + step;
-          if (p <= tl[q] && X[(t + q - g0) * kHubTile + p - 1] < thr[q]) lo[q] = p;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        pos += lo[q];
-        if (PRED && lo[q] > 0) pred = max(pred, X[(t + q - g0) * kHubTile + lo[q] - 1]);
-      }
-    }
-  }
-  return pos;
-}
-
-// pick_by_suffix over the global suffix array through the shared-memory coarse
-// index (pick_wide), loads through L2.
-__device__ __forceinline__ int hub_pick(const double* suffix, const double* coarse, int cs, int lo, int hi,
-                                        double u) {
-  int qlo = (lo + cs - 1) / cs, qhi = hi / cs;
-  int a = lo;
-  if (qlo <= qhi && coarse[qlo] > u) {
-    while (qlo < qhi) {
-      const int mid = qlo + (qhi - qlo + 1) / 2;
-      if (coarse[mid] > u) qlo = mid; else qhi = mid - 1;
-    }
-    a = max(lo, qlo * cs);
-  }
-  int b = min(hi, a + cs);
-  while (a < b) {
-    const int mid = a + (b - a + 1) / 2;
-    if (__ldcg(suffix + mid) > u) a = mid; else b = mid - 1;
-  }
-  return a;
-}
-
-__device__ __noinline__ void hub_chunk(const FactorDev& d, const HubDesc& h, int c, char* smem, int* emitted) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const HubArr A = hub_arrays(d, h.slab, h.cap);
-  unsigned long long* X = reinterpret_cast<unsigned long long*>(smem);
-  const int b0 = c * kHubTile;
-  switch (h.phase) {
-    case kHubGather: {
-      const int cnt = min(kHubTile, h.R - b0);
-      unsigned long long key = ~0ull;
-      double w = 0.0;
-      if (tid < cnt) load_raw_dir(d, h.k, h.fb, h.fdeg, b0 + tid, h.dirrow, key, w);
-      const int r = bcast_rank_cta<false>(key, cnt, X);
-      if (tid < cnt) {
-        __stcg(A.RK + b0 + r, key);
-        __stcg(A.RW + b0 + r, w);
-      }
-      if (tid == 0) __stcg(A.HB + c, 0);
-      break;
-    }
-    case kHubRank: {
-      const int cnt = min(kHubTile, h.R - b0);
-      const bool v = tid < cnt;
-      const unsigned long long key = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
-      const double w = v ? __ldcg(A.RW + b0 + tid) : 0.0;
-      unsigned long long pred = v && tid > 0 ? __ldcg(A.RK + b0 + tid - 1) : 0ull;  // 0: none (rows are >= 1)
-      const int pos = tid + hub_cross_rank<false, true>(A.RK, h.R, c, key, v, X, pred);
-      if (v) {
-        __stcg(A.SK + pos, key);
-        __stcg(A.SW + pos, w);
-        if ((pred >> 32) != (key >> 32)) atomicAdd(A.HB + (pos / kHubTile), 1);
-      }
-      break;
-    }
-    case kHubMerge: {
-      const int cnt = min(kHubTile, h.R - b0);
-      int* ws = reinterpret_cast<int*>(X);
-      int before = 0;
-      for (int j = tid; j < c; j += kThreads) before += __ldcg(A.HB + j);
-      before = cta_sum(before, ws);
-      const int p = b0 + tid;
-      const bool v = tid < cnt;
-      const unsigned long long key = v ? __ldcg(A.SK + p) : 0ull;
-      const unsigned long long prev = v && p > 0 ? __ldcg(A.SK + p - 1) : 0ull;
-      const bool head = v && (prev >> 32) != (key >> 32);
-      const unsigned hb = __ballot_sync(kFull, head);
-      __syncthreads();  // ws reused
-      if (lane == 0) ws[kWarps + (tid >> 5)] = __popc(hb);
-      __syncthreads();
-      int off = before + __popc(hb & lanemask_lt());
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) off += w < (tid >> 5) ? ws[kWarps + w] : 0;
-      if (head) {  // the run p, p+1, ... summed left to right, 8 loads in flight
-        const unsigned row = static_cast<unsigned>(key >> 32);
-        double acc = __ldcg(A.SW + p);
-        int mult = 1;
-        bool open = true;
-        for (int q = p + 1; open && q < h.R; q += 8) {
-          unsigned long long kk[8];
-          double ww[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            kk[u] = q + u < h.R ? __ldcg(A.SK + q + u) : ~0ull;
-            ww[u] = q + u < h.R ? __ldcg(A.SW + q + u) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (open && static_cast<unsigned>(kk[u] >> 32) == row) {
-              acc = __dadd_rn(acc, ww[u]);
-              ++mult;
-            } else {
-              open = false;
-            }
-          }
-        }
-        __stcg(A.RK + off, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned>(mult));
-        __stcg(A.RW + off, acc);
-      }
-      break;
-    }
-    case kHubWTile: {
-      const int cnt = min(kHubTile, h.m - b0);
-      const bool v = tid < cnt;
-      const unsigned long long wk = v ? dbits(__ldcg(A.RW + b0 + tid)) : kInfBits;
-      const unsigned long long a = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
-      const int r = bcast_rank_cta<true>(wk, cnt, X);
-      if (v) {
-        __stcg(A.SK + b0 + r, wk);
-        __stcg(reinterpret_cast<unsigned long long*>(A.SW) + b0 + r, a);
-      }
-      break;
-    }
-    case kHubWRank: {
-      const int cnt = min(kHubTile, h.m - b0);
-      const bool v = tid < cnt;
-      const unsigned long long wk = v ? __ldcg(A.SK + b0 + tid) : kInfBits;
-      const unsigned long long a = v ? __ldcg(reinterpret_cast<const unsigned long long*>(A.SW) + b0 + tid) : 0ull;
-      unsigned long long unused = 0;
-      const int pos = tid + hub_cross_rank<true, false>(A.SK, h.m, c, wk, v, X, unused);
-      if (v) {
-        __stcg(A.WK + pos, a);
-        __stcg(A.WB + pos, bitsd(wk));
-      }
-      break;
-    }
-    case kHubSample: {
-      double* coarse = reinterpret_cast<double*>(X);
-      const int m = h.m, cs = h.cs;
-      for (int q = tid; q * cs < m; q += kThreads) coarse[q] = __ldcg(A.C + static_cast<long long>(q) * cs);
-      __syncthreads();
-      const int i = b0 + tid;
-      bool em = false;
-      int lo = 0, hi = 0, slot = -1;
-      double wv = 0.0;
-      if (i < m - 1) {  // sample_clique_sorted (sampling.hpp:77-83), as draw_sample
-        const SampleKey sk = sample_key(d, h.k);
-        const double s = __ldcg(A.C + i + 1);
-        const double u = __dmul_rn(unit_uniform(sk.seed, sk.key, static_cast<unsigned long long>(i)), s);
-        const int j = hub_pick(A.C, coarse, cs, i + 1, m - 1, u);
-        wv = __ddiv_rn(__dmul_rn(s, __ldcg(A.WB + i)), h.lkk);
-        if (wv >= kDropThreshold) {
-          const int ra = static_cast<int>(__ldcg(A.WK + i) >> 32), rc = static_cast<int>(__ldcg(A.WK + j) >> 32);
-          lo = min(ra, rc);
-          hi = max(ra, rc);
-          em = true;
-        }
-      }
-      if (em) {
-        slot = reserve_fill_slot(d, lo);
-        red_add_relaxed_u64(&d.cnt[hi], 1ull);
-      }
-      __syncwarp();
-      if (em && slot >= 0) write_fill(d, lo, slot, hi, h.k, wv);
-      const int e = __popc(__ballot_sync(kFull, em));
-      if (lane == 0 && e) atomicAdd(emitted, e);
-      if (i < m) {  // the column of G (row order) and ASAP levels
-        const unsigned long long a = __ldcg(A.RK + i);
-        const int row = static_cast<int>(a >> 32);
-        d.arena_rows[h.start + i] = row;
-        d.arena_vals[h.start + i] = __ddiv_rn(-__ldcg(A.RW + i), h.lkk);
-        if (d.level) atomicMax(&d.level[row], h.lvk + 1);
-      }
-      break;
-    }
-    case kHubRelease: {
-      const int i = b0 + tid;
-      bool rdy = false, big = false;
-      int row = 0;
-      if (i < h.m) {
-        const unsigned long long a = __ldcg(A.RK + i);
-        row = static_cast<int>(a >> 32);
-        const int mult = static_cast<int>(a & 0xffffffffu);
-        const int fd = __ldg(&d.fdeg[row]);
-        const unsigned long long old =
-            atom_add_relaxed_u64(&d.cnt[row], static_cast<unsigned long long>(-static_cast<long long>(mult)));
-        if (d.verify && dp_of(old) < mult) fail(d, kErrInternal, row);
-        if (dp_of(old) == mult) {
-          rdy = true;
-          big = static_cast<int>(ready_info(row, fd, old) >> 32) > d.small_cap;
-        }
-      }
-      publish(d, rdy, big, row, lane);
-      break;
-    }
-    default:
-      break;
-  }
-}
-
-// Take and run chunks of job `job` until its posted phase has none left. The
-// owner (own) works from its shared descriptor; a helper copies the posted one.
-__device__ __noinline__ void hub_work(const FactorDev& d, int job, char* smem, CtaShared& sh, bool own) {
-  HubJob& J = d.hub_jobs[job];
-  const int tid = threadIdx.x;
+// The big-CTA elimination loop: claims (or keeps) vertices and eliminates
+// them in shared memory until the next one is a hub column (returns 1, vertex
+// in sh.k, prologue done), a waiting CTA is asked to help a hub job (2, job
+// in sh.help), or the work is over / aborted (0). Starts from sh.k (-1: claim).
+template <bool HUBS>
+__device__ __forceinline__ int big_loop(const FactorDev& d, char* smem, CtaShared& sh) {
+  int done_local = 0;
+  int k = sh.k;
+  int chain = 0;
+  int action = 0;
   while (true) {
-    __syncthreads();  // the previous chunk's shared state is free
-    if (tid == 0) {
-      const unsigned long long old = atom_add_relaxed_u64(&J.next, 1ull);
-      const int c = static_cast<int>(old & 0xffffffull);
-      sh.hub_c = c < static_cast<int>((old >> 24) & 0xffffffull) ? c : -1;
-      sh.hub_cseq = static_cast<int>(old >> 48);
-    }
-    __syncthreads();
-    const int c = sh.hub_c;
-    if (c < 0) break;
-    fence_acq_rel();  // acquire: the phase's inputs (published before its post) are visible
-    if (!own) {       // stable until every chunk of the phase is done (ours included)
-      const unsigned* src = reinterpret_cast<const unsigned*>(&J.desc[sh.hub_cseq & 1]);
-      unsigned* dst = reinterpret_cast<unsigned*>(&sh.hd);
-      for (int w = tid; w < static_cast<int>(sizeof(HubDesc) / 4); w += kThreads) dst[w] = __ldcg(src + w);
+    bool kept = true;
+    if (k < 0) {
+      kept = false;
+      chain = 0;
+      if (threadIdx.x == 0) {
+        if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
+        if (sh.ticket < 0) sh.ticket = atomicAdd(&d.ctrl->b_head, 1);
+        int help = -1;
+        const int v = claim_at(d, true, sh.ticket, HUBS ? &help : nullptr);
+        sh.k = v;
+        sh.help = help;
+        if (v != -3) sh.ticket = -1;
+      }
+      done_local = 0;
       __syncthreads();
-    }
-    hub_chunk(d, sh.hd, c, smem, &J.emitted);
-    fence_acq_rel();  // release: this chunk's stores before its completion count
-    __syncthreads();
-    if (tid == 0) red_add_relaxed_u64(&J.done, 1ull);
-  }
-}
-
-// Owner: post phase `phase` with nch chunks (descriptor first, then the
-// release of the `next` word that helpers claim chunks from).
-__device__ __forceinline__ void hub_post(const FactorDev& d, int job, CtaShared& sh, int phase, int nch) {
-  HubJob& J = d.hub_jobs[job];
-  const int tid = threadIdx.x;
-  __syncthreads();  // sh.hd complete
-  if (tid < 32) {
-    const int seq = (sh.hub_seq + 1) & 0xffff;
-    sh.hd.phase = phase;  // lane-uniform write
-    __syncwarp();
-    const unsigned* src = reinterpret_cast<const unsigned*>(&sh.hd);
-    unsigned* dst = reinterpret_cast<unsigned*>(&J.desc[seq & 1]);
-    for (int w = tid; w < static_cast<int>(sizeof(HubDesc) / 4); w += 32) __stcg(dst + w, src[w]);
-    fence_acq_rel();
-    __syncwarp();
-    if (tid == 0) {
-      sh.hub_seq = seq;
-      st_relaxed_u64(&J.done, static_cast<unsigned long long>(seq) << 32);
-      fence_acq_rel();
-      st_relaxed_u64(&J.next, (static_cast<unsigned long long>(seq) << 48) |
-                                  (static_cast<unsigned long long>(nch) << 24));
-    }
-  }
-  __syncthreads();
-}
-
-// Owner: wait until every chunk of the posted phase is done (false: the
-// factorization aborted meanwhile).
-__device__ __forceinline__ bool hub_wait(const FactorDev& d, int job, CtaShared& sh, int nch) {
-  if (threadIdx.x == 0) {
-    const unsigned long long target = (static_cast<unsigned long long>(sh.hub_seq) << 32) |
-                                      static_cast<unsigned long long>(nch);
-    int iter = 0;
-    sh.bad = 0;
-    while (ld_relaxed_u64(&d.hub_jobs[job].done) != target) {
-      if ((++iter & 255) == 0 && ld_relaxed(&d.ctrl->status) != 0) {
-        sh.bad = 1;
+      k = sh.k;
+      __syncthreads();
+      if (k == -3) {  // help a posted hub phase, then wait on the same slot again
+        action = 2;
         break;
       }
-      __nanosleep(32);
+      if (k < 0) break;
     }
-  }
-  __syncthreads();
-  fence_acq_rel();  // acquire: the chunks' stores are visible
-  return sh.bad == 0;
-}
-
-__device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* smem, CtaShared& sh, int phase,
-                                          int nch) {
-  hub_post(d, job, sh, phase, nch);
-  hub_work(d, job, smem, sh, true);
-  return hub_wait(d, job, sh, nch);
-}
-
-__device__ __forceinline__ void hub_release_slot(const FactorDev& d, CtaShared& sh) {
-  if (threadIdx.x == 0 && sh.hub_slot >= 0) {
-    atomicAnd(&d.ctrl->hub_mask, ~(1u << sh.hub_slot));
-    atomicExch(&d.ctrl->hub_pub[sh.hub_slot], 0);
-    sh.hub_slot = -1;
-  }
-}
-
-// The owner's side of a cooperative wide-column elimination. Returns -1 (the
-// rows it made ready are all published) or -2 (abort).
-__device__ __noinline__ int hub_eliminate(const FactorDev& d, int k, char* smem, CtaShared& sh) {
-  const int tid = threadIdx.x;
-  const bool lead = tid == 0;
-  Ctrl* ctrl = d.ctrl;
-  const int job = blockIdx.x;
-  const int R = sh.R;
-  if (d.verify && lead && dp_of(ld_relaxed_u64(&d.cnt[k])) != 0) fail(d, kErrInternal, k);
-  maybe_delay(d, k, 0);
-  if (lead) {
-    sh.bad = 0;
-    const int P = next_pow2(R);
-    if (P > sh.slab_cap) {  // this CTA's slab is reused; grow it (bump allocation) when too small
-      const int cap = max(P, 2 * sh.slab_cap);
-      const long long base = static_cast<long long>(atomicAdd(&ctrl->large_bump, static_cast<unsigned long long>(cap)));
-      if (base + cap > d.large_cap) {
-        fail(d, kErrArena, k);
-        sh.bad = 1;
+    fence_acq_rel();
+    const bool lead = threadIdx.x == 0;
+    PHASE(0);
+    if (d.vsub && lead) {
+      d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
+      d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
+    }
+    cta_prologue(d, k, sh, kept);
+    if (sh.R > kBigCap) {  // the cooperative hub path (the caller calls it)
+      if (HUBS) {
+        if (lead) sh.k = k;
+        action = 1;
+      } else if (lead) {
+        fail(d, kErrNeedHubs, k);
       }
-      sh.slab = base;
-      sh.slab_cap = cap;
+      break;
     }
-    atomicAdd(&ctrl->large_cols, 1);
-    atomicMax(&ctrl->max_raw, R);
-    sh.start = static_cast<long long>(atomicAdd(&ctrl->arena_bump, static_cast<unsigned long long>(R)));
-    HubDesc& h = sh.hd;
-    h.k = k;
-    h.R = R;
-    h.m = 0;
-    h.nt = (R + kHubTile - 1) / kHubTile;
-    h.mt = 0;
-    h.fdeg = sh.fdeg;
-    h.fb = sh.fb;
-    h.lvk = d.level ? ld_relaxed(&d.level[k]) : 0;
-    h.cs = 0;
-    h.cap = sh.slab_cap;
-    h.slab = sh.slab;
-    h.start = 0;
-    h.lkk = 0.0;
-    // a public slot, so that waiting big CTAs find the job (none free: the
-    // owner works alone)
-    sh.hub_slot = -1;
-    if (!sh.bad) {
-      for (int t = 0; t < kHubSlots; ++t) {
-        const int j = (job + t) & (kHubSlots - 1);
-        if (ld_relaxed(&ctrl->hub_pub[j]) == 0 && atomicCAS(&ctrl->hub_pub[j], 0, job + 1) == 0) {
-          sh.hub_slot = j;
-          atomicOr(&ctrl->hub_mask, 1u << j);
-          break;
-        }
-      }
-    }
+    const bool allow = ++chain < d.keep_limit;
+    const int next = cta_eliminate(d, k, smem, sh, allow);
+    if (next == -2) break;
+    PHASE(7);
+    ++done_local;
+    k = next;
+    __syncthreads();
   }
-  if (tid < kDirChunks) sh.hd.dirrow[tid] = sh.dirrow[tid];
+  if (threadIdx.x == 0 && done_local) atomicAdd(&d.ctrl->eliminated, done_local);
   __syncthreads();
-  if (sh.bad) return -2;
-  SUB(0);
-  unsigned long long* wst = (d.vsub && lead) ? d.vsub + d.n * 8ll + 4ll * k : nullptr;
-  const int nt = sh.hd.nt;
-  bool ok = hub_phase(d, job, smem, sh, kHubGather, nt);
-  if (wst) wst[0] = globaltimer_ns();
-  ok = ok && hub_phase(d, job, smem, sh, kHubRank, nt);
-  if (wst) wst[1] = globaltimer_ns();
-  ok = ok && hub_phase(d, job, smem, sh, kHubMerge, nt);
-  if (!ok) {
-    hub_release_slot(d, sh);
-    return -2;
-  }
-  const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
-  int m = 0;
-  for (int j = tid; j < nt; j += kThreads) m += __ldcg(A.HB + j);
-  m = cta_sum(m, reinterpret_cast<int*>(smem));
-  if (wst) wst[2] = globaltimer_ns();
-  PHASE(1);
-  PHASE(2);
-  if (k == d.trace_k) snapshot_dp(d, 0, tid, kThreads);
-  if (m == 0) {  // (a raw entry always merges into a row)
-    hub_release_slot(d, sh);
-    if (lead) d.diag[k] = 0.0;
-    return -1;
-  }
-  if (lead) {
-    sh.hd.m = m;
-    sh.hd.mt = (m + kHubTile - 1) / kHubTile;
-  }
-  __syncthreads();
-  const int mt = sh.hd.mt;
-  double* stage = reinterpret_cast<double*>(smem);
-  double lkk;
-  if (m >= 2) {
-    // lkk (row order) on the owner while the helpers rank the weight tiles;
-    // then the owner joins the phase
-    hub_post(d, job, sh, kHubWTile, mt);
-    lkk = hub_total(A.RW, m, stage);
-    PHASE(3);
-    hub_work(d, job, smem, sh, true);
-    ok = hub_wait(d, job, sh, mt) && hub_phase(d, job, smem, sh, kHubWRank, mt);
-    if (wst) wst[3] = globaltimer_ns();
-    if (ok) hub_suffix(A.WB, A.C, m, stage);
-  } else {
-    lkk = hub_total(A.RW, m, stage);
-    PHASE(3);
-  }
-  PHASE(4);
-  if (ok && sh.start + m > d.arena_cap) {
-    if (lead) fail(d, kErrArena, k);
-    ok = false;
-  }
-  if (!ok) {
-    hub_release_slot(d, sh);
-    return -2;
-  }
-  if (lead) {
-    sh.hd.lkk = lkk;
-    sh.hd.start = sh.start;
-    sh.hd.cs = coarse_step(m);
-    d.diag[k] = lkk;
-    d.col_start[k] = sh.start;
-    d.col_len[k] = m;
-    d.hub_jobs[job].emitted = 0;  // ordered before the post by its fences
-  }
-  ok = hub_phase(d, job, smem, sh, kHubSample, mt);
-  PHASE(5);
-  if (lead) d.samples[k] = ld_relaxed(&d.hub_jobs[job].emitted);
-  maybe_delay(d, k, 1);
-  if (ok && k == d.trace_k) snapshot_dp(d, 1, tid, kThreads);
-  ok = ok && hub_phase(d, job, smem, sh, kHubRelease, mt);
-  PHASE(6);
-  if (ok && k == d.trace_k) snapshot_dp(d, 2, tid, kThreads);
-  hub_release_slot(d, sh);
-  return ok ? -1 : -2;
+  return action;
 }
 
 // ============================================================ kernel
+// HUBS: with the cooperative wide-column path (an ABI call into hub.cu; its
+// presence alone costs the kernel registers: 132 B of spills in the CTA
+// hash-merge rank loop vs none, 128^3 K3 +3%). Graphs without hub vertices
+// run the instance without it; a column wider than kBigCap there aborts the
+// run, which the host repeats with HUBS (capi.cu).
+template <bool HUBS>
 __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_constant__ FactorDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ CtaShared sh;
@@ -2226,60 +1571,39 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_con
     return;
   }
 
-  // big CTA: the whole CTA eliminates one vertex at a time
+  // big CTA: the whole CTA eliminates one vertex at a time. The calls into
+  // the hub path (hub.cu, an ABI call) sit outside the elimination loop with
+  // the loop's state parked in shared memory, so no register is live across
+  // them (values live across an ABI call cost the loop registers/spills:
+  // 128^3 K3 +0.7 ms when the call sat inside the loop).
   if (threadIdx.x == 0) {
     sh.slab = -1;
     sh.slab_cap = 0;
     sh.ticket = -1;
     sh.hub_seq = 0;
-    sh.hub_slot = -1;
+    sh.k = -1;
   }
   __syncthreads();
-  int done_local = 0;
-  int k = -1;
-  int chain = 0;
   while (true) {
-    bool kept = true;
-    if (k < 0) {
-      kept = false;
-      chain = 0;
+    const int action = big_loop<HUBS>(d, smem, sh);  // 0 done / abort, 1 hub column sh.k, 2 help job sh.help
+    if (action == 0) break;
+    if constexpr (!HUBS) {
+      break;
+    } else if (action == 1) {
+      const int r = hub_entry(d, sh.k, -1, smem, sh);
+      __syncthreads();
+      if (r == -2) break;
       if (threadIdx.x == 0) {
-        if (done_local) atomicAdd(&d.ctrl->eliminated, done_local);
-        if (sh.ticket < 0) sh.ticket = atomicAdd(&d.ctrl->b_head, 1);
-        int help = -1;
-        const int v = claim_at(d, true, sh.ticket, &help);
-        sh.k = v;
-        sh.help = help;
-        if (v != -3) sh.ticket = -1;
+        PHASE_K(7, sh.k);
+        atomicAdd(&d.ctrl->eliminated, 1);
+        sh.k = -1;
       }
-      done_local = 0;
-      __syncthreads();
-      k = sh.k;
-      __syncthreads();
-      if (k == -3) {  // help a posted hub phase, then wait on the same slot again
-        hub_work(d, sh.help, smem, sh, false);
-        k = -1;
-        continue;
-      }
-      if (k < 0) break;
+    } else {
+      hub_entry(d, -1, sh.help, smem, sh);
+      if (threadIdx.x == 0) sh.k = -1;
     }
-    fence_acq_rel();
-    const bool lead = threadIdx.x == 0;
-    PHASE(0);
-    if (d.vsub && lead) {
-      d.vsub[8 * static_cast<long long>(k) + 6] = (static_cast<unsigned long long>(blockIdx.x) << 8) | 0xff;
-      d.vsub[8 * static_cast<long long>(k) + 7] = kept ? 1 : 2;
-    }
-    cta_prologue(d, k, sh, kept);
-    const bool allow = ++chain < d.keep_limit;
-    const int next = sh.R > kBigCap ? hub_eliminate(d, k, smem, sh) : cta_eliminate(d, k, smem, sh, allow);
-    if (next == -2) break;
-    PHASE(7);
-    ++done_local;
-    k = next;
     __syncthreads();
   }
-  if (threadIdx.x == 0 && done_local) atomicAdd(&d.ctrl->eliminated, done_local);
 }
 
 int num_sms(int device) {
@@ -2290,26 +1614,47 @@ int num_sms(int device) {
 
 }  // namespace
 
-int eliminate_occupancy_grid(int device) {
-  cudaFuncSetAttribute(eliminate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
+template <bool HUBS>
+int occupancy_grid(int device) {
+  cudaFuncSetAttribute(eliminate_kernel<HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eliminate_kernel, kThreads, kCtaSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eliminate_kernel<HUBS>, kThreads, kCtaSmem);
   if (per_sm < 1) per_sm = 1;
   return per_sm * num_sms(device);
 }
+
+// The two kernel instances live in two translation units: this one (mesh
+// instance, whole-program) and eliminate_hubs.cu (the same source with
+// K3_HUBS, relocatable device code so that it can call hub.cu). Relocatable
+// compilation alone cost the mesh path 4% (128^3 K3 19.56 vs 20.40 ms).
+int occupancy_hubs(int device);
+cudaError_t launch_hubs(const FactorDev& d, int grid, cudaStream_t s);
+
+#ifndef K3_HUBS
+// Co-resident capacity (both instances: the smaller one)
+int eliminate_occupancy_grid(int device) { return std::min(occupancy_hubs(device), occupancy_grid<false>(device)); }
 
 cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used) {
   if (d.n == 0) return cudaSuccess;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int occ = eliminate_occupancy_grid(dev);
+  const int occ = d.hubs ? occupancy_hubs(dev) : occupancy_grid<false>(dev);
   int grid = grid_ctas > 0 ? grid_ctas : occ;
   if (grid > occ) grid = occ;  // persistent: every CTA must be co-resident
   if (grid < 2) grid = 2;      // at least one small and one big CTA
   if (grid_used) *grid_used = grid;
-  eliminate_kernel<<<grid, kThreads, kCtaSmem, s>>>(d);
   note_launches(1);
+  if (d.hubs) return launch_hubs(d, grid, s);
+  eliminate_kernel<false><<<grid, kThreads, kCtaSmem, s>>>(d);
   return cudaGetLastError();
 }
+#else
+int occupancy_hubs(int device) { return occupancy_grid<true>(device); }
+
+cudaError_t launch_hubs(const FactorDev& d, int grid, cudaStream_t s) {
+  eliminate_kernel<true><<<grid, kThreads, kCtaSmem, s>>>(d);
+  return cudaGetLastError();
+}
+#endif
 
 }  // namespace parac_gpu

@@ -10,7 +10,7 @@ using namespace dev;
 
 constexpr double kDropThreshold = 1e-300;  // factor_common.hpp:149
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
-enum : int { kErrArena = 10, kErrStall = 11, kErrPerm = 8, kErrInternal = 17 };
+enum : int { kErrArena = 10, kErrStall = 11, kErrPerm = 8, kErrInternal = 17, kErrNeedHubs = kStatusNeedHubs };
 
 __device__ __forceinline__ void fail(const FactorDev& d, int code, long long info) {
   if (atomicCAS(&d.ctrl->status, 0, code) == 0) d.ctrl->err_info = info;

@@ -38,11 +38,10 @@ constexpr int kBigCap = 1024;
 // Cooperative wide columns (raw size > kBigCap, R-MAT hubs). The big CTA that
 // claims such a column (the owner) runs its elimination as a sequence of
 // phases, each cut into 256-entry chunks and posted as a job; big CTAs that
-// are waiting for a queue slot take chunks of any posted job (helpers). The
-// owner takes chunks too, so a column finishes with or without helpers.
-constexpr int kHubSlots = 32;  // public job slots (Ctrl::hub_mask bits)
+// are waiting for a queue slot take chunks (helpers). The owner takes chunks
+// too, so a column finishes with or without helpers.
 struct HubDesc {                // one phase of one column (read by every chunk)
-  int k, R, m, nt, mt, fdeg, lvk, cs, phase, cap;
+  int k, R, m, nt, mt, fdeg, lvk, cs, phase, cap, trace, pad_;
   long long fb, slab, start;
   double lkk;
   unsigned dirrow[kDirChunks];
@@ -55,6 +54,15 @@ struct HubJob {  // one per CTA of the elimination grid
   alignas(256) HubDesc desc[2];          // by seq parity
   alignas(256) int emitted;              // fills emitted by the sampling phase
 };
+// Optional per-column trace of the hub path (record_times; tools/profile_factor.py):
+// [0] k [1] R [2] m [3] owner start [4] owner end (globaltimer ns), then per
+// step p = 1..9 (7 phases, 8 = lkk chain, 9 = suffix chain) at 8 + 4 (p - 1):
+// posted, first chunk started, last chunk ended, owner chunks << 32 | helper chunks
+constexpr int kHubTraceWords = 48;
+// Ctrl::status when a column wider than kBigCap met the kernel instance
+// without the hub path: the host re-runs with it (never returned to callers)
+constexpr int kStatusNeedHubs = 90;
+constexpr int kHubTraceCap = 1 << 16;
 
 // Control block. The counters every elimination touches (queue heads and
 // tails, the column arena bump, the eliminated count, the status word the
@@ -76,8 +84,7 @@ struct Ctrl {
   long long total_fills;
   long long err_info;
   alignas(256) int sm_slot[256];             // CTAs started per SM (role assignment)
-  alignas(256) unsigned hub_mask;            // public hub job slots in use (helpers poll this word)
-  alignas(256) int hub_pub[kHubSlots];       // slot -> job index + 1 (0: free)
+  alignas(256) int hub_hint;                 // job index + 1 of the latest posted hub phase (0: none)
 };
 
 struct FactorDev {
@@ -125,6 +132,9 @@ struct FactorDev {
   char* large_pool;
   long long large_cap;
   HubJob* hub_jobs;  // [grid] cooperative wide-column jobs, one per CTA
+  unsigned long long* hub_trace;  // optional [kHubTraceCap * kHubTraceWords]
+  unsigned long long hub_linger_ns;  // a helper waits this long for a job's next phase
+  int hubs;          // launch the kernel with the cooperative hub path (hub graphs; see launch_eliminate)
   // control
   Ctrl* ctrl;
   unsigned long long sample_seed;

@@ -1,0 +1,133 @@
+// Pieces of K3 (the persistent elimination kernel) shared by its two
+// translation units: eliminate.cu (the kernel, the warp and CTA paths) and
+// hub.cu (the cooperative wide-column path, compiled separately so that its
+// register allocation does not constrain the kernel's: see hub.cu).
+#pragma once
+#include "factor_device.cuh"
+#include "factor_kernels.cuh"
+
+namespace parac_gpu {
+namespace k3 {
+
+using namespace dev;
+using namespace fdev;
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kEntryBytes = kSlabEntryBytes;
+// small warps: A, B, C + two rank-sort segment buffers (X1, X2)
+constexpr int kSmallBytes = kSmallCap * 8 * 5;
+// big CTAs: A, B, C (kBigCap x 8 B each) + D, E (second exchange buffer)
+constexpr int kBigBytes = kBigCap * 8 * 5;
+constexpr int kCtaSmem = kWarps * kSmallBytes > kBigBytes ? kWarps * kSmallBytes : kBigBytes;
+
+#define PHASE(i) \
+  do { if (d.vtimes && lead) d.vtimes[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
+// sub-phase stamps (record_times diagnostics): 0 setup done, 1 gather landed,
+// 2 weight sort done, 3 samples drawn, 4 fills written, 5 fence done
+#define PHASE_K(i, kk) \
+  do { if (d.vtimes) d.vtimes[8 * static_cast<long long>(kk) + (i)] = globaltimer_ns(); } while (0)
+#define SUB(i) \
+  do { if (d.vsub && lead) d.vsub[8 * static_cast<long long>(k) + (i)] = globaltimer_ns(); } while (0)
+
+// Shared state of a big CTA (one vertex at a time).
+struct CtaShared {
+  int k;
+  int m;
+  int nready;
+  int emitted;
+  int carry_row;
+  int bad;
+  double lkk;
+  long long start;
+  long long slab;      // this CTA's wide-column slab (entries), -1 none
+  int slab_cap;
+  long long fb;        // cta_prologue: forward offset, degree, raw size
+  int fdeg, R;
+  unsigned dirrow[kDirChunks];
+  int wcount[kWarps];
+  unsigned long long best[kWarps];
+  int next_R;          // raw size of the kept vertex
+  int mbump, mcount;   // cta_hash_merge: stage bump, distinct rows
+  unsigned long long bestkey;  // keep-one: max keep_key over the rows made ready
+  int hbad;            // cta_hash_merge: a run longer than kRunCap
+  // cooperative wide columns (hub path)
+  int ticket;          // big-queue slot this CTA waits on (-1: none), kept while it helps
+  int help;            // job a waiting CTA was sent to help
+  int hub_c, hub_cseq; // chunk taken, and the phase sequence it belongs to
+  int hub_seq;         // owner: sequence number of its last posted phase
+  HubDesc hd;          // the phase being worked on
+};
+
+// c += #{keys of pairs [q0, q1) of P below thr} (two accumulators per element)
+__device__ __forceinline__ void count_below(const ulonglong2* P, int q0, int q1, unsigned long long thr, int& ca,
+                                            int& cb) {
+#pragma unroll 2
+  for (int q = q0; q < q1; ++q) {
+    const ulonglong2 p = P[q];
+    ca += static_cast<int>(p.x < thr);
+    cb += static_cast<int>(p.y < thr);
+  }
+}
+// The mixed block (keys t = 2q, 2q+1 relative to the block): threshold k + 1
+// before position `pos` in the block, k from it on.
+__device__ __forceinline__ void count_below_mixed(const ulonglong2* P, int pairs, unsigned long long k, int pos,
+                                                  int& ca, int& cb) {
+  const unsigned long long k1 = k + 1;
+#pragma unroll 2
+  for (int q = 0; q < pairs; ++q) {
+    const ulonglong2 p = P[q];
+    ca += static_cast<int>(p.x < (2 * q < pos ? k1 : k));
+    cb += static_cast<int>(p.y < (2 * q + 1 < pos ? k1 : k));
+  }
+}
+
+// CTA: element g = threadIdx.x < R <= NT (one per thread); the first NT
+// threads take part (NT < kThreads: named barrier 1, the other warps are free
+// to do something else meanwhile).
+template <bool STABLE, int NT = kThreads>
+__device__ __forceinline__ int bcast_rank_cta(unsigned long long k, int R, unsigned long long* X) {
+  const int tid = threadIdx.x, lane = tid & 31, wb = tid & ~31;
+  if (tid < R) X[tid] = k;
+  if (tid == 0 && (R & 1)) X[R] = ~0ull;  // pad the last pair: never below a threshold
+  if (NT == kThreads) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(X);
+  const int pairs = (R + 1) >> 1;
+  int ca = 0, cb = 0;
+  if (!STABLE) {
+    count_below(X2, 0, pairs, k, ca, cb);
+  } else {
+    const int qm = min(wb >> 1, pairs), qe = min((wb + 32) >> 1, pairs);
+    count_below(X2, 0, qm, k + 1, ca, cb);                   // keys before g's warp block: <= k
+    count_below_mixed(X2 + qm, qe - qm, k, lane, ca, cb);    // g's warp block
+    count_below(X2, qe, pairs, k, ca, cb);                   // keys after it: < k
+  }
+  return ca + cb;
+}
+
+// Final raw size of a vertex that just became ready, (R << 32 | row): its
+// forward degree (static, loaded alongside the decrement) plus the final fill
+// count returned by the decrement itself (high word of the counter).
+__device__ __forceinline__ unsigned long long ready_info(int r, int fdeg, unsigned long long old_cnt) {
+  return (static_cast<unsigned long long>(fdeg + static_cast<int>(old_cnt >> 32)) << 32) |
+         static_cast<unsigned>(r);
+}
+__device__ __forceinline__ int dp_of(unsigned long long c) { return static_cast<int>(c & 0xffffffffull); }
+
+// TestHooks::on_phase analogue (factor_par.cpp:112-120): the eliminating
+// warp/CTA (t in [0, nt)) copies every dependency counter after its own
+// updates of this phase are performed (the caller has fenced). Inline: an
+// out-of-line call made ptxas spill around it (188 B vs 60 B in K3).
+__device__ __forceinline__ void snapshot_dp(const FactorDev& d, int phase, int t, int nt) {
+  long long* out = d.trace_dp + static_cast<long long>(phase) * d.n;
+  for (int i = t; i < d.n; i += nt) out[i] = dp_of(ld_relaxed_u64(&d.cnt[i]));
+  if (t == 0) d.trace_taken[phase] = 1;
+}
+
+// The cooperative wide-column path (hub.cu): k >= 0 -> this CTA (the owner)
+// eliminates k, returns -1 or -2 (abort); k < 0 -> help job `job`.
+__device__ int hub_entry(const FactorDev& d, int k, int job, char* smem, CtaShared& sh);
+
+}  // namespace k3
+}  // namespace parac_gpu

@@ -222,6 +222,7 @@ class FactorStats:
     assemble_ms: float = 0.0
     device_ms: float = 0.0
     upload_ms: float = 0.0
+    attempts: int = 0
 
 
 @dataclass
@@ -427,6 +428,7 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
         stats.assemble_ms = info.assemble_ms
         stats.device_ms = info.device_ms
         stats.upload_ms = info.upload_ms
+        stats.attempts = info.attempts
         # FactorStats::seconds is wall time at the API, as in the reference
         # (factor_seq.cpp:46, factor_par.cpp); device_ms holds the device time
         stats.seconds = time.perf_counter() - t0

@@ -214,3 +214,19 @@ def test_phase_trace_on_a_hub_column(gpu_ctx, port):
     # chunks that decremented them, so later eliminations may already have
     # moved the leaves' counters by the time of this snapshot)
     assert snaps["decremented"][0] == 0
+
+
+def test_hub_column_on_the_mesh_kernel_instance_reruns(gpu_ctx, port, monkeypatch):
+    """A column wider than 1024 raw entries met by the kernel instance without
+    the hub path (chosen for graphs without hub vertices; forced here) aborts
+    the pass, and the library re-runs it with the hub path: same bits."""
+    monkeypatch.setenv("PARAC_HUBS", "0")
+    g = P.gen_rmat(12, 16, 0)
+    perm = P.ordering_random(g.n, 0).perm
+    f, st = gpu_factor(gpu_ctx, g, perm, 0)
+    assert st.large_columns > 0 and st.attempts == 2
+    assert f.same_values(factor_from_port(port.factor(g, perm, 0)))
+    # without the override the instance with the hub path runs first
+    monkeypatch.delenv("PARAC_HUBS")
+    f2, st2 = gpu_factor(gpu_ctx, g, perm, 0)
+    assert st2.attempts == 1 and f2.same_values(f)

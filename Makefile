@@ -30,6 +30,7 @@ lib: $(LIB)
 $(OBJDIR)/eliminate_hubs.o: NVFLAGS += -rdc=true
 $(OBJDIR)/eliminate_hubs.o: $(PKG)/csrc/cuda/eliminate.cu
 $(OBJDIR)/hub.o: NVFLAGS += -rdc=true -maxrregcount=64
+$(OBJDIR)/hub_chains.o: NVFLAGS += -rdc=true -maxrregcount=64
 
 $(OBJDIR)/%.o: $(PKG)/csrc/cuda/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)

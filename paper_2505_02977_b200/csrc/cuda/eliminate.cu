@@ -1507,9 +1507,17 @@ __device__ __forceinline__ int big_loop(const FactorDev& d, char* smem, CtaShare
 // run, which the host repeats with HUBS (capi.cu).
 template <bool HUBS>
 __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_constant__ FactorDev d) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ CtaShared sh;
-  char* smem = reinterpret_cast<char*>(smem_raw);
+  // the hub instance keeps its CtaShared in dynamic shared memory, where
+  // hub.cu names it (k3_sh); the mesh instance keeps it static
+  __shared__ CtaShared sh_static;
+  CtaShared& sh = HUBS ? k3_sh() : sh_static;
+  char* smem = k3_scratch();
+  if (HUBS) {  // the FactorDev copy hub.cu works from
+    const unsigned* src = reinterpret_cast<const unsigned*>(&d);
+    unsigned* dst = reinterpret_cast<unsigned*>(k3_scratch() + kCtaSmem + kShBytes);
+    for (int w = threadIdx.x; w < static_cast<int>(sizeof(FactorDev) / 4); w += kThreads) dst[w] = src[w];
+    __syncthreads();
+  }
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   if (ld_relaxed(&d.ctrl->status) != 0) return;
@@ -1590,7 +1598,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_con
     if constexpr (!HUBS) {
       break;
     } else if (action == 1) {
-      const int r = hub_entry(d, sh.k, -1, smem, sh);
+      const int r = hub_entry(d, sh.k, -1);
       __syncthreads();
       if (r == -2) break;
       if (threadIdx.x == 0) {
@@ -1599,7 +1607,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_con
         sh.k = -1;
       }
     } else {
-      hub_entry(d, -1, sh.help, smem, sh);
+      hub_entry(d, -1, sh.help);
       if (threadIdx.x == 0) sh.k = -1;
     }
     __syncthreads();
@@ -1615,10 +1623,13 @@ int num_sms(int device) {
 }  // namespace
 
 template <bool HUBS>
+constexpr int dyn_smem() { return HUBS ? kDynSmemHub : kCtaSmem; }
+
+template <bool HUBS>
 int occupancy_grid(int device) {
-  cudaFuncSetAttribute(eliminate_kernel<HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmem);
+  cudaFuncSetAttribute(eliminate_kernel<HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem<HUBS>());
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eliminate_kernel<HUBS>, kThreads, kCtaSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eliminate_kernel<HUBS>, kThreads, dyn_smem<HUBS>());
   if (per_sm < 1) per_sm = 1;
   return per_sm * num_sms(device);
 }
@@ -1645,14 +1656,14 @@ cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, 
   if (grid_used) *grid_used = grid;
   note_launches(1);
   if (d.hubs) return launch_hubs(d, grid, s);
-  eliminate_kernel<false><<<grid, kThreads, kCtaSmem, s>>>(d);
+  eliminate_kernel<false><<<grid, kThreads, dyn_smem<false>(), s>>>(d);
   return cudaGetLastError();
 }
 #else
 int occupancy_hubs(int device) { return occupancy_grid<true>(device); }
 
 cudaError_t launch_hubs(const FactorDev& d, int grid, cudaStream_t s) {
-  eliminate_kernel<true><<<grid, kThreads, kCtaSmem, s>>>(d);
+  eliminate_kernel<true><<<grid, kThreads, dyn_smem<true>(), s>>>(d);
   return cudaGetLastError();
 }
 #endif

@@ -59,12 +59,6 @@ __device__ __forceinline__ HubArr hub_arrays(const FactorDev& d, long long slab,
           reinterpret_cast<double*>(b + 6 * c8), reinterpret_cast<int*>(b + 6 * c8)};
 }
 
-// record_times diagnostics: this column's trace record and step p's 4 words
-__device__ __forceinline__ unsigned long long* hub_rec(const FactorDev& d, const HubDesc& h) {
-  return h.trace >= 0 ? d.hub_trace + static_cast<long long>(h.trace) * kHubTraceWords : nullptr;
-}
-__device__ __forceinline__ unsigned long long* hub_step(unsigned long long* rec, int p) { return rec + 8 + 4 * (p - 1); }
-
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -79,24 +73,6 @@ __device__ __forceinline__ int cta_sum(int v, int* ws) {
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) t += ws[w];
   return t;
-}
-
-// dst[i] = src[i * stride], i < cnt, by threads t = 0..nt-1 (four loads in
-// flight per thread: a loop of single load -> store pairs waits one L2 round
-// trip per element)
-template <typename T>
-__device__ __forceinline__ void stage_in(T* dst, const T* src, int cnt, int t, int nt, int stride = 1) {
-  for (int i0 = t; i0 < cnt; i0 += 4 * nt) {
-    T v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * nt;
-      if (i < cnt) v[u] = __ldcg(src + static_cast<long long>(i) * stride);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i0 + u * nt < cnt) dst[i0 + u * nt] = v[u];
-  }
 }
 
 // Place of `key` (an element of sorted tile c of the sorted-tile array K[0, n))
@@ -114,7 +90,7 @@ __device__ __forceinline__ int hub_cross_rank(const unsigned long long* K, int n
     const int g1 = min(nt, g0 + kHubGroup);
     const int len = min(n, g1 * kHubTile) - g0 * kHubTile;
     __syncthreads();  // the previous group (or the caller's use of X) is done
-    stage_in(X, K + static_cast<long long>(g0) * kHubTile, len, tid, kThreads);
+    stage_in<8>(X, K + static_cast<long long>(g0) * kHubTile, len, tid, kThreads);
     __syncthreads();
     if (!valid) continue;
     for (int t = g0; t < g1; t += 4) {
@@ -166,7 +142,10 @@ __device__ __forceinline__ int hub_pick(const double* suffix, const double* coar
   return a;
 }
 
-__device__ __noinline__ void hub_chunk(const FactorDev& d, const HubDesc& h, int c, char* smem, int* emitted) {
+__device__ __noinline__ void hub_chunk(int c, int* emitted) {
+  const FactorDev& d = k3_dev();
+  const HubDesc& h = k3_sh().hd;
+  char* smem = k3_scratch();
   const int tid = threadIdx.x, lane = tid & 31;
   const HubArr A = hub_arrays(d, h.slab, h.cap);
   unsigned long long* X = reinterpret_cast<unsigned long long*>(smem);
@@ -341,7 +320,7 @@ __device__ __forceinline__ void hub_run_chunk(const FactorDev& d, HubJob& J, int
                                               bool own) {
   unsigned long long* rec = threadIdx.x == 0 ? hub_rec(d, sh.hd) : nullptr;
   if (rec) atomicMin(hub_step(rec, sh.hd.phase) + 1, globaltimer_ns());
-  hub_chunk(d, sh.hd, c, smem, &J.emitted);
+  hub_chunk(c, &J.emitted);
   fence_acq_rel();
   __syncthreads();
   if (threadIdx.x == 0) red_add_relaxed_u64(&J.done, 1ull);
@@ -481,120 +460,6 @@ __device__ __forceinline__ void hub_finish(const FactorDev& d, int job, CtaShare
   }
 }
 
-// ---- the owner's serial chains, side by side: lkk = ((0 + w0) + w1) + ...
-// over the merged column in row order (factor_common.hpp:117-121), and the
-// suffix sums of the weight-ordered column strictly right to left
-// (sampling.hpp:72-76). Each chain is walked by one thread over
-// kChainChunk-value chunks that the other warps of its group stage in shared
-// memory (double-buffered, loads batched), so it runs at the FP64 add
-// latency; the suffix chain's outputs go back through shared memory and its
-// group writes them out coalesced. Group A (lkk): warps 0, 2, 3 (named
-// barrier 1); group B (suffix): warps 1, 4..7 (named barrier 2).
-constexpr int kChainChunk = 512;
-
-__device__ __forceinline__ void named_bar(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// s + x[0] + ... + x[cnt-1], left to right (8 staged values per step)
-__device__ __forceinline__ double chain_sum(double s, const double* x, int cnt) {
-  int t = 0;
-  for (; t + 8 <= cnt; t += 8) {
-    double a[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = x[t + q];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s = __dadd_rn(s, a[q]);
-  }
-  for (; t < cnt; ++t) s = __dadd_rn(s, x[t]);
-  return s;
-}
-
-// o[g] = x[g] + (o[g+1] or the carried s), g = cnt-1 .. 0 (first chunk: the
-// chain starts at x[cnt-1] itself). Returns the carried sum.
-__device__ __forceinline__ double chain_suffix(double s, bool first, const double* x, double* o, int cnt) {
-  int g = cnt - 1;
-  if (first) {
-    s = x[g];
-    o[g] = s;
-    --g;
-  }
-  for (; g >= 7; g -= 8) {
-    double a[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = x[g - q];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      s = __dadd_rn(a[q], s);
-      o[g - q] = s;
-    }
-  }
-  for (; g >= 0; --g) {
-    s = __dadd_rn(x[g], s);
-    o[g] = s;
-  }
-  return s;
-}
-
-// Returns lkk (every thread); with suffix, C[0, m) = suffix sums of WB.
-__device__ __noinline__ double hub_chains(const double* W, const double* WB, double* C, int m, bool suffix,
-                                          double* smem) {
-  constexpr int CH = kChainChunk;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nch = (m + CH - 1) / CH;
-  double* LA = smem;           // lkk input, 2 x CH
-  double* SB = smem + 2 * CH;  // suffix input, 2 x CH
-  double* SO = smem + 4 * CH;  // suffix output, 2 x CH
-  double* res = smem + 6 * CH;
-  if (warp == 0 || warp == 2 || warp == 3) {
-    const int gt = warp == 0 ? -1 : (warp - 2) * 32 + lane;  // stager 0..63
-    if (gt >= 0) stage_in(LA, W, min(CH, m), gt, 64);
-    named_bar(1, 96);
-    double s = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      if (gt >= 0) {
-        if (c + 1 < nch) stage_in(LA + ((c + 1) & 1) * CH, W + (c + 1) * CH, min(CH, m - (c + 1) * CH), gt, 64);
-      } else if (lane == 0) {
-        s = chain_sum(s, LA + (c & 1) * CH, min(CH, m - c * CH));
-      }
-      named_bar(1, 96);
-    }
-    if (tid == 0) *res = s;
-  } else if (suffix) {
-    const int gt = warp == 1 ? -1 : (warp - 4) * 32 + lane;  // stager / writer 0..127
-    if (gt >= 0) {
-      const int lo = max(0, m - CH);
-      stage_in(SB, WB + lo, m - lo, gt, 128);
-    }
-    named_bar(2, 160);
-    double s = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      const int lo = max(0, m - (c + 1) * CH), hi = m - c * CH;
-      if (gt >= 0) {
-        if (c + 1 < nch) {
-          const int lo2 = max(0, m - (c + 2) * CH);
-          stage_in(SB + ((c + 1) & 1) * CH, WB + lo2, lo - lo2, gt, 128);
-        }
-        if (c >= 1) {  // chunk c-1 = [hi, hi + CH)
-          const double* o = SO + ((c - 1) & 1) * CH;
-          for (int i = gt; i < CH; i += 128) __stcg(C + hi + i, o[i]);
-        }
-      } else if (lane == 0) {
-        s = chain_suffix(s, c == 0, SB + (c & 1) * CH, SO + (c & 1) * CH, hi - lo);
-      }
-      named_bar(2, 160);
-    }
-    if (gt >= 0) {  // the last chunk: [0, m - (nch - 1) * CH)
-      const double* o = SO + ((nch - 1) & 1) * CH;
-      for (int i = gt; i < m - (nch - 1) * CH; i += 128) __stcg(C + i, o[i]);
-    }
-  }
-  __syncthreads();
-  const double lkk = *res;
-  __syncthreads();  // res / buffers free for the caller
-  return lkk;
-}
-
 // The owner's side of a cooperative wide-column elimination: the phases in
 // order, with the owner's own steps between them (column size after the
 // merge, the serial chains before sampling). Little state lives across the
@@ -672,13 +537,15 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       const int m = sh.hd.m;
       if (m == 0) break;  // (a raw entry always merges into a row)
       unsigned long long* rec = lead ? hub_rec(d, sh.hd) : nullptr;
-      if (rec) hub_step(rec, 8)[0] = globaltimer_ns();
+      if (rec) {
+        hub_step(rec, 8)[0] = globaltimer_ns();
+        hub_step(rec, 9)[0] = hub_step(rec, 8)[0];
+      }
       {
         const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
-        const double lkk = hub_chains(A.RW, A.WB, A.C, m, m >= 2, reinterpret_cast<double*>(smem));
+        const double lkk = hub_chains(A.RW, A.WB, A.C, m, m >= 2, rec);
         if (lead) sh.hd.lkk = lkk;
       }
-      if (rec) hub_step(rec, 8)[2] = globaltimer_ns();
       PHASE(4);
       if (lead) {
         if (sh.start + m > d.arena_cap) {
@@ -725,7 +592,10 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
 }  // namespace
 
 // The kernel's single entry into the hub path (declared in k3_common.cuh).
-__device__ int hub_entry(const FactorDev& d, int k, int job, char* smem, CtaShared& sh) {
+__device__ int hub_entry(const FactorDev&, int k, int job) {
+  const FactorDev& d = k3_dev();
+  char* smem = k3_scratch();
+  CtaShared& sh = k3_sh();
   if (k >= 0) return hub_eliminate(d, k, smem, sh);
   hub_help(d, job, smem, sh);
   return -1;

@@ -125,9 +125,56 @@ __device__ __forceinline__ void snapshot_dp(const FactorDev& d, int phase, int t
   if (t == 0) d.trace_taken[phase] = 1;
 }
 
+// record_times diagnostics: this column's trace record and step p's 4 words
+__device__ __forceinline__ unsigned long long* hub_rec(const FactorDev& d, const HubDesc& h) {
+  return h.trace >= 0 ? d.hub_trace + static_cast<long long>(h.trace) * kHubTraceWords : nullptr;
+}
+__device__ __forceinline__ unsigned long long* hub_step(unsigned long long* rec, int p) { return rec + 8 + 4 * (p - 1); }
+
+// dst[i] = src[i * stride], i < cnt, by threads t = 0..nt-1 (four loads in
+// flight per thread: a loop of single load -> store pairs waits one L2 round
+// trip per element)
+template <int U = 4, typename T>
+__device__ __forceinline__ void stage_in(T* dst, const T* src, int cnt, int t, int nt, int stride = 1) {
+  for (int i0 = t; i0 < cnt; i0 += U * nt) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nt;
+      if (i < cnt) v[u] = __ldcg(src + static_cast<long long>(i) * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * nt < cnt) dst[i0 + u * nt] = v[u];
+  }
+}
+
+// The owner's serial chains of a hub column (hub_chains.cu): returns lkk of
+// the row-ordered merged weights W[0, m); with suffix, C = suffix sums of the
+// weight-ordered WB. rec: optional trace record.
+__device__ double hub_chains(const double* W, const double* WB, double* C, int m, bool suffix,
+                             unsigned long long* rec);
+
+// The hub kernel instance's dynamic shared memory: the per-CTA scratch
+// (kCtaSmem bytes), then the CtaShared block. Every translation unit names it
+// through this extern array, so the accesses compile to shared-memory
+// instructions: a pointer handed across an out-of-line call is generic
+// (LD/ST instead of LDS/STS, ~2x the latency in the serial chains).
+extern __shared__ __align__(16) unsigned char k3_dyn_smem[];
+// A copy of the kernel's FactorDev follows (the kernel parameter itself is
+// reachable from another unit only through a generic pointer).
+constexpr int kShBytes = (static_cast<int>(sizeof(CtaShared)) + 15) & ~15;
+constexpr int kDevBytes = (static_cast<int>(sizeof(FactorDev)) + 15) & ~15;
+constexpr int kDynSmemHub = kCtaSmem + kShBytes + kDevBytes;
+__device__ __forceinline__ char* k3_scratch() { return reinterpret_cast<char*>(k3_dyn_smem); }
+__device__ __forceinline__ CtaShared& k3_sh() { return *reinterpret_cast<CtaShared*>(k3_dyn_smem + kCtaSmem); }
+__device__ __forceinline__ const FactorDev& k3_dev() {
+  return *reinterpret_cast<const FactorDev*>(k3_dyn_smem + kCtaSmem + kShBytes);
+}
+
 // The cooperative wide-column path (hub.cu): k >= 0 -> this CTA (the owner)
 // eliminates k, returns -1 or -2 (abort); k < 0 -> help job `job`.
-__device__ int hub_entry(const FactorDev& d, int k, int job, char* smem, CtaShared& sh);
+__device__ int hub_entry(const FactorDev& d, int k, int job);
 
 }  // namespace k3
 }  // namespace parac_gpu

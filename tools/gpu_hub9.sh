@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+echo "== rmat20 $(timeout 300 python tools/rmat_time.py --scale 20 --reps 2 2>&1 | tail -1)" >> gpurun_out/variants.txt
+timeout 300 python tools/hub_trace.py --scale 20 --json gpurun_out/hub_trace20.json > /dev/null 2>&1

@@ -21,15 +21,22 @@ import paper_2505_02977_b200 as P  # noqa: E402
 WORDS = 48
 STEPS = ["gather+tile", "cross rank", "merge", "weight tiles", "weight rank", "sample+column", "release",
          "lkk chain", "suffix chain"]
+# each phase is posted by the CTA that completed the previous one's last chunk
+# (the owner posts gather and sample): span = post -> last chunk end
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=int, default=20)
+    ap.add_argument("--star", type=int, default=0, help="a star with this many leaves instead (one hub column)")
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
-    g = P.gen_rmat(args.scale, 16, 0)
-    o = P.ordering_random(g.n, 0)
+    if args.star:  # centre 0 eliminated first, every leaf waits on it
+        n = args.star + 1
+        g = P.LaplacianGraph.from_edges(n, [(0, v, 1.0 + (v % 7) * 0.25) for v in range(1, n)])
+    else:
+        g = P.gen_rmat(args.scale, 16, 0)
+    o = P.Ordering.identity(g.n) if args.star else P.ordering_random(g.n, 0)
     ctx = P.GpuContext(0)
     st = P.FactorStats()
     for _ in range(2):
@@ -56,6 +63,11 @@ def main():
             if not ok.any():
                 continue
             e = {"span_us": float(((last - post)[ok]).mean() / 1e3)}
+            if p >= 8:  # chain thread: cycles in the chain << 32 | cycles at its group barrier
+                e["chain_busy_cycles"] = float((ch[ok] >> np.uint64(32)).astype(np.float64).mean())
+                e["barrier_wait_cycles"] = float((ch[ok] & np.uint64(0xffffffff)).astype(np.float64).mean())
+                per = (ch[ok] >> np.uint64(32)).astype(np.float64) / np.maximum(m[sel][ok], 1)
+                e["cycles_per_element_p10_p50_p90"] = [float(np.percentile(per, q)) for q in (10, 50, 90)]
             if p <= 7:
                 okf = ok & (first < 2 ** 63)
                 e["join_us"] = float(((first - post)[okf]).mean() / 1e3) if okf.any() else None

@@ -255,7 +255,7 @@ __device__ __noinline__ void hub_chunk(int c, int* emitted) {
       const bool smp = i < m - 1, col = i < m;
       double* S = reinterpret_cast<double*>(X);
       const bool full = m <= kHubFullSuffix;
-      if (full) stage_in(S, A.C, m, tid, kThreads);
+      if (full) stage_in<8>(S, A.C, m, tid, kThreads);
       else stage_in(S, A.C, (m + h.cs - 1) / h.cs, tid, kThreads, h.cs);
       __syncthreads();
       bool em = false;
@@ -360,12 +360,12 @@ __device__ __forceinline__ void hub_help(const FactorDev& d, int job, char* smem
         const int hj = ld_relaxed(&d.ctrl->hub_hint) - 1;
         if (hj >= 0 && hj != j) {
           const unsigned long long hx = ld_relaxed_u64(&d.hub_jobs[hj].next);
-          if ((hx & 0xffffffull) < ((hx >> 24) & 0xffffffull)) {
-            j = hj;
+          if (nch == 0 || (hx & 0xffffffull) < ((hx >> 24) & 0xffffffull)) {
+            j = hj;  // (this job is over: stay with the newest one)
             continue;
           }
         }
-        if (nch == 0) break;  // finished
+        if (nch == 0) break;  // finished, and no other job posted
         if (sh.ticket >= 0 && ld_relaxed(&d.bqueue[sh.ticket]) >= 0) break;
         if (globaltimer_ns() - idle0 > d.hub_linger_ns || ld_relaxed(&d.ctrl->status) != 0) break;
         __nanosleep(64);

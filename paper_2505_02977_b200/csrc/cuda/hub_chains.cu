@@ -50,10 +50,13 @@ __device__ __forceinline__ double chain_sum(double s, const double* x, int cnt) 
 }
 
 // o[g] = x[g] + (o[g+1] or the carried s), g = cnt-1 .. 0 (first chunk: the
-// chain starts at x[cnt-1] itself). Returns the carried sum. The next 8
-// values load before the current 8 are added and stored: with x and o both
-// shared memory the compiler cannot move those loads above the stores itself
-// (measured 12.3 -> ~9.5 cycles per element in isolation).
+// chain starts at x[cnt-1] itself). Returns the carried sum. The running sum
+// is the first operand (addition commutes exactly; this order is what the
+// lkk chain runs at). The next 8
+// values load before the current 8 are added and stored (with x and o both
+// shared memory the compiler cannot move those loads above the stores
+// itself), in 16-byte pairs once g is odd: one load and one store per two
+// elements.
 __device__ __forceinline__ double chain_suffix(double s, bool first, const double* x, double* o, int cnt) {
   int g = cnt - 1;
   if (first) {
@@ -61,31 +64,42 @@ __device__ __forceinline__ double chain_suffix(double s, bool first, const doubl
     o[g] = s;
     --g;
   }
+  if (g >= 0 && (g & 1) == 0) {  // from here g is odd: pairs (g-1, g) are 16-byte aligned
+    s = __dadd_rn(s, x[g]);
+    o[g] = s;
+    --g;
+  }
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double2* o2 = reinterpret_cast<double2*>(o);
   if (g >= 7) {
-    double a[8];
+    double2 a[4];  // a[q] = elements (g-1-2q, g-2q)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = x[g - q];
+    for (int q = 0; q < 4; ++q) a[q] = x2[(g - 1) / 2 - q];
     for (; g - 15 >= 0; g -= 8) {
-      double b[8];
+      double2 b[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) b[q] = x[g - 8 - q];
+      for (int q = 0; q < 4; ++q) b[q] = x2[(g - 9) / 2 - q];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        s = __dadd_rn(a[q], s);
-        o[g - q] = s;
+      for (int q = 0; q < 4; ++q) {
+        s = __dadd_rn(s, a[q].y);
+        const double hi = s;
+        s = __dadd_rn(s, a[q].x);
+        o2[(g - 1) / 2 - q] = make_double2(s, hi);
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = b[q];
+      for (int q = 0; q < 4; ++q) a[q] = b[q];
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      s = __dadd_rn(a[q], s);
-      o[g - q] = s;
+    for (int q = 0; q < 4; ++q) {
+      s = __dadd_rn(s, a[q].y);
+      const double hi = s;
+      s = __dadd_rn(s, a[q].x);
+      o2[(g - 1) / 2 - q] = make_double2(s, hi);
     }
     g -= 8;
   }
   for (; g >= 0; --g) {
-    s = __dadd_rn(x[g], s);
+    s = __dadd_rn(s, x[g]);
     o[g] = s;
   }
   return s;

@@ -32,6 +32,24 @@ __device__ __forceinline__ double chain_suffix(double s, const double* x, double
   }
   return s;
 }
+__device__ __forceinline__ double chain_suffix_sfirst(double s, const double* x, double* o, int cnt) {
+  int g = cnt - 1;
+  for (; g >= 7; g -= 8) {
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = x[g - q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s = __dadd_rn(s, a[q]);
+      o[g - q] = s;
+    }
+  }
+  for (; g >= 0; --g) {
+    s = __dadd_rn(s, x[g]);
+    o[g] = s;
+  }
+  return s;
+}
 __global__ void k(const double* in, int n, int mode, double* out, long long* cyc) {
   __shared__ double X[2048], O[2048];
   for (int i = threadIdx.x; i < n; i += blockDim.x) X[i] = in[i];
@@ -42,6 +60,7 @@ __global__ void k(const double* in, int n, int mode, double* out, long long* cyc
   if (lane == 0) {
     if (mode == 0 && warp == 0) s = chain_sum(0.0, X, n);
     if (mode == 1 && warp == 1) s = chain_suffix(0.0, X, O, n);
+    if (mode == 3 && warp == 1) s = chain_suffix_sfirst(0.0, X, O, n);
     if (mode == 2 && warp == 0) s = chain_sum(0.0, X, n);
     if (mode == 2 && warp == 1) s = chain_suffix(0.0, X, O, n);
   }
@@ -59,8 +78,8 @@ int main() {
   cudaMallocManaged(&out, 16);
   cudaMallocManaged(&cyc, 16);
   for (int i = 0; i < n; ++i) in[i] = 1.0 / (i + 1);
-  const char* names[3] = {"sum alone", "suffix alone", "both (warp 0 sum, warp 1 suffix)"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* names[4] = {"sum alone", "suffix alone", "both (warp 0 sum, warp 1 suffix)", "suffix, sum as first operand"};
+  for (int mode = 0; mode < 4; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cyc[0] = cyc[1] = 0;
       k<<<1, 256>>>(in, n, mode, out, cyc);

@@ -263,7 +263,7 @@ int parac_gpu_download_phase_snapshots(parac_gpu_ctx* ctx, int64_t* dp, int32_t*
 int parac_gpu_download_subtimes(parac_gpu_ctx* ctx, uint64_t* sub);
 
 /* Diagnostics: the cooperative hub path's per-column trace of the same
- * record_times run (kHubTraceWords = 48 words per wide column, layout in
+ * record_times run (kHubTraceWords = 64 words per wide column, layout in
  * csrc/cuda/factor_kernels.cuh). Copies min(cap, *count) records; *count =
  * wide columns recorded. */
 int parac_gpu_download_hub_trace(parac_gpu_ctx* ctx, uint64_t* out, int32_t cap, int32_t* count);

@@ -57,8 +57,9 @@ struct HubJob {  // one per CTA of the elimination grid
 // Optional per-column trace of the hub path (record_times; tools/profile_factor.py):
 // [0] k [1] R [2] m [3] owner start [4] owner end (globaltimer ns), then per
 // step p = 1..9 (7 phases, 8 = lkk chain, 9 = suffix chain) at 8 + 4 (p - 1):
-// posted, first chunk started, last chunk ended, owner chunks << 32 | helper chunks
-constexpr int kHubTraceWords = 48;
+// posted, first chunk started, last chunk ended, owner chunks << 32 | helper chunks;
+// at 48 + p (p = 1..7): the sum of the phase's chunk durations (ns)
+constexpr int kHubTraceWords = 64;
 // Ctrl::status when a column wider than kBigCap met the kernel instance
 // without the hub path: the host re-runs with it (never returned to callers)
 constexpr int kStatusNeedHubs = 90;
@@ -134,6 +135,7 @@ struct FactorDev {
   HubJob* hub_jobs;  // [grid] cooperative wide-column jobs, one per CTA
   unsigned long long* hub_trace;  // optional [kHubTraceCap * kHubTraceWords]
   unsigned long long hub_linger_ns;  // a helper waits this long for a job's next phase
+  unsigned hub_wait_ns;              // longest sleep of a waiting big CTA between looks at the hub hint
   int hubs;          // launch the kernel with the cooperative hub path (hub graphs; see launch_eliminate)
   // control
   Ctrl* ctrl;

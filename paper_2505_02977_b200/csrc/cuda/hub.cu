@@ -75,6 +75,18 @@ __device__ __forceinline__ int cta_sum(int v, int* ws) {
   return t;
 }
 
+// Stable rank of thread tid's key among the first cnt threads' keys (one
+// 256-key tile): rank_sort's segment ranks + log2(256/32) merge passes, ~4x
+// fewer shared-memory reads than the all-pairs broadcast rank (raw keys are
+// unique; weight keys need the stable rule, which both give).
+__device__ __forceinline__ int hub_tile_rank(unsigned long long key, int cnt, unsigned long long* X) {
+  const unsigned long long k[1] = {key};
+  int r[1];
+  int* I = reinterpret_cast<int*>(X + 2 * kHubTile);
+  rank_sort<kThreads, 1>(k, cnt, X, X + kHubTile, I, I + kHubTile, r);
+  return r[0];
+}
+
 // Place of `key` (an element of sorted tile c of the sorted-tile array K[0, n))
 // among the other tiles: #{keys < key} in each (STABLE: earlier tiles count
 // keys <= key, the stable rule for the weight sort). Tiles are staged into
@@ -156,7 +168,7 @@ __device__ __noinline__ void hub_chunk(int c, int* emitted) {
       unsigned long long key = ~0ull;
       double w = 0.0;
       if (tid < cnt) load_raw_dir(d, h.k, h.fb, h.fdeg, b0 + tid, h.dirrow, key, w);
-      const int r = bcast_rank_cta<false>(key, cnt, X);
+      const int r = hub_tile_rank(key, cnt, X);
       if (tid < cnt) {
         __stcg(A.RK + b0 + r, key);
         __stcg(A.RW + b0 + r, w);
@@ -230,7 +242,7 @@ __device__ __noinline__ void hub_chunk(int c, int* emitted) {
       const bool v = tid < cnt;
       const unsigned long long wk = v ? dbits(__ldcg(A.RW + b0 + tid)) : kInfBits;
       const unsigned long long a = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
-      const int r = bcast_rank_cta<true>(wk, cnt, X);
+      const int r = hub_tile_rank(wk, cnt, X);
       if (v) {
         __stcg(A.SK + b0 + r, wk);
         __stcg(reinterpret_cast<unsigned long long*>(A.SW) + b0 + r, a);
@@ -319,14 +331,17 @@ __device__ __noinline__ void hub_chunk(int c, int* emitted) {
 __device__ __forceinline__ void hub_run_chunk(const FactorDev& d, HubJob& J, int c, char* smem, CtaShared& sh,
                                               bool own) {
   unsigned long long* rec = threadIdx.x == 0 ? hub_rec(d, sh.hd) : nullptr;
-  if (rec) atomicMin(hub_step(rec, sh.hd.phase) + 1, globaltimer_ns());
+  const unsigned long long t0 = rec ? globaltimer_ns() : 0ull;
+  if (rec) atomicMin(hub_step(rec, sh.hd.phase) + 1, t0);
   hub_chunk(c, &J.emitted);
   fence_acq_rel();
   __syncthreads();
   if (threadIdx.x == 0) red_add_relaxed_u64(&J.done, 1ull);
   if (rec) {
-    atomicMax(hub_step(rec, sh.hd.phase) + 2, globaltimer_ns());
+    const unsigned long long t1 = globaltimer_ns();
+    atomicMax(hub_step(rec, sh.hd.phase) + 2, t1);
     atomicAdd(hub_step(rec, sh.hd.phase) + 3, own ? 1ull << 32 : 1ull);
+    atomicAdd(rec + 48 + sh.hd.phase, t1 - t0);
   }
 }
 

@@ -59,6 +59,116 @@ struct CtaShared {
   HubDesc hd;          // the phase being worked on
 };
 
+// Number of keys in the sorted run A[0, len) that are < key (<= key when
+// inclusive); w is the run capacity (a power of two >= len).
+__device__ __forceinline__ int count_before(const unsigned long long* A, int len, int w, unsigned long long key,
+                                            bool inclusive) {
+  int lo = 0;
+  for (int step = w >> 1; step > 0; step >>= 1) {
+    const int probe = lo + step - 1;
+    if (probe < len) {
+      const unsigned long long m = A[probe];
+      lo = (inclusive ? m <= key : m < key) ? lo + step : lo;
+    }
+  }
+  if (lo == w - 1 && len == w) {
+    const unsigned long long m = A[w - 1];
+    lo += static_cast<int>(inclusive ? m <= key : m < key);
+  }
+  return lo;
+}
+
+// Stable sort of R <= T*ITEMS u64 keys held in registers (element g = i*T +
+// tid; ties keep g order), T = 32 (one warp) or kThreads (the CTA):
+//   1. rank inside the element's 32-element segment (32 broadcast loads of the
+//      unsorted keys staged in X2) and write the sorted segment to X1, with
+//      each key's element index alongside (IA);
+//   2. merge runs pairwise, 32 -> 64 -> ... -> R: every position finds its
+//      place in the merged pair with one binary search in the partner run
+//      (left elements count partner keys <, right ones <=: the stable rule),
+//      ping-ponging (X1, IA) <-> (X2, IB); one barrier per level.
+// The dependent chain is log2(R/32) short searches instead of one search per
+// other segment. Finally rank[i] = sorted position of element g.
+// Raw keys (row << 32 | source+1) are unique. The weight sort needs (weight,
+// row) order; its input is already row-ascending, so a STABLE sort on the
+// weight bits alone gives exactly fill_sorted_view's order
+// (factor_common.hpp:133-145).
+template <int T, int ITEMS>
+__device__ __forceinline__ void rank_sort(const unsigned long long (&k)[ITEMS], int R, unsigned long long* X1,
+                                          unsigned long long* X2, int* IA, int* IB, int (&rank)[ITEMS],
+                                          long long* cyc = nullptr) {
+  const int tid = T == 32 ? lane_id() : static_cast<int>(threadIdx.x);
+  const int lane = tid & 31;
+  const int wid = tid >> 5;
+  long long c0 = 0;
+  if (cyc && tid == 0) c0 = clock64();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * T + tid;
+    if (g < R) X2[g] = k[i];
+  }
+  if (T == 32) __syncwarp(); else __syncthreads();
+  if (cyc && tid == 0) cyc[0] = clock64() - c0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int seg = i * (T / 32) + wid;
+    const int len = min(32, R - seg * 32);  // <= 0: segment fully padding
+    const unsigned long long* K = X2 + seg * 32;
+    if (len > 0) {
+      int c = 0;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const unsigned long long o = t < len ? K[t] : ~0ull;
+        c += static_cast<int>((o < k[i]) | ((o == k[i]) & (t < lane)));
+      }
+      if (lane < len) {
+        X1[seg * 32 + c] = k[i];
+        IA[seg * 32 + c] = seg * 32 + lane;
+      }
+    }
+  }
+  if (T == 32) __syncwarp(); else __syncthreads();
+  if (cyc && tid == 0) cyc[1] = clock64() - c0;
+  unsigned long long *ks = X1, *kd = X2;
+  int *is = IA, *id = IB;
+  for (int w = 32; w < R; w *= 2) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int p = i * T + tid;
+      if (p < R) {
+        const unsigned long long key = ks[p];
+        const int g = is[p];
+        const int ps = p & ~(2 * w - 1);
+        int np;
+        if (p < ps + w) {  // left run: partner = right run, strict
+          const int len = max(0, min(w, R - (ps + w)));
+          np = p + count_before(ks + ps + w, len, w, key, false);
+        } else {           // right run: partner = left run, inclusive
+          np = (p - w) + count_before(ks + ps, w, w, key, true);
+        }
+        kd[np] = key;
+        id[np] = g;
+      }
+    }
+    if (T == 32) __syncwarp(); else __syncthreads();
+    unsigned long long* tk = ks; ks = kd; kd = tk;
+    int* ti = is; is = id; id = ti;
+  }
+  // ranks: the sorted position of each element index
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int p = i * T + tid;
+    if (p < R) id[is[p]] = p;
+  }
+  if (T == 32) __syncwarp(); else __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int g = i * T + tid;
+    rank[i] = g < R ? id[g] : 0;
+  }
+  if (cyc && tid == 0) cyc[2] = clock64() - c0;
+}
+
 // c += #{keys of pairs [q0, q1) of P below thr} (two accumulators per element)
 __device__ __forceinline__ void count_below(const ulonglong2* P, int q0, int q1, unsigned long long thr, int& ca,
                                             int& cb) {

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Validation + evidence: full GPU tests, smoke, default bench, R-MAT 22 bench,
+# launch list and ncu captures of K3 (mesh) and of the hub path (R-MAT 16).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --workload rmat_22 --no-pcg --no-dropin --no-batch --steps 2 --warmup 3 > gpurun_out/bench_rmat.json 2> gpurun_out/bench_rmat.err
+timeout 300 python tools/hub_trace.py --scale 22 --json gpurun_out/hub_trace22.json > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python tools/ncu_factor.py --pcg > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:eliminate_kernel -c 1 -o gpurun_out/k3_full -f python tools/ncu_factor.py > gpurun_out/ncu_full.log 2>&1

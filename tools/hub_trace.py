@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 import paper_2505_02977_b200 as P  # noqa: E402
 
-WORDS = 48
+WORDS = 64
 STEPS = ["gather+tile", "cross rank", "merge", "weight tiles", "weight rank", "sample+column", "release",
          "lkk chain", "suffix chain"]
 # each phase is posted by the CTA that completed the previous one's last chunk
@@ -73,6 +73,8 @@ def main():
                 e["join_us"] = float(((first - post)[okf]).mean() / 1e3) if okf.any() else None
                 e["owner_chunks"] = float((ch[ok] >> np.uint64(32)).astype(np.float64).mean())
                 e["helper_chunks"] = float((ch[ok] & np.uint64(0xffffffff)).astype(np.float64).mean())
+                nchunks = (ch[ok] >> np.uint64(32)) + (ch[ok] & np.uint64(0xffffffff))
+                e["chunk_us"] = float((rec[sel, 48 + p][ok] / np.maximum(nchunks.astype(np.float64), 1)).mean() / 1e3)
             d["steps"][name] = e
         # gaps: owner time between steps (post of p+1 - last end of p)
         return d

@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
 synccheck): factor + PCG at 10^3, a 3-problem batch, an R-MAT graph whose hubs
-take the wide-column slab path, each checked against the oracle's checksum.
+take the cooperative hub path (with helpers, and with the owner alone on a
+2-CTA grid), each checked against the oracle's checksum.
   compute-sanitizer --tool memcheck python tools/sanitize_run.py"""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -40,3 +41,7 @@ o = P.ordering_random(g.n, 0)
 f = P.factor_gpu(g, o, 0, opts, ctx=ctx)
 check(g, o.perm, 0, f)
 print("rmat 12 ok, max degree", int((g.ptr[1:] - g.ptr[:-1]).max()))
+
+f2 = P.factor_gpu(g, o, 0, P.GpuOptions(watchdog_seconds=1200.0, grid_ctas=2), ctx=ctx)
+check(g, o.perm, 0, f2)
+print("rmat owner-alone ok")

@@ -1334,6 +1334,7 @@ template <bool HUBS>
 __device__ __forceinline__ int big_loop(const FactorDev& d, char* smem, CtaShared& sh) {
   int done_local = 0;
   int k = sh.k;
+  __syncthreads();  // every thread has read sh.k before thread 0 claims into it
   int chain = 0;
   int action = 0;
   while (true) {

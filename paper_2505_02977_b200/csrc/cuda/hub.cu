@@ -350,10 +350,8 @@ __device__ __forceinline__ void hub_run_chunk(const FactorDev& d, HubJob& J, int
 __device__ __forceinline__ void hub_help(const FactorDev& d, int job, char* smem, CtaShared& sh) {
   const int tid = threadIdx.x;
   unsigned long long idle0 = 0;
-  if (tid == 0) {
-    idle0 = globaltimer_ns();
-    sh.help = job;
-  }
+  if (tid == 0) idle0 = globaltimer_ns();  // (sh.help == job: the kernel passes it)
+  (void)job;
   while (true) {
     if (tid == 0) {
       int c = -1, seq = 0;

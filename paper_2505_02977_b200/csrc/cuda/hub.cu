@@ -609,6 +609,7 @@ __device__ int hub_entry(const FactorDev&, int k, int job) {
   const FactorDev& d = k3_dev();
   char* smem = k3_scratch();
   CtaShared& sh = k3_sh();
+  __syncthreads();  // every thread has read its arguments (from sh) before thread 0 rewrites sh
   if (k >= 0) return hub_eliminate(d, k, smem, sh);
   hub_help(d, job, smem, sh);
   return -1;

@@ -129,6 +129,19 @@ def test_batch_union_equals_standalone(gpu_ctx, port, gold):
         assert f"{f.checksum():016x}" == e["checksum"], nm
 
 
+def test_batch_with_hub_members(gpu_ctx, port):
+    """Hub columns inside a batch: R-MAT members (several hub jobs at once,
+    per-member sample keys inside the cooperative phases) next to a mesh,
+    each member byte-identical to its stand-alone factorization."""
+    gs = [P.gen_rmat(13, 16, 1), P.gen_poisson3d(12), P.gen_rmat(12, 16, 2)]
+    perms = [P.ordering_random(g.n, i).perm for i, g in enumerate(gs)]
+    seeds = [5, 6, 7]
+    fs, info = P.factor_batch_gpu(gs, [P.Ordering(p) for p in perms], seeds, ctx=gpu_ctx)
+    assert info.large_columns > 0, "no member column took the hub path"
+    for i, (g, perm, seed, f) in enumerate(zip(gs, perms, seeds, fs)):
+        assert_same(f, factor_from_port(port.factor(g, perm, seed)), f"member {i}")
+
+
 @pytest.mark.parametrize("scale,opts", [(15, {}), (16, {}), (15, dict(grid_ctas=2)),
                                         (15, dict(grid_ctas=9, verify=True)),
                                         (15, dict(delay_ns=3000, verify=True))])

@@ -409,6 +409,8 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   {  // PARAC_HUB_LINGER_NS: how long a helper stays with a hub job between its phases (tuning)
     const char* e = std::getenv("PARAC_HUB_LINGER_NS");
     d.hub_linger_ns = e ? std::strtoull(e, nullptr, 10) : 40000ull;
+    const char* hp = std::getenv("PARAC_HUB_PIPE");
+    d.hub_pipe = hp ? std::atoi(hp) : 1;
     const char* w = std::getenv("PARAC_HUB_WAIT_NS");
     d.hub_wait_ns = w ? static_cast<unsigned>(std::atoi(w)) : 4096u;
     // the kernel instance with the hub path on graphs with hub vertices, or

@@ -41,7 +41,7 @@ constexpr int kBigCap = 1024;
 // are waiting for a queue slot take chunks (helpers). The owner takes chunks
 // too, so a column finishes with or without helpers.
 struct HubDesc {                // one phase of one column (read by every chunk)
-  int k, R, m, nt, mt, fdeg, lvk, cs, phase, cap, trace, pad_;
+  int k, R, m, nt, mt, fdeg, lvk, cs, phase, cap, trace, pipe;  // pipe: sampling follows the suffix chain
   long long fb, slab, start;
   double lkk;
   unsigned dirrow[kDirChunks];
@@ -53,6 +53,7 @@ struct HubJob {  // one per CTA of the elimination grid
   alignas(256) unsigned long long done;  // seq << 32 | chunks completed
   alignas(256) HubDesc desc[2];          // by seq parity
   alignas(256) int emitted;              // fills emitted by the sampling phase
+  alignas(256) int progress;             // suffix sums C[progress, m) are written (pipelined sampling)
 };
 // Optional per-column trace of the hub path (record_times; tools/profile_factor.py):
 // [0] k [1] R [2] m [3] owner start [4] owner end (globaltimer ns), then per
@@ -137,6 +138,7 @@ struct FactorDev {
   unsigned long long hub_linger_ns;  // a helper waits this long for a job's next phase
   unsigned hub_wait_ns;              // longest sleep of a waiting big CTA between looks at the hub hint
   int hubs;          // launch the kernel with the cooperative hub path (hub graphs; see launch_eliminate)
+  int hub_pipe;      // hub columns: sampling starts while the suffix chain runs (1; PARAC_HUB_PIPE=0 off)
   // control
   Ctrl* ctrl;
   unsigned long long sample_seed;

@@ -41,6 +41,7 @@ namespace {
 // after every chunk of the previous one is done, so chunks of one phase never
 // read what the same phase writes.
 enum : int { kHubGather = 1, kHubRank, kHubMerge, kHubWTile, kHubWRank, kHubSample, kHubRelease };
+static_assert(kHubSample == kHubSamplePhase, "hub_chains.cu posts the sampling phase by number");
 constexpr int kHubTile = kThreads;                    // entries per chunk, one per thread
 constexpr int kHubGroup = kCtaSmem / (8 * kHubTile);  // tiles staged per shared-memory group
 constexpr int kHubFullSuffix = kCtaSmem / 8;          // suffix arrays up to this size sit in shared memory
@@ -59,9 +60,6 @@ __device__ __forceinline__ HubArr hub_arrays(const FactorDev& d, long long slab,
           reinterpret_cast<double*>(b + 6 * c8), reinterpret_cast<int*>(b + 6 * c8)};
 }
 
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 // CTA sum of one int per thread (ws: kWarps ints of shared memory).
 __device__ __forceinline__ int cta_sum(int v, int* ws) {
@@ -154,7 +152,8 @@ __device__ __forceinline__ int hub_pick(const double* suffix, const double* coar
   return a;
 }
 
-__device__ __noinline__ void hub_chunk(int c, int* emitted) {
+__device__ __noinline__ void hub_chunk(int c, HubJob& J) {
+  int* emitted = &J.emitted;
   const FactorDev& d = k3_dev();
   const HubDesc& h = k3_sh().hd;
   char* smem = k3_scratch();
@@ -263,12 +262,30 @@ __device__ __noinline__ void hub_chunk(int c, int* emitted) {
       break;
     }
     case kHubSample: {
-      const int m = h.m, i = b0 + tid;
+      // pipelined (h.pipe): chunks are taken top down and each waits until the
+      // suffix chain has written C[b + 1, m), all its samples search
+      const int m = h.m, bs = h.pipe ? (h.mt - 1 - c) * kHubTile : b0, i = bs + tid;
       const bool smp = i < m - 1, col = i < m;
+      if (h.pipe) {
+        if (tid == 0) {
+          int iter = 0;
+          while (ld_relaxed(&J.progress) > bs + 1) {
+            if ((++iter & 1023) == 0 && ld_relaxed(&d.ctrl->status) != 0) break;
+            __nanosleep(64);
+          }
+        }
+        __syncthreads();
+        fence_acq_rel();  // acquire: the suffix range published by the progress word
+      }
       double* S = reinterpret_cast<double*>(X);
       const bool full = m <= kHubFullSuffix;
-      if (full) stage_in<8>(S, A.C, m, tid, kThreads);
-      else stage_in(S, A.C, (m + h.cs - 1) / h.cs, tid, kThreads, h.cs);
+      const int s0 = min(m, bs + 1);  // the lowest suffix entry this chunk's samples read
+      if (full) {
+        stage_in<8>(S + s0, A.C + s0, m - s0, tid, kThreads);
+      } else {
+        const int q0 = (s0 + h.cs - 1) / h.cs;
+        stage_in(S + q0, A.C + static_cast<long long>(q0) * h.cs, (m + h.cs - 1) / h.cs - q0, tid, kThreads, h.cs);
+      }
       __syncthreads();
       bool em = false;
       int lo = 0, hi = 0, slot = -1;
@@ -333,7 +350,7 @@ __device__ __forceinline__ void hub_run_chunk(const FactorDev& d, HubJob& J, int
   unsigned long long* rec = threadIdx.x == 0 ? hub_rec(d, sh.hd) : nullptr;
   const unsigned long long t0 = rec ? globaltimer_ns() : 0ull;
   if (rec) atomicMin(hub_step(rec, sh.hd.phase) + 1, t0);
-  hub_chunk(c, &J.emitted);
+  hub_chunk(c, J);
   fence_acq_rel();
   __syncthreads();
   if (threadIdx.x == 0) red_add_relaxed_u64(&J.done, 1ull);
@@ -403,40 +420,15 @@ __device__ __forceinline__ void hub_help(const FactorDev& d, int job, char* smem
   }
 }
 
-// Owner: post phase `phase` with nch chunks (descriptor, then the release of
-// the `next` word), keeping chunk 0 for itself; work; wait for every chunk.
-// Returns false when the factorization aborted meanwhile.
-__device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* smem, CtaShared& sh, int phase, int nch) {
+// Owner: take chunks of its posted phase (first: the chunk it already holds,
+// -1 none) until none is left, then wait for every chunk. Returns false when
+// the factorization aborted meanwhile.
+__device__ __forceinline__ bool hub_run(const FactorDev& d, int job, char* smem, CtaShared& sh, int nch, int first) {
   HubJob& J = d.hub_jobs[job];
   const int tid = threadIdx.x;
-  __syncthreads();  // sh.hd complete
-  if (tid < 32) {
-    const int seq = (sh.hub_seq + 1) & 0xffff;
-    sh.hd.phase = phase;  // lane-uniform write
-    __syncwarp();
-    const unsigned* src = reinterpret_cast<const unsigned*>(&sh.hd);
-    unsigned* dst = reinterpret_cast<unsigned*>(&J.desc[seq & 1]);
-    for (int w = tid; w < static_cast<int>(sizeof(HubDesc) / 4); w += 32) __stcg(dst + w, src[w]);
-    if (tid == 0) {
-      if (unsigned long long* rec = hub_rec(d, sh.hd)) {
-        hub_step(rec, phase)[0] = globaltimer_ns();
-        hub_step(rec, phase)[1] = ~0ull;
-      }
-      st_relaxed_u64(&J.done, static_cast<unsigned long long>(seq) << 32);
-    }
-    fence_acq_rel();
-    __syncwarp();
-    if (tid == 0) {
-      sh.hub_seq = seq;
-      st_relaxed_u64(&J.next, (static_cast<unsigned long long>(seq) << 48) |
-                                  (static_cast<unsigned long long>(nch) << 24) | 1ull);
-      asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&d.ctrl->hub_hint), "r"(job + 1) : "memory");
-    }
-  }
-  __syncthreads();
-  int c = 0;
+  int c = first;
   while (true) {
-    hub_run_chunk(d, J, c, smem, sh, true);
+    if (c >= 0) hub_run_chunk(d, J, c, smem, sh, true);
     if (tid == 0) {
       const unsigned long long old = atom_add_relaxed_u64(&J.next, 1ull);
       const int cc = static_cast<int>(old & 0xffffffull);
@@ -445,6 +437,7 @@ __device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* sme
     __syncthreads();
     c = sh.hub_c;
     if (c < 0) break;
+    fence_acq_rel();  // acquire: the phase's inputs
   }
   if (tid == 0) {
     const unsigned long long target = (static_cast<unsigned long long>(sh.hub_seq) << 32) |
@@ -462,6 +455,17 @@ __device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* sme
   __syncthreads();
   fence_acq_rel();  // acquire: the chunks' stores are visible
   return sh.bad == 0;
+}
+
+// Owner: post phase `phase` with nch chunks, keeping chunk 0 for itself, and run it.
+__device__ __forceinline__ bool hub_phase(const FactorDev& d, int job, char* smem, CtaShared& sh, int phase, int nch) {
+  __syncthreads();  // sh.hd complete
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) sh.hd.phase = phase;
+    hub_post_warp(d, job, sh, (sh.hub_seq + 1) & 0xffff, nch, 1);
+  }
+  __syncthreads();
+  return hub_run(d, job, smem, sh, nch, 0);
 }
 
 // Owner: the job is over (helpers leave: a word with no chunks and nch 0).
@@ -545,21 +549,15 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       __syncthreads();
     }
     if ((ph == kHubWTile || ph == kHubWRank) && sh.hd.m < 2) continue;  // one row: nothing to sort
+    bool posted = false;  // the sampling phase was posted (pipelined) from the chains
     if (ph == kHubSample) {
       PHASE(3);
       const int m = sh.hd.m;
       if (m == 0) break;  // (a raw entry always merges into a row)
-      unsigned long long* rec = lead ? hub_rec(d, sh.hd) : nullptr;
-      if (rec) {
-        hub_step(rec, 8)[0] = globaltimer_ns();
-        hub_step(rec, 9)[0] = hub_step(rec, 8)[0];
-      }
-      {
-        const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
-        const double lkk = hub_chains(A.RW, A.WB, A.C, m, m >= 2, rec);
-        if (lead) sh.hd.lkk = lkk;
-      }
-      PHASE(4);
+      // pipelined sampling: posted as soon as lkk is known, its chunks follow
+      // the suffix chain down (not with the dependency trace on this column,
+      // whose snapshot sits between sampling and release)
+      const bool pipe = m >= 2 && d.hub_pipe != 0 && k != d.trace_k;
       if (lead) {
         if (sh.start + m > d.arena_cap) {
           fail(d, kErrArena, k);
@@ -567,16 +565,33 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
         }
         sh.hd.start = sh.start;
         sh.hd.cs = coarse_step(m);
-        d.diag[k] = sh.hd.lkk;
+        sh.hd.pipe = 0;
         d.col_start[k] = sh.start;
         d.col_len[k] = m;
         d.hub_jobs[job].emitted = 0;  // ordered before the post by its fence
+        d.hub_jobs[job].progress = m;
       }
       __syncthreads();
       if (sh.bad) {
         ok = false;
         break;
       }
+      unsigned long long* rec = lead ? hub_rec(d, sh.hd) : nullptr;
+      if (rec) {
+        hub_step(rec, 8)[0] = globaltimer_ns();
+        hub_step(rec, 9)[0] = hub_step(rec, 8)[0];
+      }
+      {
+        const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
+        const double lkk = hub_chains(A.RW, A.WB, A.C, m, m >= 2, rec, pipe ? job : -1);
+        if (lead) {
+          sh.hd.lkk = lkk;
+          d.diag[k] = lkk;
+        }
+      }
+      PHASE(4);
+      __syncthreads();
+      posted = pipe;
     }
     if (ph == kHubRelease) {
       PHASE(5);
@@ -584,7 +599,8 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       maybe_delay(d, k, 1);
       if (k == d.trace_k) snapshot_dp(d, 1, tid, kThreads);
     }
-    ok = hub_phase(d, job, smem, sh, ph, ph <= kHubMerge ? sh.hd.nt : sh.hd.mt);
+    ok = posted ? hub_run(d, job, smem, sh, sh.hd.mt, -1)
+                : hub_phase(d, job, smem, sh, ph, ph <= kHubMerge ? sh.hd.nt : sh.hd.mt);
     if (d.vsub && lead && ph <= kHubWRank) {  // wide-column stamps (tools/profile_factor.py)
       unsigned long long* wst = d.vsub + d.n * 8ll + 4ll * k;
       if (ph <= kHubMerge) wst[ph - 1] = globaltimer_ns();

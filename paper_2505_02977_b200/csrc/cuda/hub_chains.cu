@@ -108,7 +108,7 @@ __device__ __forceinline__ double chain_suffix(double s, bool first, const doubl
 // Returns lkk (every thread); with suffix, C[0, m) = suffix sums of WB.
 // rec: optional trace record (the ends of the two chains)
 __device__ double hub_chains(const double* W, const double* WB, double* C, int m, bool suffix,
-                             unsigned long long* rec) {
+                             unsigned long long* rec, int post_job) {
   double* smem = reinterpret_cast<double*>(k3_scratch());
   constexpr int CH = kChainChunk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -141,6 +141,16 @@ __device__ double hub_chains(const double* W, const double* WB, double* C, int m
       reinterpret_cast<long long*>(res)[3] = busy;
       reinterpret_cast<long long*>(res)[4] = waitc;
     }
+    if (post_job >= 0 && warp == 0) {  // sampling can start: lkk is known, the suffix follows
+      CtaShared& sh = k3_sh();
+      const FactorDev& d = k3_dev();
+      if (lane == 0) {
+        sh.hd.lkk = s;
+        sh.hd.phase = kHubSamplePhase;
+        sh.hd.pipe = 1;
+      }
+      hub_post_warp(d, post_job, sh, (sh.hub_seq + 1) & 0xffff, sh.hd.mt, 0);
+    }
   } else if (suffix) {
     const int gt = warp == 1 ? -1 : (warp - 4) * 32 + lane;  // stager / writer 0..127
     if (gt >= 0) {
@@ -159,6 +169,7 @@ __device__ double hub_chains(const double* W, const double* WB, double* C, int m
         if (c >= 1) {  // chunk c-1 = [hi, hi + CH)
           const double* o = SO + ((c - 1) & 1) * CH;
           for (int i = gt; i < CH; i += 128) __stcg(C + hi + i, o[i]);
+          if (post_job >= 0) fence_acq_rel();  // release: C[hi, m) before the progress word
         }
       } else if (lane == 0) {
         const long long c0 = clock64();
@@ -168,10 +179,20 @@ __device__ double hub_chains(const double* W, const double* WB, double* C, int m
       const long long w0 = clock64();
       named_bar(2, 160);
       waitc += clock64() - w0;
+      if (post_job >= 0 && c >= 1 && gt == 0)  // sampling chunks whose suffix range is written may start
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&k3_dev().hub_jobs[post_job].progress), "r"(hi)
+                     : "memory");
     }
     if (gt >= 0) {  // the last chunk: [0, m - (nch - 1) * CH)
       const double* o = SO + ((nch - 1) & 1) * CH;
       for (int i = gt; i < m - (nch - 1) * CH; i += 128) __stcg(C + i, o[i]);
+      if (post_job >= 0) fence_acq_rel();
+    }
+    if (post_job >= 0) {
+      named_bar(2, 128 + 32);
+      if (gt == 0)
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&k3_dev().hub_jobs[post_job].progress), "r"(0)
+                     : "memory");
     }
     if (tid == 32) {
       reinterpret_cast<unsigned long long*>(res)[2] = globaltimer_ns();

@@ -259,11 +259,51 @@ __device__ __forceinline__ void stage_in(T* dst, const T* src, int cnt, int t, i
   }
 }
 
+// the sampling phase's id (hub.cu's phase enum), for the post from hub_chains.cu
+constexpr int kHubSamplePhase = 6;
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Post phase sh.hd.phase of job `job` as sequence seq with nch chunks, first
+// of them already taken (the caller keeps chunk 0 when first == 1): the
+// descriptor, then the release of `next`. One full warp calls it.
+__device__ __forceinline__ void hub_post_warp(const FactorDev& d, int job, CtaShared& sh, int seq, int nch,
+                                              int first) {
+  HubJob& J = d.hub_jobs[job];
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const unsigned* src = reinterpret_cast<const unsigned*>(&sh.hd);
+  unsigned* dst = reinterpret_cast<unsigned*>(&J.desc[seq & 1]);
+  for (int w = lane; w < static_cast<int>(sizeof(HubDesc) / 4); w += 32) __stcg(dst + w, src[w]);
+  if (lane == 0) {
+    if (unsigned long long* rec = hub_rec(d, sh.hd)) {
+      const int p = sh.hd.phase;
+      hub_step(rec, p)[0] = globaltimer_ns();
+      hub_step(rec, p)[1] = ~0ull;
+    }
+    st_relaxed_u64(&J.done, static_cast<unsigned long long>(seq) << 32);
+  }
+  fence_acq_rel();
+  __syncwarp();
+  if (lane == 0) {
+    sh.hub_seq = seq;
+    st_relaxed_u64(&J.next, (static_cast<unsigned long long>(seq) << 48) |
+                                (static_cast<unsigned long long>(nch) << 24) | static_cast<unsigned>(first));
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(&d.ctrl->hub_hint), "r"(job + 1) : "memory");
+  }
+  __syncwarp();
+}
+
 // The owner's serial chains of a hub column (hub_chains.cu): returns lkk of
 // the row-ordered merged weights W[0, m); with suffix, C = suffix sums of the
 // weight-ordered WB. rec: optional trace record.
+// post_job >= 0: once lkk is known, warp 0 posts the sampling phase
+// (pipelined: its chunks wait on HubJob::progress, which the suffix group
+// publishes chunk by chunk).
 __device__ double hub_chains(const double* W, const double* WB, double* C, int m, bool suffix,
-                             unsigned long long* rec);
+                             unsigned long long* rec, int post_job);
 
 // The hub kernel instance's dynamic shared memory: the per-CTA scratch
 // (kCtaSmem bytes), then the CtaShared block. Every translation unit names it

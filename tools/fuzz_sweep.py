@@ -1,4 +1,4 @@
-"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve|--batch].
+"""Long run of tests/test_fuzz_gpu.py's generator: python tools/fuzz_sweep.py START COUNT [--solve|--batch|--rmat].
 Without --solve: factors byte for byte; with it: exact-mode preconditioner bytes,
 fast mode within 1e-10, and the default PCG (exact at these sizes) bit-identical
 to the oracle's pcg_solve (--fast: the fast PCG, iterations within 10%).
@@ -82,6 +82,30 @@ def batch_case(cs):
     return None
 
 
+def rmat_case(cs):
+    # R-MAT graphs of scales 10-14 (hub columns: several cooperative jobs at
+    # once), random or nnz-sort orderings, grids from 2 CTAs (owner alone) to
+    # the full co-resident grid
+    rng = np.random.default_rng(7000 + cs)
+    scale = 10 + cs % 5
+    g = P.gen_rmat(scale, int(rng.integers(8, 24)), int(rng.integers(0, 1 << 30)))
+    seed = int(rng.integers(0, 1 << 31))
+    o = P.ordering_random(g.n, seed) if cs % 3 else P.ordering_nnz_sort(g, seed)
+    grid = int(rng.choice([0, 0, 2, 9, 37]))
+    f = P.factor_gpu(g, o, seed, P.GpuOptions(grid_ctas=grid), ctx=ctx)
+    if not f.same_values(factor_from_port(port.factor(g, o.perm, seed))):
+        return f"rmat scale {scale} grid {grid} n={g.n}"
+    return None
+
+
+if "--rmat" in sys.argv:
+    for cs in range(start, start + count):
+        msg = rmat_case(cs)
+        if msg:
+            bad += 1
+            print("MISMATCH", cs, msg, flush=True)
+    print(f"rmat cases {count} mismatches {bad} seconds {time.time() - t0:.1f}")
+    sys.exit(0)
 if "--batch" in sys.argv:
     for cs in range(start, start + count):
         msg = batch_case(cs)

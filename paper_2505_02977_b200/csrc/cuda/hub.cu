@@ -22,8 +22,9 @@ namespace {
 // (claim_at, via Ctrl::hub_hint) and stay with the job between its phases
 // (hub_help). The owner takes chunks too, so a column completes without
 // helpers. Same arithmetic and orders as the reference:
-//   kHubGather  raw entries of tile c, ranked in shared memory (raw keys are
-//               unique) -> RK/RW, each 256-entry tile sorted by (row, source)
+//   kHubGather  raw entries of tile c, ranked in shared memory (rank_sort;
+//               raw keys are unique) -> RK/RW, each 256-entry tile sorted by
+//               (row, source)
 //   kHubRank    each entry's place among the other tiles (binary searches over
 //               tiles staged in shared memory) -> SK/SW, the raw column sorted;
 //               run heads counted per 256-entry block of the sorted order (HB)
@@ -35,11 +36,14 @@ namespace {
 //   (owner)     lkk in row order (factor_common.hpp:117-121) and the suffix
 //               sums right to left (sampling.hpp:72-76), side by side
 //   kHubSample  samples i (sampling.hpp:77-83) + fill emission, the column of
-//               G in row order, ASAP levels
+//               G in row order, ASAP levels; posted from the chains as soon as
+//               lkk is known, its chunks taken top down, each starting once
+//               the suffix sums it searches are written (HubJob::progress)
 //   kHubRelease decrements by multiplicity, ready rows published
 // A phase is posted (descriptor, then the release of its `next` word) only
 // after every chunk of the previous one is done, so chunks of one phase never
-// read what the same phase writes.
+// read what the same phase writes (sampling reads the suffix sums only below
+// the published progress).
 enum : int { kHubGather = 1, kHubRank, kHubMerge, kHubWTile, kHubWRank, kHubSample, kHubRelease };
 static_assert(kHubSample == kHubSamplePhase, "hub_chains.cu posts the sampling phase by number");
 constexpr int kHubTile = kThreads;                    // entries per chunk, one per thread

@@ -270,6 +270,12 @@ __device__ __noinline__ void hub_chunk(int c, HubJob& J) {
       // suffix chain has written C[b + 1, m), all its samples search
       const int m = h.m, bs = h.pipe ? (h.mt - 1 - c) * kHubTile : b0, i = bs + tid;
       const bool smp = i < m - 1, col = i < m;
+      if (col) {  // the column of G (row order) and ASAP levels: lkk suffices
+        const int row = static_cast<int>(__ldcg(A.RK + i) >> 32);
+        d.arena_rows[h.start + i] = row;
+        d.arena_vals[h.start + i] = __ddiv_rn(-__ldcg(A.RW + i), h.lkk);
+        if (d.level) atomicMax(&d.level[row], h.lvk + 1);
+      }
       if (h.pipe) {
         if (tid == 0) {
           int iter = 0;
@@ -315,12 +321,6 @@ __device__ __noinline__ void hub_chunk(int c, HubJob& J) {
       if (em && slot >= 0) write_fill(d, lo, slot, hi, h.k, wv);
       const int e = __popc(__ballot_sync(kFull, em));
       if (lane == 0 && e) atomicAdd(emitted, e);
-      if (col) {  // the column of G (row order) and ASAP levels
-        const int row = static_cast<int>(__ldcg(A.RK + i) >> 32);
-        d.arena_rows[h.start + i] = row;
-        d.arena_vals[h.start + i] = __ddiv_rn(-__ldcg(A.RW + i), h.lkk);
-        if (d.level) atomicMax(&d.level[row], h.lvk + 1);
-      }
       break;
     }
     case kHubRelease: {

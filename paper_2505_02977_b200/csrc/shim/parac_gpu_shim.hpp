@@ -87,6 +87,9 @@ struct Session {
   // shape (n, adjacency entries) and factor size of the last factorization:
   // the guess for sizing the next same-shape factor's outputs early
   std::int64_t last_n = -1, last_nnz = -1, last_z = 0;
+  // the row pointer rebuilt for each call (kept: a fresh 17 MB vector per
+  // 128^3 call paid its page faults every time)
+  std::vector<std::int64_t> ptr;
 };
 inline Session& session(int device) {
   static Session sessions[kMaxDevices];
@@ -144,9 +147,9 @@ void size_output(std::vector<T>& v, std::size_t count) {
 // contiguous adjacency arrays (graph.hpp:36-44), so the row pointer is rebuilt
 // from degree() and the arrays are passed without copying.
 struct CsrView {
-  std::vector<std::int64_t> ptr;
+  std::vector<std::int64_t>& ptr;
   parac_csr csr{};
-  explicit CsrView(const LaplacianGraph& g) {
+  CsrView(const LaplacianGraph& g, std::vector<std::int64_t>& buf) : ptr(buf) {
     const VertexId n = g.num_vertices();
     ptr.resize(static_cast<std::size_t>(n) + 1, 0);
     // ptr[v] = offset of v's neighbour span in the contiguous adjacency
@@ -156,11 +159,12 @@ struct CsrView {
       for (VertexId v = a; v < b; ++v) ptr[v] = static_cast<std::int64_t>(g.neighbors(v).data() - base);
     };
     if (n >= (1 << 20)) {
-      std::thread th[3];
-      for (int i = 0; i < 3; ++i)
-        th[i] = std::thread(fill, static_cast<VertexId>(static_cast<std::int64_t>(n) * (i + 1) / 4),
-                            static_cast<VertexId>(static_cast<std::int64_t>(n) * (i + 2) / 4));
-      fill(0, static_cast<VertexId>(n / 4));
+      constexpr int kParts = 8;
+      std::thread th[kParts - 1];
+      for (int i = 1; i < kParts; ++i)
+        th[i - 1] = std::thread(fill, static_cast<VertexId>(static_cast<std::int64_t>(n) * i / kParts),
+                                static_cast<VertexId>(static_cast<std::int64_t>(n) * (i + 1) / kParts));
+      fill(0, static_cast<VertexId>(n / kParts));
       for (auto& t : th) t.join();
     } else {
       fill(0, n);
@@ -199,7 +203,7 @@ inline LdlFactor factor_gpu(const LaplacianGraph& graph, const Ordering& orderin
   if (ordering.size() != n)
     throw Error(Errc::dimension_mismatch, "ordering size does not match the graph");
   auto ctx = make_ctx(options.device);
-  CsrView v(graph);
+  CsrView v(graph, ctx.s->ptr);
   parac_gpu_options o;
   parac_gpu_default_options(&o);
   o.column_arena_entries = options.arena_budget;
@@ -303,6 +307,7 @@ inline std::vector<LdlFactor> factor_batch_gpu(std::span<const LaplacianGraph> g
   if (orderings.size() != count || seeds.size() != count || count == 0)
     throw Error(Errc::dimension_mismatch, "batch lists differ in length");
   auto ctx = make_ctx(options.device);
+  std::vector<std::vector<std::int64_t>> ptrs(count);  // one row pointer per problem
   std::vector<CsrView> views;
   views.reserve(count);
   std::vector<parac_csr> csrs(count);
@@ -310,7 +315,7 @@ inline std::vector<LdlFactor> factor_batch_gpu(std::span<const LaplacianGraph> g
   for (std::size_t i = 0; i < count; ++i) {
     if (orderings[i].size() != graphs[i].num_vertices())
       throw Error(Errc::dimension_mismatch, "ordering size does not match the graph");
-    views.emplace_back(graphs[i]);
+    views.emplace_back(graphs[i], ptrs[i]);
     csrs[i] = views.back().csr;
     perms[i] = orderings[i].perm.data();
   }
@@ -349,7 +354,7 @@ inline std::pair<std::vector<double>, SolveReport> pcg_solve_gpu(const Laplacian
   if (factor.n != n || static_cast<VertexId>(b.size()) != n)
     throw Error(Errc::dimension_mismatch, "graph, factor and rhs sizes differ");
   auto ctx = make_ctx(device);
-  CsrView v(graph);
+  CsrView v(graph, ctx.s->ptr);
   check(parac_gpu_upload(ctx.get(), &v.csr, factor.perm.data()));
   stage_factor(ctx.get(), factor);
   std::vector<double> x(static_cast<std::size_t>(n));
@@ -382,7 +387,7 @@ inline std::vector<double> laplacian_apply_gpu(const LaplacianGraph& graph,
   if (static_cast<VertexId>(x.size()) != graph.num_vertices())
     throw Error(Errc::dimension_mismatch, "vector size differs from the graph");
   auto ctx = make_ctx(device);
-  CsrView v(graph);
+  CsrView v(graph, ctx.s->ptr);
   std::vector<std::int32_t> ident(static_cast<std::size_t>(graph.num_vertices()));
   for (VertexId i = 0; i < graph.num_vertices(); ++i) ident[i] = i;
   check(parac_gpu_upload(ctx.get(), &v.csr, ident.data()));

@@ -368,11 +368,11 @@ __device__ __forceinline__ void hub_run_chunk(const FactorDev& d, HubJob& J, int
 
 // Helper: take chunks of job `job` (any of its phases) until it finishes, this
 // CTA's own queue slot is filled, or no phase is posted for hub_linger_ns.
-__device__ __forceinline__ void hub_help(const FactorDev& d, int job, char* smem, CtaShared& sh) {
+// The job to start with is sh.help (set by claim_at's caller).
+__device__ __forceinline__ void hub_help(const FactorDev& d, char* smem, CtaShared& sh) {
   const int tid = threadIdx.x;
   unsigned long long idle0 = 0;
-  if (tid == 0) idle0 = globaltimer_ns();  // (sh.help == job: the kernel passes it)
-  (void)job;
+  if (tid == 0) idle0 = globaltimer_ns();
   while (true) {
     if (tid == 0) {
       int c = -1, seq = 0;
@@ -631,7 +631,8 @@ __device__ int hub_entry(const FactorDev&, int k, int job) {
   CtaShared& sh = k3_sh();
   __syncthreads();  // every thread has read its arguments (from sh) before thread 0 rewrites sh
   if (k >= 0) return hub_eliminate(d, k, smem, sh);
-  hub_help(d, job, smem, sh);
+  (void)job;  // == sh.help
+  hub_help(d, smem, sh);
   return -1;
 }
 

@@ -1590,6 +1590,8 @@ void build_fast_v3(const SolveInputs& in, SolveState& s, int sms) {
   const int dev = in.device >= 0 && in.device < 64 ? in.device : 0;
   if (!csize[dev]) {
     csize[dev] = pick_cluster(head_sweep_kernel<true>, kHeadSmem, kHThreads);
+    if (const char* hc = std::getenv("PARAC_HEAD_CLUSTER"))  // tuning: a smaller head cluster (1..16)
+      csize[dev] = std::max(1, std::min(csize[dev], std::atoi(hc)));
     cudaFuncSetAttribute(head_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHeadSmem));
     cudaFuncSetAttribute(head_sweep_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }

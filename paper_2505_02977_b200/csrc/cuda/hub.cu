@@ -104,7 +104,7 @@ __device__ __forceinline__ int hub_cross_rank(const unsigned long long* K, int n
     const int g1 = min(nt, g0 + kHubGroup);
     const int len = min(n, g1 * kHubTile) - g0 * kHubTile;
     __syncthreads();  // the previous group (or the caller's use of X) is done
-    stage_in<8>(X, K + static_cast<long long>(g0) * kHubTile, len, tid, kThreads);
+    stage_async(X, K + static_cast<long long>(g0) * kHubTile, len);
     __syncthreads();
     if (!valid) continue;
     for (int t = g0; t < g1; t += 4) {
@@ -291,7 +291,8 @@ __device__ __noinline__ void hub_chunk(int c, HubJob& J) {
       const bool full = m <= kHubFullSuffix;
       const int s0 = min(m, bs + 1);  // the lowest suffix entry this chunk's samples read
       if (full) {
-        stage_in<8>(S + s0, A.C + s0, m - s0, tid, kThreads);
+        stage_async(reinterpret_cast<unsigned long long*>(S + s0),
+                    reinterpret_cast<const unsigned long long*>(A.C + s0), m - s0);
       } else {
         const int q0 = (s0 + h.cs - 1) / h.cs;
         stage_in(S + q0, A.C + static_cast<long long>(q0) * h.cs, (m + h.cs - 1) / h.cs - q0, tid, kThreads, h.cs);

@@ -296,6 +296,24 @@ __device__ __forceinline__ void hub_post_warp(const FactorDev& d, int job, CtaSh
   __syncwarp();
 }
 
+// dst[0, cnt) = src[0, cnt) (8-byte elements, global -> shared) by the whole
+// CTA with 16-byte cp.async (through L2: other SMs wrote src), all in flight
+// at once and no registers held; dst and src must share their 16-byte phase.
+// The caller synchronises (__syncthreads) before reading dst.
+__device__ __forceinline__ void stage_async(unsigned long long* dst, const unsigned long long* src, int cnt) {
+  const int tid = threadIdx.x;
+  const int lead = min(cnt, (reinterpret_cast<unsigned long long>(src) & 15ull) ? 1 : 0);
+  if (tid == 0 && lead) dst[0] = __ldcg(src);
+  const int pairs = (cnt - lead) >> 1;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(dst + lead));
+  for (int p = tid; p < pairs; p += kThreads)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + 16u * p), "l"(src + lead + 2 * p)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (tid == 0 && cnt - lead - 2 * pairs) dst[cnt - 1] = __ldcg(src + cnt - 1);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // The owner's serial chains of a hub column (hub_chains.cu): returns lkk of
 // the row-ordered merged weights W[0, m); with suffix, C = suffix sums of the
 // weight-ordered WB. rec: optional trace record.

@@ -29,10 +29,12 @@ namespace {
 //               tiles staged in shared memory) -> SK/SW, the raw column sorted;
 //               run heads counted per 256-entry block of the sorted order (HB)
 //   kHubMerge   each run head sums its run left to right (factor_common.hpp:
-//               100-113) -> merged column (row << 32 | mult, weight) in RK/RW
-//   kHubWTile   each tile ranked stably by weight bits -> SK (bits) / SW (payload)
-//   kHubWRank   place among the other tiles (earlier tiles: ties count) ->
-//               WK / WB in (weight, row) order (factor_common.hpp:133-145)
+//               100-113) -> merged column (row << 32 | mult, weight) in RK/RW;
+//               the block's merged rows, ranked stably by weight bits, form
+//               weight tile c -> WK (bits) / WB (payload) from pref[c]
+//   kHubWRank   place of each weight-tile entry among the other tiles
+//               (earlier tiles: ties count) -> SK (payload) / SW (weight) in
+//               (weight, row) order (factor_common.hpp:133-145)
 //   (owner)     lkk in row order (factor_common.hpp:117-121) and the suffix
 //               sums right to left (sampling.hpp:72-76), side by side
 //   kHubSample  samples i (sampling.hpp:77-83) + fill emission, the column of
@@ -44,6 +46,8 @@ namespace {
 // after every chunk of the previous one is done, so chunks of one phase never
 // read what the same phase writes (sampling reads the suffix sums only below
 // the published progress).
+// (kHubWTile, a separate weight-tile phase, is fused into kHubMerge; the id
+// stays for the trace's step numbering)
 enum : int { kHubGather = 1, kHubRank, kHubMerge, kHubWTile, kHubWRank, kHubSample, kHubRelease };
 static_assert(kHubSample == kHubSamplePhase, "hub_chains.cu posts the sampling phase by number");
 constexpr int kHubTile = kThreads;                    // entries per chunk, one per thread
@@ -53,8 +57,11 @@ constexpr int kHubFullSuffix = kCtaSmem / 8;          // suffix arrays up to thi
 struct HubArr {
   unsigned long long *RK, *SK, *WK;
   double *RW, *SW, *WB, *C;
-  int* HB;  // run heads per sorted block (in C's space: C is written after kHubMerge)
+  int* HB;  // run heads per sorted block (in C's space: C is written after the weight rank)
 };
+// weight tile t (the merged rows of sorted block t) starts at pref[t] (HB's
+// exclusive prefix; pref[nt] = m), right after HB in C's space
+__device__ __forceinline__ int* hub_pref(const HubArr& A, int nt) { return A.HB + nt; }
 __device__ __forceinline__ HubArr hub_arrays(const FactorDev& d, long long slab, int cap) {
   char* b = d.large_pool + slab * kEntryBytes;
   const long long c8 = 8ll * cap;
@@ -130,6 +137,51 @@ __device__ __forceinline__ int hub_cross_rank(const unsigned long long* K, int n
         pos += lo[q];
         if (PRED && lo[q] > 0) pred = max(pred, X[(t + q - g0) * kHubTile + lo[q] - 1]);
       }
+    }
+  }
+  return pos;
+}
+
+// hub_cross_rank over tiles of variable length (<= kHubTile): tile t is
+// K[toff[t], toff[t+1]). Staged kHubGroup - 1 tiles at a time (at X + the
+// 16-byte phase of their first key, + their bounds after them).
+template <bool STABLE>
+__device__ __forceinline__ int hub_cross_rank_var(const unsigned long long* K, const int* toff_g, int nt, int c,
+                                                  unsigned long long key, bool valid, unsigned long long* X) {
+  constexpr int G = kHubGroup - 1;
+  const int tid = threadIdx.x;
+  int* tb = reinterpret_cast<int*>(X + G * kHubTile + 2);  // the group's G + 1 tile bounds
+  int pos = 0;
+  for (int g0 = 0; g0 < nt; g0 += G) {
+    const int g1 = min(nt, g0 + G);
+    __syncthreads();  // the previous group (or the caller's use of X) is done
+    if (tid <= g1 - g0) tb[tid] = __ldcg(toff_g + g0 + tid);
+    __syncthreads();
+    const int base = tb[0], xo = base & 1;
+    stage_async(X + xo, K + base, tb[g1 - g0] - base);
+    __syncthreads();
+    if (!valid) continue;
+    for (int t = g0; t < g1; t += 4) {
+      int lo[4], tl[4], st[4];
+      unsigned long long thr[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int tt = t + q;
+        lo[q] = 0;
+        tl[q] = (tt < g1 && tt != c) ? tb[tt + 1 - g0] - tb[tt - g0] : 0;
+        st[q] = tt < g1 ? xo + tb[tt - g0] - base : 0;
+        thr[q] = STABLE && tt < c ? key + 1 : key;
+      }
+#pragma unroll
+      for (int step = kHubTile; step > 0; step >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int p = lo[q] + step;
+          if (p <= tl[q] && X[st[q] + p - 1] < thr[q]) lo[q] = p;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pos += lo[q];
     }
   }
   return pos;
@@ -237,31 +289,36 @@ __device__ __noinline__ void hub_chunk(int c, HubJob& J) {
         }
         __stcg(A.RK + off, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned>(mult));
         __stcg(A.RW + off, acc);
+        X[1024 + off - before] = dbits(acc);  // this block's merged rows, for its weight tile
+        X[1280 + off - before] = (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned>(mult);
       }
+      // the weight tile of sorted block c: its merged rows (row order) ranked
+      // stably by weight bits -> WK (bits) / WB (payload) at pref[c] = before
+      int nh = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) nh += ws[kWarps + w];
+      __syncthreads();
+      const bool tv = tid < nh;
+      const unsigned long long wk = tv ? X[1024 + tid] : kInfBits;
+      const unsigned long long pl = tv ? X[1280 + tid] : 0ull;
+      const int r = hub_tile_rank(wk, nh, X);
+      if (tv) {
+        __stcg(A.WK + before + r, wk);
+        __stcg(reinterpret_cast<unsigned long long*>(A.WB) + before + r, pl);
+      }
+      if (tid == 0) __stcg(hub_pref(A, h.nt) + c, before);
       break;
     }
-    case kHubWTile: {
-      const int cnt = min(kHubTile, h.m - b0);
-      const bool v = tid < cnt;
-      const unsigned long long wk = v ? dbits(__ldcg(A.RW + b0 + tid)) : kInfBits;
-      const unsigned long long a = v ? __ldcg(A.RK + b0 + tid) : ~0ull;
-      const int r = hub_tile_rank(wk, cnt, X);
+    case kHubWRank: {  // tile c of the weight tiles: each entry's place among the other tiles
+      const int* pref = hub_pref(A, h.nt);
+      const int t0 = __ldcg(pref + c), len = __ldcg(pref + c + 1) - t0;
+      const bool v = tid < len;
+      const unsigned long long wk = v ? __ldcg(A.WK + t0 + tid) : kInfBits;
+      const unsigned long long a = v ? __ldcg(reinterpret_cast<const unsigned long long*>(A.WB) + t0 + tid) : 0ull;
+      const int pos = tid + hub_cross_rank_var<true>(A.WK, pref, h.nt, c, wk, v, X);
       if (v) {
-        __stcg(A.SK + b0 + r, wk);
-        __stcg(reinterpret_cast<unsigned long long*>(A.SW) + b0 + r, a);
-      }
-      break;
-    }
-    case kHubWRank: {
-      const int cnt = min(kHubTile, h.m - b0);
-      const bool v = tid < cnt;
-      const unsigned long long wk = v ? __ldcg(A.SK + b0 + tid) : kInfBits;
-      const unsigned long long a = v ? __ldcg(reinterpret_cast<const unsigned long long*>(A.SW) + b0 + tid) : 0ull;
-      unsigned long long unused = 0;
-      const int pos = tid + hub_cross_rank<true, false>(A.SK, h.m, c, wk, v, X, unused);
-      if (v) {
-        __stcg(A.WK + pos, a);
-        __stcg(A.WB + pos, bitsd(wk));
+        __stcg(A.SK + pos, a);
+        __stcg(A.SW + pos, bitsd(wk));
       }
       break;
     }
@@ -306,9 +363,9 @@ __device__ __noinline__ void hub_chunk(int c, HubJob& J) {
         const double s = full ? S[i + 1] : __ldcg(A.C + i + 1);
         const double u = __dmul_rn(unit_uniform(sk.seed, sk.key, static_cast<unsigned long long>(i)), s);
         const int j = full ? pick_by_suffix(S, i + 1, m - 1, u) : hub_pick(A.C, S, h.cs, i + 1, m - 1, u);
-        wv = __ddiv_rn(__dmul_rn(s, __ldcg(A.WB + i)), h.lkk);
+        wv = __ddiv_rn(__dmul_rn(s, __ldcg(A.SW + i)), h.lkk);
         if (wv >= kDropThreshold) {
-          const int ra = static_cast<int>(__ldcg(A.WK + i) >> 32), rc = static_cast<int>(__ldcg(A.WK + j) >> 32);
+          const int ra = static_cast<int>(__ldcg(A.SK + i) >> 32), rc = static_cast<int>(__ldcg(A.SK + j) >> 32);
           lo = min(ra, rc);
           hi = max(ra, rc);
           em = true;
@@ -539,12 +596,14 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
   SUB(0);
   bool ok = true;
   for (int ph = kHubGather; ok && ph <= kHubRelease; ++ph) {
-    if (ph == kHubWTile) {  // the merged column's size: run heads of every sorted block
+    if (ph == kHubWTile) continue;  // fused into the merge (each block ranks its merged rows)
+    if (ph == kHubWRank) {  // the merged column's size: run heads of every sorted block
       const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
       int m = 0;
       for (int j = tid; j < sh.hd.nt; j += kThreads) m += __ldcg(A.HB + j);
       m = cta_sum(m, reinterpret_cast<int*>(smem));
       if (lead) {
+        __stcg(hub_pref(A, sh.hd.nt) + sh.hd.nt, m);  // pref[nt] = m (ordered before the post by its fence)
         sh.hd.m = m;
         sh.hd.mt = (m + kHubTile - 1) / kHubTile;
       }
@@ -553,7 +612,7 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       if (k == d.trace_k) snapshot_dp(d, 0, tid, kThreads);
       __syncthreads();
     }
-    if ((ph == kHubWTile || ph == kHubWRank) && sh.hd.m < 2) continue;  // one row: nothing to sort
+    if (ph == kHubWRank && sh.hd.m < 2) continue;  // one row: nothing to sort
     bool posted = false;  // the sampling phase was posted (pipelined) from the chains
     if (ph == kHubSample) {
       PHASE(3);
@@ -588,7 +647,7 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       }
       {
         const HubArr A = hub_arrays(d, sh.hd.slab, sh.hd.cap);
-        const double lkk = hub_chains(A.RW, A.WB, A.C, m, m >= 2, rec, pipe ? job : -1);
+        const double lkk = hub_chains(A.RW, A.SW, A.C, m, m >= 2, rec, pipe ? job : -1);
         if (lead) {
           sh.hd.lkk = lkk;
           d.diag[k] = lkk;
@@ -605,7 +664,7 @@ __device__ __forceinline__ int hub_eliminate(const FactorDev& d, int k, char* sm
       if (k == d.trace_k) snapshot_dp(d, 1, tid, kThreads);
     }
     ok = posted ? hub_run(d, job, smem, sh, sh.hd.mt, -1)
-                : hub_phase(d, job, smem, sh, ph, ph <= kHubMerge ? sh.hd.nt : sh.hd.mt);
+                : hub_phase(d, job, smem, sh, ph, ph <= kHubMerge || ph == kHubWRank ? sh.hd.nt : sh.hd.mt);
     if (d.vsub && lead && ph <= kHubWRank) {  // wide-column stamps (tools/profile_factor.py)
       unsigned long long* wst = d.vsub + d.n * 8ll + 4ll * k;
       if (ph <= kHubMerge) wst[ph - 1] = globaltimer_ns();

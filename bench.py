@@ -14,8 +14,9 @@ so per-GPU work is fixed and scaling is "weak"; there is no data-path collective
 Step = one factorization of the workload with its inputs resident in HBM
 (`value`, device time from CUDA events on the library's stream, L2 flushed
 between steps). `e2e` = the same factorization through the C ABI
-(parac_gpu_factor + parac_gpu_download) from pinned host buffers, host<->device
-copies inside the timed region. `--impl reference` times the reference's own
+(parac_gpu_factor_to_host: upload, factor, and the factor copied out while the
+elimination runs) from and into pinned host buffers, host<->device copies
+inside the timed region. `--impl reference` times the reference's own
 multithreaded CPU path (oracle/_ref: factor_parallel_left/right, unmodified
 sources) on this host's cores.
 """
@@ -449,9 +450,11 @@ def run_ours(args):
         flush.zero_()
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
-        check(lib.parac_gpu_factor(ctx.handle, C.byref(csr), perm_ptr, seed, C.byref(opts), C.byref(info)))
-        check(lib.parac_gpu_download(ctx.handle, out_bufs[0][0], out_bufs[1][0], out_bufs[2][0],
-                                     out_bufs[3][0], None, None, None))
+        # upload, factor, and the factor copied out while it is computed
+        # (parac_gpu_factor_to_host: the streamed assembly + download)
+        check(lib.parac_gpu_factor_to_host(ctx.handle, C.byref(csr), perm_ptr, seed, C.byref(opts), C.byref(info),
+                                           out_bufs[0][0], out_bufs[1][0], out_bufs[2][0], out_bufs[3][0],
+                                           max(Z, 1)))
         e2e_s.append(time.perf_counter() - t0)
     barrier(pg, device)
     e2e_total = allreduce(pg, device, sum(e2e_s), "MAX")

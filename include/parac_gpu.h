@@ -216,6 +216,26 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
 int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
                      const parac_gpu_options* opt, parac_gpu_factor_info* info);
 
+/* The factorization split in two, so that the host can work while the device
+ * factors: _begin launches it (returns at once); _end waits for it and copies
+ * the factor out WHILE the elimination runs -- each column is copied as soon
+ * as it and every column before it are final (the CSC assembly is streamed
+ * beside the elimination). Together they replace factor_parallel_left
+ * (include/parac/factor_par.hpp:53-62) returning its LdlFactor
+ * (include/parac/factor.hpp:18-25): col_ptr[n+1], rows/values[capacity],
+ * diag[n], any of them NULL. The factor stays resident either way. Errors as
+ * parac_gpu_factor_resident; PARAC_BUDGET_EXCEEDED when Z > capacity (rows/
+ * values incomplete, info->nnz_off_diagonal = Z: size them and call
+ * parac_gpu_download). Pinned outputs are filled by DMA, pageable ones
+ * through pinned staging. */
+int parac_gpu_factor_begin(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt);
+int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* col_ptr, int32_t* rows,
+                         double* values, double* diag, int64_t capacity);
+/* upload + factor_begin + factor_end: one call from host input to host factor. */
+int parac_gpu_factor_to_host(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
+                             const parac_gpu_options* opt, parac_gpu_factor_info* info, int64_t* col_ptr,
+                             int32_t* rows, double* values, double* diag, int64_t capacity);
+
 /* ---- batch (BASELINE config[4]: many independent Laplacians per GPU) ------
  * Stage `count` problems (graph i, ordering perms[i], seed seeds[i]) as one
  * disjoint-union problem so a single persistent elimination factors all of

@@ -82,6 +82,10 @@ SIGNATURES = {
     "parac_gpu_factor_resident": (C.c_int, [vp, u64, P(parac_gpu_options), P(parac_gpu_factor_info)]),
     "parac_gpu_factor": (C.c_int, [vp, P(parac_csr), vp, u64, P(parac_gpu_options),
                                    P(parac_gpu_factor_info)]),
+    "parac_gpu_factor_begin": (C.c_int, [vp, u64, P(parac_gpu_options)]),
+    "parac_gpu_factor_end": (C.c_int, [vp, P(parac_gpu_factor_info), vp, vp, vp, vp, i64]),
+    "parac_gpu_factor_to_host": (C.c_int, [vp, P(parac_csr), vp, u64, P(parac_gpu_options),
+                                           P(parac_gpu_factor_info), vp, vp, vp, vp, i64]),
     "parac_gpu_download": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "parac_gpu_download_times": (C.c_int, [vp, vp]),
     "parac_gpu_download_subtimes": (C.c_int, [vp, vp]),

@@ -231,6 +231,13 @@ struct Timer {
 
 using namespace parac_gpu;
 
+namespace {
+struct Budgets {
+  long long ovf, arena, large;
+  int c0;
+};
+}  // namespace
+
 struct parac_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -286,6 +293,23 @@ struct parac_gpu_ctx {
   SolveState solve;
   // pinned bounce buffers for pageable caller memory
   Stager stage;
+  // streamed assembly (stream_assemble.cu): per-block eliminated counts,
+  // chained prefix, claim/publish counters, the streamer's stream, a copy
+  // stream for the download, and the mapped pinned progress word
+  bool streaming = false;  // the pending attempt assembles beside K3
+  DevBuf<int> blk_done, stream_ctl;
+  DevBuf<unsigned long long> blk_incl;
+  cudaStream_t s_stream = nullptr, s_copy = nullptr;
+  unsigned long long* prog_h = nullptr;
+  unsigned long long* prog_d = nullptr;
+  // a factorization launched by parac_gpu_factor_begin, completed by _end
+  bool pending = false;
+  std::uint64_t p_seed = 0;
+  parac_gpu_options p_opt{};
+  Budgets p_b{};
+  int p_attempts = 0;
+  double p_failed_ms = 0.0;
+  std::chrono::steady_clock::time_point p_t0;
 };
 
 namespace {
@@ -302,11 +326,6 @@ void require_ctx(parac_gpu_ctx* ctx) {
   if (!ctx) throw Failure{internal_error, "null context"};
   activate(ctx);
 }
-
-struct Budgets {
-  long long ovf, arena, large;
-  int c0;
-};
 
 Budgets default_budgets(int n, long long E, long long max_degree, const parac_gpu_options& o) {
   Budgets b;
@@ -335,9 +354,46 @@ Budgets default_budgets(int n, long long E, long long max_degree, const parac_gp
   return b;
 }
 
-// One attempt of the factorization with the given budgets. Returns status.
-int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& o,
-               const Budgets& b, parac_gpu_factor_info* info) {
+// Streamed assembly beside K3 (stream_assemble.cu): on by default for single
+// problems (PARAC_STREAM=0: assemble after K3), PARAC_STREAM_CTAS CTAs (8)
+int stream_ctas() {
+  const char* e = std::getenv("PARAC_STREAM_CTAS");
+  return e ? std::max(1, std::min(64, std::atoi(e))) : 8;
+}
+bool stream_wanted(const parac_gpu_ctx* ctx) {
+  const char* e = std::getenv("PARAC_STREAM");
+  const int m = e ? std::atoi(e) : 1;
+  return (m == 1 || m == 3) && ctx->batch_count == 0 && ctx->n > 0;
+}
+// PARAC_STREAM=3 (diagnostics): the streamer runs after K3 on K3's stream --
+// its throughput alone
+bool stream_serial() {
+  const char* e = std::getenv("PARAC_STREAM");
+  return e && std::atoi(e) == 3;
+}
+// PARAC_STREAM=2 (diagnostics): K3 counts the blocks' columns, the assembly
+// still runs after it -- the cost of the counting alone
+bool stream_count_only() {
+  const char* e = std::getenv("PARAC_STREAM");
+  return e && std::atoi(e) == 2;
+}
+void ensure_stream_resources(parac_gpu_ctx* ctx) {
+  if (!ctx->s_stream) check(cudaStreamCreateWithFlags(&ctx->s_stream, cudaStreamNonBlocking), "stream");
+  if (!ctx->s_copy) check(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking), "stream");
+  if (!ctx->prog_h) {
+    void* h = nullptr;
+    check(cudaHostAlloc(&h, 64, cudaHostAllocMapped), "cudaHostAlloc (progress word)");
+    ctx->prog_h = static_cast<unsigned long long*>(h);
+    void* dp = nullptr;
+    check(cudaHostGetDevicePointer(&dp, h, 0), "cudaHostGetDevicePointer");
+    ctx->prog_d = static_cast<unsigned long long*>(dp);
+  }
+}
+
+// Launch half of one attempt of the factorization with the given budgets
+// (stream-ordered; complete_factor waits for it).
+void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& o,
+                   const Budgets& b) {
   const int n = ctx->n;
   const long long E = ctx->nnz / 2;
   cudaStream_t s = ctx->stream;
@@ -485,7 +541,24 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
     d.hub_trace = ctx->hub_trace.p;
   }
 
+  d.blk_done = nullptr;
+  const bool count = ctx->streaming || stream_count_only();
+  if (count) {
+    ensure_stream_resources(ctx);
+    const std::size_t nb = static_cast<std::size_t>((n + kStreamBlock - 1) >> kStreamShift);
+    ctx->blk_done.ensure(nb);
+    ctx->blk_incl.ensure(nb);
+    ctx->stream_ctl.ensure(2);
+    *static_cast<volatile unsigned long long*>(ctx->prog_h) = 0;  // no stream work of an earlier attempt is in flight
+    d.blk_done = ctx->blk_done.p;
+  }
   check(cudaEventRecord(ctx->ev[0], s), "event");
+  if (count) {
+    const std::size_t nb = static_cast<std::size_t>((n + kStreamBlock - 1) >> kStreamShift);
+    check(cudaMemsetAsync(ctx->blk_done.p, 0, nb * sizeof(int), s), "memset");
+    check(cudaMemsetAsync(ctx->blk_incl.p, 0, nb * sizeof(unsigned long long), s), "memset");
+    check(cudaMemsetAsync(ctx->stream_ctl.p, 0, 2 * sizeof(int), s), "memset");
+  }
   check(cudaMemsetAsync(ctx->inv.p, 0xff, nn * sizeof(int), s), "memset");
   check(cudaMemsetAsync(ctx->dir.p, 0, nn * kDirChunks * sizeof(unsigned), s), "memset");
   check(cudaMemsetAsync(ctx->ctrl.p, 0, sizeof(Ctrl), s), "memset");
@@ -494,10 +567,109 @@ int run_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_options& 
   check(launch_initial_ready(d, ctx->tiles.p, s), "initial_ready launch");
   check(cudaEventRecord(ctx->ev[1], s), "event");
   int grid = 0;
-  check(launch_eliminate(d, o.grid_ctas, s, &grid), "eliminate launch");
-  check(cudaEventRecord(ctx->ev[2], s), "event");
-  check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, s), "assemble");
+  const int sctas = ctx->streaming ? stream_ctas() : 0;
+  const bool serial = ctx->streaming && stream_serial();
+  check(launch_eliminate(d, o.grid_ctas, serial ? 0 : sctas, s, &grid), "eliminate launch");
+  if (serial) check(cudaEventRecord(ctx->ev[2], s), "event");
+  if (ctx->streaming) {  // the assembly beside K3, on its own stream (after K1/K2)
+    StreamDev sd{};
+    sd.n = n;
+    sd.nb = (n + kStreamBlock - 1) >> kStreamShift;
+    sd.blk_done = ctx->blk_done.p;
+    sd.col_len = ctx->col_len.p;
+    sd.col_start = ctx->col_start.p;
+    sd.arena_rows = ctx->arena_rows.p;
+    sd.arena_vals = ctx->arena_vals.p;
+    sd.col_ptr = ctx->col_ptr.p;
+    sd.rows = ctx->rows.p;
+    sd.vals = ctx->vals.p;
+    sd.blk_incl = ctx->blk_incl.p;
+    sd.next_blk = ctx->stream_ctl.p;
+    sd.published = ctx->stream_ctl.p + 1;
+    sd.host = ctx->prog_d;
+    sd.ctrl = ctx->ctrl.p;
+    cudaStream_t ss = serial ? s : ctx->s_stream;
+    if (!serial) check(cudaStreamWaitEvent(ss, ctx->ev[1], 0), "stream wait");
+    check(launch_stream_assemble(sd, sctas, ss), "stream assemble launch");
+    check(cudaEventRecord(ctx->ev[4], ss), "event");
+  }
+  if (!serial) check(cudaEventRecord(ctx->ev[2], s), "event");
+  if (ctx->streaming) {
+    check(launch_sum_samples(d, s), "sum samples");
+    check(cudaStreamWaitEvent(s, ctx->ev[4], 0), "stream join");
+  } else {
+    check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, s), "assemble");
+  }
   check(cudaEventRecord(ctx->ev[3], s), "event");
+}
+
+// Where the completion half copies the factor (any pointer may be null;
+// rows/values hold cap entries).
+struct HostOut {
+  std::int64_t* col_ptr;
+  std::int32_t* rows;
+  double* values;
+  double* diag;
+  long long cap;
+};
+
+// Device -> host copy of [off, off + bytes) of one array: pinned targets by
+// DMA on the copy stream (waited for at the end), pageable ones through the
+// staging buffers (synchronous)
+void copy_range(parac_gpu_ctx* ctx, void* dst, const void* src, std::size_t bytes) {
+  if (!dst || bytes == 0) return;
+  if (host_pinned(dst)) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_copy), "d2h");
+  else ctx->stage.d2h(dst, src, bytes, ctx->s_copy);
+}
+
+// The download beside the elimination: polls the streamer's progress word and
+// copies each newly final range (entries, and the blocks' col_ptr/diag) while
+// K3 runs. Returns once every block is copied or the device work ended
+// without it (an aborted attempt; the caller reads the status).
+void stream_download(parac_gpu_ctx* ctx, const HostOut& out) {
+  const int n = ctx->n;
+  const int nb = (n + kStreamBlock - 1) >> kStreamShift;
+  volatile unsigned long long* prog = ctx->prog_h;
+  const long long kMinEntries = 1 << 19;  // ~6 MB of rows+values per round of copies
+  int done_b = 0;
+  long long done_z = 0;
+  auto take = [&](unsigned long long w) {
+    const int pb = static_cast<int>(w & 0xffffffu);
+    const long long pz = static_cast<long long>(w >> 24);
+    if (pb <= done_b || (pb < nb && pz - done_z < kMinEntries)) return;
+    const long long p0 = static_cast<long long>(done_b) << kStreamShift;
+    const long long p1 = std::min<long long>(static_cast<long long>(pb) << kStreamShift, n);
+    const long long z1 = std::min(pz, out.cap);
+    if (z1 > done_z) {
+      copy_range(ctx, out.rows ? out.rows + done_z : nullptr, ctx->rows.p + done_z, sizeof(int) * (z1 - done_z));
+      copy_range(ctx, out.values ? out.values + done_z : nullptr, ctx->vals.p + done_z,
+                 sizeof(double) * (z1 - done_z));
+    }
+    const long long q1 = pb == nb ? p1 + 1 : p1;  // col_ptr[n] with the last block
+    copy_range(ctx, out.col_ptr ? out.col_ptr + p0 : nullptr, ctx->col_ptr.p + p0, sizeof(long long) * (q1 - p0));
+    copy_range(ctx, out.diag ? out.diag + p0 : nullptr, ctx->diag.p + p0, sizeof(double) * (p1 - p0));
+    done_b = pb;
+    done_z = pz;
+  };
+  while (done_b < nb) {
+    take(*prog);
+    if (done_b == nb) break;
+    if (cudaEventQuery(ctx->ev[3]) == cudaSuccess) {  // device work over: the last word is final
+      take(*prog);
+      break;
+    }
+    std::this_thread::yield();
+  }
+  check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
+}
+
+// Completion half: the streamed download (when out is given and the attempt
+// streams), then the status. Returns status.
+int complete_factor(parac_gpu_ctx* ctx, const parac_gpu_options& o, const Budgets& b, const HostOut* out) {
+  const int n = ctx->n;
+  cudaStream_t s = ctx->stream;
+  const double wd = o.watchdog_seconds > 0 ? o.watchdog_seconds : 60.0;
+  if (out && ctx->streaming) stream_download(ctx, *out);
   Ctrl c{};
   long long z = 0;
   check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl copy");
@@ -594,6 +766,12 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   ctx->vals.release(); ctx->f_diag_ext.release(); ctx->f_perm_ext.release();
   solve_release(ctx->solve);
   ctx->stage.release();
+  if (ctx->s_stream) cudaStreamSynchronize(ctx->s_stream);
+  if (ctx->s_copy) cudaStreamSynchronize(ctx->s_copy);
+  ctx->blk_done.release(); ctx->stream_ctl.release(); ctx->blk_incl.release();
+  if (ctx->prog_h) cudaFreeHost(ctx->prog_h);
+  if (ctx->s_stream) cudaStreamDestroy(ctx->s_stream);
+  if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
   for (auto& ev : ctx->ev) cudaEventDestroy(ev);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -790,51 +968,81 @@ int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, in
   });
 }
 
-int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt,
-                              parac_gpu_factor_info* info) {
-  Timer wall;
+int parac_gpu_factor_begin(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt) {
   parac_gpu_options o;
   if (opt) o = *opt; else parac_gpu_default_options(&o);
-  int rc = guarded([&] {
+  return guarded([&] {
     require_ctx(ctx);
     if (ctx->n < 0) throw Failure{dimension_mismatch, "no graph staged (call parac_gpu_upload)"};
+    if (ctx->pending) throw Failure{internal_error, "a factorization is pending (call parac_gpu_factor_end)"};
+    // the previous resident factor is gone as soon as its buffers are reused
+    ctx->f_n = -1;
+    solve_invalidate_factor(ctx->solve);
+    ctx->p_t0 = std::chrono::steady_clock::now();
+    ctx->p_seed = seed;
+    ctx->p_opt = o;
+    ctx->p_b = default_budgets(ctx->n, ctx->nnz / 2, ctx->max_degree, o);
+    ctx->p_attempts = 0;
+    ctx->p_failed_ms = 0.0;
+    ctx->streaming = stream_wanted(ctx);
+    launch_factor(ctx, seed, o, ctx->p_b);
+    ctx->pending = true;
+  });
+}
+
+int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* col_ptr, int32_t* rows,
+                         double* values, double* diag, int64_t capacity) {
+  int rc = guarded([&] {
+    require_ctx(ctx);
+    if (!ctx->pending) throw Failure{internal_error, "no factorization pending (call parac_gpu_factor_begin)"};
   });
   if (rc) return rc;
-  // the previous resident factor is gone as soon as its buffers are reused
-  ctx->f_n = -1;
-  solve_invalidate_factor(ctx->solve);
+  const HostOut out{col_ptr, rows, values, diag, capacity};
+  const bool want = col_ptr || rows || values || diag;
+  const parac_gpu_options& o = ctx->p_opt;
+  Budgets& b = ctx->p_b;
   const int n = ctx->n;
   const long long E = ctx->nnz / 2;
-  Budgets b = default_budgets(n, E, ctx->max_degree, o);
-  double failed_ms = 0.0;  // device time of attempts that ran out of library-chosen budget
-  int attempts = 0;
-  for (int attempt = 0;; ++attempt) {
-    rc = 0;
+  for (;;) {
     int st = 0;
-    rc = guarded([&] { st = run_factor(ctx, seed, o, b, info); });
-    if (rc) return rc;
-    attempts = attempt + 1;
+    rc = guarded([&] { st = complete_factor(ctx, o, b, want ? &out : nullptr); });
+    if (rc) {
+      ctx->pending = false;
+      return rc;
+    }
+    ++ctx->p_attempts;
     if (st == 0) break;
     {
       float t = 0;
       if (cudaEventSynchronize(ctx->ev[3]) == cudaSuccess && cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[3]) == cudaSuccess)
-        failed_ms += t;
+        ctx->p_failed_ms += t;
       if (std::getenv("PARAC_VERBOSE"))
-        std::fprintf(stderr, "parac_gpu: attempt %d ran out of budget after %.1f ms: %s\n", attempt, t,
+        std::fprintf(stderr, "parac_gpu: attempt %d ran out of budget after %.1f ms: %s\n", ctx->p_attempts - 1, t,
                      last_error());
     }
     // Budget exhaustion with library-chosen budgets: grow and retry (the
     // caller's explicit budgets fail cleanly, like ParOptions::arena_budget).
     const bool defaults = o.fill_pool_entries < 0 && o.column_arena_entries < 0;
-    if (st == kStatusNeedHubs && attempt < 8) continue;  // now with the hub path
-    if (st == arena_exhausted && defaults && attempt < 4) {
+    bool again = false;
+    if (st == kStatusNeedHubs && ctx->p_attempts <= 8) {
+      again = true;  // now with the hub path
+    } else if (st == arena_exhausted && defaults && ctx->p_attempts <= 4) {
       b.ovf *= 2;
       b.arena *= 2;
       b.large *= 4;
-      continue;
+      again = true;
     }
-    return st;
+    if (!again) {
+      ctx->pending = false;
+      return st;
+    }
+    rc = guarded([&] { launch_factor(ctx, ctx->p_seed, o, b); });
+    if (rc) {
+      ctx->pending = false;
+      return rc;
+    }
   }
+  ctx->pending = false;
   rc = guarded([&] {
     const Ctrl c = ctx->last_ctrl;
     const long long Z = ctx->last_z;
@@ -866,11 +1074,46 @@ int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu
       info->setup_ms = t01;
       info->eliminate_ms = t12;
       info->assemble_ms = t23;
-      info->device_ms = t03 + failed_ms;
-      info->wall_ms = wall.ms();
-      info->attempts = attempts;
+      info->device_ms = t03 + ctx->p_failed_ms;
+      info->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ctx->p_t0).count();
+      info->attempts = ctx->p_attempts;
+    }
+    if (want && Z > capacity && (rows || values))
+      throw Failure{budget_exceeded, "factor has " + std::to_string(Z) + " off-diagonal entries, outputs hold " +
+                                         std::to_string(capacity) + " (the factor stays resident: parac_gpu_download)"};
+    if (want && !ctx->streaming) {  // the assembly ran after K3: plain download
+      const long long z = std::min<long long>(Z, std::max<long long>(capacity, 0));
+      if (col_ptr) ctx->stage.d2h(col_ptr, ctx->col_ptr.p, sizeof(long long) * (n + 1), ctx->stream);
+      if (rows && z) ctx->stage.d2h(rows, ctx->rows.p, sizeof(int) * z, ctx->stream);
+      if (values && z) ctx->stage.d2h(values, ctx->vals.p, sizeof(double) * z, ctx->stream);
+      if (diag && n) ctx->stage.d2h(diag, ctx->diag.p, sizeof(double) * n, ctx->stream);
+      check(cudaStreamSynchronize(ctx->stream), "d2h sync");
     }
   });
+  return rc;
+}
+
+int parac_gpu_factor_resident(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt,
+                              parac_gpu_factor_info* info) {
+  const int rc = parac_gpu_factor_begin(ctx, seed, opt);
+  if (rc) return rc;
+  return parac_gpu_factor_end(ctx, info, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+int parac_gpu_factor_to_host(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm, uint64_t seed,
+                             const parac_gpu_options* opt, parac_gpu_factor_info* info, int64_t* col_ptr,
+                             int32_t* rows, double* values, double* diag, int64_t capacity) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = parac_gpu_upload(ctx, g, perm);
+  if (rc) return rc;
+  const double up = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  rc = parac_gpu_factor_begin(ctx, seed, opt);
+  if (rc) return rc;
+  rc = parac_gpu_factor_end(ctx, info, col_ptr, rows, values, diag, capacity);
+  if (info && (rc == 0 || rc == budget_exceeded)) {
+    info->upload_ms = up;
+    info->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   return rc;
 }
 

@@ -851,7 +851,10 @@ __device__ Next warp_eliminate(const FactorDev& d, Next nx, Scratch S, int lane,
   }
   PHASE(2);
   if (m == 0) {  // factor_seq.cpp:92-95 (col_len/col_start already 0 from K1)
-    if (lead) d.diag[k] = 0.0;
+    if (lead) {
+      d.diag[k] = 0.0;
+      if (d.blk_done) fence_acq_rel();  // release: the streamed assembly reads it after the count
+    }
     return {-1, -1, 0, 0};
   }
 
@@ -1233,7 +1236,10 @@ __device__ int cta_eliminate(const FactorDev& d, int k, char* smem, CtaShared& s
   }
   PHASE(2);
   if (m == 0) {
-    if (lead) d.diag[k] = 0.0;
+    if (lead) {
+      d.diag[k] = 0.0;
+      if (d.blk_done) fence_acq_rel();  // release (streamed assembly)
+    }
     return -1;
   }
 
@@ -1382,6 +1388,7 @@ __device__ __forceinline__ int big_loop(const FactorDev& d, char* smem, CtaShare
     const int next = cta_eliminate(d, k, smem, sh, allow);
     if (next == -2) break;
     PHASE(7);
+    if (d.blk_done && lead) red_add_relaxed(&d.blk_done[k >> kStreamShift], 1);  // after the release fence
     ++done_local;
     k = next;
     __syncthreads();
@@ -1463,6 +1470,7 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_con
       if (nn.k == -2) break;
       if (nn.k != -3) {
         PHASE(7);
+        if (d.blk_done && lead) red_add_relaxed(&d.blk_done[k >> kStreamShift], 1);  // after the release fence
         ++done_local;
       }
       nx = nn.k >= 0 ? nn : Next{-1, -1, 0, 0};
@@ -1495,6 +1503,10 @@ __global__ void __launch_bounds__(kThreads, 4) eliminate_kernel(const __grid_con
       if (r == -2) break;
       if (threadIdx.x == 0) {
         PHASE_K(7, sh.k);
+        if (d.blk_done) {  // the owner acquired every chunk's stores (hub_run); release them
+          fence_acq_rel();
+          red_add_relaxed(&d.blk_done[sh.k >> kStreamShift], 1);
+        }
         atomicAdd(&d.ctrl->eliminated, 1);
         sh.k = -1;
       }
@@ -1537,13 +1549,15 @@ cudaError_t launch_hubs(const FactorDev& d, int grid, cudaStream_t s);
 // The largest grid either instance launches (sizes the per-CTA hub job records)
 int eliminate_occupancy_grid(int device) { return std::max(occupancy_hubs(device), occupancy_grid<false>(device)); }
 
-cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used) {
+cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, int reserve, cudaStream_t s, int* grid_used) {
   if (d.n == 0) return cudaSuccess;
   int dev = 0;
   cudaGetDevice(&dev);
   const int occ = d.hubs ? occupancy_hubs(dev) : occupancy_grid<false>(dev);
   int grid = grid_ctas > 0 ? grid_ctas : occ;
-  if (grid > occ) grid = occ;  // persistent: every CTA must be co-resident
+  // persistent: every CTA must be co-resident, beside `reserve` CTA slots
+  // left to a concurrent kernel (the streamed assembly)
+  if (grid > occ - reserve) grid = occ - reserve;
   if (grid < 2) grid = 2;      // at least one small and one big CTA
   if (grid_used) *grid_used = grid;
   note_launches(1);

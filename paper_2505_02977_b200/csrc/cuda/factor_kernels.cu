@@ -414,6 +414,15 @@ cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, d
   return cudaGetLastError();
 }
 
+cudaError_t launch_sum_samples(const FactorDev& d, cudaStream_t s) {
+  if (d.n == 0) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  sum_samples_kernel<<<num_sms(dev) * 2, 256, 0, s>>>(d);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- batch
 namespace {
 __device__ __forceinline__ int batch_of(const long long* base, int count, long long x) {

@@ -162,13 +162,39 @@ struct FactorDev {
   int trace_k;
   long long* trace_dp;
   int* trace_taken;
+  // streamed assembly (stream_assemble.cu): eliminated columns per block of
+  // kStreamBlock positions, one relaxed add per column after its release
+  // fence; nullptr when the assembly runs after the elimination
+  int* blk_done;
 };
+
+// Streamed CSC assembly beside K3 (stream_assemble.cu).
+constexpr int kStreamShift = 11;
+constexpr int kStreamBlock = 1 << kStreamShift;
+struct StreamDev {
+  int n, nb;                        // positions, blocks
+  const int* blk_done;              // [nb] eliminated columns per block (K3)
+  const int* col_len;
+  const long long* col_start;
+  const int* arena_rows;
+  const double* arena_vals;
+  long long* col_ptr;               // the resident CSC factor (as launch_assemble writes it)
+  int* rows;
+  double* vals;
+  unsigned long long* blk_incl;     // [nb] inclusive entry offset | bit 63 (chained prefix)
+  int* next_blk;                    // block claim counter
+  int* published;                   // blocks released to the host, in order
+  unsigned long long* host;         // mapped pinned progress word (entries << 24 | blocks), or nullptr
+  Ctrl* ctrl;                       // status (K3 aborted), eliminated
+};
+cudaError_t launch_stream_assemble(const StreamDev& s, int ctas, cudaStream_t st);
+cudaError_t launch_sum_samples(const FactorDev& d, cudaStream_t s);
 
 // Launchers (stream-ordered). All return cudaError_t of the launch.
 cudaError_t launch_pos_graph(const FactorDev& d, long long* tile_scratch, cudaStream_t s);
 cudaError_t launch_initial_ready(const FactorDev& d, long long* tile_scratch, cudaStream_t s);
 int initial_ready_scratch(int n);  // long longs of tile_scratch launch_initial_ready needs
-cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, cudaStream_t s, int* grid_used);
+cudaError_t launch_eliminate(const FactorDev& d, int grid_ctas, int reserve, cudaStream_t s, int* grid_used);
 cudaError_t launch_assemble(const FactorDev& d, long long* col_ptr, int* rows, double* vals,
                             long long* tile_scratch, cudaStream_t s);
 cudaError_t launch_scan(const int* in, long long n, long long* out, long long* tile_scratch,

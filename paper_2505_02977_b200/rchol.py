@@ -335,6 +335,33 @@ class GpuContext:
         self._resident = None
         return info
 
+    def factor_to_host(self, seed: int, options: Optional[GpuOptions] = None, out=None,
+                       capacity: Optional[int] = None):
+        """parac_gpu_factor_begin + parac_gpu_factor_end on the staged input:
+        the factor is copied to host arrays while it is computed (each column
+        as soon as it and every column before it are final). out = (col_ptr,
+        rows, values, diag) host arrays (pinned or pageable), default fresh
+        numpy arrays sized from the last factor of this context or capacity.
+        Returns (info, out); raises Error(budget_exceeded)
+        when Z exceeds the capacity (the factor stays resident)."""
+        graph, _ = self._graph
+        n = graph.n
+        o = (options or GpuOptions()).native()
+        if out is None:
+            cap = capacity if capacity is not None else 0
+            out = (np.empty(n + 1, np.int64), np.empty(max(cap, 1), np.int32),
+                   np.empty(max(cap, 1), np.float64), np.empty(max(n, 1), np.float64))
+        cap = capacity if capacity is not None else len(out[1])
+        info = L.parac_gpu_factor_info()
+        _check(lib.parac_gpu_factor_begin(self.handle, seed, C.byref(o)))
+        self._factor_n = -1
+        self._resident = None
+        rc = lib.parac_gpu_factor_end(self.handle, C.byref(info), *[_ptr(a) for a in out], cap)
+        if rc in (0, int(Errc.budget_exceeded)):
+            self._factor_n = info.n
+        _check(rc)
+        return info, out
+
     def download(self, with_stats: bool = True):
         graph, ordering = self._graph
         n = graph.n

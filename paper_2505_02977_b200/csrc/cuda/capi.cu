@@ -588,6 +588,11 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
     sd.published = ctx->stream_ctl.p + 1;
     sd.host = ctx->prog_d;
     sd.ctrl = ctx->ctrl.p;
+    {  // PARAC_STREAM_START=f: the streamer starts once f*n positions are eliminated
+      const char* e = std::getenv("PARAC_STREAM_START");
+      const double f = e ? std::atof(e) : 0.0;
+      sd.start_after = serial ? 0 : static_cast<int>(f * n);
+    }
     cudaStream_t ss = serial ? s : ctx->s_stream;
     if (!serial) check(cudaStreamWaitEvent(ss, ctx->ev[1], 0), "stream wait");
     check(launch_stream_assemble(sd, sctas, ss), "stream assemble launch");

@@ -173,6 +173,7 @@ constexpr int kStreamShift = 11;
 constexpr int kStreamBlock = 1 << kStreamShift;
 struct StreamDev {
   int n, nb;                        // positions, blocks
+  int start_after;                  // begin once K3 has eliminated this many positions
   const int* blk_done;              // [nb] eliminated columns per block (K3)
   const int* col_len;
   const long long* col_start;

@@ -105,6 +105,14 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
   __shared__ long long base_sh;
   __shared__ int blk_sh, ok_sh;
   const int tid = threadIdx.x;
+  if (tid == 0 && s.start_after > 0) {  // stay out of the wide phase's way (it is throughput-bound)
+    unsigned ns = 1024;
+    while (ld_relaxed(&s.ctrl->eliminated) < s.start_after && !aborted(s)) {
+      __nanosleep(ns);
+      if (ns < 8192) ns <<= 1;
+    }
+  }
+  __syncthreads();
   while (true) {
     if (tid == 0) {
       const int b = atomicAdd(s.next_blk, 1);

@@ -438,8 +438,32 @@ def factor_gpu(graph: LaplacianGraph, ordering: Ordering, seed: int,
     t0 = time.perf_counter()
     ctx = ctx or default_context()
     ctx.upload(graph, ordering)
-    info = ctx.factor_resident(seed, options)
-    f, st = ctx.download(with_stats=stats is not None)
+    n = graph.n
+    # the factor is copied out while it is computed (parac_gpu_factor_end):
+    # outputs are sized by a bound on Z -- np.empty only reserves address
+    # space, pages are touched by the copy -- and a factor beyond the bound
+    # is fetched afterwards from the resident copy
+    cap = 4 * graph.nnz_off_diagonal() + n + 1024
+    out = (np.empty(n + 1, np.int64), np.empty(cap, np.int32), np.empty(cap, np.float64),
+           np.empty(max(n, 1), np.float64))
+    info = L.parac_gpu_factor_info()
+    _check(lib.parac_gpu_factor_begin(ctx.handle, seed, C.byref((options or GpuOptions()).native())))
+    ctx._factor_n = -1
+    ctx._resident = None
+    rc = lib.parac_gpu_factor_end(ctx.handle, C.byref(info), *[_ptr(a) for a in out], cap)
+    if rc not in (0, int(Errc.budget_exceeded)):
+        _check(rc)
+    ctx._factor_n = info.n
+    if rc == 0:
+        z = info.nnz_off_diagonal
+        f = LdlFactor(n, out[0], out[1][:z], out[2][:z], out[3][:n], ordering.perm)
+        st = [None] * 3
+        if stats is not None:
+            st = [np.empty(max(n, 1), np.int32) for _ in range(3)]
+            _check(lib.parac_gpu_download(ctx.handle, None, None, None, None, *[_ptr(a) for a in st]))
+            st = [a[:n] for a in st]
+    else:  # a factor beyond the bound: fetch it from the resident copy
+        f, st = ctx.download(with_stats=stats is not None)
     for a in (f.col_ptr, f.rows, f.values, f.diag):
         a.flags.writeable = False
     ctx._resident = f  # the device copy stays resident for solves on this factor

@@ -638,25 +638,31 @@ def measure_batch(args, P, L, torch, rank, world, local, pg, e2e=True):
            "edges_per_gpu": g.num_edges() * len(mine), "launches": launches, "clocks": clk,
            "scaling": "strong", "what": "64 x gen_poisson3d(64) split round-robin over the ranks, "
                                        "one disjoint-union device pass per rank, max-over-ranks device time"}
-    # e2e: parac_gpu_factor_batch from pinned host inputs + download of every factor
+    # e2e: parac_gpu_factor_batch_to_host from pinned host inputs into pinned host outputs
     if e2e:
+        out_arrays = [(C.c_void_p * len(outs))(*[o[j][0] for o in outs]) for j in range(4)]
+        caps = np.array([max(z, 1) for z in zs], np.int64)
         barrier(pg, device)
         e2e_s = []
+        e2e_parts = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize(device)
             t0 = time.perf_counter()
-            check(lib.parac_gpu_factor_batch(ctx.handle, len(mine), csrs, pptr, seeds.ctypes.data, C.byref(opts),
-                                             C.byref(info)))
-            for i, o in enumerate(outs):
-                check(lib.parac_gpu_download_batch(ctx.handle, i, o[0][0], o[1][0], o[2][0], o[3][0]))
+            # upload, factor, and every member copied out while the union is
+            # factored (parac_gpu_factor_batch_to_host: the streamed download)
+            check(lib.parac_gpu_factor_batch_to_host(ctx.handle, len(mine), csrs, pptr, seeds.ctypes.data,
+                                                     C.byref(opts), C.byref(info), *out_arrays, caps.ctypes.data))
             e2e_s.append(time.perf_counter() - t0)
+            e2e_parts.append((info.upload_ms, info.device_ms))
         barrier(pg, device)
         e2e_total = allreduce(pg, device, sum(e2e_s), "MAX")
         h2d = len(mine) * (8 * (g.n + 1) + 12 * 2 * g.num_edges() + 4 * g.n)
         d2h = sum(8 * (g.n + 1) + 12 * z + 8 * g.n for z in zs)
         res["e2e"] = {"value": total_nnz / e2e_total, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3}
+                      "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3,
+                      "upload_wall_ms": sum(u for u, _ in e2e_parts) / len(e2e_parts),
+                      "device_ms": sum(d for _, d in e2e_parts) / len(e2e_parts)}
     else:  # outputs of the last resident pass
         for i, o in enumerate(outs):
             check(lib.parac_gpu_download_batch(ctx.handle, i, o[0][0], o[1][0], o[2][0], o[3][0]))

@@ -249,6 +249,20 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
 int parac_gpu_factor_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
                            const int32_t* const* perms, const uint64_t* seeds, const parac_gpu_options* opt,
                            parac_gpu_factor_info* info);
+/* The batch counterpart of parac_gpu_factor_end (after parac_gpu_upload_batch +
+ * parac_gpu_factor_begin): every member's LdlFactor arrays, in its own position
+ * space, copied out while the union is factored. Arrays of `count` pointers
+ * (any array or entry may be NULL); capacities[i] = entries of rows[i] /
+ * values[i]. PARAC_BUDGET_EXCEEDED when a member's Z exceeds its capacity
+ * (the factor stays resident: parac_gpu_batch_nnz + parac_gpu_download_batch). */
+int parac_gpu_factor_batch_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* const* col_ptrs,
+                               int32_t* const* rows, double* const* values, double* const* diags,
+                               const int64_t* capacities);
+/* upload_batch + factor_begin + factor_batch_end. */
+int parac_gpu_factor_batch_to_host(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                                   const int32_t* const* perms, const uint64_t* seeds, const parac_gpu_options* opt,
+                                   parac_gpu_factor_info* info, int64_t* const* col_ptrs, int32_t* const* rows,
+                                   double* const* values, double* const* diags, const int64_t* capacities);
 /* Off-diagonal count of problem i's factor (size its rows/values buffers). */
 int parac_gpu_batch_nnz(parac_gpu_ctx* ctx, int32_t i, int64_t* nnz_off);
 /* Problem i's LdlFactor arrays, in its own position space. */

@@ -94,6 +94,9 @@ SIGNATURES = {
     "parac_gpu_upload_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp]),
     "parac_gpu_factor_batch": (C.c_int, [vp, i32, P(parac_csr), vp, vp, P(parac_gpu_options),
                                          P(parac_gpu_factor_info)]),
+    "parac_gpu_factor_batch_end": (C.c_int, [vp, P(parac_gpu_factor_info), vp, vp, vp, vp, vp]),
+    "parac_gpu_factor_batch_to_host": (C.c_int, [vp, i32, P(parac_csr), vp, vp, P(parac_gpu_options),
+                                                 P(parac_gpu_factor_info), vp, vp, vp, vp, vp]),
     "parac_gpu_batch_nnz": (C.c_int, [vp, i32, P(i64)]),
     "parac_gpu_download_batch": (C.c_int, [vp, i32, vp, vp, vp, vp]),
     "parac_gpu_upload_factor": (C.c_int, [vp, i32, vp, vp, vp, vp, vp]),

@@ -300,8 +300,12 @@ struct parac_gpu_ctx {
   DevBuf<int> blk_done, stream_ctl;
   DevBuf<unsigned long long> blk_incl;
   cudaStream_t s_stream = nullptr, s_copy = nullptr;
-  unsigned long long* prog_h = nullptr;
-  unsigned long long* prog_d = nullptr;
+  unsigned long long* blkh_h = nullptr;  // [blkh_cap] per-block release words (host view)
+  unsigned long long* blkh_d = nullptr;  // (device view)
+  std::size_t blkh_cap = 0;
+  // batch: streamer blocks that never straddle problems (positions, nb+1)
+  std::vector<int> blk_k0_h;
+  DevBuf<int> blk_k0;
   // a factorization launched by parac_gpu_factor_begin, completed by _end
   bool pending = false;
   std::uint64_t p_seed = 0;
@@ -363,7 +367,14 @@ int stream_ctas() {
 bool stream_wanted(const parac_gpu_ctx* ctx) {
   const char* e = std::getenv("PARAC_STREAM");
   const int m = e ? std::atoi(e) : 1;
-  return (m == 1 || m == 3) && ctx->batch_count == 0 && ctx->n > 0;
+  // Batches assemble after K3 unless PARAC_STREAM_BATCH=1: with the union's
+  // global CSC layout, member p's offsets wait for every earlier member's
+  // last (latest) columns, so blocks release only near K3's end while the
+  // streamer's slots slow the throughput-bound batch K3 (64 x 64^3: device
+  // 68.5 -> 77 ms, e2e 159 -> 154 ms measured)
+  const char* eb = std::getenv("PARAC_STREAM_BATCH");
+  if (ctx->batch_count > 0 && !(eb && std::atoi(eb) == 1)) return false;
+  return (m == 1 || m == 3) && ctx->n > 0;
 }
 // PARAC_STREAM=3 (diagnostics): the streamer runs after K3 on K3's stream --
 // its throughput alone
@@ -380,14 +391,21 @@ bool stream_count_only() {
 void ensure_stream_resources(parac_gpu_ctx* ctx) {
   if (!ctx->s_stream) check(cudaStreamCreateWithFlags(&ctx->s_stream, cudaStreamNonBlocking), "stream");
   if (!ctx->s_copy) check(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking), "stream");
-  if (!ctx->prog_h) {
-    void* h = nullptr;
-    check(cudaHostAlloc(&h, 64, cudaHostAllocMapped), "cudaHostAlloc (progress word)");
-    ctx->prog_h = static_cast<unsigned long long*>(h);
-    void* dp = nullptr;
-    check(cudaHostGetDevicePointer(&dp, h, 0), "cudaHostGetDevicePointer");
-    ctx->prog_d = static_cast<unsigned long long*>(dp);
-  }
+}
+
+// The streamer's per-block release words (mapped pinned), nblk of them.
+void ensure_release_words(parac_gpu_ctx* ctx, std::size_t nblk) {
+  if (nblk <= ctx->blkh_cap) return;
+  if (ctx->blkh_h) cudaFreeHost(ctx->blkh_h);
+  ctx->blkh_h = nullptr;
+  ctx->blkh_cap = 0;
+  void* h = nullptr;
+  check(cudaHostAlloc(&h, sizeof(unsigned long long) * nblk, cudaHostAllocMapped), "cudaHostAlloc (release words)");
+  ctx->blkh_h = static_cast<unsigned long long*>(h);
+  void* dp = nullptr;
+  check(cudaHostGetDevicePointer(&dp, h, 0), "cudaHostGetDevicePointer");
+  ctx->blkh_d = static_cast<unsigned long long*>(dp);
+  ctx->blkh_cap = nblk;
 }
 
 // Launch half of one attempt of the factorization with the given budgets
@@ -546,17 +564,21 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
   if (count) {
     ensure_stream_resources(ctx);
     const std::size_t nb = static_cast<std::size_t>((n + kStreamBlock - 1) >> kStreamShift);
+    const std::size_t nblk = ctx->batch_count > 0 ? ctx->blk_k0_h.size() - 1 : nb;
     ctx->blk_done.ensure(nb);
-    ctx->blk_incl.ensure(nb);
+    ctx->blk_incl.ensure(std::max<std::size_t>(nblk, 1));
     ctx->stream_ctl.ensure(2);
-    *static_cast<volatile unsigned long long*>(ctx->prog_h) = 0;  // no stream work of an earlier attempt is in flight
+    ensure_release_words(ctx, std::max<std::size_t>(nblk, 1));
+    // no stream work of an earlier attempt is in flight
+    std::memset(ctx->blkh_h, 0, sizeof(unsigned long long) * std::max<std::size_t>(nblk, 1));
     d.blk_done = ctx->blk_done.p;
   }
   check(cudaEventRecord(ctx->ev[0], s), "event");
   if (count) {
     const std::size_t nb = static_cast<std::size_t>((n + kStreamBlock - 1) >> kStreamShift);
     check(cudaMemsetAsync(ctx->blk_done.p, 0, nb * sizeof(int), s), "memset");
-    check(cudaMemsetAsync(ctx->blk_incl.p, 0, nb * sizeof(unsigned long long), s), "memset");
+    const std::size_t nblk = ctx->batch_count > 0 ? ctx->blk_k0_h.size() - 1 : nb;
+    check(cudaMemsetAsync(ctx->blk_incl.p, 0, std::max<std::size_t>(nblk, 1) * sizeof(unsigned long long), s), "memset");
     check(cudaMemsetAsync(ctx->stream_ctl.p, 0, 2 * sizeof(int), s), "memset");
   }
   check(cudaMemsetAsync(ctx->inv.p, 0xff, nn * sizeof(int), s), "memset");
@@ -574,7 +596,11 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
   if (ctx->streaming) {  // the assembly beside K3, on its own stream (after K1/K2)
     StreamDev sd{};
     sd.n = n;
-    sd.nb = (n + kStreamBlock - 1) >> kStreamShift;
+    const bool batch = ctx->batch_count > 0;
+    sd.nb = batch ? static_cast<int>(ctx->blk_k0_h.size()) - 1 : (n + kStreamBlock - 1) >> kStreamShift;
+    sd.blk_k0 = batch ? ctx->blk_k0.p : nullptr;
+    sd.pos_pid = batch ? ctx->pos_pid.p : nullptr;
+    sd.pid_base = batch ? ctx->pid_base.p : nullptr;
     sd.blk_done = ctx->blk_done.p;
     sd.col_len = ctx->col_len.p;
     sd.col_start = ctx->col_start.p;
@@ -585,8 +611,7 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
     sd.vals = ctx->vals.p;
     sd.blk_incl = ctx->blk_incl.p;
     sd.next_blk = ctx->stream_ctl.p;
-    sd.published = ctx->stream_ctl.p + 1;
-    sd.host = ctx->prog_d;
+    sd.host_blk = ctx->blkh_d;
     sd.ctrl = ctx->ctrl.p;
     {  // PARAC_STREAM_START=f: the streamer starts once f*n positions are eliminated
       const char* e = std::getenv("PARAC_STREAM_START");
@@ -634,13 +659,14 @@ void copy_range(parac_gpu_ctx* ctx, void* dst, const void* src, std::size_t byte
 void stream_download(parac_gpu_ctx* ctx, const HostOut& out) {
   const int n = ctx->n;
   const int nb = (n + kStreamBlock - 1) >> kStreamShift;
-  volatile unsigned long long* prog = ctx->prog_h;
+  volatile unsigned long long* rel = ctx->blkh_h;
   const long long kMinEntries = 1 << 19;  // ~6 MB of rows+values per round of copies
-  int done_b = 0;
+  int done_b = 0, seen_b = 0;
   long long done_z = 0;
-  auto take = [&](unsigned long long w) {
-    const int pb = static_cast<int>(w & 0xffffffu);
-    const long long pz = static_cast<long long>(w >> 24);
+  auto take = [&](int) {
+    while (seen_b < nb && (rel[seen_b] >> 63)) ++seen_b;  // the contiguous released prefix
+    const int pb = seen_b;
+    const long long pz = pb > 0 ? static_cast<long long>(rel[pb - 1] & ~(1ull << 63)) : 0;
     if (pb <= done_b || (pb < nb && pz - done_z < kMinEntries)) return;
     const long long p0 = static_cast<long long>(done_b) << kStreamShift;
     const long long p1 = std::min<long long>(static_cast<long long>(pb) << kStreamShift, n);
@@ -657,10 +683,10 @@ void stream_download(parac_gpu_ctx* ctx, const HostOut& out) {
     done_z = pz;
   };
   while (done_b < nb) {
-    take(*prog);
+    take(0);
     if (done_b == nb) break;
-    if (cudaEventQuery(ctx->ev[3]) == cudaSuccess) {  // device work over: the last word is final
-      take(*prog);
+    if (cudaEventQuery(ctx->ev[3]) == cudaSuccess) {  // device work over: the words are final
+      take(0);
       break;
     }
     std::this_thread::yield();
@@ -668,13 +694,120 @@ void stream_download(parac_gpu_ctx* ctx, const HostOut& out) {
   check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
 }
 
-// Completion half: the streamed download (when out is given and the attempt
-// streams), then the status. Returns status.
-int complete_factor(parac_gpu_ctx* ctx, const parac_gpu_options& o, const Budgets& b, const HostOut* out) {
+// Per-problem outputs of a batch (each array: problem i's buffer, or null).
+struct BatchOut {
+  std::int64_t* const* col_ptr;
+  std::int32_t* const* rows;
+  double* const* values;
+  double* const* diag;
+  const std::int64_t* caps;
+  bool short_cap = false;  // some problem's factor exceeded its capacity
+};
+
+// The batch download beside the elimination. Blocks never straddle problems
+// (upload_batch), so each released range of positions / entries splits into
+// per-problem pieces: positions by the staged problem offsets, entries by
+// each problem's first entry offset (the release word of the block before
+// its first block). A problem's col_ptr is made local
+// (minus its first entry offset) once all its blocks are copied.
+void stream_download_batch(parac_gpu_ctx* ctx, BatchOut& out) {
+  const int count = ctx->batch_count;
+  const std::vector<long long>& base = ctx->batch_base_h;
+  const std::vector<int>& bk = ctx->blk_k0_h;
+  const int nb = static_cast<int>(bk.size()) - 1;
+  volatile unsigned long long* rel = ctx->blkh_h;
+  constexpr unsigned long long kRel = 1ull << 63;
+  std::vector<int> first(count, -1), last(count, -1);
+  for (int b = 0, p = 0; b < nb; ++b) {
+    while (bk[b] >= base[p + 1]) ++p;
+    if (first[p] < 0) first[p] = b;
+    last[p] = b;
+  }
+  std::vector<int> ne;  // problems with vertices, in order
+  for (int p = 0; p < count; ++p)
+    if (base[p + 1] > base[p]) ne.push_back(p);
+  const long long kMinEntries = 1 << 19;
+  int done_b = 0;
+  long long done_z = 0;
+  std::size_t qi = 0, rebased = 0;
+  int seen_b = 0;
+  // a problem's first entry offset: the release word of the block before its first
+  auto zstart = [&](int p) -> long long {
+    return first[p] > 0 ? static_cast<long long>(rel[first[p] - 1] & ~kRel) : 0;
+  };
+  auto rebase_ready = [&](int pb) {
+    std::size_t r = rebased;
+    while (r < ne.size() && last[ne[r]] < pb) ++r;
+    if (r == rebased) return;
+    check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
+    for (; rebased < r; ++rebased) {
+      const int p = ne[rebased];
+      std::int64_t* cp = out.col_ptr ? out.col_ptr[p] : nullptr;
+      if (!cp) continue;
+      const long long z0 = zstart(p);
+      for (long long k = 0, m = base[p + 1] - base[p]; k <= m; ++k) cp[k] -= z0;
+    }
+  };
+  auto take = [&](int) {
+    while (seen_b < nb && (rel[seen_b] & kRel)) ++seen_b;
+    const int pb = seen_b;
+    const long long pz = pb > 0 ? static_cast<long long>(rel[pb - 1] & ~kRel) : 0;
+    if (pb <= done_b || (pb < nb && pz - done_z < kMinEntries)) return;
+    const long long P0 = bk[done_b], P1 = bk[pb];
+    for (int p = 0; p < count; ++p) {  // positions [P0, P1], P1 = the last block's end (col_ptr only)
+      // (a problem ending at P0 was completed -- and rebased -- last round)
+      if (base[p + 1] <= P0 || base[p] > P1) continue;
+      const long long lo = std::max(P0, base[p]), hi = std::min(P1, base[p + 1]);
+      if (out.col_ptr && out.col_ptr[p])
+        copy_range(ctx, out.col_ptr[p] + (lo - base[p]), ctx->col_ptr.p + lo, sizeof(long long) * (hi - lo + 1));
+      if (hi > lo && out.diag && out.diag[p])
+        copy_range(ctx, out.diag[p] + (lo - base[p]), ctx->diag.p + lo, sizeof(double) * (hi - lo));
+    }
+    while (done_z < pz && qi < ne.size()) {  // entries [done_z, pz), problem by problem
+      const int p = ne[qi];
+      const long long z0 = zstart(p);
+      const bool next_known = qi + 1 < ne.size() && first[ne[qi + 1]] < pb;
+      const long long zend = next_known ? zstart(ne[qi + 1]) : pz;
+      const long long e1 = std::min(zend, pz);
+      const long long cap = out.caps ? out.caps[p] : 0;
+      const long long c1 = std::min(e1, z0 + cap);
+      if (c1 > done_z) {
+        if (out.rows && out.rows[p])
+          copy_range(ctx, out.rows[p] + (done_z - z0), ctx->rows.p + done_z, sizeof(int) * (c1 - done_z));
+        if (out.values && out.values[p])
+          copy_range(ctx, out.values[p] + (done_z - z0), ctx->vals.p + done_z, sizeof(double) * (c1 - done_z));
+      }
+      if (e1 > z0 + cap) out.short_cap = true;
+      done_z = e1;
+      if (next_known && e1 == zend) ++qi;
+      else break;
+    }
+    done_b = pb;
+    rebase_ready(pb);
+  };
+  while (done_b < nb) {
+    take(0);
+    if (done_b == nb) break;
+    if (cudaEventQuery(ctx->ev[3]) == cudaSuccess) {
+      take(0);
+      break;
+    }
+    std::this_thread::yield();
+  }
+  check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
+  for (int p = 0; p < count; ++p)  // problems without vertices: col_ptr = {0}
+    if (base[p + 1] == base[p] && out.col_ptr && out.col_ptr[p]) out.col_ptr[p][0] = 0;
+}
+
+// Completion half: the streamed download (when outputs are given and the
+// attempt streams), then the status. Returns status.
+int complete_factor(parac_gpu_ctx* ctx, const parac_gpu_options& o, const Budgets& b, const HostOut* out,
+                    BatchOut* bout = nullptr) {
   const int n = ctx->n;
   cudaStream_t s = ctx->stream;
   const double wd = o.watchdog_seconds > 0 ? o.watchdog_seconds : 60.0;
   if (out && ctx->streaming) stream_download(ctx, *out);
+  if (bout && ctx->streaming) stream_download_batch(ctx, *bout);
   Ctrl c{};
   long long z = 0;
   check(cudaMemcpyAsync(&c, ctx->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s), "ctrl copy");
@@ -774,7 +907,8 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
   if (ctx->s_stream) cudaStreamSynchronize(ctx->s_stream);
   if (ctx->s_copy) cudaStreamSynchronize(ctx->s_copy);
   ctx->blk_done.release(); ctx->stream_ctl.release(); ctx->blk_incl.release();
-  if (ctx->prog_h) cudaFreeHost(ctx->prog_h);
+  if (ctx->blkh_h) cudaFreeHost(ctx->blkh_h);
+  ctx->blk_k0.release();
   if (ctx->s_stream) cudaStreamDestroy(ctx->s_stream);
   if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
   for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -855,17 +989,44 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     solve_invalidate(ctx->solve);
     // every member's ordering must be a permutation of its own [0, n_i): the
     // union check on the device cannot tell a valid union of invalid members
+    long long total_n = 0;
     for (int i = 0; i < count; ++i) {
       const int ni = graphs[i].n;
       if (ni < 0 || !graphs[i].ptr || (ni > 0 && !perms[i])) throw Failure{dimension_mismatch, "bad graph in batch"};
-      std::vector<unsigned char> seen(static_cast<std::size_t>(ni), 0);
-      for (int v = 0; v < ni; ++v) {
-        const int q = perms[i][v];
-        if (q < 0 || q >= ni || seen[q])
-          throw Failure{not_a_permutation, "ordering of batch problem " + std::to_string(i) +
-                                               " is not a permutation (vertex " + std::to_string(v) + ")"};
-        seen[q] = 1;
+      total_n += ni;
+    }
+    {  // members checked side by side on host threads; the lowest failing member is reported
+      std::vector<int> bad_v(static_cast<std::size_t>(count), -1);
+      auto check_member = [&](int i) {
+        const int ni = graphs[i].n;
+        std::vector<unsigned char> seen(static_cast<std::size_t>(ni), 0);
+        for (int v = 0; v < ni; ++v) {
+          const int q = perms[i][v];
+          if (q < 0 || q >= ni || seen[q]) {
+            bad_v[i] = v;
+            return;
+          }
+          seen[q] = 1;
+        }
+      };
+      const int nt = total_n >= (1 << 20)
+                         ? static_cast<int>(std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u))
+                         : 1;
+      if (nt <= 1 || count == 1) {
+        for (int i = 0; i < count; ++i) check_member(i);
+      } else {
+        std::atomic<int> next{0};
+        std::vector<std::thread> th;
+        for (int t = 0; t < std::min(nt, count); ++t)
+          th.emplace_back([&] {
+            for (int i; (i = next.fetch_add(1)) < count;) check_member(i);
+          });
+        for (auto& t : th) t.join();
       }
+      for (int i = 0; i < count; ++i)
+        if (bad_v[i] >= 0)
+          throw Failure{not_a_permutation, "ordering of batch problem " + std::to_string(i) +
+                                               " is not a permutation (vertex " + std::to_string(bad_v[i]) + ")"};
     }
     long long N = 0, NNZ = 0;
     std::vector<long long> base(static_cast<std::size_t>(count) + 1, 0), ebase(base);
@@ -922,6 +1083,14 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     solve_invalidate(ctx->solve);
     ctx->batch_count = count;
     ctx->batch_base_h = base;
+    // streamer blocks (stream_assemble.cu): up to kStreamBlock positions, never across problems
+    ctx->blk_k0_h.clear();
+    for (int i = 0; i < count; ++i)
+      for (long long k = base[i]; k < base[i + 1]; k += kStreamBlock) ctx->blk_k0_h.push_back(static_cast<int>(k));
+    ctx->blk_k0_h.push_back(static_cast<int>(N));
+    ctx->blk_k0.ensure(ctx->blk_k0_h.size());
+    check(cudaMemcpy(ctx->blk_k0.p, ctx->blk_k0_h.data(), sizeof(int) * ctx->blk_k0_h.size(), cudaMemcpyHostToDevice),
+          "h2d");
   });
 }
 
@@ -995,14 +1164,23 @@ int parac_gpu_factor_begin(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_op
   });
 }
 
-int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* col_ptr, int32_t* rows,
-                         double* values, double* diag, int64_t capacity) {
+}  // extern "C"
+
+namespace {
+// parac_gpu_factor_end / parac_gpu_factor_batch_end: one problem's outputs
+// (hout) or every batch member's (bout), either may be null.
+int factor_end_impl(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, const HostOut* hout, BatchOut* bout) {
   int rc = guarded([&] {
     require_ctx(ctx);
     if (!ctx->pending) throw Failure{internal_error, "no factorization pending (call parac_gpu_factor_begin)"};
   });
   if (rc) return rc;
-  const HostOut out{col_ptr, rows, values, diag, capacity};
+  const HostOut out = hout ? *hout : HostOut{nullptr, nullptr, nullptr, nullptr, 0};
+  int64_t* const col_ptr = out.col_ptr;
+  int32_t* const rows = out.rows;
+  double* const values = out.values;
+  double* const diag = out.diag;
+  const long long capacity = out.cap;
   const bool want = col_ptr || rows || values || diag;
   const parac_gpu_options& o = ctx->p_opt;
   Budgets& b = ctx->p_b;
@@ -1010,7 +1188,7 @@ int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_
   const long long E = ctx->nnz / 2;
   for (;;) {
     int st = 0;
-    rc = guarded([&] { st = complete_factor(ctx, o, b, want ? &out : nullptr); });
+    rc = guarded([&] { st = complete_factor(ctx, o, b, want ? &out : nullptr, bout); });
     if (rc) {
       ctx->pending = false;
       return rc;
@@ -1055,7 +1233,7 @@ int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_
     ctx->f_nnz = Z;
     ctx->f_has_stats = true;
     ctx->f_external = false;
-    if (ctx->batch_count > 0) {  // each problem's rows in its own position space
+    if (ctx->batch_count > 0 && !ctx->streaming) {  // each problem's rows in its own position space (the streamer did it)
       check(launch_batch_local_rows(n, ctx->col_ptr.p, ctx->pos_pid.p, ctx->pid_base.p, ctx->rows.p, ctx->stream),
             "batch rows");
       check(cudaStreamSynchronize(ctx->stream), "batch rows sync");
@@ -1094,7 +1272,93 @@ int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_
       if (diag && n) ctx->stage.d2h(diag, ctx->diag.p, sizeof(double) * n, ctx->stream);
       check(cudaStreamSynchronize(ctx->stream), "d2h sync");
     }
+    if (bout && !ctx->streaming) {  // the assembly ran after K3: every member's copies in flight at once
+      ensure_stream_resources(ctx);
+      const int count = ctx->batch_count;
+      const std::vector<long long>& base = ctx->batch_base_h;
+      std::vector<long long> zb(static_cast<std::size_t>(count) + 1);
+      for (int i = 0; i <= count; ++i)  // each member's first entry offset (and the total)
+        check(cudaMemcpyAsync(&zb[i], ctx->col_ptr.p + base[i], sizeof(long long), cudaMemcpyDeviceToHost, ctx->s_copy),
+              "d2h");
+      check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
+      for (int i = 0; i < count; ++i) {
+        const long long z0 = zb[i], z = zb[i + 1] - z0, m = base[i + 1] - base[i];
+        const bool fits = !bout->caps || z <= bout->caps[i];
+        if (!fits) bout->short_cap = true;
+        if (bout->col_ptr && bout->col_ptr[i])
+          copy_range(ctx, bout->col_ptr[i], ctx->col_ptr.p + base[i], sizeof(long long) * (m + 1));
+        if (fits && bout->rows && bout->rows[i]) copy_range(ctx, bout->rows[i], ctx->rows.p + z0, sizeof(int) * z);
+        if (fits && bout->values && bout->values[i])
+          copy_range(ctx, bout->values[i], ctx->vals.p + z0, sizeof(double) * z);
+        if (bout->diag && bout->diag[i]) copy_range(ctx, bout->diag[i], ctx->diag.p + base[i], sizeof(double) * m);
+      }
+      check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
+      if (bout->col_ptr) {  // local column pointers (rows were made local on the device), members on threads
+        std::atomic<int> next{0};
+        auto work = [&] {
+          for (int i; (i = next.fetch_add(1)) < count;) {
+            std::int64_t* cp = bout->col_ptr[i];
+            if (!cp) continue;
+            for (long long k = 0, m = base[i + 1] - base[i]; k <= m; ++k) cp[k] -= zb[i];
+          }
+        };
+        const int nt = static_cast<int>(std::min<long long>(std::min(count, 8), std::max<long long>(1, ctx->n >> 20)));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto& t : th) t.join();
+      }
+    }
+    if (bout && bout->short_cap)
+      throw Failure{budget_exceeded, "a batch member's factor exceeds its output capacity (the factor stays "
+                                     "resident: parac_gpu_batch_nnz + parac_gpu_download_batch)"};
   });
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* col_ptr, int32_t* rows,
+                         double* values, double* diag, int64_t capacity) {
+  const bool want = col_ptr || rows || values || diag;
+  if (want && ctx && ctx->batch_count > 0) {
+    const int rc = factor_end_impl(ctx, info, nullptr, nullptr);  // complete it; the outputs do not apply
+    if (rc) return rc;
+    return guarded([] { throw Failure{dimension_mismatch, "a batch is staged: use parac_gpu_factor_batch_end"}; });
+  }
+  const HostOut out{col_ptr, rows, values, diag, capacity};
+  return factor_end_impl(ctx, info, &out, nullptr);
+}
+
+int parac_gpu_factor_batch_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* const* col_ptrs,
+                               int32_t* const* rows, double* const* values, double* const* diags,
+                               const int64_t* capacities) {
+  if (ctx && ctx->pending && ctx->batch_count <= 0) {
+    const int rc = factor_end_impl(ctx, info, nullptr, nullptr);
+    if (rc) return rc;
+    return guarded([] { throw Failure{dimension_mismatch, "no batch staged: use parac_gpu_factor_end"}; });
+  }
+  BatchOut out{col_ptrs, rows, values, diags, capacities};
+  const bool want = col_ptrs || rows || values || diags;
+  return factor_end_impl(ctx, info, nullptr, want ? &out : nullptr);
+}
+
+int parac_gpu_factor_batch_to_host(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
+                                   const int32_t* const* perms, const uint64_t* seeds, const parac_gpu_options* opt,
+                                   parac_gpu_factor_info* info, int64_t* const* col_ptrs, int32_t* const* rows,
+                                   double* const* values, double* const* diags, const int64_t* capacities) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = parac_gpu_upload_batch(ctx, count, graphs, perms, seeds);
+  if (rc) return rc;
+  const double up = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  rc = parac_gpu_factor_begin(ctx, 0, opt);
+  if (rc) return rc;
+  rc = parac_gpu_factor_batch_end(ctx, info, col_ptrs, rows, values, diags, capacities);
+  if (info && (rc == 0 || rc == budget_exceeded)) {
+    info->upload_ms = up;
+    info->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   return rc;
 }
 

@@ -182,11 +182,16 @@ struct StreamDev {
   long long* col_ptr;               // the resident CSC factor (as launch_assemble writes it)
   int* rows;
   double* vals;
-  unsigned long long* blk_incl;     // [nb] inclusive entry offset | bit 63 (chained prefix)
+  unsigned long long* blk_incl;     // [nb] block total | bit 62, then inclusive entry offset | bit 63
   int* next_blk;                    // block claim counter
-  int* published;                   // blocks released to the host, in order
-  unsigned long long* host;         // mapped pinned progress word (entries << 24 | blocks), or nullptr
+  unsigned long long* host_blk;     // [nb] mapped pinned: inclusive entry end | bit 63 once released
   Ctrl* ctrl;                       // status (K3 aborted), eliminated
+  // batch (disjoint union): blocks never straddle problems -- block b is
+  // positions [blk_k0[b], blk_k0[b+1]) (nullptr: b * kStreamBlock); rows are
+  // made local to their problem (pos_pid / pid_base)
+  const int* blk_k0;
+  const int* pos_pid;
+  const long long* pid_base;
 };
 cudaError_t launch_stream_assemble(const StreamDev& s, int ctas, cudaStream_t st);
 cudaError_t launch_sum_samples(const FactorDev& d, cudaStream_t s);

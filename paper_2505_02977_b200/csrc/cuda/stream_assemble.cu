@@ -7,8 +7,8 @@
 // at 128^3, 88% of the factor's entries sit below the lowest not-yet-
 // eliminated position 6 ms into the 20 ms elimination, 98% at 10 ms
 // (tools/watermark.py). The streamer copies those columns while K3 still runs
-// and tells the host, through a word in mapped pinned memory, how much of
-// the output is final, so the device->host copy overlaps the elimination too.
+// and tells the host, through per-block words in mapped pinned memory, how
+// much of the output is final, so the device->host copy overlaps the elimination too.
 //
 // Positions are cut into blocks of kStreamBlock. K3 counts each block's
 // eliminated columns (FactorDev::blk_done, one relaxed red per column after
@@ -16,12 +16,13 @@
 // blocks in ascending order; for each block:
 //   1. wait until all its columns are eliminated (acquire);
 //   2. exclusive scan of the column lengths in shared memory;
-//   3. chained prefix across blocks (blk_incl[b] = inclusive entry offset,
-//      flag bit 63), so block b's base offset is known once b-1 published;
+//   3. block offsets by decoupled look-back (blk_incl[b] = the block's total,
+//      then its inclusive entry offset, flagged): no serial chain per block;
 //   4. col_ptr for the block, then every entry copied arena -> rows/vals,
 //      a warp per group of 32 columns, lanes 32 entries apart (coalesced);
-//   5. in block order: release the block to the host (system-scope fence,
-//      then the packed progress word (entries << 24 | blocks)).
+//   5. release the block to the host: system-scope fence, then its flagged
+//      inclusive entry end in mapped memory (host_blk[b]); the host advances
+//      over the contiguous prefix of released blocks.
 // The result is bit-identical to launch_assemble's (same offsets, same
 // copies). An abort of K3 (Ctrl::status != 0) ends the streamer.
 #include "common.cuh"
@@ -64,7 +65,9 @@ __device__ __forceinline__ long long cta_exclusive_scan(long long v, long long* 
   return before + x - v;
 }
 constexpr int kPer = kStreamBlock / kStreamThreads;
-constexpr unsigned long long kFlag = 1ull << 63;
+constexpr unsigned long long kFlag = 1ull << 63;  // blk_incl: inclusive prefix
+constexpr unsigned long long kAgg = 1ull << 62;   // blk_incl: the block's own total only
+constexpr unsigned long long kVal = kAgg - 1;
 constexpr int kStreamErrInternal = 17;  // Errc::internal_error
 
 __device__ __forceinline__ void st_relaxed_u64g(unsigned long long* p, unsigned long long v) {
@@ -117,13 +120,23 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
     if (tid == 0) {
       const int b = atomicAdd(s.next_blk, 1);
       blk_sh = b;
-      ok_sh = b < s.nb && wait_geq(s, &s.blk_done[b], min(kStreamBlock, s.n - b * kStreamBlock));
+      bool ok = b < s.nb;
+      if (ok) {  // every K3 counter bucket the block touches is complete
+        const int a0 = s.blk_k0 ? s.blk_k0[b] : b * kStreamBlock;
+        const int a1 = s.blk_k0 ? s.blk_k0[b + 1] : min(a0 + kStreamBlock, s.n);
+        for (int j = a0 >> kStreamShift; ok && j <= (a1 - 1) >> kStreamShift; ++j)
+          ok = wait_geq(s, &s.blk_done[j], min(kStreamBlock, s.n - j * kStreamBlock));
+      }
+      ok_sh = ok;
     }
     __syncthreads();
     if (!ok_sh) return;
     const int b = blk_sh;
-    const int k0 = b * kStreamBlock;
-    const int cnt = min(kStreamBlock, s.n - k0);
+    const int k0 = s.blk_k0 ? s.blk_k0[b] : b * kStreamBlock;
+    const int cnt = (s.blk_k0 ? s.blk_k0[b + 1] : min(k0 + kStreamBlock, s.n)) - k0;
+    // batch: the block's problem (rows made local to it)
+    const int pid = s.pos_pid ? s.pos_pid[k0] : 0;
+    const int row_base = s.pos_pid ? static_cast<int>(s.pid_base[pid]) : 0;
     fence_acq_rel();  // acquire: the block's columns (published before their counts)
 
     // 2. local offsets
@@ -154,17 +167,21 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
     // 3. chained prefix (block b-1 was claimed earlier by a running CTA)
     if (tid == 0) {
       loc[kStreamBlock] = tot;
+      // decoupled look-back: publish this block's aggregate at once, then sum
+      // predecessors' aggregates back to the first inclusive prefix
+      if (b > 0) st_relaxed_u64g(&s.blk_incl[b], kAgg | static_cast<unsigned long long>(tot));
       long long bs = 0;
       bool ok = true;
-      if (b > 0) {
-        unsigned long long w;
-        unsigned ns = 32;
-        while (!((w = ld_relaxed_u64(&s.blk_incl[b - 1])) & kFlag)) {
+      for (int j = b - 1; j >= 0;) {
+        const unsigned long long w = ld_relaxed_u64(&s.blk_incl[j]);
+        if (!(w & (kFlag | kAgg))) {
           if (aborted(s)) { ok = false; break; }
-          __nanosleep(ns);
-          if (ns < 1024) ns <<= 1;
+          __nanosleep(32);
+          continue;
         }
-        bs = static_cast<long long>(w & ~kFlag);
+        bs += static_cast<long long>(w & kVal);
+        if (w & kFlag) break;
+        --j;
       }
       if (ok) st_relaxed_u64g(&s.blk_incl[b], kFlag | static_cast<unsigned long long>(bs + tot));
       base_sh = bs;
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
 
     // 4. col_ptr and the entries
     for (int i = tid; i < cnt; i += kStreamThreads) s.col_ptr[k0 + i] = bs + loc[i];
-    if (tid == 0 && k0 + cnt == s.n) s.col_ptr[s.n] = bs + tot;
+    if (tid == 0) s.col_ptr[k0 + cnt] = bs + tot;  // the next block writes the same value
     // Each warp copies groups of 32 consecutive columns (group g: columns
     // [32g, 32g + 32), warps take groups round robin). Lanes walk the group's
     // entries 32 apart (coalesced); an entry's column comes from a 5-step
@@ -215,25 +232,21 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
         for (int u = 0; u < U; ++u) {
           const long long e = e0 + u * 32 + lane;
           if (e < T) {
-            __stcs(s.rows + bs + g0 + e, r[u]);
+            __stcs(s.rows + bs + g0 + e, r[u] - row_base);
             __stcs(s.vals + bs + g0 + e, x[u]);
           }
         }
       }
     }
 
-    // 5. release to the host, in block order
-    if (s.host) {
+    // 5. release to the host: the block's inclusive entry end, flagged, in
+    // mapped memory (the host finds the contiguous prefix itself)
+    if (s.host_blk) {
       __threadfence();
       __syncthreads();
       if (tid == 0) {
-        __threadfence_system();  // this block's stores, before its turn (not on the in-order chain)
-        const bool ok = wait_geq(s, s.published, b);
-        if (ok) {
-          st_sys_u64(s.host, (static_cast<unsigned long long>(bs + tot) << 24) | static_cast<unsigned>(b + 1));
-          st_release(s.published, b + 1);
-        }
-        ok_sh = ok;
+        __threadfence_system();
+        st_sys_u64(s.host_blk + b, kFlag | static_cast<unsigned long long>(bs + tot));
       }
     }
     __syncthreads();

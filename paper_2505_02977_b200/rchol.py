@@ -509,21 +509,31 @@ def factor_batch_gpu(graphs: Sequence[LaplacianGraph], orderings: Sequence[Order
     csrs, perms, sd, keep = _batch_args(graphs, orderings, seeds)
     o = (options or GpuOptions()).native()
     info = L.parac_gpu_factor_info()
-    _check(lib.parac_gpu_factor_batch(ctx.handle, len(graphs), csrs, perms, _ptr(sd), C.byref(o),
-                                      C.byref(info)))
+    k = len(graphs)
+    # every member copied out while the union is factored
+    # (parac_gpu_factor_batch_to_host); rows/values sized by a bound on each
+    # member's Z (address space only), a larger member fetched afterwards
+    caps = np.array([4 * g.nnz_off_diagonal() + g.n + 1024 for g in graphs], np.int64)
+    bufs = [(np.empty(g.n + 1, np.int64), np.empty(int(c), np.int32), np.empty(int(c), np.float64),
+             np.empty(max(g.n, 1), np.float64)) for g, c in zip(graphs, caps)]
+    arr = [(C.c_void_p * k)(*[_ptr(b[j]) for b in bufs]) for j in range(4)]
+    rc = lib.parac_gpu_factor_batch_to_host(ctx.handle, k, csrs, perms, _ptr(sd), C.byref(o), C.byref(info),
+                                            *arr, _ptr(caps))
+    if rc not in (0, int(Errc.budget_exceeded)):
+        _check(rc)
     ctx._factor_n = info.n
     ctx._graph = None      # the context now holds the batch union,
     ctx._resident = None   # not any single graph or factor
     out = []
-    for i, (g, ordg) in enumerate(zip(graphs, orderings)):
+    for i, (g, ordg, b) in enumerate(zip(graphs, orderings, bufs)):
         z = C.c_int64()
         _check(lib.parac_gpu_batch_nnz(ctx.handle, i, C.byref(z)))
         z = int(z.value)
-        col_ptr = np.empty(g.n + 1, np.int64)
-        rows = np.empty(max(z, 1), np.int32)
-        vals = np.empty(max(z, 1), np.float64)
-        diag = np.empty(max(g.n, 1), np.float64)
-        _check(lib.parac_gpu_download_batch(ctx.handle, i, _ptr(col_ptr), _ptr(rows), _ptr(vals), _ptr(diag)))
+        col_ptr, rows, vals, diag = b
+        if z > caps[i]:
+            rows = np.empty(max(z, 1), np.int32)
+            vals = np.empty(max(z, 1), np.float64)
+            _check(lib.parac_gpu_download_batch(ctx.handle, i, _ptr(col_ptr), _ptr(rows), _ptr(vals), _ptr(diag)))
         out.append(LdlFactor(g.n, col_ptr, rows[:z], vals[:z], diag[:g.n], ordg.perm))
     del keep
     return out, info

@@ -120,3 +120,74 @@ def test_begin_end_protocol_errors(gpu_ctx):
     assert lib.parac_gpu_factor_end(gpu_ctx.handle, info, None, None, None, None, 0) == P.Errc.arena_exhausted
     f = P.factor_gpu(g, P.ordering_random(g.n, 0), 0, ctx=gpu_ctx)
     assert f.nnz_off_diagonal() > 0
+
+
+def batch_members():
+    gs = [P.gen_poisson3d(20), P.gen_random_connected(300, 500, 3), P.gen_rmat(12, 16, 1),
+          P.gen_poisson2d(70), P.gen_random_connected(5, 4, 1)]
+    perms = [P.ordering_random(g.n, i + 1).perm for i, g in enumerate(gs)]
+    seeds = [3, 4, 5, 6, 7]
+    return gs, perms, seeds
+
+
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_batch_streamed_members_are_standalone_factors(gpu_ctx, port, monkeypatch, stream):
+    # members of 8000, 300, 4096, 4900 and 5 positions: blocks never straddle
+    # members, while K3's 2048-position counters do (batch streaming is
+    # opt-in: PARAC_STREAM_BATCH=1)
+    monkeypatch.setenv("PARAC_STREAM", stream)
+    monkeypatch.setenv("PARAC_STREAM_BATCH", "1")
+    gs, perms, seeds = batch_members()
+    fs, info = P.factor_batch_gpu(gs, [P.Ordering(p) for p in perms], seeds, ctx=gpu_ctx)
+    for i, (g, perm, seed, f) in enumerate(zip(gs, perms, seeds, fs)):
+        assert f.same_values(factor_from_port(port.factor(g, perm, seed))), f"member {i}"
+
+
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_batch_to_host_pinned_and_short_capacity(gpu_ctx, port, monkeypatch, stream):
+    monkeypatch.setenv("PARAC_STREAM_BATCH", stream)
+    torch = pytest.importorskip("torch")
+    import ctypes as C
+    lib, L = P.rchol.lib, P.rchol.L
+    gs, perms, seeds = batch_members()
+    want = [factor_from_port(port.factor(g, p, s)) for g, p, s in zip(gs, perms, seeds)]
+    zs = [w.nnz_off_diagonal() for w in want]
+    caps = np.array(zs, np.int64)
+    caps[2] -= 1  # member 2's rows/values one entry short
+    pin = lambda k, dt: torch.zeros(max(k, 1), dtype=dt, pin_memory=True).numpy()
+    bufs = [(pin(g.n + 1, torch.int64), pin(z, torch.int32), pin(z, torch.float64), pin(g.n, torch.float64))
+            for g, z in zip(gs, zs)]
+    arr = [(C.c_void_p * len(gs))(*[b[j].ctypes.data for b in bufs]) for j in range(4)]
+    csrs = (L.parac_csr * len(gs))(*[g.csr() for g in gs])
+    pp = (C.c_void_p * len(gs))(*[p.ctypes.data for p in perms])
+    sd = np.array(seeds, np.uint64)
+    info = L.parac_gpu_factor_info()
+    rc = lib.parac_gpu_factor_batch_to_host(gpu_ctx.handle, len(gs), csrs, pp, sd.ctypes.data,
+                                            P.GpuOptions().native(), info, *arr, caps.ctypes.data)
+    assert rc == P.Errc.budget_exceeded
+    for i, (g, w, b) in enumerate(zip(gs, want, bufs)):
+        if i == 2:
+            continue
+        f = P.LdlFactor(g.n, b[0], b[1][:zs[i]], b[2][:zs[i]], b[3][:g.n], perms[i])
+        assert f.same_values(w), f"member {i}"
+    # the short member from the resident union
+    z = C.c_int64()
+    assert lib.parac_gpu_batch_nnz(gpu_ctx.handle, 2, C.byref(z)) == 0 and z.value == zs[2]
+    cp, r, v, d = (np.empty(gs[2].n + 1, np.int64), np.empty(zs[2], np.int32), np.empty(zs[2]),
+                   np.empty(gs[2].n))
+    assert lib.parac_gpu_download_batch(gpu_ctx.handle, 2, cp.ctypes.data, r.ctypes.data, v.ctypes.data,
+                                        d.ctypes.data) == 0
+    assert P.LdlFactor(gs[2].n, cp, r, v, d, perms[2]).same_values(want[2])
+
+
+def test_single_and_batch_end_reject_the_other_layout(gpu_ctx):
+    lib, L = P.rchol.lib, P.rchol.L
+    info = L.parac_gpu_factor_info()
+    g = P.gen_poisson3d(6)
+    gpu_ctx.upload(g, P.ordering_random(g.n, 0))
+    assert lib.parac_gpu_factor_begin(gpu_ctx.handle, 0, P.GpuOptions().native()) == 0
+    assert lib.parac_gpu_factor_batch_end(gpu_ctx.handle, info, None, None, None, None, None) == \
+        P.Errc.dimension_mismatch
+    # the pending factorization was completed: the context is usable
+    f = P.factor_gpu(g, P.ordering_random(g.n, 0), 0, ctx=gpu_ctx)
+    assert f.nnz_off_diagonal() > 0

@@ -303,9 +303,17 @@ struct parac_gpu_ctx {
   unsigned long long* blkh_h = nullptr;  // [blkh_cap] per-block release words (host view)
   unsigned long long* blkh_d = nullptr;  // (device view)
   std::size_t blkh_cap = 0;
-  // batch: streamer blocks that never straddle problems (positions, nb+1)
-  std::vector<int> blk_k0_h;
-  DevBuf<int> blk_k0;
+  // batch: streamer blocks that never straddle problems (positions, nb+1),
+  // each block's member and that member's first block, the claim order
+  // (members interleaved), and the member regions of a streamed batch
+  // (stream_assemble.cu): member p's entries at region[p], its local col_ptr
+  // in lcol[base_p + p ...]
+  std::vector<int> blk_k0_h, blk_mem_h, blk_first_h, claim_h;
+  std::vector<long long> batch_ebase_h;
+  DevBuf<int> blk_k0, blk_first, claim, overflow;
+  DevBuf<long long> region, reg_cap, lcol;
+  bool batch_regions = false;                 // the resident batch factor is in the region layout
+  std::vector<long long> region_h, reg_cap_h, batch_z_h;  // per member: region start, capacity, off-diagonal count
   // a factorization launched by parac_gpu_factor_begin, completed by _end
   bool pending = false;
   std::uint64_t p_seed = 0;
@@ -358,22 +366,22 @@ Budgets default_budgets(int n, long long E, long long max_degree, const parac_gp
   return b;
 }
 
-// Streamed assembly beside K3 (stream_assemble.cu): on by default for single
-// problems (PARAC_STREAM=0: assemble after K3), PARAC_STREAM_CTAS CTAs (8)
-int stream_ctas() {
+// Streamed assembly beside K3 (stream_assemble.cu): on by default
+// (PARAC_STREAM=0: assemble after K3), PARAC_STREAM_CTAS CTAs
+int stream_ctas(const parac_gpu_ctx* ctx) {
   const char* e = std::getenv("PARAC_STREAM_CTAS");
-  return e ? std::max(1, std::min(64, std::atoi(e))) : 8;
+  // batches: 16 (64 x 64^3: 8 CTAs fell behind the elimination by 10 ms; 16
+  // and 32 kept up, 16 with the shorter K3)
+  return e ? std::max(1, std::min(64, std::atoi(e))) : ctx->batch_count > 0 ? 16 : 8;
 }
 bool stream_wanted(const parac_gpu_ctx* ctx) {
   const char* e = std::getenv("PARAC_STREAM");
   const int m = e ? std::atoi(e) : 1;
-  // Batches assemble after K3 unless PARAC_STREAM_BATCH=1: with the union's
-  // global CSC layout, member p's offsets wait for every earlier member's
-  // last (latest) columns, so blocks release only near K3's end while the
-  // streamer's slots slow the throughput-bound batch K3 (64 x 64^3: device
-  // 68.5 -> 77 ms, e2e 159 -> 154 ms measured)
+  // PARAC_STREAM_BATCH=0: batches assemble after K3 (their streamed layout is
+  // per member, stream_assemble.cu; 64 x 64^3 e2e 148.5 -> 114.6 ms, device
+  // time unchanged)
   const char* eb = std::getenv("PARAC_STREAM_BATCH");
-  if (ctx->batch_count > 0 && !(eb && std::atoi(eb) == 1)) return false;
+  if (ctx->batch_count > 0 && eb && std::atoi(eb) == 0) return false;
   return (m == 1 || m == 3) && ctx->n > 0;
 }
 // PARAC_STREAM=3 (diagnostics): the streamer runs after K3 on K3's stream --
@@ -573,6 +581,31 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
     std::memset(ctx->blkh_h, 0, sizeof(unsigned long long) * std::max<std::size_t>(nblk, 1));
     d.blk_done = ctx->blk_done.p;
   }
+  if (ctx->streaming && ctx->batch_count > 0) {  // member regions: a share of the column arena's budget each, by size
+    const int count = ctx->batch_count;
+    const std::vector<long long>& base = ctx->batch_base_h;
+    const std::vector<long long>& eb = ctx->batch_ebase_h;
+    const double tot_w = static_cast<double>(std::max<long long>(E + n, 1));
+    ctx->region_h.assign(count + 1, 0);
+    std::vector<long long>& cap = ctx->reg_cap_h;
+    cap.assign(count, 0);
+    for (int i = 0; i < count; ++i) {
+      const long long w = (eb[i + 1] - eb[i]) / 2 + (base[i + 1] - base[i]);
+      cap[i] = static_cast<long long>(static_cast<double>(b.arena) * (static_cast<double>(w) / tot_w)) + 4096;
+      ctx->region_h[i + 1] = ctx->region_h[i] + cap[i];
+    }
+    const std::size_t rtot = static_cast<std::size_t>(std::max<long long>(ctx->region_h[count], 1));
+    ctx->rows.ensure(rtot);
+    ctx->vals.ensure(rtot);
+    ctx->region.ensure(count);
+    ctx->reg_cap.ensure(count);
+    ctx->lcol.ensure(static_cast<std::size_t>(n) + count);
+    ctx->overflow.ensure(1);
+    check(cudaMemcpyAsync(ctx->region.p, ctx->region_h.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, s),
+          "h2d");
+    check(cudaMemcpyAsync(ctx->reg_cap.p, cap.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, s), "h2d");
+    check(cudaMemsetAsync(ctx->overflow.p, 0, sizeof(int), s), "memset");
+  }
   check(cudaEventRecord(ctx->ev[0], s), "event");
   if (count) {
     const std::size_t nb = static_cast<std::size_t>((n + kStreamBlock - 1) >> kStreamShift);
@@ -589,7 +622,7 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
   check(launch_initial_ready(d, ctx->tiles.p, s), "initial_ready launch");
   check(cudaEventRecord(ctx->ev[1], s), "event");
   int grid = 0;
-  const int sctas = ctx->streaming ? stream_ctas() : 0;
+  const int sctas = ctx->streaming ? stream_ctas(ctx) : 0;
   const bool serial = ctx->streaming && stream_serial();
   check(launch_eliminate(d, o.grid_ctas, serial ? 0 : sctas, s, &grid), "eliminate launch");
   if (serial) check(cudaEventRecord(ctx->ev[2], s), "event");
@@ -601,6 +634,14 @@ void launch_factor(parac_gpu_ctx* ctx, std::uint64_t seed, const parac_gpu_optio
     sd.blk_k0 = batch ? ctx->blk_k0.p : nullptr;
     sd.pos_pid = batch ? ctx->pos_pid.p : nullptr;
     sd.pid_base = batch ? ctx->pid_base.p : nullptr;
+    if (batch) {
+      sd.claim = ctx->claim.p;
+      sd.blk_first = ctx->blk_first.p;
+      sd.region = ctx->region.p;
+      sd.reg_cap = ctx->reg_cap.p;
+      sd.lcol = ctx->lcol.p;
+      sd.overflow = ctx->overflow.p;
+    }
     sd.blk_done = ctx->blk_done.p;
     sd.col_len = ctx->col_len.p;
     sd.col_start = ctx->col_start.p;
@@ -702,14 +743,14 @@ struct BatchOut {
   double* const* diag;
   const std::int64_t* caps;
   bool short_cap = false;  // some problem's factor exceeded its capacity
+  bool redo = false;       // a member outgrew its region: downloaded again from the union CSC
 };
 
-// The batch download beside the elimination. Blocks never straddle problems
-// (upload_batch), so each released range of positions / entries splits into
-// per-problem pieces: positions by the staged problem offsets, entries by
-// each problem's first entry offset (the release word of the block before
-// its first block). A problem's col_ptr is made local
-// (minus its first entry offset) once all its blocks are copied.
+// The batch download beside the elimination (member regions). Member p's
+// blocks release independently of the other members'; for each member the
+// contiguous released prefix of its blocks is copied: its local col_ptr
+// (lcol), diag, and its entries from its region -- all in its own position and
+// entry space, so nothing is rebased on the host.
 void stream_download_batch(parac_gpu_ctx* ctx, BatchOut& out) {
   const int count = ctx->batch_count;
   const std::vector<long long>& base = ctx->batch_base_h;
@@ -717,85 +758,64 @@ void stream_download_batch(parac_gpu_ctx* ctx, BatchOut& out) {
   const int nb = static_cast<int>(bk.size()) - 1;
   volatile unsigned long long* rel = ctx->blkh_h;
   constexpr unsigned long long kRel = 1ull << 63;
-  std::vector<int> first(count, -1), last(count, -1);
-  for (int b = 0, p = 0; b < nb; ++b) {
-    while (bk[b] >= base[p + 1]) ++p;
-    if (first[p] < 0) first[p] = b;
+  std::vector<int> cur(count, -1), last(count, -1);
+  for (int b = 0; b < nb; ++b) {
+    const int p = ctx->blk_mem_h[b];
+    if (cur[p] < 0) cur[p] = b;
     last[p] = b;
   }
-  std::vector<int> ne;  // problems with vertices, in order
+  std::vector<long long> dz(count, 0);
+  std::vector<int> active;
   for (int p = 0; p < count; ++p)
-    if (base[p + 1] > base[p]) ne.push_back(p);
+    if (cur[p] >= 0) active.push_back(p);
   const long long kMinEntries = 1 << 19;
-  int done_b = 0;
-  long long done_z = 0;
-  std::size_t qi = 0, rebased = 0;
-  int seen_b = 0;
-  // a problem's first entry offset: the release word of the block before its first
-  auto zstart = [&](int p) -> long long {
-    return first[p] > 0 ? static_cast<long long>(rel[first[p] - 1] & ~kRel) : 0;
-  };
-  auto rebase_ready = [&](int pb) {
-    std::size_t r = rebased;
-    while (r < ne.size() && last[ne[r]] < pb) ++r;
-    if (r == rebased) return;
-    check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
-    for (; rebased < r; ++rebased) {
-      const int p = ne[rebased];
-      std::int64_t* cp = out.col_ptr ? out.col_ptr[p] : nullptr;
-      if (!cp) continue;
-      const long long z0 = zstart(p);
-      for (long long k = 0, m = base[p + 1] - base[p]; k <= m; ++k) cp[k] -= z0;
-    }
-  };
-  auto take = [&](int) {
-    while (seen_b < nb && (rel[seen_b] & kRel)) ++seen_b;
-    const int pb = seen_b;
-    const long long pz = pb > 0 ? static_cast<long long>(rel[pb - 1] & ~kRel) : 0;
-    if (pb <= done_b || (pb < nb && pz - done_z < kMinEntries)) return;
-    const long long P0 = bk[done_b], P1 = bk[pb];
-    for (int p = 0; p < count; ++p) {  // positions [P0, P1], P1 = the last block's end (col_ptr only)
-      // (a problem ending at P0 was completed -- and rebased -- last round)
-      if (base[p + 1] <= P0 || base[p] > P1) continue;
-      const long long lo = std::max(P0, base[p]), hi = std::min(P1, base[p + 1]);
-      if (out.col_ptr && out.col_ptr[p])
-        copy_range(ctx, out.col_ptr[p] + (lo - base[p]), ctx->col_ptr.p + lo, sizeof(long long) * (hi - lo + 1));
-      if (hi > lo && out.diag && out.diag[p])
-        copy_range(ctx, out.diag[p] + (lo - base[p]), ctx->diag.p + lo, sizeof(double) * (hi - lo));
-    }
-    while (done_z < pz && qi < ne.size()) {  // entries [done_z, pz), problem by problem
-      const int p = ne[qi];
-      const long long z0 = zstart(p);
-      const bool next_known = qi + 1 < ne.size() && first[ne[qi + 1]] < pb;
-      const long long zend = next_known ? zstart(ne[qi + 1]) : pz;
-      const long long e1 = std::min(zend, pz);
-      const long long cap = out.caps ? out.caps[p] : 0;
-      const long long c1 = std::min(e1, z0 + cap);
-      if (c1 > done_z) {
-        if (out.rows && out.rows[p])
-          copy_range(ctx, out.rows[p] + (done_z - z0), ctx->rows.p + done_z, sizeof(int) * (c1 - done_z));
-        if (out.values && out.values[p])
-          copy_range(ctx, out.values[p] + (done_z - z0), ctx->vals.p + done_z, sizeof(double) * (c1 - done_z));
+  auto pass = [&](bool final_pass) {
+    for (std::size_t ai = 0; ai < active.size();) {
+      const int p = active[ai];
+      int c = cur[p];
+      while (c <= last[p] && (rel[c] & kRel)) ++c;
+      const long long z1 = c > cur[p] ? static_cast<long long>(rel[c - 1] & ~kRel) : dz[p];
+      const bool done = c > last[p];
+      if (c == cur[p] || (!done && !final_pass && z1 - dz[p] < kMinEntries)) {
+        ++ai;
+        continue;
       }
-      if (e1 > z0 + cap) out.short_cap = true;
-      done_z = e1;
-      if (next_known && e1 == zend) ++qi;
-      else break;
+      const long long P0 = bk[cur[p]], P1 = bk[c];  // positions [P0, P1): col_ptr through P1
+      if (out.col_ptr && out.col_ptr[p])
+        copy_range(ctx, out.col_ptr[p] + (P0 - base[p]), ctx->lcol.p + P0 + p, sizeof(long long) * (P1 - P0 + 1));
+      if (out.diag && out.diag[p])
+        copy_range(ctx, out.diag[p] + (P0 - base[p]), ctx->diag.p + P0, sizeof(double) * (P1 - P0));
+      const long long cap = out.caps ? out.caps[p] : 0;
+      const long long c1 = std::min(z1, cap);
+      if (c1 > dz[p]) {
+        const long long r0 = ctx->region_h[p];
+        if (out.rows && out.rows[p])
+          copy_range(ctx, out.rows[p] + dz[p], ctx->rows.p + r0 + dz[p], sizeof(int) * (c1 - dz[p]));
+        if (out.values && out.values[p])
+          copy_range(ctx, out.values[p] + dz[p], ctx->vals.p + r0 + dz[p], sizeof(double) * (c1 - dz[p]));
+      }
+      if (z1 > cap) out.short_cap = true;
+      dz[p] = z1;
+      cur[p] = c;
+      if (done) {
+        active[ai] = active.back();
+        active.pop_back();
+      } else {
+        ++ai;
+      }
     }
-    done_b = pb;
-    rebase_ready(pb);
   };
-  while (done_b < nb) {
-    take(0);
-    if (done_b == nb) break;
+  while (!active.empty()) {
+    pass(false);
+    if (active.empty()) break;
     if (cudaEventQuery(ctx->ev[3]) == cudaSuccess) {
-      take(0);
+      pass(true);
       break;
     }
     std::this_thread::yield();
   }
   check(cudaStreamSynchronize(ctx->s_copy), "d2h sync");
-  for (int p = 0; p < count; ++p)  // problems without vertices: col_ptr = {0}
+  for (int p = 0; p < count; ++p)  // members without vertices: col_ptr = {0}
     if (base[p + 1] == base[p] && out.col_ptr && out.col_ptr[p]) out.col_ptr[p][0] = 0;
 }
 
@@ -1091,6 +1111,34 @@ int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* g
     ctx->blk_k0.ensure(ctx->blk_k0_h.size());
     check(cudaMemcpy(ctx->blk_k0.p, ctx->blk_k0_h.data(), sizeof(int) * ctx->blk_k0_h.size(), cudaMemcpyHostToDevice),
           "h2d");
+    const int nblk = static_cast<int>(ctx->blk_k0_h.size()) - 1;
+    ctx->blk_mem_h.assign(nblk, 0);
+    ctx->blk_first_h.assign(nblk, 0);
+    std::vector<int> mfirst(count, -1), mcount(count, 0);
+    for (int b = 0, p = 0; b < nblk; ++b) {
+      while (ctx->blk_k0_h[b] >= base[p + 1]) ++p;
+      if (mfirst[p] < 0) mfirst[p] = b;
+      ctx->blk_mem_h[b] = p;
+      ctx->blk_first_h[b] = mfirst[p];
+      ++mcount[p];
+    }
+    ctx->claim_h.clear();  // j-th block of every member, then the (j+1)-th: members progress side by side
+    for (int j = 0, more = 1; more; ++j) {
+      more = 0;
+      for (int p = 0; p < count; ++p)
+        if (j < mcount[p]) {
+          ctx->claim_h.push_back(mfirst[p] + j);
+          more = 1;
+        }
+    }
+    ctx->blk_first.ensure(std::max(nblk, 1));
+    ctx->claim.ensure(std::max(nblk, 1));
+    if (nblk > 0) {
+      check(cudaMemcpy(ctx->blk_first.p, ctx->blk_first_h.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice), "h2d");
+      check(cudaMemcpy(ctx->claim.p, ctx->claim_h.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice), "h2d");
+    }
+    ctx->batch_ebase_h = ebase;
+    ctx->batch_regions = false;
   });
 }
 
@@ -1114,6 +1162,10 @@ int parac_gpu_batch_nnz(parac_gpu_ctx* ctx, int32_t i, int64_t* nnz_off) {
     require_ctx(ctx);
     if (ctx->f_n < 0 || ctx->batch_count <= 0 || i < 0 || i >= ctx->batch_count)
       throw Failure{dimension_mismatch, "no resident batch factor / index out of range"};
+    if (ctx->batch_regions) {
+      *nnz_off = ctx->batch_z_h[i];
+      return;
+    }
     long long c[2];
     const long long b = ctx->batch_base_h[i], e = ctx->batch_base_h[i + 1];
     check(cudaMemcpy(&c[0], ctx->col_ptr.p + b, sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
@@ -1131,6 +1183,17 @@ int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, in
     const long long b = ctx->batch_base_h[i], e = ctx->batch_base_h[i + 1];
     const long long n = e - b;
     cudaStream_t s = ctx->stream;
+    if (ctx->batch_regions) {  // streamed: member i's local col_ptr and its region
+      const long long z = ctx->batch_z_h[i], r0 = ctx->region_h[i];
+      if (col_ptr) check(cudaMemcpyAsync(col_ptr, ctx->lcol.p + b + i, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost, s), "d2h");
+      if (rows && z) check(cudaMemcpyAsync(rows, ctx->rows.p + r0, sizeof(int) * z, cudaMemcpyDeviceToHost, s), "d2h");
+      if (values && z) check(cudaMemcpyAsync(values, ctx->vals.p + r0, sizeof(double) * z, cudaMemcpyDeviceToHost, s), "d2h");
+      if (diag && n) check(cudaMemcpyAsync(diag, ctx->diag.p + b, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "d2h");
+      check(cudaStreamSynchronize(s), "d2h sync");
+      if (!col_ptr) return;
+      if (n == 0) col_ptr[0] = 0;
+      return;
+    }
     check(cudaMemcpyAsync(col_ptr, ctx->col_ptr.p + b, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost, s), "d2h");
     check(cudaStreamSynchronize(s), "d2h sync");
     const long long z0 = col_ptr[0], z = col_ptr[n] - z0;
@@ -1227,6 +1290,39 @@ int factor_end_impl(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, const HostO
   }
   ctx->pending = false;
   rc = guarded([&] {
+    if (ctx->streaming && ctx->batch_count > 0) {  // member regions (stream_assemble.cu)
+      int ov = 0;
+      check(cudaMemcpy(&ov, ctx->overflow.p, sizeof(int), cudaMemcpyDeviceToHost), "d2h");
+      if (ov) {  // a member outgrew its region: the union CSC after all, assembled now
+        FactorDev d{};
+        d.n = n;
+        d.col_len = ctx->col_len.p;
+        d.col_start = ctx->col_start.p;
+        d.arena_rows = ctx->arena_rows.p;
+        d.arena_vals = ctx->arena_vals.p;
+        d.samples = ctx->samples.p;
+        d.ctrl = ctx->ctrl.p;  // (its total_fills was read already)
+        check(launch_assemble(d, ctx->col_ptr.p, ctx->rows.p, ctx->vals.p, ctx->tiles.p, ctx->stream), "assemble");
+        check(launch_batch_local_rows(n, ctx->col_ptr.p, ctx->pos_pid.p, ctx->pid_base.p, ctx->rows.p, ctx->stream),
+              "batch rows");
+        check(cudaMemcpyAsync(&ctx->last_z, ctx->col_ptr.p + n, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream),
+              "d2h");
+        check(cudaStreamSynchronize(ctx->stream), "assemble sync");
+        ctx->batch_regions = false;
+        if (bout) bout->redo = true;
+      } else {
+        const int count = ctx->batch_count;
+        ctx->batch_z_h.assign(count, 0);
+        for (int b = 0, nb = static_cast<int>(ctx->blk_mem_h.size()); b < nb; ++b)  // the member's last block's word
+          ctx->batch_z_h[ctx->blk_mem_h[b]] = static_cast<long long>(ctx->blkh_h[b] & ~(1ull << 63));
+        long long Zs = 0;
+        for (long long z : ctx->batch_z_h) Zs += z;
+        ctx->last_z = Zs;
+        ctx->batch_regions = true;
+      }
+    } else {
+      ctx->batch_regions = false;
+    }
     const Ctrl c = ctx->last_ctrl;
     const long long Z = ctx->last_z;
     ctx->f_n = n;
@@ -1272,7 +1368,8 @@ int factor_end_impl(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, const HostO
       if (diag && n) ctx->stage.d2h(diag, ctx->diag.p, sizeof(double) * n, ctx->stream);
       check(cudaStreamSynchronize(ctx->stream), "d2h sync");
     }
-    if (bout && !ctx->streaming) {  // the assembly ran after K3: every member's copies in flight at once
+    if (bout && (!ctx->streaming || bout->redo)) {  // assembled after K3: every member's copies in flight at once
+      bout->short_cap = false;
       ensure_stream_resources(ctx);
       const int count = ctx->batch_count;
       const std::vector<long long>& base = ctx->batch_base_h;
@@ -1406,6 +1503,8 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
   return guarded([&] {
     require_ctx(ctx);
     if (ctx->f_n < 0) throw Failure{dimension_mismatch, "no resident factor"};
+    if (ctx->batch_count > 0 && ctx->batch_regions)
+      throw Failure{dimension_mismatch, "the resident factor is a streamed batch: parac_gpu_download_batch"};
     const int n = ctx->f_n;
     const long long Z = ctx->f_nnz;
     cudaStream_t s = ctx->stream;

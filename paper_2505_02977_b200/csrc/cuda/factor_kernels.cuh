@@ -192,6 +192,17 @@ struct StreamDev {
   const int* blk_k0;
   const int* pos_pid;
   const long long* pid_base;
+  // batch regions (optional): member p's entries at region[p] + its local
+  // offsets (capacity reg_cap[p]; beyond it *overflow = 1 and the block is not
+  // copied), its local col_ptr at lcol[base_p + p ...]; offsets by look-back
+  // within the member (blk_first[b] = its first block); blocks claimed in the
+  // order claim[] (members interleaved)
+  const int* claim;
+  const int* blk_first;
+  const long long* region;
+  const long long* reg_cap;
+  long long* lcol;
+  int* overflow;
 };
 cudaError_t launch_stream_assemble(const StreamDev& s, int ctas, cudaStream_t st);
 cudaError_t launch_sum_samples(const FactorDev& d, cudaStream_t s);

@@ -118,9 +118,10 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
   __syncthreads();
   while (true) {
     if (tid == 0) {
-      const int b = atomicAdd(s.next_blk, 1);
+      const int i = atomicAdd(s.next_blk, 1);
+      const int b = i < s.nb && s.claim ? s.claim[i] : i;
       blk_sh = b;
-      bool ok = b < s.nb;
+      bool ok = i < s.nb;
       if (ok) {  // every K3 counter bucket the block touches is complete
         const int a0 = s.blk_k0 ? s.blk_k0[b] : b * kStreamBlock;
         const int a1 = s.blk_k0 ? s.blk_k0[b + 1] : min(a0 + kStreamBlock, s.n);
@@ -169,10 +170,13 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
       loc[kStreamBlock] = tot;
       // decoupled look-back: publish this block's aggregate at once, then sum
       // predecessors' aggregates back to the first inclusive prefix
-      if (b > 0) st_relaxed_u64g(&s.blk_incl[b], kAgg | static_cast<unsigned long long>(tot));
+      // (batch regions: offsets are local to the member, the look-back stops
+      // at the member's first block)
+      const int jmin = s.blk_first ? s.blk_first[b] : 0;
+      if (b > jmin) st_relaxed_u64g(&s.blk_incl[b], kAgg | static_cast<unsigned long long>(tot));
       long long bs = 0;
       bool ok = true;
-      for (int j = b - 1; j >= 0;) {
+      for (int j = b - 1; j >= jmin;) {
         const unsigned long long w = ld_relaxed_u64(&s.blk_incl[j]);
         if (!(w & (kFlag | kAgg))) {
           if (aborted(s)) { ok = false; break; }
@@ -191,9 +195,18 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
     if (!ok_sh) return;
     const long long bs = base_sh;
 
-    // 4. col_ptr and the entries
-    for (int i = tid; i < cnt; i += kStreamThreads) s.col_ptr[k0 + i] = bs + loc[i];
-    if (tid == 0) s.col_ptr[k0 + cnt] = bs + tot;  // the next block writes the same value
+    // 4. col_ptr and the entries (batch regions: the member's local col_ptr
+    // at lcol[k + member], its entries from region[member])
+    long long* cpo = s.lcol ? s.lcol + pid : s.col_ptr;
+    for (int i = tid; i < cnt; i += kStreamThreads) cpo[k0 + i] = bs + loc[i];
+    if (tid == 0) cpo[k0 + cnt] = bs + tot;  // the next block writes the same value
+    long long ob = bs;  // output offset of the block's first entry
+    bool fits = true;
+    if (s.region) {
+      ob += s.region[pid];
+      fits = bs + tot <= s.reg_cap[pid];
+      if (!fits && tid == 0) atomicExch(s.overflow, 1);  // the host re-assembles after K3
+    }
     // Each warp copies groups of 32 consecutive columns (group g: columns
     // [32g, 32g + 32), warps take groups round robin). Lanes walk the group's
     // entries 32 apart (coalesced); an entry's column comes from a 5-step
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
     const int warp = tid >> 5, lane = tid & 31;
     const int groups = (cnt + 31) >> 5;
     constexpr int U = 8;
-    for (int g = warp; g < groups; g += kStreamThreads / 32) {
+    for (int g = warp; fits && g < groups; g += kStreamThreads / 32) {
       const int c0 = g << 5;
       const int nc = min(32, cnt - c0);
       const long long* gl = loc + c0;  // gl[0..nc] (loc[cnt] = tot)
@@ -232,8 +245,8 @@ __global__ void __launch_bounds__(kStreamThreads, 4) stream_assemble_kernel(Stre
         for (int u = 0; u < U; ++u) {
           const long long e = e0 + u * 32 + lane;
           if (e < T) {
-            __stcs(s.rows + bs + g0 + e, r[u] - row_base);
-            __stcs(s.vals + bs + g0 + e, x[u]);
+            __stcs(s.rows + ob + g0 + e, r[u] - row_base);
+            __stcs(s.vals + ob + g0 + e, x[u]);
           }
         }
       }

@@ -133,10 +133,9 @@ def batch_members():
 @pytest.mark.parametrize("stream", ["1", "0"])
 def test_batch_streamed_members_are_standalone_factors(gpu_ctx, port, monkeypatch, stream):
     # members of 8000, 300, 4096, 4900 and 5 positions: blocks never straddle
-    # members, while K3's 2048-position counters do (batch streaming is
-    # opt-in: PARAC_STREAM_BATCH=1)
+    # members, while K3's 2048-position counters do; each member assembled
+    # into its own region (or, PARAC_STREAM=0, the union CSC after K3)
     monkeypatch.setenv("PARAC_STREAM", stream)
-    monkeypatch.setenv("PARAC_STREAM_BATCH", "1")
     gs, perms, seeds = batch_members()
     fs, info = P.factor_batch_gpu(gs, [P.Ordering(p) for p in perms], seeds, ctx=gpu_ctx)
     for i, (g, perm, seed, f) in enumerate(zip(gs, perms, seeds, fs)):
@@ -178,6 +177,22 @@ def test_batch_to_host_pinned_and_short_capacity(gpu_ctx, port, monkeypatch, str
     assert lib.parac_gpu_download_batch(gpu_ctx.handle, 2, cp.ctypes.data, r.ctypes.data, v.ctypes.data,
                                         d.ctypes.data) == 0
     assert P.LdlFactor(gs[2].n, cp, r, v, d, perms[2]).same_values(want[2])
+
+
+def test_batch_region_overflow_falls_back_to_the_union(gpu_ctx, port):
+    # tiny explicit arena: member regions (shares of it) overflow, the library
+    # assembles the union CSC after K3 instead -- or the budget fails cleanly
+    gs, perms, seeds = batch_members()
+    want = [factor_from_port(port.factor(g, p, s)) for g, p, s in zip(gs, perms, seeds)]
+    z = sum(w.nnz_off_diagonal() for w in want)
+    try:
+        fs, info = P.factor_batch_gpu(gs, [P.Ordering(p) for p in perms], seeds,
+                                      P.GpuOptions(column_arena_entries=z + 64, fill_pool_entries=1 << 22), ctx=gpu_ctx)
+    except P.Error as e:
+        assert e.code == P.Errc.arena_exhausted
+        return
+    for i, (f, w) in enumerate(zip(fs, want)):
+        assert f.same_values(w), f"member {i}"
 
 
 def test_single_and_batch_end_reject_the_other_layout(gpu_ctx):

@@ -334,9 +334,15 @@ int device_sms(parac_gpu_ctx* ctx) {
   return sms;
 }
 
-void require_ctx(parac_gpu_ctx* ctx) {
+void require_ctx_any(parac_gpu_ctx* ctx) {
   if (!ctx) throw Failure{internal_error, "null context"};
   activate(ctx);
+}
+// Every entry point but parac_gpu_factor_end: the buffers of a pending
+// factorization (parac_gpu_factor_begin) are in use on the device.
+void require_ctx(parac_gpu_ctx* ctx) {
+  require_ctx_any(ctx);
+  if (ctx->pending) throw Failure{internal_error, "a factorization is pending (call parac_gpu_factor_end)"};
 }
 
 Budgets default_budgets(int n, long long E, long long max_degree, const parac_gpu_options& o) {
@@ -1234,7 +1240,7 @@ namespace {
 // (hout) or every batch member's (bout), either may be null.
 int factor_end_impl(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, const HostOut* hout, BatchOut* bout) {
   int rc = guarded([&] {
-    require_ctx(ctx);
+    require_ctx_any(ctx);
     if (!ctx->pending) throw Failure{internal_error, "no factorization pending (call parac_gpu_factor_begin)"};
   });
   if (rc) return rc;

@@ -112,6 +112,9 @@ def test_begin_end_protocol_errors(gpu_ctx):
     assert lib.parac_gpu_factor_begin(gpu_ctx.handle, 0, o) == 0
     # a second begin while one is pending
     assert lib.parac_gpu_factor_begin(gpu_ctx.handle, 0, o) == P.Errc.internal_error
+    # nothing else touches the context's buffers while it is pending
+    assert lib.parac_gpu_upload(gpu_ctx.handle, g.csr(), P.ordering_random(g.n, 0).perm.ctypes.data) == \
+        P.Errc.internal_error
     assert lib.parac_gpu_factor_end(gpu_ctx.handle, info, None, None, None, None, 0) == 0
     assert info.n == g.n and info.nnz_off_diagonal > 0
     # explicit budgets fail cleanly through _end, and the context recovers

@@ -350,14 +350,18 @@ Budgets default_budgets(int n, long long E, long long max_degree, const parac_gp
   const long long base = E + n;
   // 64 preallocated slots per position cover the fill count of ~99.5% of
   // 128^3 positions (p99 66), so the directory lookup is rare.
-  // Preallocated fill slots per position: as many as ~8.6 GB allow, up to 256
-  // (covers the fill counts of all but the widest columns at 128^3: no
-  // overflow-directory round trips on the emission or gather path), at least 64.
+  // Preallocated fill slots per position: as many as ~17.6 GB allow, up to
+  // 512, at least 64. The widest (latest, critical-path) columns gather
+  // hundreds of fills; beyond the preallocated slots each costs directory
+  // round trips on the emission and gather paths. Measured K3 at 128^3 by
+  // slots: 32: 20.7, 64: 20.55, 128: 20.3, 256: 19.91, 384: 19.60, 512: 19.49,
+  // 1024: 19.51 ms; 27-point 96^3 256 -> 512: 30.31 -> 29.43 ms. A compact
+  // store (fewer slots, more overflow) is slower, not faster.
   if (o.first_chunk > 0) {
     b.c0 = o.first_chunk;
   } else {
-    const long long cap = 8600000000LL / (16LL * std::max(n, 1));
-    b.c0 = cap >= 256 ? 256 : cap >= 128 ? 128 : 64;
+    const long long cap = 17600000000LL / (16LL * std::max(n, 1));
+    b.c0 = cap >= 512 ? 512 : cap >= 256 ? 256 : cap >= 128 ? 128 : 64;
   }
   // hub graphs: fills concentrate on a few positions whose overflow chunks
   // grow geometrically (up to 2x waste), and raw columns are wide

@@ -345,13 +345,16 @@ void require_ctx(parac_gpu_ctx* ctx) {
   if (ctx->pending) throw Failure{internal_error, "a factorization is pending (call parac_gpu_factor_end)"};
 }
 
-Budgets default_budgets(int n, long long E, long long max_degree, const parac_gpu_options& o) {
+Budgets default_budgets(int n, long long E, long long max_degree, const parac_gpu_options& o,
+                        std::size_t own_pool_bytes = 0) {
   Budgets b;
   const long long base = E + n;
   // 64 preallocated slots per position cover the fill count of ~99.5% of
   // 128^3 positions (p99 66), so the directory lookup is rare.
-  // Preallocated fill slots per position: as many as ~17.6 GB allow, up to
-  // 512, at least 64. The widest (latest, critical-path) columns gather
+  // Preallocated fill slots per position: as many as 40% of the device's
+  // free memory allows (the context's own fill pool counted as free, so the
+  // choice is stable across calls; at least ~17.6 GB's worth), up to 512, at
+  // least 64. The widest (latest, critical-path) columns gather
   // hundreds of fills; beyond the preallocated slots each costs directory
   // round trips on the emission and gather paths. Measured K3 at 128^3 by
   // slots: 32: 20.7, 64: 20.55, 128: 20.3, 256: 19.91, 384: 19.60, 512: 19.49,
@@ -360,7 +363,11 @@ Budgets default_budgets(int n, long long E, long long max_degree, const parac_gp
   if (o.first_chunk > 0) {
     b.c0 = o.first_chunk;
   } else {
-    const long long cap = 17600000000LL / (16LL * std::max(n, 1));
+    std::size_t free_b = 0, total_b = 0;
+    long long budget = 17600000000LL;  // (measured: the 64 x 64^3 batch, 64 -> 256 slots: K3 64.1 -> 62.5 ms)
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+      budget = std::max(budget, static_cast<long long>(0.4 * static_cast<double>(free_b + own_pool_bytes)));
+    const long long cap = budget / (16LL * std::max(n, 1));
     b.c0 = cap >= 512 ? 512 : cap >= 256 ? 256 : cap >= 128 ? 128 : 64;
   }
   // hub graphs: fills concentrate on a few positions whose overflow chunks
@@ -1228,7 +1235,7 @@ int parac_gpu_factor_begin(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_op
     ctx->p_t0 = std::chrono::steady_clock::now();
     ctx->p_seed = seed;
     ctx->p_opt = o;
-    ctx->p_b = default_budgets(ctx->n, ctx->nnz / 2, ctx->max_degree, o);
+    ctx->p_b = default_budgets(ctx->n, ctx->nnz / 2, ctx->max_degree, o, ctx->pool0.cap * sizeof(int4));
     ctx->p_attempts = 0;
     ctx->p_failed_ms = 0.0;
     ctx->streaming = stream_wanted(ctx);

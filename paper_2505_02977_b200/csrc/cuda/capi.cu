@@ -17,6 +17,7 @@
 
 #include "../../../include/parac_gpu.h"
 #include "../host/errors.hpp"
+#include "../host/nvtx.hpp"
 #include "../host/host_rng.hpp"
 #include "factor_kernels.cuh"
 #include "solve_kernels.cuh"
@@ -954,6 +955,7 @@ void parac_gpu_destroy(parac_gpu_ctx* ctx) {
 }
 
 int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t seed, int32_t* perm) {
+  NvtxRange nvtx_range("parac_gpu_ordering_nnz_sort");
   return guarded([&] {
     require_ctx(ctx);
     if (!g || g->n < 0 || (g->n > 0 && (!g->ptr || !perm))) throw Failure{dimension_mismatch, "bad graph"};
@@ -974,6 +976,7 @@ int parac_gpu_ordering_nnz_sort(parac_gpu_ctx* ctx, const parac_csr* g, uint64_t
 }
 
 int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm) {
+  NvtxRange nvtx_range("parac_gpu_upload");
   return guarded([&] {
     require_ctx(ctx);
     if (!g || g->n < 0 || !g->ptr) throw Failure{dimension_mismatch, "bad graph"};
@@ -1017,6 +1020,7 @@ int parac_gpu_upload(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
 // problem's factor is byte-identical to its stand-alone factorization.
 int parac_gpu_upload_batch(parac_gpu_ctx* ctx, int32_t count, const parac_csr* graphs,
                            const int32_t* const* perms, const uint64_t* seeds) {
+  NvtxRange nvtx_range("parac_gpu_upload_batch");
   return guarded([&] {
     require_ctx(ctx);
     if (count <= 0 || !graphs || !perms || !seeds) throw Failure{dimension_mismatch, "empty batch"};
@@ -1193,6 +1197,7 @@ int parac_gpu_batch_nnz(parac_gpu_ctx* ctx, int32_t i, int64_t* nnz_off) {
 
 int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, int32_t* rows, double* values,
                              double* diag) {
+  NvtxRange nvtx_range("parac_gpu_download_batch");
   return guarded([&] {
     require_ctx(ctx);
     if (ctx->f_n < 0 || ctx->batch_count <= 0 || i < 0 || i >= ctx->batch_count)
@@ -1223,6 +1228,7 @@ int parac_gpu_download_batch(parac_gpu_ctx* ctx, int32_t i, int64_t* col_ptr, in
 }
 
 int parac_gpu_factor_begin(parac_gpu_ctx* ctx, uint64_t seed, const parac_gpu_options* opt) {
+  NvtxRange nvtx_range("parac_gpu_factor_begin");
   parac_gpu_options o;
   if (opt) o = *opt; else parac_gpu_default_options(&o);
   return guarded([&] {
@@ -1435,6 +1441,7 @@ extern "C" {
 
 int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* col_ptr, int32_t* rows,
                          double* values, double* diag, int64_t capacity) {
+  NvtxRange nvtx_range("parac_gpu_factor_end");
   const bool want = col_ptr || rows || values || diag;
   if (want && ctx && ctx->batch_count > 0) {
     const int rc = factor_end_impl(ctx, info, nullptr, nullptr);  // complete it; the outputs do not apply
@@ -1448,6 +1455,7 @@ int parac_gpu_factor_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_
 int parac_gpu_factor_batch_end(parac_gpu_ctx* ctx, parac_gpu_factor_info* info, int64_t* const* col_ptrs,
                                int32_t* const* rows, double* const* values, double* const* diags,
                                const int64_t* capacities) {
+  NvtxRange nvtx_range("parac_gpu_factor_batch_end");
   if (ctx && ctx->pending && ctx->batch_count <= 0) {
     const int rc = factor_end_impl(ctx, info, nullptr, nullptr);
     if (rc) return rc;
@@ -1517,6 +1525,7 @@ int parac_gpu_factor(parac_gpu_ctx* ctx, const parac_csr* g, const int32_t* perm
 int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, double* values,
                        double* diag, int32_t* merged_degree, int32_t* samples_emitted,
                        int32_t* fills_received) {
+  NvtxRange nvtx_range("parac_gpu_download");
   return guarded([&] {
     require_ctx(ctx);
     if (ctx->f_n < 0) throw Failure{dimension_mismatch, "no resident factor"};
@@ -1546,6 +1555,7 @@ int parac_gpu_download(parac_gpu_ctx* ctx, int64_t* col_ptr, int32_t* rows, doub
 int parac_gpu_upload_factor(parac_gpu_ctx* ctx, int32_t n, const int64_t* col_ptr,
                             const int32_t* rows, const double* values, const double* diag,
                             const int32_t* perm) {
+  NvtxRange nvtx_range("parac_gpu_upload_factor");
   return guarded([&] {
     require_ctx(ctx);
     // The sweeps trust the factor's structure (levels are built by waiting on

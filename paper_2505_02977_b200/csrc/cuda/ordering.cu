@@ -8,8 +8,8 @@
 // 0..n-1 by (tie bits, then degree) yields exactly the reference order (the
 // vertex id breaks remaining ties through stability). When the largest degree
 // fits in 11 bits the two keys pack into one 64-bit key and one sort suffices.
-// Then perm[vertex at p] = p.
-#include <cub/device/device_radix_sort.cuh>
+// Then perm[vertex at p] = p. The sort is the hand-written one in
+// radix_sort.cuh.
 
 #include <algorithm>
 #include <string>
@@ -17,6 +17,7 @@
 #include "../host/errors.hpp"
 #include "common.cuh"
 #include "factor_kernels.cuh"
+#include "radix_sort.cuh"
 
 namespace parac_gpu {
 void note_launches(long long k);  // defined in capi.cu
@@ -99,34 +100,23 @@ void nnz_sort_device(int n, const long long* d_ptr, std::uint64_t tie_seed, int*
   cuda_check(cudaMallocAsync(&v1, N * 4, st), "alloc");
   nnz_keys_kernel<<<grid, 256, 0, st>>>(n, d_ptr, tie_seed, packed ? 1 : 0, k0, v0);
   note_launches(2);
-  cub::DoubleBuffer<unsigned long long> keys(k0, k1);
-  cub::DoubleBuffer<int> vals(v0, v1);
-  std::size_t tmp_bytes = 0;
+  unsigned long long* kb[2] = {k0, k1};
+  int* vb[2] = {v0, v1};
   const int end1 = packed ? 53 + dbits : 53;
-  cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, vals, n, 0, end1, st), "cub size");
-  // the degree pass sorts 32-bit keys of the same count: its temp need is no larger
-  void* tmp = nullptr;
-  cuda_check(cudaMallocAsync(&tmp, tmp_bytes, st), "alloc");
-  cuda_check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, vals, n, 0, end1, st), "cub sort");
-  if (!packed) {  // stable second pass by degree
-    unsigned int* d0 = reinterpret_cast<unsigned int*>(keys.Alternate());
-    unsigned int* d1 = d0 + N;  // the alternate key buffer holds 2N u32
-    degree_of_kernel<<<grid, 256, 0, st>>>(n, d_ptr, vals.Current(), d0);
+  int cur = radix::sort_pairs(n, kb, vb, end1, st);
+  if (!packed) {  // stable second pass by degree, u32 keys in the spare 64-bit key buffer
+    unsigned int* d0 = reinterpret_cast<unsigned int*>(kb[cur ^ 1]);
+    unsigned int* db[2] = {d0, d0 + N};  // the spare key buffer holds 2N u32
+    int* vb2[2] = {vb[cur], vb[cur ^ 1]};
+    degree_of_kernel<<<grid, 256, 0, st>>>(n, d_ptr, vb2[0], d0);
     note_launches(1);
-    cub::DoubleBuffer<unsigned int> dk(d0, d1);
-    std::size_t tmp2 = 0;
-    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, dk, vals, n, 0, dbits, st), "cub size");
-    if (tmp2 > tmp_bytes) {
-      cuda_check(cudaFreeAsync(tmp, st), "free");
-      cuda_check(cudaMallocAsync(&tmp, tmp2, st), "alloc");
-      tmp_bytes = tmp2;
-    }
-    cuda_check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, vals, n, 0, dbits, st), "cub sort");
+    const int c2 = radix::sort_pairs(n, db, vb2, dbits, st);
+    cur = vb2[c2] == v0 ? 0 : 1;
   }
-  positions_kernel<<<grid, 256, 0, st>>>(n, vals.Current(), d_perm);
+  positions_kernel<<<grid, 256, 0, st>>>(n, vb[cur], d_perm);
   note_launches(1);
   for (void* p : {static_cast<void*>(k0), static_cast<void*>(k1), static_cast<void*>(v0), static_cast<void*>(v1),
-                  tmp, static_cast<void*>(d_max)})
+                  static_cast<void*>(d_max)})
     cuda_check(cudaFreeAsync(p, st), "free");
 }
 

@@ -12,8 +12,6 @@
 // dot products use a deterministic two-level tree (run-to-run reproducible, not
 // the reference's serial order), which SURVEY §8(a) a16 validated does not move
 // iteration counts.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -27,9 +25,11 @@
 
 #include "../../../include/parac_gpu.h"
 #include "../host/errors.hpp"
+#include "../host/nvtx.hpp"
 #include "common.cuh"
 #include "factor_kernels.cuh"
 #include "solve_kernels.cuh"
+#include "radix_sort.cuh"
 
 namespace parac_gpu {
 
@@ -256,6 +256,27 @@ __global__ void gt_long_gather_kernel(int n, const long long* gt_ptr, const int*
     }
   }
 }
+// Long rows sorted by one radix sort over all of them: key (row slot << cb) |
+// column, value = entry index; the slots are contiguous in [beg, end) order,
+// so the sorted sequence lands back in each row's own range.
+__global__ void gt_long_keys_kernel(int nl, const int* beg, const int* end, const int* ck, int cb,
+                                    unsigned long long* key, int* idx) {
+  for (int i = blockIdx.x; i < nl; i += gridDim.x)
+    for (int t = beg[i] + threadIdx.x; t < end[i]; t += blockDim.x) {
+      key[t] = (static_cast<unsigned long long>(i) << cb) | static_cast<unsigned>(ck[t]);
+      idx[t] = t;
+    }
+}
+
+__global__ void gt_long_unkey_kernel(long long T, const unsigned long long* key, const int* idx, unsigned long long cmask,
+                                     const double* cv, int* ck2, double* cv2) {
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < T;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    ck2[t] = static_cast<int>(key[t] & cmask);
+    cv2[t] = cv[idx[t]];
+  }
+}
+
 __global__ void gt_long_scatter_kernel(int nl, const long long* gt_ptr, const int* beg, const int* end,
                                        const int* rows, const int* ck, const double* cv, int* gt_col,
                                        double* gt_val) {
@@ -1836,18 +1857,30 @@ void prepare_factor(const SolveInputs& in) {
       check(cudaMallocAsync(&cv2, sizeof(double) * T, st), "alloc");
       gt_long_gather_kernel<<<sms * 8, 256, 0, st>>>(n, s.gt_ptr, flag, rpos, loff, s.gt_col, s.gt_val, beg, end,
                                                      rows, ck, cv);
-      std::size_t tb = 0;
-      check(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, ck, ck2, cv, cv2, static_cast<int>(T), nl, beg, end,
-                                                st), "segmented sort size");
-      void* tmp = nullptr;
-      check(cudaMallocAsync(&tmp, std::max<std::size_t>(tb, 1), st), "alloc");
-      check(cub::DeviceSegmentedSort::SortPairs(tmp, tb, ck, ck2, cv, cv2, static_cast<int>(T), nl, beg, end, st),
-            "segmented sort");
+      int cb = 1;
+      while (cb < 31 && (1LL << cb) < n) ++cb;
+      int sb = 1;
+      while (sb < 31 && (1LL << sb) < nl) ++sb;
+      unsigned long long *ka, *kb2;
+      int *ia, *ib;
+      check(cudaMallocAsync(&ka, sizeof(unsigned long long) * T, st), "alloc");
+      check(cudaMallocAsync(&kb2, sizeof(unsigned long long) * T, st), "alloc");
+      check(cudaMallocAsync(&ia, sizeof(int) * T, st), "alloc");
+      check(cudaMallocAsync(&ib, sizeof(int) * T, st), "alloc");
+      gt_long_keys_kernel<<<std::min(nl, sms * 8), 256, 0, st>>>(nl, beg, end, ck, cb, ka, ia);
+      note_launches(1);
+      unsigned long long* kk[2] = {ka, kb2};
+      int* ii[2] = {ia, ib};
+      const int cur = radix::sort_pairs(static_cast<int>(T), kk, ii, cb + sb, st);
+      gt_long_unkey_kernel<<<sms * 8, 256, 0, st>>>(T, kk[cur], ii[cur], (1ULL << cb) - 1, cv, ck2, cv2);
+      note_launches(1);
+      for (void* q : {static_cast<void*>(ka), static_cast<void*>(kb2), static_cast<void*>(ia), static_cast<void*>(ib)})
+        check(cudaFreeAsync(q, st), "free");
       gt_long_scatter_kernel<<<sms * 8, 256, 0, st>>>(nl, s.gt_ptr, beg, end, rows, ck2, cv2, s.gt_col, s.gt_val);
       note_launches(2);
       for (void* q : {static_cast<void*>(beg), static_cast<void*>(end), static_cast<void*>(rows),
                       static_cast<void*>(ck), static_cast<void*>(ck2), static_cast<void*>(cv),
-                      static_cast<void*>(cv2), tmp})
+                      static_cast<void*>(cv2)})
         check(cudaFreeAsync(q, st), "free");
     }
     check(cudaFreeAsync(rpos, st), "free");
@@ -1884,22 +1917,27 @@ void prepare_factor(const SolveInputs& in) {
   // level-order layout -- and with it every fast-mode summation order -- is
   // the same on every build of the same factor (an atomic scatter was not)
   {
-    int* keys_out = nullptr;
+    int* key_a = nullptr;
+    int* key_b = nullptr;
     int* pos_in = nullptr;
-    check(cudaMallocAsync(&keys_out, sizeof(int) * static_cast<std::size_t>(std::max(n, 1)), st), "alloc");
-    check(cudaMallocAsync(&pos_in, sizeof(int) * static_cast<std::size_t>(std::max(n, 1)), st), "alloc");
+    const std::size_t nb = sizeof(int) * static_cast<std::size_t>(std::max(n, 1));
+    check(cudaMallocAsync(&key_a, nb, st), "alloc");
+    check(cudaMallocAsync(&key_b, nb, st), "alloc");
+    check(cudaMallocAsync(&pos_in, nb, st), "alloc");
+    check(cudaMemcpyAsync(key_a, s.level, sizeof(int) * static_cast<std::size_t>(n), cudaMemcpyDeviceToDevice, st),
+          "level copy");
     iota_kernel<<<blocks, 256, 0, st>>>(n, pos_in);
     note_launches(1);
     int bits = 1;
     while (bits < 31 && (1 << bits) <= depth) ++bits;
-    std::size_t tb = 0;
-    check(cub::DeviceRadixSort::SortPairs(nullptr, tb, s.level, keys_out, pos_in, s.order, n, 0, bits, st),
-          "level sort size");
-    void* tmp = nullptr;
-    check(cudaMallocAsync(&tmp, std::max<std::size_t>(tb, 1), st), "alloc");
-    check(cub::DeviceRadixSort::SortPairs(tmp, tb, s.level, keys_out, pos_in, s.order, n, 0, bits, st),
-          "level sort");
-    for (void* q : {static_cast<void*>(keys_out), static_cast<void*>(pos_in), tmp}) check(cudaFreeAsync(q, st), "free");
+    int* kb[2] = {key_a, key_b};
+    int* vb[2] = {pos_in, s.order};
+    const int cur = radix::sort_pairs(n, kb, vb, bits, st);
+    if (vb[cur] != s.order)
+      check(cudaMemcpyAsync(s.order, vb[cur], sizeof(int) * static_cast<std::size_t>(n), cudaMemcpyDeviceToDevice, st),
+            "order copy");
+    for (void* q : {static_cast<void*>(key_a), static_cast<void*>(key_b), static_cast<void*>(pos_in)})
+      check(cudaFreeAsync(q, st), "free");
   }
   stamp("levels");
   build_level_layout(in, s, sms);
@@ -2287,6 +2325,7 @@ void ensure_for(const SolveInputs& in) {
 extern "C" {
 
 int parac_gpu_laplacian_apply(parac_gpu_ctx* ctx, const double* x, double* y) {
+  NvtxRange nvtx_range("parac_gpu_laplacian_apply");
   return guarded([&] {
     ctx_activate(ctx);
     SolveInputs in = solve_inputs(ctx);
@@ -2302,6 +2341,7 @@ int parac_gpu_laplacian_apply(parac_gpu_ctx* ctx, const double* x, double* y) {
 }
 
 int parac_gpu_apply_preconditioner(parac_gpu_ctx* ctx, const double* r, double* z) {
+  NvtxRange nvtx_range("parac_gpu_apply_preconditioner");
   return guarded([&] {
     ctx_activate(ctx);
     SolveInputs in = solve_inputs(ctx);
@@ -2336,6 +2376,7 @@ int parac_gpu_set_preconditioner_mode(parac_gpu_ctx* ctx, int32_t mode) {
 }
 
 int parac_gpu_schedule_levels(parac_gpu_ctx* ctx, int32_t* levels, int32_t* depth) {
+  NvtxRange nvtx_range("parac_gpu_schedule_levels");
   return guarded([&] {
     ctx_activate(ctx);
     SolveInputs in = solve_inputs(ctx);
@@ -2354,6 +2395,7 @@ int parac_gpu_schedule_levels(parac_gpu_ctx* ctx, int32_t* levels, int32_t* dept
 // pcg_solve, src/solver.cpp:95-175.
 int parac_gpu_pcg(parac_gpu_ctx* ctx, const double* b, double tol, int32_t max_iters, double* x,
                   parac_gpu_solve_report* report) {
+  NvtxRange nvtx_range("parac_gpu_pcg");
   WallTimer wall;
   return guarded([&] {
     ctx_activate(ctx);

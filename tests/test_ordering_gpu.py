@@ -19,6 +19,9 @@ pytestmark = pytest.mark.gpu
     ("poisson2d_64", lambda: P.gen_poisson2d(64), 11),
     ("random_connected", lambda: P.gen_random_connected(5000, 20000, 7, False), 5),
     ("rmat_16", lambda: P.gen_rmat(16, 16, 0), 0),  # max degree > 2^11: two-pass path
+    # many radix tiles with a ragged last tile (4096-element tiles), both paths
+    ("random_connected_ragged", lambda: P.gen_random_connected(100_003, 300_000, 2, False), 1),
+    ("rmat_18", lambda: P.gen_rmat(18, 8, 1), 2),
 ])
 def test_nnz_sort_device_equals_host(gpu_ctx, name, build, seed):
     g = build()
